@@ -1,0 +1,356 @@
+"""Oracle of the compress -> exchange -> decompress-average -> residual step.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain NumPy, single thread,
+explicit float32 at every operation.  Readings R1..R25 are DESIGN.md's list (they
+are SURVEY.md §8(c) C1..C25, adopted unchanged unless DESIGN.md says otherwise).
+
+Per cluster c, per bucket of n fp32 elements, step t (SURVEY.md §8(c) plain definition):
+
+    method = IDENTITY if t < start_step else codec.method
+    p      = fl(g + r)  (lossy methods with error feedback, R15)
+    FP16 : h = RNE16(p), error iff any h is +-inf;  D = float(h)      PAPER.md:125-130 Eq.5
+    INT8 : m = max|p|, s = fl(m/127) (s := 1 if m == 0 or s == 0)
+           q = clamp(rint(fl(p/s)), -127, 127);  D = fl(q*s)
+    TOPK : k largest |p| by fp32 bit key, ties -> lower index,        PAPER.md:63, :99 (cited only; R11-R14)
+           idx ascending; values f32 | RNE16 | int8 with the INT8 rule
+    r_new = fl(p - D)                                                  R15 (error feedback)
+    exchange: slot c <- cluster c's payload body
+    out   = fl(tree_sum(D_0..D_{P-1}) / P)                             PAPER.md:76 "aggregated"; R16
+"""
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "IDENTITY", "FP16", "INT8", "TOPK", "VAL_F32", "VAL_F16", "VAL_I8",
+    "NONFINITE", "OVERFLOW", "NebulaError", "Codec", "select_method", "topk_k",
+    "pad16", "payload_bytes", "body_ratio", "fp16_encode", "int8_scale", "int8_quantize",
+    "int8_dequantize", "topk_select", "topk_stats", "compress", "decode_payload",
+    "tree_sum", "average", "CompressResult", "cluster_step", "oracle_step",
+    "hierarchical_step", "svd_ratio", "FP16_OVERFLOW_ABS",
+]
+
+F32 = np.float32
+IDENTITY, FP16, INT8, TOPK = 0, 1, 2, 3
+VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
+VALUE_BYTES = {VAL_F32: 4, VAL_F16: 2, VAL_I8: 1}
+NONFINITE, OVERFLOW = "NONFINITE", "OVERFLOW"
+
+# R10: RNE to binary16 overflows to +-inf exactly when |p| >= 65520 (= 65504 + half an
+# ulp of the top binade, 32/2); [65504, 65520) rounds down to 65504.  Used only in
+# messages and pins — the oracle decides overflow from the conversion result itself.
+FP16_OVERFLOW_ABS = 65520.0
+
+
+class NebulaError(Exception):
+    """Device-detected error of the C ABI (SPEC.md:129 fp16 overflow -> explicit
+    failure; SPEC.md:358 non-finite gradient -> step rejected)."""
+
+    def __init__(self, code: str, msg: str = ""):
+        super().__init__(f"{code}: {msg}")
+        self.code = code
+
+
+@dataclass(frozen=True)
+class Codec:
+    """SPEC.md:111-122 CodecMethod/CodecSchedule, extended with TOPK (R11-R14) and
+    error feedback (R15)."""
+    method: int = INT8
+    topk_values: int = VAL_F32
+    topk_k: int = 0            # >0: exact k (capped at n); 0: derive from density (R12)
+    topk_density: float = 0.01
+    error_feedback: bool = True
+    start_step: int = 0
+
+
+def select_method(codec: Codec, step: int) -> int:
+    """SPEC.md:164 'Identity when step < start_step; the schedule's directional method
+    otherwise'; PAPER.md:453 'starting using communication compression from step'."""
+    return IDENTITY if step < codec.start_step else codec.method
+
+
+def topk_k(n: int, codec: Codec) -> int:
+    """R12: k = clamp(floor(rho*n + 0.5), 1, n) evaluated in double, or the caller's k."""
+    if n == 0:
+        return 0
+    if codec.topk_k > 0:
+        return min(int(codec.topk_k), n)
+    k = math.floor(float(codec.topk_density) * float(n) + 0.5)
+    return max(1, min(n, k))
+
+
+def pad16(nbytes: int) -> int:
+    return (nbytes + 15) // 16 * 16
+
+
+def payload_bytes(method: int, n: int, k: int = 0, value_type: int = VAL_F32) -> int:
+    """R18 body layout: 16-byte preamble {u32 method, u32 count, f32 scale, u32 aux}
+    followed by 16-byte-padded sections.  Dense: values[n].  TOPK: idx u32[k], val[k]."""
+    if method == IDENTITY:
+        return 16 + pad16(4 * n)
+    if method == FP16:
+        return 16 + pad16(2 * n)
+    if method == INT8:
+        return 16 + pad16(n)
+    if method == TOPK:
+        return 16 + pad16(4 * k) + pad16(VALUE_BYTES[value_type] * k)
+    raise ValueError(method)
+
+
+def body_ratio(method: int, n: int, k: int = 0, value_type: int = VAL_F32) -> float:
+    """R19 / Table 5 convention: transmitted value bytes,
+    preamble and padding excluded, over the dense 32-bit baseline 4n."""
+    if method == IDENTITY:
+        b = 4 * n
+    elif method == FP16:
+        b = 2 * n
+    elif method == INT8:
+        b = n
+    else:
+        b = (4 + VALUE_BYTES[value_type]) * k
+    return b / (4.0 * n)
+
+
+def svd_ratio(m: int, n: int, r: int) -> float:
+    """PAPER.md:120-123 Eq. 4: R_svd = (m*r + r + r*n) / (m*n)  (NEXT-1; pinned now)."""
+    return (m * r + r + r * n) / (m * n)
+
+
+# --------------------------------------------------------------------------- codecs
+def _check_finite(p: np.ndarray) -> None:
+    if p.size and not np.all(np.isfinite(p)):
+        raise NebulaError(NONFINITE, "non-finite gradient (+ residual) element")
+
+
+def fp16_encode(p: np.ndarray) -> np.ndarray:
+    """PAPER.md:130 Eq. 5 C_FP16 'converts the 32-bit floating point numbers to 16-bit';
+    SPEC.md:127-129: RNE, subnormals kept, overflow is an explicit failure (R10)."""
+    with np.errstate(over="ignore"):
+        h = p.astype(np.float16)            # IEEE binary32 -> binary16, round-to-nearest-even
+    if h.size and np.any(np.isinf(h)):
+        bad = float(np.max(np.abs(p)))
+        raise NebulaError(OVERFLOW, f"|p| = {bad} >= {FP16_OVERFLOW_ABS} overflows fp16")
+    return h
+
+
+def int8_scale(p: np.ndarray) -> np.float32:
+    """SPEC.md:137 'scale = max|X|/127 (scale = 1 if X == 0)'; R3 per bucket, fp32;
+    R4: also s := 1 when fl(m/127) underflows to 0."""
+    m = np.max(np.abs(p)) if p.size else F32(0.0)
+    m = F32(m)
+    s = F32(m / F32(127.0))
+    if m == F32(0.0) or s == F32(0.0):
+        s = F32(1.0)
+    return s
+
+
+def int8_quantize(p: np.ndarray, s: np.float32) -> np.ndarray:
+    """SPEC.md:137 'stored value = round(x/scale) clamped to [-127,127]'; R5 ties-to-even,
+    R6 IEEE division (not a reciprocal multiply), R7 clamp."""
+    q = np.rint(p / F32(s))                  # fl(p/s) in binary32, then round half to even
+    return np.clip(q, -127, 127).astype(np.int8)
+
+
+def int8_dequantize(q: np.ndarray, s: np.float32) -> np.ndarray:
+    """R8: D = fl(q * s), one rounding (q is exact in binary32)."""
+    return q.astype(F32) * F32(s)
+
+
+def _keys(p: np.ndarray) -> np.ndarray:
+    """R11: selection key = fp32 bit pattern with the sign cleared (|p| order, -0 == +0)."""
+    return p.view(np.uint32) & np.uint32(0x7FFFFFFF)
+
+
+def topk_select(p: np.ndarray, k: int) -> np.ndarray:
+    """R11: the k largest |p| (bit key); among equal keys the lower index wins; returned
+    indices ascending.  Sort by (key descending, index ascending) and keep the first k."""
+    n = p.size
+    if k == 0:
+        return np.zeros(0, dtype=np.uint32)
+    keys = _keys(p).astype(np.int64)
+    order = np.lexsort((np.arange(n, dtype=np.int64), -keys))
+    return np.sort(order[:k]).astype(np.uint32)
+
+
+def topk_stats(p: np.ndarray, k: int) -> dict:
+    """R25 'ranks': the integer order statistics of the selection — threshold key T
+    (key of the k-th selected element), count_above = #{key > T}, need_T = k - count_above
+    (how many of the key == T elements, lowest indices first, are taken)."""
+    if k == 0:
+        return {"k": 0, "threshold": 0, "count_above": 0, "need": 0}
+    keys = _keys(p).astype(np.int64)
+    order = np.lexsort((np.arange(p.size, dtype=np.int64), -keys))
+    T = int(keys[order[k - 1]])
+    above = int(np.count_nonzero(keys > T))
+    return {"k": k, "threshold": T, "count_above": above, "need": k - above}
+
+
+# --------------------------------------------------------------------------- payloads
+def _preamble(method: int, count: int, scale: float, aux: int) -> bytes:
+    return struct.pack("<IIfI", method, count, scale, aux)
+
+
+def _pad(b: bytes) -> bytes:
+    return b + bytes(pad16(len(b)) - len(b))
+
+
+@dataclass
+class CompressResult:
+    payload: bytes
+    D: np.ndarray                 # decoded dense view of the payload, fp32[n]
+    r_new: np.ndarray | None      # residual after the step (None without error feedback)
+    method: int
+    stats: dict = field(default_factory=dict)
+
+
+def compress(p: np.ndarray, method: int, codec: Codec) -> tuple[bytes, np.ndarray, dict]:
+    """Encode p with ``method`` -> (payload bytes, D = decode(payload), stats).
+    Raises NebulaError(NONFINITE) on NaN/Inf (SPEC.md:32 'all entries finite', :358) and
+    NebulaError(OVERFLOW) when an fp16-encoded value overflows."""
+    p = np.ascontiguousarray(p, dtype=F32)
+    n = p.size
+    _check_finite(p)
+    if method == IDENTITY:
+        return _preamble(IDENTITY, n, 1.0, 0) + _pad(p.tobytes()), p.copy(), {}
+    if method == FP16:
+        h = fp16_encode(p)
+        return _preamble(FP16, n, 1.0, 0) + _pad(h.tobytes()), h.astype(F32), {}
+    if method == INT8:
+        s = int8_scale(p)
+        q = int8_quantize(p, s)
+        return (_preamble(INT8, n, float(s), 0) + _pad(q.tobytes()),
+                int8_dequantize(q, s), {"scale": float(s)})
+    if method == TOPK:
+        k = topk_k(n, codec)
+        idx = topk_select(p, k)
+        v = p[idx.astype(np.int64)]
+        D = np.zeros(n, dtype=F32)           # +0.0 where not selected (R16)
+        scale = F32(1.0)
+        if codec.topk_values == VAL_F32:
+            vb, dv = v.tobytes(), v
+        elif codec.topk_values == VAL_F16:
+            h = fp16_encode(v)
+            vb, dv = h.tobytes(), h.astype(F32)
+        elif codec.topk_values == VAL_I8:
+            scale = int8_scale(p)            # R13: max over the bucket (always selected)
+            q = int8_quantize(v, scale)
+            vb, dv = q.tobytes(), int8_dequantize(q, scale)
+        else:
+            raise ValueError(codec.topk_values)
+        D[idx.astype(np.int64)] = dv
+        payload = (_preamble(TOPK, k, float(scale), codec.topk_values)
+                   + _pad(idx.astype("<u4").tobytes()) + _pad(vb))
+        stats = topk_stats(p, k)
+        stats["scale"] = float(scale)
+        return payload, D, stats
+    raise ValueError(method)
+
+
+def decode_payload(payload: bytes, n: int) -> np.ndarray:
+    """Inverse of the R18 layout -> dense fp32[n] (+0.0 where top-k did not select)."""
+    method, count, scale, aux = struct.unpack_from("<IIfI", payload, 0)
+    body = memoryview(payload)[16:]
+    if method == IDENTITY:
+        return np.frombuffer(body, dtype="<f4", count=n).astype(F32)
+    if method == FP16:
+        return np.frombuffer(body, dtype="<f2", count=n).astype(F32)
+    if method == INT8:
+        q = np.frombuffer(body, dtype=np.int8, count=n)
+        return int8_dequantize(q, F32(scale))
+    if method == TOPK:
+        k = count
+        idx = np.frombuffer(body, dtype="<u4", count=k).astype(np.int64)
+        vals = body[pad16(4 * k):]
+        if aux == VAL_F32:
+            dv = np.frombuffer(vals, dtype="<f4", count=k).astype(F32)
+        elif aux == VAL_F16:
+            dv = np.frombuffer(vals, dtype="<f2", count=k).astype(F32)
+        else:
+            dv = int8_dequantize(np.frombuffer(vals, dtype=np.int8, count=k), F32(scale))
+        D = np.zeros(n, dtype=F32)
+        D[idx] = dv
+        return D
+    raise ValueError(method)
+
+
+# --------------------------------------------------------------------------- average
+def tree_sum(parts: list) -> np.ndarray:
+    """R16: fixed pairwise tree over cluster ids: sum(lo,hi) = sum(lo,mid) + sum(mid,hi),
+    mid = lo + ceil((hi-lo)/2); every '+' is one binary32 rounding."""
+    def rec(lo, hi):
+        if hi - lo == 1:
+            return np.asarray(parts[lo], dtype=F32)
+        mid = lo + (hi - lo + 1) // 2
+        return (rec(lo, mid) + rec(mid, hi)).astype(F32)
+    return rec(0, len(parts))
+
+
+def average(payloads: list, n: int) -> np.ndarray:
+    """PAPER.md:76 'the gradients are aggregated by the server' / north_star
+    'decompressed and averaged': out = fl(tree_sum(decode(payload_c)) / P).  Every
+    cluster's own term is decoded from its own payload (R16)."""
+    P = len(payloads)
+    acc = tree_sum([decode_payload(b, n) for b in payloads])
+    return (acc / F32(P)).astype(F32)
+
+
+# --------------------------------------------------------------------------- steps
+def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int) -> CompressResult:
+    """One cluster's compress with error feedback (R15):
+    lossy: p = fl(g + r); payload = C(p); r_new = fl(p - D(C(p))).
+    IDENTITY (t < start_step): payload = g, residual untouched."""
+    g = np.ascontiguousarray(g, dtype=F32)
+    method = select_method(codec, step)
+    if method == IDENTITY:
+        payload, D, st = compress(g, IDENTITY, codec)
+        return CompressResult(payload, D, None if r is None else r.copy(), IDENTITY, st)
+    if codec.error_feedback:
+        if r is None:
+            r = np.zeros_like(g)
+        p = (g + np.asarray(r, dtype=F32)).astype(F32)
+    else:
+        p = g
+    payload, D, st = compress(p, method, codec)
+    r_new = (p - D).astype(F32) if codec.error_feedback else (None if r is None else r.copy())
+    return CompressResult(payload, D, r_new, method, st)
+
+
+def oracle_step(gs: list, rs: list, codec: Codec, step: int):
+    """Whole step for P clusters: compress each cluster, exchange the
+    payload bodies (slot c = cluster c), and have every cluster decompress-average all
+    P slots.  Returns (out, [r_new_c], [payload_c], [stats_c])."""
+    res = [cluster_step(g, r, codec, step) for g, r in zip(gs, rs)]
+    n = np.asarray(gs[0]).size
+    out = average([x.payload for x in res], n)
+    return out, [x.r_new for x in res], [x.payload for x in res], [x.stats for x in res]
+
+
+def hierarchical_step(gs: list, rs: list, codec: Codec, step: int):
+    """P clusters x G GPUs (R20, PAPER.md:95 / :288 intra-cluster parallelism + compressed
+    inter-cluster hop).  gs[c][l] is GPU l of cluster c's full bucket (n % G == 0);
+    rs[c][l] its residual shard.  The cluster gradient is the fp32 mean of its G GPUs
+    (sum in GPU order, then / G; tests feed dyadic inputs so any order is exact);
+    GPU l codes shard l; peers with the same l exchange; shards are all-gathered.
+    Returns (out, rs_new[c][l], payloads[c][l])."""
+    P, G = len(gs), len(gs[0])
+    n = np.asarray(gs[0][0]).size
+    assert n % G == 0
+    m = n // G
+    outs, rs_new, pls = [], [[None] * G for _ in range(P)], [[None] * G for _ in range(P)]
+    for l in range(G):
+        shards = []
+        for c in range(P):
+            acc = np.asarray(gs[c][0][l * m:(l + 1) * m], dtype=F32)
+            for j in range(1, G):
+                acc = (acc + np.asarray(gs[c][j][l * m:(l + 1) * m], dtype=F32)).astype(F32)
+            shards.append((acc / F32(G)).astype(F32))
+        out_l, r_l, p_l, _ = oracle_step(shards, [rs[c][l] for c in range(P)], codec, step)
+        outs.append(out_l)
+        for c in range(P):
+            rs_new[c][l] = r_l[c]
+            pls[c][l] = p_l[c]
+    return np.concatenate(outs).astype(F32), rs_new, pls
