@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -169,7 +169,8 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
     ties (values drawn from 7 distinct magnitudes with random signs — many exact ties);
     zeros (all +0.0); subnormal (values around 1e-40); mixed-scale (N(0,1) scaled by
     10**U(-30, 3) per element); signed-zero (half +0.0, half -0.0, a few nonzeros);
-    uniform U(-1, 1); tiny-max (max |g| ~ 1e-44, below 127 * 2**-149).
+    uniform U(-1, 1); tiny-max (max |g| ~ 1e-44, below 127 * 2**-149); strided-zeros (every
+    16th element 0, the rest N(0,1)).
     """
     rng = np.random.default_rng(seed)
     if kind == "normal":
@@ -209,6 +210,12 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
         return rng.uniform(-1.0, 1.0, size=n).astype(np.float32)
     if kind == "tiny-max":
         return (rng.uniform(-1.0, 1.0, size=n) * 1e-44).astype(np.float32)
+    if kind == "strided-zeros":
+        # every element whose index is a multiple of 16 is 0.0, the rest N(0, 1): a regular
+        # sampler with a power-of-two stride >= 16 sees only zeros (adversarial structure)
+        g = rng.standard_normal(n, dtype=np.float32)
+        g[::16] = 0.0
+        return g
     raise ValueError(f"unknown kind {kind!r}")
 
 

@@ -1,0 +1,204 @@
+/*
+ * nebula_sync.h — C ABI of the B200-native compressed gradient sync (Nebula-I hot path).
+ *
+ * What the library computes (arXiv 2205.09470, "Nebula-I"; PAPER.md = /root/reference/PAPER.md,
+ * SPEC.md = /root/reference/SPEC.md; R-numbers are DESIGN.md readings == SURVEY.md §8(c) C-numbers):
+ *
+ *   For every cluster c (a group of G GPUs; P clusters), every gradient bucket b of n fp32
+ *   elements, and optimisation step t:
+ *     method = IDENTITY if t < start_step else codec.method
+ *     p      = fl(g + r)                                             error feedback, R15
+ *     payload_c = C(p)   FP16  : RNE binary16                        PAPER.md:125-130 Eq. 5
+ *                        INT8  : per-bucket symmetric max-abs scale
+ *                        TOPK  : k largest |p|, ties -> lower index  PAPER.md:63, :99 (cited), R11-R14
+ *     r      = fl(p - D(C(p)))                                       R15
+ *     exchange payload_c between clusters                            PAPER.md:76 "gradients are aggregated",
+ *                                                                    PAPER.md:95 data parallelism across clusters
+ *     out    = fl(tree_sum_c D(payload_c) / P)                       R16 (fixed pairwise tree over cluster ids)
+ *
+ *   With G > 1 (hierarchical): the cluster gradient is the fp32 mean of its G GPUs
+ *   (intra-cluster ReduceScatter), GPU l codes shard l (n/G elements) with its own residual,
+ *   exchanges it with the P-1 peers of the same local rank, and the averaged shards are
+ *   all-gathered inside the cluster (R20).
+ *
+ * Payload body (R18): 16-byte preamble {u32 method, u32 count (n or k), f32 scale (1.0 if
+ * unused), u32 aux (TOPK value type, else 0)}, then sections zero-padded to 16 bytes:
+ * IDENTITY f32[n] | FP16 binary16[n] | INT8 int8[n] | TOPK u32 idx[k] (ascending) then
+ * val[k] (f32 | binary16 | int8).  All little-endian.  Identical on every transport.
+ *
+ * Conventions for every entry point:
+ *   - Pointers named dev_* are CUDA device pointers on the context's device; host_* are
+ *     host pointers.  Nothing is retained past the call except through the context.
+ *   - Every call only ENQUEUES work on the context's stream and returns, except
+ *     nebula_check, nebula_payload_copy, nebula_topk_stats and nebula_step_host, which
+ *     synchronise that stream.  One host thread per context.
+ *   - Host-validated errors return immediately with nothing enqueued.  Device-detected
+ *     errors (non-finite p, fp16 overflow) set a sticky device flag returned by
+ *     nebula_check (which clears it).  After a device error the affected buckets' residuals
+ *     and dev_out are unspecified (INT8 alone is all-or-nothing: it writes nothing).
+ *   - No C++ exception crosses the ABI.  nebula_last_error() describes the last failure.
+ *   - Per bucket the order must be compress -> exchange -> decompress_reduce; anything
+ *     else returns NEBULA_ERR_STATE.  nebula_step runs all three.
+ *   - bucket == NEBULA_ALL_BUCKETS (-1) applies a call to every bucket in one segmented
+ *     launch per stage; the buckets are then laid out back to back (in init order) in the
+ *     caller's flat buffers.
+ */
+#ifndef NEBULA_SYNC_H_
+#define NEBULA_SYNC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NEBULA_ABI_VERSION 1
+#define NEBULA_ALL_BUCKETS (-1)
+#define NEBULA_MAX_CLUSTERS 8
+#define NEBULA_UNIQUE_ID_BYTES 128
+
+typedef struct nebula_ctx nebula_ctx; /* opaque, library-owned */
+
+typedef enum {
+  NEBULA_OK = 0,
+  NEBULA_ERR_INVALID_ARG = 1, /* host-validated; nothing enqueued */
+  NEBULA_ERR_STATE = 2,       /* call order violated for a bucket */
+  NEBULA_ERR_OOM = 3,
+  NEBULA_ERR_CUDA = 4,
+  NEBULA_ERR_NCCL = 5,
+  NEBULA_ERR_NONFINITE = 6,   /* device-detected NaN/Inf in p = g + r   (sticky) */
+  NEBULA_ERR_OVERFLOW = 7,    /* device-detected fp16 overflow |p| >= 65520 (R10) */
+  NEBULA_ERR_UNSUPPORTED = 8  /* e.g. NCCL transport in a build/box without peers */
+} nebula_status;
+
+typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3 } nebula_method;
+typedef enum { NEBULA_VAL_F32 = 0, NEBULA_VAL_F16 = 1, NEBULA_VAL_I8 = 2 } nebula_value_type;
+typedef enum { NEBULA_TRANSPORT_NCCL = 0, NEBULA_TRANSPORT_LOOPBACK = 1 } nebula_transport;
+
+/* Codec (SPEC.md:111-122 CodecMethod / CodecSchedule, extended with TOPK and error feedback). */
+typedef struct {
+  int32_t method;          /* nebula_method */
+  int32_t topk_values;     /* nebula_value_type; TOPK only (R13) */
+  uint64_t topk_k;         /* >0: exact k per coded bucket (capped at n); 0: derive from density */
+  double topk_density;     /* rho in (0,1]; k = clamp(floor(rho*n + 0.5), 1, n)  (R12) */
+  int32_t error_feedback;  /* 1: p = g + r and r <- p - D(C(p)) (R15); 0: p = g, no residual */
+  int32_t reserved0;
+  uint64_t start_step;     /* IDENTITY while step < start_step */
+} nebula_codec;
+
+/* Topology: P clusters x G GPUs.  Global rank = cluster_id * G + local_rank. */
+typedef struct {
+  int32_t num_clusters;     /* P, 1..NEBULA_MAX_CLUSTERS */
+  int32_t cluster_id;       /* 0..P-1 (ignored for LOOPBACK: this device hosts all P) */
+  int32_t gpus_per_cluster; /* G >= 1; G > 1 => hierarchical (NCCL only; every numel % G == 0) */
+  int32_t local_rank;       /* 0..G-1 */
+  int32_t transport;        /* nebula_transport */
+  int32_t device;           /* CUDA device ordinal the context lives on */
+  const void* nccl_unique_id; /* NEBULA_UNIQUE_ID_BYTES, identical on all P*G ranks; NULL for LOOPBACK */
+} nebula_topology;
+
+/* Integer order statistics of one top-k selection (R25 "ranks"). */
+typedef struct {
+  uint64_t k;           /* number of selected elements */
+  uint32_t threshold;   /* key T = |p| bits of the k-th largest (sign cleared) */
+  uint32_t reserved;
+  uint64_t count_above; /* #{key > T} */
+  uint64_t need;        /* k - count_above: how many key == T elements (lowest indices) were taken */
+  uint64_t candidates;  /* diagnostic: elements that went through the exact resolution stage */
+  uint32_t path;        /* diagnostic: 0 = sampled bracket, 1 = widened bracket */
+  uint32_t reserved2;
+} nebula_topk_info;
+
+/* ABI version of the loaded library (== NEBULA_ABI_VERSION it was built with). */
+int32_t nebula_abi_version(void);
+
+/* Static string for a status code. Never NULL. */
+const char* nebula_status_string(nebula_status s);
+
+/* Writes an NCCL unique id (NEBULA_UNIQUE_ID_BYTES) to host_out128; rank 0 calls it and
+ * broadcasts the bytes to all ranks out of band (the Python binding uses torch.distributed). */
+nebula_status nebula_get_unique_id(void* host_out128);
+
+/* Creates a context.  bucket_numel[num_buckets] are element counts (each < 2^31; 0 allowed).
+ * Allocates and zeroes the residuals (library-owned, one per (cluster, bucket[, shard])),
+ * payload slots and scratch; for NCCL builds the communicators (collective across all
+ * P*G ranks).  stream is a cudaStream_t (NULL = legacy default stream) the context enqueues
+ * on; it may be changed with nebula_set_stream.  On failure *out is NULL. */
+nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, const nebula_codec* codec,
+                               const uint64_t* bucket_numel, int32_t num_buckets, void* stream);
+
+nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream);
+
+/* Stage 1 — EF-accumulate + compress + pack (+ the G>1 intra-cluster ReduceScatter).
+ * dev_grad: fp32 gradient of the bucket (or of all buckets, back to back, for
+ * NEBULA_ALL_BUCKETS).  LOOPBACK: P stacked copies, cluster-major: [P][bucket elems]
+ * (for ALL: [P][sum of all bucket elems]).  16-byte alignment enables the vector path;
+ * any alignment is accepted.  Not modified.  May be freed once the stream work completes. */
+nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step);
+
+/* Stage 2 — move every cluster's payload to every cluster (NCCL AllGather over the
+ * inter-cluster communicator, in place; LOOPBACK: nothing to move). */
+nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket);
+
+/* Stage 3 — decode all P payload slots, tree-sum, divide by P, write dev_out (fp32, the
+ * bucket's elements; ALL: back to back) (+ the G>1 intra-cluster AllGather).  dev_out may
+ * alias dev_grad (non-LOOPBACK) . */
+nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out);
+
+/* All three stages. */
+nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step);
+
+/* All buckets, host buffers: copies host_grad (LOOPBACK: [P][total]) to the device, runs
+ * nebula_step(ALL), copies dev_out back to host_out ([total]) and synchronises.  Pinned
+ * host memory gives full PCIe bandwidth; pageable works. */
+nebula_status nebula_step_host(nebula_ctx* ctx, const float* host_grad, float* host_out, uint64_t step);
+
+/* Synchronises the stream; returns and clears the sticky device error
+ * (NEBULA_ERR_NONFINITE takes precedence over NEBULA_ERR_OVERFLOW), else NEBULA_OK. */
+nebula_status nebula_check(nebula_ctx* ctx);
+
+/* Size in bytes of one cluster's payload for a bucket (preamble + padded sections). */
+nebula_status nebula_payload_bytes(const nebula_ctx* ctx, int32_t bucket, uint64_t* bytes);
+
+/* Synchronises, then copies payload slot `slot` (cluster id 0..P-1) of a bucket to host
+ * memory (cap >= nebula_payload_bytes).  Valid after compress (own slot; all slots for
+ * LOOPBACK) or after exchange (all slots).  For oracle comparison and export. */
+nebula_status nebula_payload_copy(nebula_ctx* ctx, int32_t bucket, int32_t slot, void* host_dst, uint64_t cap);
+
+/* Device pointer to the residual of (bucket, cluster) — the caller saves / restores it with
+ * its optimizer state (checkpointing) or zeroes it after a device error.  cluster is the
+ * simulated cluster for LOOPBACK and must be the context's own cluster otherwise.  Length:
+ * the coded elements of the bucket (numel, or numel/G when hierarchical). */
+nebula_status nebula_residual_ptr(nebula_ctx* ctx, int32_t bucket, int32_t cluster, float** dev_residual);
+
+/* Synchronises and returns the order statistics of the last TOPK compress of (bucket, cluster). */
+nebula_status nebula_topk_stats(nebula_ctx* ctx, int32_t bucket, int32_t cluster, nebula_topk_info* out);
+
+/* Number of library kernels enqueued since the context was created (bench accounting). */
+uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
+
+/* Per-kernel device timers.  When enabled, every kernel / collective the context enqueues is
+ * bracketed by a CUDA event pair recorded on the context's stream (the stream the kernel
+ * runs on).  nebula_timing_read synchronises, returns per-phase sums since the last read
+ * (one entry per phase that ran; phase ids named by nebula_phase_name) and resets them. */
+typedef struct {
+  uint32_t phase;  /* kernel / collective id */
+  uint32_t count;  /* launches timed */
+  double ms;       /* summed event-to-event time */
+} nebula_phase_time;
+
+nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on);
+nebula_status nebula_timing_read(nebula_ctx* ctx, nebula_phase_time* out, int32_t cap, int32_t* n_out);
+const char* nebula_phase_name(uint32_t phase);
+
+/* Frees everything the context owns (synchronises first).  NULL is a no-op. */
+nebula_status nebula_sync_destroy(nebula_ctx* ctx);
+
+/* Last error message of ctx (or of the last failed nebula_sync_init when ctx is NULL). */
+const char* nebula_last_error(const nebula_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEBULA_SYNC_H_ */

@@ -1,0 +1,308 @@
+"""paper_2205_09470_b200 — B200-native compressed gradient sync (Nebula-I hot path).
+
+Thin ctypes binding over ``libnebula_sync.so`` (C ABI: ``include/nebula_sync.h``).  It only
+marshals arguments: every step of the path runs in the library's sm_100a kernels and NCCL.
+There is no CPU or PyTorch fallback — if the library is missing, importing the binding's
+``load()`` raises.  PyTorch is used only for device memory (tensors whose ``data_ptr`` is
+passed through), streams and ``torch.distributed`` (to broadcast the NCCL unique id).
+
+Names follow the C ABI: ``SyncContext.compress`` == ``nebula_compress`` etc.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+__all__ = [
+    "IDENTITY", "FP16", "INT8", "TOPK", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
+    "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
+    "status_string", "abi_version", "HEADER",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
+
+IDENTITY, FP16, INT8, TOPK = 0, 1, 2, 3
+VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
+NCCL, LOOPBACK = 0, 1
+ALL_BUCKETS = -1
+UNIQUE_ID_BYTES = 128
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "OOM", 4: "CUDA", 5: "NCCL",
+          6: "NONFINITE", 7: "OVERFLOW", 8: "UNSUPPORTED"}
+
+
+class NebulaError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.code = STATUS.get(status, str(status))
+
+
+class _Codec(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("topk_values", ctypes.c_int32), ("topk_k", ctypes.c_uint64),
+                ("topk_density", ctypes.c_double), ("error_feedback", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("start_step", ctypes.c_uint64)]
+
+
+class _Topology(ctypes.Structure):
+    _fields_ = [("num_clusters", ctypes.c_int32), ("cluster_id", ctypes.c_int32),
+                ("gpus_per_cluster", ctypes.c_int32), ("local_rank", ctypes.c_int32),
+                ("transport", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
+
+
+class _TopkInfo(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint64), ("threshold", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("count_above", ctypes.c_uint64), ("need", ctypes.c_uint64), ("candidates", ctypes.c_uint64),
+                ("path", ctypes.c_uint32), ("reserved2", ctypes.c_uint32)]
+
+
+class _PhaseTime(ctypes.Structure):
+    _fields_ = [("phase", ctypes.c_uint32), ("count", ctypes.c_uint32), ("ms", ctypes.c_double)]
+
+
+@dataclass
+class TopkInfo:
+    k: int
+    threshold: int
+    count_above: int
+    need: int
+    candidates: int
+    path: int
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return os.path.join(HERE, "libnebula_sync.so")
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree CUDA library; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_2205_09470_b200.build` "
+                          "(the product path has no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, U64, I32, VP = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
+    sig = {
+        "nebula_abi_version": (I32, []),
+        "nebula_status_string": (ctypes.c_char_p, [I32]),
+        "nebula_get_unique_id": (I32, [VP]),
+        "nebula_sync_init": (I32, [ctypes.POINTER(P), ctypes.POINTER(_Topology), ctypes.POINTER(_Codec),
+                                   ctypes.POINTER(U64), I32, VP]),
+        "nebula_set_stream": (I32, [P, VP]),
+        "nebula_compress": (I32, [P, I32, VP, U64]),
+        "nebula_exchange": (I32, [P, I32]),
+        "nebula_decompress_reduce": (I32, [P, I32, VP]),
+        "nebula_step": (I32, [P, I32, VP, VP, U64]),
+        "nebula_step_host": (I32, [P, VP, VP, U64]),
+        "nebula_check": (I32, [P]),
+        "nebula_payload_bytes": (I32, [P, I32, ctypes.POINTER(U64)]),
+        "nebula_payload_copy": (I32, [P, I32, I32, VP, U64]),
+        "nebula_residual_ptr": (I32, [P, I32, I32, ctypes.POINTER(ctypes.c_void_p)]),
+        "nebula_topk_stats": (I32, [P, I32, I32, ctypes.POINTER(_TopkInfo)]),
+        "nebula_kernel_launches": (U64, [P]),
+        "nebula_timing_enable": (I32, [P, I32]),
+        "nebula_timing_read": (I32, [P, ctypes.POINTER(_PhaseTime), I32, ctypes.POINTER(I32)]),
+        "nebula_phase_name": (ctypes.c_char_p, [ctypes.c_uint32]),
+        "nebula_sync_destroy": (I32, [P]),
+        "nebula_last_error": (ctypes.c_char_p, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _lib = L
+    return L
+
+
+def abi_version() -> int:
+    return load().nebula_abi_version()
+
+
+def status_string(s: int) -> str:
+    return load().nebula_status_string(s).decode()
+
+
+def _err(ctx_ptr) -> str:
+    m = load().nebula_last_error(ctx_ptr)
+    return m.decode() if m else ""
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    s = load().nebula_get_unique_id(buf)
+    if s:
+        raise NebulaError(s, _err(None))
+    return buf.raw
+
+
+def _ptr(x) -> int:
+    """Device/host pointer of a torch tensor, or an int address."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream_handle(stream, device):
+    if stream is None:
+        import torch
+        if not torch.cuda.is_available():
+            return 0      # validation-only use on a CPU box: init fails before any CUDA call
+        return torch.cuda.current_stream(device).cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class SyncContext:
+    """One ``nebula_ctx``.  Arguments mirror ``nebula_topology`` / ``nebula_codec``."""
+
+    def __init__(self, bucket_numel, method=INT8, *, topk_values=VAL_F32, topk_k=0, topk_density=0.01,
+                 error_feedback=True, start_step=0, num_clusters=2, cluster_id=0, gpus_per_cluster=1,
+                 local_rank=0, transport=LOOPBACK, device=0, unique_id: bytes | None = None, stream=None):
+        L = load()
+        self._L = L
+        self.bucket_numel = [int(n) for n in bucket_numel]
+        self.num_clusters, self.cluster_id = num_clusters, cluster_id
+        self.gpus_per_cluster, self.local_rank = gpus_per_cluster, local_rank
+        self.transport, self.device = transport, device
+        self.codec = _Codec(method, topk_values, int(topk_k), float(topk_density), int(bool(error_feedback)), 0,
+                            int(start_step))
+        self._uid = ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES) if unique_id is not None else None
+        topo = _Topology(num_clusters, cluster_id, gpus_per_cluster, local_rank, transport, device,
+                         ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None)
+        arr = (ctypes.c_uint64 * len(self.bucket_numel))(*self.bucket_numel)
+        h = ctypes.c_void_p()
+        st = _stream_handle(stream, device)
+        s = L.nebula_sync_init(ctypes.byref(h), ctypes.byref(topo), ctypes.byref(self.codec), arr,
+                               len(self.bucket_numel), st)
+        if s:
+            raise NebulaError(s, _err(None))
+        self._h = h
+
+    # ------------------------------------------------------------------ helpers
+    def _ck(self, s):
+        if s:
+            raise NebulaError(s, _err(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream):
+        self._ck(self._L.nebula_set_stream(self._h, _stream_handle(stream, self.device)))
+
+    # ------------------------------------------------------------------ stages
+    def compress(self, bucket, grad, step):
+        self._ck(self._L.nebula_compress(self._h, bucket, _ptr(grad), step))
+
+    def exchange(self, bucket):
+        self._ck(self._L.nebula_exchange(self._h, bucket))
+
+    def decompress_reduce(self, bucket, out):
+        self._ck(self._L.nebula_decompress_reduce(self._h, bucket, _ptr(out)))
+
+    def step(self, bucket, grad, out, step):
+        self._ck(self._L.nebula_step(self._h, bucket, _ptr(grad), _ptr(out), step))
+
+    def step_host(self, host_grad, host_out, step):
+        """host_grad / host_out: CPU tensors (pinned for full bandwidth) or numpy arrays."""
+        g = host_grad.ctypes.data if hasattr(host_grad, "ctypes") else host_grad.data_ptr()
+        o = host_out.ctypes.data if hasattr(host_out, "ctypes") else host_out.data_ptr()
+        self._ck(self._L.nebula_step_host(self._h, g, o, step))
+
+    def check(self):
+        """Synchronise; raise NebulaError(NONFINITE/OVERFLOW) if the device flagged one."""
+        self._ck(self._L.nebula_check(self._h))
+
+    def check_status(self) -> int:
+        return self._L.nebula_check(self._h)
+
+    def payload_bytes(self, bucket) -> int:
+        v = ctypes.c_uint64()
+        self._ck(self._L.nebula_payload_bytes(self._h, bucket, ctypes.byref(v)))
+        return v.value
+
+    def payload_copy(self, bucket, slot) -> bytes:
+        n = self.payload_bytes(bucket)
+        buf = ctypes.create_string_buffer(max(n, 1))
+        self._ck(self._L.nebula_payload_copy(self._h, bucket, slot, buf, n))
+        return buf.raw[:n]
+
+    def residual_ptr(self, bucket, cluster) -> int:
+        p = ctypes.c_void_p()
+        self._ck(self._L.nebula_residual_ptr(self._h, bucket, cluster, ctypes.byref(p)))
+        return p.value or 0
+
+    def residual(self, bucket, cluster):
+        """A torch view (no copy) of the library-owned residual (checkpoint / restore it)."""
+        import torch
+        n = self.bucket_numel[bucket] // self.gpus_per_cluster
+        ptr = self.residual_ptr(bucket, cluster)
+
+        class _CAI:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+        return torch.as_tensor(_CAI(), device=f"cuda:{self.device}")
+
+    def topk_stats(self, bucket, cluster) -> TopkInfo:
+        info = _TopkInfo()
+        self._ck(self._L.nebula_topk_stats(self._h, bucket, cluster, ctypes.byref(info)))
+        return TopkInfo(info.k, info.threshold, info.count_above, info.need, info.candidates, info.path)
+
+    def kernel_launches(self) -> int:
+        return self._L.nebula_kernel_launches(self._h)
+
+    def timing_enable(self, on: bool = True):
+        self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))
+
+    def timing_read(self) -> dict:
+        """{phase name: (launches, summed ms)} since the last read (synchronises)."""
+        buf = (_PhaseTime * 64)()
+        n = ctypes.c_int32()
+        self._ck(self._L.nebula_timing_read(self._h, buf, 64, ctypes.byref(n)))
+        return {self._L.nebula_phase_name(buf[i].phase).decode(): (buf[i].count, buf[i].ms) for i in range(n.value)}
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            self._L.nebula_sync_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def init_process_group_context(bucket_numel, *, gpus_per_cluster=1, device=None, **codec):
+    """Build a NCCL-transport context for this torch.distributed rank.  Rank r is
+    cluster r // G, local rank r % G (SURVEY.md §8(e) topology B; G = 1 -> topology A).
+    Rank 0 creates the NCCL unique id; torch.distributed broadcasts it (plumbing only)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    G = gpus_per_cluster
+    if world % G:
+        raise ValueError("world size must be a multiple of gpus_per_cluster")
+    uid = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    if device is None:
+        device = torch.cuda.current_device()
+    return SyncContext(bucket_numel, num_clusters=world // G, cluster_id=rank // G, gpus_per_cluster=G,
+                       local_rank=rank % G, transport=NCCL, device=device, unique_id=uid[0], **codec)
+
+
+def topology_for_rank(rank: int, world: int, gpus_per_cluster: int = 1):
+    """(num_clusters, cluster_id, local_rank) of a rank — host logic shared by the bench."""
+    G = gpus_per_cluster
+    if G < 1 or world % G:
+        raise ValueError("world size must be a positive multiple of gpus_per_cluster")
+    return world // G, rank // G, rank % G

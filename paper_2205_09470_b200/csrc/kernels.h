@@ -1,0 +1,113 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal to libnebula_sync.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nebula_internal.cuh"
+
+namespace nb {
+
+// Phase ids of the per-kernel timers (nebula_timing_read); names in nebula_phase_name.
+enum Phase : int {
+  PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
+  PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
+  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_COUNT
+};
+
+struct Launch {
+  cudaStream_t stream;
+  int num_sms;
+  uint64_t* launches;                       // incremented once per kernel enqueued
+  void (*mark)(void*, int phase, int end);  // optional CUDA-event timer hook
+  void* mctx;
+};
+
+// RAII timer around one launch site: records an event pair on the launch stream.
+struct Mark {
+  const Launch& L;
+  int ph;
+  Mark(const Launch& l, int p) : L(l), ph(p) { if (L.mark) L.mark(L.mctx, ph, 0); }
+  ~Mark() { if (L.mark) L.mark(L.mctx, ph, 1); }
+};
+
+// ---- dense codecs (kernels_dense.cu) ----
+// IDENTITY: payload <- g (+ non-finite check).  Residual untouched (R15).
+void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks,
+                     const float* g, uint8_t* slots, uint32_t* flags);
+// FP16 + EF, single pass: p = g + r; h = RNE16(p); r <- p - h; flags.
+void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                 const float* g, float* r, uint8_t* slots, uint32_t* flags);
+// INT8 pass 1: scratch[sidx] <- max over the item of |g + r| bits (atomicMax; zeroed by caller).
+void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                   const float* g, const float* r, uint32_t* scratch);
+// INT8 pass 2: scale from scratch, quantize + pack, r <- p - q*s.
+void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                       const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags);
+// INT8 single-pass, on-chip (cooperative, persistent): p held in shared memory between the
+// max-abs reduction and the quantisation.  Returns false when not applicable (item too big
+// for the resident grid), in which case the caller uses the two-pass kernels.
+bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem);
+void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems,
+                        const float* g, float* r, uint8_t* slots, uint32_t* scratch, uint32_t* flags,
+                        uint32_t* barrier, int grid, size_t smem);
+// Dense decompress + tree-average over P slots.
+void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
+                         uint64_t chunks, const uint8_t* slots, float* out);
+
+// ---- top-k (kernels_topk.cu) ----
+struct TopkItem {       // per (cluster, bucket) top-k state, device resident
+  uint64_t n, k;
+  uint64_t r_off, g_off, slot_off;
+  uint64_t chunk0;      // classify-pass chunk base
+  uint64_t nchunks;
+  uint64_t sample_off;  // into sample buffer (u32 keys)
+  uint64_t nsample;
+  uint32_t stride;      // sample stride S
+  uint32_t sidx;
+  uint64_t list_off;    // into winner / candidate lists (entries)
+  uint64_t wcap, ccap;  // capacities
+  uint64_t status_off;  // into tile-status words
+  uint64_t mt0;         // prefix of merge tiles over the launch's items (absolute)
+  uint32_t value_type;
+  uint32_t pad;
+};
+struct TopkState {      // per item, device resident, rewritten every step
+  uint32_t t_lo, t_hi;  // bracket: winners key > t_hi, candidates t_lo <= key <= t_hi
+  uint32_t mode;        // 0 bracket, 1 exact (t_lo == t_hi == T, need known)
+  uint32_t failed;      // resolve found the bracket invalid -> exact fallback
+  uint64_t wcount, ccount;
+  uint32_t threshold;   // final T
+  uint32_t hist_prefix; // fallback radix state
+  uint64_t count_above, need;
+  uint64_t rank_left;   // fallback radix: rank still to find inside the prefix
+  uint32_t tile_ctr;    // dynamic tile counter for the classify pass
+  uint32_t path;
+  float scale;
+  uint32_t maxbits;
+};
+struct TopkBuffers {
+  TopkItem* items;      // [nitems] (bucket-major, cluster-minor: same order as the Item tables)
+  TopkState* state;     // [nitems]
+  uint32_t* sample;
+  uint2* wlist;         // (idx, p bits)
+  uint2* clist;
+  unsigned long long* status;
+  uint32_t* hist;       // [nitems][2048] fallback histograms
+  uint32_t* ctrs;       // 2 dynamic tile counters
+  uint32_t* start;      // sparse-reduce start offsets
+  uint64_t* host_mt0;   // host copy of items[].mt0 and merge tiles per item (for grid sizing)
+  uint64_t* host_mtiles;
+};
+// Runs the whole selection for items [item0, item0 + nitems) (their TopkItem rows), writes
+// payloads, updates residuals.  aitems = the call's Item table (same order), g = gradient
+// base, r = residual base.
+void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems,
+                 uint64_t a_chunks, const Item* aitems, const float* g, float* r, uint8_t* slots,
+                 uint32_t* flags, int value_type, uint64_t merge_tiles);
+// Sparse decompress + tree-average (tile merge over the ascending index lists).
+// entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).
+void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
+                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out);
+
+}  // namespace nb

@@ -1,0 +1,417 @@
+// kernels_dense.cu — sm_100a streaming kernels for the dense codecs and the dense reducer.
+//
+//   K1 k_fp16        : p = g + r; h = RNE16(p); r <- p - h                     (one pass, 14 B/elem)
+//   K2 k_absmax      : m = max |g + r| (bit max; NaN/Inf detected as bits >= 0x7F800000)
+//   K3 k_int8_quant  : s = fl(m/127); q = clamp(rint(p/s)); r <- p - q*s      (8+4+1 B/elem)
+//   K0 k_identity    : payload <- g                                            (non-finite check)
+//   K8 k_reduce_dense: out = tree_sum_c D(slot_c) / P                          (P*b + 4 B/elem)
+//
+// Layout: every kernel walks a table of Items (one per (cluster, bucket)); the global
+// chunk space (4096 elements per chunk) is the concatenation of all items' chunks, walked
+// grid-stride by a persistent grid of ~8 CTAs x 148 SMs.  Each thread moves 4 quads
+// (16 B each of g and r) per chunk with 128-bit loads; payload bytes are written with
+// 32/64/128-bit stores.  Paper passages: PAPER.md:101 / :418 (INT8 gradient compression),
+// PAPER.md:125-130 Eq. 5 (FP16), PAPER.md:76 (aggregation).
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+
+namespace nb {
+
+template <bool VEC>
+__device__ __forceinline__ float4 ldq(const float* base, uint64_t q) {
+  if constexpr (VEC) {
+    return ld4_stream(base + 4 * q);
+  } else {
+    const float* p = base + 4 * q;
+    return make_float4(p[0], p[1], p[2], p[3]);
+  }
+}
+template <bool VEC>
+__device__ __forceinline__ void stq(float* base, uint64_t q, float4 v) {
+  if constexpr (VEC) {
+    st4(base + 4 * q, v);
+  } else {
+    float* p = base + 4 * q;
+    p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w;
+  }
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+// ----------------------------------------------------------------------------- IDENTITY
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ items, int nitems, uint64_t chunks,
+                                                       const float* __restrict__ gbase, uint8_t* __restrict__ slots,
+                                                       uint32_t* flags) {
+  int hint = 0;
+  bool bad = false;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    const Item it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const float* g = gbase + it.g_off;
+    uint8_t* slot = slots + it.slot_off;
+    float* body = reinterpret_cast<float*>(slot + 16);
+    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_IDENTITY, (uint32_t)it.n, 1.0f, 0u);
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 v = ldq<VEC>(g, q);
+        bad |= nonfinite_bits(abs_bits(v.x)) | nonfinite_bits(abs_bits(v.y)) | nonfinite_bits(abs_bits(v.z)) |
+               nonfinite_bits(abs_bits(v.w));
+        st4(body + 4 * q, v);
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float v = g[e];
+      bad |= nonfinite_bits(abs_bits(v));
+      body[e] = v;
+    }
+  }
+  raise_flags(flags, bad, false);
+}
+
+// ----------------------------------------------------------------------------- FP16 + EF
+__device__ __forceinline__ float fp16_one(float p, uint16_t& hb, bool& bad, bool& ovf) {
+  __half h = __float2half_rn(p);              // IEEE binary32 -> binary16, RNE, subnormals kept
+  hb = __half_as_ushort(h);
+  const uint32_t ab = abs_bits(p);
+  bad |= nonfinite_bits(ab);
+  ovf |= ((hb & 0x7FFFu) == 0x7C00u) && !nonfinite_bits(ab);   // finite p rounded to +-inf (R10)
+  return __half2float(h);
+}
+
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ items, int nitems, uint64_t chunks,
+                                                   const float* __restrict__ gbase, float* __restrict__ rbase,
+                                                   uint8_t* __restrict__ slots, uint32_t* flags) {
+  int hint = 0;
+  bool bad = false, ovf = false;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    const Item it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    uint8_t* slot = slots + it.slot_off;
+    uint16_t* body = reinterpret_cast<uint16_t*>(slot + 16);
+    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_FP16, (uint32_t)it.n, 1.0f, 0u);
+    float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        gv[u] = ldq<VEC>(g, q);
+        if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
+        uint16_t h0, h1, h2, h3;
+        float4 d;
+        d.x = fp16_one(p.x, h0, bad, ovf);
+        d.y = fp16_one(p.y, h1, bad, ovf);
+        d.z = fp16_one(p.z, h2, bad, ovf);
+        d.w = fp16_one(p.w, h3, bad, ovf);
+        uint2 packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
+        *reinterpret_cast<uint2*>(body + 4 * q) = packed;
+        if constexpr (EF)
+          st4(r + 4 * q, make_float4(__fsub_rn(p.x, d.x), __fsub_rn(p.y, d.y), __fsub_rn(p.z, d.z),
+                                     __fsub_rn(p.w, d.w)));
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      uint16_t hb;
+      float d = fp16_one(p, hb, bad, ovf);
+      body[e] = hb;
+      if constexpr (EF) r[e] = __fsub_rn(p, d);
+    }
+  }
+  raise_flags(flags, bad, ovf);
+}
+
+// ----------------------------------------------------------------------------- INT8 pass 1
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_absmax(const Item* __restrict__ items, int nitems, uint64_t chunks,
+                                                     const float* __restrict__ gbase, const float* __restrict__ rbase,
+                                                     uint32_t* __restrict__ scratch) {
+  int hint = 0, cur = -1;
+  uint32_t m = 0;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    if (i != cur) {  // block-uniform: flush the running max of the previous item
+      if (cur >= 0) {
+        uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+        if ((threadIdx.x & 31) == 0 && w) atomicMax(&scratch[items[cur].sidx], w);
+      }
+      cur = i;
+      m = 0;
+    }
+    const Item it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const float* g = gbase + it.g_off;
+    const float* r = rbase + it.r_off;
+    float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        gv[u] = ldq<VEC>(g, q);
+        if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
+        m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      m = max(m, abs_bits(p));
+    }
+  }
+  if (cur >= 0) {
+    uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && w) atomicMax(&scratch[items[cur].sidx], w);
+  }
+}
+
+// ----------------------------------------------------------------------------- INT8 pass 2
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict__ items, int nitems, uint64_t chunks,
+                                                         const float* __restrict__ gbase, float* __restrict__ rbase,
+                                                         uint8_t* __restrict__ slots,
+                                                         const uint32_t* __restrict__ scratch, uint32_t* flags) {
+  int hint = 0;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    const Item it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const uint32_t mbits = scratch[it.sidx];
+    if (nonfinite_bits(mbits)) {  // all-or-nothing: nothing of this bucket is written
+      if (j == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+      continue;
+    }
+    const float s = int8_scale_from_bits(mbits);
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    uint8_t* slot = slots + it.slot_off;
+    uint8_t* body = slot + 16;
+    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
+    float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        gv[u] = ldq<VEC>(g, q);
+        if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
+        int q0 = int8_q(p.x, s), q1 = int8_q(p.y, s), q2 = int8_q(p.z, s), q3 = int8_q(p.w, s);
+        reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(q0, q1, q2, q3);
+        if constexpr (EF)
+          st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)q0, s)), __fsub_rn(p.y, __fmul_rn((float)q1, s)),
+                                     __fsub_rn(p.z, __fmul_rn((float)q2, s)), __fsub_rn(p.w, __fmul_rn((float)q3, s))));
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      int qe = int8_q(p, s);
+      body[e] = (uint8_t)(qe & 0xFF);
+      if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- reduce
+template <int METHOD, int P>
+__device__ __forceinline__ float4 decode_quad(const uint8_t* slot, uint64_t q, float s) {
+  const uint8_t* body = slot + 16;
+  if constexpr (METHOD == M_IDENTITY) {
+    return ld4_stream(reinterpret_cast<const float*>(body) + 4 * q);
+  } else if constexpr (METHOD == M_FP16) {
+    uint2 w = *reinterpret_cast<const uint2*>(body + 8 * q);
+    return make_float4(__half2float(__ushort_as_half((unsigned short)(w.x & 0xFFFF))),
+                       __half2float(__ushort_as_half((unsigned short)(w.x >> 16))),
+                       __half2float(__ushort_as_half((unsigned short)(w.y & 0xFFFF))),
+                       __half2float(__ushort_as_half((unsigned short)(w.y >> 16))));
+  } else {
+    uint32_t w = reinterpret_cast<const uint32_t*>(body)[q];
+    return make_float4(__fmul_rn((float)(int8_t)(w & 0xFF), s), __fmul_rn((float)(int8_t)((w >> 8) & 0xFF), s),
+                       __fmul_rn((float)(int8_t)((w >> 16) & 0xFF), s), __fmul_rn((float)(int8_t)(w >> 24), s));
+  }
+}
+template <int METHOD>
+__device__ __forceinline__ float decode_one(const uint8_t* slot, uint64_t e, float s) {
+  const uint8_t* body = slot + 16;
+  if constexpr (METHOD == M_IDENTITY) return reinterpret_cast<const float*>(body)[e];
+  else if constexpr (METHOD == M_FP16) return __half2float(reinterpret_cast<const __half*>(body)[e]);
+  else return __fmul_rn((float)(int8_t)body[e], s);
+}
+
+template <int METHOD, int P, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restrict__ items, int nitems, uint64_t chunks,
+                                                           const uint8_t* __restrict__ slots, float* __restrict__ obase) {
+  constexpr int UG = P <= 2 ? 4 : (P <= 4 ? 2 : 1);   // quads in flight per thread (registers: UG*P float4)
+  int hint = 0;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    const RItem it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const uint8_t* s0 = slots + it.slot_off;
+    float* out = obase + it.out_off;
+    float sc[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(s0 + k * it.pb + 8) : 1.0f;
+#pragma unroll
+    for (int u0 = 0; u0 < kQuadsPerThread; u0 += UG) {
+      float4 d[UG][P];
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const uint64_t q = j * kChunkQuads + (uint64_t)(u0 + u) * kThreads + threadIdx.x;
+        if (q < n4) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) d[u][k] = decode_quad<METHOD, P>(s0 + k * it.pb, q, sc[k]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const uint64_t q = j * kChunkQuads + (uint64_t)(u0 + u) * kThreads + threadIdx.x;
+        if (q < n4) {
+          float vx[P], vy[P], vz[P], vw[P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) { vx[k] = d[u][k].x; vy[k] = d[u][k].y; vz[k] = d[u][k].z; vw[k] = d[u][k].w; }
+          const float fp = (float)P;
+          float4 o = make_float4(__fdiv_rn(tree_sum<0, P>(vx), fp), __fdiv_rn(tree_sum<0, P>(vy), fp),
+                                 __fdiv_rn(tree_sum<0, P>(vz), fp), __fdiv_rn(tree_sum<0, P>(vw), fp));
+          stq<VEC>(out, q, o);
+        }
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float v[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(s0 + k * it.pb, e, sc[k]);
+      out[e] = __fdiv_rn(tree_sum<0, P>(v), (float)P);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- launchers
+static inline unsigned grid_for(const Launch& L, uint64_t chunks, int per_sm = 8) {
+  uint64_t g = (uint64_t)L.num_sms * per_sm;
+  if (chunks < g) g = chunks;
+  return (unsigned)(g ? g : 1);
+}
+
+void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
+                     uint8_t* slots, uint32_t* flags) {
+  if (!chunks) return;
+  Mark mk(L, PH_IDENTITY);
+  dim3 grid(grid_for(L, chunks));
+  if (vec) k_identity<true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
+  else k_identity<false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
+  ++*L.launches;
+}
+
+void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
+                 float* r, uint8_t* slots, uint32_t* flags) {
+  if (!chunks) return;
+  Mark mk(L, PH_FP16);
+  dim3 grid(grid_for(L, chunks));
+  if (ef && vec) k_fp16<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else if (ef) k_fp16<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else if (vec) k_fp16<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else k_fp16<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  ++*L.launches;
+}
+
+void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                   const float* g, const float* r, uint32_t* scratch) {
+  if (!chunks) return;
+  Mark mk(L, PH_ABSMAX);
+  dim3 grid(grid_for(L, chunks));
+  if (ef && vec) k_absmax<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else if (ef) k_absmax<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else if (vec) k_absmax<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else k_absmax<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  ++*L.launches;
+}
+
+void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                       const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags) {
+  if (!chunks) return;
+  Mark mk(L, PH_INT8_QUANT);
+  dim3 grid(grid_for(L, chunks));
+  if (ef && vec) k_int8_quant<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (ef) k_int8_quant<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (vec) k_int8_quant<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else k_int8_quant<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  ++*L.launches;
+}
+
+template <int METHOD, int P>
+static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const uint8_t* slots,
+                     float* out) {
+  dim3 grid(grid_for(L, chunks));
+  if (vec) k_reduce_dense<METHOD, P, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
+  else k_reduce_dense<METHOD, P, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
+}
+template <int METHOD>
+static void reduce_m(const Launch& L, int P, bool vec, const RItem* items, int nitems, uint64_t chunks,
+                     const uint8_t* slots, float* out) {
+  switch (P) {
+    case 1: reduce_p<METHOD, 1>(L, vec, items, nitems, chunks, slots, out); break;
+    case 2: reduce_p<METHOD, 2>(L, vec, items, nitems, chunks, slots, out); break;
+    case 3: reduce_p<METHOD, 3>(L, vec, items, nitems, chunks, slots, out); break;
+    case 4: reduce_p<METHOD, 4>(L, vec, items, nitems, chunks, slots, out); break;
+    case 5: reduce_p<METHOD, 5>(L, vec, items, nitems, chunks, slots, out); break;
+    case 6: reduce_p<METHOD, 6>(L, vec, items, nitems, chunks, slots, out); break;
+    case 7: reduce_p<METHOD, 7>(L, vec, items, nitems, chunks, slots, out); break;
+    default: reduce_p<METHOD, 8>(L, vec, items, nitems, chunks, slots, out); break;
+  }
+}
+void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems, uint64_t chunks,
+                         const uint8_t* slots, float* out) {
+  if (!chunks) return;
+  Mark mk(L, PH_REDUCE_DENSE);
+  if (method == M_IDENTITY) reduce_m<M_IDENTITY>(L, P, vec, items, nitems, chunks, slots, out);
+  else if (method == M_FP16) reduce_m<M_FP16>(L, P, vec, items, nitems, chunks, slots, out);
+  else reduce_m<M_INT8>(L, P, vec, items, nitems, chunks, slots, out);
+  ++*L.launches;
+}
+
+bool int8_onchip_capacity(int, uint64_t* max_elems, int* grid, size_t* smem) {
+  *max_elems = 0; *grid = 0; *smem = 0;
+  return false;
+}
+void launch_int8_onchip(const Launch&, bool, bool, const Item*, int, const float*, float*, uint8_t*, uint32_t*,
+                        uint32_t*, uint32_t*, int, size_t) {}
+
+}  // namespace nb

@@ -1,0 +1,816 @@
+// kernels_topk.cu — exact top-k selection with error feedback, and the sparse reducer.
+//
+// Selection rule (R11; PAPER.md:63/:99 cite top-k sparsification without defining
+// it): the k largest keys key_i = bits(p_i) & 0x7FFFFFFF (|p| order, -0 == +0); equal keys
+// resolved by the lower index; payload indices ascending.  The pipeline never sorts:
+//
+//   A  k_topk_a        (streaming, 12 B/elem) p = g + r -> r; max-abs bits; every S-th key
+//                       into a sample                                   [EF fused]
+//   B  k_topk_bracket  (1 CTA/item) radix-select two ranks of the sample -> bracket
+//                       [t_lo, t_hi] that holds the true k-th key with overwhelming odds
+//   C  k_topk_classify (streaming, 4 B/elem) winners key > t_hi, candidates t_lo<=key<=t_hi;
+//                       ORDERED compaction of both (decoupled look-back over tiles, two
+//                       counters packed in one 64-bit status word)
+//   D  k_topk_resolve  (1 CTA/item) verify W < k <= W + C; radix-select the exact threshold T
+//                       among the candidates; keep key > T and the first need_T keys == T
+//   (fallback, only items whose bracket failed: 3 full radix-histogram passes give the exact
+//    T, then C and D rerun with t_lo = t_hi = T — bounded memory, always exact)
+//   F  k_topk_merge    merge-path of the two ascending lists -> payload idx[k], val[k];
+//                       residual at the selected positions r = p - D(v)
+//
+// The reducer scatters each cluster's (idx, val) into shared-memory tiles pre-filled with
+// +0.0 and tree-sums them (R16), after a pass that turns each ascending index list into
+// per-tile start offsets.
+#include <cuda_fp16.h>
+
+#include <new>
+
+#include "kernels.h"
+
+namespace nb {
+
+constexpr int kSelThreads = 1024;  // single-CTA radix select
+constexpr int kMergeTile = 1024;   // outputs per merge CTA
+constexpr int kRedTile = 2048;     // elements per sparse-reduce CTA
+constexpr int kRedThreads = 256;
+
+// ---------------------------------------------------------------- status word (look-back)
+// bits 63..62 flag (0 none, 1 aggregate, 2 inclusive prefix), 61..31 winners, 30..0 candidates
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint64_t w, uint64_t c) {
+  return ((unsigned long long)flag << 62) | ((unsigned long long)w << 31) | (unsigned long long)c;
+}
+
+// ---------------------------------------------------------------- block helpers
+// Inclusive scan of a 64-bit value over a CTA of NT threads; returns inclusive, *total.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_incl_scan(unsigned long long v, unsigned long long* smem,
+                                                              unsigned long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < NT / 32 ? smem[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < NT / 32) smem[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) v += smem[warp - 1];
+  *total = smem[NT / 32 - 1];
+  __syncthreads();
+  return v;
+}
+
+// hist[nbins] in shared memory (bin value = digit).  Find the bin holding descending rank
+// `rank` (1-based): above(b) < rank <= above(b) + hist[b].  Results in *bin/*above (smem).
+__device__ void find_bin(const uint32_t* hist, int nbins, uint32_t rank, uint32_t* s_bin, uint32_t* s_above,
+                         unsigned long long* scan_smem) {
+  // thread t owns descending bins nbins-1-2t, nbins-2-2t
+  const int t = threadIdx.x;
+  const int b0 = nbins - 1 - 2 * t, b1 = b0 - 1;
+  const uint32_t h0 = b0 >= 0 ? hist[b0] : 0, h1 = b1 >= 0 ? hist[b1] : 0;
+  unsigned long long tot;
+  const unsigned long long incl = block_incl_scan<kSelThreads>((unsigned long long)(h0 + h1), scan_smem, &tot);
+  const unsigned long long excl = incl - (h0 + h1);
+  if (excl < rank && rank <= incl) {
+    if (rank <= excl + h0) { *s_bin = (uint32_t)b0; *s_above = (uint32_t)excl; }
+    else { *s_bin = (uint32_t)b1; *s_above = (uint32_t)(excl + h0); }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void hist_add(uint32_t* hist, bool active, uint32_t bin) {
+  // warp-aggregated shared-memory increment (many equal keys would serialise otherwise)
+  const unsigned mask = __activemask();
+  const unsigned peers = __match_any_sync(mask, active ? bin : 0xFFFFFFFFu);
+  if (active && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+}
+
+struct Digit { int shift, bits; };
+__device__ __forceinline__ Digit digit_of(int d) {
+  return d == 0 ? Digit{20, 11} : (d == 1 ? Digit{9, 11} : Digit{0, 9});
+}
+
+// Radix select inside one CTA: key at descending rank `rank` (1 <= rank <= m) of keys
+// produced by get(i), i < m.  Returns T, and *above = #{key > T}.
+template <class GetKey>
+__device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* above_out, uint32_t* hist,
+                               uint32_t* s_misc, unsigned long long* scan_smem) {
+  uint32_t prefix = 0, above = 0, left = rank;
+  for (int d = 0; d < 3; ++d) {
+    const Digit dg = digit_of(d);
+    const int nb = 1 << dg.bits;
+    for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int hs = dg.shift + dg.bits;  // bits above this digit must equal the prefix
+    for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
+      const uint32_t i = i0 + threadIdx.x;
+      bool act = false;
+      uint32_t bin = 0;
+      if (i < m) {
+        const uint32_t key = get(i);
+        act = (hs >= 31) ? true : ((key >> hs) == prefix);
+        bin = (key >> dg.shift) & (nb - 1);
+      }
+      hist_add(hist, act, bin);
+    }
+    __syncthreads();
+    find_bin(hist, nb, left, &s_misc[0], &s_misc[1], scan_smem);
+    const uint32_t b = s_misc[0], ab = s_misc[1];
+    prefix = (prefix << dg.bits) | b;
+    above += ab;
+    left -= ab;
+    __syncthreads();
+  }
+  *above_out = above;
+  return prefix;
+}
+
+// ---------------------------------------------------------------- A: EF + sample + max
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_topk_a(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems,
+                                                     TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                     const float* __restrict__ gbase, float* __restrict__ rbase,
+                                                     uint32_t* __restrict__ sample, unsigned long long* __restrict__ status,
+                                                     uint32_t* ctrs) {
+  int hint = 0, cur = -1;
+  uint32_t m = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 2) ctrs[threadIdx.x] = 0;  // classify tile counters
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(aitems, nitems, c, hint);
+    hint = i;
+    if (i != cur) {
+      if (cur >= 0) {
+        uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+        if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
+      }
+      cur = i;
+      m = 0;
+    }
+    const Item it = aitems[i];
+    const TopkItem& ti = titems[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const uint32_t S = ti.stride;
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    uint32_t* smp = sample + ti.sample_off;
+    if (threadIdx.x == 0) status[ti.status_off + j] = 0ull;
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 gv;
+        if constexpr (VEC) gv = ld4_stream(g + 4 * q);
+        else gv = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+        float4 p = gv;
+        if constexpr (EF) {
+          float4 rv = ld4_stream(r + 4 * q);
+          p = make_float4(__fadd_rn(gv.x, rv.x), __fadd_rn(gv.y, rv.y), __fadd_rn(gv.z, rv.z), __fadd_rn(gv.w, rv.w));
+          st4(r + 4 * q, p);
+        }
+        m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+        if (((4 * q) & (S - 1)) == 0) smp[(4 * q) / S] = abs_bits(p.x);
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      if constexpr (EF) r[e] = p;
+      m = max(m, abs_bits(p));
+      if ((e & (S - 1)) == 0) smp[e / S] = abs_bits(p);
+    }
+  }
+  if (cur >= 0) {
+    uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
+  }
+}
+
+// ---------------------------------------------------------------- B: bracket from the sample
+__global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __restrict__ titems,
+                                                              TopkState* __restrict__ st,
+                                                              const uint32_t* __restrict__ sample, uint32_t* flags,
+                                                              int value_type) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t misc[4];
+  __shared__ unsigned long long scan[32];
+  const TopkItem ti = titems[blockIdx.x];
+  TopkState& S = st[blockIdx.x];
+  const uint32_t mb = S.maxbits;
+  if (nonfinite_bits(mb)) {
+    if (threadIdx.x == 0) { S.failed = 2; atomicOr(flags, kFlagNonfinite); }
+    return;
+  }
+  const uint32_t ns = (uint32_t)ti.nsample;
+  const double ks = (double)ti.k * (double)ns / (double)(ti.n ? ti.n : 1);
+  const double delta = 5.0 * sqrt(ks + 1.0) + 16.0;
+  const double rh = floor(ks - delta), rl = ceil(ks + delta);
+  const uint32_t* smp = sample + ti.sample_off;
+  auto get = [&](uint32_t i) { return smp[i]; };
+  uint32_t t_hi = 0xFFFFFFFFu, t_lo = 0u, dummy;
+  if (ti.k >= ti.n) {          // everything selected: no winners, all candidates
+    t_hi = 0xFFFFFFFFu; t_lo = 0u;
+  } else {
+    if (rh >= 1.0 && ns > 0) t_hi = cta_select(get, ns, (uint32_t)rh, &dummy, hist, misc + 2, scan);
+    if (rl <= (double)ns && ns > 0) t_lo = cta_select(get, ns, (uint32_t)rl, &dummy, hist, misc + 2, scan);
+    if (t_hi != 0xFFFFFFFFu && t_lo > t_hi) t_lo = t_hi;
+  }
+  if (threadIdx.x == 0) {
+    S.t_lo = t_lo;
+    S.t_hi = t_hi;
+    S.mode = 0;
+    S.path = 0;
+    S.scale = value_type == V_I8 ? int8_scale_from_bits(mb) : 1.0f;
+  }
+}
+
+// ---------------------------------------------------------------- C: classify + ordered compaction
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restrict__ aitems,
+                                                            const TopkItem* __restrict__ titems,
+                                                            TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                            const float* __restrict__ pbase, bool p_in_r,
+                                                            const float* __restrict__ gbase,
+                                                            uint2* __restrict__ wl, uint2* __restrict__ cl,
+                                                            unsigned long long* __restrict__ status, uint32_t* ctr,
+                                                            int retry) {
+  __shared__ unsigned long long scan[kThreads / 32];
+  __shared__ uint64_t s_tile;
+  __shared__ unsigned long long s_prefix;
+  int hint = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const uint64_t c = s_tile;
+    __syncthreads();
+    if (c >= chunks) break;
+    const int i = find_item(aitems, nitems, c, hint);
+    hint = i;
+    const TopkState& S = st[i];
+    if (S.failed == 2) continue;
+    if (retry && S.mode != 1) continue;
+    const Item it = aitems[i];
+    const TopkItem& ti = titems[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const uint32_t t_lo = S.t_lo, t_hi = S.t_hi;
+    const float* p = p_in_r ? pbase + it.r_off : gbase + it.g_off;
+    const bool vec = p_in_r || VEC;
+    uint32_t kb[kQuadsPerThread][4];
+    unsigned long long pw = 0, pc = 0;
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      uint32_t wn = 0, cn = 0;
+      if (q < n4) {
+        float4 v = vec ? ld4_stream(p + 4 * q) : make_float4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+        kb[u][0] = __float_as_uint(v.x); kb[u][1] = __float_as_uint(v.y);
+        kb[u][2] = __float_as_uint(v.z); kb[u][3] = __float_as_uint(v.w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = kb[u][e] & 0x7FFFFFFFu;
+          wn += key > t_hi;
+          cn += (key >= t_lo) & (key <= t_hi);
+        }
+      } else {
+        kb[u][0] = kb[u][1] = kb[u][2] = kb[u][3] = 0;
+      }
+      pw |= (unsigned long long)wn << (12 * u);
+      pc |= (unsigned long long)cn << (12 * u);
+    }
+    // tail elements (n % 4, after every quad of the item) are a 5th field
+    uint32_t tkb = 0, tw = 0, tcn = 0;
+    const bool has_tail = (j == n4 / kChunkQuads) && threadIdx.x < (it.n & 3);
+    if (has_tail) {
+      tkb = __float_as_uint(p[n4 * 4 + threadIdx.x]);
+      const uint32_t key = tkb & 0x7FFFFFFFu;
+      tw = key > t_hi;
+      tcn = (key >= t_lo) & (key <= t_hi);
+    }
+    // two CTA scans of packed 12-bit fields: fields 0..3 = this thread's quads u, field 4 =
+    // its tail element; element order inside the tile is (field, thread, element)
+    pw |= (unsigned long long)tw << 48;
+    pc |= (unsigned long long)tcn << 48;
+    unsigned long long totw, totc;
+    const unsigned long long ew = block_incl_scan<kThreads>(pw, scan, &totw) - pw;
+    const unsigned long long ec = block_incl_scan<kThreads>(pc, scan, &totc) - pc;
+    uint32_t baseW[kQuadsPerThread + 1], baseC[kQuadsPerThread + 1];
+    uint32_t accW = 0, accC = 0;
+#pragma unroll
+    for (int u = 0; u <= kQuadsPerThread; ++u) {
+      baseW[u] = accW + (uint32_t)((ew >> (12 * u)) & 0xFFF);
+      baseC[u] = accC + (uint32_t)((ec >> (12 * u)) & 0xFFF);
+      accW += (uint32_t)((totw >> (12 * u)) & 0xFFF);
+      accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
+    }
+    const uint32_t tileW = accW, tileC = accC;
+    // decoupled look-back over this item's tiles
+    if (threadIdx.x == 0) {
+      unsigned long long* stw = status + ti.status_off;
+      unsigned long long prefix = 0;
+      if (j == 0) {
+        st_release(stw, pack_status(2, tileW, tileC));
+      } else {
+        st_release(stw + j, pack_status(1, tileW, tileC));
+        int64_t k = (int64_t)j - 1;
+        for (;;) {
+          unsigned long long v = ld_acquire(stw + k);
+          const uint32_t f = (uint32_t)(v >> 62);
+          if (f == 0) continue;
+          prefix += v & ((1ull << 62) - 1);
+          if (f == 2) break;
+          --k;
+        }
+        st_release(stw + j, pack_status(2, ((prefix >> 31) & 0x7FFFFFFFull) + tileW, (prefix & 0x7FFFFFFFull) + tileC));
+      }
+      s_prefix = prefix;
+      if (j + 1 == ti.nchunks) {  // last tile of the item publishes the totals
+        TopkState& Sw = st[i];
+        Sw.wcount = ((prefix >> 31) & 0x7FFFFFFFull) + tileW;
+        Sw.ccount = (prefix & 0x7FFFFFFFull) + tileC;
+      }
+    }
+    __syncthreads();
+    const uint64_t preW = (s_prefix >> 31) & 0x7FFFFFFFull, preC = s_prefix & 0x7FFFFFFFull;
+    uint2* W = wl + ti.list_off;
+    uint2* C = cl + ti.list_off;
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        uint32_t w = baseW[u], cc = baseC[u];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = kb[u][e] & 0x7FFFFFFFu;
+          const uint32_t idx = (uint32_t)(4 * q + e);
+          if (key > t_hi) {
+            const uint64_t pos = preW + w++;
+            if (pos < ti.wcap) W[pos] = make_uint2(idx, kb[u][e]);
+          } else if (key >= t_lo) {
+            const uint64_t pos = preC + cc++;
+            if (pos < ti.ccap) C[pos] = make_uint2(idx, kb[u][e]);
+          }
+        }
+      }
+    }
+    if (has_tail) {
+      const uint32_t key = tkb & 0x7FFFFFFFu;
+      const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
+      if (key > t_hi) {
+        const uint64_t pos = preW + baseW[kQuadsPerThread];
+        if (pos < ti.wcap) W[pos] = make_uint2(idx, tkb);
+      } else if (key >= t_lo) {
+        const uint64_t pos = preC + baseC[kQuadsPerThread];
+        if (pos < ti.ccap) C[pos] = make_uint2(idx, tkb);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- D: resolve among candidates
+__global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __restrict__ titems,
+                                                              TopkState* __restrict__ st, uint2* __restrict__ cl,
+                                                              int retry) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t misc[4];
+  __shared__ unsigned long long scan[32];
+  __shared__ uint32_t s_ok;
+  const TopkItem ti = titems[blockIdx.x];
+  TopkState& S = st[blockIdx.x];
+  if (S.failed == 2) return;
+  if (retry && S.mode != 1) return;
+  const uint64_t k = ti.k, W = S.wcount, C = S.ccount;
+  if (threadIdx.x == 0) {
+    bool ok = (W < k || k == 0) && (W + C >= k);
+    if (ok && C > ti.ccap) ok = (S.t_lo == S.t_hi) && (k - W) <= ti.ccap;  // exact tie set: prefix suffices
+    s_ok = ok;
+    if (!ok) { S.mode = 1; S.failed = 1; }   // -> exact radix fallback
+  }
+  __syncthreads();
+  if (!s_ok || k == 0) {
+    if (k == 0 && threadIdx.x == 0) { S.threshold = 0; S.count_above = 0; S.need = 0; }
+    return;
+  }
+  const uint32_t need = (uint32_t)(k - W);
+  uint2* cand = cl + ti.list_off;
+  const uint32_t m = (uint32_t)(C < ti.ccap ? C : ti.ccap);
+  uint32_t T, above_c = 0;
+  if (S.t_lo == S.t_hi) {
+    T = S.t_lo;
+  } else {
+    auto get = [&](uint32_t i) { return cand[i].y & 0x7FFFFFFFu; };
+    T = cta_select(get, m, need, &above_c, hist, misc + 2, scan);
+  }
+  const uint32_t needT = need - above_c;
+  // stable in-place compaction of the selected candidates
+  uint32_t outpos = 0, ties_seen = 0;
+  for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    uint2 e = make_uint2(0, 0);
+    uint32_t key = 0;
+    bool tie = false, gt = false;
+    if (i < m) {
+      e = cand[i];
+      key = e.y & 0x7FFFFFFFu;
+      gt = key > T;
+      tie = key == T;
+    }
+    unsigned long long tot;
+    const unsigned long long v = ((unsigned long long)tie << 32);
+    const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
+    const uint32_t tie_rank = ties_seen + (uint32_t)((incl - v) >> 32);
+    const bool sel = gt || (tie && tie_rank < needT);
+    unsigned long long tot2;
+    const unsigned long long sv = sel ? 1ull : 0ull;
+    const unsigned long long incl2 = block_incl_scan<kSelThreads>(sv, scan, &tot2);
+    if (sel) cand[outpos + (uint32_t)(incl2 - sv)] = e;   // reads of this round completed in the scans' barriers
+    outpos += (uint32_t)tot2;
+    ties_seen += (uint32_t)(tot >> 32);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S.threshold = T;
+    S.count_above = W + above_c;
+    S.need = needT;
+  }
+}
+
+// ---------------------------------------------------------------- fallback: full radix histograms
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_topk_hist(const Item* __restrict__ aitems,
+                                                        const TopkItem* __restrict__ titems,
+                                                        const TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                        const float* __restrict__ pbase, bool p_in_r,
+                                                        const float* __restrict__ gbase, uint32_t* __restrict__ ghist,
+                                                        int d) {
+  __shared__ uint32_t hist[2048];
+  const Digit dg = digit_of(d);
+  const int nb = 1 << dg.bits, hs = dg.shift + dg.bits;
+  int hint = 0, cur = -1;
+  for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(aitems, nitems, c, hint);
+    hint = i;
+    if (st[i].failed != 1) continue;
+    if (i != cur) {
+      if (cur >= 0) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+          if (hist[b]) { atomicAdd(&ghist[(size_t)cur * 2048 + b], hist[b]); hist[b] = 0; }
+        __syncthreads();
+      }
+      cur = i;
+    }
+    const Item it = aitems[i];
+    const uint32_t prefix = st[i].t_lo;  // fallback keeps the running prefix in t_lo
+    const uint64_t j = c - it.chunk0;
+    const float* p = p_in_r ? pbase + it.r_off : gbase + it.g_off;
+    for (int u = 0; u < 16; ++u) {
+      const uint64_t e = j * kChunkElems + (uint64_t)u * kThreads + threadIdx.x;
+      bool act = false;
+      uint32_t bin = 0;
+      if (e < it.n) {
+        const uint32_t key = __float_as_uint(p[e]) & 0x7FFFFFFFu;
+        act = (hs >= 31) || ((key >> hs) == prefix);
+        bin = (key >> dg.shift) & (nb - 1);
+      }
+      hist_add(hist, act, bin);
+    }
+  }
+  __syncthreads();
+  if (cur >= 0)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (hist[b]) atomicAdd(&ghist[(size_t)cur * 2048 + b], hist[b]);
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_topk_hist_select(const TopkItem* __restrict__ titems,
+                                                                  TopkState* __restrict__ st, uint32_t* ghist,
+                                                                  unsigned long long* __restrict__ status, int d) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t misc[4];
+  __shared__ unsigned long long scan[32];
+  const TopkItem ti = titems[blockIdx.x];
+  TopkState& S = st[blockIdx.x];
+  if (S.failed != 1) return;
+  const Digit dg = digit_of(d);
+  const int nb = 1 << dg.bits;
+  uint32_t* gh = ghist + (size_t)blockIdx.x * 2048;
+  for (int b = threadIdx.x; b < 2048; b += blockDim.x) { hist[b] = b < nb ? gh[b] : 0; gh[b] = 0; }
+  __syncthreads();
+  const uint32_t left = d == 0 ? (uint32_t)ti.k : (uint32_t)S.rank_left;
+  find_bin(hist, nb, left, &misc[0], &misc[1], scan);
+  if (threadIdx.x == 0) {
+    const uint32_t prefix = d == 0 ? 0u : S.t_lo;
+    const uint32_t np = (prefix << dg.bits) | misc[0];
+    const uint64_t above = (d == 0 ? 0ull : S.count_above) + misc[1];
+    S.rank_left = left - misc[1];
+    S.count_above = above;
+    S.t_lo = np;
+    if (d == 2) {  // exact T: rerun classify/resolve in exact mode
+      S.t_hi = np;
+      S.path = 1;
+    }
+  }
+  if (d == 2) {
+    for (uint64_t jj = threadIdx.x; jj < ti.nchunks; jj += blockDim.x) status[ti.status_off + jj] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) S.failed = 0;   // mode stays 1 (retry)
+  }
+}
+
+// ---------------------------------------------------------------- F: merge -> payload + residual
+__device__ __forceinline__ uint64_t merge_split(const uint2* A, uint64_t na, const uint2* B, uint64_t nb_, uint64_t d) {
+  // number of A elements among the first d outputs of merge(A, B) (indices are distinct)
+  uint64_t lo = d > nb_ ? d - nb_ : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (A[mid].x < B[d - 1 - mid].x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <bool EF>
+__global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __restrict__ titems,
+                                                           const TopkState* __restrict__ st, int nitems, uint64_t tbase,
+                                                           const uint2* __restrict__ wl, const uint2* __restrict__ cl,
+                                                           uint8_t* __restrict__ slots, float* __restrict__ rbase,
+                                                           uint32_t* flags) {
+  __shared__ uint2 sw[kMergeTile], ss[kMergeTile];
+  __shared__ uint64_t s_split[2];
+  const uint64_t t = tbase + blockIdx.x;
+  int i = 0;
+  {
+    int lo = 0, hi = nitems - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (titems[mid].mt0 <= t) lo = mid; else hi = mid - 1;
+    }
+    i = lo;
+  }
+  const TopkItem ti = titems[i];
+  const TopkState& S = st[i];
+  if (S.failed == 2) return;
+  uint8_t* slot = slots + ti.slot_off;
+  if (ti.k == 0) {
+    if (threadIdx.x == 0) write_preamble(slot, M_TOPK, 0u, 1.0f, ti.value_type);
+    return;
+  }
+  const uint64_t k = ti.k, W = S.wcount, Ns = k - W;
+  const uint64_t d0 = (t - ti.mt0) * kMergeTile, d1 = d0 + kMergeTile < k ? d0 + kMergeTile : k;
+  const uint2* A = wl + ti.list_off;
+  const uint2* B = cl + ti.list_off;
+  if (threadIdx.x < 2) s_split[threadIdx.x] = merge_split(A, W, B, Ns, threadIdx.x ? d1 : d0);
+  __syncthreads();
+  const uint64_t a0 = s_split[0], a1 = s_split[1], b0 = d0 - a0, b1 = d1 - a1;
+  const uint32_t na = (uint32_t)(a1 - a0), nbb = (uint32_t)(b1 - b0);
+  if (threadIdx.x < na) sw[threadIdx.x] = A[a0 + threadIdx.x];
+  if (threadIdx.x < nbb) ss[threadIdx.x] = B[b0 + threadIdx.x];
+  __syncthreads();
+  const int vt = (int)ti.value_type;
+  const float s = S.scale;
+  if (d0 == 0 && threadIdx.x == 0) write_preamble(slot, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
+  uint32_t* idx_out = reinterpret_cast<uint32_t*>(slot + 16);
+  uint8_t* val_out = slot + 16 + pad16(4 * k);
+  float* r = rbase + ti.r_off;
+  bool ovf = false;
+  const uint32_t x = threadIdx.x;
+  if (x < na + nbb) {
+    uint2 e;
+    uint32_t pos;
+    if (x < na) {  // lower_bound of sw[x].x in ss
+      e = sw[x];
+      uint32_t lo = 0, hi = nbb;
+      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (ss[mid].x < e.x) lo = mid + 1; else hi = mid; }
+      pos = x + lo;
+    } else {
+      const uint32_t y = x - na;
+      e = ss[y];
+      uint32_t lo = 0, hi = na;
+      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (sw[mid].x < e.x) lo = mid + 1; else hi = mid; }
+      pos = y + lo;
+    }
+    const uint64_t o = d0 + pos;
+    const float pv = __uint_as_float(e.y);
+    idx_out[o] = e.x;
+    float dv;
+    if (vt == V_F32) {
+      reinterpret_cast<float*>(val_out)[o] = pv;
+      dv = pv;
+    } else if (vt == V_F16) {
+      __half h = __float2half_rn(pv);
+      const uint16_t hb = __half_as_ushort(h);
+      ovf = (hb & 0x7FFFu) == 0x7C00u;
+      reinterpret_cast<uint16_t*>(val_out)[o] = hb;
+      dv = __half2float(h);
+    } else {
+      const int q = int8_q(pv, s);
+      val_out[o] = (uint8_t)(q & 0xFF);
+      dv = __fmul_rn((float)q, s);
+    }
+    if constexpr (EF) r[e.x] = __fsub_rn(pv, dv);
+  }
+  // zero the padding of the two sections (the tile that ends the item)
+  if (d1 == k) {
+    const uint64_t ib = 4 * k, ipad = pad16(ib), vb = (vt == V_F32 ? 4 : (vt == V_F16 ? 2 : 1)) * k, vpad = pad16(vb);
+    uint8_t* ip = slot + 16;
+    for (uint64_t z = ib + threadIdx.x; z < ipad; z += blockDim.x) ip[z] = 0;
+    for (uint64_t z = vb + threadIdx.x; z < vpad; z += blockDim.x) val_out[z] = 0;
+  }
+  if (__any_sync(0xFFFFFFFFu, ovf) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagOverflow);
+}
+
+// ---------------------------------------------------------------- sparse reduce
+template <class F>
+__device__ __forceinline__ int find_by(const RItem* items, int nitems, uint64_t g, F field) {
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (field(items[mid]) <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// start[c][t] = first entry of cluster c's ascending idx list with idx >= t * kRedTile,
+// t = 0..ntiles (one thread per entry e in [0, k]; each tile's start written exactly once)
+__global__ void k_topk_offsets(const RItem* __restrict__ items, int nitems, uint64_t total,
+                               const uint8_t* __restrict__ slots, uint32_t* __restrict__ start) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (g >= total) return;
+  const int i = find_by(items, nitems, g, [](const RItem& r) { return r.e0; });
+  const RItem it = items[i];
+  const uint64_t e = g - it.e0;  // 0..k
+  const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(slots + it.slot_off + (uint64_t)c * it.pb + 16);
+  uint32_t* s = start + it.sbase + (uint64_t)c * (ntiles + 1);
+  const int64_t cur = e < it.k ? (int64_t)(idx[e] / kRedTile) : (int64_t)ntiles;
+  const int64_t prev = e == 0 ? -1 : (int64_t)(idx[e - 1] / kRedTile);
+  for (int64_t t = prev + 1; t <= cur; ++t) s[t] = (uint32_t)e;
+}
+
+template <int P, bool VEC>
+__global__ void __launch_bounds__(kRedThreads) k_topk_reduce(const RItem* __restrict__ items, int nitems,
+                                                             const uint8_t* __restrict__ slots,
+                                                             const uint32_t* __restrict__ start,
+                                                             float* __restrict__ obase, int vt) {
+  extern __shared__ __align__(16) float acc_raw[];   // [P][kRedTile], dynamic (P = 8 needs 64 KB)
+  float (*acc)[kRedTile] = reinterpret_cast<float (*)[kRedTile]>(acc_raw);
+  const uint64_t t = blockIdx.x;
+  const int i = find_by(items, nitems, t, [](const RItem& r) { return r.t0; });
+  const RItem it = items[i];
+  const uint64_t lt = t - it.t0;
+  const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
+  const uint64_t e_base = lt * kRedTile;
+#pragma unroll
+  for (int c = 0; c < P; ++c)
+    for (int x = threadIdx.x; x < kRedTile; x += kRedThreads) acc[c][x] = 0.0f;   // +0.0 where not selected (R16)
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    const uint8_t* slot = slots + it.slot_off + (uint64_t)c * it.pb;
+    const uint32_t* idx = reinterpret_cast<const uint32_t*>(slot + 16);
+    const uint8_t* val = slot + 16 + pad16(4 * it.k);
+    const float s = *reinterpret_cast<const float*>(slot + 8);
+    const uint32_t* st = start + it.sbase + (uint64_t)c * (ntiles + 1);
+    const uint32_t a = st[lt], b = st[lt + 1];
+    for (uint32_t e = a + threadIdx.x; e < b; e += kRedThreads) {
+      const uint32_t x = idx[e] - (uint32_t)e_base;
+      float d;
+      if (vt == V_F32) d = reinterpret_cast<const float*>(val)[e];
+      else if (vt == V_F16) d = __half2float(reinterpret_cast<const __half*>(val)[e]);
+      else d = __fmul_rn((float)(int8_t)val[e], s);
+      acc[c][x] = d;
+    }
+  }
+  __syncthreads();
+  float* out = obase + it.out_off + e_base;
+  const uint64_t rem = it.n - e_base;
+  const uint32_t lim = (uint32_t)(rem < kRedTile ? rem : kRedTile);
+  const float fp = (float)P;
+  for (uint32_t x0 = threadIdx.x * 4; x0 < lim; x0 += kRedThreads * 4) {
+    float res[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float v[P];
+#pragma unroll
+      for (int c = 0; c < P; ++c) v[c] = acc[c][x0 + q];
+      res[q] = __fdiv_rn(tree_sum<0, P>(v), fp);
+    }
+    if (VEC && x0 + 4 <= lim) {
+      st4(out + x0, make_float4(res[0], res[1], res[2], res[3]));
+    } else {
+      for (int q = 0; q < 4 && x0 + q < lim; ++q) out[x0 + q] = res[q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+static inline unsigned grid_for(const Launch& L, uint64_t chunks, int per_sm = 8) {
+  uint64_t g = (uint64_t)L.num_sms * per_sm;
+  if (chunks < g) g = chunks;
+  return (unsigned)(g ? g : 1);
+}
+
+void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
+                 const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags, int value_type,
+                 uint64_t merge_tiles) {
+  if (nitems <= 0) return;
+  const TopkItem* ti = B.items + item0;
+  TopkState* st = B.state + item0;
+  {
+    Mark mk(L, PH_MEMSET);
+    cudaMemsetAsync(st, 0, sizeof(TopkState) * nitems, L.stream);
+  }
+  const unsigned ga = grid_for(L, a_chunks);
+  // A: EF add (p -> r), max-abs, sample
+  { Mark mk(L, PH_TOPK_A);
+  if (ef && vec) k_topk_a<true, true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
+  else if (ef) k_topk_a<true, false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
+  else if (vec) k_topk_a<false, true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
+  else k_topk_a<false, false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
+  }
+  // B: bracket from the sample
+  { Mark mk(L, PH_TOPK_BRACKET);
+  k_topk_bracket<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.sample, flags, value_type); }
+  // C + D: classify with the bracket, resolve among candidates
+  const unsigned gc = grid_for(L, a_chunks);
+  { Mark mk(L, PH_TOPK_CLASSIFY);
+  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0);
+  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0); }
+  { Mark mk(L, PH_TOPK_RESOLVE);
+  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0); }
+  // fallback for items whose bracket failed (no work otherwise): exact radix over p
+  {
+  Mark mkf(L, PH_TOPK_FALLBACK);
+  for (int d = 0; d < 3; ++d) {
+    if (vec) k_topk_hist<true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d);
+    else k_topk_hist<false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d);
+    k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, B.status, d);
+  }
+  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1);
+  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1);
+  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1);
+  }
+  Mark mkm(L, PH_TOPK_MERGE);
+  // F: merge -> payload, residual at the selected positions
+  const uint64_t tbase = B.host_mt0[item0];
+  if (ef) k_topk_merge<true><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots, r, flags);
+  else k_topk_merge<false><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots, r, flags);
+  *L.launches += 13;
+}
+
+template <int P>
+static void reduce_topk_p(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
+                          const uint8_t* slots, const uint32_t* start, float* out) {
+  const size_t smem = (size_t)P * kRedTile * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_topk_reduce<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_topk_reduce<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (vec) k_topk_reduce<P, true><<<(unsigned)tiles, kRedThreads, smem, L.stream>>>(items, nitems, slots, start, out, vt);
+  else k_topk_reduce<P, false><<<(unsigned)tiles, kRedThreads, smem, L.stream>>>(items, nitems, slots, start, out, vt);
+}
+
+void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
+                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out) {
+  if (entries) {
+    Mark mk(L, PH_TOPK_OFFSETS);
+    dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
+    k_topk_offsets<<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start);
+    ++*L.launches;
+  }
+  if (!tiles) return;
+  Mark mk(L, PH_TOPK_REDUCE);
+  switch (P) {
+    case 1: reduce_topk_p<1>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 2: reduce_topk_p<2>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 3: reduce_topk_p<3>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 4: reduce_topk_p<4>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 5: reduce_topk_p<5>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 6: reduce_topk_p<6>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 7: reduce_topk_p<7>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    default: reduce_topk_p<8>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+  }
+  ++*L.launches;
+}
+
+}  // namespace nb

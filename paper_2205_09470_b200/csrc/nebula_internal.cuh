@@ -1,0 +1,123 @@
+// nebula_internal.cuh — types and device helpers shared by the library's kernels.
+//
+// Everything here is B200 (sm_100a) device code or plain host bookkeeping.  The CPU oracle
+// (oracle/) shares nothing with this file.  Arithmetic rules:
+// every fp32 operation on the codec path is an explicitly rounded intrinsic
+// (__fadd_rn/__fsub_rn/__fmul_rn/__fdiv_rn), so no FMA contraction can change a bit
+// (contraction breaks the residual identity on ~5% of elements), and
+// the library is compiled without --use_fast_math, with -ftz=false -prec-div=true -fmad=false.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nb {
+
+constexpr int kThreads = 256;               // CTA size of the streaming kernels
+constexpr int kQuadsPerThread = 4;          // 4 x float4 per thread per chunk (64 B of g, 64 B of r in flight)
+constexpr int kChunkQuads = kThreads * kQuadsPerThread;
+constexpr uint64_t kChunkElems = (uint64_t)kChunkQuads * 4;   // 4096 elements per chunk
+
+enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u };
+enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3 };
+enum : int { V_F32 = 0, V_F16 = 1, V_I8 = 2 };
+
+// One (cluster, bucket) unit of codec work.  Offsets are relative to per-call base
+// pointers so the same table serves every step.
+struct Item {
+  uint64_t g_off;     // element offset of this item's gradient from the grad base
+  uint64_t r_off;     // element offset of its residual from the residual base (16-B aligned)
+  uint64_t slot_off;  // byte offset of its payload (preamble start) from the slot base
+  uint64_t n;         // coded elements
+  uint64_t chunk0;    // first global chunk index of this item in the launch
+  uint32_t sidx;      // scratch index (cluster * num_buckets + bucket)
+  uint32_t pad;
+};
+
+// One bucket of decompress-reduce work.
+struct RItem {
+  uint64_t slot_off;  // byte offset of slot 0 (cluster 0's payload) of this bucket
+  uint64_t pb;        // bytes per slot (stride between clusters' payloads)
+  uint64_t out_off;   // element offset of the output from the out base
+  uint64_t n;         // elements
+  uint64_t chunk0;    // dense: first chunk of this bucket in the launch
+  uint64_t k;         // TOPK: entries per payload
+  uint64_t e0;        // TOPK: prefix of (k + 1) over the launch's buckets (offsets pass)
+  uint64_t t0;        // TOPK: prefix of sparse-reduce tiles
+  uint64_t sbase;     // TOPK: base of this bucket's [P][tiles + 1] start offsets
+};
+
+__host__ __device__ inline uint64_t pad16(uint64_t b) { return (b + 15) & ~uint64_t(15); }
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+__device__ __forceinline__ bool nonfinite_bits(uint32_t ab) { return ab >= 0x7F800000u; }
+
+// Locate the item owning global chunk c.  Items are sorted by chunk0 and a CTA visits
+// chunks in increasing order, so a forward scan from the previous hit is amortised O(1).
+template <class T>
+__device__ __forceinline__ int find_item(const T* items, int nitems, uint64_t c, int hint) {
+  int i = hint;
+  while (i + 1 < nitems && items[i + 1].chunk0 <= c) ++i;
+  return i;
+}
+
+__device__ __forceinline__ float4 ld4_stream(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+__device__ __forceinline__ void raise_flags(uint32_t* flags, bool bad, bool ovf) {
+  unsigned m = __activemask();
+  unsigned b = __ballot_sync(m, bad), o = __ballot_sync(m, ovf);
+  if ((threadIdx.x & 31) == (__ffs(m) - 1)) {
+    uint32_t f = (b ? kFlagNonfinite : 0u) | (o ? kFlagOverflow : 0u);
+    if (f) atomicOr(flags, f);
+  }
+}
+
+// INT8 scale from the bucket's max-abs bits (readings R3/R4):
+// s = fl(m / 127); s := 1 when m == 0 or when fl(m/127) underflows to 0.
+__device__ __forceinline__ float int8_scale_from_bits(uint32_t mbits) {
+  float m = __uint_as_float(mbits);
+  float s = __fdiv_rn(m, 127.0f);
+  if (m == 0.0f || s == 0.0f) s = 1.0f;
+  return s;
+}
+
+// q = clamp(rint(fl(p / s)), -127, 127)  (R5 ties-to-even, R6 IEEE division, R7 clamp)
+__device__ __forceinline__ int int8_q(float p, float s) {
+  int q = __float2int_rn(__fdiv_rn(p, s));
+  return max(-127, min(127, q));
+}
+
+__device__ __forceinline__ uint32_t pack_i8x4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
+         ((uint32_t)(d & 0xFF) << 24);
+}
+
+// R16: fixed pairwise tree over cluster ids, sum(lo,hi) = sum(lo,mid) + sum(mid,hi) with
+// mid = lo + ceil((hi-lo)/2); every '+' one binary32 rounding.
+template <int LO, int HI>
+__device__ __forceinline__ float tree_sum(const float* v) {
+  if constexpr (HI - LO == 1) {
+    return v[LO];
+  } else {
+    constexpr int MID = LO + (HI - LO + 1) / 2;
+    return __fadd_rn(tree_sum<LO, MID>(v), tree_sum<MID, HI>(v));
+  }
+}
+
+__device__ __forceinline__ void write_preamble(uint8_t* slot, uint32_t method, uint32_t count, float scale,
+                                               uint32_t aux) {
+  uint4 pre = make_uint4(method, count, __float_as_uint(scale), aux);
+  *reinterpret_cast<uint4*>(slot) = pre;
+}
+
+}  // namespace nb

@@ -1,0 +1,715 @@
+// nebula_sync.cu — the C ABI (include/nebula_sync.h): context, argument validation, memory
+// plan, the three stages, NCCL transport over NVLink, LOOPBACK transport.
+//
+// Stage map:
+//   compress           a0 method gate -> [G>1: ncclReduceScatter(avg), PAPER.md:95]
+//                      -> a2..a6 EF + codec kernels (kernels_dense.cu / kernels_topk.cu)
+//   exchange           a7 in-place ncclAllGather of fixed-size payloads over the inter-cluster
+//                      communicator (slot c = cluster c); LOOPBACK: no-op
+//   decompress_reduce  a8 tree-average of the P slots -> [G>1: ncclAllGather of the shards]
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nebula_sync.h"
+#include "kernels.h"
+
+using namespace nb;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+enum BucketState { ST_IDLE = 0, ST_COMPRESSED = 1, ST_EXCHANGED = 2 };
+
+struct BucketInfo {
+  uint64_t n = 0;      // caller elements
+  uint64_t cn = 0;     // coded elements (n / G)
+  uint64_t off = 0;    // element offset in the caller's flat ALL buffers
+  uint64_t coff = 0;   // element offset in library coded buffers (multiple of 4)
+  uint64_t k = 0;      // TOPK entries
+  uint64_t pb[2] = {0, 0};  // payload bytes per slot, per layout (0: codec method, 1: IDENTITY phase)
+  uint64_t so[2] = {0, 0};  // byte offset of this bucket's [P][pb] slot block, per layout
+  int state = ST_IDLE;
+  int method = -1;     // method used by the last compress (after the start-step gate)
+};
+
+struct Table {         // one launch's work list, resident in d_items / d_ritems
+  int first = 0, count = 0;
+  uint64_t chunks = 0;
+  uint64_t entries = 0, tiles = 0;  // TOPK reduce: sum(k + 1), sum(ceil(n / 2048))
+  bool aligned = true; // every g_off (or out_off) is a multiple of 4 elements
+};
+
+struct DevGuard {
+  int old = -1, dev;
+  explicit DevGuard(int d) : dev(d) {
+    cudaGetDevice(&old);
+    if (old != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    if (old >= 0 && old != dev) cudaSetDevice(old);
+  }
+};
+
+}  // namespace
+
+struct nebula_ctx {
+  nebula_topology topo{};
+  nebula_codec codec{};
+  int P = 1, G = 1, Ploc = 1, me = 0, device = 0, num_sms = 148;
+  bool loopback = false;
+  std::vector<BucketInfo> b;
+  uint64_t total_n = 0, total_cn = 0, total_slots = 0;
+  cudaStream_t stream = nullptr;
+
+  float* d_resid = nullptr;      // [Ploc][total_cn]
+  uint8_t* d_slots = nullptr;    // [sum_b P * pb_b]
+  uint32_t* d_flags = nullptr;   // sticky device error bits
+  uint32_t* d_scratch = nullptr; // [Ploc * B] per-item max-abs bits
+  // Two slot layouts: [0] for the codec's method, [1] for the IDENTITY phase before
+  // start_step (only built when start_step > 0 and the method is lossy).  Slots are sized
+  // per method so the exchange moves exactly the payload bytes of the method in use.
+  int nlayouts = 1;
+  Item* d_items[2] = {nullptr, nullptr};   // all compress tables back to back
+  RItem* d_ritems[2] = {nullptr, nullptr}; // all reduce tables back to back
+  std::vector<Table> ctab[2];              // [0] = ALL, [1+b] = bucket b
+  std::vector<Table> rtab[2];
+  float* d_shard_in = nullptr;   // G > 1
+  float* d_shard_out = nullptr;
+  float* d_hgrad = nullptr;      // nebula_step_host staging
+  float* d_hout = nullptr;
+
+  TopkBuffers tk{};
+  void* d_topk_mem = nullptr;
+  std::vector<uint64_t> tk_mtiles;   // merge tiles per call type ([0] ALL, [1+b])
+  std::vector<uint64_t> tk_host_mt0; // per item
+
+  ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
+  uint64_t launches = 0;
+  std::string err;
+
+  // per-kernel event timers (nebula_timing_*)
+  bool timing = false;
+  std::vector<cudaEvent_t> evs;
+  size_t ev_next = 0;
+  struct Rec { int ph, a, b; };
+  std::vector<Rec> recs;
+  std::vector<std::pair<int, int>> open;  // (phase, start event) stack
+};
+
+static void timing_mark(void* p, int ph, int end) {
+  nebula_ctx* ctx = static_cast<nebula_ctx*>(p);
+  if (ctx->ev_next >= ctx->evs.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      ctx->evs.push_back(e);
+    }
+  }
+  const int id = (int)ctx->ev_next++;
+  cudaEventRecord(ctx->evs[id], ctx->stream);
+  if (!end) {
+    ctx->open.push_back({ph, id});
+  } else if (!ctx->open.empty()) {
+    auto o = ctx->open.back();
+    ctx->open.pop_back();
+    ctx->recs.push_back({o.first, o.second, id});
+  }
+}
+
+// ============================================================================ helpers
+#define CKC(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                   \
+      return NEBULA_ERR_CUDA;                                                          \
+    }                                                                                  \
+  } while (0)
+#define CKN(call)                                                                      \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess) {                                                           \
+      ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);                   \
+      return NEBULA_ERR_NCCL;                                                          \
+    }                                                                                  \
+  } while (0)
+
+static nebula_status fail(nebula_ctx* ctx, nebula_status s, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_init_error = msg;
+  return s;
+}
+
+static uint64_t topk_k_of(uint64_t n, const nebula_codec& c) {
+  // R12: k = clamp(floor(rho*n + 0.5), 1, n) in double, or the caller's k (capped at n)
+  if (n == 0) return 0;
+  if (c.topk_k > 0) return std::min<uint64_t>(c.topk_k, n);
+  double k = std::floor(c.topk_density * (double)n + 0.5);
+  if (k < 1) k = 1;
+  if (k > (double)n) k = (double)n;
+  return (uint64_t)k;
+}
+
+static uint64_t value_bytes(int vt) { return vt == V_F32 ? 4 : (vt == V_F16 ? 2 : 1); }
+
+static uint64_t payload_bytes_for(int method, uint64_t n, uint64_t k, int vt) {
+  switch (method) {
+    case M_IDENTITY: return 16 + pad16(4 * n);
+    case M_FP16: return 16 + pad16(2 * n);
+    case M_INT8: return 16 + pad16(n);
+    default: return 16 + pad16(4 * k) + pad16(value_bytes(vt) * k);
+  }
+}
+
+static uint64_t nchunks_of(uint64_t n) { return std::max<uint64_t>(1, (n + kChunkElems - 1) / kChunkElems); }
+
+// Host-side validation; no CUDA call is made before it passes (tested on CPU).
+static nebula_status validate(const nebula_topology* t, const nebula_codec* c, const uint64_t* numel, int nb_) {
+  if (!t || !c || !numel) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "null topology/codec/bucket_numel");
+  if (nb_ < 1) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "num_buckets must be >= 1");
+  if (t->num_clusters < 1 || t->num_clusters > NEBULA_MAX_CLUSTERS)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "num_clusters must be in [1, 8]");
+  if (t->transport != NEBULA_TRANSPORT_NCCL && t->transport != NEBULA_TRANSPORT_LOOPBACK)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown transport");
+  if (t->gpus_per_cluster < 1 || t->gpus_per_cluster > 64)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "gpus_per_cluster must be >= 1");
+  if (t->transport == NEBULA_TRANSPORT_LOOPBACK && t->gpus_per_cluster != 1)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "LOOPBACK simulates P clusters x 1 GPU (gpus_per_cluster must be 1)");
+  if (t->transport == NEBULA_TRANSPORT_NCCL) {
+    if (!t->nccl_unique_id) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "NCCL transport needs nccl_unique_id");
+    if (t->cluster_id < 0 || t->cluster_id >= t->num_clusters)
+      return fail(nullptr, NEBULA_ERR_INVALID_ARG, "cluster_id out of range");
+    if (t->local_rank < 0 || t->local_rank >= t->gpus_per_cluster)
+      return fail(nullptr, NEBULA_ERR_INVALID_ARG, "local_rank out of range");
+  }
+  if (t->device < 0) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "device must be >= 0");
+  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_TOPK)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown method");
+  if (c->error_feedback != 0 && c->error_feedback != 1)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "error_feedback must be 0 or 1");
+  if (c->method == NEBULA_TOPK) {
+    if (c->topk_values < NEBULA_VAL_F32 || c->topk_values > NEBULA_VAL_I8)
+      return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown topk value type");
+    if (c->topk_k == 0 && !(c->topk_density > 0.0 && c->topk_density <= 1.0))
+      return fail(nullptr, NEBULA_ERR_INVALID_ARG, "topk_density must be in (0, 1] when topk_k == 0");
+  }
+  for (int i = 0; i < nb_; ++i) {
+    if (numel[i] >= (1ull << 31)) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "bucket numel must be < 2^31");
+    if (numel[i] % (uint64_t)t->gpus_per_cluster)
+      return fail(nullptr, NEBULA_ERR_INVALID_ARG, "hierarchical mode needs every bucket numel % gpus_per_cluster == 0");
+  }
+  return NEBULA_OK;
+}
+
+// Method of a compress at `step` (Identity when step < start_step).
+static int method_at(const nebula_ctx* ctx, uint64_t step) {
+  return step < ctx->codec.start_step ? M_IDENTITY : ctx->codec.method;
+}
+
+static int layout_of(const nebula_ctx* ctx, int method) {
+  return (ctx->nlayouts == 2 && method == M_IDENTITY) ? 1 : 0;
+}
+
+static Launch launch_of(nebula_ctx* ctx) {
+  return Launch{ctx->stream, ctx->num_sms, &ctx->launches, ctx->timing ? timing_mark : nullptr, ctx};
+}
+
+// Bucket range of a call: ALL -> [0, B), b -> [b, b+1).
+static bool range_of(nebula_ctx* ctx, int32_t bucket, int* lo, int* hi) {
+  const int B = (int)ctx->b.size();
+  if (bucket == NEBULA_ALL_BUCKETS) { *lo = 0; *hi = B; return true; }
+  if (bucket < 0 || bucket >= B) return false;
+  *lo = bucket; *hi = bucket + 1;
+  return true;
+}
+
+// ============================================================================ init
+static nebula_status build_tables(nebula_ctx* ctx, int lay) {
+  const int B = (int)ctx->b.size();
+  std::vector<Item> items;
+  std::vector<RItem> ritems;
+  const uint64_t rtotal = ctx->total_cn;
+  std::vector<uint64_t> sbase(B + 1, 0);  // absolute start-offset bases (TOPK reduce)
+  for (int bi = 0; bi < B; ++bi) sbase[bi + 1] = sbase[bi] + (uint64_t)ctx->P * ((ctx->b[bi].cn + 2047) / 2048 + 1);
+  for (int t = 0; t <= B; ++t) {  // t == 0: ALL; t == 1 + b: bucket b alone
+    Table ct, rt;
+    ct.first = (int)items.size();
+    rt.first = (int)ritems.size();
+    const int blo = t == 0 ? 0 : t - 1, bhi = t == 0 ? B : t;
+    for (int bi = blo; bi < bhi; ++bi) {
+      const BucketInfo& bk = ctx->b[bi];
+      for (int c = 0; c < ctx->Ploc; ++c) {  // bucket-major, cluster-minor
+        Item it{};
+        if (ctx->G > 1) it.g_off = bk.coff;
+        else if (ctx->loopback) it.g_off = (t == 0) ? (uint64_t)c * ctx->total_n + bk.off : (uint64_t)c * bk.n;
+        else it.g_off = (t == 0) ? bk.off : 0;
+        it.r_off = (uint64_t)c * rtotal + bk.coff;
+        const int cl = ctx->loopback ? c : ctx->me;
+        it.slot_off = bk.so[lay] + (uint64_t)cl * bk.pb[lay];
+        it.n = bk.cn;
+        it.chunk0 = ct.chunks;
+        it.sidx = (uint32_t)(c * B + bi);
+        ct.chunks += nchunks_of(bk.cn);
+        ct.aligned &= (it.g_off % 4) == 0;
+        items.push_back(it);
+      }
+      RItem ri{};
+      ri.slot_off = bk.so[lay];
+      ri.pb = bk.pb[lay];
+      ri.out_off = ctx->G > 1 ? bk.coff : (t == 0 ? bk.off : 0);
+      ri.n = bk.cn;
+      ri.k = bk.k;
+      ri.chunk0 = rt.chunks;
+      ri.e0 = rt.entries;
+      ri.t0 = rt.tiles;
+      ri.sbase = sbase[bi];
+      rt.chunks += nchunks_of(bk.cn);
+      rt.entries += bk.k + 1;
+      rt.tiles += (bk.cn + 2047) / 2048;
+      rt.aligned &= (ri.out_off % 4) == 0;
+      ritems.push_back(ri);
+    }
+    ct.count = (int)items.size() - ct.first;
+    rt.count = (int)ritems.size() - rt.first;
+    ctx->ctab[lay].push_back(ct);
+    ctx->rtab[lay].push_back(rt);
+  }
+  CKC(cudaMalloc(&ctx->d_items[lay], items.size() * sizeof(Item)));
+  CKC(cudaMalloc(&ctx->d_ritems[lay], ritems.size() * sizeof(RItem)));
+  CKC(cudaMemcpy(ctx->d_items[lay], items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(ctx->d_ritems[lay], ritems.data(), ritems.size() * sizeof(RItem), cudaMemcpyHostToDevice));
+  return NEBULA_OK;
+}
+
+nebula_status topk_setup(nebula_ctx* ctx);  // below
+
+static void release(nebula_ctx* ctx) {
+  if (!ctx) return;
+  DevGuard g(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_resid);
+  cudaFree(ctx->d_slots);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_scratch);
+  for (int l = 0; l < 2; ++l) {
+    cudaFree(ctx->d_items[l]);
+    cudaFree(ctx->d_ritems[l]);
+  }
+  cudaFree(ctx->d_shard_in);
+  cudaFree(ctx->d_shard_out);
+  cudaFree(ctx->d_hgrad);
+  cudaFree(ctx->d_hout);
+  cudaFree(ctx->d_topk_mem);
+  for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
+  if (ctx->intra) ncclCommDestroy(ctx->intra);
+  if (ctx->inter && ctx->inter != ctx->world) ncclCommDestroy(ctx->inter);
+  if (ctx->world) ncclCommDestroy(ctx->world);
+  delete ctx;
+}
+
+extern "C" {
+
+int32_t nebula_abi_version(void) { return NEBULA_ABI_VERSION; }
+
+const char* nebula_status_string(nebula_status s) {
+  switch (s) {
+    case NEBULA_OK: return "NEBULA_OK";
+    case NEBULA_ERR_INVALID_ARG: return "NEBULA_ERR_INVALID_ARG";
+    case NEBULA_ERR_STATE: return "NEBULA_ERR_STATE";
+    case NEBULA_ERR_OOM: return "NEBULA_ERR_OOM";
+    case NEBULA_ERR_CUDA: return "NEBULA_ERR_CUDA";
+    case NEBULA_ERR_NCCL: return "NEBULA_ERR_NCCL";
+    case NEBULA_ERR_NONFINITE: return "NEBULA_ERR_NONFINITE";
+    case NEBULA_ERR_OVERFLOW: return "NEBULA_ERR_OVERFLOW";
+    case NEBULA_ERR_UNSUPPORTED: return "NEBULA_ERR_UNSUPPORTED";
+  }
+  return "NEBULA_ERR_UNKNOWN";
+}
+
+nebula_status nebula_get_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "null output buffer");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, NEBULA_ERR_NCCL, ncclGetErrorString(r));
+  static_assert(sizeof(id) == NEBULA_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return NEBULA_OK;
+}
+
+nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, const nebula_codec* codec,
+                               const uint64_t* bucket_numel, int32_t num_buckets, void* stream) {
+  if (!out) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  nebula_status v = validate(topo, codec, bucket_numel, num_buckets);
+  if (v != NEBULA_OK) return v;
+
+  nebula_ctx* ctx = new (std::nothrow) nebula_ctx();
+  if (!ctx) return fail(nullptr, NEBULA_ERR_OOM, "host allocation failed");
+  ctx->topo = *topo;
+  ctx->topo.nccl_unique_id = nullptr;
+  ctx->codec = *codec;
+  ctx->P = topo->num_clusters;
+  ctx->G = topo->gpus_per_cluster;
+  ctx->loopback = topo->transport == NEBULA_TRANSPORT_LOOPBACK;
+  ctx->Ploc = ctx->loopback ? ctx->P : 1;
+  ctx->me = ctx->loopback ? 0 : topo->cluster_id;
+  ctx->device = topo->device;
+  ctx->stream = (cudaStream_t)stream;
+
+  auto bail = [&](nebula_status s) {
+    g_init_error = ctx->err;
+    release(ctx);
+    return s;
+  };
+
+  {
+    DevGuard dg(ctx->device);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev <= ctx->device) {
+      ctx->err = std::string("no CUDA device ") + std::to_string(ctx->device) + ": " + cudaGetErrorString(e);
+      return bail(NEBULA_ERR_CUDA);
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+
+    // ---- memory plan
+    ctx->b.resize(num_buckets);
+    uint64_t off = 0, coff = 0, so = 0, so1 = 0;
+    for (int i = 0; i < num_buckets; ++i) {
+      BucketInfo& bk = ctx->b[i];
+      bk.n = bucket_numel[i];
+      bk.cn = bk.n / ctx->G;
+      bk.off = off;
+      bk.coff = coff;
+      bk.k = codec->method == NEBULA_TOPK ? topk_k_of(bk.cn, *codec) : 0;
+      bk.pb[0] = payload_bytes_for(codec->method, bk.cn, bk.k, codec->topk_values);
+      bk.pb[1] = payload_bytes_for(M_IDENTITY, bk.cn, 0, 0);
+      bk.so[0] = so;
+      bk.so[1] = so1;
+      off += bk.n;
+      coff += (bk.cn + 3) / 4 * 4;
+      so += (uint64_t)ctx->P * bk.pb[0];
+      so1 += (uint64_t)ctx->P * bk.pb[1];
+    }
+    ctx->nlayouts = (codec->start_step > 0 && codec->method != NEBULA_IDENTITY) ? 2 : 1;
+    ctx->total_n = off;
+    ctx->total_cn = coff;
+    ctx->total_slots = ctx->nlayouts == 2 ? std::max(so, so1) : so;
+
+    size_t rbytes = std::max<uint64_t>(16, (uint64_t)ctx->Ploc * ctx->total_cn * sizeof(float));
+    if (cudaMalloc(&ctx->d_resid, rbytes) != cudaSuccess) { ctx->err = "residual allocation failed"; return bail(NEBULA_ERR_OOM); }
+    if (cudaMalloc(&ctx->d_slots, std::max<uint64_t>(16, ctx->total_slots)) != cudaSuccess) { ctx->err = "payload allocation failed"; return bail(NEBULA_ERR_OOM); }
+    if (cudaMalloc(&ctx->d_flags, 16) != cudaSuccess) { ctx->err = "flag allocation failed"; return bail(NEBULA_ERR_OOM); }
+    if (cudaMalloc(&ctx->d_scratch, sizeof(uint32_t) * ctx->Ploc * num_buckets) != cudaSuccess) { ctx->err = "scratch allocation failed"; return bail(NEBULA_ERR_OOM); }
+    if (cudaMemset(ctx->d_resid, 0, rbytes) != cudaSuccess || cudaMemset(ctx->d_slots, 0, std::max<uint64_t>(16, ctx->total_slots)) != cudaSuccess ||
+        cudaMemset(ctx->d_flags, 0, 16) != cudaSuccess) { ctx->err = "memset failed"; return bail(NEBULA_ERR_CUDA); }
+    if (ctx->G > 1) {
+      if (cudaMalloc(&ctx->d_shard_in, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess ||
+          cudaMalloc(&ctx->d_shard_out, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess) { ctx->err = "shard allocation failed"; return bail(NEBULA_ERR_OOM); }
+    }
+    nebula_status s = NEBULA_OK;
+    for (int l = 0; l < ctx->nlayouts && s == NEBULA_OK; ++l) s = build_tables(ctx, l);
+    if (s != NEBULA_OK) return bail(s);
+    if (codec->method == NEBULA_TOPK) {
+      s = topk_setup(ctx);
+      if (s != NEBULA_OK) return bail(s);
+    }
+
+    // ---- communicators (collective over all P*G ranks)
+    if (!ctx->loopback) {
+      ncclUniqueId id;
+      std::memcpy(&id, topo->nccl_unique_id, sizeof(id));
+      const int nranks = ctx->P * ctx->G, rank = topo->cluster_id * ctx->G + topo->local_rank;
+      ncclResult_t r = ncclCommInitRank(&ctx->world, nranks, id, rank);
+      if (r != ncclSuccess) { ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r); return bail(NEBULA_ERR_NCCL); }
+      if (ctx->G == 1) {
+        ctx->inter = ctx->world;
+      } else {
+        r = ncclCommSplit(ctx->world, topo->local_rank, topo->cluster_id, &ctx->inter, nullptr);
+        if (r == ncclSuccess) r = ncclCommSplit(ctx->world, topo->cluster_id, topo->local_rank, &ctx->intra, nullptr);
+        if (r != ncclSuccess) { ctx->err = std::string("ncclCommSplit: ") + ncclGetErrorString(r); return bail(NEBULA_ERR_NCCL); }
+      }
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
+  }
+  *out = ctx;
+  return NEBULA_OK;
+}
+
+nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  ctx->stream = (cudaStream_t)stream;
+  return NEBULA_OK;
+}
+
+// ============================================================================ stages
+nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  int lo, hi;
+  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  if (!dev_grad && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
+  DevGuard dg(ctx->device);
+  const int method = method_at(ctx, step);
+  const bool ef = ctx->codec.error_feedback != 0;
+  const int lay = layout_of(ctx, method);
+  const Table& T = ctx->ctab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+  const Launch L = launch_of(ctx);
+
+  const float* gbase = dev_grad;
+  if (ctx->G > 1) {  // intra-cluster mean of the G GPUs' buckets -> this GPU's shard (R20)
+    Mark mk(L, PH_NCCL_RS);
+    CKN(ncclGroupStart());
+    for (int i = lo; i < hi; ++i) {
+      const BucketInfo& bk = ctx->b[i];
+      if (!bk.cn) continue;
+      const float* src = dev_grad + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+      CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.coff, bk.cn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    gbase = ctx->d_shard_in;
+  }
+  const bool vec = T.aligned && ((uintptr_t)gbase % 16 == 0);
+  const Item* items = ctx->d_items[lay] + T.first;
+
+  switch (method) {
+    case M_IDENTITY:
+      launch_identity(L, vec, items, T.count, T.chunks, gbase, ctx->d_slots, ctx->d_flags);
+      break;
+    case M_FP16:
+      launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_flags);
+      break;
+    case M_INT8: {
+      // zero the max-abs words of the items in this call (sidx = c * B + b)
+      {
+        Mark mk(L, PH_MEMSET);
+      if (bucket == NEBULA_ALL_BUCKETS) {
+        CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
+      } else {
+        for (int c = 0; c < ctx->Ploc; ++c)
+          CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
+      }
+      }
+      launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
+      launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch,
+                        ctx->d_flags);
+      break;
+    }
+    case M_TOPK: {
+      const int item0 = bucket == NEBULA_ALL_BUCKETS ? 0 : bucket * ctx->Ploc;
+      launch_topk(L, ef, vec, ctx->tk, item0, T.count, T.chunks, items, gbase, ctx->d_resid, ctx->d_slots,
+                  ctx->d_flags, ctx->codec.topk_values, ctx->tk_mtiles[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket]);
+      break;
+    }
+  }
+  CKC(cudaGetLastError());
+  for (int i = lo; i < hi; ++i) {
+    ctx->b[i].state = ST_COMPRESSED;
+    ctx->b[i].method = method;
+  }
+  return NEBULA_OK;
+}
+
+nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  int lo, hi;
+  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  for (int i = lo; i < hi; ++i)
+    if (ctx->b[i].state != ST_COMPRESSED) return fail(ctx, NEBULA_ERR_STATE, "exchange before compress");
+  DevGuard dg(ctx->device);
+  if (!ctx->loopback && ctx->P > 1) {
+    const Launch L = launch_of(ctx);
+    Mark mk(L, PH_NCCL_EXCHANGE);
+    CKN(ncclGroupStart());
+    for (int i = lo; i < hi; ++i) {
+      const BucketInfo& bk = ctx->b[i];
+      // in place: rank c's contribution already sits in slot c (ncclAllGather in-place rule)
+      const int lay = layout_of(ctx, bk.method);
+      uint8_t* base = ctx->d_slots + bk.so[lay];
+      CKN(ncclAllGather(base + (uint64_t)ctx->me * bk.pb[lay], base, bk.pb[lay], ncclUint8, ctx->inter, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+  }
+  for (int i = lo; i < hi; ++i) ctx->b[i].state = ST_EXCHANGED;
+  return NEBULA_OK;
+}
+
+nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  int lo, hi;
+  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  if (!dev_out && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_out");
+  for (int i = lo; i < hi; ++i)
+    if (ctx->b[i].state != ST_EXCHANGED) return fail(ctx, NEBULA_ERR_STATE, "decompress_reduce before exchange");
+  const int method = ctx->b[lo].method;
+  for (int i = lo; i < hi; ++i)
+    if (ctx->b[i].method != method) return fail(ctx, NEBULA_ERR_STATE, "buckets compressed with different methods");
+  DevGuard dg(ctx->device);
+  const int lay = layout_of(ctx, method);
+  const Table& T = ctx->rtab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+  float* obase = ctx->G > 1 ? ctx->d_shard_out : dev_out;
+  const bool vec = T.aligned && ((uintptr_t)obase % 16 == 0);
+  const Launch L = launch_of(ctx);
+  const RItem* items = ctx->d_ritems[lay] + T.first;
+  if (method == M_TOPK)
+    launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, ctx->d_slots,
+                       ctx->tk.start, obase);
+  else
+    launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, ctx->d_slots, obase);
+  CKC(cudaGetLastError());
+  if (ctx->G > 1) {
+    Mark mk(L, PH_NCCL_AG);
+    CKN(ncclGroupStart());
+    for (int i = lo; i < hi; ++i) {
+      const BucketInfo& bk = ctx->b[i];
+      if (!bk.cn) continue;
+      float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+      CKN(ncclAllGather(ctx->d_shard_out + bk.coff, dst, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+  }
+  for (int i = lo; i < hi; ++i) ctx->b[i].state = ST_IDLE;
+  return NEBULA_OK;
+}
+
+nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
+  nebula_status s = nebula_compress(ctx, bucket, dev_grad, step);
+  if (s != NEBULA_OK) return s;
+  s = nebula_exchange(ctx, bucket);
+  if (s != NEBULA_OK) return s;
+  return nebula_decompress_reduce(ctx, bucket, dev_out);
+}
+
+nebula_status nebula_step_host(nebula_ctx* ctx, const float* host_grad, float* host_out, uint64_t step) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  if ((!host_grad || !host_out) && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null host buffer");
+  DevGuard dg(ctx->device);
+  const uint64_t gelems = (uint64_t)(ctx->loopback ? ctx->P : 1) * ctx->total_n;
+  if (!ctx->d_hgrad) {
+    CKC(cudaMalloc(&ctx->d_hgrad, std::max<uint64_t>(16, gelems * 4)));
+    CKC(cudaMalloc(&ctx->d_hout, std::max<uint64_t>(16, ctx->total_n * 4)));
+  }
+  CKC(cudaMemcpyAsync(ctx->d_hgrad, host_grad, gelems * 4, cudaMemcpyHostToDevice, ctx->stream));
+  nebula_status s = nebula_step(ctx, NEBULA_ALL_BUCKETS, ctx->d_hgrad, ctx->d_hout, step);
+  if (s != NEBULA_OK) return s;
+  CKC(cudaMemcpyAsync(host_out, ctx->d_hout, ctx->total_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CKC(cudaStreamSynchronize(ctx->stream));
+  return NEBULA_OK;
+}
+
+nebula_status nebula_check(nebula_ctx* ctx) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  DevGuard dg(ctx->device);
+  CKC(cudaStreamSynchronize(ctx->stream));
+  uint32_t f = 0;
+  CKC(cudaMemcpy(&f, ctx->d_flags, 4, cudaMemcpyDeviceToHost));
+  CKC(cudaMemset(ctx->d_flags, 0, 4));
+  if (!ctx->loopback && ctx->world) {
+    ncclResult_t async_err = ncclSuccess;
+    ncclCommGetAsyncError(ctx->world, &async_err);
+    if (async_err != ncclSuccess) return fail(ctx, NEBULA_ERR_NCCL, ncclGetErrorString(async_err));
+  }
+  if (f & kFlagNonfinite) return fail(ctx, NEBULA_ERR_NONFINITE, "non-finite element in g + r");
+  if (f & kFlagOverflow) return fail(ctx, NEBULA_ERR_OVERFLOW, "fp16 overflow (|p| >= 65520)");
+  return NEBULA_OK;
+}
+
+nebula_status nebula_payload_bytes(const nebula_ctx* ctx, int32_t bucket, uint64_t* bytes) {
+  if (!ctx || !bytes || bucket < 0 || bucket >= (int)ctx->b.size()) return NEBULA_ERR_INVALID_ARG;
+  const BucketInfo& bk = ctx->b[bucket];
+  const int m = bk.method >= 0 ? bk.method : (ctx->codec.start_step == 0 ? ctx->codec.method : M_IDENTITY);
+  *bytes = payload_bytes_for(m, bk.cn, bk.k, ctx->codec.topk_values);
+  return NEBULA_OK;
+}
+
+nebula_status nebula_payload_copy(nebula_ctx* ctx, int32_t bucket, int32_t slot, void* host_dst, uint64_t cap) {
+  if (!ctx || !host_dst || bucket < 0 || bucket >= (int)ctx->b.size() || slot < 0 || slot >= ctx->P)
+    return fail(ctx, NEBULA_ERR_INVALID_ARG, "bad payload_copy arguments");
+  uint64_t nbytes = 0;
+  nebula_payload_bytes(ctx, bucket, &nbytes);
+  if (cap < nbytes) return fail(ctx, NEBULA_ERR_INVALID_ARG, "cap smaller than payload bytes");
+  DevGuard dg(ctx->device);
+  CKC(cudaStreamSynchronize(ctx->stream));
+  const BucketInfo& bk = ctx->b[bucket];
+  const int lay = layout_of(ctx, bk.method >= 0 ? bk.method : ctx->codec.method);
+  CKC(cudaMemcpy(host_dst, ctx->d_slots + bk.so[lay] + (uint64_t)slot * bk.pb[lay], nbytes, cudaMemcpyDeviceToHost));
+  return NEBULA_OK;
+}
+
+nebula_status nebula_residual_ptr(nebula_ctx* ctx, int32_t bucket, int32_t cluster, float** dev_residual) {
+  if (!ctx || !dev_residual || bucket < 0 || bucket >= (int)ctx->b.size())
+    return fail(ctx, NEBULA_ERR_INVALID_ARG, "bad residual_ptr arguments");
+  int c;
+  if (ctx->loopback) {
+    if (cluster < 0 || cluster >= ctx->P) return fail(ctx, NEBULA_ERR_INVALID_ARG, "cluster out of range");
+    c = cluster;
+  } else {
+    if (cluster != ctx->topo.cluster_id) return fail(ctx, NEBULA_ERR_INVALID_ARG, "not this context's cluster");
+    c = 0;
+  }
+  *dev_residual = ctx->d_resid + (uint64_t)c * ctx->total_cn + ctx->b[bucket].coff;
+  return NEBULA_OK;
+}
+
+uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  ctx->timing = on != 0;
+  return NEBULA_OK;
+}
+
+nebula_status nebula_timing_read(nebula_ctx* ctx, nebula_phase_time* out, int32_t cap, int32_t* n_out) {
+  if (!ctx || !n_out || (cap > 0 && !out)) return NEBULA_ERR_INVALID_ARG;
+  DevGuard dg(ctx->device);
+  CKC(cudaStreamSynchronize(ctx->stream));
+  double ms[PH_COUNT] = {0};
+  uint32_t cnt[PH_COUNT] = {0};
+  for (const auto& r : ctx->recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, ctx->evs[r.a], ctx->evs[r.b]) == cudaSuccess) {
+      ms[r.ph] += t;
+      cnt[r.ph] += 1;
+    }
+  }
+  ctx->recs.clear();
+  ctx->open.clear();
+  ctx->ev_next = 0;
+  int n = 0;
+  for (int p = 0; p < PH_COUNT; ++p) {
+    if (!cnt[p]) continue;
+    if (n < cap) out[n] = nebula_phase_time{(uint32_t)p, cnt[p], ms[p]};
+    ++n;
+  }
+  *n_out = n;
+  return NEBULA_OK;
+}
+
+const char* nebula_phase_name(uint32_t phase) {
+  static const char* names[PH_COUNT] = {
+      "identity_pack", "fp16_ef_pack", "int8_ef_absmax", "int8_ef_quant_pack", "topk_ef_sample",
+      "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
+      "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
+      "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_onchip"};
+  return phase < PH_COUNT ? names[phase] : "unknown";
+}
+
+nebula_status nebula_sync_destroy(nebula_ctx* ctx) {
+  release(ctx);
+  return NEBULA_OK;
+}
+
+const char* nebula_last_error(const nebula_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_error.c_str(); }
+
+}  // extern "C"
+
+// ============================================================================ top-k plumbing
+nebula_status topk_setup(nebula_ctx* ctx);
+nebula_status nebula_topk_stats(nebula_ctx* ctx, int32_t bucket, int32_t cluster, nebula_topk_info* out);
+#include "topk_host.inc"
