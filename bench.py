@@ -39,7 +39,7 @@ METRIC = "GB/s fp32 gradient synced per GPU (1/2/4/8 B200); % HBM roofline"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="nebula", choices=["nebula", "reference"])
     ap.add_argument("--method", default="int8", choices=list(METHODS))
@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--bucket-mib", type=float, default=25.0)
     ap.add_argument("--clusters", type=int, default=2, help="simulated clusters at N=1 (LOOPBACK)")
     ap.add_argument("--no-ef", action="store_true")
+    ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -81,6 +82,8 @@ def kernel_bytes(phase, method, vt, P, ef, n_elems, k_total):
         return (4 + e + e) * n_elems
     if phase == "topk_classify":
         return 4 * n_elems
+    if phase == "int8_onchip":
+        return (4 + e + e + 1) * n_elems
     return None
 
 
@@ -92,34 +95,48 @@ def reduce_bytes(method, vt, P, n_out, k_per_cluster):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled (every 20 ms) during the timed region.
+    The sampler is started (and its first row awaited) before the region; only rows stamped
+    inside [start, stop] are summarised (the nearest row if the region is shorter)."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
-        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown," \
             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
             "clocks_event_reasons.sw_power_cap,power.draw"
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                          "-lms", "20", "-i", str(self.device)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            deadline = time.time() + 5
+            while not self.rows and time.time() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def start(self):
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.12)
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -127,19 +144,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t) + 0.02]
+        if not rows and self.rows and self.t0 is not None:
+            rows = [min(self.rows, key=lambda tr: abs(tr[0] - self.t0))[1]]
+        sm, mx, reasons, pw = [], None, set(), []
+        for r in rows:
             try:
                 sm.append(float(r[0]))
                 mx = float(r[1])
-                for i, nm in enumerate(names):
-                    if r[3 + i].lower().startswith("active"):
+                for i, nm in enumerate(self.NAMES):
+                    if r[2 + i].lower().startswith("active"):
                         reasons.add(nm)
+                pw.append(float(r[6]))
             except Exception:
                 continue
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
@@ -267,6 +287,8 @@ def main():
         ctx = nb.SyncContext(sizes, method, num_clusters=P, transport=nb.LOOPBACK, device=local, **common)
     else:
         ctx = nb.init_process_group_context(sizes, device=local, **common)
+    if method == 2:
+        ctx.set_int8_kernel(args.int8_kernel)
     torch.cuda.synchronize()
 
     def barrier():
@@ -285,12 +307,15 @@ def main():
     l0 = ctx.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        barrier()
+        clk.start()
         e0.record(stream)
         for _ in range(args.steps):
             ctx.step(nb.ALL_BUCKETS, g, out, step)
             step += 1
         e1.record(stream)
         barrier()
+        clk.stop()
     launches = ctx.kernel_launches() - l0
     ms = e0.elapsed_time(e1)
     phases = ctx.timing_read()

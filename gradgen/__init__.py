@@ -173,6 +173,8 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
     16th element 0, the rest N(0,1)).
     """
     rng = np.random.default_rng(seed)
+    if n == 0:
+        return np.zeros(0, dtype=np.float32)
     if kind == "normal":
         return (rng.standard_normal(n, dtype=np.float32) * np.float32(sigma)).astype(np.float32)
     if kind == "model-like":

@@ -178,6 +178,14 @@ nebula_status nebula_topk_stats(nebula_ctx* ctx, int32_t bucket, int32_t cluster
 /* Number of library kernels enqueued since the context was created (bench accounting). */
 uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 
+/* Tuning knobs (results are bit-identical whichever kernel runs).
+ *   NEBULA_OPT_INT8_KERNEL: 0 auto (default), 1 two-pass streaming (max-abs pass + quantise
+ *   pass, 21 B/elem), 2 single-pass on-chip (cooperative grid, p kept in shared memory across
+ *   one grid barrier per bucket, 13 B/elem).  Auto picks on-chip when buckets average
+ *   >= 1M elements. */
+#define NEBULA_OPT_INT8_KERNEL 1
+nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
+
 /* Per-kernel device timers.  When enabled, every kernel / collective the context enqueues is
  * bracketed by a CUDA event pair recorded on the context's stream (the stream the kernel
  * runs on).  nebula_timing_read synchronises, returns per-phase sums since the last read

@@ -27,6 +27,7 @@ IDENTITY, FP16, INT8, TOPK = 0, 1, 2, 3
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK = 0, 1
 ALL_BUCKETS = -1
+OPT_INT8_KERNEL = 1
 UNIQUE_ID_BYTES = 128
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "OOM", 4: "CUDA", 5: "NCCL",
@@ -109,6 +110,7 @@ def load() -> ctypes.CDLL:
         "nebula_topk_stats": (I32, [P, I32, I32, ctypes.POINTER(_TopkInfo)]),
         "nebula_kernel_launches": (U64, [P]),
         "nebula_timing_enable": (I32, [P, I32]),
+        "nebula_set_option": (I32, [P, I32, ctypes.c_int64]),
         "nebula_timing_read": (I32, [P, ctypes.POINTER(_PhaseTime), I32, ctypes.POINTER(I32)]),
         "nebula_phase_name": (ctypes.c_char_p, [ctypes.c_uint32]),
         "nebula_sync_destroy": (I32, [P]),
@@ -259,6 +261,13 @@ class SyncContext:
 
     def kernel_launches(self) -> int:
         return self._L.nebula_kernel_launches(self._h)
+
+    def set_option(self, option: int, value: int):
+        self._ck(self._L.nebula_set_option(self._h, option, value))
+
+    def set_int8_kernel(self, which: str):
+        """'auto' | 'two-pass' | 'onchip' (NEBULA_OPT_INT8_KERNEL)."""
+        self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2}[which])
 
     def timing_enable(self, on: bool = True):
         self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))

@@ -40,6 +40,15 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
 
+// R18: sections are zero-padded to 16 bytes (slots are reused across methods/steps, so the
+// padding is rewritten every time; threads 16.. of the tail chunk, disjoint from the tail
+// element writers 0..3).
+__device__ __forceinline__ void zero_padding(uint8_t* body, uint64_t nbytes) {
+  const uint64_t end = pad16(nbytes);
+  const uint64_t z = nbytes + (threadIdx.x >= 16 ? threadIdx.x - 16 : end);
+  if (z < end) body[z] = 0;
+}
+
 // ----------------------------------------------------------------------------- IDENTITY
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ items, int nitems, uint64_t chunks,
@@ -66,11 +75,14 @@ __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ 
         st4(body + 4 * q, v);
       }
     }
-    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      float v = g[e];
-      bad |= nonfinite_bits(abs_bits(v));
-      body[e] = v;
+    if (j == n4 / kChunkQuads) {
+      if (threadIdx.x < (it.n & 3)) {
+        const uint64_t e = n4 * 4 + threadIdx.x;
+        float v = g[e];
+        bad |= nonfinite_bits(abs_bits(v));
+        body[e] = v;
+      }
+      zero_padding(slot + 16, 4 * it.n);
     }
   }
   raise_flags(flags, bad, false);
@@ -129,13 +141,16 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
                                      __fsub_rn(p.w, d.w)));
       }
     }
-    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-      uint16_t hb;
-      float d = fp16_one(p, hb, bad, ovf);
-      body[e] = hb;
-      if constexpr (EF) r[e] = __fsub_rn(p, d);
+    if (j == n4 / kChunkQuads) {
+      if (threadIdx.x < (it.n & 3)) {
+        const uint64_t e = n4 * 4 + threadIdx.x;
+        float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+        uint16_t hb;
+        float d = fp16_one(p, hb, bad, ovf);
+        body[e] = hb;
+        if constexpr (EF) r[e] = __fsub_rn(p, d);
+      }
+      zero_padding(slot + 16, 2 * it.n);
     }
   }
   raise_flags(flags, bad, ovf);
@@ -236,12 +251,15 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
                                      __fsub_rn(p.z, __fmul_rn((float)q2, s)), __fsub_rn(p.w, __fmul_rn((float)q3, s))));
       }
     }
-    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-      int qe = int8_q(p, s);
-      body[e] = (uint8_t)(qe & 0xFF);
-      if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+    if (j == n4 / kChunkQuads) {
+      if (threadIdx.x < (it.n & 3)) {
+        const uint64_t e = n4 * 4 + threadIdx.x;
+        float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+        int qe = int8_q(p, s);
+        body[e] = (uint8_t)(qe & 0xFF);
+        if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+      }
+      zero_padding(body, it.n);
     }
   }
 }
@@ -272,22 +290,34 @@ __device__ __forceinline__ float decode_one(const uint8_t* slot, uint64_t e, flo
   else return __fmul_rn((float)(int8_t)body[e], s);
 }
 
+// out = fl(tree_sum / P).  For P a power of two, x * (1/P) is the same correctly rounded
+// value as x / P (1/P is exact), so the multiply is used; otherwise IEEE division.
+template <int P>
+__device__ __forceinline__ float div_p(float x) {
+  if constexpr ((P & (P - 1)) == 0) return __fmul_rn(x, 1.0f / (float)P);
+  else return __fdiv_rn(x, (float)P);
+}
+
 template <int METHOD, int P, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restrict__ items, int nitems, uint64_t chunks,
                                                            const uint8_t* __restrict__ slots, float* __restrict__ obase) {
   constexpr int UG = P <= 2 ? 4 : (P <= 4 ? 2 : 1);   // quads in flight per thread (registers: UG*P float4)
-  int hint = 0;
+  int hint = 0, cur = -1;
+  RItem it{};
+  float sc[P];
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     const int i = find_item(items, nitems, c, hint);
     hint = i;
-    const RItem it = items[i];
+    if (i != cur) {   // per-bucket constants loaded once, not per chunk (block-uniform branch)
+      it = items[i];
+      cur = i;
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(slots + it.slot_off + k * it.pb + 8) : 1.0f;
+    }
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
     const uint8_t* s0 = slots + it.slot_off;
     float* out = obase + it.out_off;
-    float sc[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-      sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(s0 + k * it.pb + 8) : 1.0f;
 #pragma unroll
     for (int u0 = 0; u0 < kQuadsPerThread; u0 += UG) {
       float4 d[UG][P];
@@ -306,9 +336,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
           float vx[P], vy[P], vz[P], vw[P];
 #pragma unroll
           for (int k = 0; k < P; ++k) { vx[k] = d[u][k].x; vy[k] = d[u][k].y; vz[k] = d[u][k].z; vw[k] = d[u][k].w; }
-          const float fp = (float)P;
-          float4 o = make_float4(__fdiv_rn(tree_sum<0, P>(vx), fp), __fdiv_rn(tree_sum<0, P>(vy), fp),
-                                 __fdiv_rn(tree_sum<0, P>(vz), fp), __fdiv_rn(tree_sum<0, P>(vw), fp));
+          float4 o = make_float4(div_p<P>(tree_sum<0, P>(vx)), div_p<P>(tree_sum<0, P>(vy)),
+                                 div_p<P>(tree_sum<0, P>(vz)), div_p<P>(tree_sum<0, P>(vw)));
           stq<VEC>(out, q, o);
         }
       }
@@ -318,8 +347,139 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       float v[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(s0 + k * it.pb, e, sc[k]);
-      out[e] = __fdiv_rn(tree_sum<0, P>(v), (float)P);
+      out[e] = div_p<P>(tree_sum<0, P>(v));
     }
+  }
+}
+
+// ----------------------------------------------------------------------------- INT8 on-chip
+// Single pass over HBM for INT8 + EF (13 B/elem instead of 21): a cooperative persistent
+// grid walks the items one at a time.  Each CTA loads a contiguous slice of the item,
+// forms p = g + r into shared memory and reduces its max; one grid barrier publishes the
+// bucket's max; the CTA then quantises from shared memory, writing r and the payload.
+// Slices longer than the shared-memory capacity spill: the overflow is re-read from HBM in
+// the second phase (the two-pass schedule, for that part only).
+constexpr int kOnchipThreads = 1024;
+constexpr int kOnchipUnroll = 4;
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kOnchipThreads, 1)
+    k_int8_onchip(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
+                  float* __restrict__ rbase, uint8_t* __restrict__ slots, uint32_t* scratch, uint32_t* flags,
+                  unsigned* bar, uint32_t cap4) {
+  extern __shared__ float4 sp[];   // [cap4] p values of this CTA's slice
+  __shared__ uint32_t s_red[32];
+  const unsigned G = gridDim.x;
+  unsigned epoch = 0;
+  for (int i = 0; i < nitems; ++i) {
+    const Item it = items[i];
+    const uint64_t n4 = it.n >> 2;
+    const uint64_t per = (n4 + G - 1) / G;
+    const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    uint32_t m = 0;
+    // phase 1: p = g + r -> shared memory (first cap4 quads of the slice), running max
+    for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kOnchipThreads * kOnchipUnroll) {
+      float4 gv[kOnchipUnroll], rv[kOnchipUnroll];
+#pragma unroll
+      for (int u = 0; u < kOnchipUnroll; ++u) {
+        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
+        if (q < q1) {
+          gv[u] = ldq<VEC>(g, q);
+          if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kOnchipUnroll; ++u) {
+        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
+        if (q < q1) {
+          const float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
+          m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+          const uint64_t lq = q - q0;
+          if (lq < cap4) sp[lq] = p;
+        }
+      }
+    }
+    const bool tail_cta = blockIdx.x == G - 1;
+    float tp = 0.0f;
+    if (tail_cta && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      tp = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      m = max(m, abs_bits(tp));
+    }
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t w = s_red[threadIdx.x];
+      w = __reduce_max_sync(0xFFFFFFFFu, w);
+      if (threadIdx.x == 0 && w) atomicMax(&scratch[it.sidx], w);
+    }
+    epoch += 1;
+    grid_barrier(bar, epoch * G);
+    const uint32_t mbits = *((volatile uint32_t*)&scratch[it.sidx]);
+    if (nonfinite_bits(mbits)) {   // all-or-nothing: nothing of this bucket is written
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+      __syncthreads();
+      continue;
+    }
+    const float s = int8_scale_from_bits(mbits);
+    uint8_t* slot = slots + it.slot_off;
+    uint8_t* body = slot + 16;
+    if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
+    // phase 2: quantise from shared memory (spill part re-read), write payload + residual
+    for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kOnchipThreads * kOnchipUnroll) {
+      float4 pv[kOnchipUnroll];
+#pragma unroll
+      for (int u = 0; u < kOnchipUnroll; ++u) {
+        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
+        if (q < q1) {
+          const uint64_t lq = q - q0;
+          if (lq < cap4) {
+            pv[u] = sp[lq];
+          } else {
+            const float4 gg = ldq<VEC>(g, q);
+            pv[u] = EF ? add4(gg, ld4_stream(r + 4 * q)) : gg;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kOnchipUnroll; ++u) {
+        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
+        if (q < q1) {
+          const float4 p = pv[u];
+          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+          reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(a0, a1, a2, a3);
+          if constexpr (EF)
+            st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                       __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))));
+        }
+      }
+    }
+    if (tail_cta) {
+      if (threadIdx.x < (it.n & 3)) {
+        const uint64_t e = n4 * 4 + threadIdx.x;
+        const int qe = int8_q(tp, s);
+        body[e] = (uint8_t)(qe & 0xFF);
+        if constexpr (EF) r[e] = __fsub_rn(tp, __fmul_rn((float)qe, s));
+      }
+      zero_padding(body, it.n);
+    }
+    __syncthreads();   // shared memory is reused by the next item
   }
 }
 
@@ -407,11 +567,38 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
   ++*L.launches;
 }
 
-bool int8_onchip_capacity(int, uint64_t* max_elems, int* grid, size_t* smem) {
-  *max_elems = 0; *grid = 0; *smem = 0;
-  return false;
+bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem) {
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  size_t bytes = (size_t)optin - 1024;   // static smem of the kernel + headroom
+  bytes = bytes / 16 * 16;
+  const void* fns[4] = {(const void*)k_int8_onchip<true, true>, (const void*)k_int8_onchip<true, false>,
+                        (const void*)k_int8_onchip<false, true>, (const void*)k_int8_onchip<false, false>};
+  for (const void* f : fns)
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int8_onchip<true, true>, kOnchipThreads, bytes) !=
+          cudaSuccess || per_sm < 1)
+    return false;
+  *grid = sms * per_sm;
+  *smem = bytes;
+  *max_elems = (uint64_t)(*grid) * (bytes / 16) * 4;
+  return true;
 }
-void launch_int8_onchip(const Launch&, bool, bool, const Item*, int, const float*, float*, uint8_t*, uint32_t*,
-                        uint32_t*, uint32_t*, int, size_t) {}
+
+void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,
+                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* barrier, int grid, size_t smem) {
+  Mark mk(L, PH_INT8_ONCHIP);
+  cudaMemsetAsync(barrier, 0, sizeof(unsigned), L.stream);
+  uint32_t cap4 = (uint32_t)(smem / 16);
+  unsigned* bar = barrier;
+  void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                  (void*)&flags, (void*)&bar, (void*)&cap4};
+  const void* f = ef ? (vec ? (const void*)k_int8_onchip<true, true> : (const void*)k_int8_onchip<true, false>)
+                     : (vec ? (const void*)k_int8_onchip<false, true> : (const void*)k_int8_onchip<false, false>);
+  cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kOnchipThreads), args, smem, L.stream);
+  ++*L.launches;
+}
 
 }  // namespace nb

@@ -94,6 +94,14 @@ struct nebula_ctx {
   uint64_t launches = 0;
   std::string err;
 
+  // INT8 single-pass on-chip kernel (cooperative grid)
+  int int8_kernel = 0;          // NEBULA_OPT_INT8_KERNEL
+  bool onchip_ok = false;
+  int onchip_grid = 0;
+  size_t onchip_smem = 0;
+  uint64_t onchip_elems = 0;
+  uint32_t* d_bar = nullptr;
+
   // per-kernel event timers (nebula_timing_*)
   bool timing = false;
   std::vector<cudaEvent_t> evs;
@@ -230,6 +238,12 @@ static bool range_of(nebula_ctx* ctx, int32_t bucket, int* lo, int* hi) {
   return true;
 }
 
+static uint64_t elems_of(const nebula_ctx* ctx, int lo, int hi) {
+  uint64_t s = 0;
+  for (int i = lo; i < hi; ++i) s += ctx->b[i].n;
+  return s;
+}
+
 // ============================================================================ init
 static nebula_status build_tables(nebula_ctx* ctx, int lay) {
   const int B = (int)ctx->b.size();
@@ -307,6 +321,7 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_hgrad);
   cudaFree(ctx->d_hout);
   cudaFree(ctx->d_topk_mem);
+  cudaFree(ctx->d_bar);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
   if (ctx->intra) ncclCommDestroy(ctx->intra);
   if (ctx->inter && ctx->inter != ctx->world) ncclCommDestroy(ctx->inter);
@@ -421,6 +436,11 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       s = topk_setup(ctx);
       if (s != NEBULA_OK) return bail(s);
     }
+    if (codec->method == NEBULA_INT8) {
+      ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
+      if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, 16) != cudaSuccess) { ctx->err = "barrier allocation failed"; return bail(NEBULA_ERR_OOM); }
+      cudaGetLastError();
+    }
 
     // ---- communicators (collective over all P*G ranks)
     if (!ctx->loopback) {
@@ -454,7 +474,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
-  if (!dev_grad && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
+  if (!dev_grad && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
   DevGuard dg(ctx->device);
   const int method = method_at(ctx, step);
   const bool ef = ctx->codec.error_feedback != 0;
@@ -496,9 +516,19 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
           CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
       }
       }
-      launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-      launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch,
-                        ctx->d_flags);
+      bool onchip = false;
+      if (ctx->onchip_ok) {
+        if (ctx->int8_kernel == 2) onchip = true;
+        else if (ctx->int8_kernel == 0) onchip = elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20);
+      }
+      if (onchip) {
+        launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch, ctx->d_flags,
+                           ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem);
+      } else {
+        launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
+        launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch,
+                          ctx->d_flags);
+      }
       break;
     }
     case M_TOPK: {
@@ -544,7 +574,7 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
-  if (!dev_out && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_out");
+  if (!dev_out && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_out");
   for (int i = lo; i < hi; ++i)
     if (ctx->b[i].state != ST_EXCHANGED) return fail(ctx, NEBULA_ERR_STATE, "decompress_reduce before exchange");
   const int method = ctx->b[lo].method;
@@ -658,6 +688,18 @@ nebula_status nebula_residual_ptr(nebula_ctx* ctx, int32_t bucket, int32_t clust
 }
 
 uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  if (option == NEBULA_OPT_INT8_KERNEL) {
+    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be 0, 1 or 2");
+    if (value == 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
+      return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
+    ctx->int8_kernel = (int)value;
+    return NEBULA_OK;
+  }
+  return fail(ctx, NEBULA_ERR_INVALID_ARG, "unknown option");
+}
 
 nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;

@@ -30,10 +30,12 @@ def bits(a):
 
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
-                 start_step=0, per_bucket=False, misalign=False, mutate=None):
+                 start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
+    if int8_kernel:
+        ctx.set_int8_kernel(int8_kernel)
     codec = O.Codec(method=method, topk_values=vt, topk_k=k, topk_density=rho, error_feedback=ef,
                     start_step=start_step)
     total = sum(sizes)
@@ -102,6 +104,15 @@ def _first_diff(a, b):
 @pytest.mark.parametrize("sizes", [[1], [7], [4096], [4099, 12288, 77777]])
 def test_dense_parity(nb, method, P, sizes):
     assert run_loopback(nb, method, sizes, P) > 0
+
+
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip"])
+@pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
+@pytest.mark.parametrize("ef", [True, False])
+def test_int8_kernels(nb, int8_kernel, sizes, ef):
+    # both INT8 schedules are bit-identical to the oracle; [9_000_003] exceeds the on-chip
+    # capacity of one grid (~8.4M elements) and exercises the spill (re-read) path
+    run_loopback(nb, O.INT8, sizes, 2, steps=2, ef=ef, int8_kernel=int8_kernel)
 
 
 @pytest.mark.parametrize("method", [O.INT8, O.FP16])
@@ -187,9 +198,11 @@ def test_nonfinite_is_reported(nb, method, bad):
     ctx.destroy()
 
 
-def test_int8_nonfinite_writes_nothing(nb):
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip"])
+def test_int8_nonfinite_writes_nothing(nb, int8_kernel):
     import torch
     ctx = nb.SyncContext([1000], nb.INT8, num_clusters=1, transport=nb.LOOPBACK)
+    ctx.set_int8_kernel(int8_kernel)
     g = torch.randn(1000, device="cuda")
     out = torch.empty(1000, device="cuda")
     ctx.step(0, g, out, 0)
@@ -215,6 +228,8 @@ def test_fp16_overflow_is_reported(nb, method, vt):
     with pytest.raises(nb.NebulaError) as e:
         ctx.check()
     assert e.value.code == "OVERFLOW"
+    for c in range(2):         # after a device error the residual is unspecified: reset it
+        ctx.residual(0, c).zero_()
     g[1500] = 65519.0          # rounds to 65504: not an overflow (R10)
     ctx.step(0, g, out, 1)
     ctx.check()
