@@ -82,7 +82,7 @@ def kernel_bytes(phase, method, vt, P, ef, n_elems, k_total):
         return (4 + e + e) * n_elems
     if phase == "topk_classify":
         return 4 * n_elems
-    if phase == "int8_onchip":
+    if phase == "int8_fused_ef_quant_pack":
         return (4 + e + e + 1) * n_elems
     return None
 

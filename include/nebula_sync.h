@@ -35,7 +35,8 @@
  *   - Host-validated errors return immediately with nothing enqueued.  Device-detected
  *     errors (non-finite p, fp16 overflow) set a sticky device flag returned by
  *     nebula_check (which clears it).  After a device error the affected buckets' residuals
- *     and dev_out are unspecified (INT8 alone is all-or-nothing: it writes nothing).
+ *     and dev_out are unspecified (the caller skips the step and zeroes or restores the
+ *     residual via nebula_residual_ptr); INT8 writes no payload for such a bucket.
  *   - No C++ exception crosses the ABI.  nebula_last_error() describes the last failure.
  *   - Per bucket the order must be compress -> exchange -> decompress_reduce; anything
  *     else returns NEBULA_ERR_STATE.  nebula_step runs all three.
@@ -180,9 +181,9 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 
 /* Tuning knobs (results are bit-identical whichever kernel runs).
  *   NEBULA_OPT_INT8_KERNEL: 0 auto (default), 1 two-pass streaming (max-abs pass + quantise
- *   pass, 21 B/elem), 2 single-pass on-chip (cooperative grid, p kept in shared memory across
- *   one grid barrier per bucket, 13 B/elem).  Auto picks on-chip when buckets average
- *   >= 1M elements. */
+ *   pass, 21 B/elem of HBM traffic), 2 fused single pass (cooperative persistent grid, p parked
+ *   in r / L2 across a split arrive/wait barrier per bucket, 13 B/elem).  Auto picks the fused
+ *   kernel when buckets average >= 1M elements. */
 #define NEBULA_OPT_INT8_KERNEL 1
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 

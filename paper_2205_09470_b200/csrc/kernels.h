@@ -44,13 +44,14 @@ void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int ni
 // INT8 pass 2: scale from scratch, quantize + pack, r <- p - q*s.
 void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags);
-// INT8 single-pass, on-chip (cooperative, persistent): p held in shared memory between the
-// max-abs reduction and the quantisation.  Returns false when not applicable (item too big
-// for the resident grid), in which case the caller uses the two-pass kernels.
+// INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
+// p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
+// when a cooperative launch is not possible; the caller then uses the two-pass kernels.
+// done_words: >= nitems words (zeroed by the launcher).
 bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem);
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems,
                         const float* g, float* r, uint8_t* slots, uint32_t* scratch, uint32_t* flags,
-                        uint32_t* barrier, int grid, size_t smem);
+                        uint32_t* done_words, int grid, size_t smem);
 // Dense decompress + tree-average over P slots.
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
                          uint64_t chunks, const uint8_t* slots, float* out);

@@ -14,6 +14,8 @@
 // PAPER.md:125-130 Eq. 5 (FP16), PAPER.md:76 (aggregation).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace nb {
@@ -352,134 +354,138 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
   }
 }
 
-// ----------------------------------------------------------------------------- INT8 on-chip
-// Single pass over HBM for INT8 + EF (13 B/elem instead of 21): a cooperative persistent
-// grid walks the items one at a time.  Each CTA loads a contiguous slice of the item,
-// forms p = g + r into shared memory and reduces its max; one grid barrier publishes the
-// bucket's max; the CTA then quantises from shared memory, writing r and the payload.
-// Slices longer than the shared-memory capacity spill: the overflow is re-read from HBM in
-// the second phase (the two-pass schedule, for that part only).
-constexpr int kOnchipThreads = 1024;
-constexpr int kOnchipUnroll = 4;
+// ----------------------------------------------------------------------------- INT8 fused
+// Single HBM pass for INT8 + EF (13 B/elem instead of 21).  A cooperative persistent grid
+// walks the buckets in order with a SPLIT (arrive / wait) barrier per bucket:
+//
+//   A(i)   : p = g + r over this CTA's slice of bucket i, stored back into r (the dirty
+//            lines stay in the 126 MB L2), running max -> atomicMax, then ARRIVE on done[i]
+//   B(i-1) : WAIT until all CTAs arrived on done[i-1] (they did one bucket ago, so this
+//            rarely stalls), s = fl(max/127), re-read p from r (an L2 hit), quantise,
+//            write the payload and the residual r = p - q*s
+//
+// The same CTA owns the same slice in A and B, so the only cross-CTA data is the max.
+// HBM sees g and r read once and r + payload written once; if the L2 did not hold p the
+// cost degrades to the two-pass traffic, never to a wrong result.  Without error feedback
+// B re-reads g instead of p.
+constexpr int kFusedThreads = 512;
+constexpr int kFusedUnroll = 4;
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+__device__ __forceinline__ void arrive(unsigned* done) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    atomicAdd(bar, 1u);
+    atomicAdd(done, 1u);
+  }
+}
+__device__ __forceinline__ void wait_all(const unsigned* done, unsigned target) {
+  if (threadIdx.x == 0) {
     unsigned v;
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
     } while (v < target);
   }
   __syncthreads();
 }
 
 template <bool EF, bool VEC>
-__global__ void __launch_bounds__(kOnchipThreads, 1)
-    k_int8_onchip(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
-                  float* __restrict__ rbase, uint8_t* __restrict__ slots, uint32_t* scratch, uint32_t* flags,
-                  unsigned* bar, uint32_t cap4) {
-  extern __shared__ float4 sp[];   // [cap4] p values of this CTA's slice
-  __shared__ uint32_t s_red[32];
+__global__ void __launch_bounds__(kFusedThreads, 2)
+    k_int8_fused(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
+                 float* __restrict__ rbase, uint8_t* __restrict__ slots, uint32_t* scratch, uint32_t* flags,
+                 unsigned* done) {
+  __shared__ uint32_t s_red[kFusedThreads / 32];
   const unsigned G = gridDim.x;
-  unsigned epoch = 0;
-  for (int i = 0; i < nitems; ++i) {
-    const Item it = items[i];
-    const uint64_t n4 = it.n >> 2;
-    const uint64_t per = (n4 + G - 1) / G;
-    const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
-    const float* g = gbase + it.g_off;
-    float* r = rbase + it.r_off;
-    uint32_t m = 0;
-    // phase 1: p = g + r -> shared memory (first cap4 quads of the slice), running max
-    for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kOnchipThreads * kOnchipUnroll) {
-      float4 gv[kOnchipUnroll], rv[kOnchipUnroll];
+  for (int i = 0; i <= nitems; ++i) {
+    if (i < nitems) {   // ---------------- A(i)
+      const Item it = items[i];
+      const uint64_t n4 = it.n >> 2, per = (n4 + G - 1) / G;
+      const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
+      const float* g = gbase + it.g_off;
+      float* r = rbase + it.r_off;
+      uint32_t m = 0;
+      for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kFusedThreads * kFusedUnroll) {
+        float4 gv[kFusedUnroll], rv[kFusedUnroll];
 #pragma unroll
-      for (int u = 0; u < kOnchipUnroll; ++u) {
-        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
-        if (q < q1) {
-          gv[u] = ldq<VEC>(g, q);
-          if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+        for (int u = 0; u < kFusedUnroll; ++u) {
+          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
+          if (q < q1) {
+            gv[u] = ldq<VEC>(g, q);
+            if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+          }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < kOnchipUnroll; ++u) {
-        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
-        if (q < q1) {
-          const float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
-          m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
-          const uint64_t lq = q - q0;
-          if (lq < cap4) sp[lq] = p;
-        }
-      }
-    }
-    const bool tail_cta = blockIdx.x == G - 1;
-    float tp = 0.0f;
-    if (tail_cta && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      tp = EF ? __fadd_rn(g[e], r[e]) : g[e];
-      m = max(m, abs_bits(tp));
-    }
-    m = __reduce_max_sync(0xFFFFFFFFu, m);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint32_t w = s_red[threadIdx.x];
-      w = __reduce_max_sync(0xFFFFFFFFu, w);
-      if (threadIdx.x == 0 && w) atomicMax(&scratch[it.sidx], w);
-    }
-    epoch += 1;
-    grid_barrier(bar, epoch * G);
-    const uint32_t mbits = *((volatile uint32_t*)&scratch[it.sidx]);
-    if (nonfinite_bits(mbits)) {   // all-or-nothing: nothing of this bucket is written
-      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
-      __syncthreads();
-      continue;
-    }
-    const float s = int8_scale_from_bits(mbits);
-    uint8_t* slot = slots + it.slot_off;
-    uint8_t* body = slot + 16;
-    if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
-    // phase 2: quantise from shared memory (spill part re-read), write payload + residual
-    for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kOnchipThreads * kOnchipUnroll) {
-      float4 pv[kOnchipUnroll];
-#pragma unroll
-      for (int u = 0; u < kOnchipUnroll; ++u) {
-        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
-        if (q < q1) {
-          const uint64_t lq = q - q0;
-          if (lq < cap4) {
-            pv[u] = sp[lq];
-          } else {
-            const float4 gg = ldq<VEC>(g, q);
-            pv[u] = EF ? add4(gg, ld4_stream(r + 4 * q)) : gg;
+        for (int u = 0; u < kFusedUnroll; ++u) {
+          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
+          if (q < q1) {
+            const float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
+            m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+            if constexpr (EF) st4(r + 4 * q, p);
           }
         }
       }
+      if (blockIdx.x == G - 1 && threadIdx.x < (it.n & 3)) {
+        const uint64_t e = n4 * 4 + threadIdx.x;
+        const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+        if constexpr (EF) r[e] = p;
+        m = max(m, abs_bits(p));
+      }
+      m = __reduce_max_sync(0xFFFFFFFFu, m);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        uint32_t w = threadIdx.x < kFusedThreads / 32 ? s_red[threadIdx.x] : 0u;
+        w = __reduce_max_sync(0xFFFFFFFFu, w);
+        if (threadIdx.x == 0 && w) atomicMax(&scratch[it.sidx], w);
+      }
+      arrive(&done[i]);
+    }
+    if (i > 0) {        // ---------------- B(i-1)
+      const Item it = items[i - 1];
+      wait_all(&done[i - 1], G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[it.sidx]);
+      if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload, residual keeps p (unspecified)
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        continue;
+      }
+      const float s = int8_scale_from_bits(mbits);
+      const uint64_t n4 = it.n >> 2, per = (n4 + G - 1) / G;
+      const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
+      const float* g = gbase + it.g_off;
+      float* r = rbase + it.r_off;
+      uint8_t* slot = slots + it.slot_off;
+      uint8_t* body = slot + 16;
+      if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
+      for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kFusedThreads * kFusedUnroll) {
+        float4 pv[kFusedUnroll];
 #pragma unroll
-      for (int u = 0; u < kOnchipUnroll; ++u) {
-        const uint64_t q = qb + (uint64_t)u * kOnchipThreads;
-        if (q < q1) {
-          const float4 p = pv[u];
-          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
-          reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(a0, a1, a2, a3);
-          if constexpr (EF)
-            st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
-                                       __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))));
+        for (int u = 0; u < kFusedUnroll; ++u) {
+          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
+          if (q < q1) pv[u] = EF ? ld4_stream(r + 4 * q) : ldq<VEC>(g, q);
+        }
+#pragma unroll
+        for (int u = 0; u < kFusedUnroll; ++u) {
+          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
+          if (q < q1) {
+            const float4 p = pv[u];
+            const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+            reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(a0, a1, a2, a3);
+            if constexpr (EF)
+              st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                         __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))));
+          }
         }
       }
-    }
-    if (tail_cta) {
-      if (threadIdx.x < (it.n & 3)) {
-        const uint64_t e = n4 * 4 + threadIdx.x;
-        const int qe = int8_q(tp, s);
-        body[e] = (uint8_t)(qe & 0xFF);
-        if constexpr (EF) r[e] = __fsub_rn(tp, __fmul_rn((float)qe, s));
+      if (blockIdx.x == G - 1) {
+        if (threadIdx.x < (it.n & 3)) {
+          const uint64_t e = n4 * 4 + threadIdx.x;
+          const float p = EF ? r[e] : g[e];
+          const int qe = int8_q(p, s);
+          body[e] = (uint8_t)(qe & 0xFF);
+          if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        }
+        zero_padding(body, it.n);
       }
-      zero_padding(body, it.n);
     }
-    __syncthreads();   // shared memory is reused by the next item
   }
 }
 
@@ -567,37 +573,35 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
   ++*L.launches;
 }
 
-bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem) {
-  int sms = 0, optin = 0;
+bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {
+  int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  size_t bytes = (size_t)optin - 1024;   // static smem of the kernel + headroom
-  bytes = bytes / 16 * 16;
-  const void* fns[4] = {(const void*)k_int8_onchip<true, true>, (const void*)k_int8_onchip<true, false>,
-                        (const void*)k_int8_onchip<false, true>, (const void*)k_int8_onchip<false, false>};
-  for (const void* f : fns)
-    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) return false;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int8_onchip<true, true>, kOnchipThreads, bytes) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int8_fused<true, true>, kFusedThreads, 0) !=
           cudaSuccess || per_sm < 1)
     return false;
-  *grid = sms * per_sm;
-  *smem = bytes;
-  *max_elems = (uint64_t)(*grid) * (bytes / 16) * 4;
+  int p2 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<true, false>, kFusedThreads, 0);
+  per_sm = std::min(per_sm, std::max(1, p2));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<false, true>, kFusedThreads, 0);
+  per_sm = std::min(per_sm, std::max(1, p2));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<false, false>, kFusedThreads, 0);
+  per_sm = std::min(per_sm, std::max(1, p2));
+  *grid = sms * std::min(per_sm, 2);
+  *smem = 0;
+  *max_items = 0;
   return true;
 }
 
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,
-                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* barrier, int grid, size_t smem) {
+                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid, size_t) {
   Mark mk(L, PH_INT8_ONCHIP);
-  cudaMemsetAsync(barrier, 0, sizeof(unsigned), L.stream);
-  uint32_t cap4 = (uint32_t)(smem / 16);
-  unsigned* bar = barrier;
+  cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+  unsigned* done = done_words;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
-                  (void*)&flags, (void*)&bar, (void*)&cap4};
-  const void* f = ef ? (vec ? (const void*)k_int8_onchip<true, true> : (const void*)k_int8_onchip<true, false>)
-                     : (vec ? (const void*)k_int8_onchip<false, true> : (const void*)k_int8_onchip<false, false>);
-  cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kOnchipThreads), args, smem, L.stream);
+                  (void*)&flags, (void*)&done};
+  const void* f = ef ? (vec ? (const void*)k_int8_fused<true, true> : (const void*)k_int8_fused<true, false>)
+                     : (vec ? (const void*)k_int8_fused<false, true> : (const void*)k_int8_fused<false, false>);
+  cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kFusedThreads), args, 0, L.stream);
   ++*L.launches;
 }
 

@@ -438,7 +438,10 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     }
     if (codec->method == NEBULA_INT8) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
-      if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, 16) != cudaSuccess) { ctx->err = "barrier allocation failed"; return bail(NEBULA_ERR_OOM); }
+      if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
+        ctx->err = "barrier allocation failed";
+        return bail(NEBULA_ERR_OOM);
+      }
       cudaGetLastError();
     }
 
@@ -738,7 +741,7 @@ const char* nebula_phase_name(uint32_t phase) {
       "identity_pack", "fp16_ef_pack", "int8_ef_absmax", "int8_ef_quant_pack", "topk_ef_sample",
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
-      "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_onchip"};
+      "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 
