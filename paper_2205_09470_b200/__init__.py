@@ -291,27 +291,31 @@ class SyncContext:
             pass
 
 
-def init_process_group_context(bucket_numel, *, gpus_per_cluster=1, device=None, **codec):
-    """Build a NCCL-transport context for this torch.distributed rank.  Rank r is
-    cluster r // G, local rank r % G (SURVEY.md §8(e) topology B; G = 1 -> topology A).
-    Rank 0 creates the NCCL unique id; torch.distributed broadcasts it (plumbing only)."""
-    import torch
+def broadcast_unique_id(src: int = 0, group=None) -> bytes:
+    """Rank `src` creates the NCCL unique id (nebula_get_unique_id); torch.distributed
+    broadcasts the 128 bytes to every rank (plumbing only; works on gloo or nccl)."""
     import torch.distributed as dist
-    rank, world = dist.get_rank(), dist.get_world_size()
-    G = gpus_per_cluster
-    if world % G:
-        raise ValueError("world size must be a multiple of gpus_per_cluster")
-    uid = [get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    if device is None:
-        device = torch.cuda.current_device()
-    return SyncContext(bucket_numel, num_clusters=world // G, cluster_id=rank // G, gpus_per_cluster=G,
-                       local_rank=rank % G, transport=NCCL, device=device, unique_id=uid[0], **codec)
+    uid = [get_unique_id() if dist.get_rank() == src else None]
+    dist.broadcast_object_list(uid, src=src, group=group)
+    return uid[0]
 
 
 def topology_for_rank(rank: int, world: int, gpus_per_cluster: int = 1):
-    """(num_clusters, cluster_id, local_rank) of a rank — host logic shared by the bench."""
+    """(num_clusters, cluster_id, local_rank) of a rank: cluster r // G, local rank r % G
+    (G = 1 -> topology A, G > 1 -> topology B)."""
     G = gpus_per_cluster
     if G < 1 or world % G:
         raise ValueError("world size must be a positive multiple of gpus_per_cluster")
     return world // G, rank // G, rank % G
+
+
+def init_process_group_context(bucket_numel, *, gpus_per_cluster=1, device=None, **codec):
+    """Build a NCCL-transport context for this torch.distributed rank."""
+    import torch
+    import torch.distributed as dist
+    P, c, l = topology_for_rank(dist.get_rank(), dist.get_world_size(), gpus_per_cluster)
+    uid = broadcast_unique_id()
+    if device is None:
+        device = torch.cuda.current_device()
+    return SyncContext(bucket_numel, num_clusters=P, cluster_id=c, gpus_per_cluster=gpus_per_cluster,
+                       local_rank=l, transport=NCCL, device=device, unique_id=uid, **codec)

@@ -108,7 +108,9 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
                  uint32_t* flags, int value_type, uint64_t merge_tiles);
 // Sparse decompress + tree-average (tile merge over the ascending index lists).
 // entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).
+// zero_begin/zero_count: the output range of the call (filled with +0.0 first).
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
-                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out);
+                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out,
+                        float* zero_begin, uint64_t zero_count);
 
 }  // namespace nb

@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
                  unsigned* done) {
   __shared__ uint32_t s_red[kFusedThreads / 32];
   const unsigned G = gridDim.x;
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   for (int i = 0; i <= nitems; ++i) {
     if (i < nitems) {   // ---------------- A(i)
       const Item it = items[i];
@@ -409,8 +410,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         for (int u = 0; u < kFusedUnroll; ++u) {
           const uint64_t q = qb + (uint64_t)u * kFusedThreads;
           if (q < q1) {
-            gv[u] = ldq<VEC>(g, q);
-            if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+            if constexpr (VEC) gv[u] = ld4_hint(g + 4 * q, pol_stream);
+            else gv[u] = ldq<false>(g, q);
+            if constexpr (EF) rv[u] = ld4_hint(r + 4 * q, pol_stream);
           }
         }
 #pragma unroll
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           if (q < q1) {
             const float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
             m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
-            if constexpr (EF) st4(r + 4 * q, p);
+            if constexpr (EF) st4_hint(r + 4 * q, p, pol_keep);   // parked for phase B
           }
         }
       }
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
 #pragma unroll
         for (int u = 0; u < kFusedUnroll; ++u) {
           const uint64_t q = qb + (uint64_t)u * kFusedThreads;
-          if (q < q1) pv[u] = EF ? ld4_stream(r + 4 * q) : ldq<VEC>(g, q);
+          if (q < q1) pv[u] = EF ? ld4_hint(r + 4 * q, pol_stream) : ldq<VEC>(g, q);
         }
 #pragma unroll
         for (int u = 0; u < kFusedUnroll; ++u) {
@@ -468,10 +470,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           if (q < q1) {
             const float4 p = pv[u];
             const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
-            reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(a0, a1, a2, a3);
+            st_u32_hint(reinterpret_cast<uint32_t*>(body) + q, pack_i8x4(a0, a1, a2, a3), pol_stream);
             if constexpr (EF)
-              st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
-                                         __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))));
+              st4_hint(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                         __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                       pol_stream);
           }
         }
       }

@@ -32,7 +32,6 @@ namespace nb {
 constexpr int kSelThreads = 1024;  // single-CTA radix select
 constexpr int kMergeTile = 1024;   // outputs per merge CTA
 constexpr int kRedTile = 2048;     // elements per sparse-reduce CTA
-constexpr int kRedThreads = 256;
 
 // ---------------------------------------------------------------- status word (look-back)
 // bits 63..62 flag (0 none, 1 aggregate, 2 inclusive prefix), 61..31 winners, 30..0 candidates
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_a(const Item* __restrict__ ai
                                                      uint32_t* ctrs) {
   int hint = 0, cur = -1;
   uint32_t m = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 2) ctrs[threadIdx.x] = 0;  // classify tile counters
+  if (blockIdx.x == 0 && threadIdx.x < 3) ctrs[threadIdx.x] = 0;  // classify tile counters, any-failed flag
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     const int i = find_item(aitems, nitems, c, hint);
     hint = i;
@@ -249,7 +248,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restri
                                                             const float* __restrict__ gbase,
                                                             uint2* __restrict__ wl, uint2* __restrict__ cl,
                                                             unsigned long long* __restrict__ status, uint32_t* ctr,
-                                                            int retry) {
+                                                            int retry, const uint32_t* any_failed) {
+  if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long scan[kThreads / 32];
   __shared__ uint64_t s_tile;
   __shared__ unsigned long long s_prefix;
@@ -319,30 +319,42 @@ __global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restri
       accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
     }
     const uint32_t tileW = accW, tileC = accC;
-    // decoupled look-back over this item's tiles
-    if (threadIdx.x == 0) {
+    // decoupled look-back over this item's tiles, one warp wide: 32 predecessor status words
+    // per round trip; the lowest lane holding an inclusive prefix ends the walk
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
       unsigned long long* stw = status + ti.status_off;
+      constexpr unsigned long long VAL = (1ull << 62) - 1;
       unsigned long long prefix = 0;
       if (j == 0) {
-        st_release(stw, pack_status(2, tileW, tileC));
+        if (lane == 0) st_release(stw, pack_status(2, tileW, tileC));
       } else {
-        st_release(stw + j, pack_status(1, tileW, tileC));
-        int64_t k = (int64_t)j - 1;
+        if (lane == 0) st_release(stw + j, pack_status(1, tileW, tileC));
+        int64_t base = (int64_t)j - 1;
         for (;;) {
-          unsigned long long v = ld_acquire(stw + k);
+          const int64_t k = base - lane;
+          const unsigned long long v = k >= 0 ? ld_acquire(stw + k) : pack_status(2, 0, 0);
           const uint32_t f = (uint32_t)(v >> 62);
-          if (f == 0) continue;
-          prefix += v & ((1ull << 62) - 1);
-          if (f == 2) break;
-          --k;
+          if (__any_sync(0xFFFFFFFFu, f == 0)) continue;          // a predecessor has not published yet
+          const unsigned inc = __ballot_sync(0xFFFFFFFFu, f == 2);
+          const int stop = inc ? __ffs(inc) - 1 : 31;
+          unsigned long long part = lane <= stop ? (v & VAL) : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+          prefix += part;
+          if (inc) break;
+          base -= 32;
         }
-        st_release(stw + j, pack_status(2, ((prefix >> 31) & 0x7FFFFFFFull) + tileW, (prefix & 0x7FFFFFFFull) + tileC));
+        if (lane == 0)
+          st_release(stw + j, pack_status(2, ((prefix >> 31) & 0x7FFFFFFFull) + tileW, (prefix & 0x7FFFFFFFull) + tileC));
       }
-      s_prefix = prefix;
-      if (j + 1 == ti.nchunks) {  // last tile of the item publishes the totals
-        TopkState& Sw = st[i];
-        Sw.wcount = ((prefix >> 31) & 0x7FFFFFFFull) + tileW;
-        Sw.ccount = (prefix & 0x7FFFFFFFull) + tileC;
+      if (lane == 0) {
+        s_prefix = prefix;
+        if (j + 1 == ti.nchunks) {  // last tile of the item publishes the totals
+          TopkState& Sw = st[i];
+          Sw.wcount = ((prefix >> 31) & 0x7FFFFFFFull) + tileW;
+          Sw.ccount = (prefix & 0x7FFFFFFFull) + tileC;
+        }
       }
     }
     __syncthreads();
@@ -385,7 +397,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restri
 // ---------------------------------------------------------------- D: resolve among candidates
 __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st, uint2* __restrict__ cl,
-                                                              int retry) {
+                                                              int retry, uint32_t* any_failed) {
+  if (retry && *((volatile uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
   __shared__ unsigned long long scan[32];
@@ -399,7 +412,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
     bool ok = (W < k || k == 0) && (W + C >= k);
     if (ok && C > ti.ccap) ok = (S.t_lo == S.t_hi) && (k - W) <= ti.ccap;  // exact tie set: prefix suffices
     s_ok = ok;
-    if (!ok) { S.mode = 1; S.failed = 1; }   // -> exact radix fallback
+    if (!ok) { S.mode = 1; S.failed = 1; atomicOr(any_failed, 1u); }   // -> exact radix fallback
   }
   __syncthreads();
   if (!s_ok || k == 0) {
@@ -457,7 +470,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist(const Item* __restrict__
                                                         const TopkState* __restrict__ st, int nitems, uint64_t chunks,
                                                         const float* __restrict__ pbase, bool p_in_r,
                                                         const float* __restrict__ gbase, uint32_t* __restrict__ ghist,
-                                                        int d) {
+                                                        int d, const uint32_t* any_failed) {
+  if (*((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   const Digit dg = digit_of(d);
   const int nb = 1 << dg.bits, hs = dg.shift + dg.bits;
@@ -501,7 +515,9 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist(const Item* __restrict__
 
 __global__ void __launch_bounds__(kSelThreads) k_topk_hist_select(const TopkItem* __restrict__ titems,
                                                                   TopkState* __restrict__ st, uint32_t* ghist,
-                                                                  unsigned long long* __restrict__ status, int d) {
+                                                                  unsigned long long* __restrict__ status, int d,
+                                                                  const uint32_t* any_failed) {
+  if (*((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
   __shared__ unsigned long long scan[32];
@@ -665,60 +681,61 @@ __global__ void k_topk_offsets(const RItem* __restrict__ items, int nitems, uint
   for (int64_t t = prev + 1; t <= cur; ++t) s[t] = (uint32_t)e;
 }
 
-template <int P, bool VEC>
-__global__ void __launch_bounds__(kRedThreads) k_topk_reduce(const RItem* __restrict__ items, int nitems,
-                                                             const uint8_t* __restrict__ slots,
-                                                             const uint32_t* __restrict__ start,
-                                                             float* __restrict__ obase, int vt) {
-  extern __shared__ __align__(16) float acc_raw[];   // [P][kRedTile], dynamic (P = 8 needs 64 KB)
-  float (*acc)[kRedTile] = reinterpret_cast<float (*)[kRedTile]>(acc_raw);
-  const uint64_t t = blockIdx.x;
-  const int i = find_by(items, nitems, t, [](const RItem& r) { return r.t0; });
+// Sparse average, owner-computes: the output range was zero-filled (+0.0: every index no
+// cluster selected averages to +0.0/P = +0.0, R16).  One thread per (cluster c, entry e):
+// x = idx_c[e]; the other clusters' lists are searched only inside tile(x)'s range (from the
+// start offsets); the lowest cluster holding x is its owner and writes
+// out[x] = fl(tree_sum(D_0(x) .. D_{P-1}(x)) / P) with +0.0 for clusters that did not select x.
+template <int P>
+__device__ __forceinline__ float div_p_sparse(float x) {
+  if constexpr ((P & (P - 1)) == 0) return __fmul_rn(x, 1.0f / (float)P);
+  else return __fdiv_rn(x, (float)P);
+}
+
+__device__ __forceinline__ float topk_decode(const uint8_t* val, uint64_t e, int vt, float s) {
+  if (vt == V_F32) return reinterpret_cast<const float*>(val)[e];
+  if (vt == V_F16) return __half2float(reinterpret_cast<const __half*>(val)[e]);
+  return __fmul_rn((float)(int8_t)val[e], s);
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ items, int nitems, uint64_t total,
+                                                      const uint8_t* __restrict__ slots,
+                                                      const uint32_t* __restrict__ start, float* __restrict__ obase,
+                                                      int vt) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (g >= total) return;
+  const int i = find_by(items, nitems, g, [](const RItem& r) { return r.e0; });
   const RItem it = items[i];
-  const uint64_t lt = t - it.t0;
+  const uint64_t e = g - it.e0;
+  if (e >= it.k) return;
   const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
-  const uint64_t e_base = lt * kRedTile;
+  const uint64_t voff = 16 + pad16(4 * it.k);
+  const uint8_t* sc = slots + it.slot_off + (uint64_t)c * it.pb;
+  const uint32_t x = reinterpret_cast<const uint32_t*>(sc + 16)[e];
+  const uint32_t t = x / kRedTile;
+  float v[P];
 #pragma unroll
-  for (int c = 0; c < P; ++c)
-    for (int x = threadIdx.x; x < kRedTile; x += kRedThreads) acc[c][x] = 0.0f;   // +0.0 where not selected (R16)
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < P; ++c) {
-    const uint8_t* slot = slots + it.slot_off + (uint64_t)c * it.pb;
-    const uint32_t* idx = reinterpret_cast<const uint32_t*>(slot + 16);
-    const uint8_t* val = slot + 16 + pad16(4 * it.k);
-    const float s = *reinterpret_cast<const float*>(slot + 8);
-    const uint32_t* st = start + it.sbase + (uint64_t)c * (ntiles + 1);
-    const uint32_t a = st[lt], b = st[lt + 1];
-    for (uint32_t e = a + threadIdx.x; e < b; e += kRedThreads) {
-      const uint32_t x = idx[e] - (uint32_t)e_base;
-      float d;
-      if (vt == V_F32) d = reinterpret_cast<const float*>(val)[e];
-      else if (vt == V_F16) d = __half2float(reinterpret_cast<const __half*>(val)[e]);
-      else d = __fmul_rn((float)(int8_t)val[e], s);
-      acc[c][x] = d;
+  for (int c2 = 0; c2 < P; ++c2) {
+    const uint8_t* s2 = slots + it.slot_off + (uint64_t)c2 * it.pb;
+    const float scale = *reinterpret_cast<const float*>(s2 + 8);
+    if (c2 == c) {
+      v[c2] = topk_decode(s2 + voff, e, vt, scale);
+      continue;
     }
+    const uint32_t* st2 = start + it.sbase + (uint64_t)c2 * (ntiles + 1);
+    uint32_t lo = st2[t], hi = st2[t + 1];
+    const uint32_t* idx2 = reinterpret_cast<const uint32_t*>(s2 + 16);
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (idx2[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    const bool found = lo < st2[t + 1] && idx2[lo] == x;
+    if (found && c2 < c) return;           // a lower cluster owns x
+    v[c2] = found ? topk_decode(s2 + voff, lo, vt, scale) : 0.0f;
   }
-  __syncthreads();
-  float* out = obase + it.out_off + e_base;
-  const uint64_t rem = it.n - e_base;
-  const uint32_t lim = (uint32_t)(rem < kRedTile ? rem : kRedTile);
-  const float fp = (float)P;
-  for (uint32_t x0 = threadIdx.x * 4; x0 < lim; x0 += kRedThreads * 4) {
-    float res[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float v[P];
-#pragma unroll
-      for (int c = 0; c < P; ++c) v[c] = acc[c][x0 + q];
-      res[q] = __fdiv_rn(tree_sum<0, P>(v), fp);
-    }
-    if (VEC && x0 + 4 <= lim) {
-      st4(out + x0, make_float4(res[0], res[1], res[2], res[3]));
-    } else {
-      for (int q = 0; q < 4 && x0 + q < lim; ++q) out[x0 + q] = res[q];
-    }
-  }
+  obase[it.out_off + x] = div_p_sparse<P>(tree_sum<0, P>(v));
 }
 
 // ---------------------------------------------------------------- launchers
@@ -752,21 +769,21 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
   // C + D: classify with the bracket, resolve among candidates
   const unsigned gc = grid_for(L, a_chunks);
   { Mark mk(L, PH_TOPK_CLASSIFY);
-  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0);
-  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0); }
+  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0, B.ctrs + 2);
+  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0, B.ctrs + 2); }
   { Mark mk(L, PH_TOPK_RESOLVE);
-  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0); }
+  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, B.ctrs + 2); }
   // fallback for items whose bracket failed (no work otherwise): exact radix over p
   {
   Mark mkf(L, PH_TOPK_FALLBACK);
   for (int d = 0; d < 3; ++d) {
-    if (vec) k_topk_hist<true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d);
-    else k_topk_hist<false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d);
-    k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, B.status, d);
+    if (vec) k_topk_hist<true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d, B.ctrs + 2);
+    else k_topk_hist<false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d, B.ctrs + 2);
+    k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, B.status, d, B.ctrs + 2);
   }
-  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1);
-  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1);
-  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1);
+  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1, B.ctrs + 2);
+  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1, B.ctrs + 2);
+  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, B.ctrs + 2);
   }
   Mark mkm(L, PH_TOPK_MERGE);
   // F: merge -> payload, residual at the selected positions
@@ -777,38 +794,37 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
 }
 
 template <int P>
-static void reduce_topk_p(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
-                          const uint8_t* slots, const uint32_t* start, float* out) {
-  const size_t smem = (size_t)P * kRedTile * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_topk_reduce<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_topk_reduce<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  if (vec) k_topk_reduce<P, true><<<(unsigned)tiles, kRedThreads, smem, L.stream>>>(items, nitems, slots, start, out, vt);
-  else k_topk_reduce<P, false><<<(unsigned)tiles, kRedThreads, smem, L.stream>>>(items, nitems, slots, start, out, vt);
+static void scatter_p(const Launch& L, int vt, const RItem* items, int nitems, uint64_t entries, const uint8_t* slots,
+                      const uint32_t* start, float* out) {
+  dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
+  k_topk_scatter<P><<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start, out, vt);
 }
 
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
-                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out) {
-  if (entries) {
+                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out,
+                        float* zero_begin, uint64_t zero_count) {
+  (void)vec; (void)tiles;
+  {
+    Mark mk(L, PH_MEMSET);
+    if (zero_count) cudaMemsetAsync(zero_begin, 0, zero_count * sizeof(float), L.stream);
+  }
+  if (!entries) return;
+  {
     Mark mk(L, PH_TOPK_OFFSETS);
     dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
     k_topk_offsets<<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start);
     ++*L.launches;
   }
-  if (!tiles) return;
   Mark mk(L, PH_TOPK_REDUCE);
   switch (P) {
-    case 1: reduce_topk_p<1>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 2: reduce_topk_p<2>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 3: reduce_topk_p<3>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 4: reduce_topk_p<4>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 5: reduce_topk_p<5>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 6: reduce_topk_p<6>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    case 7: reduce_topk_p<7>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
-    default: reduce_topk_p<8>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    case 1: scatter_p<1>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 2: scatter_p<2>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 3: scatter_p<3>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 4: scatter_p<4>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 5: scatter_p<5>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 6: scatter_p<6>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 7: scatter_p<7>(L, value_type, items, nitems, entries, slots, start, out); break;
+    default: scatter_p<8>(L, value_type, items, nitems, entries, slots, start, out); break;
   }
   ++*L.launches;
 }

@@ -591,8 +591,20 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
   const Launch L = launch_of(ctx);
   const RItem* items = ctx->d_ritems[lay] + T.first;
   if (method == M_TOPK)
+  {
+    // output range of this call: buckets [lo, hi) are contiguous in the out buffer
+    float* zb;
+    uint64_t zc;
+    if (ctx->G > 1) {
+      zb = obase + ctx->b[lo].coff;
+      zc = (hi == (int)ctx->b.size() ? ctx->total_cn : ctx->b[hi].coff) - ctx->b[lo].coff;
+    } else {
+      zb = obase;
+      zc = elems_of(ctx, lo, hi);
+    }
     launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, ctx->d_slots,
-                       ctx->tk.start, obase);
+                       ctx->tk.start, obase, zb, zc);
+  }
   else
     launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, ctx->d_slots, obase);
   CKC(cudaGetLastError());
