@@ -93,12 +93,13 @@ struct TopkBuffers {
   uint32_t* sample;
   uint2* wlist;         // (idx, p bits)
   uint2* clist;
-  unsigned long long* status;
+  unsigned long long* status;  // per-tile (winners << 32 | candidates) counts, then prefixes
   uint32_t* hist;       // [nitems][2048] fallback histograms
   uint32_t* ctrs;       // 2 dynamic tile counters
   uint32_t* start;      // sparse-reduce start offsets
   uint64_t* host_mt0;   // host copy of items[].mt0 and merge tiles per item (for grid sizing)
   uint64_t* host_mtiles;
+  uint64_t* host_sample_off;  // [nitems + 1] prefix of sample counts
 };
 // Runs the whole selection for items [item0, item0 + nitems) (their TopkItem rows), writes
 // payloads, updates residuals.  aitems = the call's Item table (same order), g = gradient

@@ -4,17 +4,18 @@
 // it): the k largest keys key_i = bits(p_i) & 0x7FFFFFFF (|p| order, -0 == +0); equal keys
 // resolved by the lower index; payload indices ascending.  The pipeline never sorts:
 //
-//   A  k_topk_a        (streaming, 12 B/elem) p = g + r -> r; max-abs bits; every S-th key
-//                       into a sample                                   [EF fused]
+//   S  k_topk_sample   (gather, ~0.5 B/elem) key(fl(g + r)) at every S-th position
 //   B  k_topk_bracket  (1 CTA/item) radix-select two ranks of the sample -> bracket
 //                       [t_lo, t_hi] that holds the true k-th key with overwhelming odds
-//   C  k_topk_classify (streaming, 4 B/elem) winners key > t_hi, candidates t_lo<=key<=t_hi;
-//                       ORDERED compaction of both (decoupled look-back over tiles, two
-//                       counters packed in one 64-bit status word)
+//   A  k_topk_pass     (streaming, 12 B/elem) p = g + r -> r; max-abs bits; per-tile counts of
+//                       winners (key > t_hi) and candidates (t_lo <= key <= t_hi)   [EF fused]
+//   X  k_topk_scan     (1 CTA/item) exclusive scan of the tile counts -> tile offsets, totals
+//   C  k_topk_write    (streaming, 4 B/elem) re-read p, emit winners and candidates
+//                       (idx, p bits) in ascending index order at the tile offsets
 //   D  k_topk_resolve  (1 CTA/item) verify W < k <= W + C; radix-select the exact threshold T
 //                       among the candidates; keep key > T and the first need_T keys == T
 //   (fallback, only items whose bracket failed: 3 full radix-histogram passes give the exact
-//    T, then C and D rerun with t_lo = t_hi = T — bounded memory, always exact)
+//    T, then count/scan/write/resolve rerun with t_lo = t_hi = T — bounded memory, exact)
 //   F  k_topk_merge    merge-path of the two ascending lists -> payload idx[k], val[k];
 //                       residual at the selected positions r = p - D(v)
 //
@@ -33,19 +34,8 @@ constexpr int kSelThreads = 1024;  // single-CTA radix select
 constexpr int kMergeTile = 1024;   // outputs per merge CTA
 constexpr int kRedTile = 2048;     // elements per sparse-reduce CTA
 
-// ---------------------------------------------------------------- status word (look-back)
-// bits 63..62 flag (0 none, 1 aggregate, 2 inclusive prefix), 61..31 winners, 30..0 candidates
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint64_t w, uint64_t c) {
-  return ((unsigned long long)flag << 62) | ((unsigned long long)w << 31) | (unsigned long long)c;
-}
+// tile words: (winners << 32) | candidates — per-tile counts, then exclusive prefixes
+__device__ __forceinline__ unsigned long long pack_wc(uint64_t w, uint64_t c) { return (w << 32) | c; }
 
 // ---------------------------------------------------------------- block helpers
 // Inclusive scan of a 64-bit value over a CTA of NT threads; returns inclusive, *total.
@@ -141,81 +131,15 @@ __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* 
   return prefix;
 }
 
-// ---------------------------------------------------------------- A: EF + sample + max
-template <bool EF, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_topk_a(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems,
-                                                     TopkState* __restrict__ st, int nitems, uint64_t chunks,
-                                                     const float* __restrict__ gbase, float* __restrict__ rbase,
-                                                     uint32_t* __restrict__ sample, unsigned long long* __restrict__ status,
-                                                     uint32_t* ctrs) {
-  int hint = 0, cur = -1;
-  uint32_t m = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 3) ctrs[threadIdx.x] = 0;  // classify tile counters, any-failed flag
-  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
-    const int i = find_item(aitems, nitems, c, hint);
-    hint = i;
-    if (i != cur) {
-      if (cur >= 0) {
-        uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
-        if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
-      }
-      cur = i;
-      m = 0;
-    }
-    const Item it = aitems[i];
-    const TopkItem& ti = titems[i];
-    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
-    const uint32_t S = ti.stride;
-    const float* g = gbase + it.g_off;
-    float* r = rbase + it.r_off;
-    uint32_t* smp = sample + ti.sample_off;
-    if (threadIdx.x == 0) status[ti.status_off + j] = 0ull;
-#pragma unroll
-    for (int u = 0; u < kQuadsPerThread; ++u) {
-      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
-      if (q < n4) {
-        float4 gv;
-        if constexpr (VEC) gv = ld4_stream(g + 4 * q);
-        else gv = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
-        float4 p = gv;
-        if constexpr (EF) {
-          float4 rv = ld4_stream(r + 4 * q);
-          p = make_float4(__fadd_rn(gv.x, rv.x), __fadd_rn(gv.y, rv.y), __fadd_rn(gv.z, rv.z), __fadd_rn(gv.w, rv.w));
-          st4(r + 4 * q, p);
-        }
-        m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
-        if (((4 * q) & (S - 1)) == 0) smp[(4 * q) / S] = abs_bits(p.x);
-      }
-    }
-    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-      if constexpr (EF) r[e] = p;
-      m = max(m, abs_bits(p));
-      if ((e & (S - 1)) == 0) smp[e / S] = abs_bits(p);
-    }
-  }
-  if (cur >= 0) {
-    uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
-    if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
-  }
-}
-
 // ---------------------------------------------------------------- B: bracket from the sample
 __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st,
-                                                              const uint32_t* __restrict__ sample, uint32_t* flags,
-                                                              int value_type) {
+                                                              const uint32_t* __restrict__ sample) {
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
   __shared__ unsigned long long scan[32];
   const TopkItem ti = titems[blockIdx.x];
   TopkState& S = st[blockIdx.x];
-  const uint32_t mb = S.maxbits;
-  if (nonfinite_bits(mb)) {
-    if (threadIdx.x == 0) { S.failed = 2; atomicOr(flags, kFlagNonfinite); }
-    return;
-  }
   const uint32_t ns = (uint32_t)ti.nsample;
   const double ks = (double)ti.k * (double)ns / (double)(ti.n ? ti.n : 1);
   const double delta = 5.0 * sqrt(ks + 1.0) + 16.0;
@@ -235,31 +159,170 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __
     S.t_hi = t_hi;
     S.mode = 0;
     S.path = 0;
-    S.scale = value_type == V_I8 ? int8_scale_from_bits(mb) : 1.0f;
   }
 }
 
-// ---------------------------------------------------------------- C: classify + ordered compaction
+// ---------------------------------------------------------------- S: sample p = g + r
+// One thread per sample: key(fl(g_e + r_e)) at e = m * S.  The same binary32 addition as
+// pass A, so the sample sees exactly the p the selection will see.
+template <bool EF>
+__global__ void k_topk_sample(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems, int nitems,
+                              uint64_t sbase, uint64_t total, const float* __restrict__ gbase,
+                              const float* __restrict__ rbase, uint32_t* __restrict__ sample, uint32_t* ctrs) {
+  if (blockIdx.x == 0 && threadIdx.x < 4) ctrs[threadIdx.x] = 0;   // [2] = any bracket failed
+  const uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= total) return;
+  const uint64_t a = sbase + gi;
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (titems[mid].sample_off <= a) lo = mid; else hi = mid - 1;
+  }
+  const TopkItem& ti = titems[lo];
+  const uint64_t e = (a - ti.sample_off) * ti.stride;
+  const float gv = gbase[aitems[lo].g_off + e];
+  const float p = EF ? __fadd_rn(gv, rbase[ti.r_off + e]) : gv;
+  sample[a] = abs_bits(p);
+}
+
+// ---------------------------------------------------------------- A: EF pass + tile counts
+// COUNT_ONLY = false: p = g + r -> r, max-abs, counts.  COUNT_ONLY = true (fallback retry):
+// counts over p for the items whose exact threshold was just found.
+template <bool COUNT_ONLY, bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__ aitems,
+                                                        const TopkItem* __restrict__ titems,
+                                                        TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                        const float* __restrict__ gbase, float* __restrict__ rbase,
+                                                        unsigned long long* __restrict__ tiles,
+                                                        const uint32_t* any_failed) {
+  if (COUNT_ONLY && *((volatile const uint32_t*)any_failed) == 0) return;
+  __shared__ unsigned long long s_cnt[kThreads / 32];
+  int hint = 0, cur = -1;
+  uint32_t m = 0, t_lo = 0, t_hi = 0;
+  bool skip = false;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(aitems, nitems, c, hint);
+    hint = i;
+    if (i != cur) {
+      if (!COUNT_ONLY && cur >= 0) {
+        const uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+        if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
+      }
+      cur = i;
+      m = 0;
+      t_lo = st[i].t_lo;
+      t_hi = st[i].t_hi;
+      skip = COUNT_ONLY && st[i].mode != 1;
+    }
+    if (skip) continue;
+    const Item it = aitems[i];
+    const TopkItem& ti = titems[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    const float* src = (COUNT_ONLY && EF) ? r : g;
+    uint32_t wn = 0, cn = 0;
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        float4 p;
+        if (VEC || (COUNT_ONLY && EF)) p = ld4_stream(src + 4 * q);
+        else p = make_float4(src[4 * q], src[4 * q + 1], src[4 * q + 2], src[4 * q + 3]);
+        if constexpr (!COUNT_ONLY && EF) {
+          const float4 rv = ld4_stream(r + 4 * q);
+          p = make_float4(__fadd_rn(p.x, rv.x), __fadd_rn(p.y, rv.y), __fadd_rn(p.z, rv.z), __fadd_rn(p.w, rv.w));
+          st4(r + 4 * q, p);
+        }
+        const uint32_t k0 = abs_bits(p.x), k1 = abs_bits(p.y), k2 = abs_bits(p.z), k3 = abs_bits(p.w);
+        if (!COUNT_ONLY) m = max(m, max(max(k0, k1), max(k2, k3)));
+        wn += (k0 > t_hi) + (k1 > t_hi) + (k2 > t_hi) + (k3 > t_hi);
+        cn += (k0 >= t_lo && k0 <= t_hi) + (k1 >= t_lo && k1 <= t_hi) + (k2 >= t_lo && k2 <= t_hi) +
+              (k3 >= t_lo && k3 <= t_hi);
+      }
+    }
+    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      float p;
+      if (COUNT_ONLY) p = src[e];
+      else p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      if (!COUNT_ONLY && EF) r[e] = p;
+      const uint32_t k0 = abs_bits(p);
+      if (!COUNT_ONLY) m = max(m, k0);
+      wn += k0 > t_hi;
+      cn += (k0 >= t_lo && k0 <= t_hi);
+    }
+    unsigned long long v = pack_wc(wn, cn);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) t += s_cnt[w];
+      tiles[ti.status_off + j] = t;
+    }
+    __syncthreads();
+  }
+  if (!COUNT_ONLY && cur >= 0) {
+    const uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && w) atomicMax(&st[cur].maxbits, w);
+  }
+}
+
+// ---------------------------------------------------------------- X: scan tile counts
+// 1 CTA per item: exclusive prefix of the (W, C) tile words in place; totals; after pass A
+// also the non-finite check and the int8 value scale (both need the bucket's max).
+__global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __restrict__ titems,
+                                                           TopkState* __restrict__ st,
+                                                           unsigned long long* __restrict__ tiles, int retry,
+                                                           uint32_t* flags, int value_type,
+                                                           const uint32_t* any_failed) {
+  if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
+  __shared__ unsigned long long scan[32];
+  const TopkItem ti = titems[blockIdx.x];
+  TopkState& S = st[blockIdx.x];
+  if (retry) {
+    if (S.mode != 1 || S.failed == 2) return;
+  } else {
+    const uint32_t mb = S.maxbits;
+    if (nonfinite_bits(mb)) {
+      if (threadIdx.x == 0) { S.failed = 2; atomicOr(flags, kFlagNonfinite); }
+      return;
+    }
+    if (threadIdx.x == 0) S.scale = value_type == V_I8 ? int8_scale_from_bits(mb) : 1.0f;
+  }
+  unsigned long long* tw = tiles + ti.status_off;
+  unsigned long long carry = 0;
+  for (uint64_t j0 = 0; j0 < ti.nchunks; j0 += kSelThreads) {
+    const uint64_t j = j0 + threadIdx.x;
+    const unsigned long long v = j < ti.nchunks ? tw[j] : 0ull;
+    unsigned long long tot;
+    const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
+    if (j < ti.nchunks) tw[j] = carry + incl - v;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    S.wcount = carry >> 32;
+    S.ccount = carry & 0xFFFFFFFFull;
+  }
+}
+
+// ---------------------------------------------------------------- C: ordered write
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restrict__ aitems,
-                                                            const TopkItem* __restrict__ titems,
-                                                            TopkState* __restrict__ st, int nitems, uint64_t chunks,
-                                                            const float* __restrict__ pbase, bool p_in_r,
-                                                            const float* __restrict__ gbase,
-                                                            uint2* __restrict__ wl, uint2* __restrict__ cl,
-                                                            unsigned long long* __restrict__ status, uint32_t* ctr,
-                                                            int retry, const uint32_t* any_failed) {
+__global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict__ aitems,
+                                                         const TopkItem* __restrict__ titems,
+                                                         const TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                         const float* __restrict__ pbase, bool p_in_r,
+                                                         const float* __restrict__ gbase,
+                                                         uint2* __restrict__ wl, uint2* __restrict__ cl,
+                                                         const unsigned long long* __restrict__ tiles, int retry,
+                                                         const uint32_t* any_failed) {
   if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long scan[kThreads / 32];
-  __shared__ uint64_t s_tile;
-  __shared__ unsigned long long s_prefix;
   int hint = 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint64_t c = s_tile;
-    __syncthreads();
-    if (c >= chunks) break;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     const int i = find_item(aitems, nitems, c, hint);
     hint = i;
     const TopkState& S = st[i];
@@ -318,47 +381,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_classify(const Item* __restri
       accW += (uint32_t)((totw >> (12 * u)) & 0xFFF);
       accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
     }
-    const uint32_t tileW = accW, tileC = accC;
-    // decoupled look-back over this item's tiles, one warp wide: 32 predecessor status words
-    // per round trip; the lowest lane holding an inclusive prefix ends the walk
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      unsigned long long* stw = status + ti.status_off;
-      constexpr unsigned long long VAL = (1ull << 62) - 1;
-      unsigned long long prefix = 0;
-      if (j == 0) {
-        if (lane == 0) st_release(stw, pack_status(2, tileW, tileC));
-      } else {
-        if (lane == 0) st_release(stw + j, pack_status(1, tileW, tileC));
-        int64_t base = (int64_t)j - 1;
-        for (;;) {
-          const int64_t k = base - lane;
-          const unsigned long long v = k >= 0 ? ld_acquire(stw + k) : pack_status(2, 0, 0);
-          const uint32_t f = (uint32_t)(v >> 62);
-          if (__any_sync(0xFFFFFFFFu, f == 0)) continue;          // a predecessor has not published yet
-          const unsigned inc = __ballot_sync(0xFFFFFFFFu, f == 2);
-          const int stop = inc ? __ffs(inc) - 1 : 31;
-          unsigned long long part = lane <= stop ? (v & VAL) : 0ull;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
-          prefix += part;
-          if (inc) break;
-          base -= 32;
-        }
-        if (lane == 0)
-          st_release(stw + j, pack_status(2, ((prefix >> 31) & 0x7FFFFFFFull) + tileW, (prefix & 0x7FFFFFFFull) + tileC));
-      }
-      if (lane == 0) {
-        s_prefix = prefix;
-        if (j + 1 == ti.nchunks) {  // last tile of the item publishes the totals
-          TopkState& Sw = st[i];
-          Sw.wcount = ((prefix >> 31) & 0x7FFFFFFFull) + tileW;
-          Sw.ccount = (prefix & 0x7FFFFFFFull) + tileC;
-        }
-      }
-    }
-    __syncthreads();
-    const uint64_t preW = (s_prefix >> 31) & 0x7FFFFFFFull, preC = s_prefix & 0x7FFFFFFFull;
+    const unsigned long long off = tiles[ti.status_off + j];
+    const uint64_t preW = off >> 32, preC = off & 0xFFFFFFFFull;
     uint2* W = wl + ti.list_off;
     uint2* C = cl + ti.list_off;
 #pragma unroll
@@ -514,8 +538,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist(const Item* __restrict__
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_topk_hist_select(const TopkItem* __restrict__ titems,
-                                                                  TopkState* __restrict__ st, uint32_t* ghist,
-                                                                  unsigned long long* __restrict__ status, int d,
+                                                                  TopkState* __restrict__ st, uint32_t* ghist, int d,
                                                                   const uint32_t* any_failed) {
   if (*((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
@@ -544,9 +567,8 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_hist_select(const TopkItem
     }
   }
   if (d == 2) {
-    for (uint64_t jj = threadIdx.x; jj < ti.nchunks; jj += blockDim.x) status[ti.status_off + jj] = 0ull;
     __syncthreads();
-    if (threadIdx.x == 0) S.failed = 0;   // mode stays 1 (retry)
+    if (threadIdx.x == 0) S.failed = 0;   // mode stays 1: count / scan / write / resolve rerun
   }
 }
 
@@ -745,52 +767,69 @@ static inline unsigned grid_for(const Launch& L, uint64_t chunks, int per_sm = 8
   return (unsigned)(g ? g : 1);
 }
 
-void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
-                 const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags, int value_type,
-                 uint64_t merge_tiles) {
-  if (nitems <= 0) return;
+template <bool EF, bool VEC>
+static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
+                            const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags,
+                            int value_type, uint64_t merge_tiles) {
   const TopkItem* ti = B.items + item0;
   TopkState* st = B.state + item0;
+  uint32_t* anyf = B.ctrs + 2;
+  const unsigned ga = grid_for(L, a_chunks);
+  const uint64_t sbase = B.host_sample_off[item0];
+  const uint64_t scount = B.host_sample_off[item0 + nitems] - sbase;
   {
     Mark mk(L, PH_MEMSET);
     cudaMemsetAsync(st, 0, sizeof(TopkState) * nitems, L.stream);
   }
-  const unsigned ga = grid_for(L, a_chunks);
-  // A: EF add (p -> r), max-abs, sample
-  { Mark mk(L, PH_TOPK_A);
-  if (ef && vec) k_topk_a<true, true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
-  else if (ef) k_topk_a<true, false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
-  else if (vec) k_topk_a<false, true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
-  else k_topk_a<false, false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.sample, B.status, B.ctrs);
-  }
-  // B: bracket from the sample
-  { Mark mk(L, PH_TOPK_BRACKET);
-  k_topk_bracket<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.sample, flags, value_type); }
-  // C + D: classify with the bracket, resolve among candidates
-  const unsigned gc = grid_for(L, a_chunks);
-  { Mark mk(L, PH_TOPK_CLASSIFY);
-  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0, B.ctrs + 2);
-  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs, 0, B.ctrs + 2); }
-  { Mark mk(L, PH_TOPK_RESOLVE);
-  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, B.ctrs + 2); }
-  // fallback for items whose bracket failed (no work otherwise): exact radix over p
   {
-  Mark mkf(L, PH_TOPK_FALLBACK);
-  for (int d = 0; d < 3; ++d) {
-    if (vec) k_topk_hist<true><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d, B.ctrs + 2);
-    else k_topk_hist<false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.hist + (size_t)item0 * 2048, d, B.ctrs + 2);
-    k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, B.status, d, B.ctrs + 2);
+    Mark mk(L, PH_TOPK_BRACKET);
+    k_topk_sample<EF><<<(unsigned)((scount + 255) / 256 ? (scount + 255) / 256 : 1), 256, 0, L.stream>>>(
+        aitems, ti, nitems, sbase, scount, g, r, B.sample, B.ctrs);
+    k_topk_bracket<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.sample);
   }
-  if (vec) k_topk_classify<true><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1, B.ctrs + 2);
-  else k_topk_classify<false><<<gc, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, ef, g, B.wlist, B.clist, B.status, B.ctrs + 1, 1, B.ctrs + 2);
-  k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, B.ctrs + 2);
+  {
+    Mark mk(L, PH_TOPK_A);
+    k_topk_pass<false, EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
   }
-  Mark mkm(L, PH_TOPK_MERGE);
-  // F: merge -> payload, residual at the selected positions
+  {
+    Mark mk(L, PH_TOPK_CLASSIFY);
+    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 0, flags, value_type, anyf);
+    k_topk_write<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
+                                                     B.status, 0, anyf);
+  }
+  {
+    Mark mk(L, PH_TOPK_RESOLVE);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
+  }
+  {
+    // fallback for items whose bracket failed (every kernel exits at once otherwise)
+    Mark mk(L, PH_TOPK_FALLBACK);
+    for (int d = 0; d < 3; ++d) {
+      k_topk_hist<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g,
+                                                      B.hist + (size_t)item0 * 2048, d, anyf);
+      k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, d, anyf);
+    }
+    k_topk_pass<true, EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
+    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 1, flags, value_type, anyf);
+    k_topk_write<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
+                                                     B.status, 1, anyf);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf);
+  }
+  Mark mk(L, PH_TOPK_MERGE);
   const uint64_t tbase = B.host_mt0[item0];
-  if (ef) k_topk_merge<true><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots, r, flags);
-  else k_topk_merge<false><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots, r, flags);
-  *L.launches += 13;
+  k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots,
+                                                                      r, flags);
+  *L.launches += 17;
+}
+
+void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
+                 const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags, int value_type,
+                 uint64_t merge_tiles) {
+  if (nitems <= 0) return;
+  if (ef && vec) topk_select_all<true, true>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);
+  else if (ef) topk_select_all<true, false>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);
+  else if (vec) topk_select_all<false, true>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);
+  else topk_select_all<false, false>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);
 }
 
 template <int P>

@@ -89,6 +89,7 @@ struct nebula_ctx {
   void* d_topk_mem = nullptr;
   std::vector<uint64_t> tk_mtiles;   // merge tiles per call type ([0] ALL, [1+b])
   std::vector<uint64_t> tk_host_mt0; // per item
+  std::vector<uint64_t> tk_sample_off; // [items + 1]
 
   ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
   uint64_t launches = 0;
