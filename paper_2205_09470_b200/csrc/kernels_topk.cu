@@ -101,6 +101,7 @@ __device__ __forceinline__ Digit digit_of(int d) {
 template <class GetKey>
 __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* above_out, uint32_t* hist,
                                uint32_t* s_misc, unsigned long long* scan_smem) {
+  constexpr int U = 8;   // keys in flight per thread (the loop is latency-bound otherwise)
   uint32_t prefix = 0, above = 0, left = rank;
   for (int d = 0; d < 3; ++d) {
     const Digit dg = digit_of(d);
@@ -108,16 +109,19 @@ __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* 
     for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     const int hs = dg.shift + dg.bits;  // bits above this digit must equal the prefix
-    for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
-      const uint32_t i = i0 + threadIdx.x;
-      bool act = false;
-      uint32_t bin = 0;
-      if (i < m) {
-        const uint32_t key = get(i);
-        act = (hs >= 31) ? true : ((key >> hs) == prefix);
-        bin = (key >> dg.shift) & (nb - 1);
+    for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x * U) {
+      uint32_t key[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+        key[u] = i < m ? get(i) : 0u;
       }
-      hist_add(hist, act, bin);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+        const bool act = i < m && ((hs >= 31) || ((key[u] >> hs) == prefix));
+        hist_add(hist, act, (key[u] >> dg.shift) & (nb - 1));
+      }
     }
     __syncthreads();
     find_bin(hist, nb, left, &s_misc[0], &s_misc[1], scan_smem);
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
                                                          const unsigned long long* __restrict__ tiles, int retry,
                                                          const uint32_t* any_failed) {
   if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
-  __shared__ unsigned long long scan[kThreads / 32];
+  __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
   int hint = 0;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     const int i = find_item(aitems, nitems, c, hint);
@@ -365,13 +369,30 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
       tw = key > t_hi;
       tcn = (key >= t_lo) & (key <= t_hi);
     }
-    // two CTA scans of packed 12-bit fields: fields 0..3 = this thread's quads u, field 4 =
-    // its tail element; element order inside the tile is (field, thread, element)
+    // packed 12-bit fields: 0..3 = this thread's quads u, 4 = its tail element; element order
+    // inside the tile is (field, thread, element).  Warp-level inclusive scans, one barrier to
+    // share the 8 warp totals, every thread folds the totals of the warps before it.
     pw |= (unsigned long long)tw << 48;
     pc |= (unsigned long long)tcn << 48;
-    unsigned long long totw, totc;
-    const unsigned long long ew = block_incl_scan<kThreads>(pw, scan, &totw) - pw;
-    const unsigned long long ec = block_incl_scan<kThreads>(pc, scan, &totc) - pc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long iw = pw, ic = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long a1 = __shfl_up_sync(0xFFFFFFFFu, iw, o);
+      const unsigned long long a2 = __shfl_up_sync(0xFFFFFFFFu, ic, o);
+      if (lane >= o) { iw += a1; ic += a2; }
+    }
+    if (lane == 31) { s_wt[warp] = iw; s_ct[warp] = ic; }
+    __syncthreads();
+    unsigned long long ew = iw - pw, ec = ic - pc, totw = 0, totc = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long a1 = s_wt[w], a2 = s_ct[w];
+      if (w < warp) { ew += a1; ec += a2; }
+      totw += a1;
+      totc += a2;
+    }
+    __syncthreads();   // s_wt / s_ct are rewritten by the next chunk
     uint32_t baseW[kQuadsPerThread + 1], baseC[kQuadsPerThread + 1];
     uint32_t accW = 0, accC = 0;
 #pragma unroll
