@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Distributed parity check (run under torchrun, one process per GPU, NCCL transport).
+
+Every rank is one GPU of cluster rank // G.  Each step every rank regenerates ALL ranks'
+seeded gradients on the host (gradgen), runs the C-ABI step on its own, and checks:
+  * its output is bit-identical to the oracle (flat P x 1: oracle_step; G > 1:
+    hierarchical_step on dyadic inputs whose fp32 cluster mean is exact in any order),
+  * its own payload slot and residual are bit-identical to the oracle's,
+  * all ranks' outputs are bit-identical (all-gathered and compared on every rank).
+Prints "DIST OK ..." on rank 0 and exits 0, else raises.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def dyadic(n, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.integers(-4096, 4096, n).astype(np.float32) * np.float32(2.0 ** -14)).astype(np.float32)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus-per-cluster", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import paper_2205_09470_b200 as nb
+    from gradgen import seed_for, synthetic
+
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    G = args.gpus_per_cluster
+    P, cl, lr = nb.topology_for_rank(rank, world, G)
+    sizes = [4096 * G, 12288 * G, 300004 * G, 8 * G]
+    total = sum(sizes)
+    cases = [(O.INT8, 0, "two-pass"), (O.INT8, 0, "onchip"), (O.FP16, 0, None), (O.IDENTITY, 0, None),
+             (O.TOPK, O.VAL_F32, None), (O.TOPK, O.VAL_I8, None), (O.TOPK, O.VAL_F16, None)]
+    for method, vt, kern in cases:
+        for per_bucket in (False, True):
+            ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
+                                                topk_values=vt, topk_density=0.05)
+            if kern:
+                ctx.set_int8_kernel(kern)
+            codec = O.Codec(method=method, topk_values=vt, topk_density=0.05)
+            m = [s // G for s in sizes]
+            rs = [[[np.zeros(mb, np.float32) for mb in m] for _ in range(G)] for _ in range(P)]
+            for t in range(args.steps):
+                # gradient of (cluster c, gpu l, bucket b)
+                def grad(c, l, b):
+                    if G > 1:
+                        return dyadic(sizes[b], seed_for(c, l, t, salt=b))
+                    return synthetic(sizes[b], seed_for(c, l, t, salt=b), "model-like")
+                mine = np.concatenate([grad(cl, lr, b) for b in range(len(sizes))])
+                g = torch.from_numpy(mine).cuda()
+                out = torch.full((total,), float("nan"), device="cuda")
+                if per_bucket:
+                    off = 0
+                    for b, n in enumerate(sizes):
+                        ctx.step(b, g[off:off + n], out[off:off + n], t)
+                        off += n
+                else:
+                    ctx.step(nb.ALL_BUCKETS, g, out, t)
+                ctx.check()
+                got = out.cpu().numpy()
+                # cross-rank identity
+                allo = [torch.empty_like(out) for _ in range(world)]
+                dist.all_gather(allo, out)
+                for o in allo:
+                    assert torch.equal(o.view(torch.int32), out.view(torch.int32)), "ranks disagree"
+                off = 0
+                for b, n in enumerate(sizes):
+                    if G == 1:
+                        exp, r_new, payloads, _ = O.oracle_step([grad(c, 0, b) for c in range(P)],
+                                                                [rs[c][0][b] for c in range(P)], codec, t)
+                        myr, mypl = r_new[cl], payloads[cl]
+                        for c in range(P):
+                            rs[c][0][b] = r_new[c] if r_new[c] is not None else rs[c][0][b]
+                    else:
+                        exp, r_new, pls = O.hierarchical_step([[grad(c, l, b) for l in range(G)] for c in range(P)],
+                                                              [[rs[c][l][b] for l in range(G)] for c in range(P)],
+                                                              codec, t)
+                        myr, mypl = r_new[cl][lr], pls[cl][lr]
+                        for c in range(P):
+                            for l in range(G):
+                                rs[c][l][b] = r_new[c][l] if r_new[c][l] is not None else rs[c][l][b]
+                    assert np.array_equal(got[off:off + n].view(np.uint32), exp.view(np.uint32)), \
+                        f"rank {rank} out mismatch method {method} vt {vt} bucket {b} step {t}"
+                    assert ctx.payload_copy(b, cl) == mypl, f"rank {rank} payload mismatch b{b} t{t}"
+                    if myr is not None:
+                        rg = ctx.residual(b, cl).cpu().numpy()
+                        assert np.array_equal(rg.view(np.uint32), myr.view(np.uint32)), \
+                            f"rank {rank} residual mismatch b{b} t{t}"
+                    # every slot (all clusters' payloads) after the exchange == oracle payloads
+                    if G == 1:
+                        for c in range(P):
+                            assert ctx.payload_copy(b, c) == payloads[c], f"slot {c} mismatch b{b}"
+                    off += n
+            ctx.destroy()
+    dist.barrier()
+    if rank == 0:
+        print(f"DIST OK world={world} P={P} G={G} cases={len(cases)}x2 steps={args.steps}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
