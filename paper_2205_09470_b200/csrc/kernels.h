@@ -23,6 +23,16 @@ struct Launch {
   void* mctx;
 };
 
+// Persistent-grid size for a grid-stride kernel: exactly the resident CTAs (SMs x the
+// kernel's occupancy), never more than the work — a grid larger than one wave leaves a
+// partial second wave (the tail effect ncu showed on the reducer).
+int occupancy_per_sm(const void* kernel, int threads, size_t smem);
+inline unsigned persistent_grid(const Launch& L, uint64_t chunks, const void* kernel, int threads, size_t smem = 0) {
+  uint64_t g = (uint64_t)L.num_sms * (uint64_t)occupancy_per_sm(kernel, threads, smem);
+  if (chunks < g) g = chunks;
+  return (unsigned)(g ? g : 1);
+}
+
 // RAII timer around one launch site: records an event pair on the launch stream.
 struct Mark {
   const Launch& L;

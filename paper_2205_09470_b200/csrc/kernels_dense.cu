@@ -15,6 +15,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "kernels.h"
 
@@ -356,20 +358,22 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
 
 // ----------------------------------------------------------------------------- INT8 fused
 // Single HBM pass for INT8 + EF (13 B/elem instead of 21).  A cooperative persistent grid
-// walks the buckets in order with a SPLIT (arrive / wait) barrier per bucket:
+// walks the buckets; iteration t of every CTA interleaves, in ONE loop over its slice,
 //
-//   A(i)   : p = g + r over this CTA's slice of bucket i, stored back into r (the dirty
-//            lines stay in the 126 MB L2), running max -> atomicMax, then ARRIVE on done[i]
-//   B(i-1) : WAIT until all CTAs arrived on done[i-1] (they did one bucket ago, so this
-//            rarely stalls), s = fl(max/127), re-read p from r (an L2 hit), quantise,
-//            write the payload and the residual r = p - q*s
+//   A(t)   : p = g + r for bucket t, parked back into r (L2 evict_last), running max, then
+//            ARRIVE on done[t] (atomicMax of the bucket max before it)
+//   B(t-2) : s = fl(max/127) of bucket t-2, re-read p from r (an L2 hit), quantise, write
+//            the payload and the residual r = p - q*s (L2 evict_first)
 //
-// The same CTA owns the same slice in A and B, so the only cross-CTA data is the max.
-// HBM sees g and r read once and r + payload written once; if the L2 did not hold p the
-// cost degrades to the two-pass traffic, never to a wrong result.  Without error feedback
-// B re-reads g instead of p.
+// B(t-2) WAITS until all CTAs arrived on done[t-2], which they did one whole iteration ago,
+// so in steady state nobody stalls (a split arrive/wait barrier with a lag of two), and the
+// loads of both phases are in flight together.  The same CTA owns the same slice of a bucket
+// in A and B, so the only cross-CTA datum is the max.  L2 holds p of two buckets (~52 MB at
+// 25 MiB buckets) next to the streamed traffic; if it did not, the cost degrades to the
+// two-pass traffic, never to a wrong result.  Without EF, B re-reads g.
 constexpr int kFusedThreads = 512;
-constexpr int kFusedUnroll = 4;
+constexpr int kFusedUnroll = 2;
+constexpr int kFusedLag = 2;
 
 __device__ __forceinline__ void arrive(unsigned* done) {
   __syncthreads();
@@ -388,6 +392,15 @@ __device__ __forceinline__ void wait_all(const unsigned* done, unsigned target) 
   __syncthreads();
 }
 
+struct Slice {
+  uint64_t q0, q1;
+};
+__device__ __forceinline__ Slice slice_of(uint64_t n4, unsigned G) {
+  const uint64_t per = (n4 + G - 1) / G;
+  const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per);
+  return Slice{q0, min(n4, q0 + per)};
+}
+
 template <bool EF, bool VEC>
 __global__ void __launch_bounds__(kFusedThreads, 2)
     k_int8_fused(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
@@ -396,116 +409,137 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
   __shared__ uint32_t s_red[kFusedThreads / 32];
   const unsigned G = gridDim.x;
   const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
-  for (int i = 0; i <= nitems; ++i) {
-    if (i < nitems) {   // ---------------- A(i)
-      const Item it = items[i];
-      const uint64_t n4 = it.n >> 2, per = (n4 + G - 1) / G;
-      const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
-      const float* g = gbase + it.g_off;
-      float* r = rbase + it.r_off;
-      uint32_t m = 0;
-      for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kFusedThreads * kFusedUnroll) {
-        float4 gv[kFusedUnroll], rv[kFusedUnroll];
+  for (int t = 0; t < nitems + kFusedLag; ++t) {
+    const int ia = t, ib = t - kFusedLag;
+    const bool doA = ia < nitems;
+    bool doB = ib >= 0;
+    // ---- B setup (wait for everyone's A(ib), finished an iteration ago)
+    Item itB{};
+    Slice sb{0, 0};
+    float s = 1.0f;
+    if (doB) {
+      itB = items[ib];
+      wait_all(&done[ib], G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
+      if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload for this bucket
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        doB = false;
+      } else {
+        s = int8_scale_from_bits(mbits);
+        sb = slice_of(itB.n >> 2, G);
+        if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slots + itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
+      }
+    }
+    // ---- A setup
+    Item itA{};
+    Slice sa{0, 0};
+    if (doA) {
+      itA = items[ia];
+      sa = slice_of(itA.n >> 2, G);
+    }
+    const float* gA = gbase + itA.g_off;
+    float* rA = rbase + itA.r_off;
+    const float* gB = gbase + itB.g_off;
+    float* rB = rbase + itB.r_off;
+    uint32_t* bodyB = reinterpret_cast<uint32_t*>(slots + itB.slot_off + 16);
+    const uint64_t lenA = sa.q1 - sa.q0, lenB = doB ? sb.q1 - sb.q0 : 0;
+    const uint64_t len = max(lenA, lenB);
+    uint32_t m = 0;
+    for (uint64_t kb = threadIdx.x; kb < len; kb += (uint64_t)kFusedThreads * kFusedUnroll) {
+      float4 ga[kFusedUnroll], ra[kFusedUnroll], pb[kFusedUnroll];
 #pragma unroll
-        for (int u = 0; u < kFusedUnroll; ++u) {
-          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
-          if (q < q1) {
-            if constexpr (VEC) gv[u] = ld4_hint(g + 4 * q, pol_stream);
-            else gv[u] = ldq<false>(g, q);
-            if constexpr (EF) rv[u] = ld4_hint(r + 4 * q, pol_stream);
-          }
+      for (int u = 0; u < kFusedUnroll; ++u) {
+        const uint64_t k = kb + (uint64_t)u * kFusedThreads;
+        if (k < lenA) {
+          const uint64_t q = sa.q0 + k;
+          if constexpr (VEC) ga[u] = ld4_hint(gA + 4 * q, pol_stream);
+          else ga[u] = ldq<false>(gA, q);
+          if constexpr (EF) ra[u] = ld4_hint(rA + 4 * q, pol_stream);
         }
-#pragma unroll
-        for (int u = 0; u < kFusedUnroll; ++u) {
-          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
-          if (q < q1) {
-            const float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
-            m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
-            if constexpr (EF) st4_hint(r + 4 * q, p, pol_keep);   // parked for phase B
-          }
+        if (k < lenB) {
+          const uint64_t q = sb.q0 + k;
+          if constexpr (EF) pb[u] = ld4_hint(rB + 4 * q, pol_stream);
+          else pb[u] = ldq<VEC>(gB, q);
         }
       }
-      if (blockIdx.x == G - 1 && threadIdx.x < (it.n & 3)) {
-        const uint64_t e = n4 * 4 + threadIdx.x;
-        const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-        if constexpr (EF) r[e] = p;
+#pragma unroll
+      for (int u = 0; u < kFusedUnroll; ++u) {
+        const uint64_t k = kb + (uint64_t)u * kFusedThreads;
+        if (k < lenA) {
+          const uint64_t q = sa.q0 + k;
+          const float4 p = EF ? add4(ga[u], ra[u]) : ga[u];
+          m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+          if constexpr (EF) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t)
+        }
+        if (k < lenB) {
+          const uint64_t q = sb.q0 + k;
+          const float4 p = pb[u];
+          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+          st_u32_hint(bodyB + q, pack_i8x4(a0, a1, a2, a3), pol_stream);
+          if constexpr (EF)
+            st4_hint(rB + 4 * q,
+                     make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                 __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                     pol_stream);
+        }
+      }
+    }
+    // ---- tails (n % 4 elements after the last quad) on the last CTA
+    if (blockIdx.x == G - 1) {
+      if (doA && threadIdx.x < (itA.n & 3)) {
+        const uint64_t e = (itA.n >> 2) * 4 + threadIdx.x;
+        const float p = EF ? __fadd_rn(gA[e], rA[e]) : gA[e];
+        if constexpr (EF) rA[e] = p;
         m = max(m, abs_bits(p));
       }
+      if (doB) {
+        if (threadIdx.x < (itB.n & 3)) {
+          const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
+          const float p = EF ? rB[e] : gB[e];
+          const int qe = int8_q(p, s);
+          reinterpret_cast<uint8_t*>(bodyB)[e] = (uint8_t)(qe & 0xFF);
+          if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        }
+        zero_padding(reinterpret_cast<uint8_t*>(bodyB), itB.n);
+      }
+    }
+    // ---- A epilogue: bucket max, arrive
+    if (doA) {
       m = __reduce_max_sync(0xFFFFFFFFu, m);
       if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
       __syncthreads();
       if (threadIdx.x < 32) {
         uint32_t w = threadIdx.x < kFusedThreads / 32 ? s_red[threadIdx.x] : 0u;
         w = __reduce_max_sync(0xFFFFFFFFu, w);
-        if (threadIdx.x == 0 && w) atomicMax(&scratch[it.sidx], w);
+        if (threadIdx.x == 0 && w) atomicMax(&scratch[itA.sidx], w);
       }
-      arrive(&done[i]);
+      arrive(&done[ia]);
     }
-    if (i > 0) {        // ---------------- B(i-1)
-      const Item it = items[i - 1];
-      wait_all(&done[i - 1], G);
-      const uint32_t mbits = *((volatile const uint32_t*)&scratch[it.sidx]);
-      if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload, residual keeps p (unspecified)
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
-        continue;
-      }
-      const float s = int8_scale_from_bits(mbits);
-      const uint64_t n4 = it.n >> 2, per = (n4 + G - 1) / G;
-      const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per), q1 = min(n4, q0 + per);
-      const float* g = gbase + it.g_off;
-      float* r = rbase + it.r_off;
-      uint8_t* slot = slots + it.slot_off;
-      uint8_t* body = slot + 16;
-      if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
-      for (uint64_t qb = q0 + threadIdx.x; qb < q1; qb += (uint64_t)kFusedThreads * kFusedUnroll) {
-        float4 pv[kFusedUnroll];
-#pragma unroll
-        for (int u = 0; u < kFusedUnroll; ++u) {
-          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
-          if (q < q1) pv[u] = EF ? ld4_hint(r + 4 * q, pol_stream) : ldq<VEC>(g, q);
-        }
-#pragma unroll
-        for (int u = 0; u < kFusedUnroll; ++u) {
-          const uint64_t q = qb + (uint64_t)u * kFusedThreads;
-          if (q < q1) {
-            const float4 p = pv[u];
-            const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
-            st_u32_hint(reinterpret_cast<uint32_t*>(body) + q, pack_i8x4(a0, a1, a2, a3), pol_stream);
-            if constexpr (EF)
-              st4_hint(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
-                                         __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
-                       pol_stream);
-          }
-        }
-      }
-      if (blockIdx.x == G - 1) {
-        if (threadIdx.x < (it.n & 3)) {
-          const uint64_t e = n4 * 4 + threadIdx.x;
-          const float p = EF ? r[e] : g[e];
-          const int qe = int8_q(p, s);
-          body[e] = (uint8_t)(qe & 0xFF);
-          if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
-        }
-        zero_padding(body, it.n);
-      }
-    }
+    __syncthreads();
   }
 }
 
 // ----------------------------------------------------------------------------- launchers
-static inline unsigned grid_for(const Launch& L, uint64_t chunks, int per_sm = 8) {
-  uint64_t g = (uint64_t)L.num_sms * per_sm;
-  if (chunks < g) g = chunks;
-  return (unsigned)(g ? g : 1);
+int occupancy_per_sm(const void* kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess || per < 1) per = 1;
+  cache[kernel] = per;
+  return per;
 }
+
+#define GRID(kernel) persistent_grid(L, chunks, (const void*)(kernel), kThreads)
 
 void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
                      uint8_t* slots, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_IDENTITY);
-  dim3 grid(grid_for(L, chunks));
-  if (vec) k_identity<true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
-  else k_identity<false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
+  if (vec) k_identity<true><<<GRID(k_identity<true>), kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
+  else k_identity<false><<<GRID(k_identity<false>), kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
   ++*L.launches;
 }
 
@@ -513,11 +547,10 @@ void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nite
                  float* r, uint8_t* slots, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_FP16);
-  dim3 grid(grid_for(L, chunks));
-  if (ef && vec) k_fp16<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
-  else if (ef) k_fp16<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
-  else if (vec) k_fp16<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
-  else k_fp16<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  if (ef && vec) k_fp16<true, true><<<GRID((k_fp16<true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else if (ef) k_fp16<true, false><<<GRID((k_fp16<true, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else if (vec) k_fp16<false, true><<<GRID((k_fp16<false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else k_fp16<false, false><<<GRID((k_fp16<false, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
   ++*L.launches;
 }
 
@@ -525,11 +558,10 @@ void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int ni
                    const float* g, const float* r, uint32_t* scratch) {
   if (!chunks) return;
   Mark mk(L, PH_ABSMAX);
-  dim3 grid(grid_for(L, chunks));
-  if (ef && vec) k_absmax<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
-  else if (ef) k_absmax<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
-  else if (vec) k_absmax<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
-  else k_absmax<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  if (ef && vec) k_absmax<true, true><<<GRID((k_absmax<true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else if (ef) k_absmax<true, false><<<GRID((k_absmax<true, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else if (vec) k_absmax<false, true><<<GRID((k_absmax<false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
+  else k_absmax<false, false><<<GRID((k_absmax<false, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, scratch);
   ++*L.launches;
 }
 
@@ -537,20 +569,18 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
                        const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_INT8_QUANT);
-  dim3 grid(grid_for(L, chunks));
-  if (ef && vec) k_int8_quant<true, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else if (ef) k_int8_quant<true, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else if (vec) k_int8_quant<false, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else k_int8_quant<false, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  if (ef && vec) k_int8_quant<true, true><<<GRID((k_int8_quant<true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (ef) k_int8_quant<true, false><<<GRID((k_int8_quant<true, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (vec) k_int8_quant<false, true><<<GRID((k_int8_quant<false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else k_int8_quant<false, false><<<GRID((k_int8_quant<false, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
   ++*L.launches;
 }
 
 template <int METHOD, int P>
 static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const uint8_t* slots,
                      float* out) {
-  dim3 grid(grid_for(L, chunks));
-  if (vec) k_reduce_dense<METHOD, P, true><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
-  else k_reduce_dense<METHOD, P, false><<<grid, kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
+  if (vec) k_reduce_dense<METHOD, P, true><<<GRID((k_reduce_dense<METHOD, P, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
+  else k_reduce_dense<METHOD, P, false><<<GRID((k_reduce_dense<METHOD, P, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
 }
 template <int METHOD>
 static void reduce_m(const Launch& L, int P, bool vec, const RItem* items, int nitems, uint64_t chunks,

@@ -782,11 +782,6 @@ __global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ 
 }
 
 // ---------------------------------------------------------------- launchers
-static inline unsigned grid_for(const Launch& L, uint64_t chunks, int per_sm = 8) {
-  uint64_t g = (uint64_t)L.num_sms * per_sm;
-  if (chunks < g) g = chunks;
-  return (unsigned)(g ? g : 1);
-}
 
 template <bool EF, bool VEC>
 static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
@@ -795,7 +790,9 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   const TopkItem* ti = B.items + item0;
   TopkState* st = B.state + item0;
   uint32_t* anyf = B.ctrs + 2;
-  const unsigned ga = grid_for(L, a_chunks);
+  const unsigned ga = persistent_grid(L, a_chunks, (const void*)k_topk_pass<false, EF, VEC>, kThreads);
+  const unsigned gw = persistent_grid(L, a_chunks, (const void*)k_topk_write<VEC>, kThreads);
+  const unsigned gh = persistent_grid(L, a_chunks, (const void*)k_topk_hist<VEC>, kThreads);
   const uint64_t sbase = B.host_sample_off[item0];
   const uint64_t scount = B.host_sample_off[item0 + nitems] - sbase;
   {
@@ -815,7 +812,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     Mark mk(L, PH_TOPK_CLASSIFY);
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 0, flags, value_type, anyf);
-    k_topk_write<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
+    k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
                                                      B.status, 0, anyf);
   }
   {
@@ -826,13 +823,13 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
     Mark mk(L, PH_TOPK_FALLBACK);
     for (int d = 0; d < 3; ++d) {
-      k_topk_hist<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g,
+      k_topk_hist<VEC><<<gh, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g,
                                                       B.hist + (size_t)item0 * 2048, d, anyf);
       k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, d, anyf);
     }
     k_topk_pass<true, EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 1, flags, value_type, anyf);
-    k_topk_write<VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
+    k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
                                                      B.status, 1, anyf);
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf);
   }
