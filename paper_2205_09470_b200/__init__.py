@@ -267,7 +267,8 @@ class SyncContext:
 
     def set_int8_kernel(self, which: str):
         """'auto' | 'two-pass' | 'onchip' (NEBULA_OPT_INT8_KERNEL)."""
-        self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2}[which])
+        self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2, "fused-recompute": 3,
+                                          "fused-park-lag1": 4, "fused-recompute-lag1": 5}[which])
 
     def timing_enable(self, on: bool = True):
         self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))

@@ -61,7 +61,7 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
 bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem);
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems,
                         const float* g, float* r, uint8_t* slots, uint32_t* scratch, uint32_t* flags,
-                        uint32_t* done_words, int grid, size_t smem);
+                        uint32_t* done_words, int grid, size_t smem, int variant);
 // Dense decompress + tree-average over P slots.
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
                          uint64_t chunks, const uint8_t* slots, float* out);
@@ -80,6 +80,7 @@ struct TopkItem {       // per (cluster, bucket) top-k state, device resident
   uint64_t wcap, ccap;  // capacities
   uint64_t status_off;  // into tile-status words
   uint64_t mt0;         // prefix of merge tiles over the launch's items (absolute)
+  uint64_t stage_off;   // into the staging buffer (entries); capacity wcap + ccap
   uint32_t value_type;
   uint32_t pad;
 };
@@ -92,10 +93,11 @@ struct TopkState {      // per item, device resident, rewritten every step
   uint32_t hist_prefix; // fallback radix state
   uint64_t count_above, need;
   uint64_t rank_left;   // fallback radix: rank still to find inside the prefix
-  uint32_t tile_ctr;    // dynamic tile counter for the classify pass
+  uint32_t tile_ctr;    // (unused)
   uint32_t path;
   float scale;
   uint32_t maxbits;
+  unsigned long long stage_top;   // staged entries reserved by pass A
 };
 struct TopkBuffers {
   TopkItem* items;      // [nitems] (bucket-major, cluster-minor: same order as the Item tables)
@@ -103,7 +105,10 @@ struct TopkBuffers {
   uint32_t* sample;
   uint2* wlist;         // (idx, p bits)
   uint2* clist;
-  unsigned long long* status;  // per-tile (winners << 32 | candidates) counts, then prefixes
+  unsigned long long* status;  // per-chunk (winners << 32 | candidates) counts
+  unsigned long long* pref;    // per-chunk exclusive prefixes of the counts
+  unsigned long long* soff;    // per-chunk offset of its staged entries
+  uint2* stage;                // pass-A staging: per chunk W entries then C entries
   uint32_t* hist;       // [nitems][2048] fallback histograms
   uint32_t* ctrs;       // 2 dynamic tile counters
   uint32_t* start;      // sparse-reduce start offsets

@@ -401,7 +401,10 @@ __device__ __forceinline__ Slice slice_of(uint64_t n4, unsigned G) {
   return Slice{q0, min(n4, q0 + per)};
 }
 
-template <bool EF, bool VEC>
+// PARK: phase A stores p into r and B re-reads p (4 B); otherwise A only reads g and r with
+// L2 evict_last and B re-reads both and recomputes p = g + r (same binary32 addition, so
+// bit-identical) — clean lines, nothing to write back.  LAG: B(t - LAG) runs with A(t).
+template <bool EF, bool VEC, bool PARK, int LAG>
 __global__ void __launch_bounds__(kFusedThreads, 2)
     k_int8_fused(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
                  float* __restrict__ rbase, uint8_t* __restrict__ slots, uint32_t* scratch, uint32_t* flags,
@@ -409,8 +412,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
   __shared__ uint32_t s_red[kFusedThreads / 32];
   const unsigned G = gridDim.x;
   const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
-  for (int t = 0; t < nitems + kFusedLag; ++t) {
-    const int ia = t, ib = t - kFusedLag;
+  for (int t = 0; t < nitems + LAG; ++t) {
+    const int ia = t, ib = t - LAG;
     const bool doA = ia < nitems;
     bool doB = ib >= 0;
     // ---- B setup (wait for everyone's A(ib), finished an iteration ago)
@@ -452,14 +455,21 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         const uint64_t k = kb + (uint64_t)u * kFusedThreads;
         if (k < lenA) {
           const uint64_t q = sa.q0 + k;
-          if constexpr (VEC) ga[u] = ld4_hint(gA + 4 * q, pol_stream);
+          const uint64_t polA = PARK ? pol_stream : pol_keep;
+          if constexpr (VEC) ga[u] = ld4_hint(gA + 4 * q, polA);
           else ga[u] = ldq<false>(gA, q);
-          if constexpr (EF) ra[u] = ld4_hint(rA + 4 * q, pol_stream);
+          if constexpr (EF) ra[u] = ld4_hint(rA + 4 * q, polA);
         }
         if (k < lenB) {
           const uint64_t q = sb.q0 + k;
-          if constexpr (EF) pb[u] = ld4_hint(rB + 4 * q, pol_stream);
-          else pb[u] = ldq<VEC>(gB, q);
+          if constexpr (EF && PARK) {
+            pb[u] = ld4_hint(rB + 4 * q, pol_stream);
+          } else if constexpr (EF) {
+            const float4 gg = VEC ? ld4_hint(gB + 4 * q, pol_stream) : ldq<false>(gB, q);
+            pb[u] = add4(gg, ld4_hint(rB + 4 * q, pol_stream));
+          } else {
+            pb[u] = ldq<VEC>(gB, q);
+          }
         }
       }
 #pragma unroll
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           const uint64_t q = sa.q0 + k;
           const float4 p = EF ? add4(ga[u], ra[u]) : ga[u];
           m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
-          if constexpr (EF) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t)
+          if constexpr (EF && PARK) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t + LAG)
         }
         if (k < lenB) {
           const uint64_t q = sb.q0 + k;
@@ -489,13 +499,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
       if (doA && threadIdx.x < (itA.n & 3)) {
         const uint64_t e = (itA.n >> 2) * 4 + threadIdx.x;
         const float p = EF ? __fadd_rn(gA[e], rA[e]) : gA[e];
-        if constexpr (EF) rA[e] = p;
+        if constexpr (EF && PARK) rA[e] = p;
         m = max(m, abs_bits(p));
       }
       if (doB) {
         if (threadIdx.x < (itB.n & 3)) {
           const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
-          const float p = EF ? rB[e] : gB[e];
+          const float p = EF ? (PARK ? rB[e] : __fadd_rn(gB[e], rB[e])) : gB[e];
           const int qe = int8_q(p, s);
           reinterpret_cast<uint8_t*>(bodyB)[e] = (uint8_t)(qe & 0xFF);
           if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
@@ -609,16 +619,18 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
 bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int8_fused<true, true>, kFusedThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int8_fused<true, true, true, 2>, kFusedThreads, 0) !=
           cudaSuccess || per_sm < 1)
     return false;
-  int p2 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<true, false>, kFusedThreads, 0);
-  per_sm = std::min(per_sm, std::max(1, p2));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<false, true>, kFusedThreads, 0);
-  per_sm = std::min(per_sm, std::max(1, p2));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_int8_fused<false, false>, kFusedThreads, 0);
-  per_sm = std::min(per_sm, std::max(1, p2));
+  const void* all[] = {(const void*)k_int8_fused<true, true, true, 2>, (const void*)k_int8_fused<true, false, true, 2>,
+                       (const void*)k_int8_fused<false, true, true, 2>, (const void*)k_int8_fused<false, false, true, 2>,
+                       (const void*)k_int8_fused<true, true, false, 2>, (const void*)k_int8_fused<true, true, true, 1>,
+                       (const void*)k_int8_fused<true, true, false, 1>};
+  for (const void* f : all) {
+    int p2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, f, kFusedThreads, 0);
+    per_sm = std::min(per_sm, std::max(1, p2));
+  }
   *grid = sms * std::min(per_sm, 2);
   *smem = 0;
   *max_items = 0;
@@ -626,14 +638,19 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
 }
 
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,
-                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid, size_t) {
+                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid, size_t,
+                        int variant) {
   Mark mk(L, PH_INT8_ONCHIP);
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
                   (void*)&flags, (void*)&done};
-  const void* f = ef ? (vec ? (const void*)k_int8_fused<true, true> : (const void*)k_int8_fused<true, false>)
-                     : (vec ? (const void*)k_int8_fused<false, true> : (const void*)k_int8_fused<false, false>);
+  // variant: 0 park p / lag 2 (default), 1 recompute / lag 2, 2 park / lag 1, 3 recompute / lag 1
+  const void* f = ef ? (vec ? (const void*)k_int8_fused<true, true, true, 2> : (const void*)k_int8_fused<true, false, true, 2>)
+                     : (vec ? (const void*)k_int8_fused<false, true, true, 2> : (const void*)k_int8_fused<false, false, true, 2>);
+  if (ef && vec && variant == 1) f = (const void*)k_int8_fused<true, true, false, 2>;
+  if (ef && vec && variant == 2) f = (const void*)k_int8_fused<true, true, true, 1>;
+  if (ef && vec && variant == 3) f = (const void*)k_int8_fused<true, true, false, 1>;
   cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kFusedThreads), args, 0, L.stream);
   ++*L.launches;
 }

@@ -7,15 +7,19 @@
 //   S  k_topk_sample   (gather, ~0.5 B/elem) key(fl(g + r)) at every S-th position
 //   B  k_topk_bracket  (1 CTA/item) radix-select two ranks of the sample -> bracket
 //                       [t_lo, t_hi] that holds the true k-th key with overwhelming odds
-//   A  k_topk_pass     (streaming, 12 B/elem) p = g + r -> r; max-abs bits; per-tile counts of
-//                       winners (key > t_hi) and candidates (t_lo <= key <= t_hi)   [EF fused]
-//   X  k_topk_scan     (1 CTA/item) exclusive scan of the tile counts -> tile offsets, totals
-//   C  k_topk_write    (streaming, 4 B/elem) re-read p, emit winners and candidates
-//                       (idx, p bits) in ascending index order at the tile offsets
+//   A  k_topk_stage    (streaming, 12 B/elem) p = g + r -> r; max-abs bits; winners
+//                       (key > t_hi) and candidates (t_lo <= key <= t_hi) of each 4096-element
+//                       chunk, in index order, staged at a per-chunk slot reserved with one
+//                       atomic; per-chunk counts                                  [EF fused]
+//   X  k_topk_scan     (1 CTA/item) exclusive scan of the chunk counts -> chunk offsets, totals
+//   M  k_topk_move     (one warp per chunk) staged entries -> ascending winner / candidate
+//                       lists at the chunk offsets (touches only the entries, ~2% of n)
 //   D  k_topk_resolve  (1 CTA/item) verify W < k <= W + C; radix-select the exact threshold T
 //                       among the candidates; keep key > T and the first need_T keys == T
-//   (fallback, only items whose bracket failed: 3 full radix-histogram passes give the exact
-//    T, then count/scan/write/resolve rerun with t_lo = t_hi = T — bounded memory, exact)
+//   (fallback, only items whose bracket failed or whose staging overflowed: 3 full
+//    radix-histogram passes give the exact T, then a count pass, the scan, an ordered write
+//    pass (k_topk_write, positions known up front, so a huge tie set needs no staging) and
+//    resolve rerun with t_lo = t_hi = T — bounded memory, exact)
 //   F  k_topk_merge    merge-path of the two ascending lists -> payload idx[k], val[k];
 //                       residual at the selected positions r = p - D(v)
 //
@@ -275,12 +279,209 @@ __global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- A: EF pass + classify + stage
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict__ aitems,
+                                                         const TopkItem* __restrict__ titems,
+                                                         TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                         const float* __restrict__ gbase, float* __restrict__ rbase,
+                                                         unsigned long long* __restrict__ counts,
+                                                         unsigned long long* __restrict__ soff,
+                                                         uint2* __restrict__ stage) {
+  __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
+  __shared__ unsigned long long s_base;
+  int hint = 0, cur = -1;
+  uint32_t m = 0, t_lo = 0, t_hi = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int i = find_item(aitems, nitems, c, hint);
+    hint = i;
+    if (i != cur) {
+      if (cur >= 0) {
+        const uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+        if (lane == 0 && w) atomicMax(&st[cur].maxbits, w);
+      }
+      cur = i;
+      m = 0;
+      t_lo = st[i].t_lo;
+      t_hi = st[i].t_hi;
+    }
+    const Item it = aitems[i];
+    const TopkItem& ti = titems[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    uint32_t kb[kQuadsPerThread][4];
+    float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      if (q < n4) {
+        if constexpr (VEC) gv[u] = ld4_stream(g + 4 * q);
+        else gv[u] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+        if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+      }
+    }
+    unsigned long long pw = 0, pc = 0;
+#pragma unroll
+    for (int u = 0; u < kQuadsPerThread; ++u) {
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      uint32_t wn = 0, cn = 0;
+      if (q < n4) {
+        float4 p = gv[u];
+        if constexpr (EF) {
+          p = make_float4(__fadd_rn(p.x, rv[u].x), __fadd_rn(p.y, rv[u].y), __fadd_rn(p.z, rv[u].z),
+                          __fadd_rn(p.w, rv[u].w));
+          st4(r + 4 * q, p);
+        }
+        kb[u][0] = __float_as_uint(p.x); kb[u][1] = __float_as_uint(p.y);
+        kb[u][2] = __float_as_uint(p.z); kb[u][3] = __float_as_uint(p.w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = kb[u][e] & 0x7FFFFFFFu;
+          m = max(m, key);
+          wn += key > t_hi;
+          cn += (key >= t_lo) & (key <= t_hi);
+        }
+      } else {
+        kb[u][0] = kb[u][1] = kb[u][2] = kb[u][3] = 0;
+      }
+      pw |= (unsigned long long)wn << (12 * u);
+      pc |= (unsigned long long)cn << (12 * u);
+    }
+    uint32_t tkb = 0, tw = 0, tcn = 0;
+    const bool has_tail = (j == n4 / kChunkQuads) && threadIdx.x < (it.n & 3);
+    if (has_tail) {
+      const uint64_t e = n4 * 4 + threadIdx.x;
+      const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      if constexpr (EF) r[e] = p;
+      tkb = __float_as_uint(p);
+      const uint32_t key = tkb & 0x7FFFFFFFu;
+      m = max(m, key);
+      tw = key > t_hi;
+      tcn = (key >= t_lo) & (key <= t_hi);
+    }
+    // element order inside the chunk: (field u = 0..3 then tail, thread, element)
+    pw |= (unsigned long long)tw << 48;
+    pc |= (unsigned long long)tcn << 48;
+    unsigned long long iw = pw, ic = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long a1 = __shfl_up_sync(0xFFFFFFFFu, iw, o);
+      const unsigned long long a2 = __shfl_up_sync(0xFFFFFFFFu, ic, o);
+      if (lane >= o) { iw += a1; ic += a2; }
+    }
+    if (lane == 31) { s_wt[warp] = iw; s_ct[warp] = ic; }
+    __syncthreads();
+    unsigned long long ew = iw - pw, ec = ic - pc, totw = 0, totc = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long a1 = s_wt[w], a2 = s_ct[w];
+      if (w < warp) { ew += a1; ec += a2; }
+      totw += a1;
+      totc += a2;
+    }
+    uint32_t baseW[kQuadsPerThread + 1], baseC[kQuadsPerThread + 1];
+    uint32_t accW = 0, accC = 0;
+#pragma unroll
+    for (int u = 0; u <= kQuadsPerThread; ++u) {
+      baseW[u] = accW + (uint32_t)((ew >> (12 * u)) & 0xFFF);
+      baseC[u] = accC + (uint32_t)((ec >> (12 * u)) & 0xFFF);
+      accW += (uint32_t)((totw >> (12 * u)) & 0xFFF);
+      accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
+    }
+    const uint32_t tileW = accW, tileC = accC;
+    if (threadIdx.x == 0) {
+      const unsigned long long base = (tileW + tileC) ? atomicAdd(&st[i].stage_top, (unsigned long long)(tileW + tileC)) : 0ull;
+      s_base = base;
+      counts[ti.status_off + j] = pack_wc(tileW, tileC);
+      soff[ti.status_off + j] = base;
+    }
+    __syncthreads();
+    if (tileW + tileC) {
+      const uint64_t cap = ti.wcap + ti.ccap, base = s_base;
+      uint2* S = stage + ti.stage_off;
+#pragma unroll
+      for (int u = 0; u < kQuadsPerThread; ++u) {
+        const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+        if (q < n4) {
+          uint32_t w = baseW[u], cc = baseC[u];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t key = kb[u][e] & 0x7FFFFFFFu;
+            const uint32_t idx = (uint32_t)(4 * q + e);
+            if (key > t_hi) {
+              const uint64_t pos = base + w++;
+              if (pos < cap) S[pos] = make_uint2(idx, kb[u][e]);
+            } else if (key >= t_lo) {
+              const uint64_t pos = base + tileW + cc++;
+              if (pos < cap) S[pos] = make_uint2(idx, kb[u][e]);
+            }
+          }
+        }
+      }
+      if (has_tail) {
+        const uint32_t key = tkb & 0x7FFFFFFFu;
+        const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
+        if (key > t_hi) {
+          const uint64_t pos = base + baseW[kQuadsPerThread];
+          if (pos < cap) S[pos] = make_uint2(idx, tkb);
+        } else if (key >= t_lo) {
+          const uint64_t pos = base + tileW + baseC[kQuadsPerThread];
+          if (pos < cap) S[pos] = make_uint2(idx, tkb);
+        }
+      }
+    }
+  }
+  if (cur >= 0) {
+    const uint32_t w = __reduce_max_sync(0xFFFFFFFFu, m);
+    if (lane == 0 && w) atomicMax(&st[cur].maxbits, w);
+  }
+}
+
+// ---------------------------------------------------------------- M: staged -> ordered lists
+// One warp per chunk: copy its W staged winners to wl[prefix_W ...] and its C candidates to
+// cl[prefix_C ...].  Items whose staging overflowed are skipped (resolve fails them).
+__global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems,
+                                                   const TopkState* __restrict__ st, int nitems, uint64_t chunks,
+                                                   const unsigned long long* __restrict__ counts,
+                                                   const unsigned long long* __restrict__ pref,
+                                                   const unsigned long long* __restrict__ soff,
+                                                   const uint2* __restrict__ stage, uint2* __restrict__ wl,
+                                                   uint2* __restrict__ cl) {
+  const uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= chunks) return;
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (aitems[mid].chunk0 <= c) lo = mid; else hi = mid - 1;
+  }
+  const TopkItem& ti = titems[lo];
+  const TopkState& S = st[lo];
+  if (S.failed == 2 || S.stage_top > ti.wcap + ti.ccap) return;
+  const uint64_t j = c - aitems[lo].chunk0;
+  const unsigned long long cnt = counts[ti.status_off + j];
+  const uint32_t W = (uint32_t)(cnt >> 32), C = (uint32_t)(cnt & 0xFFFFFFFFu);
+  if (!(W + C)) return;
+  const unsigned long long pf = pref[ti.status_off + j];
+  const uint64_t pw = pf >> 32, pc = pf & 0xFFFFFFFFull;
+  const uint2* src = stage + ti.stage_off + soff[ti.status_off + j];
+  uint2* dw = wl + ti.list_off;
+  uint2* dc = cl + ti.list_off;
+  for (uint32_t x = lane; x < W; x += 32)
+    if (pw + x < ti.wcap) dw[pw + x] = src[x];
+  for (uint32_t x = lane; x < C; x += 32)
+    if (pc + x < ti.ccap) dc[pc + x] = src[W + x];
+}
+
 // ---------------------------------------------------------------- X: scan tile counts
 // 1 CTA per item: exclusive prefix of the (W, C) tile words in place; totals; after pass A
 // also the non-finite check and the int8 value scale (both need the bucket's max).
 __global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __restrict__ titems,
                                                            TopkState* __restrict__ st,
-                                                           unsigned long long* __restrict__ tiles, int retry,
+                                                           const unsigned long long* __restrict__ tiles,
+                                                           unsigned long long* __restrict__ pref, int retry,
                                                            uint32_t* flags, int value_type,
                                                            const uint32_t* any_failed) {
   if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
@@ -297,14 +498,15 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __res
     }
     if (threadIdx.x == 0) S.scale = value_type == V_I8 ? int8_scale_from_bits(mb) : 1.0f;
   }
-  unsigned long long* tw = tiles + ti.status_off;
+  const unsigned long long* tw = tiles + ti.status_off;
+  unsigned long long* pw = pref + ti.status_off;
   unsigned long long carry = 0;
   for (uint64_t j0 = 0; j0 < ti.nchunks; j0 += kSelThreads) {
     const uint64_t j = j0 + threadIdx.x;
     const unsigned long long v = j < ti.nchunks ? tw[j] : 0ull;
     unsigned long long tot;
     const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
-    if (j < ti.nchunks) tw[j] = carry + incl - v;
+    if (j < ti.nchunks) pw[j] = carry + incl - v;
     carry += tot;
   }
   if (threadIdx.x == 0) {
@@ -321,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
                                                          const float* __restrict__ pbase, bool p_in_r,
                                                          const float* __restrict__ gbase,
                                                          uint2* __restrict__ wl, uint2* __restrict__ cl,
-                                                         const unsigned long long* __restrict__ tiles, int retry,
+                                                         const unsigned long long* __restrict__ pref, int retry,
                                                          const uint32_t* any_failed) {
   if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
@@ -402,7 +604,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
       accW += (uint32_t)((totw >> (12 * u)) & 0xFFF);
       accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
     }
-    const unsigned long long off = tiles[ti.status_off + j];
+    const unsigned long long off = pref[ti.status_off + j];
     const uint64_t preW = off >> 32, preC = off & 0xFFFFFFFFull;
     uint2* W = wl + ti.list_off;
     uint2* C = cl + ti.list_off;
@@ -454,7 +656,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   if (retry && S.mode != 1) return;
   const uint64_t k = ti.k, W = S.wcount, C = S.ccount;
   if (threadIdx.x == 0) {
-    bool ok = (W < k || k == 0) && (W + C >= k);
+    bool ok = (W < k || k == 0) && (W + C >= k) && (retry || S.stage_top <= ti.wcap + ti.ccap);
     if (ok && C > ti.ccap) ok = (S.t_lo == S.t_hi) && (k - W) <= ti.ccap;  // exact tie set: prefix suffices
     s_ok = ok;
     if (!ok) { S.mode = 1; S.failed = 1; atomicOr(any_failed, 1u); }   // -> exact radix fallback
@@ -790,7 +992,8 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   const TopkItem* ti = B.items + item0;
   TopkState* st = B.state + item0;
   uint32_t* anyf = B.ctrs + 2;
-  const unsigned ga = persistent_grid(L, a_chunks, (const void*)k_topk_pass<false, EF, VEC>, kThreads);
+  const unsigned ga = persistent_grid(L, a_chunks, (const void*)k_topk_stage<EF, VEC>, kThreads);
+  const unsigned gp = persistent_grid(L, a_chunks, (const void*)k_topk_pass<true, EF, VEC>, kThreads);
   const unsigned gw = persistent_grid(L, a_chunks, (const void*)k_topk_write<VEC>, kThreads);
   const unsigned gh = persistent_grid(L, a_chunks, (const void*)k_topk_hist<VEC>, kThreads);
   const uint64_t sbase = B.host_sample_off[item0];
@@ -807,13 +1010,15 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   }
   {
     Mark mk(L, PH_TOPK_A);
-    k_topk_pass<false, EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
+    k_topk_stage<EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, B.soff,
+                                                         B.stage);
   }
   {
     Mark mk(L, PH_TOPK_CLASSIFY);
-    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 0, flags, value_type, anyf);
-    k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
-                                                     B.status, 0, anyf);
+    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 0, flags, value_type, anyf);
+    k_topk_move<<<(unsigned)((a_chunks * 32 + 255) / 256), 256, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks,
+                                                                             B.status, B.pref, B.soff, B.stage,
+                                                                             B.wlist, B.clist);
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
@@ -827,10 +1032,10 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
                                                       B.hist + (size_t)item0 * 2048, d, anyf);
       k_topk_hist_select<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.hist + (size_t)item0 * 2048, d, anyf);
     }
-    k_topk_pass<true, EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
-    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, 1, flags, value_type, anyf);
+    k_topk_pass<true, EF, VEC><<<gp, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, anyf);
+    k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 1, flags, value_type, anyf);
     k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
-                                                     B.status, 1, anyf);
+                                                     B.pref, 1, anyf);
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf);
   }
   Mark mk(L, PH_TOPK_MERGE);

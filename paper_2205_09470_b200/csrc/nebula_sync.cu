@@ -522,12 +522,12 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       }
       bool onchip = false;
       if (ctx->onchip_ok) {
-        if (ctx->int8_kernel == 2) onchip = true;
+        if (ctx->int8_kernel >= 2) onchip = true;
         else if (ctx->int8_kernel == 0) onchip = elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20);
       }
       if (onchip) {
         launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch, ctx->d_flags,
-                           ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem);
+                           ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem, ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : 0);
       } else {
         launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
         launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch,
@@ -708,8 +708,8 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launc
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
-    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be 0, 1 or 2");
-    if (value == 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
+    if (value < 0 || value > 5) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 5]");
+    if (value >= 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;
     return NEBULA_OK;
