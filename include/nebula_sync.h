@@ -181,9 +181,11 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 
 /* Tuning knobs (results are bit-identical whichever kernel runs).
  *   NEBULA_OPT_INT8_KERNEL: 0 auto (default), 1 two-pass streaming (max-abs pass + quantise
- *   pass, 21 B/elem of HBM traffic), 2 fused single pass (cooperative persistent grid, p parked
- *   in r / L2 across a split arrive/wait barrier per bucket, 13 B/elem).  Auto picks the fused
- *   kernel when buckets average >= 1M elements. */
+ *   pass, 21 B/elem of HBM traffic), 2..5 fused single pass (cooperative persistent grid, a
+ *   split arrive/wait barrier per bucket; 13 B/elem algorithmic): 2 p parked in r/L2 with the
+ *   quantise phase lagging two buckets, 3 the same recomputing p from L2-retained g and r,
+ *   4 parked with lag 1, 5 recompute with lag 1.  Auto = 4 when buckets average >= 1M
+ *   elements, else 1. */
 #define NEBULA_OPT_INT8_KERNEL 1
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 

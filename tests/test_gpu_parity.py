@@ -106,7 +106,8 @@ def test_dense_parity(nb, method, P, sizes):
     assert run_loopback(nb, method, sizes, P) > 0
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-recompute", "fused-park-lag1",
+                                         "fused-recompute-lag1"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
 @pytest.mark.parametrize("ef", [True, False])
 def test_int8_kernels(nb, int8_kernel, sizes, ef):
