@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--bucket-mib", type=float, default=25.0)
     ap.add_argument("--clusters", type=int, default=2, help="simulated clusters at N=1 (LOOPBACK)")
     ap.add_argument("--no-ef", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
                                                               "fused-park-lag1", "fused-recompute-lag1"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -235,7 +236,7 @@ def workload_config(args, n, P):
     return {"workload": f"{args.workload}-" + (f"loopback-P{P}" if args.gpus == 1 else f"nccl-P{P}xG1"),
             "elements_per_cluster": n, "clusters": P, "gpus_per_cluster": 1, "method": mname,
             "bucketing": f"fixed {args.bucket_mib:g} MiB slices of the flat gradient",
-            "transport": "loopback" if args.gpus == 1 else "nccl-nvlink",
+            "transport": "loopback" if args.gpus == 1 else "nvlink",
             "l2": "inputs (>= 1.1 GB per cluster) exceed the 126 MB L2; no flush needed"}
 
 
@@ -290,6 +291,8 @@ def main():
         ctx = nb.init_process_group_context(sizes, device=local, **common)
     if method == 2:
         ctx.set_int8_kernel(args.int8_kernel)
+    if world > 1 and args.exchange != "auto":
+        ctx.set_exchange(args.exchange)
     torch.cuda.synchronize()
 
     def barrier():
@@ -402,7 +405,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(args, n, P), "roofline": roof, "step_roofline": step_roof,
+                "config": dict(workload_config(args, n, P), exchange=ctx.exchange_mode()), "roofline": roof, "step_roofline": step_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "kernels": kern,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -28,6 +28,8 @@ VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK = 0, 1
 ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
+OPT_EXCHANGE = 2
+EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push"}
 UNIQUE_ID_BYTES = 128
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "OOM", 4: "CUDA", 5: "NCCL",
@@ -111,6 +113,7 @@ def load() -> ctypes.CDLL:
         "nebula_kernel_launches": (U64, [P]),
         "nebula_timing_enable": (I32, [P, I32]),
         "nebula_set_option": (I32, [P, I32, ctypes.c_int64]),
+        "nebula_exchange_mode": (I32, [P]),
         "nebula_timing_read": (I32, [P, ctypes.POINTER(_PhaseTime), I32, ctypes.POINTER(I32)]),
         "nebula_phase_name": (ctypes.c_char_p, [ctypes.c_uint32]),
         "nebula_sync_destroy": (I32, [P]),
@@ -269,6 +272,13 @@ class SyncContext:
         """'auto' | 'two-pass' | 'onchip' (NEBULA_OPT_INT8_KERNEL)."""
         self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2, "fused-recompute": 3,
                                           "fused-park-lag1": 4, "fused-recompute-lag1": 5}[which])
+
+    def set_exchange(self, which: str):
+        """'auto' | 'nccl' | 'p2p' (NEBULA_OPT_EXCHANGE; between steps only)."""
+        self.set_option(OPT_EXCHANGE, {"auto": 0, "nccl": 1, "p2p": 2}[which])
+
+    def exchange_mode(self) -> str:
+        return EXCHANGE_MODES[self._L.nebula_exchange_mode(self._h)]
 
     def timing_enable(self, on: bool = True):
         self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))

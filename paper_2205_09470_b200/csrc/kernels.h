@@ -12,7 +12,7 @@ namespace nb {
 enum Phase : int {
   PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
-  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_COUNT
+  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_COUNT
 };
 
 struct Launch {
@@ -44,27 +44,37 @@ struct Mark {
 // ---- dense codecs (kernels_dense.cu) ----
 // IDENTITY: payload <- g (+ non-finite check).  Residual untouched (R15).
 void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks,
-                     const float* g, uint8_t* slots, uint32_t* flags);
+                     const float* g, const Dests& slots, uint32_t* flags);
 // FP16 + EF, single pass: p = g + r; h = RNE16(p); r <- p - h; flags.
 void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
-                 const float* g, float* r, uint8_t* slots, uint32_t* flags);
+                 const float* g, float* r, const Dests& slots, uint32_t* flags);
 // INT8 pass 1: scratch[sidx] <- max over the item of |g + r| bits (atomicMax; zeroed by caller).
 void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                    const float* g, const float* r, uint32_t* scratch);
 // INT8 pass 2: scale from scratch, quantize + pack, r <- p - q*s.
 void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
-                       const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags);
+                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
 // INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
 // p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
 // when a cooperative launch is not possible; the caller then uses the two-pass kernels.
 // done_words: >= nitems words (zeroed by the launcher).
 bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem);
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems,
-                        const float* g, float* r, uint8_t* slots, uint32_t* scratch, uint32_t* flags,
+                        const float* g, float* r, const Dests& slots, uint32_t* scratch, uint32_t* flags,
                         uint32_t* done_words, int grid, size_t smem, int variant);
 // Dense decompress + tree-average over P slots.
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
                          uint64_t chunks, const uint8_t* slots, float* out);
+
+// ---- P2P push exchange (kernels_dense.cu) ----
+struct Peers {
+  unsigned long long* arrive[8];  // every cluster's arrival flags (IPC-mapped; own at [me])
+  int n, me;
+};
+// For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
+// its slots (system-scope release), then wait until every peer said the same to us.
+void launch_exchange_flags(const Launch& L, const Peers& pe, unsigned long long* local_arrive, int lo, int hi,
+                           uint64_t seq, uint32_t* flags);
 
 // ---- top-k (kernels_topk.cu) ----
 struct TopkItem {       // per (cluster, bucket) top-k state, device resident
@@ -120,7 +130,7 @@ struct TopkBuffers {
 // payloads, updates residuals.  aitems = the call's Item table (same order), g = gradient
 // base, r = residual base.
 void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems,
-                 uint64_t a_chunks, const Item* aitems, const float* g, float* r, uint8_t* slots,
+                 uint64_t a_chunks, const Item* aitems, const float* g, float* r, const Dests& slots,
                  uint32_t* flags, int value_type, uint64_t merge_tiles);
 // Sparse decompress + tree-average (tile merge over the ascending index lists).
 // entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).

@@ -47,16 +47,16 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 // R18: sections are zero-padded to 16 bytes (slots are reused across methods/steps, so the
 // padding is rewritten every time; threads 16.. of the tail chunk, disjoint from the tail
 // element writers 0..3).
-__device__ __forceinline__ void zero_padding(uint8_t* body, uint64_t nbytes) {
+__device__ __forceinline__ void zero_padding(const Dests& d, uint64_t body_off, uint64_t nbytes) {
   const uint64_t end = pad16(nbytes);
   const uint64_t z = nbytes + (threadIdx.x >= 16 ? threadIdx.x - 16 : end);
-  if (z < end) body[z] = 0;
+  if (z < end) put<uint8_t>(d, body_off + z, (uint8_t)0);
 }
 
 // ----------------------------------------------------------------------------- IDENTITY
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ items, int nitems, uint64_t chunks,
-                                                       const float* __restrict__ gbase, uint8_t* __restrict__ slots,
+                                                       const float* __restrict__ gbase, Dests dst,
                                                        uint32_t* flags) {
   int hint = 0;
   bool bad = false;
@@ -66,9 +66,8 @@ __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ 
     const Item it = items[i];
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
     const float* g = gbase + it.g_off;
-    uint8_t* slot = slots + it.slot_off;
-    float* body = reinterpret_cast<float*>(slot + 16);
-    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_IDENTITY, (uint32_t)it.n, 1.0f, 0u);
+    const uint64_t bo = it.slot_off + 16;   // body offset inside every destination
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, M_IDENTITY, (uint32_t)it.n, 1.0f, 0u);
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
       const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
@@ -76,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ 
         float4 v = ldq<VEC>(g, q);
         bad |= nonfinite_bits(abs_bits(v.x)) | nonfinite_bits(abs_bits(v.y)) | nonfinite_bits(abs_bits(v.z)) |
                nonfinite_bits(abs_bits(v.w));
-        st4(body + 4 * q, v);
+        put(dst, bo + 16 * q, v);
       }
     }
     if (j == n4 / kChunkQuads) {
@@ -84,12 +83,13 @@ __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ 
         const uint64_t e = n4 * 4 + threadIdx.x;
         float v = g[e];
         bad |= nonfinite_bits(abs_bits(v));
-        body[e] = v;
+        put(dst, bo + 4 * e, v);
       }
-      zero_padding(slot + 16, 4 * it.n);
+      zero_padding(dst, bo, 4 * it.n);
     }
   }
   raise_flags(flags, bad, false);
+  if (dst.n > 1) __threadfence_system();   // pushed payload visible system-wide before the flag
 }
 
 // ----------------------------------------------------------------------------- FP16 + EF
@@ -105,7 +105,7 @@ __device__ __forceinline__ float fp16_one(float p, uint16_t& hb, bool& bad, bool
 template <bool EF, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ items, int nitems, uint64_t chunks,
                                                    const float* __restrict__ gbase, float* __restrict__ rbase,
-                                                   uint8_t* __restrict__ slots, uint32_t* flags) {
+                                                   Dests dst, uint32_t* flags) {
   int hint = 0;
   bool bad = false, ovf = false;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
@@ -115,9 +115,8 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
-    uint8_t* slot = slots + it.slot_off;
-    uint16_t* body = reinterpret_cast<uint16_t*>(slot + 16);
-    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_FP16, (uint32_t)it.n, 1.0f, 0u);
+    const uint64_t bo = it.slot_off + 16;
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, M_FP16, (uint32_t)it.n, 1.0f, 0u);
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
@@ -139,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
         d.z = fp16_one(p.z, h2, bad, ovf);
         d.w = fp16_one(p.w, h3, bad, ovf);
         uint2 packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
-        *reinterpret_cast<uint2*>(body + 4 * q) = packed;
+        put(dst, bo + 8 * q, packed);
         if constexpr (EF)
           st4(r + 4 * q, make_float4(__fsub_rn(p.x, d.x), __fsub_rn(p.y, d.y), __fsub_rn(p.z, d.z),
                                      __fsub_rn(p.w, d.w)));
@@ -151,13 +150,14 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
         float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
         uint16_t hb;
         float d = fp16_one(p, hb, bad, ovf);
-        body[e] = hb;
+        put(dst, bo + 2 * e, hb);
         if constexpr (EF) r[e] = __fsub_rn(p, d);
       }
-      zero_padding(slot + 16, 2 * it.n);
+      zero_padding(dst, bo, 2 * it.n);
     }
   }
   raise_flags(flags, bad, ovf);
+  if (dst.n > 1) __threadfence_system();
 }
 
 // ----------------------------------------------------------------------------- INT8 pass 1
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const Item* __restrict__ it
 template <bool EF, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict__ items, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
-                                                         uint8_t* __restrict__ slots,
+                                                         Dests dst,
                                                          const uint32_t* __restrict__ scratch, uint32_t* flags) {
   int hint = 0;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
@@ -231,9 +231,8 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
     const float s = int8_scale_from_bits(mbits);
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
-    uint8_t* slot = slots + it.slot_off;
-    uint8_t* body = slot + 16;
-    if (j == 0 && threadIdx.x == 0) write_preamble(slot, M_INT8, (uint32_t)it.n, s, 0u);
+    const uint64_t bo = it.slot_off + 16;
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, s, 0u);
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       if (q < n4) {
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
         int q0 = int8_q(p.x, s), q1 = int8_q(p.y, s), q2 = int8_q(p.z, s), q3 = int8_q(p.w, s);
-        reinterpret_cast<uint32_t*>(body)[q] = pack_i8x4(q0, q1, q2, q3);
+        put(dst, bo + 4 * q, pack_i8x4(q0, q1, q2, q3));
         if constexpr (EF)
           st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)q0, s)), __fsub_rn(p.y, __fmul_rn((float)q1, s)),
                                      __fsub_rn(p.z, __fmul_rn((float)q2, s)), __fsub_rn(p.w, __fmul_rn((float)q3, s))));
@@ -260,12 +259,13 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
         const uint64_t e = n4 * 4 + threadIdx.x;
         float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
         int qe = int8_q(p, s);
-        body[e] = (uint8_t)(qe & 0xFF);
+        put(dst, bo + e, (uint8_t)(qe & 0xFF));
         if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
       }
-      zero_padding(body, it.n);
+      zero_padding(dst, bo, it.n);
     }
   }
+  if (dst.n > 1) __threadfence_system();
 }
 
 // ----------------------------------------------------------------------------- reduce
@@ -407,7 +407,7 @@ __device__ __forceinline__ Slice slice_of(uint64_t n4, unsigned G) {
 template <bool EF, bool VEC, bool PARK, int LAG>
 __global__ void __launch_bounds__(kFusedThreads, 2)
     k_int8_fused(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
-                 float* __restrict__ rbase, uint8_t* __restrict__ slots, uint32_t* scratch, uint32_t* flags,
+                 float* __restrict__ rbase, Dests dst, uint32_t* scratch, uint32_t* flags,
                  unsigned* done) {
   __shared__ uint32_t s_red[kFusedThreads / 32];
   const unsigned G = gridDim.x;
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
       } else {
         s = int8_scale_from_bits(mbits);
         sb = slice_of(itB.n >> 2, G);
-        if (blockIdx.x == 0 && threadIdx.x == 0) write_preamble(slots + itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
+        if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
       }
     }
     // ---- A setup
@@ -444,7 +444,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     float* rA = rbase + itA.r_off;
     const float* gB = gbase + itB.g_off;
     float* rB = rbase + itB.r_off;
-    uint32_t* bodyB = reinterpret_cast<uint32_t*>(slots + itB.slot_off + 16);
+    const uint64_t boB = itB.slot_off + 16;
+    uint32_t* bodyB = reinterpret_cast<uint32_t*>(dst.p[0] + boB);
     const uint64_t lenA = sa.q1 - sa.q0, lenB = doB ? sb.q1 - sb.q0 : 0;
     const uint64_t len = max(lenA, lenB);
     uint32_t m = 0;
@@ -485,7 +486,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           const uint64_t q = sb.q0 + k;
           const float4 p = pb[u];
           const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
-          st_u32_hint(bodyB + q, pack_i8x4(a0, a1, a2, a3), pol_stream);
+          const uint32_t w = pack_i8x4(a0, a1, a2, a3);
+          st_u32_hint(bodyB + q, w, pol_stream);
+#pragma unroll 1
+          for (int d = 1; d < dst.n; ++d) reinterpret_cast<uint32_t*>(dst.p[d] + boB)[q] = w;   // NVLink push
           if constexpr (EF)
             st4_hint(rB + 4 * q,
                      make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
@@ -507,10 +511,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
           const float p = EF ? (PARK ? rB[e] : __fadd_rn(gB[e], rB[e])) : gB[e];
           const int qe = int8_q(p, s);
-          reinterpret_cast<uint8_t*>(bodyB)[e] = (uint8_t)(qe & 0xFF);
+          put(dst, boB + e, (uint8_t)(qe & 0xFF));
           if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
         }
-        zero_padding(reinterpret_cast<uint8_t*>(bodyB), itB.n);
+        zero_padding(dst, boB, itB.n);
       }
     }
     // ---- A epilogue: bucket max, arrive
@@ -527,6 +531,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     }
     __syncthreads();
   }
+  if (dst.n > 1) __threadfence_system();
 }
 
 // ----------------------------------------------------------------------------- launchers
@@ -545,7 +550,7 @@ int occupancy_per_sm(const void* kernel, int threads, size_t smem) {
 #define GRID(kernel) persistent_grid(L, chunks, (const void*)(kernel), kThreads)
 
 void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
-                     uint8_t* slots, uint32_t* flags) {
+                     const Dests& slots, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_IDENTITY);
   if (vec) k_identity<true><<<GRID(k_identity<true>), kThreads, 0, L.stream>>>(items, nitems, chunks, g, slots, flags);
@@ -554,7 +559,7 @@ void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, u
 }
 
 void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
-                 float* r, uint8_t* slots, uint32_t* flags) {
+                 float* r, const Dests& slots, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_FP16);
   if (ef && vec) k_fp16<true, true><<<GRID((k_fp16<true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
@@ -576,7 +581,7 @@ void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int ni
 }
 
 void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
-                       const float* g, float* r, uint8_t* slots, const uint32_t* scratch, uint32_t* flags) {
+                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags) {
   if (!chunks) return;
   Mark mk(L, PH_INT8_QUANT);
   if (ef && vec) k_int8_quant<true, true><<<GRID((k_int8_quant<true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
@@ -638,8 +643,9 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
 }
 
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,
-                        uint8_t* slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid, size_t,
-                        int variant) {
+                        const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid,
+                        size_t, int variant) {
+  Dests slots = slots_in;
   Mark mk(L, PH_INT8_ONCHIP);
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;
@@ -652,6 +658,53 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
   if (ef && vec && variant == 2) f = (const void*)k_int8_fused<true, true, true, 1>;
   if (ef && vec && variant == 3) f = (const void*)k_int8_fused<true, true, false, 1>;
   cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kFusedThreads), args, 0, L.stream);
+  ++*L.launches;
+}
+
+// ----------------------------------------------------------------------------- P2P flags
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Signal every peer that our payloads of exchange `seq` sit in its slots, then wait for every
+// peer's signal.  The compress kernels ended with a system-scope fence after their pushes, and
+// stream order puts them before this kernel; the release store publishes them.  A peer that
+// never signals (dead rank) sets kFlagPeerTimeout after 60 s instead of hanging the GPU.
+__global__ void k_exchange_flags(Peers pe, unsigned long long* local, int lo, int hi, unsigned long long seq,
+                                 uint32_t* flags) {
+  const int P = pe.n, me = pe.me, total = (hi - lo) * P;
+  __threadfence_system();
+  for (int x = threadIdx.x; x < total; x += blockDim.x) {
+    const int b = lo + x / P, c = x % P;
+    if (c != me) st_release_sys(pe.arrive[c] + (size_t)b * P + me, seq);
+  }
+  const unsigned long long t0 = globaltimer_ns();
+  for (int x = threadIdx.x; x < total; x += blockDim.x) {
+    const int b = lo + x / P, c = x % P;
+    if (c == me) continue;
+    while (ld_acquire_sys(local + (size_t)b * P + c) < seq) {
+      if (globaltimer_ns() - t0 > 60ull * 1000000000ull) {
+        atomicOr(flags, kFlagPeerTimeout);
+        return;
+      }
+    }
+  }
+}
+
+void launch_exchange_flags(const Launch& L, const Peers& pe, unsigned long long* local_arrive, int lo, int hi,
+                           uint64_t seq, uint32_t* flags) {
+  Mark mk(L, PH_P2P_FLAGS);
+  k_exchange_flags<<<1, 256, 0, L.stream>>>(pe, local_arrive, lo, hi, (unsigned long long)seq, flags);
   ++*L.launches;
 }
 

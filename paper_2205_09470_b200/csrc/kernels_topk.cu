@@ -811,8 +811,7 @@ template <bool EF>
 __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __restrict__ titems,
                                                            const TopkState* __restrict__ st, int nitems, uint64_t tbase,
                                                            const uint2* __restrict__ wl, const uint2* __restrict__ cl,
-                                                           uint8_t* __restrict__ slots, float* __restrict__ rbase,
-                                                           uint32_t* flags) {
+                                                           Dests dst, float* __restrict__ rbase, uint32_t* flags) {
   __shared__ uint2 sw[kMergeTile], ss[kMergeTile];
   __shared__ uint64_t s_split[2];
   const uint64_t t = tbase + blockIdx.x;
@@ -828,9 +827,12 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   const TopkItem ti = titems[i];
   const TopkState& S = st[i];
   if (S.failed == 2) return;
-  uint8_t* slot = slots + ti.slot_off;
+  const uint64_t so = ti.slot_off;
   if (ti.k == 0) {
-    if (threadIdx.x == 0) write_preamble(slot, M_TOPK, 0u, 1.0f, ti.value_type);
+    if (threadIdx.x == 0) {
+      put_preamble(dst, so, M_TOPK, 0u, 1.0f, ti.value_type);
+      if (dst.n > 1) __threadfence_system();
+    }
     return;
   }
   const uint64_t k = ti.k, W = S.wcount, Ns = k - W;
@@ -846,9 +848,8 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   __syncthreads();
   const int vt = (int)ti.value_type;
   const float s = S.scale;
-  if (d0 == 0 && threadIdx.x == 0) write_preamble(slot, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
-  uint32_t* idx_out = reinterpret_cast<uint32_t*>(slot + 16);
-  uint8_t* val_out = slot + 16 + pad16(4 * k);
+  if (d0 == 0 && threadIdx.x == 0) put_preamble(dst, so, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
+  const uint64_t io = so + 16, vo = so + 16 + pad16(4 * k);   // idx / value section offsets
   float* r = rbase + ti.r_off;
   bool ovf = false;
   const uint32_t x = threadIdx.x;
@@ -869,20 +870,20 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
     }
     const uint64_t o = d0 + pos;
     const float pv = __uint_as_float(e.y);
-    idx_out[o] = e.x;
+    put(dst, io + 4 * o, e.x);
     float dv;
     if (vt == V_F32) {
-      reinterpret_cast<float*>(val_out)[o] = pv;
+      put(dst, vo + 4 * o, pv);
       dv = pv;
     } else if (vt == V_F16) {
       __half h = __float2half_rn(pv);
       const uint16_t hb = __half_as_ushort(h);
       ovf = (hb & 0x7FFFu) == 0x7C00u;
-      reinterpret_cast<uint16_t*>(val_out)[o] = hb;
+      put(dst, vo + 2 * o, hb);
       dv = __half2float(h);
     } else {
       const int q = int8_q(pv, s);
-      val_out[o] = (uint8_t)(q & 0xFF);
+      put(dst, vo + o, (uint8_t)(q & 0xFF));
       dv = __fmul_rn((float)q, s);
     }
     if constexpr (EF) r[e.x] = __fsub_rn(pv, dv);
@@ -890,11 +891,11 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   // zero the padding of the two sections (the tile that ends the item)
   if (d1 == k) {
     const uint64_t ib = 4 * k, ipad = pad16(ib), vb = (vt == V_F32 ? 4 : (vt == V_F16 ? 2 : 1)) * k, vpad = pad16(vb);
-    uint8_t* ip = slot + 16;
-    for (uint64_t z = ib + threadIdx.x; z < ipad; z += blockDim.x) ip[z] = 0;
-    for (uint64_t z = vb + threadIdx.x; z < vpad; z += blockDim.x) val_out[z] = 0;
+    for (uint64_t z = ib + threadIdx.x; z < ipad; z += blockDim.x) put(dst, io + z, (uint8_t)0);
+    for (uint64_t z = vb + threadIdx.x; z < vpad; z += blockDim.x) put(dst, vo + z, (uint8_t)0);
   }
   if (__any_sync(0xFFFFFFFFu, ovf) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagOverflow);
+  if (dst.n > 1) __threadfence_system();   // pushed payload visible system-wide before the flag
 }
 
 // ---------------------------------------------------------------- sparse reduce
@@ -987,7 +988,7 @@ __global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ 
 
 template <bool EF, bool VEC>
 static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
-                            const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags,
+                            const Item* aitems, const float* g, float* r, const Dests& slots, uint32_t* flags,
                             int value_type, uint64_t merge_tiles) {
   const TopkItem* ti = B.items + item0;
   TopkState* st = B.state + item0;
@@ -1046,7 +1047,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
 }
 
 void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
-                 const Item* aitems, const float* g, float* r, uint8_t* slots, uint32_t* flags, int value_type,
+                 const Item* aitems, const float* g, float* r, const Dests& slots, uint32_t* flags, int value_type,
                  uint64_t merge_tiles) {
   if (nitems <= 0) return;
   if (ef && vec) topk_select_all<true, true>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);

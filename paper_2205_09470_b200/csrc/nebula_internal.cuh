@@ -19,7 +19,7 @@ constexpr int kQuadsPerThread = 4;          // 4 x float4 per thread per chunk (
 constexpr int kChunkQuads = kThreads * kQuadsPerThread;
 constexpr uint64_t kChunkElems = (uint64_t)kChunkQuads * 4;   // 4096 elements per chunk
 
-enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u };
+enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u, kFlagPeerTimeout = 4u };
 enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3 };
 enum : int { V_F32 = 0, V_F16 = 1, V_I8 = 2 };
 
@@ -144,6 +144,24 @@ __device__ __forceinline__ void write_preamble(uint8_t* slot, uint32_t method, u
                                                uint32_t aux) {
   uint4 pre = make_uint4(method, count, __float_as_uint(scale), aux);
   *reinterpret_cast<uint4*>(slot) = pre;
+}
+
+// Where a compressor writes its payload: p[0] = this cluster's own slot, p[1..n-1] = the same
+// slot in every peer's (IPC-mapped, NVLink) slot buffer when the exchange is fused into the
+// compress kernels (P2P push).  Offsets are identical on every rank.  Passed by value (kernel
+// parameter space), n = 1 for LOOPBACK and for the NCCL all-gather exchange.
+struct Dests {
+  uint8_t* p[8];
+  int n;
+};
+template <class T>
+__device__ __forceinline__ void put(const Dests& d, uint64_t off, T v) {
+#pragma unroll 1
+  for (int k = 0; k < d.n; ++k) *reinterpret_cast<T*>(d.p[k] + off) = v;
+}
+__device__ __forceinline__ void put_preamble(const Dests& d, uint64_t off, uint32_t method, uint32_t count, float scale,
+                                             uint32_t aux) {
+  put(d, off, make_uint4(method, count, __float_as_uint(scale), aux));
 }
 
 }  // namespace nb

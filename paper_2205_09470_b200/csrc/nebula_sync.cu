@@ -37,6 +37,7 @@ struct BucketInfo {
   uint64_t so[2] = {0, 0};  // byte offset of this bucket's [P][pb] slot block, per layout
   int state = ST_IDLE;
   int method = -1;     // method used by the last compress (after the start-step gate)
+  uint64_t seq = 0;    // compresses so far (P2P push: slot parity = seq & 1, arrival flag value)
 };
 
 struct Table {         // one launch's work list, resident in d_items / d_ritems
@@ -93,6 +94,16 @@ struct nebula_ctx {
 
   ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
   uint64_t launches = 0;
+
+  // exchange transport: 0 LOOPBACK (nothing moves), 1 NCCL in-place all-gather, 2 P2P push (the
+  // compress kernels store every payload into all peers' slots over NVLink; exchange = flags)
+  int xmode = 0;
+  int xopt = 0;                            // NEBULA_OPT_EXCHANGE: 0 auto, 1 NCCL, 2 P2P
+  bool p2p_ok = false;
+  uint64_t slot_span = 0;                  // bytes of one parity half of d_slots
+  uint8_t* peer_slots[NEBULA_MAX_CLUSTERS] = {};            // IPC-mapped d_slots of each cluster
+  unsigned long long* peer_arrive[NEBULA_MAX_CLUSTERS] = {}; // IPC-mapped arrival flags
+  unsigned long long* d_arrive = nullptr;  // [B][P] last seq received from each sender
   std::string err;
 
   // INT8 single-pass on-chip kernel (cooperative grid)
@@ -324,10 +335,107 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_topk_mem);
   cudaFree(ctx->d_bar);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
+  for (int c = 0; c < NEBULA_MAX_CLUSTERS; ++c) {
+    if (c == ctx->me) continue;
+    if (ctx->peer_slots[c]) cudaIpcCloseMemHandle(ctx->peer_slots[c]);
+    if (ctx->peer_arrive[c]) cudaIpcCloseMemHandle(ctx->peer_arrive[c]);
+  }
+  cudaFree(ctx->d_arrive);
   if (ctx->intra) ncclCommDestroy(ctx->intra);
   if (ctx->inter && ctx->inter != ctx->world) ncclCommDestroy(ctx->inter);
   if (ctx->world) ncclCommDestroy(ctx->world);
   delete ctx;
+}
+
+// P2P push setup (collective over the inter-cluster communicator): every cluster shares its
+// device ordinal, a host id and CUDA IPC handles of its slot buffer and arrival flags through
+// ncclAllGather; the push is enabled only if EVERY rank can map every peer (same host,
+// cudaDeviceCanAccessPeer), so all ranks agree on the transport.
+struct P2PInfo {
+  cudaIpcMemHandle_t slots, arrive;
+  int32_t device, ok;
+  uint64_t host;
+};
+
+static uint64_t host_id() {
+  char name[256] = {0};
+  FILE* f = fopen("/proc/sys/kernel/hostname", "r");
+  if (f) {
+    if (!fgets(name, sizeof(name), f)) name[0] = 0;
+    fclose(f);
+  }
+  uint64_t h = 1469598103934665603ull;
+  for (const char* p = name; *p; ++p) h = (h ^ (uint64_t)(unsigned char)*p) * 1099511628211ull;
+  return h;
+}
+
+static nebula_status p2p_setup(nebula_ctx* ctx) {
+  const int P = ctx->P, B = (int)ctx->b.size();
+  CKC(cudaMalloc(&ctx->d_arrive, sizeof(unsigned long long) * (size_t)B * P));
+  CKC(cudaMemset(ctx->d_arrive, 0, sizeof(unsigned long long) * (size_t)B * P));
+  P2PInfo mine{};
+  mine.device = ctx->device;
+  mine.host = host_id();
+  mine.ok = cudaIpcGetMemHandle(&mine.slots, ctx->d_slots) == cudaSuccess &&
+            cudaIpcGetMemHandle(&mine.arrive, ctx->d_arrive) == cudaSuccess;
+  cudaGetLastError();
+  P2PInfo* d_info = nullptr;
+  CKC(cudaMalloc(&d_info, sizeof(P2PInfo) * P));
+  CKC(cudaMemcpy(d_info + ctx->me, &mine, sizeof(P2PInfo), cudaMemcpyHostToDevice));
+  CKN(ncclAllGather(d_info + ctx->me, d_info, sizeof(P2PInfo), ncclUint8, ctx->inter, ctx->stream));
+  CKC(cudaStreamSynchronize(ctx->stream));
+  std::vector<P2PInfo> all(P);
+  CKC(cudaMemcpy(all.data(), d_info, sizeof(P2PInfo) * P, cudaMemcpyDeviceToHost));
+  int ok = 1;
+  for (int c = 0; c < P; ++c) {
+    if (c == ctx->me) continue;
+    int can = 0;
+    if (!all[c].ok || all[c].host != mine.host || all[c].device == ctx->device ||
+        cudaDeviceCanAccessPeer(&can, ctx->device, all[c].device) != cudaSuccess || !can)
+      ok = 0;
+  }
+  cudaGetLastError();
+  // agree: P2P only if every rank can reach every peer
+  int32_t* d_ok = reinterpret_cast<int32_t*>(d_info);
+  CKC(cudaMemcpy(d_ok, &ok, sizeof(int32_t), cudaMemcpyHostToDevice));
+  CKN(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, ctx->inter, ctx->stream));
+  CKC(cudaStreamSynchronize(ctx->stream));
+  CKC(cudaMemcpy(&ok, d_ok, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  cudaFree(d_info);
+  if (!ok) return NEBULA_OK;   // NCCL all-gather transport
+  for (int c = 0; c < P; ++c) {
+    if (c == ctx->me) {
+      ctx->peer_slots[c] = ctx->d_slots;
+      ctx->peer_arrive[c] = ctx->d_arrive;
+      continue;
+    }
+    void* ps = nullptr;
+    void* pa = nullptr;
+    CKC(cudaIpcOpenMemHandle(&ps, all[c].slots, cudaIpcMemLazyEnablePeerAccess));
+    CKC(cudaIpcOpenMemHandle(&pa, all[c].arrive, cudaIpcMemLazyEnablePeerAccess));
+    ctx->peer_slots[c] = static_cast<uint8_t*>(ps);
+    ctx->peer_arrive[c] = static_cast<unsigned long long*>(pa);
+  }
+  ctx->p2p_ok = true;
+  return NEBULA_OK;
+}
+
+// Slot buffer of a bucket's current exchange (P2P push double-buffers by seq parity).
+static uint8_t* slots_of(const nebula_ctx* ctx, const BucketInfo& bk) {
+  return ctx->d_slots + (ctx->xmode == 2 ? (bk.seq & 1) * ctx->slot_span : 0);
+}
+
+// Payload destinations of a compress: own slot buffer, plus every peer's for the P2P push.
+static Dests dests_of(const nebula_ctx* ctx, const BucketInfo& bk) {
+  Dests d{};
+  d.p[0] = slots_of(ctx, bk);
+  d.n = 1;
+  if (ctx->xmode == 2) {
+    const uint64_t half = (bk.seq & 1) * ctx->slot_span;
+    for (int c = 0; c < ctx->P; ++c)
+      if (c != ctx->me) d.p[d.n++] = ctx->peer_slots[c] + half;
+  }
+  return d;
 }
 
 extern "C" {
@@ -421,10 +529,12 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
 
     size_t rbytes = std::max<uint64_t>(16, (uint64_t)ctx->Ploc * ctx->total_cn * sizeof(float));
     if (cudaMalloc(&ctx->d_resid, rbytes) != cudaSuccess) { ctx->err = "residual allocation failed"; return bail(NEBULA_ERR_OOM); }
-    if (cudaMalloc(&ctx->d_slots, std::max<uint64_t>(16, ctx->total_slots)) != cudaSuccess) { ctx->err = "payload allocation failed"; return bail(NEBULA_ERR_OOM); }
+    ctx->slot_span = pad16(std::max<uint64_t>(16, ctx->total_slots));
+    const int halves = (!ctx->loopback && ctx->P > 1) ? 2 : 1;   // double buffer for the P2P push
+    if (cudaMalloc(&ctx->d_slots, halves * ctx->slot_span) != cudaSuccess) { ctx->err = "payload allocation failed"; return bail(NEBULA_ERR_OOM); }
     if (cudaMalloc(&ctx->d_flags, 16) != cudaSuccess) { ctx->err = "flag allocation failed"; return bail(NEBULA_ERR_OOM); }
     if (cudaMalloc(&ctx->d_scratch, sizeof(uint32_t) * ctx->Ploc * num_buckets) != cudaSuccess) { ctx->err = "scratch allocation failed"; return bail(NEBULA_ERR_OOM); }
-    if (cudaMemset(ctx->d_resid, 0, rbytes) != cudaSuccess || cudaMemset(ctx->d_slots, 0, std::max<uint64_t>(16, ctx->total_slots)) != cudaSuccess ||
+    if (cudaMemset(ctx->d_resid, 0, rbytes) != cudaSuccess || cudaMemset(ctx->d_slots, 0, halves * ctx->slot_span) != cudaSuccess ||
         cudaMemset(ctx->d_flags, 0, 16) != cudaSuccess) { ctx->err = "memset failed"; return bail(NEBULA_ERR_CUDA); }
     if (ctx->G > 1) {
       if (cudaMalloc(&ctx->d_shard_in, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess ||
@@ -461,6 +571,14 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
         if (r != ncclSuccess) { ctx->err = std::string("ncclCommSplit: ") + ncclGetErrorString(r); return bail(NEBULA_ERR_NCCL); }
       }
     }
+    if (!ctx->loopback) {
+      ctx->xmode = 1;
+      if (ctx->P > 1) {
+        nebula_status ps = p2p_setup(ctx);
+        if (ps != NEBULA_OK) return bail(ps);
+        if (ctx->p2p_ok) ctx->xmode = 2;
+      }
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
   }
   *out = ctx;
@@ -485,6 +603,11 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   const int lay = layout_of(ctx, method);
   const Table& T = ctx->ctab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
   const Launch L = launch_of(ctx);
+  for (int i = lo + 1; i < hi; ++i)
+    if ((ctx->b[i].seq & 1) != (ctx->b[lo].seq & 1))
+      return fail(ctx, NEBULA_ERR_STATE, "ALL-bucket call over buckets at different exchange parities");
+  for (int i = lo; i < hi; ++i) ctx->b[i].seq += 1;
+  const Dests dst = dests_of(ctx, ctx->b[lo]);
 
   const float* gbase = dev_grad;
   if (ctx->G > 1) {  // intra-cluster mean of the G GPUs' buckets -> this GPU's shard (R20)
@@ -504,10 +627,10 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
 
   switch (method) {
     case M_IDENTITY:
-      launch_identity(L, vec, items, T.count, T.chunks, gbase, ctx->d_slots, ctx->d_flags);
+      launch_identity(L, vec, items, T.count, T.chunks, gbase, dst, ctx->d_flags);
       break;
     case M_FP16:
-      launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_flags);
+      launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_flags);
       break;
     case M_INT8: {
       // zero the max-abs words of the items in this call (sidx = c * B + b)
@@ -526,19 +649,19 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
         else if (ctx->int8_kernel == 0) onchip = elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20);
       }
       if (onchip) {
-        launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch, ctx->d_flags,
+        launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
                            ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem,
                            ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : 2 /* auto: park p, lag 1 (fastest measured) */);
       } else {
         launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-        launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_slots, ctx->d_scratch,
+        launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
                           ctx->d_flags);
       }
       break;
     }
     case M_TOPK: {
       const int item0 = bucket == NEBULA_ALL_BUCKETS ? 0 : bucket * ctx->Ploc;
-      launch_topk(L, ef, vec, ctx->tk, item0, T.count, T.chunks, items, gbase, ctx->d_resid, ctx->d_slots,
+      launch_topk(L, ef, vec, ctx->tk, item0, T.count, T.chunks, items, gbase, ctx->d_resid, dst,
                   ctx->d_flags, ctx->codec.topk_values, ctx->tk_mtiles[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket]);
       break;
     }
@@ -558,7 +681,15 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
   for (int i = lo; i < hi; ++i)
     if (ctx->b[i].state != ST_COMPRESSED) return fail(ctx, NEBULA_ERR_STATE, "exchange before compress");
   DevGuard dg(ctx->device);
-  if (!ctx->loopback && ctx->P > 1) {
+  if (ctx->xmode == 2) {   // payloads already pushed by the compress kernels: signal + wait
+    const Launch L = launch_of(ctx);
+    Peers pe{};
+    for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
+    pe.n = ctx->P;
+    pe.me = ctx->me;
+    launch_exchange_flags(L, pe, ctx->d_arrive, lo, hi, ctx->b[lo].seq, ctx->d_flags);
+    CKC(cudaGetLastError());
+  } else if (!ctx->loopback && ctx->P > 1) {
     const Launch L = launch_of(ctx);
     Mark mk(L, PH_NCCL_EXCHANGE);
     CKN(ncclGroupStart());
@@ -566,7 +697,7 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
       const BucketInfo& bk = ctx->b[i];
       // in place: rank c's contribution already sits in slot c (ncclAllGather in-place rule)
       const int lay = layout_of(ctx, bk.method);
-      uint8_t* base = ctx->d_slots + bk.so[lay];
+      uint8_t* base = slots_of(ctx, bk) + bk.so[lay];
       CKN(ncclAllGather(base + (uint64_t)ctx->me * bk.pb[lay], base, bk.pb[lay], ncclUint8, ctx->inter, ctx->stream));
     }
     CKN(ncclGroupEnd());
@@ -604,11 +735,11 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
       zb = obase;
       zc = elems_of(ctx, lo, hi);
     }
-    launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, ctx->d_slots,
+    launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, slots_of(ctx, ctx->b[lo]),
                        ctx->tk.start, obase, zb, zc);
   }
   else
-    launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, ctx->d_slots, obase);
+    launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, slots_of(ctx, ctx->b[lo]), obase);
   CKC(cudaGetLastError());
   if (ctx->G > 1) {
     Mark mk(L, PH_NCCL_AG);
@@ -662,6 +793,7 @@ nebula_status nebula_check(nebula_ctx* ctx) {
     ncclCommGetAsyncError(ctx->world, &async_err);
     if (async_err != ncclSuccess) return fail(ctx, NEBULA_ERR_NCCL, ncclGetErrorString(async_err));
   }
+  if (f & kFlagPeerTimeout) return fail(ctx, NEBULA_ERR_NCCL, "P2P exchange: a peer's payload did not arrive (timeout)");
   if (f & kFlagNonfinite) return fail(ctx, NEBULA_ERR_NONFINITE, "non-finite element in g + r");
   if (f & kFlagOverflow) return fail(ctx, NEBULA_ERR_OVERFLOW, "fp16 overflow (|p| >= 65520)");
   return NEBULA_OK;
@@ -685,7 +817,7 @@ nebula_status nebula_payload_copy(nebula_ctx* ctx, int32_t bucket, int32_t slot,
   CKC(cudaStreamSynchronize(ctx->stream));
   const BucketInfo& bk = ctx->b[bucket];
   const int lay = layout_of(ctx, bk.method >= 0 ? bk.method : ctx->codec.method);
-  CKC(cudaMemcpy(host_dst, ctx->d_slots + bk.so[lay] + (uint64_t)slot * bk.pb[lay], nbytes, cudaMemcpyDeviceToHost));
+  CKC(cudaMemcpy(host_dst, slots_of(ctx, bk) + bk.so[lay] + (uint64_t)slot * bk.pb[lay], nbytes, cudaMemcpyDeviceToHost));
   return NEBULA_OK;
 }
 
@@ -715,8 +847,20 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->int8_kernel = (int)value;
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_EXCHANGE) {
+    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exchange option must be 0, 1 or 2");
+    if (ctx->loopback) return NEBULA_OK;   // nothing moves
+    if (value == 2 && !ctx->p2p_ok) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "P2P push not available (peers not mappable)");
+    for (const auto& bk : ctx->b)
+      if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
+    ctx->xopt = (int)value;
+    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : 2;
+    return NEBULA_OK;
+  }
   return fail(ctx, NEBULA_ERR_INVALID_ARG, "unknown option");
 }
+
+int32_t nebula_exchange_mode(const nebula_ctx* ctx) { return ctx ? ctx->xmode : -1; }
 
 nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
@@ -755,7 +899,8 @@ const char* nebula_phase_name(uint32_t phase) {
       "identity_pack", "fp16_ef_pack", "int8_ef_absmax", "int8_ef_quant_pack", "topk_ef_sample",
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
-      "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack"};
+      "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
+      "p2p_exchange_flags"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

@@ -46,12 +46,20 @@ def main():
     total = sum(sizes)
     cases = [(O.INT8, 0, "two-pass"), (O.INT8, 0, "onchip"), (O.FP16, 0, None), (O.IDENTITY, 0, None),
              (O.TOPK, O.VAL_F32, None), (O.TOPK, O.VAL_I8, None), (O.TOPK, O.VAL_F16, None)]
+    modes_seen = set()
     for method, vt, kern in cases:
-        for per_bucket in (False, True):
+        for per_bucket, xch in ((False, "p2p"), (True, "p2p"), (False, "nccl")):
             ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
                                                 topk_values=vt, topk_density=0.05)
             if kern:
                 ctx.set_int8_kernel(kern)
+            if P > 1:
+                try:
+                    ctx.set_exchange(xch)
+                except nb.NebulaError:
+                    assert xch == "p2p"
+                    ctx.set_exchange("nccl")
+            modes_seen.add(ctx.exchange_mode())
             codec = O.Codec(method=method, topk_values=vt, topk_density=0.05)
             m = [s // G for s in sizes]
             rs = [[[np.zeros(mb, np.float32) for mb in m] for _ in range(G)] for _ in range(P)]
@@ -109,7 +117,8 @@ def main():
             ctx.destroy()
     dist.barrier()
     if rank == 0:
-        print(f"DIST OK world={world} P={P} G={G} cases={len(cases)}x2 steps={args.steps}", flush=True)
+        print(f"DIST OK world={world} P={P} G={G} cases={len(cases)}x3 steps={args.steps} "
+              f"exchange={sorted(modes_seen)}", flush=True)
     dist.destroy_process_group()
 
 
