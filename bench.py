@@ -288,7 +288,7 @@ def main():
     if world == 1:
         ctx = nb.SyncContext(sizes, method, num_clusters=P, transport=nb.LOOPBACK, device=local, **common)
     else:
-        ctx = nb.init_process_group_context(sizes, device=local, **common)
+        ctx = nb.init_process_group_context(sizes, device=local, method=method, **common)
     if method == 2:
         ctx.set_int8_kernel(args.int8_kernel)
     if world > 1 and args.exchange != "auto":
