@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
       const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      uint2 packed = make_uint2(0u, 0u);
       if (q < n4) {
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
         uint16_t h0, h1, h2, h3;
@@ -137,12 +138,13 @@ __global__ void __launch_bounds__(kThreads) k_fp16(const Item* __restrict__ item
         d.y = fp16_one(p.y, h1, bad, ovf);
         d.z = fp16_one(p.z, h2, bad, ovf);
         d.w = fp16_one(p.w, h3, bad, ovf);
-        uint2 packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
-        put(dst, bo + 8 * q, packed);
+        packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
+        *reinterpret_cast<uint2*>(dst.p[0] + bo + 8 * q) = packed;
         if constexpr (EF)
           st4(r + 4 * q, make_float4(__fsub_rn(p.x, d.x), __fsub_rn(p.y, d.y), __fsub_rn(p.z, d.z),
                                      __fsub_rn(p.w, d.w)));
       }
+      push_u64(dst, bo + 8 * q, packed, q < n4);   // q % 2 == lane % 2: pairs are 16-B aligned
     }
     if (j == n4 / kChunkQuads) {
       if (threadIdx.x < (it.n & 3)) {
@@ -245,14 +247,17 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
       const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      uint32_t wv = 0u;
       if (q < n4) {
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
         int q0 = int8_q(p.x, s), q1 = int8_q(p.y, s), q2 = int8_q(p.z, s), q3 = int8_q(p.w, s);
-        put(dst, bo + 4 * q, pack_i8x4(q0, q1, q2, q3));
+        wv = pack_i8x4(q0, q1, q2, q3);
+        *reinterpret_cast<uint32_t*>(dst.p[0] + bo + 4 * q) = wv;
         if constexpr (EF)
           st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)q0, s)), __fsub_rn(p.y, __fmul_rn((float)q1, s)),
                                      __fsub_rn(p.z, __fmul_rn((float)q2, s)), __fsub_rn(p.w, __fmul_rn((float)q3, s))));
       }
+      push_u32(dst, bo + 4 * q, wv, q < n4);   // q % 4 == lane % 4: groups are 16-B aligned
     }
     if (j == n4 / kChunkQuads) {
       if (threadIdx.x < (it.n & 3)) {
@@ -396,7 +401,7 @@ struct Slice {
   uint64_t q0, q1;
 };
 __device__ __forceinline__ Slice slice_of(uint64_t n4, unsigned G) {
-  const uint64_t per = (n4 + G - 1) / G;
+  const uint64_t per = ((n4 + G - 1) / G + 3) & ~uint64_t(3);   // 4-quad aligned (16-B pushes)
   const uint64_t q0 = min(n4, (uint64_t)blockIdx.x * per);
   return Slice{q0, min(n4, q0 + per)};
 }
@@ -449,7 +454,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     const uint64_t lenA = sa.q1 - sa.q0, lenB = doB ? sb.q1 - sb.q0 : 0;
     const uint64_t len = max(lenA, lenB);
     uint32_t m = 0;
-    for (uint64_t kb = threadIdx.x; kb < len; kb += (uint64_t)kFusedThreads * kFusedUnroll) {
+    // block-uniform trip count (the lane-group pushes below use full-warp shuffles)
+    for (uint64_t kb0 = 0; kb0 < len; kb0 += (uint64_t)kFusedThreads * kFusedUnroll) {
+      const uint64_t kb = kb0 + threadIdx.x;
       float4 ga[kFusedUnroll], ra[kFusedUnroll], pb[kFusedUnroll];
 #pragma unroll
       for (int u = 0; u < kFusedUnroll; ++u) {
@@ -482,20 +489,20 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
           if constexpr (EF && PARK) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t + LAG)
         }
+        uint32_t w = 0u;
         if (k < lenB) {
           const uint64_t q = sb.q0 + k;
           const float4 p = pb[u];
           const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
-          const uint32_t w = pack_i8x4(a0, a1, a2, a3);
+          w = pack_i8x4(a0, a1, a2, a3);
           st_u32_hint(bodyB + q, w, pol_stream);
-#pragma unroll 1
-          for (int d = 1; d < dst.n; ++d) reinterpret_cast<uint32_t*>(dst.p[d] + boB)[q] = w;   // NVLink push
           if constexpr (EF)
             st4_hint(rB + 4 * q,
                      make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
                                  __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
                      pol_stream);
         }
+        push_u32(dst, boB + 4 * (sb.q0 + k), w, k < lenB);   // NVLink push, 16 B per lane group
       }
     }
     // ---- tails (n % 4 elements after the last quad) on the last CTA

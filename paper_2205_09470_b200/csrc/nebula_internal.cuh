@@ -159,6 +159,43 @@ __device__ __forceinline__ void put(const Dests& d, uint64_t off, T v) {
 #pragma unroll 1
   for (int k = 0; k < d.n; ++k) *reinterpret_cast<T*>(d.p[k] + off) = v;
 }
+// Push per-lane payload words to the PEERS (d.p[1..]) as 16-byte stores (NVLink moves wide
+// stores far better than 4-byte ones).  Lanes holding consecutive words form groups — 4 lanes
+// of u32 words or 2 lanes of u64 words — whose first lane is 16-byte aligned (callers keep
+// word index % group == lane % group); full groups are written by their first lane, partial
+// groups lane by lane.  Must be called by all 32 lanes (valid marks the lanes with a word).
+__device__ __forceinline__ void push_u32(const Dests& d, uint64_t off, uint32_t w, bool valid) {
+  if (d.n < 2) return;
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t w1 = __shfl_down_sync(0xFFFFFFFFu, w, 1), w2 = __shfl_down_sync(0xFFFFFFFFu, w, 2),
+                 w3 = __shfl_down_sync(0xFFFFFFFFu, w, 3);
+  const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+  const bool full = ((vm >> (lane & ~3u)) & 0xFu) == 0xFu;
+  if (full) {
+    if ((lane & 3u) == 0)
+#pragma unroll 1
+      for (int k = 1; k < d.n; ++k) *reinterpret_cast<uint4*>(d.p[k] + off) = make_uint4(w, w1, w2, w3);
+  } else if (valid) {
+#pragma unroll 1
+    for (int k = 1; k < d.n; ++k) *reinterpret_cast<uint32_t*>(d.p[k] + off) = w;
+  }
+}
+__device__ __forceinline__ void push_u64(const Dests& d, uint64_t off, uint2 w, bool valid) {
+  if (d.n < 2) return;
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t x1 = __shfl_down_sync(0xFFFFFFFFu, w.x, 1), y1 = __shfl_down_sync(0xFFFFFFFFu, w.y, 1);
+  const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+  const bool full = ((vm >> (lane & ~1u)) & 0x3u) == 0x3u;
+  if (full) {
+    if ((lane & 1u) == 0)
+#pragma unroll 1
+      for (int k = 1; k < d.n; ++k) *reinterpret_cast<uint4*>(d.p[k] + off) = make_uint4(w.x, w.y, x1, y1);
+  } else if (valid) {
+#pragma unroll 1
+    for (int k = 1; k < d.n; ++k) *reinterpret_cast<uint2*>(d.p[k] + off) = w;
+  }
+}
+
 __device__ __forceinline__ void put_preamble(const Dests& d, uint64_t off, uint32_t method, uint32_t count, float scale,
                                              uint32_t aux) {
   put(d, off, make_uint4(method, count, __float_as_uint(scale), aux));
