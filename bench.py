@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--bucket-mib", type=float, default=25.0)
     ap.add_argument("--clusters", type=int, default=2, help="simulated clusters at N=1 (LOOPBACK)")
     ap.add_argument("--no-ef", action="store_true")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
                                                               "fused-park-lag1", "fused-recompute-lag1"])
     ap.add_argument("--no-e2e", action="store_true")

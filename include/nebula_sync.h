@@ -189,14 +189,16 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 #define NEBULA_OPT_INT8_KERNEL 1
 /*   NEBULA_OPT_EXCHANGE (NCCL transport): 0 auto (default), 1 ncclAllGather of the payloads
  *   after the compress, 2 P2P push: the compress kernels store every payload word into the
- *   same slot of every peer's (CUDA-IPC-mapped) slot buffer over NVLink while they compute, so
- *   the transfer overlaps the codec; exchange then only exchanges per-bucket arrival flags.
- *   Slots are double-buffered by step parity.  Auto = 2 when every rank can map every peer
- *   (decided collectively at init), else 1.  Only between steps. */
+ *   same slot of every peer's (CUDA-IPC-mapped) slot buffer over NVLink while they compute,
+ *   3 P2P pull: compress writes locally, the decompress-reduce kernel loads each peer's slot
+ *   directly from the peer over NVLink.  In 2 and 3 the exchange is a per-bucket flag
+ *   handshake (release/acquire at system scope) and slots are double-buffered by step parity.
+ *   Auto = 3 when every rank can map every peer (decided collectively at init), else 1.
+ *   Only between steps. */
 #define NEBULA_OPT_EXCHANGE 2
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
-/* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push; -1 for NULL. */
+/* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */
 int32_t nebula_exchange_mode(const nebula_ctx* ctx);
 
 /* Per-kernel device timers.  When enabled, every kernel / collective the context enqueues is

@@ -29,7 +29,7 @@ NCCL, LOOPBACK = 0, 1
 ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
 OPT_EXCHANGE = 2
-EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push"}
+EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "OOM", 4: "CUDA", 5: "NCCL",
@@ -274,8 +274,8 @@ class SyncContext:
                                           "fused-park-lag1": 4, "fused-recompute-lag1": 5}[which])
 
     def set_exchange(self, which: str):
-        """'auto' | 'nccl' | 'p2p' (NEBULA_OPT_EXCHANGE; between steps only)."""
-        self.set_option(OPT_EXCHANGE, {"auto": 0, "nccl": 1, "p2p": 2}[which])
+        """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""
+        self.set_option(OPT_EXCHANGE, {"auto": 0, "nccl": 1, "push": 2, "pull": 3, "p2p": 3}[which])
 
     def exchange_mode(self) -> str:
         return EXCHANGE_MODES[self._L.nebula_exchange_mode(self._h)]

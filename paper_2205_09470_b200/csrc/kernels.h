@@ -64,7 +64,7 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
                         uint32_t* done_words, int grid, size_t smem, int variant);
 // Dense decompress + tree-average over P slots.
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
-                         uint64_t chunks, const uint8_t* slots, float* out);
+                         uint64_t chunks, const Dests& slots, float* out);
 
 // ---- P2P push exchange (kernels_dense.cu) ----
 struct Peers {
@@ -136,7 +136,7 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
 // entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).
 // zero_begin/zero_count: the output range of the call (filled with +0.0 first).
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
-                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out,
+                        uint64_t entries, uint64_t tiles, const Dests& slots, uint32_t* start, float* out,
                         float* zero_begin, uint64_t zero_count);
 
 }  // namespace nb

@@ -307,9 +307,11 @@ __device__ __forceinline__ float div_p(float x) {
   else return __fdiv_rn(x, (float)P);
 }
 
+// src.p[c] = the slot buffer holding cluster c's payload: the local buffer for LOOPBACK / NCCL
+// / push, cluster c's own (IPC-mapped) buffer for the P2P pull — then slot c is read over NVLink.
 template <int METHOD, int P, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restrict__ items, int nitems, uint64_t chunks,
-                                                           const uint8_t* __restrict__ slots, float* __restrict__ obase) {
+                                                           Dests src, float* __restrict__ obase) {
   constexpr int UG = P <= 2 ? 4 : (P <= 4 ? 2 : 1);   // quads in flight per thread (registers: UG*P float4)
   int hint = 0, cur = -1;
   RItem it{};
@@ -322,10 +324,10 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       cur = i;
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(slots + it.slot_off + k * it.pb + 8) : 1.0f;
+        sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
     }
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
-    const uint8_t* s0 = slots + it.slot_off;
+    const uint64_t so = it.slot_off;
     float* out = obase + it.out_off;
 #pragma unroll
     for (int u0 = 0; u0 < kQuadsPerThread; u0 += UG) {
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
         const uint64_t q = j * kChunkQuads + (uint64_t)(u0 + u) * kThreads + threadIdx.x;
         if (q < n4) {
 #pragma unroll
-          for (int k = 0; k < P; ++k) d[u][k] = decode_quad<METHOD, P>(s0 + k * it.pb, q, sc[k]);
+          for (int k = 0; k < P; ++k) d[u][k] = decode_quad<METHOD, P>(src.p[k] + so + k * it.pb, q, sc[k]);
         }
       }
 #pragma unroll
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       const uint64_t e = n4 * 4 + threadIdx.x;
       float v[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(s0 + k * it.pb, e, sc[k]);
+      for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(src.p[k] + so + k * it.pb, e, sc[k]);
       out[e] = div_p<P>(tree_sum<0, P>(v));
     }
   }
@@ -599,14 +601,14 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
 }
 
 template <int METHOD, int P>
-static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const uint8_t* slots,
+static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const Dests& slots,
                      float* out) {
   if (vec) k_reduce_dense<METHOD, P, true><<<GRID((k_reduce_dense<METHOD, P, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
   else k_reduce_dense<METHOD, P, false><<<GRID((k_reduce_dense<METHOD, P, false>)), kThreads, 0, L.stream>>>(items, nitems, chunks, slots, out);
 }
 template <int METHOD>
 static void reduce_m(const Launch& L, int P, bool vec, const RItem* items, int nitems, uint64_t chunks,
-                     const uint8_t* slots, float* out) {
+                     const Dests& slots, float* out) {
   switch (P) {
     case 1: reduce_p<METHOD, 1>(L, vec, items, nitems, chunks, slots, out); break;
     case 2: reduce_p<METHOD, 2>(L, vec, items, nitems, chunks, slots, out); break;
@@ -619,7 +621,7 @@ static void reduce_m(const Launch& L, int P, bool vec, const RItem* items, int n
   }
 }
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems, uint64_t chunks,
-                         const uint8_t* slots, float* out) {
+                         const Dests& slots, float* out) {
   if (!chunks) return;
   Mark mk(L, PH_REDUCE_DENSE);
   if (method == M_IDENTITY) reduce_m<M_IDENTITY>(L, P, vec, items, nitems, chunks, slots, out);

@@ -912,7 +912,7 @@ __device__ __forceinline__ int find_by(const RItem* items, int nitems, uint64_t 
 // start[c][t] = first entry of cluster c's ascending idx list with idx >= t * kRedTile,
 // t = 0..ntiles (one thread per entry e in [0, k]; each tile's start written exactly once)
 __global__ void k_topk_offsets(const RItem* __restrict__ items, int nitems, uint64_t total,
-                               const uint8_t* __restrict__ slots, uint32_t* __restrict__ start) {
+                               Dests src, uint32_t* __restrict__ start) {
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (g >= total) return;
@@ -920,7 +920,7 @@ __global__ void k_topk_offsets(const RItem* __restrict__ items, int nitems, uint
   const RItem it = items[i];
   const uint64_t e = g - it.e0;  // 0..k
   const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
-  const uint32_t* idx = reinterpret_cast<const uint32_t*>(slots + it.slot_off + (uint64_t)c * it.pb + 16);
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(src.p[c] + it.slot_off + (uint64_t)c * it.pb + 16);
   uint32_t* s = start + it.sbase + (uint64_t)c * (ntiles + 1);
   const int64_t cur = e < it.k ? (int64_t)(idx[e] / kRedTile) : (int64_t)ntiles;
   const int64_t prev = e == 0 ? -1 : (int64_t)(idx[e - 1] / kRedTile);
@@ -946,7 +946,7 @@ __device__ __forceinline__ float topk_decode(const uint8_t* val, uint64_t e, int
 
 template <int P>
 __global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ items, int nitems, uint64_t total,
-                                                      const uint8_t* __restrict__ slots,
+                                                      Dests src,
                                                       const uint32_t* __restrict__ start, float* __restrict__ obase,
                                                       int vt) {
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -958,13 +958,13 @@ __global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ 
   if (e >= it.k) return;
   const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
   const uint64_t voff = 16 + pad16(4 * it.k);
-  const uint8_t* sc = slots + it.slot_off + (uint64_t)c * it.pb;
+  const uint8_t* sc = src.p[c] + it.slot_off + (uint64_t)c * it.pb;
   const uint32_t x = reinterpret_cast<const uint32_t*>(sc + 16)[e];
   const uint32_t t = x / kRedTile;
   float v[P];
 #pragma unroll
   for (int c2 = 0; c2 < P; ++c2) {
-    const uint8_t* s2 = slots + it.slot_off + (uint64_t)c2 * it.pb;
+    const uint8_t* s2 = src.p[c2] + it.slot_off + (uint64_t)c2 * it.pb;
     const float scale = *reinterpret_cast<const float*>(s2 + 8);
     if (c2 == c) {
       v[c2] = topk_decode(s2 + voff, e, vt, scale);
@@ -1057,14 +1057,14 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
 }
 
 template <int P>
-static void scatter_p(const Launch& L, int vt, const RItem* items, int nitems, uint64_t entries, const uint8_t* slots,
+static void scatter_p(const Launch& L, int vt, const RItem* items, int nitems, uint64_t entries, const Dests& slots,
                       const uint32_t* start, float* out) {
   dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
   k_topk_scatter<P><<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start, out, vt);
 }
 
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
-                        uint64_t entries, uint64_t tiles, const uint8_t* slots, uint32_t* start, float* out,
+                        uint64_t entries, uint64_t tiles, const Dests& slots, uint32_t* start, float* out,
                         float* zero_begin, uint64_t zero_count) {
   (void)vec; (void)tiles;
   {

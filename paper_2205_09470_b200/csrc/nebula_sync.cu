@@ -96,7 +96,8 @@ struct nebula_ctx {
   uint64_t launches = 0;
 
   // exchange transport: 0 LOOPBACK (nothing moves), 1 NCCL in-place all-gather, 2 P2P push (the
-  // compress kernels store every payload into all peers' slots over NVLink; exchange = flags)
+  // compress kernels store every payload into all peers' slots over NVLink; exchange = flags),
+  // 3 P2P pull (exchange = flags; the reducer reads every peer's own slot over NVLink)
   int xmode = 0;
   int xopt = 0;                            // NEBULA_OPT_EXCHANGE: 0 auto, 1 NCCL, 2 P2P
   bool p2p_ok = false;
@@ -420,9 +421,9 @@ static nebula_status p2p_setup(nebula_ctx* ctx) {
   return NEBULA_OK;
 }
 
-// Slot buffer of a bucket's current exchange (P2P push double-buffers by seq parity).
+// Slot buffer of a bucket's current exchange (the P2P modes double-buffer by seq parity).
 static uint8_t* slots_of(const nebula_ctx* ctx, const BucketInfo& bk) {
-  return ctx->d_slots + (ctx->xmode == 2 ? (bk.seq & 1) * ctx->slot_span : 0);
+  return ctx->d_slots + (ctx->xmode >= 2 ? (bk.seq & 1) * ctx->slot_span : 0);
 }
 
 // Payload destinations of a compress: own slot buffer, plus every peer's for the P2P push.
@@ -435,6 +436,16 @@ static Dests dests_of(const nebula_ctx* ctx, const BucketInfo& bk) {
     for (int c = 0; c < ctx->P; ++c)
       if (c != ctx->me) d.p[d.n++] = ctx->peer_slots[c] + half;
   }
+  return d;
+}
+
+// Where the reducer finds cluster c's payload: the local slot buffer, or (P2P pull) cluster
+// c's own buffer through its IPC mapping.
+static Dests sources_of(const nebula_ctx* ctx, const BucketInfo& bk) {
+  Dests d{};
+  d.n = ctx->P;
+  for (int c = 0; c < ctx->P; ++c)
+    d.p[c] = ctx->xmode == 3 ? ctx->peer_slots[c] + (bk.seq & 1) * ctx->slot_span : slots_of(ctx, bk);
   return d;
 }
 
@@ -576,7 +587,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       if (ctx->P > 1) {
         nebula_status ps = p2p_setup(ctx);
         if (ps != NEBULA_OK) return bail(ps);
-        if (ctx->p2p_ok) ctx->xmode = 2;
+        if (ctx->p2p_ok) ctx->xmode = 3;   // auto: P2P pull (NVLink loads outrun SM-issued stores)
       }
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
@@ -681,7 +692,7 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
   for (int i = lo; i < hi; ++i)
     if (ctx->b[i].state != ST_COMPRESSED) return fail(ctx, NEBULA_ERR_STATE, "exchange before compress");
   DevGuard dg(ctx->device);
-  if (ctx->xmode == 2) {   // payloads already pushed by the compress kernels: signal + wait
+  if (ctx->xmode >= 2) {   // push: payloads already in our slots; pull: peers' own slots ready
     const Launch L = launch_of(ctx);
     Peers pe{};
     for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
@@ -735,11 +746,11 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
       zb = obase;
       zc = elems_of(ctx, lo, hi);
     }
-    launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, slots_of(ctx, ctx->b[lo]),
+    launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, sources_of(ctx, ctx->b[lo]),
                        ctx->tk.start, obase, zb, zc);
   }
   else
-    launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, slots_of(ctx, ctx->b[lo]), obase);
+    launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, sources_of(ctx, ctx->b[lo]), obase);
   CKC(cudaGetLastError());
   if (ctx->G > 1) {
     Mark mk(L, PH_NCCL_AG);
@@ -848,13 +859,13 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_EXCHANGE) {
-    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exchange option must be 0, 1 or 2");
+    if (value < 0 || value > 3) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exchange option must be in [0, 3]");
     if (ctx->loopback) return NEBULA_OK;   // nothing moves
-    if (value == 2 && !ctx->p2p_ok) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "P2P push not available (peers not mappable)");
+    if (value >= 2 && !ctx->p2p_ok) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "P2P not available (peers not mappable)");
     for (const auto& bk : ctx->b)
       if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
     ctx->xopt = (int)value;
-    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : 2;
+    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? 3 : (int)value);
     return NEBULA_OK;
   }
   return fail(ctx, NEBULA_ERR_INVALID_ARG, "unknown option");

@@ -48,7 +48,7 @@ def main():
              (O.TOPK, O.VAL_F32, None), (O.TOPK, O.VAL_I8, None), (O.TOPK, O.VAL_F16, None)]
     modes_seen = set()
     for method, vt, kern in cases:
-        for per_bucket, xch in ((False, "p2p"), (True, "p2p"), (False, "nccl")):
+        for per_bucket, xch in ((False, "pull"), (True, "pull"), (False, "push"), (True, "push"), (False, "nccl")):
             ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
                                                 topk_values=vt, topk_density=0.05)
             if kern:
@@ -57,7 +57,7 @@ def main():
                 try:
                     ctx.set_exchange(xch)
                 except nb.NebulaError:
-                    assert xch == "p2p"
+                    assert xch in ("pull", "push")
                     ctx.set_exchange("nccl")
             modes_seen.add(ctx.exchange_mode())
             codec = O.Codec(method=method, topk_values=vt, topk_density=0.05)
@@ -117,7 +117,7 @@ def main():
             ctx.destroy()
     dist.barrier()
     if rank == 0:
-        print(f"DIST OK world={world} P={P} G={G} cases={len(cases)}x3 steps={args.steps} "
+        print(f"DIST OK world={world} P={P} G={G} cases={len(cases)}x5 steps={args.steps} "
               f"exchange={sorted(modes_seen)}", flush=True)
     dist.destroy_process_group()
 
