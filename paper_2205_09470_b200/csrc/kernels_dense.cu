@@ -274,29 +274,27 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
 }
 
 // ----------------------------------------------------------------------------- reduce
-template <int METHOD, int P>
-__device__ __forceinline__ float4 decode_quad(const uint8_t* slot, uint64_t q, float s) {
-  const uint8_t* body = slot + 16;
-  if constexpr (METHOD == M_IDENTITY) {
-    return ld4_stream(reinterpret_cast<const float*>(body) + 4 * q);
-  } else if constexpr (METHOD == M_FP16) {
-    uint2 w = *reinterpret_cast<const uint2*>(body + 8 * q);
-    return make_float4(__half2float(__ushort_as_half((unsigned short)(w.x & 0xFFFF))),
-                       __half2float(__ushort_as_half((unsigned short)(w.x >> 16))),
-                       __half2float(__ushort_as_half((unsigned short)(w.y & 0xFFFF))),
-                       __half2float(__ushort_as_half((unsigned short)(w.y >> 16))));
-  } else {
-    uint32_t w = reinterpret_cast<const uint32_t*>(body)[q];
-    return make_float4(__fmul_rn((float)(int8_t)(w & 0xFF), s), __fmul_rn((float)(int8_t)((w >> 8) & 0xFF), s),
-                       __fmul_rn((float)(int8_t)((w >> 16) & 0xFF), s), __fmul_rn((float)(int8_t)(w >> 24), s));
-  }
-}
 template <int METHOD>
 __device__ __forceinline__ float decode_one(const uint8_t* slot, uint64_t e, float s) {
   const uint8_t* body = slot + 16;
   if constexpr (METHOD == M_IDENTITY) return reinterpret_cast<const float*>(body)[e];
   else if constexpr (METHOD == M_FP16) return __half2float(reinterpret_cast<const __half*>(body)[e]);
   else return __fmul_rn((float)(int8_t)body[e], s);
+}
+
+// Element e (compile-time after unrolling) of the 16 payload bytes w.
+template <int METHOD>
+__device__ __forceinline__ float decode_at(const uint4& w, int e, float s) {
+  const uint32_t x = (e * (METHOD == M_IDENTITY ? 4 : (METHOD == M_FP16 ? 2 : 1)) / 4) == 0 ? w.x
+                   : (e * (METHOD == M_IDENTITY ? 4 : (METHOD == M_FP16 ? 2 : 1)) / 4) == 1 ? w.y
+                   : (e * (METHOD == M_IDENTITY ? 4 : (METHOD == M_FP16 ? 2 : 1)) / 4) == 2 ? w.z : w.w;
+  if constexpr (METHOD == M_IDENTITY) {
+    return __uint_as_float(x);
+  } else if constexpr (METHOD == M_FP16) {
+    return __half2float(__ushort_as_half((unsigned short)((e & 1) ? (x >> 16) : (x & 0xFFFF))));
+  } else {
+    return __fmul_rn((float)(int8_t)((x >> (8 * (e & 3))) & 0xFF), s);
+  }
 }
 
 // out = fl(tree_sum / P).  For P a power of two, x * (1/P) is the same correctly rounded
@@ -307,12 +305,18 @@ __device__ __forceinline__ float div_p(float x) {
   else return __fdiv_rn(x, (float)P);
 }
 
-// src.p[c] = the slot buffer holding cluster c's payload: the local buffer for LOOPBACK / NCCL
-// / push, cluster c's own (IPC-mapped) buffer for the P2P pull — then slot c is read over NVLink.
+// Every lane loads 16 contiguous payload bytes per cluster (one 128-bit load: 16 INT8, 8 FP16
+// or 4 FP32 elements — wide loads are what NVLink pulls and HBM both want), decodes, tree-sums
+// and stores the E fp32 results as E/4 float4.  A chunk (4096 elements) is 256 lanes x E x
+// (4096 / (256 E)) groups.  src.p[c] = the slot buffer holding cluster c's payload: the local
+// buffer (LOOPBACK / NCCL / push) or cluster c's own IPC-mapped buffer (P2P pull, over NVLink).
 template <int METHOD, int P, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restrict__ items, int nitems, uint64_t chunks,
                                                            Dests src, float* __restrict__ obase) {
-  constexpr int UG = P <= 2 ? 4 : (P <= 4 ? 2 : 1);   // quads in flight per thread (registers: UG*P float4)
+  constexpr int B = METHOD == M_IDENTITY ? 4 : (METHOD == M_FP16 ? 2 : 1);
+  constexpr int E = 16 / B;                       // elements per 16-byte load
+  constexpr int NG = (int)(kChunkElems / (kThreads * E));   // groups per lane per chunk
+  constexpr int UG = (P * NG <= 8) ? NG : (8 / P > 0 ? 8 / P : 1);   // groups in flight
   int hint = 0, cur = -1;
   RItem it{};
   float sc[P];
@@ -326,39 +330,48 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       for (int k = 0; k < P; ++k)
         sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
     }
-    const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
-    const uint64_t so = it.slot_off;
+    const uint64_t j = c - it.chunk0, nfull = it.n / E;   // groups entirely inside the bucket
     float* out = obase + it.out_off;
 #pragma unroll
-    for (int u0 = 0; u0 < kQuadsPerThread; u0 += UG) {
-      float4 d[UG][P];
+    for (int h0 = 0; h0 < NG; h0 += UG) {
+      uint4 w[UG][P];
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
-        const uint64_t q = j * kChunkQuads + (uint64_t)(u0 + u) * kThreads + threadIdx.x;
-        if (q < n4) {
+        const uint64_t gidx = j * (kChunkElems / E) + (uint64_t)(h0 + u) * kThreads + threadIdx.x;
+        if (gidx < nfull) {
 #pragma unroll
-          for (int k = 0; k < P; ++k) d[u][k] = decode_quad<METHOD, P>(src.p[k] + so + k * it.pb, q, sc[k]);
+          for (int k = 0; k < P; ++k)
+            w[u][k] = *reinterpret_cast<const uint4*>(src.p[k] + it.slot_off + k * it.pb + 16 + 16 * gidx);
         }
       }
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
-        const uint64_t q = j * kChunkQuads + (uint64_t)(u0 + u) * kThreads + threadIdx.x;
-        if (q < n4) {
-          float vx[P], vy[P], vz[P], vw[P];
+        const uint64_t gidx = j * (kChunkElems / E) + (uint64_t)(h0 + u) * kThreads + threadIdx.x;
+        if (gidx < nfull) {
 #pragma unroll
-          for (int k = 0; k < P; ++k) { vx[k] = d[u][k].x; vy[k] = d[u][k].y; vz[k] = d[u][k].z; vw[k] = d[u][k].w; }
-          float4 o = make_float4(div_p<P>(tree_sum<0, P>(vx)), div_p<P>(tree_sum<0, P>(vy)),
-                                 div_p<P>(tree_sum<0, P>(vz)), div_p<P>(tree_sum<0, P>(vw)));
-          stq<VEC>(out, q, o);
+          for (int e0 = 0; e0 < E; e0 += 4) {
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float t[P];
+#pragma unroll
+              for (int k = 0; k < P; ++k) t[k] = decode_at<METHOD>(w[u][k], e0 + e, sc[k]);
+              o[e] = div_p<P>(tree_sum<0, P>(t));
+            }
+            stq<VEC>(out, gidx * (E / 4) + e0 / 4, make_float4(o[0], o[1], o[2], o[3]));
+          }
         }
       }
     }
-    if (j == n4 / kChunkQuads && threadIdx.x < (it.n & 3)) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
-      float v[P];
+    // elements after the last full group (< E of them) in the bucket's last chunk
+    if (j == (nfull * E) / kChunkElems) {
+      const uint64_t e = nfull * E + threadIdx.x;
+      if (e < it.n && threadIdx.x < E) {
+        float v[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(src.p[k] + so + k * it.pb, e, sc[k]);
-      out[e] = div_p<P>(tree_sum<0, P>(v));
+        for (int k = 0; k < P; ++k) v[k] = decode_one<METHOD>(src.p[k] + it.slot_off + k * it.pb, e, sc[k]);
+        out[e] = div_p<P>(tree_sum<0, P>(v));
+      }
     }
   }
 }

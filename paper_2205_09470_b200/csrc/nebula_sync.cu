@@ -828,7 +828,9 @@ nebula_status nebula_payload_copy(nebula_ctx* ctx, int32_t bucket, int32_t slot,
   CKC(cudaStreamSynchronize(ctx->stream));
   const BucketInfo& bk = ctx->b[bucket];
   const int lay = layout_of(ctx, bk.method >= 0 ? bk.method : ctx->codec.method);
-  CKC(cudaMemcpy(host_dst, slots_of(ctx, bk) + bk.so[lay] + (uint64_t)slot * bk.pb[lay], nbytes, cudaMemcpyDeviceToHost));
+  // P2P pull: cluster `slot`'s payload lives in that cluster's own (IPC-mapped) buffer
+  const uint8_t* base = sources_of(ctx, bk).p[slot];
+  CKC(cudaMemcpy(host_dst, base + bk.so[lay] + (uint64_t)slot * bk.pb[lay], nbytes, cudaMemcpyDeviceToHost));
   return NEBULA_OK;
 }
 
