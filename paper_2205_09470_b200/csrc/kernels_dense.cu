@@ -317,6 +317,11 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
   constexpr int E = 16 / B;                       // elements per 16-byte load
   constexpr int NG = (int)(kChunkElems / (kThreads * E));   // groups per lane per chunk
   constexpr int UG = (P * NG <= 8) ? NG : (8 / P > 0 ? 8 / P : 1);   // groups in flight
+  // E > 4: a lane's E results are contiguous; stage them through shared memory (row stride E+1,
+  // conflict-free) so each warp store instruction writes 512 contiguous bytes
+  constexpr int SROW = E + 1;
+  __shared__ float s_out[(E > 4) ? (kThreads / 32) * 32 * SROW : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int hint = 0, cur = -1;
   RItem it{};
   float sc[P];
@@ -347,19 +352,35 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
         const uint64_t gidx = j * (kChunkElems / E) + (uint64_t)(h0 + u) * kThreads + threadIdx.x;
-        if (gidx < nfull) {
+        const bool ok = gidx < nfull;
+        float o[E];
 #pragma unroll
-          for (int e0 = 0; e0 < E; e0 += 4) {
-            float o[4];
+        for (int e = 0; e < E; ++e) {
+          float t[P];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float t[P];
+          for (int k = 0; k < P; ++k) t[k] = ok ? decode_at<METHOD>(w[u][k], e, sc[k]) : 0.0f;
+          o[e] = div_p<P>(tree_sum<0, P>(t));
+        }
+        if constexpr (E == 4) {
+          if (ok) stq<VEC>(out, gidx, make_float4(o[0], o[1], o[2], o[3]));
+        } else {
+          float* sw = s_out + warp * 32 * SROW;
 #pragma unroll
-              for (int k = 0; k < P; ++k) t[k] = decode_at<METHOD>(w[u][k], e0 + e, sc[k]);
-              o[e] = div_p<P>(tree_sum<0, P>(t));
+          for (int e = 0; e < E; ++e) sw[lane * SROW + e] = o[e];
+          __syncwarp();
+          // warp region: groups gw0 .. gw0+31 = elements [gw0*E, gw0*E + 32E); instruction v writes
+          // quad v*32 + lane of it
+          const uint64_t gw0 = gidx - lane;
+#pragma unroll
+          for (int v = 0; v < E / 4; ++v) {
+            const int qq = v * 32 + lane;                 // quad inside the warp region
+            const int src_lane = (4 * qq) / E, src_e = (4 * qq) % E;
+            if (gw0 + src_lane < nfull) {
+              const float* r = sw + src_lane * SROW + src_e;
+              stq<VEC>(out, gw0 * (E / 4) + qq, make_float4(r[0], r[1], r[2], r[3]));
             }
-            stq<VEC>(out, gidx * (E / 4) + e0 / 4, make_float4(o[0], o[1], o[2], o[3]));
           }
+          __syncwarp();
         }
       }
     }
