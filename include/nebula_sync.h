@@ -150,9 +150,11 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
 /* All three stages. */
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step);
 
-/* All buckets, host buffers: copies host_grad (LOOPBACK: [P][total]) to the device, runs
- * nebula_step(ALL), copies dev_out back to host_out ([total]) and synchronises.  Pinned
- * host memory gives full PCIe bandwidth; pageable works. */
+/* All buckets, host buffers: copies host_grad (LOOPBACK: [P][total]) to the device, runs the
+ * step, copies the average back to host_out ([total]) and synchronises.  Pipelined per bucket
+ * over two copy streams and the context stream (bucket b+1 copies in while b is reduced and
+ * b-1 copies out), so both PCIe directions overlap the GPU work.  Pinned host memory gives
+ * full PCIe bandwidth and overlap; pageable works. */
 nebula_status nebula_step_host(nebula_ctx* ctx, const float* host_grad, float* host_out, uint64_t step);
 
 /* Synchronises the stream; returns and clears the sticky device error

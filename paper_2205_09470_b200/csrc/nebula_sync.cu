@@ -83,8 +83,10 @@ struct nebula_ctx {
   std::vector<Table> rtab[2];
   float* d_shard_in = nullptr;   // G > 1
   float* d_shard_out = nullptr;
-  float* d_hgrad = nullptr;      // nebula_step_host staging
+  float* d_hgrad = nullptr;      // nebula_step_host staging (bucket-major)
   float* d_hout = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;   // nebula_step_host copy streams
+  std::vector<cudaEvent_t> ev_in, ev_done;
 
   TopkBuffers tk{};
   void* d_topk_mem = nullptr;
@@ -333,6 +335,10 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_shard_out);
   cudaFree(ctx->d_hgrad);
   cudaFree(ctx->d_hout);
+  for (cudaEvent_t e : ctx->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_done) cudaEventDestroy(e);
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   cudaFree(ctx->d_topk_mem);
   cudaFree(ctx->d_bar);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
@@ -775,19 +781,56 @@ nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad
   return nebula_decompress_reduce(ctx, bucket, dev_out);
 }
 
+// Host-buffer step, pipelined per bucket over three streams so both PCIe directions and the
+// GPU work overlap:  h2d stream: copy bucket b in -> event;  ctx stream: wait, step(b) ->
+// event;  d2h stream: wait, copy bucket b's average out.  Device staging is bucket-major
+// ([P][n_b] per bucket for LOOPBACK, as a per-bucket call expects).
 nebula_status nebula_step_host(nebula_ctx* ctx, const float* host_grad, float* host_out, uint64_t step) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if ((!host_grad || !host_out) && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null host buffer");
   DevGuard dg(ctx->device);
-  const uint64_t gelems = (uint64_t)(ctx->loopback ? ctx->P : 1) * ctx->total_n;
+  const int Pl = ctx->loopback ? ctx->P : 1;
+  const uint64_t gelems = (uint64_t)Pl * ctx->total_n;
+  const int B = (int)ctx->b.size();
   if (!ctx->d_hgrad) {
     CKC(cudaMalloc(&ctx->d_hgrad, std::max<uint64_t>(16, gelems * 4)));
     CKC(cudaMalloc(&ctx->d_hout, std::max<uint64_t>(16, ctx->total_n * 4)));
+    CKC(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    ctx->ev_in.resize(B);
+    ctx->ev_done.resize(B);
+    for (int i = 0; i < B; ++i) {
+      CKC(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
+      CKC(cudaEventCreateWithFlags(&ctx->ev_done[i], cudaEventDisableTiming));
+    }
   }
-  CKC(cudaMemcpyAsync(ctx->d_hgrad, host_grad, gelems * 4, cudaMemcpyHostToDevice, ctx->stream));
-  nebula_status s = nebula_step(ctx, NEBULA_ALL_BUCKETS, ctx->d_hgrad, ctx->d_hout, step);
-  if (s != NEBULA_OK) return s;
-  CKC(cudaMemcpyAsync(host_out, ctx->d_hout, ctx->total_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  // the copies may only start once earlier work on the context stream is done with the staging
+  cudaEvent_t start;
+  CKC(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CKC(cudaEventRecord(start, ctx->stream));
+  CKC(cudaStreamWaitEvent(ctx->h2d, start, 0));
+  cudaEventDestroy(start);
+  for (int i = 0; i < B; ++i) {
+    const BucketInfo& bk = ctx->b[i];
+    float* dst = ctx->d_hgrad + (uint64_t)Pl * bk.off;
+    for (int c = 0; c < Pl; ++c)
+      CKC(cudaMemcpyAsync(dst + (uint64_t)c * bk.n, host_grad + (uint64_t)c * ctx->total_n + bk.off, bk.n * 4,
+                          cudaMemcpyHostToDevice, ctx->h2d));
+    CKC(cudaEventRecord(ctx->ev_in[i], ctx->h2d));
+  }
+  for (int i = 0; i < B; ++i) {
+    const BucketInfo& bk = ctx->b[i];
+    CKC(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[i], 0));
+    nebula_status s = nebula_step(ctx, i, ctx->d_hgrad + (uint64_t)Pl * bk.off, ctx->d_hout + bk.off, step);
+    if (s != NEBULA_OK) {
+      cudaStreamSynchronize(ctx->h2d);
+      return s;
+    }
+    CKC(cudaEventRecord(ctx->ev_done[i], ctx->stream));
+    CKC(cudaStreamWaitEvent(ctx->d2h, ctx->ev_done[i], 0));
+    CKC(cudaMemcpyAsync(host_out + bk.off, ctx->d_hout + bk.off, bk.n * 4, cudaMemcpyDeviceToHost, ctx->d2h));
+  }
+  CKC(cudaStreamSynchronize(ctx->d2h));
   CKC(cudaStreamSynchronize(ctx->stream));
   return NEBULA_OK;
 }
