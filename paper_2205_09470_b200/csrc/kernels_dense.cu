@@ -784,6 +784,136 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
   if (dst.n > 1) __threadfence_system();
 }
 
+// Lag-2 interleave with alternating parking (variant 5): even buckets park p in SHARED MEMORY
+// (the first cap4 quads of the CTA's slice; B(t-2) reads slot k and A(t) overwrites it in the
+// same thread, same loop trip), odd buckets park p in r / L2.  So at most one bucket's p sits
+// in L2 at a time (the footprint that kept DRAM traffic at the algorithmic 13 B/elem) while
+// the lag of two removes the per-bucket grid stall.  Slice overflow beyond cap4 parks in r.
+template <bool EF, bool VEC>
+__global__ void __launch_bounds__(kFusedThreads, 2)
+    k_int8_fused_smem(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
+                      float* __restrict__ rbase, Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done,
+                      uint32_t cap4) {
+  constexpr int U = 2;
+  extern __shared__ float4 sp[];
+  __shared__ uint32_t s_red[kFusedThreads / 32];
+  const unsigned G = gridDim.x;
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+  for (int t = 0; t < nitems + 2; ++t) {
+    const int ia = t, ib = t - 2;
+    const bool doA = ia < nitems;
+    bool doB = ib >= 0;
+    Item itB{};
+    Slice sb{0, 0};
+    float s = 1.0f;
+    if (doB) {
+      itB = items[ib];
+      wait_all(&done[ib], G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
+      if (nonfinite_bits(mbits)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        doB = false;
+      } else {
+        s = int8_scale_from_bits(mbits);
+        sb = slice_of(itB.n >> 2, G);
+        if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
+      }
+    }
+    Item itA{};
+    Slice sa{0, 0};
+    if (doA) {
+      itA = items[ia];
+      sa = slice_of(itA.n >> 2, G);
+    }
+    const bool a_smem = EF && ((ia & 1) == 0), b_smem = EF && ((ib & 1) == 0);
+    const float* gA = gbase + itA.g_off;
+    float* rA = rbase + itA.r_off;
+    const float* gB = gbase + itB.g_off;
+    float* rB = rbase + itB.r_off;
+    const uint64_t boB = itB.slot_off + 16;
+    uint32_t* bodyB = reinterpret_cast<uint32_t*>(dst.p[0] + boB);
+    const uint64_t lenA = sa.q1 - sa.q0, lenB = doB ? sb.q1 - sb.q0 : 0;
+    const uint64_t len = max(lenA, lenB);
+    uint32_t m = 0;
+    for (uint64_t kb0 = 0; kb0 < len; kb0 += (uint64_t)kFusedThreads * U) {
+      float4 ga[U], ra[U], pb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t k = kb0 + (uint64_t)u * kFusedThreads + threadIdx.x;
+        if (k < lenB) {   // B's p first: its shared-memory slot is overwritten by A below
+          const uint64_t q = sb.q0 + k;
+          if constexpr (EF) pb[u] = (b_smem && k < cap4) ? sp[k] : ld4_hint(rB + 4 * q, pol_stream);
+          else pb[u] = ldq<VEC>(gB, q);
+        }
+        if (k < lenA) {
+          const uint64_t q = sa.q0 + k;
+          if constexpr (VEC) ga[u] = ld4_hint(gA + 4 * q, pol_stream);
+          else ga[u] = ldq<false>(gA, q);
+          if constexpr (EF) ra[u] = ld4_hint(rA + 4 * q, pol_stream);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t k = kb0 + (uint64_t)u * kFusedThreads + threadIdx.x;
+        if (k < lenA) {
+          const uint64_t q = sa.q0 + k;
+          const float4 p = EF ? add4(ga[u], ra[u]) : ga[u];
+          m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+          if constexpr (EF) {
+            if (a_smem && k < cap4) sp[k] = p;
+            else st4_hint(rA + 4 * q, p, pol_keep);
+          }
+        }
+        uint32_t w = 0u;
+        if (k < lenB) {
+          const uint64_t q = sb.q0 + k;
+          const float4 p = pb[u];
+          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+          w = pack_i8x4(a0, a1, a2, a3);
+          st_u32_hint(bodyB + q, w, pol_stream);
+          if constexpr (EF)
+            st4_hint(rB + 4 * q,
+                     make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                 __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                     pol_stream);
+        }
+        push_u32(dst, boB + 4 * (sb.q0 + k), w, k < lenB);
+      }
+    }
+    if (blockIdx.x == G - 1) {
+      if (doA && threadIdx.x < (itA.n & 3)) {   // tail elements park in r (never in smem)
+        const uint64_t e = (itA.n >> 2) * 4 + threadIdx.x;
+        const float p = EF ? __fadd_rn(gA[e], rA[e]) : gA[e];
+        if constexpr (EF) rA[e] = p;
+        m = max(m, abs_bits(p));
+      }
+      if (doB) {
+        if (threadIdx.x < (itB.n & 3)) {
+          const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
+          const float p = EF ? rB[e] : gB[e];
+          const int qe = int8_q(p, s);
+          put(dst, boB + e, (uint8_t)(qe & 0xFF));
+          if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        }
+        zero_padding(dst, boB, itB.n);
+      }
+    }
+    if (doA) {
+      m = __reduce_max_sync(0xFFFFFFFFu, m);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        uint32_t w = threadIdx.x < kFusedThreads / 32 ? s_red[threadIdx.x] : 0u;
+        w = __reduce_max_sync(0xFFFFFFFFu, w);
+        if (threadIdx.x == 0 && w) atomicMax(&scratch[itA.sidx], w);
+      }
+      arrive(&done[ia]);
+    }
+    __syncthreads();
+  }
+  if (dst.n > 1) __threadfence_system();
+}
+
 bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -802,15 +932,45 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
     per_sm = std::min(per_sm, std::max(1, p2));
   }
   *grid = sms * std::min(per_sm, 2);
-  *smem = 0;
   *max_items = 0;
+  // shared-memory parking for variant 5: as much as two CTAs per SM can hold
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  size_t bytes = std::min<size_t>((size_t)optin, 100 * 1024);
+  const void* sk[] = {(const void*)k_int8_fused_smem<true, true>, (const void*)k_int8_fused_smem<true, false>,
+                      (const void*)k_int8_fused_smem<false, true>, (const void*)k_int8_fused_smem<false, false>};
+  for (;;) {
+    bool ok = true;
+    for (const void* f : sk) ok &= cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
+    int occ = 0;
+    if (ok) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_int8_fused_smem<true, true>, kFusedThreads, bytes);
+    if (ok && occ >= std::min(per_sm, 2)) break;
+    if (bytes <= 16 * 1024) { bytes = 0; break; }
+    bytes -= 8 * 1024;
+  }
+  cudaGetLastError();
+  *smem = bytes;
   return true;
 }
 
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,
                         const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words, int grid,
-                        size_t, int variant) {
+                        size_t smem_bytes, int variant) {
   Dests slots = slots_in;
+  if (variant == 5 && smem_bytes >= 16 * 1024) {
+    Mark mk(L, PH_INT8_ONCHIP);
+    cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+    unsigned* done = done_words;
+    uint32_t cap4 = (uint32_t)(smem_bytes / 16);
+    void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                    (void*)&flags, (void*)&done, (void*)&cap4};
+    const void* f = ef ? (vec ? (const void*)k_int8_fused_smem<true, true> : (const void*)k_int8_fused_smem<true, false>)
+                       : (vec ? (const void*)k_int8_fused_smem<false, true> : (const void*)k_int8_fused_smem<false, false>);
+    cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kFusedThreads), args, smem_bytes, L.stream);
+    ++*L.launches;
+    return;
+  }
+  if (variant == 5) variant = 2;
   Mark mk(L, PH_INT8_ONCHIP);
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;

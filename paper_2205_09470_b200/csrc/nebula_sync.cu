@@ -668,7 +668,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       if (onchip) {
         launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
                            ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem,
-                           ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : 4 /* auto: split schedule */);
+                           ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : 2 /* auto: park p, lag 1 */);
       } else {
         launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
         launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
@@ -897,7 +897,7 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launc
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
-    if (value < 0 || value > 6) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 6]");
+    if (value < 0 || value > 7) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 7]");
     if (value >= 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;

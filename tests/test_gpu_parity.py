@@ -107,7 +107,7 @@ def test_dense_parity(nb, method, P, sizes):
 
 
 @pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-recompute", "fused-park-lag1",
-                                         "fused-recompute-lag1", "fused-split"])
+                                         "fused-recompute-lag1", "fused-split", "fused-smem"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
 @pytest.mark.parametrize("ef", [True, False])
 def test_int8_kernels(nb, int8_kernel, sizes, ef):
@@ -199,7 +199,7 @@ def test_nonfinite_is_reported(nb, method, bad):
     ctx.destroy()
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-split"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-split", "fused-smem"])
 def test_int8_nonfinite_writes_nothing(nb, int8_kernel):
     import torch
     ctx = nb.SyncContext([1000], nb.INT8, num_clusters=1, transport=nb.LOOPBACK)
