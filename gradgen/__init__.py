@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -212,6 +212,20 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
         return rng.uniform(-1.0, 1.0, size=n).astype(np.float32)
     if kind == "tiny-max":
         return (rng.uniform(-1.0, 1.0, size=n) * 1e-44).astype(np.float32)
+    if kind == "half-ties":
+        # max |g| = 1 and every other value within a few ulps of (k + 1/2)/127: with a
+        # max-abs/127 scale the quotients sit on or next to half-integers (adversarial for any
+        # shortcut around an IEEE division followed by round-half-even)
+        k = rng.integers(-127, 127, size=n).astype(np.float64)
+        g = ((k + 0.5) / 127.0).astype(np.float32)
+        steps = rng.integers(-3, 4, size=n)
+        for d in (-3, -2, -1, 1, 2, 3):
+            sel = steps == d
+            toward = np.float32(np.inf) if d > 0 else np.float32(-np.inf)
+            for _ in range(abs(d)):
+                g[sel] = np.nextafter(g[sel], toward)
+        g[0] = np.float32(1.0)
+        return g
     if kind == "strided-zeros":
         # every element whose index is a multiple of 16 is 0.0, the rest N(0, 1): a regular
         # sampler with a power-of-two stride >= 16 sees only zeros (adversarial structure)

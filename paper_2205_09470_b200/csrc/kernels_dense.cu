@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       continue;
     }
     const float s = int8_scale_from_bits(mbits);
+    const float sinv = int8_inv(s);
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
     const uint64_t bo = it.slot_off + 16;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       uint32_t wv = 0u;
       if (q < n4) {
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
-        int q0 = int8_q(p.x, s), q1 = int8_q(p.y, s), q2 = int8_q(p.z, s), q3 = int8_q(p.w, s);
+        int q0 = int8_qi(p.x, s, sinv), q1 = int8_qi(p.y, s, sinv), q2 = int8_qi(p.z, s, sinv), q3 = int8_qi(p.w, s, sinv);
         wv = pack_i8x4(q0, q1, q2, q3);
         *reinterpret_cast<uint32_t*>(dst.p[0] + bo + 4 * q) = wv;
         if constexpr (EF)
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       if (threadIdx.x < (it.n & 3)) {
         const uint64_t e = n4 * 4 + threadIdx.x;
         float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-        int qe = int8_q(p, s);
+        int qe = int8_qi(p, s, sinv);
         put(dst, bo + e, (uint8_t)(qe & 0xFF));
         if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
       }
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     // ---- B setup (wait for everyone's A(ib), finished an iteration ago)
     Item itB{};
     Slice sb{0, 0};
-    float s = 1.0f;
+    float s = 1.0f, sinv = 1.0f;
     if (doB) {
       itB = items[ib];
       wait_all(&done[ib], G);
@@ -470,6 +471,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         doB = false;
       } else {
         s = int8_scale_from_bits(mbits);
+        sinv = int8_inv(s);
         sb = slice_of(itB.n >> 2, G);
         if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
       }
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         if (k < lenB) {
           const uint64_t q = sb.q0 + k;
           const float4 p = pb[u];
-          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+          const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv), a3 = int8_qi(p.w, s, sinv);
           w = pack_i8x4(a0, a1, a2, a3);
           st_u32_hint(bodyB + q, w, pol_stream);
           if constexpr (EF)
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         if (threadIdx.x < (itB.n & 3)) {
           const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
           const float p = EF ? (PARK ? rB[e] : __fadd_rn(gB[e], rB[e])) : gB[e];
-          const int qe = int8_q(p, s);
+          const int qe = int8_qi(p, s, sinv);
           put(dst, boB + e, (uint8_t)(qe & 0xFF));
           if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
         }
@@ -732,6 +734,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         continue;
       }
       const float s = int8_scale_from_bits(mbits);
+      const float sinv = int8_inv(s);
       const Slice sb = slice_of(it.n >> 2, G);
       const uint64_t len = sb.q1 - sb.q0;
       const float* g = gbase + it.g_off;
@@ -756,7 +759,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
           if (k < len) {
             const uint64_t q = sb.q0 + k;
             const float4 p = pv[u];
-            const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+            const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv), a3 = int8_qi(p.w, s, sinv);
             w = pack_i8x4(a0, a1, a2, a3);
             st_u32_hint(body + q, w, pol_stream);
             if constexpr (EF)
@@ -772,7 +775,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         if (threadIdx.x < (it.n & 3)) {
           const uint64_t e = (it.n >> 2) * 4 + threadIdx.x;
           const float p = EF ? r[e] : g[e];
-          const int qe = int8_q(p, s);
+          const int qe = int8_qi(p, s, sinv);
           put(dst, bo + e, (uint8_t)(qe & 0xFF));
           if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
         }
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     bool doB = ib >= 0;
     Item itB{};
     Slice sb{0, 0};
-    float s = 1.0f;
+    float s = 1.0f, sinv = 1.0f;
     if (doB) {
       itB = items[ib];
       wait_all(&done[ib], G);
@@ -815,6 +818,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         doB = false;
       } else {
         s = int8_scale_from_bits(mbits);
+        sinv = int8_inv(s);
         sb = slice_of(itB.n >> 2, G);
         if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
       }
@@ -868,7 +872,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         if (k < lenB) {
           const uint64_t q = sb.q0 + k;
           const float4 p = pb[u];
-          const int a0 = int8_q(p.x, s), a1 = int8_q(p.y, s), a2 = int8_q(p.z, s), a3 = int8_q(p.w, s);
+          const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv), a3 = int8_qi(p.w, s, sinv);
           w = pack_i8x4(a0, a1, a2, a3);
           st_u32_hint(bodyB + q, w, pol_stream);
           if constexpr (EF)
@@ -891,7 +895,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         if (threadIdx.x < (itB.n & 3)) {
           const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
           const float p = EF ? rB[e] : gB[e];
-          const int qe = int8_q(p, s);
+          const int qe = int8_qi(p, s, sinv);
           put(dst, boB + e, (uint8_t)(qe & 0xFF));
           if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
         }

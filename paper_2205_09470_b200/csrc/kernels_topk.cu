@@ -848,6 +848,7 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   __syncthreads();
   const int vt = (int)ti.value_type;
   const float s = S.scale;
+  const float sinv = int8_inv(s);
   if (d0 == 0 && threadIdx.x == 0) put_preamble(dst, so, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
   const uint64_t io = so + 16, vo = so + 16 + pad16(4 * k);   // idx / value section offsets
   float* r = rbase + ti.r_off;
@@ -882,7 +883,7 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
       put(dst, vo + 2 * o, hb);
       dv = __half2float(h);
     } else {
-      const int q = int8_q(pv, s);
+      const int q = int8_qi(pv, s, sinv);
       put(dst, vo + o, (uint8_t)(q & 0xFF));
       dv = __fmul_rn((float)q, s);
     }

@@ -123,6 +123,31 @@ __device__ __forceinline__ int int8_q(float p, float s) {
   return max(-127, min(127, q));
 }
 
+// Same result, cheaper: x = fl(p * fl(1/s)) is within 3 * 2^-24 * |x| of y = fl(p/s) (two
+// roundings of 2^-24 each plus y's own), i.e. < 2.3e-5 while |x| <= 128.  If x is farther than
+// 4e-5 from every half-integer, x and y round to the same integer (ties-to-even included:
+// neither sits on a tie), and any |x| >= 128 + 4e-5 clamps either way.  Otherwise — and
+// whenever 1/s is not a normal number — the IEEE division decides.  inv = fl(1/s) per bucket.
+__device__ __forceinline__ int int8_q_fast(float p, float s, float inv) {
+  const float x = __fmul_rn(p, inv);
+  const float ax = fabsf(x);
+  if (ax >= 128.0f + 4e-5f) return x > 0.0f ? 127 : -127;
+  const float f = ax - floorf(ax);                 // exact for |x| < 2^23
+  if (fabsf(f - 0.5f) > 4e-5f) {
+    const int q = __float2int_rn(x);
+    return max(-127, min(127, q));
+  }
+  return int8_q(p, s);
+}
+// fl(1/s) when it is a usable normal number, else 0 (then callers must use int8_q).
+__device__ __forceinline__ float int8_inv(float s) {
+  const float inv = __fdiv_rn(1.0f, s);
+  return (inv < 3.0e38f && s >= 1.17549435e-38f) ? inv : 0.0f;
+}
+__device__ __forceinline__ int int8_qi(float p, float s, float inv) {
+  return inv != 0.0f ? int8_q_fast(p, s, inv) : int8_q(p, s);
+}
+
 __device__ __forceinline__ uint32_t pack_i8x4(int a, int b, int c, int d) {
   return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
          ((uint32_t)(d & 0xFF) << 24);

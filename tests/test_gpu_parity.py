@@ -116,6 +116,17 @@ def test_int8_kernels(nb, int8_kernel, sizes, ef):
     run_loopback(nb, O.INT8, sizes, 2, steps=2, ef=ef, int8_kernel=int8_kernel)
 
 
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem"])
+def test_int8_near_half_integer_quotients(nb, int8_kernel):
+    # exercises the exact fallback of the reciprocal-multiply fast path (int8_q_fast)
+    run_loopback(nb, O.INT8, [50001, 4096], 2, kind="half-ties", steps=1, ef=False, int8_kernel=int8_kernel)
+    run_loopback(nb, O.INT8, [50001], 2, kind="half-ties", steps=2, int8_kernel=int8_kernel)
+
+
+def test_topk_i8_near_half_integer_quotients(nb):
+    run_loopback(nb, O.TOPK, [50001], 2, kind="half-ties", vt=O.VAL_I8, rho=0.3, steps=1, ef=False)
+
+
 @pytest.mark.parametrize("method", [O.INT8, O.FP16])
 @pytest.mark.parametrize("kind", ["ties", "subnormal", "mixed-scale", "signed-zero", "zeros", "tiny-max", "zipf-rows"])
 def test_dense_edge_values(nb, method, kind):
