@@ -1,0 +1,140 @@
+"""Parity at BASELINE config 2's full size, in bench.py's launch configuration: ERNIE-M-base
+gradient (278,042,880 fp32 per cluster, gradgen recipe), LOOPBACK P = 2, fixed 25 MiB buckets,
+nebula_step(ALL), default kernels.  Two steps (the second exercises the residual).
+
+The oracle is too slow for every element at this size, so:
+  * dense codecs: every bucket's scale is checked exactly (the bucket max is a NumPy max, the
+    scale the oracle's rule), and a seeded sample of 200k positions is recomputed element by
+    element with the oracle's own functions (payload bytes, residual bits, output bits);
+  * top-k: size-independent properties checked exactly on every bucket — k entries, indices
+    ascending, the selected set equals {key > T} plus the lowest-index need_T keys == T with
+    T, count_above, need_T from np.partition, values equal p (f32), residual zero at selected
+    and p elsewhere — plus sampled output positions against the oracle's tree average.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from gradgen import fixed_buckets, model_gradient
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+SAMPLE = 200_000
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import torch
+    import paper_2205_09470_b200 as nb
+    from paper_2205_09470_b200 import build
+    build.build()
+    P = 2
+    gs = [[model_gradient("ernie-m-base", cluster=c, step=t) for c in range(P)] for t in range(2)]
+    n = gs[0][0].size
+    sizes = fixed_buckets(n, 25 << 20)
+    return nb, torch, P, n, sizes, gs
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=F32).view(np.uint32)
+
+
+@pytest.mark.parametrize("method", [O.INT8, O.FP16])
+def test_fullsize_dense(setup, method):
+    nb, torch, P, n, sizes, gs = setup
+    ctx = nb.SyncContext(sizes, method, num_clusters=P, transport=nb.LOOPBACK)
+    rng = np.random.default_rng(7)
+    idx = np.unique(rng.integers(0, n, SAMPLE))
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    r = [np.zeros(n, F32) for _ in range(P)]           # oracle residual (full, cheap arrays)
+    g_dev = torch.empty(P * n, device="cuda")
+    out = torch.empty(n, device="cuda")
+    for t in range(2):
+        for c in range(P):
+            g_dev[c * n:(c + 1) * n].copy_(torch.from_numpy(gs[t][c]))
+        ctx.step(nb.ALL_BUCKETS, g_dev, out, t)
+        ctx.check()
+        got_out = out.cpu().numpy()
+        p = [(gs[t][c] + r[c]).astype(F32) for c in range(P)]
+        D = []
+        for c in range(P):
+            Dc = np.empty(n, F32)
+            for b, sz in enumerate(sizes):
+                lo, hi = offs[b], offs[b + 1]
+                pb = p[c][lo:hi]
+                if method == O.INT8:
+                    s = O.int8_scale(pb)                 # full bucket max: NumPy, exact
+                    pay = ctx.payload_copy(b, c)
+                    assert np.frombuffer(pay, "<f4", 1, 8)[0] == s, f"scale bucket {b}"
+                    q = O.int8_quantize(pb, s)           # vectorised: the oracle's own rule
+                    Dc[lo:hi] = O.int8_dequantize(q, s)
+                    sel = idx[(idx >= lo) & (idx < hi)] - lo
+                    body = np.frombuffer(pay, np.int8, sz, 16)
+                    assert np.array_equal(body[sel], q[sel]), f"payload bucket {b} cluster {c}"
+                else:
+                    h = O.fp16_encode(pb)
+                    Dc[lo:hi] = h.astype(F32)
+                    if b % 7 == 0:
+                        pay = ctx.payload_copy(b, c)
+                        assert np.array_equal(np.frombuffer(pay, "<u2", sz, 16), h.view(np.uint16))
+            D.append(Dc)
+        for c in range(P):
+            r[c] = (p[c] - D[c]).astype(F32)
+            rg = torch.empty(0)
+            for b in range(0, len(sizes), 5):
+                lo, hi = offs[b], offs[b + 1]
+                rdev = ctx.residual(b, c).cpu().numpy()
+                assert np.array_equal(_bits(rdev), _bits(r[c][lo:hi])), f"residual bucket {b}"
+        exp = (O.tree_sum([D[c][idx] for c in range(P)]) / F32(P)).astype(F32)
+        assert np.array_equal(_bits(got_out[idx]), _bits(exp)), "sampled outputs"
+    ctx.destroy()
+
+
+def test_fullsize_topk(setup):
+    nb, torch, P, n, sizes, gs = setup
+    rho = 0.01
+    ctx = nb.SyncContext(sizes, nb.TOPK, topk_density=rho, num_clusters=P, transport=nb.LOOPBACK)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    rng = np.random.default_rng(11)
+    idx = np.unique(rng.integers(0, n, SAMPLE))
+    r = [np.zeros(n, F32) for _ in range(P)]
+    g_dev = torch.empty(P * n, device="cuda")
+    out = torch.empty(n, device="cuda")
+    for t in range(2):
+        for c in range(P):
+            g_dev[c * n:(c + 1) * n].copy_(torch.from_numpy(gs[t][c]))
+        ctx.step(nb.ALL_BUCKETS, g_dev, out, t)
+        ctx.check()
+        got_out = out.cpu().numpy()
+        D = [np.zeros(n, F32) for _ in range(P)]
+        for c in range(P):
+            p = (gs[t][c] + r[c]).astype(F32)
+            for b, sz in enumerate(sizes):
+                lo, hi = offs[b], offs[b + 1]
+                pb = p[lo:hi]
+                k = O.topk_k(sz, O.Codec(method=O.TOPK, topk_density=rho))
+                keys = (pb.view(np.uint32) & 0x7FFFFFFF).astype(np.int64)
+                T = int(np.partition(keys, sz - k)[sz - k])
+                above = np.flatnonzero(keys > T)
+                need = k - above.size
+                ties = np.flatnonzero(keys == T)[:need]
+                exp_idx = np.sort(np.concatenate([above, ties]))
+                pay = ctx.payload_copy(b, c)
+                gi = np.frombuffer(pay, "<u4", k, 16).astype(np.int64)
+                gv = np.frombuffer(pay, "<f4", k, 16 + O.pad16(4 * k))
+                assert np.array_equal(gi, exp_idx), f"selection bucket {b} cluster {c} step {t}"
+                assert np.array_equal(_bits(gv), _bits(pb[exp_idx])), "values"
+                st = ctx.topk_stats(b, c)
+                assert (st.k, st.threshold, st.count_above, st.need) == (k, T, above.size, need)
+                rb = pb.copy()
+                rb[exp_idx] = (pb[exp_idx] - pb[exp_idx]).astype(F32)
+                D[c][lo + exp_idx] = pb[exp_idx]
+                if b % 5 == 0:
+                    assert np.array_equal(_bits(ctx.residual(b, c).cpu().numpy()), _bits(rb)), f"residual {b}"
+                r[c][lo:hi] = rb
+        exp = (O.tree_sum([D[c][idx] for c in range(P)]) / F32(P)).astype(F32)
+        assert np.array_equal(_bits(got_out[idx]), _bits(exp)), "sampled outputs"
+        nz = np.flatnonzero(got_out)                    # every nonzero output is a selected index
+        union = np.union1d(np.flatnonzero(D[0]), np.flatnonzero(D[1]))
+        assert np.all(np.isin(nz, union))
+    ctx.destroy()
