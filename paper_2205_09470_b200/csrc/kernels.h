@@ -118,7 +118,10 @@ struct TopkBuffers {
   unsigned long long* status;  // per-chunk (winners << 32 | candidates) counts
   unsigned long long* pref;    // per-chunk exclusive prefixes of the counts
   unsigned long long* soff;    // per-chunk offset of its staged entries
-  uint2* stage;                // pass-A staging: per chunk W entries then C entries
+  uint2* stage;                // pass-A staging: per chunk W entries then C entries, CTA-private regions
+  uint64_t stage_entries;      // staging capacity (split evenly between the pass-A CTAs)
+  uint64_t* splits;            // merge-path split points, 2 per merge tile
+  uint32_t bracket_smem_keys;  // shared-memory sample capacity of k_topk_bracket
   uint32_t* hist;       // [nitems][2048] fallback histograms
   uint32_t* ctrs;       // 2 dynamic tile counters
   uint32_t* start;      // sparse-reduce start offsets
@@ -132,6 +135,8 @@ struct TopkBuffers {
 void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems,
                  uint64_t a_chunks, const Item* aitems, const float* g, float* r, const Dests& slots,
                  uint32_t* flags, int value_type, uint64_t merge_tiles);
+// Opt the bracket kernel into `keys` x 4 bytes of dynamic shared memory (once per process).
+void topk_prepare_bracket(uint32_t keys);
 // Sparse decompress + tree-average (tile merge over the ascending index lists).
 // entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).
 // zero_begin/zero_count: the output range of the call (filled with +0.0 first).

@@ -142,7 +142,9 @@ __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* 
 // ---------------------------------------------------------------- B: bracket from the sample
 __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st,
-                                                              const uint32_t* __restrict__ sample) {
+                                                              const uint32_t* __restrict__ sample,
+                                                              uint32_t smem_keys) {
+  extern __shared__ uint32_t s_keys[];   // the item's sample, loaded once for the 6 radix passes
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
   __shared__ unsigned long long scan[32];
@@ -153,7 +155,12 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __
   const double delta = 5.0 * sqrt(ks + 1.0) + 16.0;
   const double rh = floor(ks - delta), rl = ceil(ks + delta);
   const uint32_t* smp = sample + ti.sample_off;
-  auto get = [&](uint32_t i) { return smp[i]; };
+  const bool in_smem = ns <= smem_keys;
+  if (in_smem) {
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) s_keys[i] = smp[i];
+    __syncthreads();
+  }
+  auto get = [&](uint32_t i) { return in_smem ? s_keys[i] : smp[i]; };
   uint32_t t_hi = 0xFFFFFFFFu, t_lo = 0u, dummy;
   if (ti.k >= ti.n) {          // everything selected: no winners, all candidates
     t_hi = 0xFFFFFFFFu; t_lo = 0u;
@@ -287,9 +294,14 @@ __global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict_
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
                                                          unsigned long long* __restrict__ counts,
                                                          unsigned long long* __restrict__ soff,
-                                                         uint2* __restrict__ stage) {
-  __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
-  __shared__ unsigned long long s_base;
+                                                         uint2* __restrict__ stage, uint64_t region,
+                                                         uint32_t* overflow) {
+  // warp totals, double-buffered by chunk parity: one barrier per chunk
+  __shared__ unsigned long long s_wt[2][kThreads / 32], s_ct[2][kThreads / 32];
+  // this CTA's private staging region: entries are appended in chunk order, no atomics
+  uint64_t pos = (uint64_t)blockIdx.x * region;
+  const uint64_t region_end = pos + region;
+  int par = 0;
   int hint = 0, cur = -1;
   uint32_t m = 0, t_lo = 0, t_hi = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -371,16 +383,17 @@ __global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict_
       const unsigned long long a2 = __shfl_up_sync(0xFFFFFFFFu, ic, o);
       if (lane >= o) { iw += a1; ic += a2; }
     }
-    if (lane == 31) { s_wt[warp] = iw; s_ct[warp] = ic; }
+    if (lane == 31) { s_wt[par][warp] = iw; s_ct[par][warp] = ic; }
     __syncthreads();
     unsigned long long ew = iw - pw, ec = ic - pc, totw = 0, totc = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
-      const unsigned long long a1 = s_wt[w], a2 = s_ct[w];
+      const unsigned long long a1 = s_wt[par][w], a2 = s_ct[par][w];
       if (w < warp) { ew += a1; ec += a2; }
       totw += a1;
       totc += a2;
     }
+    par ^= 1;
     uint32_t baseW[kQuadsPerThread + 1], baseC[kQuadsPerThread + 1];
     uint32_t accW = 0, accC = 0;
 #pragma unroll
@@ -391,16 +404,16 @@ __global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict_
       accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
     }
     const uint32_t tileW = accW, tileC = accC;
+    const uint64_t base = pos;                      // identical in every thread of the CTA
+    const bool fits = pos + tileW + tileC <= region_end;
+    pos += tileW + tileC;
     if (threadIdx.x == 0) {
-      const unsigned long long base = (tileW + tileC) ? atomicAdd(&st[i].stage_top, (unsigned long long)(tileW + tileC)) : 0ull;
-      s_base = base;
       counts[ti.status_off + j] = pack_wc(tileW, tileC);
       soff[ti.status_off + j] = base;
+      if (!fits) atomicOr(overflow, 1u);
     }
-    __syncthreads();
-    if (tileW + tileC) {
-      const uint64_t cap = ti.wcap + ti.ccap, base = s_base;
-      uint2* S = stage + ti.stage_off;
+    if ((tileW + tileC) && fits) {
+      uint2* S = stage;
 #pragma unroll
       for (int u = 0; u < kQuadsPerThread; ++u) {
         const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
@@ -411,11 +424,9 @@ __global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict_
             const uint32_t key = kb[u][e] & 0x7FFFFFFFu;
             const uint32_t idx = (uint32_t)(4 * q + e);
             if (key > t_hi) {
-              const uint64_t pos = base + w++;
-              if (pos < cap) S[pos] = make_uint2(idx, kb[u][e]);
+              S[base + w++] = make_uint2(idx, kb[u][e]);
             } else if (key >= t_lo) {
-              const uint64_t pos = base + tileW + cc++;
-              if (pos < cap) S[pos] = make_uint2(idx, kb[u][e]);
+              S[base + tileW + cc++] = make_uint2(idx, kb[u][e]);
             }
           }
         }
@@ -423,13 +434,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict_
       if (has_tail) {
         const uint32_t key = tkb & 0x7FFFFFFFu;
         const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
-        if (key > t_hi) {
-          const uint64_t pos = base + baseW[kQuadsPerThread];
-          if (pos < cap) S[pos] = make_uint2(idx, tkb);
-        } else if (key >= t_lo) {
-          const uint64_t pos = base + tileW + baseC[kQuadsPerThread];
-          if (pos < cap) S[pos] = make_uint2(idx, tkb);
-        }
+        if (key > t_hi) S[base + baseW[kQuadsPerThread]] = make_uint2(idx, tkb);
+        else if (key >= t_lo) S[base + tileW + baseC[kQuadsPerThread]] = make_uint2(idx, tkb);
       }
     }
   }
@@ -448,7 +454,8 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
                                                    const unsigned long long* __restrict__ pref,
                                                    const unsigned long long* __restrict__ soff,
                                                    const uint2* __restrict__ stage, uint2* __restrict__ wl,
-                                                   uint2* __restrict__ cl) {
+                                                   uint2* __restrict__ cl, const uint32_t* overflow) {
+  if (*((volatile const uint32_t*)overflow)) return;   // resolve sends every item to the fallback
   const uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= chunks) return;
@@ -459,14 +466,14 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
   }
   const TopkItem& ti = titems[lo];
   const TopkState& S = st[lo];
-  if (S.failed == 2 || S.stage_top > ti.wcap + ti.ccap) return;
+  if (S.failed == 2) return;
   const uint64_t j = c - aitems[lo].chunk0;
   const unsigned long long cnt = counts[ti.status_off + j];
   const uint32_t W = (uint32_t)(cnt >> 32), C = (uint32_t)(cnt & 0xFFFFFFFFu);
   if (!(W + C)) return;
   const unsigned long long pf = pref[ti.status_off + j];
   const uint64_t pw = pf >> 32, pc = pf & 0xFFFFFFFFull;
-  const uint2* src = stage + ti.stage_off + soff[ti.status_off + j];
+  const uint2* src = stage + soff[ti.status_off + j];
   uint2* dw = wl + ti.list_off;
   uint2* dc = cl + ti.list_off;
   for (uint32_t x = lane; x < W; x += 32)
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
 // ---------------------------------------------------------------- D: resolve among candidates
 __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st, uint2* __restrict__ cl,
-                                                              int retry, uint32_t* any_failed) {
+                                                              int retry, uint32_t* any_failed, const uint32_t* overflow) {
   if (retry && *((volatile uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
@@ -656,7 +663,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   if (retry && S.mode != 1) return;
   const uint64_t k = ti.k, W = S.wcount, C = S.ccount;
   if (threadIdx.x == 0) {
-    bool ok = (W < k || k == 0) && (W + C >= k) && (retry || S.stage_top <= ti.wcap + ti.ccap);
+    bool ok = (W < k || k == 0) && (W + C >= k) && (retry || *((volatile const uint32_t*)overflow) == 0);
     if (ok && C > ti.ccap) ok = (S.t_lo == S.t_hi) && (k - W) <= ti.ccap;  // exact tie set: prefix suffices
     s_ok = ok;
     if (!ok) { S.mode = 1; S.failed = 1; atomicOr(any_failed, 1u); }   // -> exact radix fallback
@@ -807,11 +814,34 @@ __device__ __forceinline__ uint64_t merge_split(const uint2* A, uint64_t na, con
   return lo;
 }
 
+// Merge-path split points of every merge tile, computed by one thread each (all the
+// latency-bound binary searches in flight at once instead of one per merge CTA).
+__global__ void k_topk_splits(const TopkItem* __restrict__ titems, const TopkState* __restrict__ st, int nitems,
+                              uint64_t tbase, uint64_t ntiles, const uint2* __restrict__ wl,
+                              const uint2* __restrict__ cl, uint64_t* __restrict__ splits) {
+  const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 2 * ntiles) return;
+  const uint64_t t = tbase + x / 2;
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (titems[mid].mt0 <= t) lo = mid; else hi = mid - 1;
+  }
+  const TopkItem& ti = titems[lo];
+  const TopkState& S = st[lo];
+  if (S.failed == 2 || ti.k == 0) return;
+  const uint64_t k = ti.k, W = S.wcount, Ns = k - W;
+  const uint64_t d0 = (t - ti.mt0) * kMergeTile;
+  const uint64_t d = (x & 1) ? (d0 + kMergeTile < k ? d0 + kMergeTile : k) : d0;
+  splits[x] = merge_split(wl + ti.list_off, W, cl + ti.list_off, Ns, d);
+}
+
 template <bool EF>
 __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __restrict__ titems,
                                                            const TopkState* __restrict__ st, int nitems, uint64_t tbase,
                                                            const uint2* __restrict__ wl, const uint2* __restrict__ cl,
-                                                           Dests dst, float* __restrict__ rbase, uint32_t* flags) {
+                                                           Dests dst, float* __restrict__ rbase, uint32_t* flags,
+                                                           const uint64_t* __restrict__ splits) {
   __shared__ uint2 sw[kMergeTile], ss[kMergeTile];
   __shared__ uint64_t s_split[2];
   const uint64_t t = tbase + blockIdx.x;
@@ -839,8 +869,9 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   const uint64_t d0 = (t - ti.mt0) * kMergeTile, d1 = d0 + kMergeTile < k ? d0 + kMergeTile : k;
   const uint2* A = wl + ti.list_off;
   const uint2* B = cl + ti.list_off;
-  if (threadIdx.x < 2) s_split[threadIdx.x] = merge_split(A, W, B, Ns, threadIdx.x ? d1 : d0);
+  if (threadIdx.x < 2) s_split[threadIdx.x] = splits[2 * blockIdx.x + threadIdx.x];
   __syncthreads();
+  (void)W; (void)Ns;
   const uint64_t a0 = s_split[0], a1 = s_split[1], b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t na = (uint32_t)(a1 - a0), nbb = (uint32_t)(b1 - b0);
   if (threadIdx.x < na) sw[threadIdx.x] = A[a0 + threadIdx.x];
@@ -1008,23 +1039,24 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     Mark mk(L, PH_TOPK_BRACKET);
     k_topk_sample<EF><<<(unsigned)((scount + 255) / 256 ? (scount + 255) / 256 : 1), 256, 0, L.stream>>>(
         aitems, ti, nitems, sbase, scount, g, r, B.sample, B.ctrs);
-    k_topk_bracket<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.sample);
+    k_topk_bracket<<<nitems, kSelThreads, (size_t)B.bracket_smem_keys * 4, L.stream>>>(ti, st, B.sample,
+                                                                                      B.bracket_smem_keys);
   }
   {
     Mark mk(L, PH_TOPK_A);
     k_topk_stage<EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, B.soff,
-                                                         B.stage);
+                                                         B.stage, B.stage_entries / ga, B.ctrs + 3);
   }
   {
     Mark mk(L, PH_TOPK_CLASSIFY);
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 0, flags, value_type, anyf);
     k_topk_move<<<(unsigned)((a_chunks * 32 + 255) / 256), 256, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks,
                                                                              B.status, B.pref, B.soff, B.stage,
-                                                                             B.wlist, B.clist);
+                                                                             B.wlist, B.clist, B.ctrs + 3);
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
-    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf, B.ctrs + 3);
   }
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
@@ -1038,13 +1070,19 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 1, flags, value_type, anyf);
     k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
                                                      B.pref, 1, anyf);
-    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf, B.ctrs + 3);
   }
   Mark mk(L, PH_TOPK_MERGE);
   const uint64_t tbase = B.host_mt0[item0];
+  k_topk_splits<<<(unsigned)((2 * merge_tiles + 255) / 256), 256, 0, L.stream>>>(ti, st, nitems, tbase, merge_tiles,
+                                                                                B.wlist, B.clist, B.splits);
   k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots,
-                                                                      r, flags);
-  *L.launches += 17;
+                                                                      r, flags, B.splits);
+  *L.launches += 18;
+}
+
+void topk_prepare_bracket(uint32_t keys) {
+  cudaFuncSetAttribute(k_topk_bracket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(keys * 4));
 }
 
 void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
