@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__
 
 // ---------------------------------------------------------------- A: EF pass + classify + stage
 template <bool EF, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_topk_stage(const Item* __restrict__ aitems,
+__global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restrict__ aitems,
                                                          const TopkItem* __restrict__ titems,
                                                          TopkState* __restrict__ st, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
@@ -684,30 +684,40 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
     T = cta_select(get, m, need, &above_c, hist, misc + 2, scan);
   }
   const uint32_t needT = need - above_c;
-  // stable in-place compaction of the selected candidates
-  uint32_t outpos = 0, ties_seen = 0;
-  for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
-    const uint32_t i = i0 + threadIdx.x;
-    uint2 e = make_uint2(0, 0);
-    uint32_t key = 0;
-    bool tie = false, gt = false;
-    if (i < m) {
-      e = cand[i];
-      key = e.y & 0x7FFFFFFFu;
-      gt = key > T;
-      tie = key == T;
+  // stable in-place compaction of the selected candidates with ONE packed scan per 4096
+  // entries: an entry's output position is (#key > T before it) + min(#key == T before it,
+  // need_T), so the (gt, tie) prefix pair decides both selection and position
+  uint32_t gt_seen = 0, tie_seen = 0;
+  for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x * 4) {
+    uint2 e[4];
+    uint32_t ngt = 0, ntie = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + 4 * threadIdx.x + u;
+      e[u] = i < m ? cand[i] : make_uint2(0u, 0xFFFFFFFFu);
+      const uint32_t key = e[u].y & 0x7FFFFFFFu;
+      ngt += (i < m) && key > T;
+      ntie += (i < m) && key == T;
     }
+    const unsigned long long v = ((unsigned long long)ngt << 32) | ntie;
     unsigned long long tot;
-    const unsigned long long v = ((unsigned long long)tie << 32);
-    const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
-    const uint32_t tie_rank = ties_seen + (uint32_t)((incl - v) >> 32);
-    const bool sel = gt || (tie && tie_rank < needT);
-    unsigned long long tot2;
-    const unsigned long long sv = sel ? 1ull : 0ull;
-    const unsigned long long incl2 = block_incl_scan<kSelThreads>(sv, scan, &tot2);
-    if (sel) cand[outpos + (uint32_t)(incl2 - sv)] = e;   // reads of this round completed in the scans' barriers
-    outpos += (uint32_t)tot2;
-    ties_seen += (uint32_t)(tot >> 32);
+    const unsigned long long excl = block_incl_scan<kSelThreads>(v, scan, &tot) - v;
+    uint32_t gb = gt_seen + (uint32_t)(excl >> 32), tb = tie_seen + (uint32_t)(excl & 0xFFFFFFFFu);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + 4 * threadIdx.x + u;
+      if (i >= m) break;
+      const uint32_t key = e[u].y & 0x7FFFFFFFu;
+      if (key > T) {
+        cand[gb + min(tb, needT)] = e[u];   // reads of this round completed before the scan's barriers
+        ++gb;
+      } else if (key == T) {
+        if (tb < needT) cand[gb + tb] = e[u];
+        ++tb;
+      }
+    }
+    gt_seen += (uint32_t)(tot >> 32);
+    tie_seen += (uint32_t)(tot & 0xFFFFFFFFu);
     __syncthreads();
   }
   if (threadIdx.x == 0) {
