@@ -107,7 +107,9 @@ struct TopkState {      // per item, device resident, rewritten every step
   uint32_t path;
   float scale;
   uint32_t maxbits;
-  unsigned long long stage_top;   // staged entries reserved by pass A
+  unsigned long long stage_top;   // (unused)
+  uint32_t stage_ovf;             // pass A ran out of staging space for this bucket -> fallback
+  uint32_t pad2;
 };
 struct TopkBuffers {
   TopkItem* items;      // [nitems] (bucket-major, cluster-minor: same order as the Item tables)

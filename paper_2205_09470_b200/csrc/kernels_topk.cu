@@ -294,8 +294,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
                                                          unsigned long long* __restrict__ counts,
                                                          unsigned long long* __restrict__ soff,
-                                                         uint2* __restrict__ stage, uint64_t region,
-                                                         uint32_t* overflow) {
+                                                         uint2* __restrict__ stage, uint64_t region) {
   // warp totals, double-buffered by chunk parity: one barrier per chunk
   __shared__ unsigned long long s_wt[2][kThreads / 32], s_ct[2][kThreads / 32];
   // this CTA's private staging region: entries are appended in chunk order, no atomics
@@ -318,6 +317,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
       t_lo = st[i].t_lo;
       t_hi = st[i].t_hi;
     }
+    // exact-tie bracket (t_lo == t_hi == the k-th key): the candidates are ties of which only the
+    // first need_T by index are wanted — possibly a huge set (e.g. all zeros of an embedding
+    // bucket), so they are not staged; the ordered write pass emits them at known offsets
+    const bool tie_mode = t_lo == t_hi;
     const Item it = aitems[i];
     const TopkItem& ti = titems[i];
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
@@ -404,15 +407,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
       accC += (uint32_t)((totc >> (12 * u)) & 0xFFF);
     }
     const uint32_t tileW = accW, tileC = accC;
+    const uint32_t staged = tileW + (tie_mode ? 0u : tileC);
     const uint64_t base = pos;                      // identical in every thread of the CTA
-    const bool fits = pos + tileW + tileC <= region_end;
-    pos += tileW + tileC;
+    const bool fits = pos + staged <= region_end;
+    if (fits) pos += staged;
     if (threadIdx.x == 0) {
       counts[ti.status_off + j] = pack_wc(tileW, tileC);
       soff[ti.status_off + j] = base;
-      if (!fits) atomicOr(overflow, 1u);
+      if (!fits) atomicOr(&st[i].stage_ovf, 1u);   // this bucket goes to the exact fallback
     }
-    if ((tileW + tileC) && fits) {
+    if (staged && fits) {
       uint2* S = stage;
 #pragma unroll
       for (int u = 0; u < kQuadsPerThread; ++u) {
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
             const uint32_t idx = (uint32_t)(4 * q + e);
             if (key > t_hi) {
               S[base + w++] = make_uint2(idx, kb[u][e]);
-            } else if (key >= t_lo) {
+            } else if (key >= t_lo && !tie_mode) {
               S[base + tileW + cc++] = make_uint2(idx, kb[u][e]);
             }
           }
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
         const uint32_t key = tkb & 0x7FFFFFFFu;
         const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
         if (key > t_hi) S[base + baseW[kQuadsPerThread]] = make_uint2(idx, tkb);
-        else if (key >= t_lo) S[base + tileW + baseC[kQuadsPerThread]] = make_uint2(idx, tkb);
+        else if (key >= t_lo && !tie_mode) S[base + tileW + baseC[kQuadsPerThread]] = make_uint2(idx, tkb);
       }
     }
   }
@@ -454,8 +458,7 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
                                                    const unsigned long long* __restrict__ pref,
                                                    const unsigned long long* __restrict__ soff,
                                                    const uint2* __restrict__ stage, uint2* __restrict__ wl,
-                                                   uint2* __restrict__ cl, const uint32_t* overflow) {
-  if (*((volatile const uint32_t*)overflow)) return;   // resolve sends every item to the fallback
+                                                   uint2* __restrict__ cl) {
   const uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= chunks) return;
@@ -466,7 +469,8 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
   }
   const TopkItem& ti = titems[lo];
   const TopkState& S = st[lo];
-  if (S.failed == 2) return;
+  if (S.failed == 2 || S.stage_ovf) return;   // overflowed buckets go to the fallback
+  const bool tie_mode = S.t_lo == S.t_hi;       // ties are emitted by k_topk_write
   const uint64_t j = c - aitems[lo].chunk0;
   const unsigned long long cnt = counts[ti.status_off + j];
   const uint32_t W = (uint32_t)(cnt >> 32), C = (uint32_t)(cnt & 0xFFFFFFFFu);
@@ -478,8 +482,9 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
   uint2* dc = cl + ti.list_off;
   for (uint32_t x = lane; x < W; x += 32)
     if (pw + x < ti.wcap) dw[pw + x] = src[x];
-  for (uint32_t x = lane; x < C; x += 32)
-    if (pc + x < ti.ccap) dc[pc + x] = src[W + x];
+  if (!tie_mode)
+    for (uint32_t x = lane; x < C; x += 32)
+      if (pc + x < ti.ccap) dc[pc + x] = src[W + x];
 }
 
 // ---------------------------------------------------------------- X: scan tile counts
@@ -532,7 +537,9 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
                                                          uint2* __restrict__ wl, uint2* __restrict__ cl,
                                                          const unsigned long long* __restrict__ pref, int retry,
                                                          const uint32_t* any_failed) {
-  if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
+  // retry == 1: fallback buckets (both lists); retry == 2: exact-tie buckets of the first
+  // pass (ties only, winners were staged)
+  if (retry == 1 && *((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
   int hint = 0;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
@@ -540,7 +547,9 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
     hint = i;
     const TopkState& S = st[i];
     if (S.failed == 2) continue;
-    if (retry && S.mode != 1) continue;
+    if (retry == 1 && S.mode != 1) continue;
+    if (retry == 2 && (S.t_lo != S.t_hi || S.stage_ovf)) continue;
+    const bool ties_only = retry == 2;
     const Item it = aitems[i];
     const TopkItem& ti = titems[i];
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
@@ -626,7 +635,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
           const uint32_t idx = (uint32_t)(4 * q + e);
           if (key > t_hi) {
             const uint64_t pos = preW + w++;
-            if (pos < ti.wcap) W[pos] = make_uint2(idx, kb[u][e]);
+            if (pos < ti.wcap && !ties_only) W[pos] = make_uint2(idx, kb[u][e]);
           } else if (key >= t_lo) {
             const uint64_t pos = preC + cc++;
             if (pos < ti.ccap) C[pos] = make_uint2(idx, kb[u][e]);
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
       const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
       if (key > t_hi) {
         const uint64_t pos = preW + baseW[kQuadsPerThread];
-        if (pos < ti.wcap) W[pos] = make_uint2(idx, tkb);
+        if (pos < ti.wcap && !ties_only) W[pos] = make_uint2(idx, tkb);
       } else if (key >= t_lo) {
         const uint64_t pos = preC + baseC[kQuadsPerThread];
         if (pos < ti.ccap) C[pos] = make_uint2(idx, tkb);
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
 // ---------------------------------------------------------------- D: resolve among candidates
 __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st, uint2* __restrict__ cl,
-                                                              int retry, uint32_t* any_failed, const uint32_t* overflow) {
+                                                              int retry, uint32_t* any_failed) {
   if (retry && *((volatile uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   if (retry && S.mode != 1) return;
   const uint64_t k = ti.k, W = S.wcount, C = S.ccount;
   if (threadIdx.x == 0) {
-    bool ok = (W < k || k == 0) && (W + C >= k) && (retry || *((volatile const uint32_t*)overflow) == 0);
+    bool ok = (W < k || k == 0) && (W + C >= k) && (retry || S.stage_ovf == 0);
     if (ok && C > ti.ccap) ok = (S.t_lo == S.t_hi) && (k - W) <= ti.ccap;  // exact tie set: prefix suffices
     s_ok = ok;
     if (!ok) { S.mode = 1; S.failed = 1; atomicOr(any_failed, 1u); }   // -> exact radix fallback
@@ -1055,18 +1064,21 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     Mark mk(L, PH_TOPK_A);
     k_topk_stage<EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, B.soff,
-                                                         B.stage, B.stage_entries / ga, B.ctrs + 3);
+                                                         B.stage, B.stage_entries / ga);
   }
   {
     Mark mk(L, PH_TOPK_CLASSIFY);
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 0, flags, value_type, anyf);
     k_topk_move<<<(unsigned)((a_chunks * 32 + 255) / 256), 256, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks,
                                                                              B.status, B.pref, B.soff, B.stage,
-                                                                             B.wlist, B.clist, B.ctrs + 3);
+                                                                             B.wlist, B.clist);
+    // exact-tie buckets: their first need_T ties in index order, at the scanned offsets
+    k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
+                                                     B.pref, 2, anyf);
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
-    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf, B.ctrs + 3);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
   }
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
@@ -1080,7 +1092,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     k_topk_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref, 1, flags, value_type, anyf);
     k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
                                                      B.pref, 1, anyf);
-    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf, B.ctrs + 3);
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 1, anyf);
   }
   Mark mk(L, PH_TOPK_MERGE);
   const uint64_t tbase = B.host_mt0[item0];
