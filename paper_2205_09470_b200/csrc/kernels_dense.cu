@@ -446,12 +446,12 @@ __device__ __forceinline__ Slice slice_of(uint64_t n4, unsigned G) {
 // PARK: phase A stores p into r and B re-reads p (4 B); otherwise A only reads g and r with
 // L2 evict_last and B re-reads both and recomputes p = g + r (same binary32 addition, so
 // bit-identical) — clean lines, nothing to write back.  LAG: B(t - LAG) runs with A(t).
-template <bool EF, bool VEC, bool PARK, int LAG>
-__global__ void __launch_bounds__(kFusedThreads, 2)
+template <bool EF, bool VEC, bool PARK, int LAG, int NT = kFusedThreads, int UNR = kFusedUnroll, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB)
     k_int8_fused(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase,
                  float* __restrict__ rbase, Dests dst, uint32_t* scratch, uint32_t* flags,
                  unsigned* done) {
-  __shared__ uint32_t s_red[kFusedThreads / 32];
+  __shared__ uint32_t s_red[NT / 32];
   const unsigned G = gridDim.x;
   const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   for (int t = 0; t < nitems + LAG; ++t) {
@@ -493,12 +493,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
     const uint64_t len = max(lenA, lenB);
     uint32_t m = 0;
     // block-uniform trip count (the lane-group pushes below use full-warp shuffles)
-    for (uint64_t kb0 = 0; kb0 < len; kb0 += (uint64_t)kFusedThreads * kFusedUnroll) {
+    for (uint64_t kb0 = 0; kb0 < len; kb0 += (uint64_t)NT * UNR) {
       const uint64_t kb = kb0 + threadIdx.x;
-      float4 ga[kFusedUnroll], ra[kFusedUnroll], pb[kFusedUnroll];
+      float4 ga[UNR], ra[UNR], pb[UNR];
 #pragma unroll
-      for (int u = 0; u < kFusedUnroll; ++u) {
-        const uint64_t k = kb + (uint64_t)u * kFusedThreads;
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t k = kb + (uint64_t)u * NT;
         if (k < lenA) {
           const uint64_t q = sa.q0 + k;
           const uint64_t polA = PARK ? pol_stream : pol_keep;
@@ -519,8 +519,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
         }
       }
 #pragma unroll
-      for (int u = 0; u < kFusedUnroll; ++u) {
-        const uint64_t k = kb + (uint64_t)u * kFusedThreads;
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t k = kb + (uint64_t)u * NT;
         if (k < lenA) {
           const uint64_t q = sa.q0 + k;
           const float4 p = EF ? add4(ga[u], ra[u]) : ga[u];
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
       if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
       __syncthreads();
       if (threadIdx.x < 32) {
-        uint32_t w = threadIdx.x < kFusedThreads / 32 ? s_red[threadIdx.x] : 0u;
+        uint32_t w = threadIdx.x < NT / 32 ? s_red[threadIdx.x] : 0u;
         w = __reduce_max_sync(0xFFFFFFFFu, w);
         if (threadIdx.x == 0 && w) atomicMax(&scratch[itA.sidx], w);
       }
@@ -930,6 +930,7 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
                        (const void*)k_int8_fused<true, true, false, 1>, (const void*)k_int8_fused_split<true, true>,
                        (const void*)k_int8_fused_split<true, false>, (const void*)k_int8_fused_split<false, true>,
                        (const void*)k_int8_fused_split<false, false>};
+  // (the NT/UNR sweep variants 6..8 size their own grids at launch)
   for (const void* f : all) {
     int p2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, f, kFusedThreads, 0);
@@ -975,6 +976,25 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
     return;
   }
   if (variant == 5) variant = 2;
+  if (variant >= 6 && variant <= 8 && ef && vec) {   // shape sweep of the lag-1 park kernel
+    Mark mk(L, PH_INT8_ONCHIP);
+    cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+    unsigned* done = done_words;
+    void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                    (void*)&flags, (void*)&done};
+    const void* f = variant == 6 ? (const void*)k_int8_fused<true, true, true, 1, 256, 2, 4>
+                  : variant == 7 ? (const void*)k_int8_fused<true, true, true, 1, 256, 4, 3>
+                                 : (const void*)k_int8_fused<true, true, true, 1, 1024, 2, 1>;
+    const int nt = variant == 8 ? 1024 : 256;
+    int per = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, nt, 0);
+    cudaLaunchCooperativeKernel(f, dim3(sms * std::max(1, per)), dim3(nt), args, 0, L.stream);
+    ++*L.launches;
+    return;
+  }
+  if (variant > 5) variant = 2;
   Mark mk(L, PH_INT8_ONCHIP);
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;
