@@ -45,9 +45,12 @@ def parse():
     ap.add_argument("--method", default="int8", choices=list(METHODS))
     ap.add_argument("--values", default="f32", choices=list(VALUES))
     ap.add_argument("--density", type=float, default=0.01)
-    ap.add_argument("--workload", default="ernie-m-base")
+    ap.add_argument("--workload", default="ernie-m-base",
+                    choices=["ernie-m-base", "ernie-m-large", "ernie-m-large-adapters", "transformer-big"])
     ap.add_argument("--bucket-mib", type=float, default=25.0)
     ap.add_argument("--clusters", type=int, default=2, help="simulated clusters at N=1 (LOOPBACK)")
+    ap.add_argument("--gpus-per-cluster", type=int, default=1,
+                    help="G > 1: hierarchical topology (P = N / G clusters; BASELINE config 3 is 2 x 4)")
     ap.add_argument("--no-ef", action="store_true")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
@@ -231,12 +234,12 @@ def run_reference(args):
     return 0
 
 
-def workload_config(args, n, P):
+def workload_config(args, n, P, G=1):
     mname = {0: "identity", 1: "fp16+ef", 2: "int8+ef", 3: f"topk{args.density:g}-{args.values}+ef"}[METHODS[args.method]]
     if args.no_ef:
         mname = mname.replace("+ef", "")
-    return {"workload": f"{args.workload}-" + (f"loopback-P{P}" if args.gpus == 1 else f"nccl-P{P}xG1"),
-            "elements_per_cluster": n, "clusters": P, "gpus_per_cluster": 1, "method": mname,
+    return {"workload": f"{args.workload}-" + (f"loopback-P{P}" if args.gpus == 1 else f"P{P}xG{G}"),
+            "elements_per_cluster": n, "clusters": P, "gpus_per_cluster": G, "method": mname,
             "bucketing": f"fixed {args.bucket_mib:g} MiB slices of the flat gradient",
             "transport": "loopback" if args.gpus == 1 else "nvlink",
             "l2": "inputs (>= 1.1 GB per cluster) exceed the 126 MB L2; no flush needed"}
@@ -268,7 +271,10 @@ def main():
         build.build()   # up to date after rank 0's build + barrier: loads only
     method, vt, ef = METHODS[args.method], VALUES[args.values], not args.no_ef
     n = None
-    P = args.clusters if world == 1 else world
+    G = args.gpus_per_cluster if world > 1 else 1
+    if world % G:
+        raise SystemExit("--gpus must be a multiple of --gpus-per-cluster")
+    P = args.clusters if world == 1 else world // G
     stream = torch.cuda.current_stream()
 
     # ---- inputs (seeded synthetic, gradgen recipe), resident in HBM before timing
@@ -280,17 +286,19 @@ def main():
             g[c * n:(c + 1) * n].copy_(torch.from_numpy(host[c]))
         del host
     else:
-        h = model_gradient(args.workload, cluster=rank)
+        h = model_gradient(args.workload, cluster=rank // G, local_rank=rank % G)
         n = h.size
         g = torch.from_numpy(h).cuda()
         del h
     out = torch.empty(n, dtype=torch.float32, device="cuda")
-    sizes = fixed_buckets(n, int(args.bucket_mib * 2 ** 20))
+    sizes = fixed_buckets(n, int(args.bucket_mib * 2 ** 20), multiple=4 * G)
+    if any(sz % G for sz in sizes):
+        raise SystemExit(f"{args.workload}: {n} elements cannot be split into shards of {G}")
     common = dict(topk_values=vt, topk_density=args.density, error_feedback=ef)
     if world == 1:
         ctx = nb.SyncContext(sizes, method, num_clusters=P, transport=nb.LOOPBACK, device=local, **common)
     else:
-        ctx = nb.init_process_group_context(sizes, device=local, method=method, **common)
+        ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method, **common)
     if method == 2:
         ctx.set_int8_kernel(args.int8_kernel)
     if world > 1 and args.exchange != "auto":
@@ -407,7 +415,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload_config(args, n, P), exchange=ctx.exchange_mode()), "roofline": roof, "step_roofline": step_roof,
+                "config": dict(workload_config(args, n, P, G), exchange=ctx.exchange_mode()), "roofline": roof, "step_roofline": step_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "kernels": kern,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
