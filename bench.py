@@ -346,8 +346,9 @@ def main():
 
     # ---- roofline of the dominant kernel
     peak, peak_src = load_peaks()
-    n_local = (P if world == 1 else 1) * n
-    k_per_cluster = sum(min(s, max(1, int(np.floor(args.density * s + 0.5)))) for s in sizes) if method == 3 else 0
+    n_local = (P if world == 1 else 1) * n // G          # coded elements on this GPU (a shard when G > 1)
+    k_per_cluster = sum(min(s // G, max(1, int(np.floor(args.density * (s // G) + 0.5)))) for s in sizes) \
+        if method == 3 else 0
     kern = {}
     for name, (cnt, tot) in phases.items():
         kern[name] = {"launches_per_step": cnt / args.steps, "ms_per_step": tot / args.steps,
@@ -358,7 +359,7 @@ def main():
     if dom:
         cnt, tot = phases[dom]
         if dom in ("dense_decompress_reduce", "sparse_decompress_reduce"):
-            byt = reduce_bytes(method, vt, P, n, k_per_cluster)
+            byt = reduce_bytes(method, vt, P, n // G, k_per_cluster)
         else:
             byt = kernel_bytes(dom, method, vt, P, ef, n_local, k_per_cluster * (P if world == 1 else 1))
         if byt:
