@@ -918,6 +918,206 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
   if (dst.n > 1) __threadfence_system();
 }
 
+// ----------------------------------------------------------------------------- INT8 TMA
+// Fused INT8 with TMA staging (variant 9, the default): one CTA per SM streams its slice of
+// every bucket through a 4-stage shared-memory ring filled by cp.async.bulk (TMA bulk copies
+// completing on an mbarrier transaction count).  A ring stage holds, for tile k of the
+// iteration, the g and r tiles of bucket t (phase A) and the parked-p tile of bucket t-1
+// (phase B); up to 4 tiles (192 KB) are in flight per SM no matter what the warps are doing.
+// Same lag-1 split barrier as k_int8_fused: A(t) parks p in r (L2 evict_last), B(t-1)
+// quantises from it; the wait for bucket t-1's max is taken after the first tiles' copies
+// were issued.  Stores stay ordinary st.global (they are posted).
+constexpr int kTmaThreads = 512;
+constexpr int kTmaTQ = 1024;   // quads per tile: 16 KB per stream
+constexpr int kTmaNS = 4;      // ring stages
+
+struct __align__(128) TmaStage {
+  float4 g[kTmaTQ];
+  float4 r[kTmaTQ];
+  float4 p[kTmaTQ];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+
+struct TmaTiles {          // tile geometry of one iteration (identical in every thread)
+  uint64_t qa0, lenA, qb0, lenB;
+  int ntA, ntB, nt;
+};
+
+template <bool EF>
+__device__ __forceinline__ void tma_issue(TmaStage* stg, uint64_t* bar, int k, const TmaTiles& T, const float* gA,
+                                          const float* rA, const float* srcB, uint64_t pol_stream, uint64_t pol_keep) {
+  const int sidx = k % kTmaNS;
+  uint32_t bytes = 0;
+  uint32_t nqa = 0, nqb = 0;
+  if (k < T.ntA) nqa = (uint32_t)min((uint64_t)kTmaTQ, T.lenA - (uint64_t)k * kTmaTQ);
+  if (k < T.ntB) nqb = (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)k * kTmaTQ);
+  bytes = nqa * (EF ? 32u : 16u) + nqb * 16u;
+  if (!bytes) return;
+  mbar_expect_tx(&bar[sidx], bytes);
+  if (nqa) {
+    const uint64_t q = T.qa0 + (uint64_t)k * kTmaTQ;
+    bulk_g2s(stg[sidx].g, gA + 4 * q, nqa * 16u, &bar[sidx], pol_stream);
+    if (EF) bulk_g2s(stg[sidx].r, rA + 4 * q, nqa * 16u, &bar[sidx], pol_stream);
+  }
+  if (nqb) {
+    const uint64_t q = T.qb0 + (uint64_t)k * kTmaTQ;
+    bulk_g2s(stg[sidx].p, srcB + 4 * q, nqb * 16u, &bar[sidx], pol_stream);
+  }
+}
+
+template <bool EF>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k_int8_tma(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
+               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done) {
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  TmaStage* stg = reinterpret_cast<TmaStage*>(tma_smem);
+  __shared__ __align__(8) uint64_t bar[kTmaNS];
+  __shared__ uint32_t s_red[kTmaThreads / 32];
+  const unsigned G = gridDim.x;
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaNS; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;   // parity bit per ring stage
+  for (int t = 0; t <= nitems; ++t) {
+    const bool doA = t < nitems;
+    bool doB = t >= 1;
+    Item itA{}, itB{};
+    TmaTiles T{};
+    if (doA) {
+      itA = items[t];
+      const Slice sa = slice_of(itA.n >> 2, G);
+      T.qa0 = sa.q0;
+      T.lenA = sa.q1 - sa.q0;
+    }
+    if (doB) {
+      itB = items[t - 1];
+      const Slice sb = slice_of(itB.n >> 2, G);
+      T.qb0 = sb.q0;
+      T.lenB = sb.q1 - sb.q0;
+    }
+    T.ntA = (int)((T.lenA + kTmaTQ - 1) / kTmaTQ);
+    T.ntB = (int)((T.lenB + kTmaTQ - 1) / kTmaTQ);
+    T.nt = max(T.ntA, T.ntB);
+    const float* gA = gbase + itA.g_off;
+    float* rA = rbase + itA.r_off;
+    const float* gB = gbase + itB.g_off;
+    float* rB = rbase + itB.r_off;
+    const float* srcB = EF ? rB : gB;
+    // prologue: the first ring-full of tiles is in flight before the barrier wait below
+    if (threadIdx.x == 0)
+      for (int k = 0; k < min(T.nt, kTmaNS); ++k) tma_issue<EF>(stg, bar, k, T, gA, rA, srcB, pol_stream, pol_keep);
+    float s = 1.0f, sinv = 1.0f;
+    const uint64_t boB = itB.slot_off + 16;
+    uint32_t* bodyB = reinterpret_cast<uint32_t*>(dst.p[0] + boB);
+    if (doB) {
+      wait_all(&done[t - 1], G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
+      if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload for this bucket
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        doB = false;
+      } else {
+        s = int8_scale_from_bits(mbits);
+        sinv = int8_inv(s);
+        if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
+      }
+    }
+    uint32_t m = 0;
+    for (int k = 0; k < T.nt; ++k) {
+      const int sidx = k % kTmaNS;
+      mbar_wait(&bar[sidx], (phase >> sidx) & 1u);
+      phase ^= 1u << sidx;
+      const TmaStage& S = stg[sidx];
+      const uint32_t nqa = k < T.ntA ? (uint32_t)min((uint64_t)kTmaTQ, T.lenA - (uint64_t)k * kTmaTQ) : 0u;
+      const uint32_t nqb = k < T.ntB ? (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)k * kTmaTQ) : 0u;
+#pragma unroll
+      for (int u = 0; u < kTmaTQ / kTmaThreads; ++u) {
+        const uint32_t j = u * kTmaThreads + threadIdx.x;
+        if (j < nqa) {
+          const uint64_t q = T.qa0 + (uint64_t)k * kTmaTQ + j;
+          const float4 p = EF ? add4(S.g[j], S.r[j]) : S.g[j];
+          m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+          if constexpr (EF) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t) next iteration
+        }
+        uint32_t w = 0u;
+        const uint64_t qb = T.qb0 + (uint64_t)k * kTmaTQ + j;
+        if (doB && j < nqb) {
+          const float4 p = S.p[j];
+          const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
+                    a3 = int8_qi(p.w, s, sinv);
+          w = pack_i8x4(a0, a1, a2, a3);
+          st_u32_hint(bodyB + qb, w, pol_stream);
+          if constexpr (EF)
+            st4_hint(rB + 4 * qb,
+                     make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                 __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                     pol_stream);
+        }
+        push_u32(dst, boB + 4 * qb, w, doB && j < nqb);
+      }
+      __syncthreads();   // everyone is done reading this stage
+      if (threadIdx.x == 0 && k + kTmaNS < T.nt)
+        tma_issue<EF>(stg, bar, k + kTmaNS, T, gA, rA, srcB, pol_stream, pol_keep);
+    }
+    // tails (n % 4 elements after the last quad) on the last CTA
+    if (blockIdx.x == G - 1) {
+      if (doA && threadIdx.x < (itA.n & 3)) {
+        const uint64_t e = (itA.n >> 2) * 4 + threadIdx.x;
+        const float p = EF ? __fadd_rn(gA[e], rA[e]) : gA[e];
+        if constexpr (EF) rA[e] = p;
+        m = max(m, abs_bits(p));
+      }
+      if (doB) {
+        if (threadIdx.x < (itB.n & 3)) {
+          const uint64_t e = (itB.n >> 2) * 4 + threadIdx.x;
+          const float p = EF ? rB[e] : gB[e];
+          const int qe = int8_qi(p, s, sinv);
+          put(dst, boB + e, (uint8_t)(qe & 0xFF));
+          if constexpr (EF) rB[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        }
+        zero_padding(dst, boB, itB.n);
+      }
+    }
+    // the parked p must be visible to next iteration's bulk copies (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (doA) {
+      m = __reduce_max_sync(0xFFFFFFFFu, m);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        uint32_t w = threadIdx.x < kTmaThreads / 32 ? s_red[threadIdx.x] : 0u;
+        w = __reduce_max_sync(0xFFFFFFFFu, w);
+        if (threadIdx.x == 0 && w) atomicMax(&scratch[itA.sidx], w);
+      }
+      arrive(&done[t]);
+    }
+    __syncthreads();
+  }
+  if (dst.n > 1) __threadfence_system();
+}
+
 bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -975,6 +1175,28 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
     ++*L.launches;
     return;
   }
+  if (variant == 9 && vec) {   // TMA-staged fused kernel: one CTA per SM
+    Mark mk(L, PH_INT8_ONCHIP);
+    cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+    unsigned* done = done_words;
+    void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                    (void*)&flags, (void*)&done};
+    const void* f = ef ? (const void*)k_int8_tma<true> : (const void*)k_int8_tma<false>;
+    const size_t smem = sizeof(TmaStage) * kTmaNS;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_int8_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaLaunchCooperativeKernel(f, dim3(sms), dim3(kTmaThreads), args, smem, L.stream);
+    ++*L.launches;
+    return;
+  }
+  if (variant == 9) variant = 2;
   if (variant == 5) variant = 2;
   if (variant >= 6 && variant <= 8 && ef && vec) {   // shape sweep of the lag-1 park kernel
     Mark mk(L, PH_INT8_ONCHIP);
