@@ -961,7 +961,6 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
 struct TmaTiles {          // tile geometry of one iteration (identical in every thread)
   uint64_t qa0, lenA, qb0, lenB;
   int ntA, ntB, nt;
-  int lag;                 // job j carries A tile j and B tile j - lag
 };
 
 template <bool EF>
@@ -970,9 +969,8 @@ __device__ __forceinline__ void tma_issue(TmaStage* stg, uint64_t* bar, int k, c
   const int sidx = k % kTmaNS;
   uint32_t bytes = 0;
   uint32_t nqa = 0, nqb = 0;
-  const int kb = k - T.lag;
   if (k < T.ntA) nqa = (uint32_t)min((uint64_t)kTmaTQ, T.lenA - (uint64_t)k * kTmaTQ);
-  if (kb >= 0 && kb < T.ntB) nqb = (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)kb * kTmaTQ);
+  if (k < T.ntB) nqb = (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)k * kTmaTQ);
   bytes = nqa * (EF ? 32u : 16u) + nqb * 16u;
   if (!bytes) return;
   mbar_expect_tx(&bar[sidx], bytes);
@@ -982,7 +980,7 @@ __device__ __forceinline__ void tma_issue(TmaStage* stg, uint64_t* bar, int k, c
     if (EF) bulk_g2s(stg[sidx].r, rA + 4 * q, nqa * 16u, &bar[sidx], pol_stream);
   }
   if (nqb) {
-    const uint64_t q = T.qb0 + (uint64_t)kb * kTmaTQ;
+    const uint64_t q = T.qb0 + (uint64_t)k * kTmaTQ;
     bulk_g2s(stg[sidx].p, srcB + 4 * q, nqb * 16u, &bar[sidx], pol_stream);
   }
 }
@@ -1022,8 +1020,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     T.ntA = (int)((T.lenA + kTmaTQ - 1) / kTmaTQ);
     T.ntB = (int)((T.lenB + kTmaTQ - 1) / kTmaTQ);
-    T.lag = T.ntB ? T.ntA / 4 : 0;   // B trails A: a quarter-iteration of slack for the wait
-    T.nt = max(T.ntA, T.ntB + T.lag);
+    T.nt = max(T.ntA, T.ntB);
     const float* gA = gbase + itA.g_off;
     float* rA = rbase + itA.r_off;
     const float* gB = gbase + itB.g_off;
@@ -1035,29 +1032,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     float s = 1.0f, sinv = 1.0f;
     const uint64_t boB = itB.slot_off + 16;
     uint32_t* bodyB = reinterpret_cast<uint32_t*>(dst.p[0] + boB);
-    bool have_s = false;
+    if (doB) {
+      wait_all(&done[t - 1], G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
+      if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload for this bucket
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        doB = false;
+      } else {
+        s = int8_scale_from_bits(mbits);
+        sinv = int8_inv(s);
+        if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
+      }
+    }
     uint32_t m = 0;
     for (int k = 0; k < T.nt; ++k) {
-      const int kb = k - T.lag;
-      if (doB && !have_s && kb >= 0) {   // first B tile: bucket t-1's max must be final
-        wait_all(&done[t - 1], G);
-        have_s = true;
-        const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
-        if (nonfinite_bits(mbits)) {   // all-or-nothing: no payload for this bucket
-          if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
-          doB = false;
-        } else {
-          s = int8_scale_from_bits(mbits);
-          sinv = int8_inv(s);
-          if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
-        }
-      }
       const int sidx = k % kTmaNS;
       mbar_wait(&bar[sidx], (phase >> sidx) & 1u);
       phase ^= 1u << sidx;
       const TmaStage& S = stg[sidx];
       const uint32_t nqa = k < T.ntA ? (uint32_t)min((uint64_t)kTmaTQ, T.lenA - (uint64_t)k * kTmaTQ) : 0u;
-      const uint32_t nqb = (kb >= 0 && kb < T.ntB) ? (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)kb * kTmaTQ) : 0u;
+      const uint32_t nqb = k < T.ntB ? (uint32_t)min((uint64_t)kTmaTQ, T.lenB - (uint64_t)k * kTmaTQ) : 0u;
 #pragma unroll
       for (int u = 0; u < kTmaTQ / kTmaThreads; ++u) {
         const uint32_t j = u * kTmaThreads + threadIdx.x;
@@ -1068,7 +1062,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           if constexpr (EF) st4_hint(rA + 4 * q, p, pol_keep);   // parked for B(t) next iteration
         }
         uint32_t w = 0u;
-        const uint64_t qb = T.qb0 + (uint64_t)kb * kTmaTQ + j;
+        const uint64_t qb = T.qb0 + (uint64_t)k * kTmaTQ + j;
         if (doB && j < nqb) {
           const float4 p = S.p[j];
           const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
@@ -1086,18 +1080,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       __syncthreads();   // everyone is done reading this stage
       if (threadIdx.x == 0 && k + kTmaNS < T.nt)
         tma_issue<EF>(stg, bar, k + kTmaNS, T, gA, rA, srcB, pol_stream, pol_keep);
-    }
-    if (doB && !have_s) {   // no B tile in this CTA's slice: still need the scale for the tail
-      wait_all(&done[t - 1], G);
-      const uint32_t mbits = *((volatile const uint32_t*)&scratch[itB.sidx]);
-      if (nonfinite_bits(mbits)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
-        doB = false;
-      } else {
-        s = int8_scale_from_bits(mbits);
-        sinv = int8_inv(s);
-        if (blockIdx.x == 0 && threadIdx.x == 0) put_preamble(dst, itB.slot_off, M_INT8, (uint32_t)itB.n, s, 0u);
-      }
     }
     // tails (n % 4 elements after the last quad) on the last CTA
     if (blockIdx.x == G - 1) {
