@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2)
 // Same lag-1 split barrier as k_int8_fused: A(t) parks p in r (L2 evict_last), B(t-1)
 // quantises from it; the wait for bucket t-1's max is taken after the first tiles' copies
 // were issued.  Stores stay ordinary st.global (they are posted).
-constexpr int kTmaThreads = 512;
+constexpr int kTmaThreads = 1024;
 constexpr int kTmaTQ = 1024;   // quads per tile: 16 KB per stream
 constexpr int kTmaNS = 4;      // ring stages
 
