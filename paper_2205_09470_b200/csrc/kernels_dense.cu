@@ -946,6 +946,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred P1;\n WAIT_%=:\n"
@@ -991,16 +994,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
   TmaStage* stg = reinterpret_cast<TmaStage*>(tma_smem);
-  __shared__ __align__(8) uint64_t bar[kTmaNS];
+  __shared__ __align__(8) uint64_t bar[kTmaNS];     // full: TMA bytes landed
+  __shared__ __align__(8) uint64_t empty[kTmaNS];   // empty: every warp finished reading the stage
   __shared__ uint32_t s_red[kTmaThreads / 32];
   const unsigned G = gridDim.x;
   const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kTmaNS; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < kTmaNS; ++i) {
+      mbar_init(&bar[i], 1);
+      mbar_init(&empty[i], kTmaThreads / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t phase = 0;   // parity bit per ring stage
+  uint32_t phase = 0;                 // full-barrier parity per ring stage (every thread)
+  uint32_t ephase = 0, filled = 0;    // producer (thread 0): empty parity, stages holding an unreleased fill
+  // producer: (re)fill the stage of tile k once its previous contents were released
+  auto refill = [&](int k, const TmaTiles& T, const float* gA, const float* rA, const float* srcB) {
+    const int sidx = k % kTmaNS;
+    if (filled & (1u << sidx)) {
+      mbar_wait(&empty[sidx], (ephase >> sidx) & 1u);
+      ephase ^= 1u << sidx;
+    }
+    filled |= 1u << sidx;
+    tma_issue<EF>(stg, bar, k, T, gA, rA, srcB, pol_stream, pol_keep);
+  };
   for (int t = 0; t <= nitems; ++t) {
     const bool doA = t < nitems;
     bool doB = t >= 1;
@@ -1028,7 +1046,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const float* srcB = EF ? rB : gB;
     // prologue: the first ring-full of tiles is in flight before the barrier wait below
     if (threadIdx.x == 0)
-      for (int k = 0; k < min(T.nt, kTmaNS); ++k) tma_issue<EF>(stg, bar, k, T, gA, rA, srcB, pol_stream, pol_keep);
+      for (int k = 0; k < min(T.nt, kTmaNS); ++k) refill(k, T, gA, rA, srcB);
     float s = 1.0f, sinv = 1.0f;
     const uint64_t boB = itB.slot_off + 16;
     uint32_t* bodyB = reinterpret_cast<uint32_t*>(dst.p[0] + boB);
@@ -1077,9 +1095,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         push_u32(dst, boB + 4 * qb, w, doB && j < nqb);
       }
-      __syncthreads();   // everyone is done reading this stage
-      if (threadIdx.x == 0 && k + kTmaNS < T.nt)
-        tma_issue<EF>(stg, bar, k + kTmaNS, T, gA, rA, srcB, pol_stream, pol_keep);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[sidx]);   // this warp is done with the stage
+      if (threadIdx.x == 0 && k + kTmaNS < T.nt) refill(k + kTmaNS, T, gA, rA, srcB);
     }
     // tails (n % 4 elements after the last quad) on the last CTA
     if (blockIdx.x == G - 1) {
