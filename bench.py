@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
                                                               "fused-park-lag1", "fused-recompute-lag1",
                                                               "fused-split", "fused-smem", "fused-256x2",
-                                                              "fused-256x4", "fused-1024x2", "fused-tma"])
+                                                              "fused-256x4", "fused-1024x2", "fused-tma",
+                                                              "fused-ws"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

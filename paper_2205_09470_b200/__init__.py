@@ -273,7 +273,7 @@ class SyncContext:
         self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2, "fused-recompute": 3,
                                           "fused-park-lag1": 4, "fused-recompute-lag1": 5,
                                           "fused-split": 6, "fused-smem": 7, "fused-256x2": 8, "fused-256x4": 9,
-                                          "fused-1024x2": 10, "fused-tma": 11}[which])
+                                          "fused-1024x2": 10, "fused-tma": 11, "fused-ws": 12}[which])
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""

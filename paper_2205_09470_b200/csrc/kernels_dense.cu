@@ -1136,6 +1136,263 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (dst.n > 1) __threadfence_system();
 }
 
+// ----------------------------------------------------------------------------- INT8 WS
+// Warp-specialised TMA kernel (variant 10, the default for large buckets).  One CTA per SM:
+//   warp 0          producer: one lane feeds two TMA (cp.async.bulk) rings —
+//                   ring A: g and r tiles of bucket t; ring B: parked-p tiles of bucket t'
+//   warps 1..8      "A": p = g + r, bucket max, park p in r (L2 evict_last); per bucket they
+//                   publish the CTA max (atomicMax) and ARRIVE on the grid-wide done[t]
+//   warps 9..31     "B": wait until done[t'] == grid (every CTA's max is in), quantise bucket t'
+//                   from ring B, write the payload (+ NVLink pushes) and the residual
+// A runs at most two buckets ahead of B (bounded L2 footprint); B-ring copies of bucket t' are
+// issued only after this CTA's A warps parked all of p(t') and fenced it for the async proxy.
+// No CTA-wide barrier sits on the streaming path: the grid-wide wait only stalls the B warps,
+// while the producer and the A warps keep HBM busy.
+constexpr int kWsThreads = 1024;
+constexpr int kWsAWarps = 8, kWsBWarps = 23;
+constexpr int kWsA = kWsAWarps * 32, kWsB = kWsBWarps * 32;
+constexpr int kWsTQ = 1024;
+constexpr int kWsNA = 3, kWsNB = 4;
+
+struct __align__(128) WsStageA {
+  float4 g[kWsTQ];
+  float4 r[kWsTQ];
+};
+struct __align__(128) WsStageB {
+  float4 p[kWsTQ];
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void zero_padding_t(const Dests& d, uint64_t body_off, uint64_t nbytes, int tid) {
+  const uint64_t end = pad16(nbytes);
+  const uint64_t z = nbytes + (tid >= 16 ? tid - 16 : end);
+  if (z < end) put<uint8_t>(d, body_off + z, (uint8_t)0);
+}
+
+template <bool EF>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
+              Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done) {
+  extern __shared__ __align__(128) unsigned char ws_smem[];
+  WsStageA* ringA = reinterpret_cast<WsStageA*>(ws_smem);
+  WsStageB* ringB = reinterpret_cast<WsStageB*>(ws_smem + sizeof(WsStageA) * kWsNA);
+  __shared__ __align__(8) uint64_t fullA[kWsNA], emptyA[kWsNA], fullB[kWsNB], emptyB[kWsNB];
+  __shared__ volatile uint32_t s_pdone, s_bdone;   // buckets whose A (resp. B) phase this CTA finished
+  __shared__ uint32_t s_amax[kWsAWarps];
+  __shared__ float s_scale[2];
+  const unsigned G = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], kWsAWarps); }
+    for (int i = 0; i < kWsNB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], kWsBWarps); }
+    s_pdone = 0;
+    s_bdone = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+  auto tiles_of = [&](int t, Slice& sl) {
+    sl = slice_of(items[t].n >> 2, G);
+    return (int)((sl.q1 - sl.q0 + kWsTQ - 1) / kWsTQ);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane != 0) return;
+    int ia = 0, ka = 0, ib = 0, kb = 0;
+    uint32_t fa = 0, fb = 0;   // fills issued per ring
+    Slice sa{}, sb{};
+    int nta = nitems > 0 ? tiles_of(0, sa) : 0, ntb = nitems > 0 ? tiles_of(0, sb) : 0;
+    while (ia < nitems || ib < nitems) {
+      bool progress = false;
+      if (ia < nitems) {
+        if (ka >= nta) {
+          ++ia;
+          ka = 0;
+          if (ia < nitems) nta = tiles_of(ia, sa);
+          progress = true;
+        } else if (ia <= ib + 2) {   // A leads B by at most two buckets
+          const uint32_t st = fa % kWsNA, use = fa / kWsNA;
+          if (use == 0 || mbar_test(&emptyA[st], (use - 1) & 1u)) {
+            const Item it = items[ia];
+            const uint64_t q = sa.q0 + (uint64_t)ka * kWsTQ;
+            const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sa.q1 - q);
+            mbar_expect_tx(&fullA[st], nq * (EF ? 32u : 16u));
+            bulk_g2s(ringA[st].g, gbase + it.g_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
+            if (EF) bulk_g2s(ringA[st].r, rbase + it.r_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
+            ++fa;
+            ++ka;
+            progress = true;
+          }
+        }
+      }
+      if (ib < nitems) {
+        if (kb >= ntb) {
+          ++ib;
+          kb = 0;
+          if (ib < nitems) ntb = tiles_of(ib, sb);
+          progress = true;
+        } else if (s_pdone > (uint32_t)ib) {   // p(ib) of this CTA is parked and fenced
+          const uint32_t st = fb % kWsNB, use = fb / kWsNB;
+          if (use == 0 || mbar_test(&emptyB[st], (use - 1) & 1u)) {
+            __threadfence_block();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const Item it = items[ib];
+            const uint64_t q = sb.q0 + (uint64_t)kb * kWsTQ;
+            const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sb.q1 - q);
+            mbar_expect_tx(&fullB[st], nq * 16u);
+            bulk_g2s(ringB[st].p, (EF ? rbase + it.r_off : gbase + it.g_off) + 4 * q, nq * 16u, &fullB[st], pol_stream);
+            ++fb;
+            ++kb;
+            progress = true;
+          }
+        }
+      }
+      if (!progress) __nanosleep(32);
+    }
+    return;
+  }
+
+  if (warp <= kWsAWarps) {
+    // ------------------------------------------------------------------ A warps
+    const int at = threadIdx.x - 32, aw = warp - 1;
+    uint32_t fa = 0;
+    for (int t = 0; t < nitems; ++t) {
+      if (t >= 2)
+        while (s_bdone < (uint32_t)(t - 1)) __nanosleep(64);   // B(t-2) finished: bounded L2 footprint
+      Slice sl;
+      const int nt = tiles_of(t, sl);
+      const Item it = items[t];
+      const float* g = gbase + it.g_off;
+      float* r = rbase + it.r_off;
+      uint32_t m = 0;
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t st = fa % kWsNA, use = fa / kWsNA;
+        mbar_wait(&fullA[st], use & 1u);
+        const uint64_t q0 = sl.q0 + (uint64_t)k * kWsTQ;
+        const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
+        const WsStageA& S = ringA[st];
+#pragma unroll
+        for (int u = 0; u < kWsTQ / kWsA; ++u) {
+          const uint32_t j = u * kWsA + at;
+          if (j < nq) {
+            const float4 p = EF ? add4(S.g[j], S.r[j]) : S.g[j];
+            m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
+            if constexpr (EF) st4_hint(r + 4 * (q0 + j), p, pol_keep);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[st]);
+        ++fa;
+      }
+      if (blockIdx.x == G - 1 && at < (int)(it.n & 3)) {
+        const uint64_t e = (it.n >> 2) * 4 + at;
+        const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+        if constexpr (EF) r[e] = p;
+        m = max(m, abs_bits(p));
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // parked p -> visible to ring-B copies
+      m = __reduce_max_sync(0xFFFFFFFFu, m);
+      if (lane == 0) s_amax[aw] = m;
+      named_sync(1, kWsA);
+      if (at == 0) {
+        uint32_t w = 0;
+        for (int i = 0; i < kWsAWarps; ++i) w = max(w, s_amax[i]);
+        if (w) atomicMax(&scratch[it.sidx], w);
+        __threadfence();
+        atomicAdd(&done[t], 1u);
+        __threadfence_block();
+        s_pdone = (uint32_t)(t + 1);
+      }
+      named_sync(1, kWsA);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- B warps
+  const int bt = threadIdx.x - 32 * (1 + kWsAWarps);
+  uint32_t fb = 0;
+  for (int t = 0; t < nitems; ++t) {
+    Slice sl;
+    const int nt = tiles_of(t, sl);
+    const Item it = items[t];
+    if (bt == 0) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&done[t]) : "memory");
+      } while (v < G);
+      const uint32_t mbits = *((volatile const uint32_t*)&scratch[it.sidx]);
+      if (nonfinite_bits(mbits)) {
+        s_scale[0] = 0.0f;
+        if (blockIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+      } else {
+        const float sc = int8_scale_from_bits(mbits);
+        s_scale[0] = sc;
+        s_scale[1] = int8_inv(sc);
+        if (blockIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, sc, 0u);
+      }
+    }
+    named_sync(2, kWsB);
+    const float s = s_scale[0], sinv = s_scale[1];
+    const bool ok = s != 0.0f;   // scale is never 0 (R4) except for the non-finite marker
+    const float* g = gbase + it.g_off;
+    float* r = rbase + it.r_off;
+    const uint64_t bo = it.slot_off + 16;
+    uint32_t* body = reinterpret_cast<uint32_t*>(dst.p[0] + bo);
+    for (int k = 0; k < nt; ++k) {
+      const uint32_t st = fb % kWsNB, use = fb / kWsNB;
+      mbar_wait(&fullB[st], use & 1u);
+      const uint64_t q0 = sl.q0 + (uint64_t)k * kWsTQ;
+      const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
+      const WsStageB& S = ringB[st];
+      for (uint32_t j0 = 0; j0 < (uint32_t)kWsTQ; j0 += kWsB) {
+        const uint32_t j = j0 + bt;
+        const bool valid = ok && j < nq;
+        uint32_t w = 0u;
+        if (valid) {
+          const float4 p = S.p[j];
+          const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
+                    a3 = int8_qi(p.w, s, sinv);
+          w = pack_i8x4(a0, a1, a2, a3);
+          st_u32_hint(body + q0 + j, w, pol_stream);
+          if constexpr (EF)
+            st4_hint(r + 4 * (q0 + j),
+                     make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                 __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                     pol_stream);
+        }
+        push_u32(dst, bo + 4 * (q0 + j), w, valid);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyB[st]);
+      ++fb;
+    }
+    if (blockIdx.x == G - 1 && ok) {
+      if (bt < (int)(it.n & 3)) {
+        const uint64_t e = (it.n >> 2) * 4 + bt;
+        const float p = EF ? r[e] : g[e];
+        const int qe = int8_qi(p, s, sinv);
+        put(dst, bo + e, (uint8_t)(qe & 0xFF));
+        if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+      }
+      zero_padding_t(dst, bo, it.n, bt);
+    }
+    named_sync(2, kWsB);
+    if (bt == 0) s_bdone = (uint32_t)(t + 1);
+  }
+  if (dst.n > 1) __threadfence_system();
+}
+
 bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1193,6 +1450,28 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
     ++*L.launches;
     return;
   }
+  if (variant == 10 && vec) {   // warp-specialised TMA kernel: one CTA per SM
+    Mark mk(L, PH_INT8_ONCHIP);
+    cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+    unsigned* done = done_words;
+    void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                    (void*)&flags, (void*)&done};
+    const void* f = ef ? (const void*)k_int8_ws<true> : (const void*)k_int8_ws<false>;
+    const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_int8_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaLaunchCooperativeKernel(f, dim3(sms), dim3(kWsThreads), args, smem, L.stream);
+    ++*L.launches;
+    return;
+  }
+  if (variant == 10) variant = 2;
   if (variant == 9 && vec) {   // TMA-staged fused kernel: one CTA per SM
     Mark mk(L, PH_INT8_ONCHIP);
     cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);

@@ -897,7 +897,7 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launc
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
-    if (value < 0 || value > 11) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 11]");
+    if (value < 0 || value > 12) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 12]");
     if (value >= 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;

@@ -107,7 +107,8 @@ def test_dense_parity(nb, method, P, sizes):
 
 
 @pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-recompute", "fused-park-lag1",
-                                         "fused-recompute-lag1", "fused-split", "fused-smem", "fused-tma"])
+                                         "fused-recompute-lag1", "fused-split", "fused-smem", "fused-tma",
+                                         "fused-ws"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
 @pytest.mark.parametrize("ef", [True, False])
 def test_int8_kernels(nb, int8_kernel, sizes, ef):
@@ -116,7 +117,7 @@ def test_int8_kernels(nb, int8_kernel, sizes, ef):
     run_loopback(nb, O.INT8, sizes, 2, steps=2, ef=ef, int8_kernel=int8_kernel)
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem", "fused-tma"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem", "fused-tma", "fused-ws"])
 def test_int8_near_half_integer_quotients(nb, int8_kernel):
     # exercises the exact fallback of the reciprocal-multiply fast path (int8_q_fast)
     run_loopback(nb, O.INT8, [50001, 4096], 2, kind="half-ties", steps=1, ef=False, int8_kernel=int8_kernel)
@@ -210,7 +211,8 @@ def test_nonfinite_is_reported(nb, method, bad):
     ctx.destroy()
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-split", "fused-smem", "fused-tma"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-split", "fused-smem", "fused-tma",
+                                         "fused-ws"])
 def test_int8_nonfinite_writes_nothing(nb, int8_kernel):
     import torch
     ctx = nb.SyncContext([1000], nb.INT8, num_clusters=1, transport=nb.LOOPBACK)
