@@ -186,9 +186,10 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   pass, 21 B/elem of HBM traffic), 2..5 fused single pass (cooperative persistent grid, a
  *   split arrive/wait barrier per bucket; 13 B/elem algorithmic): 2 p parked in r/L2 with the
  *   quantise phase lagging two buckets, 3 the same recomputing p from L2-retained g and r,
- *   4 parked with lag 1, 5 recompute with lag 1, 6 split schedule (per bucket: max pass,
- *   arrive, quantise the previous bucket; p parked in L2 for exactly two buckets).
- *   Auto = 6 when buckets average >= 1M elements, else 1. */
+ *   4 parked with lag 1, 5 recompute with lag 1, 6 split schedule, 7 lag 2 with alternating
+ *   shared-memory parking, 8..10 CTA-shape sweep of 4, 11 TMA ring (cp.async.bulk), 12 warp-
+ *   specialised TMA (producer warp + max/park warps + quantise warps, two TMA rings).
+ *   Auto = 12 when buckets average >= 1M elements and pointers are 16-B aligned, else 1. */
 #define NEBULA_OPT_INT8_KERNEL 1
 /*   NEBULA_OPT_EXCHANGE (NCCL transport): 0 auto (default), 1 ncclAllGather of the payloads
  *   after the compress, 2 P2P push: the compress kernels store every payload word into the

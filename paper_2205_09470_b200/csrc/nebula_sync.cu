@@ -668,7 +668,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       if (onchip) {
         launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
                            ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem,
-                           ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : 2 /* auto: park p, lag 1 */);
+                           ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : (vec ? 10 : 2) /* auto: warp-specialised TMA */);
       } else {
         launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
         launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
