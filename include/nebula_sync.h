@@ -197,7 +197,8 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   3 P2P pull: compress writes locally, the decompress-reduce kernel loads each peer's slot
  *   directly from the peer over NVLink.  In 2 and 3 the exchange is a per-bucket flag
  *   handshake (release/acquire at system scope) and slots are double-buffered by step parity.
- *   Auto = 3 when every rank can map every peer (decided collectively at init), else 1.
+ *   Auto (every rank can map every peer, decided collectively at init): 2 for P = 2, 3 for
+ *   P > 2; else 1.
  *   Only between steps. */
 #define NEBULA_OPT_EXCHANGE 2
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);

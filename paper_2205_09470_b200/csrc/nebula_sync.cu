@@ -593,7 +593,9 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       if (ctx->P > 1) {
         nebula_status ps = p2p_setup(ctx);
         if (ps != NEBULA_OK) return bail(ps);
-        if (ctx->p2p_ok) ctx->xmode = 3;   // auto: P2P pull (NVLink loads outrun SM-issued stores)
+        // auto: P = 2 -> push (one peer: the NVLink egress hides inside the compress kernel);
+        // P > 2 -> pull (NVLink loads outrun SM-issued stores once every GPU feeds P - 1 peers)
+        if (ctx->p2p_ok) ctx->xmode = ctx->P == 2 ? 2 : 3;
       }
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
@@ -910,7 +912,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     for (const auto& bk : ctx->b)
       if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
     ctx->xopt = (int)value;
-    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? 3 : (int)value);
+    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? (ctx->P == 2 ? 2 : 3) : (int)value);
     return NEBULA_OK;
   }
   return fail(ctx, NEBULA_ERR_INVALID_ARG, "unknown option");
