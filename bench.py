@@ -64,6 +64,23 @@ def parse():
     return ap.parse_args()
 
 
+def load_traffic(workload_name, method_name, bucket_mib, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of the same workload
+    (profiles/*/traffic.json), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            if d["workload"] == workload_name and d["method"] == method_name and float(d["bucket_mib"]) == bucket_mib:
+                v = d["per_launch_dram_bytes"].get(kernel)
+                if v:
+                    return int(v)
+        except Exception:
+            continue
+    return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -366,8 +383,11 @@ def main():
         if byt:
             per_launch_s = tot / cnt * 1e-3
             ach = byt / per_launch_s / 1e9
+            wc = workload_config(args, n, P, G)
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                    "frac": round(ach / peak, 4),
+                    "traffic": load_traffic(wc["workload"], wc["method"], args.bucket_mib, dom),
+                    "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": int(byt), "ms_per_launch": round(tot / cnt, 4)}
     step_bytes = step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world)
     step_roof = {"algorithmic_bytes_per_step": int(step_bytes),
