@@ -102,17 +102,25 @@ __device__ __forceinline__ Digit digit_of(int d) {
 
 // Radix select inside one CTA: key at descending rank `rank` (1 <= rank <= m) of keys
 // produced by get(i), i < m.  Returns T, and *above = #{key > T}.
+// Radix select inside one CTA: key at descending rank `rank` (1 <= rank <= m) of the 31-bit
+// keys produced by get(i), i < m.  Returns T, and *above = #{key > T}.  `known` leading key
+// bits (value taken from known_val) are shared by every key — e.g. all candidates of a bracket
+// [t_lo, t_hi] share the common prefix of t_lo and t_hi — so the digits start below them
+// (otherwise the first digits would pile every key into one shared-memory bin).
 template <class GetKey>
 __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* above_out, uint32_t* hist,
-                               uint32_t* s_misc, unsigned long long* scan_smem) {
+                               uint32_t* s_misc, unsigned long long* scan_smem, int known = 0,
+                               uint32_t known_val = 0) {
   constexpr int U = 8;   // keys in flight per thread (the loop is latency-bound otherwise)
-  uint32_t prefix = 0, above = 0, left = rank;
-  for (int d = 0; d < 3; ++d) {
-    const Digit dg = digit_of(d);
-    const int nb = 1 << dg.bits;
+  int lo_bit = 31 - known;                                   // bits [0, lo_bit) still to resolve
+  uint32_t prefix = known > 0 ? (known_val >> lo_bit) : 0u; // value of bits [lo_bit, 31)
+  uint32_t above = 0, left = rank;
+  while (lo_bit > 0) {
+    const int bits = lo_bit < 11 ? lo_bit : 11;
+    const int shift = lo_bit - bits, hs = lo_bit;
+    const int nb = 1 << bits;
     for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
     __syncthreads();
-    const int hs = dg.shift + dg.bits;  // bits above this digit must equal the prefix
     for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x * U) {
       uint32_t key[U];
 #pragma unroll
@@ -124,15 +132,16 @@ __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* 
       for (int u = 0; u < U; ++u) {
         const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
         const bool act = i < m && ((hs >= 31) || ((key[u] >> hs) == prefix));
-        hist_add(hist, act, (key[u] >> dg.shift) & (nb - 1));
+        hist_add(hist, act, (key[u] >> shift) & (nb - 1));
       }
     }
     __syncthreads();
     find_bin(hist, nb, left, &s_misc[0], &s_misc[1], scan_smem);
     const uint32_t b = s_misc[0], ab = s_misc[1];
-    prefix = (prefix << dg.bits) | b;
+    prefix = (prefix << bits) | b;
     above += ab;
     left -= ab;
+    lo_bit = shift;
     __syncthreads();
   }
   *above_out = above;
@@ -690,7 +699,11 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
     T = S.t_lo;
   } else {
     auto get = [&](uint32_t i) { return cand[i].y & 0x7FFFFFFFu; };
-    T = cta_select(get, m, need, &above_c, hist, misc + 2, scan);
+    // every candidate key lies in [t_lo, min(t_hi, 2^31 - 1)]: their common leading bits are known
+    const uint32_t hi31 = S.t_hi > 0x7FFFFFFFu ? 0x7FFFFFFFu : S.t_hi;
+    const uint32_t x = S.t_lo ^ hi31;
+    const int known = x ? (__clz(x) - 1) : 31;
+    T = cta_select(get, m, need, &above_c, hist, misc + 2, scan, known, S.t_lo);
   }
   const uint32_t needT = need - above_c;
   // stable in-place compaction of the selected candidates with ONE packed scan per 4096
