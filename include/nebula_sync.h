@@ -147,6 +147,15 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket);
  * alias dev_grad (non-LOOPBACK) . */
 nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out);
 
+/* Decode ONE cluster's payload slot into dev_out without averaging: fp32, the bucket's
+ * elements (ALL: back to back), +0.0 where top-k did not select.  The pipeline-hop use of the
+ * codecs ("FP16 quantization was used for feed-forward
+ * activation compression ... INT8 quantization was used for back propagation gradient
+ * compression", across the Scenario-II boundary PAPER.md:259) — compress with error_feedback
+ * 0, exchange, then decompress the peer's slot.  Allowed after exchange (any slot) or after
+ * compress (own slot; every slot for LOOPBACK).  Does not change the bucket's state. */
+nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, float* dev_out);
+
 /* All three stages. */
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step);
 

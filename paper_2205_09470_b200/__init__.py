@@ -104,6 +104,7 @@ def load() -> ctypes.CDLL:
         "nebula_exchange": (I32, [P, I32]),
         "nebula_decompress_reduce": (I32, [P, I32, VP]),
         "nebula_step": (I32, [P, I32, VP, VP, U64]),
+        "nebula_decompress": (I32, [P, I32, I32, VP]),
         "nebula_step_host": (I32, [P, VP, VP, U64]),
         "nebula_check": (I32, [P]),
         "nebula_payload_bytes": (I32, [P, I32, ctypes.POINTER(U64)]),
@@ -214,6 +215,10 @@ class SyncContext:
 
     def decompress_reduce(self, bucket, out):
         self._ck(self._L.nebula_decompress_reduce(self._h, bucket, _ptr(out)))
+
+    def decompress(self, bucket, slot, out):
+        """Decode one cluster's payload (no averaging): the pipeline-hop use (NEXT-2)."""
+        self._ck(self._L.nebula_decompress(self._h, bucket, slot, _ptr(out)))
 
     def step(self, bucket, grad, out, step):
         self._ck(self._L.nebula_step(self._h, bucket, _ptr(grad), _ptr(out), step))

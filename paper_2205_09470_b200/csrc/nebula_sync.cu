@@ -775,6 +775,50 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
   return NEBULA_OK;
 }
 
+// Decode ONE cluster's payload (no averaging) — the pipeline-hop use of the codecs (SURVEY.md
+// NEXT-2; PAPER.md:418 FP16 forward activations / INT8 backward gradients across the
+// Scenario-II boundary).  Reuses the reducer kernels with P = 1 on that slot.
+nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, float* dev_out) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  int lo, hi;
+  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  if (slot < 0 || slot >= ctx->P) return fail(ctx, NEBULA_ERR_INVALID_ARG, "slot out of range");
+  if (!dev_out && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_out");
+  for (int i = lo; i < hi; ++i) {
+    const int st = ctx->b[i].state;
+    const bool own = ctx->loopback || slot == ctx->me;
+    if (!(st == ST_EXCHANGED || (st == ST_COMPRESSED && own)))
+      return fail(ctx, NEBULA_ERR_STATE, "decompress needs the slot's payload (compress / exchange first)");
+  }
+  DevGuard dg(ctx->device);
+  const Launch L = launch_of(ctx);
+  for (int i = lo; i < hi; ++i) {
+    const BucketInfo& bk = ctx->b[i];
+    const int method = bk.method, lay = layout_of(ctx, method);
+    const Table& T = ctx->rtab[lay][1 + i];
+    const RItem* items = ctx->d_ritems[lay] + T.first;
+    float* out_b = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+    float* obase = ctx->G > 1 ? ctx->d_shard_out : out_b;
+    const bool vec = T.aligned && ((uintptr_t)obase % 16 == 0);
+    Dests src{};
+    src.n = 1;
+    src.p[0] = sources_of(ctx, bk).p[slot] + (uint64_t)slot * bk.pb[lay];   // slot c read as "cluster 0"
+    if (method == M_TOPK) {
+      float* zb = ctx->G > 1 ? obase + bk.coff : obase;
+      launch_reduce_topk(L, ctx->codec.topk_values, 1, vec, items, T.count, T.entries, T.tiles, src, ctx->tk.start,
+                         obase, zb, bk.cn);
+    } else {
+      launch_reduce_dense(L, method, 1, vec, items, T.count, T.chunks, src, obase);
+    }
+    CKC(cudaGetLastError());
+    if (ctx->G > 1 && bk.cn) {
+      Mark mk(L, PH_NCCL_AG);
+      CKN(ncclAllGather(ctx->d_shard_out + bk.coff, out_b, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
+    }
+  }
+  return NEBULA_OK;
+}
+
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
   nebula_status s = nebula_compress(ctx, bucket, dev_grad, step);
   if (s != NEBULA_OK) return s;

@@ -283,3 +283,37 @@ def test_step_host_matches_device_path(nb):
     assert np.array_equal(bits(out_h), bits(out_d.cpu().numpy()))
     a.destroy()
     b.destroy()
+
+
+# ------------------------------------------------------------------ pipeline hop (NEXT-2)
+@pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.INT8, 0), (O.IDENTITY, 0), (O.TOPK, O.VAL_F32),
+                                       (O.TOPK, O.VAL_I8)])
+def test_decompress_single_slot(nb, method, vt):
+    """Scenario-II hop semantics: each side decodes the OTHER side's
+    payload exactly, no averaging, no error feedback; Table 5's ratios hold for the bytes."""
+    import torch
+    sizes = [128 * 64 * 768 // 8, 4099]            # an H^E-shaped activation block (PAPER.md:350) + ragged
+    P = 2
+    ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=0.1, error_feedback=False, num_clusters=P,
+                         transport=nb.LOOPBACK)
+    codec = O.Codec(method=method, topk_values=vt, topk_density=0.1, error_feedback=False)
+    xs = [np.concatenate([synthetic(n, 90 + 7 * c + b, "normal") for b, n in enumerate(sizes)]) for c in range(P)]
+    dev = torch.from_numpy(np.concatenate(xs)).cuda()
+    ctx.compress(nb.ALL_BUCKETS, dev, 0)
+    ctx.exchange(nb.ALL_BUCKETS)
+    total = sum(sizes)
+    for slot in range(P):
+        out = torch.full((total,), float("nan"), device="cuda")
+        ctx.decompress(nb.ALL_BUCKETS, slot, out)
+        got = out.cpu().numpy()
+        off = 0
+        for b, n in enumerate(sizes):
+            res = O.cluster_step(xs[slot][off:off + n], None, codec, 0)
+            assert ctx.payload_copy(b, slot) == res.payload
+            assert np.array_equal(bits(got[off:off + n]), bits(O.decode_payload(res.payload, n)))
+            if method in (O.FP16, O.INT8):
+                assert (len(res.payload) - 16) / (4 * n) == pytest.approx({O.FP16: 0.50, O.INT8: 0.25}[method],
+                                                                        abs=16 / (4 * n))
+            off += n
+    ctx.decompress_reduce(nb.ALL_BUCKETS, torch.empty(total, device="cuda"))
+    ctx.destroy()
