@@ -53,6 +53,7 @@ def parse():
                     help="G > 1: hierarchical topology (P = N / G clusters; BASELINE config 3 is 2 x 4)")
     ap.add_argument("--no-ef", action="store_true")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
+    ap.add_argument("--fp16-kernel", default="tma", choices=["tma", "plain"])
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
                                                               "fused-park-lag1", "fused-recompute-lag1",
                                                               "fused-split", "fused-smem", "fused-256x2",
@@ -319,6 +320,8 @@ def main():
         ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method, **common)
     if method == 2:
         ctx.set_int8_kernel(args.int8_kernel)
+    if method == 1:
+        ctx.set_fp16_kernel(args.fp16_kernel)
     if world > 1 and args.exchange != "auto":
         ctx.set_exchange(args.exchange)
     torch.cuda.synchronize()

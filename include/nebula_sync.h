@@ -210,6 +210,9 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   P > 2; else 1.
  *   Only between steps. */
 #define NEBULA_OPT_EXCHANGE 2
+/*   NEBULA_OPT_FP16_KERNEL: 0 (default) TMA-ring streaming kernel for 16-B aligned calls,
+ *   1 plain 128-bit-load streaming kernel. */
+#define NEBULA_OPT_FP16_KERNEL 3
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

@@ -29,6 +29,7 @@ NCCL, LOOPBACK = 0, 1
 ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
 OPT_EXCHANGE = 2
+OPT_FP16_KERNEL = 3
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -279,6 +280,10 @@ class SyncContext:
                                           "fused-park-lag1": 4, "fused-recompute-lag1": 5,
                                           "fused-split": 6, "fused-smem": 7, "fused-256x2": 8, "fused-256x4": 9,
                                           "fused-1024x2": 10, "fused-tma": 11, "fused-ws": 12}[which])
+
+    def set_fp16_kernel(self, which: str):
+        """'tma' (default) | 'plain' (NEBULA_OPT_FP16_KERNEL)."""
+        self.set_option(OPT_FP16_KERNEL, {"tma": 0, "plain": 1}[which])
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""

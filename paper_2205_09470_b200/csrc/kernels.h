@@ -48,6 +48,9 @@ void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, u
 // FP16 + EF, single pass: p = g + r; h = RNE16(p); r <- p - h; flags.
 void launch_fp16(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                  const float* g, float* r, const Dests& slots, uint32_t* flags);
+// FP16 + EF with a TMA ring (16-B aligned calls; one CTA per SM, producer warp + 31 consumers).
+bool launch_fp16_tma(const Launch& L, bool ef, const Item* items, int nitems, uint64_t chunks, const float* g,
+                     float* r, const Dests& slots, uint32_t* flags);
 // INT8 pass 1: scratch[sidx] <- max over the item of |g + r| bits (atomicMax; zeroed by caller).
 void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                    const float* g, const float* r, uint32_t* scratch);

@@ -53,6 +53,12 @@ __device__ __forceinline__ void zero_padding(const Dests& d, uint64_t body_off, 
   if (z < end) put<uint8_t>(d, body_off + z, (uint8_t)0);
 }
 
+__device__ __forceinline__ void zero_padding_t(const Dests& d, uint64_t body_off, uint64_t nbytes, int tid) {
+  const uint64_t end = pad16(nbytes);
+  const uint64_t z = nbytes + (tid >= 16 ? tid - 16 : end);
+  if (z < end) put<uint8_t>(d, body_off + z, (uint8_t)0);
+}
+
 // ----------------------------------------------------------------------------- IDENTITY
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_identity(const Item* __restrict__ items, int nitems, uint64_t chunks,
@@ -1173,11 +1179,6 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ void zero_padding_t(const Dests& d, uint64_t body_off, uint64_t nbytes, int tid) {
-  const uint64_t end = pad16(nbytes);
-  const uint64_t z = nbytes + (tid >= 16 ? tid - 16 : end);
-  if (z < end) put<uint8_t>(d, body_off + z, (uint8_t)0);
-}
 
 template <bool EF>
 __global__ void __launch_bounds__(kWsThreads, 1)
@@ -1391,6 +1392,130 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (bt == 0) s_bdone = (uint32_t)(t + 1);
   }
   if (dst.n > 1) __threadfence_system();
+}
+
+
+// ----------------------------------------------------------------------------- FP16 TMA
+// FP16 + EF streaming with a TMA ring (default for 16-B aligned calls): one CTA per SM walks
+// the same grid-stride chunk sequence as k_fp16; warp 0 bulk-loads the g and r tiles of each
+// chunk into a 6-stage shared-memory ring (cp.async.bulk, mbarrier transaction counts), warps
+// 1..31 convert and store the payload and the residual.  No grid-wide dependency.
+constexpr int kF16Threads = 1024, kF16NS = 6;
+struct __align__(128) F16Stage {
+  float4 g[kChunkQuads];
+  float4 r[kChunkQuads];
+};
+
+template <bool EF>
+__global__ void __launch_bounds__(kF16Threads, 1)
+    k_fp16_tma(const Item* __restrict__ items, int nitems, uint64_t chunks, const float* __restrict__ gbase,
+               float* __restrict__ rbase, Dests dst, uint32_t* flags) {
+  extern __shared__ __align__(128) unsigned char f16_smem[];
+  F16Stage* ring = reinterpret_cast<F16Stage*>(f16_smem);
+  __shared__ __align__(8) uint64_t full[kF16NS], empty[kF16NS];
+  constexpr int kCons = kF16Threads - 32, kConsWarps = kCons / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kF16NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kConsWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first();
+  if (warp == 0) {   // ---------------- producer
+    if (lane != 0) return;
+    int hint = 0;
+    uint32_t f = 0;
+    for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++f) {
+      const int i = find_item(items, nitems, c, hint);
+      hint = i;
+      const Item it = items[i];
+      const uint64_t j = c - it.chunk0, n4 = it.n >> 2, q0 = j * kChunkQuads;
+      const uint32_t nq = q0 < n4 ? (uint32_t)min((uint64_t)kChunkQuads, n4 - q0) : 0u;
+      const uint32_t st = f % kF16NS, use = f / kF16NS;
+      if (use) mbar_wait(&empty[st], (use - 1) & 1u);
+      if (nq) {
+        mbar_expect_tx(&full[st], nq * (EF ? 32u : 16u));
+        bulk_g2s(ring[st].g, gbase + it.g_off + 4 * q0, nq * 16u, &full[st], pol);
+        if (EF) bulk_g2s(ring[st].r, rbase + it.r_off + 4 * q0, nq * 16u, &full[st], pol);
+      } else {
+        mbar_arrive(&full[st]);   // nothing to copy (tail-only / empty chunk): complete the phase
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  const int ct = threadIdx.x - 32;
+  bool bad = false, ovf = false;
+  int hint = 0;
+  uint32_t f = 0;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++f) {
+    const int i = find_item(items, nitems, c, hint);
+    hint = i;
+    const Item it = items[i];
+    const uint64_t j = c - it.chunk0, n4 = it.n >> 2, q0 = j * kChunkQuads;
+    const uint32_t nq = q0 < n4 ? (uint32_t)min((uint64_t)kChunkQuads, n4 - q0) : 0u;
+    const uint32_t st = f % kF16NS, use = f / kF16NS;
+    mbar_wait(&full[st], use & 1u);
+    float* r = rbase + it.r_off;
+    const uint64_t bo = it.slot_off + 16;
+    if (j == 0 && ct == 0) put_preamble(dst, it.slot_off, M_FP16, (uint32_t)it.n, 1.0f, 0u);
+    const F16Stage& S = ring[st];
+    for (uint32_t x0 = 0; x0 < (uint32_t)kChunkQuads; x0 += kCons) {
+      const uint32_t x = x0 + ct;
+      const uint64_t q = q0 + x;
+      const bool valid = x < nq;
+      uint2 packed = make_uint2(0u, 0u);
+      if (valid) {
+        const float4 p = EF ? add4(S.g[x], S.r[x]) : S.g[x];
+        uint16_t h0, h1, h2, h3;
+        float4 d;
+        d.x = fp16_one(p.x, h0, bad, ovf);
+        d.y = fp16_one(p.y, h1, bad, ovf);
+        d.z = fp16_one(p.z, h2, bad, ovf);
+        d.w = fp16_one(p.w, h3, bad, ovf);
+        packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
+        *reinterpret_cast<uint2*>(dst.p[0] + bo + 8 * q) = packed;
+        if constexpr (EF)
+          st4(r + 4 * q, make_float4(__fsub_rn(p.x, d.x), __fsub_rn(p.y, d.y), __fsub_rn(p.z, d.z), __fsub_rn(p.w, d.w)));
+      }
+      if (x0 < (uint32_t)kChunkQuads) push_u64(dst, bo + 8 * q, packed, valid);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (j == n4 / kChunkQuads) {   // tail elements (n % 4) and the 16-byte padding
+      const float* g = gbase + it.g_off;
+      if (ct < (int)(it.n & 3)) {
+        const uint64_t e = n4 * 4 + ct;
+        const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+        uint16_t hb;
+        const float d = fp16_one(p, hb, bad, ovf);
+        put(dst, bo + 2 * e, hb);
+        if constexpr (EF) r[e] = __fsub_rn(p, d);
+      }
+      zero_padding_t(dst, bo, 2 * it.n, ct);
+    }
+  }
+  raise_flags(flags, bad, ovf);
+  if (dst.n > 1) __threadfence_system();
+}
+
+bool launch_fp16_tma(const Launch& L, bool ef, const Item* items, int nitems, uint64_t chunks, const float* g,
+                     float* r, const Dests& slots, uint32_t* flags) {
+  const size_t smem = sizeof(F16Stage) * kF16NS;
+  const void* f = ef ? (const void*)k_fp16_tma<true> : (const void*)k_fp16_tma<false>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fp16_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_fp16_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  (void)f;
+  Mark mk(L, PH_FP16);
+  const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)L.num_sms);
+  if (ef) k_fp16_tma<true><<<grid, kF16Threads, smem, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  else k_fp16_tma<false><<<grid, kF16Threads, smem, L.stream>>>(items, nitems, chunks, g, r, slots, flags);
+  ++*L.launches;
+  return true;
 }
 
 bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* smem) {

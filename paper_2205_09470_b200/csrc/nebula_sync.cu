@@ -111,6 +111,7 @@ struct nebula_ctx {
 
   // INT8 single-pass on-chip kernel (cooperative grid)
   int int8_kernel = 0;          // NEBULA_OPT_INT8_KERNEL
+  int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
   bool onchip_ok = false;
   int onchip_grid = 0;
   size_t onchip_smem = 0;
@@ -649,7 +650,10 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       launch_identity(L, vec, items, T.count, T.chunks, gbase, dst, ctx->d_flags);
       break;
     case M_FP16:
-      launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_flags);
+      if (vec && ctx->fp16_kernel == 0)
+        launch_fp16_tma(L, ef, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_flags);
+      else
+        launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_flags);
       break;
     case M_INT8: {
       // zero the max-abs words of the items in this call (sidx = c * B + b)
@@ -947,6 +951,11 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     if (value >= 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;
+    return NEBULA_OK;
+  }
+  if (option == NEBULA_OPT_FP16_KERNEL) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "FP16 kernel option must be 0 or 1");
+    ctx->fp16_kernel = (int)value;
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_EXCHANGE) {

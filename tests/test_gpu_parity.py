@@ -30,12 +30,15 @@ def bits(a):
 
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
-                 start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None):
+                 start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
+                 fp16_kernel=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
     if int8_kernel:
         ctx.set_int8_kernel(int8_kernel)
+    if fp16_kernel:
+        ctx.set_fp16_kernel(fp16_kernel)
     codec = O.Codec(method=method, topk_values=vt, topk_k=k, topk_density=rho, error_feedback=ef,
                     start_step=start_step)
     total = sum(sizes)
@@ -126,6 +129,13 @@ def test_int8_near_half_integer_quotients(nb, int8_kernel):
 
 def test_topk_i8_near_half_integer_quotients(nb):
     run_loopback(nb, O.TOPK, [50001], 2, kind="half-ties", vt=O.VAL_I8, rho=0.3, steps=1, ef=False)
+
+
+@pytest.mark.parametrize("fp16_kernel", ["tma", "plain"])
+@pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20]])
+def test_fp16_kernels(nb, fp16_kernel, sizes):
+    run_loopback(nb, O.FP16, sizes, 2, steps=2, fp16_kernel=fp16_kernel)
+    run_loopback(nb, O.FP16, sizes, 3, steps=1, ef=False, fp16_kernel=fp16_kernel)
 
 
 @pytest.mark.parametrize("method", [O.INT8, O.FP16])
