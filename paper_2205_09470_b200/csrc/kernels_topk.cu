@@ -89,10 +89,18 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t rank, uint32_
 }
 
 __device__ __forceinline__ void hist_add(uint32_t* hist, bool active, uint32_t bin) {
-  // warp-aggregated shared-memory increment (many equal keys would serialise otherwise)
+  // duplicate-heavy input (e.g. all-zero keys) puts a whole warp on one bin: then one lane adds
+  // the popcount; otherwise plain per-lane shared atomics (a vote is far cheaper than match.any)
   const unsigned mask = __activemask();
-  const unsigned peers = __match_any_sync(mask, active ? bin : 0xFFFFFFFFu);
-  if (active && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+  const unsigned act = __ballot_sync(mask, active);
+  if (!act) return;
+  const int leader = __ffs(act) - 1;
+  const uint32_t b0 = __shfl_sync(mask, bin, leader);
+  if (__all_sync(mask, !active || bin == b0)) {
+    if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[b0], (uint32_t)__popc(act));
+  } else if (active) {
+    atomicAdd(&hist[bin], 1u);
+  }
 }
 
 struct Digit { int shift, bits; };
