@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-ef", action="store_true")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
     ap.add_argument("--fp16-kernel", default="tma", choices=["tma", "plain"])
+    ap.add_argument("--no-step-fusion", action="store_true",
+                    help="run compress / exchange / reduce as separate launches (NEBULA_OPT_STEP_FUSION=1)")
+    ap.add_argument("--step-config", type=int, default=None, help="fused-step warp split 0..10 (tuning)")
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
                                                               "fused-park-lag1", "fused-recompute-lag1",
                                                               "fused-split", "fused-smem", "fused-256x2",
@@ -322,6 +325,10 @@ def main():
         ctx.set_int8_kernel(args.int8_kernel)
     if method == 1:
         ctx.set_fp16_kernel(args.fp16_kernel)
+    if args.no_step_fusion:
+        ctx.set_step_fusion(False)
+    if args.step_config is not None:
+        ctx.set_option(nb.OPT_STEP_FUSION, 2 + args.step_config)
     if world > 1 and args.exchange != "auto":
         ctx.set_exchange(args.exchange)
     torch.cuda.synchronize()
@@ -381,6 +388,9 @@ def main():
         cnt, tot = phases[dom]
         if dom in ("dense_decompress_reduce", "sparse_decompress_reduce"):
             byt = reduce_bytes(method, vt, P, n // G, k_per_cluster)
+        elif dom == "int8_fused_step":   # compress of the local clusters + the average (one kernel)
+            byt = kernel_bytes("int8_fused_ef_quant_pack", method, vt, P, ef, n_local, 0) + \
+                reduce_bytes(method, vt, P, n // G, 0)
         else:
             byt = kernel_bytes(dom, method, vt, P, ef, n_local, k_per_cluster * (P if world == 1 else 1))
         if byt:

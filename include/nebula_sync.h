@@ -156,7 +156,13 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
  * compress (own slot; every slot for LOOPBACK).  Does not change the bucket's state. */
 nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, float* dev_out);
 
-/* All three stages. */
+/* All three stages.  Same results, bit for bit, as compress + exchange + decompress_reduce.
+ * For INT8 with 16-B aligned pointers, buckets averaging >= 1M elements, G = 1 and a LOOPBACK
+ * or P2P (push / pull) exchange, the three stages run as ONE cooperative kernel
+ * (NEBULA_OPT_STEP_FUSION): reduce warps average bucket b — pulling the peers' payloads over
+ * NVLink once their system-scope arrival flags say they are complete — while the compress
+ * warps of the same kernel stream bucket b+1.  A peer that never arrives sets the peer-timeout
+ * flag after 60 s (nebula_check reports it). */
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step);
 
 /* All buckets, host buffers: copies host_grad (LOOPBACK: [P][total]) to the device, runs the
@@ -213,6 +219,10 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 /*   NEBULA_OPT_FP16_KERNEL: 0 (default) TMA-ring streaming kernel for 16-B aligned calls,
  *   1 plain 128-bit-load streaming kernel. */
 #define NEBULA_OPT_FP16_KERNEL 3
+/*   NEBULA_OPT_STEP_FUSION: 0 (default) nebula_step fuses INT8 compress + exchange + reduce
+ *   into one kernel where eligible (see nebula_step), 1 never (three stage launches),
+ *   2..12 fused with warp split 0..10 of the kernel's tuning sweep. */
+#define NEBULA_OPT_STEP_FUSION 4
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

@@ -30,6 +30,7 @@ ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
 OPT_EXCHANGE = 2
 OPT_FP16_KERNEL = 3
+OPT_STEP_FUSION = 4
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -284,6 +285,11 @@ class SyncContext:
     def set_fp16_kernel(self, which: str):
         """'tma' (default) | 'plain' (NEBULA_OPT_FP16_KERNEL)."""
         self.set_option(OPT_FP16_KERNEL, {"tma": 0, "plain": 1}[which])
+
+    def set_step_fusion(self, on: bool):
+        """True (default): step() runs INT8 compress + exchange + reduce as one kernel where
+        eligible; False: three stage launches (NEBULA_OPT_STEP_FUSION)."""
+        self.set_option(OPT_STEP_FUSION, 0 if on else 1)
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""

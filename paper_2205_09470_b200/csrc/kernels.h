@@ -12,7 +12,7 @@ namespace nb {
 enum Phase : int {
   PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
-  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_COUNT
+  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_COUNT
 };
 
 struct Launch {
@@ -74,6 +74,14 @@ struct Peers {
   unsigned long long* arrive[8];  // every cluster's arrival flags (IPC-mapped; own at [me])
   int n, me;
 };
+// Fused INT8 step (compress + P2P/loopback exchange + average in one cooperative kernel).
+// items/nitems: the compress table of the call (bucket-major, PL items per bucket); ritems: the
+// reduce table (one per bucket); src.n = P sources; pe.n > 1 = P2P peers to signal / wait for.
+void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                      const Dests& dst, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
+                      int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
+                      uint64_t seq, int config);
+
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.
 void launch_exchange_flags(const Launch& L, const Peers& pe, unsigned long long* local_arrive, int lo, int hi,

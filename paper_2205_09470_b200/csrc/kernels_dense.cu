@@ -1146,17 +1146,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 // Warp-specialised TMA kernel (variant 10, the default for large buckets).  One CTA per SM:
 //   warp 0          producer: one lane feeds two TMA (cp.async.bulk) rings —
 //                   ring A: g and r tiles of bucket t; ring B: parked-p tiles of bucket t'
-//   warps 1..8      "A": p = g + r, bucket max, park p in r (L2 evict_last); per bucket they
+//   AW warps  "A":  p = g + r, bucket max, park p in r (L2 evict_last); per bucket they
 //                   publish the CTA max (atomicMax) and ARRIVE on the grid-wide done[t]
-//   warps 9..31     "B": wait until done[t'] == grid (every CTA's max is in), quantise bucket t'
+//   BW warps  "B":  wait until done[t'] == grid (every CTA's max is in), quantise bucket t'
 //                   from ring B, write the payload (+ NVLink pushes) and the residual
+//   CW warps  "C":  (fused step only, CW > 0) wait until every cluster's payload of bucket b
+//                   is complete — this GPU's B phase (grid counter bdone) and every peer's
+//                   system-scope arrival flag — then decode the P payloads (peers' over
+//                   NVLink in pull mode), tree-sum, divide and write the average of bucket b.
 // A runs at most two buckets ahead of B (bounded L2 footprint); B-ring copies of bucket t' are
 // issued only after this CTA's A warps parked all of p(t') and fenced it for the async proxy.
 // No CTA-wide barrier sits on the streaming path: the grid-wide wait only stalls the B warps,
-// while the producer and the A warps keep HBM busy.
+// while the producer and the A warps keep HBM busy; C drains bucket b while A/B stream b+1.
 constexpr int kWsThreads = 1024;
-constexpr int kWsAWarps = 8, kWsBWarps = 23;
-constexpr int kWsA = kWsAWarps * 32, kWsB = kWsBWarps * 32;
 constexpr int kWsTQ = 1024;
 constexpr int kWsNA = 3, kWsNB = 4;
 
@@ -1179,25 +1181,210 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
 }
 
+// ----------------------------------------------------------------------------- P2P flags
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint4 ld16_cg(const void* p) {   // L2 (or the peer's L2), never a stale L1 line
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
 
-template <bool EF>
+// The fused step's reduce side (unused when CW == 0).
+struct StepArgs {
+  const RItem* ritems;               // one per bucket of the call
+  Dests src;                         // src.p[c]: buffer holding cluster c's payload (local or IPC-mapped)
+  float* obase;
+  unsigned* bdone;                   // per compress item: CTAs whose B phase finished it
+  Peers pe;                          // pe.n > 1: P2P — signal / wait peers' arrival flags
+  unsigned long long* local_arrive;  // this GPU's arrival flags [bucket * P + cluster]
+  unsigned long long seq;
+  int b0;                            // global index of the call's first bucket (flag index)
+  int PL;                            // compress items per bucket (clusters computed on this GPU)
+};
+
+// Reduce role: buckets in order; this CTA's share of bucket b is the same quad slice its B
+// warps quantised, in 16-element groups (one 16-B load per cluster), staged through a per-warp
+// shared-memory transpose so each store instruction writes 512 contiguous bytes.
+template <int P>
+__device__ __forceinline__ void ws_reduce_role(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
+                                               volatile uint32_t* s_abort, float* s_out, uint32_t* flags) {
+  constexpr int E = 16, SROW = E + 1, U = P <= 2 ? 2 : 1;
+  const unsigned G = gridDim.x;
+  const int lane = ct & 31, cw = ct >> 5, ncw = nC / 32;
+  float* sw = s_out + cw * 32 * SROW;
+  const uint64_t pol = l2_evict_first();
+  for (int b = 0; b < nb; ++b) {
+    const RItem it = a.ritems[b];
+    float* scb = s_sc + (b & 1) * 8;   // double-buffered: rewritten only after the next barrier
+    if (ct == 0) {
+      for (int c = 0; c < a.PL; ++c) {
+        const unsigned* w = a.bdone + b * a.PL + c;
+        unsigned v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+          if (v >= G) break;
+          __nanosleep(128);
+        }
+      }
+      if (a.pe.n > 1) {
+        const unsigned long long t0 = globaltimer_ns();
+        for (int c = 0; c < P && !*s_abort; ++c) {
+          if (c == a.pe.me) continue;
+          while (ld_acquire_sys(a.local_arrive + (size_t)(a.b0 + b) * P + c) < a.seq) {
+            if (globaltimer_ns() - t0 > 60ull * 1000000000ull) {
+              atomicOr(flags, kFlagPeerTimeout);
+              *s_abort = 1u;
+              break;
+            }
+            __nanosleep(256);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        scb[k] = *reinterpret_cast<volatile const float*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 8);
+    }
+    named_sync(3, nC);
+    if (*s_abort) return;
+    float sc[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) sc[k] = scb[k];
+    const uint64_t n4 = it.n >> 2;
+    const Slice sl = slice_of(n4, G);
+    const uint64_t g0 = sl.q0 >> 2, g1 = sl.q1 >> 2;   // whole 16-element groups of this slice
+    float* out = a.obase + it.out_off;
+    auto slot = [&](int k, uint64_t gi) { return a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + 16 * gi; };
+    auto dec = [&](const uint4& x4, int e, float s) {
+      const uint32_t x = (e >> 2) == 0 ? x4.x : (e >> 2) == 1 ? x4.y : (e >> 2) == 2 ? x4.z : x4.w;
+      return __fmul_rn((float)(int8_t)((x >> (8 * (e & 3))) & 0xFF), s);
+    };
+    for (uint64_t gb = g0 + (uint64_t)cw * 32 * U; gb < g1; gb += (uint64_t)ncw * 32 * U) {
+      if constexpr (P <= 4) {
+        uint4 w[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t gi = gb + u * 32 + lane;
+          if (gi < g1) {
+#pragma unroll
+            for (int k = 0; k < P; ++k) w[u][k] = ld16_cg(slot(k, gi));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = gb + u * 32 + lane < g1;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            float t[P];
+#pragma unroll
+            for (int k = 0; k < P; ++k) t[k] = ok ? dec(w[u][k], e, sc[k]) : 0.0f;
+            sw[lane * SROW + e] = div_p<P>(tree_sum<0, P>(t));
+          }
+          __syncwarp();
+          const uint64_t gw0 = gb + u * 32;
+#pragma unroll
+          for (int v = 0; v < E / 4; ++v) {
+            const int qq = v * 32 + lane, src_lane = qq >> 2, src_e = (qq & 3) * 4;
+            if (gw0 + src_lane < g1) {
+              const float* r = sw + src_lane * SROW + src_e;
+              st4_hint(out + 4 * (gw0 * 4 + qq), make_float4(r[0], r[1], r[2], r[3]), pol);
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        // P > 4: the two subtrees of tree_sum<0, P> one after the other (register budget of a
+        // 1024-thread CTA); the left subtree's sums wait in the transpose buffer
+        constexpr int MID = (P + 1) / 2;
+        const uint64_t gi = gb + lane;
+        const bool ok = gi < g1;
+        {
+          uint4 w[MID];
+#pragma unroll
+          for (int k = 0; k < MID; ++k) w[k] = ok ? ld16_cg(slot(k, gi)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            float t[P];
+#pragma unroll
+            for (int k = 0; k < MID; ++k) t[k] = dec(w[k], e, sc[k]);
+            sw[lane * SROW + e] = tree_sum<0, MID>(t);
+          }
+        }
+        {
+          uint4 w[P - MID];
+#pragma unroll
+          for (int k = MID; k < P; ++k) w[k - MID] = ok ? ld16_cg(slot(k, gi)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            float t[P];
+#pragma unroll
+            for (int k = MID; k < P; ++k) t[k] = dec(w[k - MID], e, sc[k]);
+            sw[lane * SROW + e] = div_p<P>(__fadd_rn(sw[lane * SROW + e], tree_sum<MID, P>(t)));
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < E / 4; ++v) {
+          const int qq = v * 32 + lane, src_lane = qq >> 2, src_e = (qq & 3) * 4;
+          if (gb + src_lane < g1) {
+            const float* r = sw + src_lane * SROW + src_e;
+            st4_hint(out + 4 * (gb * 4 + qq), make_float4(r[0], r[1], r[2], r[3]), pol);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // the < 16 elements after the last whole group of the bucket
+    if (blockIdx.x == G - 1 && ct < 16) {
+      const uint64_t e = 16 * (n4 >> 2) + ct;
+      if (e < it.n) {
+        float v[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const int8_t q = *reinterpret_cast<volatile const int8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
+          v[k] = __fmul_rn((float)q, sc[k]);
+        }
+        out[e] = div_p<P>(tree_sum<0, P>(v));
+      }
+    }
+  }
+}
+
+template <bool EF, int AW, int BW, int CW>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
-              Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done) {
+              Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
+  static_assert(1 + AW + BW + CW == kWsThreads / 32, "warp roles must fill the CTA");
+  constexpr int kA = AW * 32, kB = BW * 32, kC = CW * 32;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   WsStageA* ringA = reinterpret_cast<WsStageA*>(ws_smem);
   WsStageB* ringB = reinterpret_cast<WsStageB*>(ws_smem + sizeof(WsStageA) * kWsNA);
   __shared__ __align__(8) uint64_t fullA[kWsNA], emptyA[kWsNA], fullB[kWsNB], emptyB[kWsNB];
   __shared__ volatile uint32_t s_pdone, s_bdone;   // buckets whose A (resp. B) phase this CTA finished
-  __shared__ uint32_t s_amax[kWsAWarps];
+  __shared__ uint32_t s_amax[AW];
   __shared__ float s_scale[2];
+  __shared__ float s_sc[16];
+  __shared__ volatile uint32_t s_abort;
   const unsigned G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kWsNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], kWsAWarps); }
-    for (int i = 0; i < kWsNB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], kWsBWarps); }
+    for (int i = 0; i < kWsNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], AW); }
+    for (int i = 0; i < kWsNB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], BW); }
     s_pdone = 0;
     s_bdone = 0;
+    s_abort = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1212,22 +1399,22 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (lane != 0) return;
     int ia = 0, ka = 0, ib = 0, kb = 0;
     uint32_t fa = 0, fb = 0;   // fills issued per ring
-    Slice sa{}, sb{};
-    int nta = nitems > 0 ? tiles_of(0, sa) : 0, ntb = nitems > 0 ? tiles_of(0, sb) : 0;
+    Slice sa_{}, sb{};
+    int nta = nitems > 0 ? tiles_of(0, sa_) : 0, ntb = nitems > 0 ? tiles_of(0, sb) : 0;
     while (ia < nitems || ib < nitems) {
       bool progress = false;
       if (ia < nitems) {
         if (ka >= nta) {
           ++ia;
           ka = 0;
-          if (ia < nitems) nta = tiles_of(ia, sa);
+          if (ia < nitems) nta = tiles_of(ia, sa_);
           progress = true;
         } else if (ia <= ib + 2) {   // A leads B by at most two buckets
           const uint32_t st = fa % kWsNA, use = fa / kWsNA;
           if (use == 0 || mbar_test(&emptyA[st], (use - 1) & 1u)) {
             const Item it = items[ia];
-            const uint64_t q = sa.q0 + (uint64_t)ka * kWsTQ;
-            const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sa.q1 - q);
+            const uint64_t q = sa_.q0 + (uint64_t)ka * kWsTQ;
+            const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sa_.q1 - q);
             mbar_expect_tx(&fullA[st], nq * (EF ? 32u : 16u));
             bulk_g2s(ringA[st].g, gbase + it.g_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
             if (EF) bulk_g2s(ringA[st].r, rbase + it.r_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
@@ -1264,7 +1451,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     return;
   }
 
-  if (warp <= kWsAWarps) {
+  if (warp <= AW) {
     // ------------------------------------------------------------------ A warps
     const int at = threadIdx.x - 32, aw = warp - 1;
     uint32_t fa = 0;
@@ -1284,8 +1471,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
         const WsStageA& S = ringA[st];
 #pragma unroll
-        for (int u = 0; u < kWsTQ / kWsA; ++u) {
-          const uint32_t j = u * kWsA + at;
+        for (int u = 0; u < (kWsTQ + kA - 1) / kA; ++u) {
+          const uint32_t j = u * kA + at;
           if (j < nq) {
             const float4 p = EF ? add4(S.g[j], S.r[j]) : S.g[j];
             m = max(m, max(max(abs_bits(p.x), abs_bits(p.y)), max(abs_bits(p.z), abs_bits(p.w))));
@@ -1305,93 +1492,126 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       asm volatile("fence.proxy.async.global;" ::: "memory");   // parked p -> visible to ring-B copies
       m = __reduce_max_sync(0xFFFFFFFFu, m);
       if (lane == 0) s_amax[aw] = m;
-      named_sync(1, kWsA);
+      named_sync(1, kA);
       if (at == 0) {
         uint32_t w = 0;
-        for (int i = 0; i < kWsAWarps; ++i) w = max(w, s_amax[i]);
+        for (int i = 0; i < AW; ++i) w = max(w, s_amax[i]);
         if (w) atomicMax(&scratch[it.sidx], w);
         __threadfence();
         atomicAdd(&done[t], 1u);
         __threadfence_block();
         s_pdone = (uint32_t)(t + 1);
       }
-      named_sync(1, kWsA);
+      named_sync(1, kA);
     }
     return;
   }
 
-  // -------------------------------------------------------------------- B warps
-  const int bt = threadIdx.x - 32 * (1 + kWsAWarps);
-  uint32_t fb = 0;
-  for (int t = 0; t < nitems; ++t) {
-    Slice sl;
-    const int nt = tiles_of(t, sl);
-    const Item it = items[t];
-    if (bt == 0) {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&done[t]) : "memory");
-      } while (v < G);
-      const uint32_t mbits = *((volatile const uint32_t*)&scratch[it.sidx]);
-      if (nonfinite_bits(mbits)) {
-        s_scale[0] = 0.0f;
-        if (blockIdx.x == 0) atomicOr(flags, kFlagNonfinite);
-      } else {
-        const float sc = int8_scale_from_bits(mbits);
-        s_scale[0] = sc;
-        s_scale[1] = int8_inv(sc);
-        if (blockIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, sc, 0u);
-      }
-    }
-    named_sync(2, kWsB);
-    const float s = s_scale[0], sinv = s_scale[1];
-    const bool ok = s != 0.0f;   // scale is never 0 (R4) except for the non-finite marker
-    const float* g = gbase + it.g_off;
-    float* r = rbase + it.r_off;
-    const uint64_t bo = it.slot_off + 16;
-    uint32_t* body = reinterpret_cast<uint32_t*>(dst.p[0] + bo);
-    for (int k = 0; k < nt; ++k) {
-      const uint32_t st = fb % kWsNB, use = fb / kWsNB;
-      mbar_wait(&fullB[st], use & 1u);
-      const uint64_t q0 = sl.q0 + (uint64_t)k * kWsTQ;
-      const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
-      const WsStageB& S = ringB[st];
-      for (uint32_t j0 = 0; j0 < (uint32_t)kWsTQ; j0 += kWsB) {
-        const uint32_t j = j0 + bt;
-        const bool valid = ok && j < nq;
-        uint32_t w = 0u;
-        if (valid) {
-          const float4 p = S.p[j];
-          const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
-                    a3 = int8_qi(p.w, s, sinv);
-          w = pack_i8x4(a0, a1, a2, a3);
-          st_u32_hint(body + q0 + j, w, pol_stream);
-          if constexpr (EF)
-            st4_hint(r + 4 * (q0 + j),
-                     make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
-                                 __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
-                     pol_stream);
+  if (warp <= AW + BW) {
+    // ------------------------------------------------------------------ B warps
+    const int bt = threadIdx.x - 32 * (1 + AW);
+    uint32_t fb = 0;
+    for (int t = 0; t < nitems; ++t) {
+      Slice sl;
+      const int nt = tiles_of(t, sl);
+      const Item it = items[t];
+      if (bt == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&done[t]) : "memory");
+        } while (v < G);
+        const uint32_t mbits = *((volatile const uint32_t*)&scratch[it.sidx]);
+        if (nonfinite_bits(mbits)) {
+          s_scale[0] = 0.0f;
+          if (blockIdx.x == 0) atomicOr(flags, kFlagNonfinite);
+        } else {
+          const float sc = int8_scale_from_bits(mbits);
+          s_scale[0] = sc;
+          s_scale[1] = int8_inv(sc);
+          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, sc, 0u);
         }
-        push_u32(dst, bo + 4 * (q0 + j), w, valid);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyB[st]);
-      ++fb;
-    }
-    if (blockIdx.x == G - 1 && ok) {
-      if (bt < (int)(it.n & 3)) {
-        const uint64_t e = (it.n >> 2) * 4 + bt;
-        const float p = EF ? r[e] : g[e];
-        const int qe = int8_qi(p, s, sinv);
-        put(dst, bo + e, (uint8_t)(qe & 0xFF));
-        if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+      named_sync(2, kB);
+      const float s = s_scale[0], sinv = s_scale[1];
+      const bool ok = s != 0.0f;   // scale is never 0 (R4) except for the non-finite marker
+      const float* g = gbase + it.g_off;
+      float* r = rbase + it.r_off;
+      const uint64_t bo = it.slot_off + 16;
+      uint32_t* body = reinterpret_cast<uint32_t*>(dst.p[0] + bo);
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t st = fb % kWsNB, use = fb / kWsNB;
+        mbar_wait(&fullB[st], use & 1u);
+        const uint64_t q0 = sl.q0 + (uint64_t)k * kWsTQ;
+        const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
+        const WsStageB& S = ringB[st];
+        for (uint32_t j0 = 0; j0 < (uint32_t)kWsTQ; j0 += kB) {
+          const uint32_t j = j0 + bt;
+          const bool valid = ok && j < nq;
+          uint32_t w = 0u;
+          if (valid) {
+            const float4 p = S.p[j];
+            const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
+                      a3 = int8_qi(p.w, s, sinv);
+            w = pack_i8x4(a0, a1, a2, a3);
+            st_u32_hint(body + q0 + j, w, CW > 0 ? pol_keep : pol_stream);   // fused: C re-reads it from L2
+            if constexpr (EF)
+              st4_hint(r + 4 * (q0 + j),
+                       make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
+                                   __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                       pol_stream);
+          }
+          push_u32(dst, bo + 4 * (q0 + j), w, valid);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyB[st]);
+        ++fb;
       }
-      zero_padding_t(dst, bo, it.n, bt);
+      if (blockIdx.x == G - 1 && ok) {
+        if (bt < (int)(it.n & 3)) {
+          const uint64_t e = (it.n >> 2) * 4 + bt;
+          const float p = EF ? r[e] : g[e];
+          const int qe = int8_qi(p, s, sinv);
+          put(dst, bo + e, (uint8_t)(qe & 0xFF));
+          if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        }
+        zero_padding_t(dst, bo, it.n, bt);
+      }
+      named_sync(2, kB);
+      if (bt == 0) {
+        if constexpr (CW > 0) {
+          // publish this CTA's share of item t; the last CTA tells the peers (P2P)
+          if (dst.n > 1) __threadfence_system();
+          else __threadfence();
+          const unsigned old = atomicAdd(&sa.bdone[t], 1u);
+          if (old == G - 1 && sa.pe.n > 1) {
+            __threadfence_system();
+            for (int c = 0; c < sa.pe.n; ++c)
+              if (c != sa.pe.me) st_release_sys(sa.pe.arrive[c] + (size_t)(sa.b0 + t) * sa.pe.n + sa.pe.me, sa.seq);
+          }
+        }
+        s_bdone = (uint32_t)(t + 1);
+      }
     }
-    named_sync(2, kWsB);
-    if (bt == 0) s_bdone = (uint32_t)(t + 1);
+    if (dst.n > 1) __threadfence_system();
+    return;
   }
-  if (dst.n > 1) __threadfence_system();
+
+  if constexpr (CW > 0) {
+    // ------------------------------------------------------------------ C warps
+    __shared__ float s_out[CW * 32 * 17];
+    const int ct = threadIdx.x - 32 * (1 + AW + BW);
+    const int nb = nitems / sa.PL;
+    switch (sa.src.n) {
+      case 1: ws_reduce_role<1>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 2: ws_reduce_role<2>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 3: ws_reduce_role<3>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 4: ws_reduce_role<4>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 5: ws_reduce_role<5>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 6: ws_reduce_role<6>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      case 7: ws_reduce_role<7>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+      default: ws_reduce_role<8>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+    }
+  }
 }
 
 
@@ -1579,14 +1799,15 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
     Mark mk(L, PH_INT8_ONCHIP);
     cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
     unsigned* done = done_words;
+    StepArgs sa{};
     void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
-                    (void*)&flags, (void*)&done};
-    const void* f = ef ? (const void*)k_int8_ws<true> : (const void*)k_int8_ws<false>;
+                    (void*)&flags, (void*)&done, (void*)&sa};
+    const void* f = ef ? (const void*)k_int8_ws<true, 8, 23, 0> : (const void*)k_int8_ws<false, 8, 23, 0>;
     const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_int8_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_int8_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
     int sms = 0, dev = 0;
@@ -1658,21 +1879,65 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
   ++*L.launches;
 }
 
-// ----------------------------------------------------------------------------- P2P flags
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+// ----------------------------------------------------------------------------- INT8 step
+// compress + exchange + decompress/average of an INT8 call in ONE cooperative kernel (the
+// warp-specialised kernel with reduce warps).  bar_words: 2 * nitems words (done, bdone).
+// Warp splits (A, B, C) of the fused step; config 0 is the default, the rest a tuning sweep.
+template <bool EF>
+static const void* step_kernel(int config) {
+  switch (config) {
+    case 1: return (const void*)k_int8_ws<EF, 4, 18, 9>;
+    case 2: return (const void*)k_int8_ws<EF, 5, 16, 10>;
+    case 3: return (const void*)k_int8_ws<EF, 4, 20, 7>;
+    case 4: return (const void*)k_int8_ws<EF, 5, 20, 6>;
+    case 5: return (const void*)k_int8_ws<EF, 4, 16, 11>;
+    case 6: return (const void*)k_int8_ws<EF, 6, 16, 9>;
+    case 7: return (const void*)k_int8_ws<EF, 3, 18, 10>;
+    case 8: return (const void*)k_int8_ws<EF, 4, 14, 13>;
+    case 9: return (const void*)k_int8_ws<EF, 3, 15, 13>;
+    case 10: return (const void*)k_int8_ws<EF, 4, 15, 12>;
+    default: return (const void*)k_int8_ws<EF, 5, 18, 8>;
+  }
 }
 
+void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                      const Dests& dst_in, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
+                      int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
+                      uint64_t seq, int config) {
+  Mark mk(L, PH_INT8_STEP);
+  cudaMemsetAsync(bar_words, 0, sizeof(unsigned) * 2 * (size_t)nitems, L.stream);
+  Dests dst = dst_in;
+  unsigned* done = bar_words;
+  StepArgs sa{};
+  sa.ritems = ritems;
+  sa.src = src;
+  sa.obase = obase;
+  sa.bdone = bar_words + nitems;
+  sa.pe = pe;
+  sa.local_arrive = local_arrive;
+  sa.seq = (unsigned long long)seq;
+  sa.b0 = b0;
+  sa.PL = PL;
+  void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&scratch,
+                  (void*)&flags, (void*)&done, (void*)&sa};
+  const void* f = ef ? step_kernel<true>(config) : step_kernel<false>(config);
+  const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
+  static bool attr = false;
+  if (!attr) {
+    for (int c = 0; c < 11; ++c) {
+      cudaFuncSetAttribute(step_kernel<true>(c), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(step_kernel<false>(c), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    attr = true;
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchCooperativeKernel(f, dim3(sms), dim3(kWsThreads), args, smem, L.stream);
+  ++*L.launches;
+}
+
+// ----------------------------------------------------------------------------- P2P flags
 // Signal every peer that our payloads of exchange `seq` sit in its slots, then wait for every
 // peer's signal.  The compress kernels ended with a system-scope fence after their pushes, and
 // stream order puts them before this kernel; the release store publishes them.  A peer that

@@ -112,6 +112,7 @@ struct nebula_ctx {
   // INT8 single-pass on-chip kernel (cooperative grid)
   int int8_kernel = 0;          // NEBULA_OPT_INT8_KERNEL
   int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
+  int step_fusion = 0;          // NEBULA_OPT_STEP_FUSION: 0 fuse INT8 steps where eligible, 1 never
   bool onchip_ok = false;
   int onchip_grid = 0;
   size_t onchip_smem = 0;
@@ -567,7 +568,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     }
     if (codec->method == NEBULA_INT8) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
-      if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
+      if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (2 * ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
         ctx->err = "barrier allocation failed";
         return bail(NEBULA_ERR_OOM);
       }
@@ -823,7 +824,68 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
   return NEBULA_OK;
 }
 
+// The fused INT8 step (one cooperative kernel for compress + exchange + reduce), when the
+// call is one the warp-specialised kernel serves and the exchange is LOOPBACK or P2P.
+static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
+                         uint64_t step) {
+  if (ctx->step_fusion == 1 || method_at(ctx, step) != M_INT8 || ctx->G != 1 || !ctx->onchip_ok) return false;
+  if (!(ctx->loopback || ctx->P == 1 || ctx->xmode >= 2)) return false;
+  if (!(ctx->int8_kernel == 0 || ctx->int8_kernel == 12)) return false;
+  if (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) < (uint64_t)(hi - lo) * (1ull << 20)) return false;
+  const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
+  const Table& T = ctx->ctab[lay][t];
+  const Table& R = ctx->rtab[lay][t];
+  if (!T.aligned || !R.aligned || (uintptr_t)g % 16 || (uintptr_t)out % 16) return false;
+  for (int i = lo + 1; i < hi; ++i)
+    if ((ctx->b[i].seq & 1) != (ctx->b[lo].seq & 1)) return false;   // the staged path reports it
+  return true;
+}
+
+static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* dev_grad,
+                                     float* dev_out) {
+  const bool ef = ctx->codec.error_feedback != 0;
+  const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
+  const Table& T = ctx->ctab[lay][t];
+  const Table& R = ctx->rtab[lay][t];
+  const Launch L = launch_of(ctx);
+  for (int i = lo; i < hi; ++i) ctx->b[i].seq += 1;
+  {
+    Mark mk(L, PH_MEMSET);
+    if (bucket == NEBULA_ALL_BUCKETS) {
+      CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
+    } else {
+      for (int c = 0; c < ctx->Ploc; ++c)
+        CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
+    }
+  }
+  Peers pe{};
+  if (!ctx->loopback && ctx->P > 1) {
+    for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
+    pe.n = ctx->P;
+    pe.me = ctx->me;
+  }
+  launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, ctx->b[lo]),
+                   ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
+                   sources_of(ctx, ctx->b[lo]), dev_out, pe, ctx->d_arrive, ctx->b[lo].seq,
+                   // auto warp split: pull mode spends more warps on the NVLink loads of the reduce
+                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 5 : 0));
+  CKC(cudaGetLastError());
+  for (int i = lo; i < hi; ++i) {
+    ctx->b[i].state = ST_IDLE;
+    ctx->b[i].method = M_INT8;
+  }
+  return NEBULA_OK;
+}
+
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
+  if (ctx) {
+    int lo, hi;
+    if (range_of(ctx, bucket, &lo, &hi) && hi > lo && dev_grad && dev_out &&
+        step_fusable(ctx, lo, hi, bucket, dev_grad, dev_out, step)) {
+      DevGuard dg(ctx->device);
+      return int8_step_fused(ctx, lo, hi, bucket, dev_grad, dev_out);
+    }
+  }
   nebula_status s = nebula_compress(ctx, bucket, dev_grad, step);
   if (s != NEBULA_OK) return s;
   s = nebula_exchange(ctx, bucket);
@@ -953,6 +1015,11 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->int8_kernel = (int)value;
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_STEP_FUSION) {
+    if (value < 0 || value > 12) return fail(ctx, NEBULA_ERR_INVALID_ARG, "step fusion option must be in [0, 12]");
+    ctx->step_fusion = (int)value;
+    return NEBULA_OK;
+  }
   if (option == NEBULA_OPT_FP16_KERNEL) {
     if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "FP16 kernel option must be 0 or 1");
     ctx->fp16_kernel = (int)value;
@@ -1011,7 +1078,7 @@ const char* nebula_phase_name(uint32_t phase) {
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
       "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
-      "p2p_exchange_flags"};
+      "p2p_exchange_flags", "int8_fused_step"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

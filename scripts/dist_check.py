@@ -44,7 +44,7 @@ def main():
     P, cl, lr = nb.topology_for_rank(rank, world, G)
     sizes = [4096 * G, 12288 * G, 300004 * G, 8 * G]
     total = sum(sizes)
-    cases = [(O.INT8, 0, "two-pass"), (O.INT8, 0, "onchip"), (O.FP16, 0, None), (O.IDENTITY, 0, None),
+    cases = [(O.INT8, 0, "two-pass"), (O.INT8, 0, "onchip"), (O.INT8, 0, "fused-ws"), (O.FP16, 0, None), (O.IDENTITY, 0, None),
              (O.TOPK, O.VAL_F32, None), (O.TOPK, O.VAL_I8, None), (O.TOPK, O.VAL_F16, None)]
     modes_seen = set()
     for method, vt, kern in cases:

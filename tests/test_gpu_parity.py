@@ -36,7 +36,10 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
     if int8_kernel:
-        ctx.set_int8_kernel(int8_kernel)
+        staged = int8_kernel.endswith("-staged")     # the same compress kernel, no step fusion
+        ctx.set_int8_kernel(int8_kernel[:-len("-staged")] if staged else int8_kernel)
+        if staged:
+            ctx.set_step_fusion(False)
     if fp16_kernel:
         ctx.set_fp16_kernel(fp16_kernel)
     codec = O.Codec(method=method, topk_values=vt, topk_k=k, topk_density=rho, error_feedback=ef,
@@ -111,7 +114,7 @@ def test_dense_parity(nb, method, P, sizes):
 
 @pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-recompute", "fused-park-lag1",
                                          "fused-recompute-lag1", "fused-split", "fused-smem", "fused-tma",
-                                         "fused-ws"])
+                                         "fused-ws", "fused-ws-staged"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
 @pytest.mark.parametrize("ef", [True, False])
 def test_int8_kernels(nb, int8_kernel, sizes, ef):
@@ -120,11 +123,41 @@ def test_int8_kernels(nb, int8_kernel, sizes, ef):
     run_loopback(nb, O.INT8, sizes, 2, steps=2, ef=ef, int8_kernel=int8_kernel)
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem", "fused-tma", "fused-ws"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem", "fused-tma", "fused-ws",
+                                         "fused-ws-staged"])
 def test_int8_near_half_integer_quotients(nb, int8_kernel):
     # exercises the exact fallback of the reciprocal-multiply fast path (int8_q_fast)
     run_loopback(nb, O.INT8, [50001, 4096], 2, kind="half-ties", steps=1, ef=False, int8_kernel=int8_kernel)
     run_loopback(nb, O.INT8, [50001], 2, kind="half-ties", steps=2, int8_kernel=int8_kernel)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_int8_fused_step(nb, P, per_bucket):
+    # the one-kernel INT8 step (compress + exchange + reduce): every P (both subtree
+    # schedules of the reduce warps), whole-group / ragged / tiny buckets, ALL and per bucket
+    run_loopback(nb, O.INT8, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003], P, steps=3, per_bucket=per_bucket,
+                 int8_kernel="fused-ws")
+
+
+def test_int8_fused_step_is_one_launch(nb):
+    import torch
+    sizes = [1 << 20, 1 << 20]
+    ctx = nb.SyncContext(sizes, nb.INT8, num_clusters=2, transport=nb.LOOPBACK)
+    g = torch.randn(2 * sum(sizes), device="cuda")
+    out = torch.empty(sum(sizes), device="cuda")
+    ctx.step(nb.ALL_BUCKETS, g, out, 0)
+    ctx.check()
+    n0 = ctx.kernel_launches()
+    ctx.step(nb.ALL_BUCKETS, g, out, 1)
+    ctx.check()
+    assert ctx.kernel_launches() - n0 == 1
+    ctx.set_step_fusion(False)
+    n0 = ctx.kernel_launches()
+    ctx.step(nb.ALL_BUCKETS, g, out, 2)
+    ctx.check()
+    assert ctx.kernel_launches() - n0 == 2
+    ctx.destroy()
 
 
 def test_topk_i8_near_half_integer_quotients(nb):
