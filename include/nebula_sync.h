@@ -158,7 +158,7 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 
 /* All three stages.  Same results, bit for bit, as compress + exchange + decompress_reduce.
  * For INT8 with 16-B aligned pointers, buckets averaging >= 1M elements, G = 1 and a LOOPBACK
- * or P2P (push / pull) exchange, the three stages run as ONE cooperative kernel
+ * or P2P pull exchange, the three stages run as ONE cooperative kernel
  * (NEBULA_OPT_STEP_FUSION): reduce warps average bucket b — pulling the peers' payloads over
  * NVLink once their system-scope arrival flags say they are complete — while the compress
  * warps of the same kernel stream bucket b+1.  A peer that never arrives sets the peer-timeout

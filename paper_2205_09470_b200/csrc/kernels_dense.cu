@@ -1215,11 +1215,127 @@ struct StepArgs {
   int PL;                            // compress items per bucket (clusters computed on this GPU)
 };
 
-// Reduce role: buckets in order; this CTA's share of bucket b is the same quad slice its B
+// Reduce role, TMA variant (LOOPBACK: every payload is local): warp 0 of the group is the
+// producer — per bucket it waits until every cluster's payload is complete (grid counter
+// bdone), then bulk-copies this CTA's quad slice of all P payloads into a 3-stage shared-memory
+// ring; the other warps decode one quad per lane from shared memory, tree-sum, divide and store
+// float4 (each warp store = 512 contiguous bytes).  The producer also writes the < 4 tail
+// elements of the last slice.  A stage descriptor with nq = ~0 ends the consumers.  (For P2P
+// pull, NVLink-latency bulk copies would sit in the TMA queue ahead of the A/B ring copies:
+// measured slower there, so pull uses the register-load variant below.)
+constexpr int kWsNC = 3;
+constexpr uint32_t kWsCStage = 16384;   // payload bytes of all P clusters per C stage
+struct WsCMeta {
+  float* out;                           // output of the stage's first quad
+  uint32_t nq;                          // quads in the stage (~0: stop)
+  float sc[8];
+};
+
+template <int P>
+__device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct, int nC, unsigned char* ringC,
+                                              uint64_t* fullC, uint64_t* emptyC, WsCMeta* meta) {
+  constexpr uint32_t TB = (kWsCStage / P) & ~15u;   // bytes per cluster per stage
+  constexpr uint32_t TQ = TB / 4;                   // quads per stage
+  const unsigned G = gridDim.x;
+  const int lane = ct & 31;
+  if (ct < 32) {
+    // ------------------------------------------------------------------ C producer
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_first();
+    uint32_t fc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const RItem it = a.ritems[b];
+      const uint64_t n4 = it.n >> 2;
+      const Slice sl = slice_of(n4, G);
+      const bool tail = blockIdx.x == G - 1 && (it.n & 3);
+      if (sl.q1 <= sl.q0 && !tail) continue;
+      for (int c = 0; c < a.PL; ++c) {
+        const unsigned* w = a.bdone + b * a.PL + c;
+        unsigned v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+          if (v >= G) break;
+          __nanosleep(64);
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy payload writes -> TMA reads
+      float sc[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        sc[k] = *reinterpret_cast<volatile const float*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 8);
+      float* out = a.obase + it.out_off;
+      for (uint64_t q = sl.q0; q < sl.q1; q += TQ) {
+        const uint32_t nq = (uint32_t)min((uint64_t)TQ, sl.q1 - q);
+        const uint32_t st = fc % kWsNC, use = fc / kWsNC;
+        if (use) mbar_wait(&emptyC[st], (use - 1) & 1u);
+        meta[st].out = out + 4 * q;
+        meta[st].nq = nq;
+#pragma unroll
+        for (int k = 0; k < P; ++k) meta[st].sc[k] = sc[k];
+        const uint32_t bytes = (nq * 4 + 15) & ~15u;   // within the 16-B padded section
+        mbar_expect_tx(&fullC[st], P * bytes);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          bulk_g2s(ringC + st * kWsCStage + k * TB, a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + 4 * q, bytes,
+                   &fullC[st], pol);
+        ++fc;
+      }
+      if (tail) {
+        for (uint64_t e = n4 * 4; e < it.n; ++e) {
+          float v[P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            const int8_t qv = *reinterpret_cast<volatile const int8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
+            v[k] = __fmul_rn((float)qv, sc[k]);
+          }
+          out[e] = div_p<P>(tree_sum<0, P>(v));
+        }
+      }
+    }
+    const uint32_t st = fc % kWsNC, use = fc / kWsNC;
+    if (use) mbar_wait(&emptyC[st], (use - 1) & 1u);
+    meta[st].nq = 0xFFFFFFFFu;
+    mbar_arrive(&fullC[st]);
+    return;
+  }
+  // -------------------------------------------------------------------- C consumers
+  const int cc = ct - 32, ncons = nC - 32;
+  const uint64_t pol = l2_evict_first();
+  uint32_t fc = 0;
+  while (true) {
+    const uint32_t st = fc % kWsNC, use = fc / kWsNC;
+    mbar_wait(&fullC[st], use & 1u);
+    const uint32_t nq = meta[st].nq;
+    if (nq == 0xFFFFFFFFu) break;
+    float* out = meta[st].out;
+    float sc[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) sc[k] = meta[st].sc[k];
+    const uint32_t* pay = reinterpret_cast<const uint32_t*>(ringC + st * kWsCStage);
+    for (uint32_t j = cc; j < nq; j += ncons) {
+      float t[4][P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const uint32_t w = pay[k * (TB / 4) + j];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e][k] = __fmul_rn((float)(int8_t)((w >> (8 * e)) & 0xFF), sc[k]);
+      }
+      st4_hint(out + 4 * j,
+               make_float4(div_p<P>(tree_sum<0, P>(t[0])), div_p<P>(tree_sum<0, P>(t[1])),
+                           div_p<P>(tree_sum<0, P>(t[2])), div_p<P>(tree_sum<0, P>(t[3]))),
+               pol);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emptyC[st]);
+    ++fc;
+  }
+}
+
+// Reduce role, register-load variant (P2P pull): buckets in order; this CTA's share of bucket b is the same quad slice its B
 // warps quantised, in 16-element groups (one 16-B load per cluster), staged through a per-warp
 // shared-memory transpose so each store instruction writes 512 contiguous bytes.
 template <int P>
-__device__ __forceinline__ void ws_reduce_role(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
+__device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
                                                volatile uint32_t* s_abort, float* s_out, uint32_t* flags) {
   constexpr int E = 16, SROW = E + 1, U = P <= 2 ? 2 : 1;
   const unsigned G = gridDim.x;
@@ -1362,7 +1478,8 @@ __device__ __forceinline__ void ws_reduce_role(const StepArgs& a, int nb, int ct
   }
 }
 
-template <bool EF, int AW, int BW, int CW>
+// CM: reduce role — 0 none (compress only), 1 TMA variant (LOOPBACK), 2 register loads (P2P pull)
+template <bool EF, int AW, int BW, int CW, int CM>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
@@ -1377,6 +1494,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   __shared__ float s_scale[2];
   __shared__ float s_sc[16];
   __shared__ volatile uint32_t s_abort;
+  __shared__ __align__(8) uint64_t fullC[kWsNC], emptyC[kWsNC];
+  __shared__ WsCMeta s_cmeta[CM == 1 ? kWsNC : 1];
   const unsigned G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -1385,6 +1504,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     s_pdone = 0;
     s_bdone = 0;
     s_abort = 0;
+    if (CM == 1)
+      for (int i = 0; i < kWsNC; ++i) { mbar_init(&fullC[i], 1); mbar_init(&emptyC[i], CW > 1 ? CW - 1 : 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1576,6 +1697,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
         zero_padding_t(dst, bo, it.n, bt);
       }
+      if constexpr (CW > 0) asm volatile("fence.proxy.async.global;" ::: "memory");   // payload -> C's TMA reads
       named_sync(2, kB);
       if (bt == 0) {
         if constexpr (CW > 0) {
@@ -1598,18 +1720,37 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 
   if constexpr (CW > 0) {
     // ------------------------------------------------------------------ C warps
-    __shared__ float s_out[CW * 32 * 17];
     const int ct = threadIdx.x - 32 * (1 + AW + BW);
     const int nb = nitems / sa.PL;
-    switch (sa.src.n) {
-      case 1: ws_reduce_role<1>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 2: ws_reduce_role<2>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 3: ws_reduce_role<3>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 4: ws_reduce_role<4>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 5: ws_reduce_role<5>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 6: ws_reduce_role<6>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      case 7: ws_reduce_role<7>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
-      default: ws_reduce_role<8>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags); break;
+    if constexpr (CM == 1) {
+      static_assert(CW >= 2, "the TMA reduce role needs a producer warp and consumer warps");
+      unsigned char* ringC = ws_smem + sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
+#define NB_C(PP) ws_reduce_tma<PP>(sa, nb, ct, kC, ringC, fullC, emptyC, s_cmeta)
+      switch (sa.src.n) {
+        case 1: NB_C(1); break;
+        case 2: NB_C(2); break;
+        case 3: NB_C(3); break;
+        case 4: NB_C(4); break;
+        case 5: NB_C(5); break;
+        case 6: NB_C(6); break;
+        case 7: NB_C(7); break;
+        default: NB_C(8); break;
+      }
+#undef NB_C
+    } else {
+      __shared__ float s_out[CW * 32 * 17];
+#define NB_C(PP) ws_reduce_ld<PP>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags)
+      switch (sa.src.n) {
+        case 1: NB_C(1); break;
+        case 2: NB_C(2); break;
+        case 3: NB_C(3); break;
+        case 4: NB_C(4); break;
+        case 5: NB_C(5); break;
+        case 6: NB_C(6); break;
+        case 7: NB_C(7); break;
+        default: NB_C(8); break;
+      }
+#undef NB_C
     }
   }
 }
@@ -1802,12 +1943,12 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
     StepArgs sa{};
     void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
                     (void*)&flags, (void*)&done, (void*)&sa};
-    const void* f = ef ? (const void*)k_int8_ws<true, 8, 23, 0> : (const void*)k_int8_ws<false, 8, 23, 0>;
+    const void* f = ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0> : (const void*)k_int8_ws<false, 8, 23, 0, 0>;
     const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
     int sms = 0, dev = 0;
@@ -1886,17 +2027,19 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
 template <bool EF>
 static const void* step_kernel(int config) {
   switch (config) {
-    case 1: return (const void*)k_int8_ws<EF, 4, 18, 9>;
-    case 2: return (const void*)k_int8_ws<EF, 5, 16, 10>;
-    case 3: return (const void*)k_int8_ws<EF, 4, 20, 7>;
-    case 4: return (const void*)k_int8_ws<EF, 5, 20, 6>;
-    case 5: return (const void*)k_int8_ws<EF, 4, 16, 11>;
-    case 6: return (const void*)k_int8_ws<EF, 6, 16, 9>;
-    case 7: return (const void*)k_int8_ws<EF, 3, 18, 10>;
-    case 8: return (const void*)k_int8_ws<EF, 4, 14, 13>;
-    case 9: return (const void*)k_int8_ws<EF, 3, 15, 13>;
-    case 10: return (const void*)k_int8_ws<EF, 4, 15, 12>;
-    default: return (const void*)k_int8_ws<EF, 5, 18, 8>;
+    // LOOPBACK (TMA reduce role)
+    case 1: return (const void*)k_int8_ws<EF, 5, 20, 6, 1>;
+    case 2: return (const void*)k_int8_ws<EF, 6, 22, 3, 1>;
+    case 3: return (const void*)k_int8_ws<EF, 6, 20, 5, 1>;
+    // P2P pull (register-load reduce role); 4 is the pull default
+    case 4: return (const void*)k_int8_ws<EF, 4, 16, 11, 2>;
+    case 5: return (const void*)k_int8_ws<EF, 5, 16, 10, 2>;
+    case 6: return (const void*)k_int8_ws<EF, 4, 15, 12, 2>;
+    case 7: return (const void*)k_int8_ws<EF, 3, 16, 12, 2>;
+    case 8: return (const void*)k_int8_ws<EF, 4, 17, 10, 2>;
+    case 9: return (const void*)k_int8_ws<EF, 5, 18, 8, 2>;
+    case 10: return (const void*)k_int8_ws<EF, 3, 17, 11, 2>;
+    default: return (const void*)k_int8_ws<EF, 8, 19, 4, 1>;   // LOOPBACK default
   }
 }
 
@@ -1921,14 +2064,13 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&scratch,
                   (void*)&flags, (void*)&done, (void*)&sa};
   const void* f = ef ? step_kernel<true>(config) : step_kernel<false>(config);
-  const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
-  static bool attr = false;
-  if (!attr) {
-    for (int c = 0; c < 11; ++c) {
-      cudaFuncSetAttribute(step_kernel<true>(c), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(step_kernel<false>(c), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    attr = true;
+  // the TMA reduce role (LOOPBACK configs) adds its ring; the register-load role uses static smem
+  const bool tma_c = config <= 3 || config > 10;
+  const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB + (tma_c ? (size_t)kWsNC * kWsCStage : 0);
+  static bool attr[2][11] = {};
+  if (!attr[ef][config < 0 || config > 10 ? 0 : config]) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[ef][config < 0 || config > 10 ? 0 : config] = true;
   }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);

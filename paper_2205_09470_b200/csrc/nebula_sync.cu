@@ -829,7 +829,9 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
                          uint64_t step) {
   if (ctx->step_fusion == 1 || method_at(ctx, step) != M_INT8 || ctx->G != 1 || !ctx->onchip_ok) return false;
-  if (!(ctx->loopback || ctx->P == 1 || ctx->xmode >= 2)) return false;
+  // LOOPBACK, or P2P pull (the reduce warps load the peers' payloads); with P2P push the
+  // compress kernel's NVLink stores are cheaper outside the fused kernel (fewer quantise warps)
+  if (!(ctx->loopback || ctx->P == 1 || ctx->xmode == 3)) return false;
   if (!(ctx->int8_kernel == 0 || ctx->int8_kernel == 12)) return false;
   if (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) < (uint64_t)(hi - lo) * (1ull << 20)) return false;
   const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
@@ -867,8 +869,7 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, ctx->b[lo]),
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
                    sources_of(ctx, ctx->b[lo]), dev_out, pe, ctx->d_arrive, ctx->b[lo].seq,
-                   // auto warp split: pull mode spends more warps on the NVLink loads of the reduce
-                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 5 : 0));
+                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0));
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
     ctx->b[i].state = ST_IDLE;
