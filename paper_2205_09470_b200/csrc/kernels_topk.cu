@@ -567,6 +567,11 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
     if (retry == 1 && S.mode != 1) continue;
     if (retry == 2 && (S.t_lo != S.t_hi || S.stage_ovf)) continue;
     const bool ties_only = retry == 2;
+    // tie mode: the selection takes the first need_T = k - W ties in index order, so chunks
+    // whose tie prefix already reaches need_T write nothing
+    const uint64_t cap_c = ties_only ? min((uint64_t)titems[i].ccap, (uint64_t)(titems[i].k > S.wcount ? titems[i].k - S.wcount : 0ull))
+                                     : (uint64_t)titems[i].ccap;
+    if (ties_only && (pref[titems[i].status_off + (c - aitems[i].chunk0)] & 0xFFFFFFFFull) >= cap_c) continue;
     const Item it = aitems[i];
     const TopkItem& ti = titems[i];
     const uint64_t j = c - it.chunk0, n4 = it.n >> 2;
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
             if (pos < ti.wcap && !ties_only) W[pos] = make_uint2(idx, kb[u][e]);
           } else if (key >= t_lo) {
             const uint64_t pos = preC + cc++;
-            if (pos < ti.ccap) C[pos] = make_uint2(idx, kb[u][e]);
+            if (pos < cap_c) C[pos] = make_uint2(idx, kb[u][e]);
           }
         }
       }
@@ -668,7 +673,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
         if (pos < ti.wcap && !ties_only) W[pos] = make_uint2(idx, tkb);
       } else if (key >= t_lo) {
         const uint64_t pos = preC + baseC[kQuadsPerThread];
-        if (pos < ti.ccap) C[pos] = make_uint2(idx, tkb);
+        if (pos < cap_c) C[pos] = make_uint2(idx, tkb);
       }
     }
   }
@@ -704,7 +709,14 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   const uint32_t m = (uint32_t)(C < ti.ccap ? C : ti.ccap);
   uint32_t T, above_c = 0;
   if (S.t_lo == S.t_hi) {
-    T = S.t_lo;
+    // exact tie set: every candidate == T and the list holds the first need ties in index
+    // order (k_topk_write), already the compacted selection
+    if (threadIdx.x == 0) {
+      S.threshold = S.t_lo;
+      S.count_above = W;
+      S.need = need;
+    }
+    return;
   } else {
     auto get = [&](uint32_t i) { return cand[i].y & 0x7FFFFFFFu; };
     // every candidate key lies in [t_lo, min(t_hi, 2^31 - 1)]: their common leading bits are known
@@ -981,29 +993,6 @@ __device__ __forceinline__ int find_by(const RItem* items, int nitems, uint64_t 
   return lo;
 }
 
-// start[c][t] = first entry of cluster c's ascending idx list with idx >= t * kRedTile,
-// t = 0..ntiles (one thread per entry e in [0, k]; each tile's start written exactly once)
-__global__ void k_topk_offsets(const RItem* __restrict__ items, int nitems, uint64_t total,
-                               Dests src, uint32_t* __restrict__ start) {
-  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
-  if (g >= total) return;
-  const int i = find_by(items, nitems, g, [](const RItem& r) { return r.e0; });
-  const RItem it = items[i];
-  const uint64_t e = g - it.e0;  // 0..k
-  const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
-  const uint32_t* idx = reinterpret_cast<const uint32_t*>(src.p[c] + it.slot_off + (uint64_t)c * it.pb + 16);
-  uint32_t* s = start + it.sbase + (uint64_t)c * (ntiles + 1);
-  const int64_t cur = e < it.k ? (int64_t)(idx[e] / kRedTile) : (int64_t)ntiles;
-  const int64_t prev = e == 0 ? -1 : (int64_t)(idx[e - 1] / kRedTile);
-  for (int64_t t = prev + 1; t <= cur; ++t) s[t] = (uint32_t)e;
-}
-
-// Sparse average, owner-computes: the output range was zero-filled (+0.0: every index no
-// cluster selected averages to +0.0/P = +0.0, R16).  One thread per (cluster c, entry e):
-// x = idx_c[e]; the other clusters' lists are searched only inside tile(x)'s range (from the
-// start offsets); the lowest cluster holding x is its owner and writes
-// out[x] = fl(tree_sum(D_0(x) .. D_{P-1}(x)) / P) with +0.0 for clusters that did not select x.
 template <int P>
 __device__ __forceinline__ float div_p_sparse(float x) {
   if constexpr ((P & (P - 1)) == 0) return __fmul_rn(x, 1.0f / (float)P);
@@ -1016,44 +1005,148 @@ __device__ __forceinline__ float topk_decode(const uint8_t* val, uint64_t e, int
   return __fmul_rn((float)(int8_t)val[e], s);
 }
 
-template <int P>
-__global__ void __launch_bounds__(256) k_topk_scatter(const RItem* __restrict__ items, int nitems, uint64_t total,
-                                                      Dests src,
-                                                      const uint32_t* __restrict__ start, float* __restrict__ obase,
-                                                      int vt) {
-  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
-  if (g >= total) return;
-  const int i = find_by(items, nitems, g, [](const RItem& r) { return r.e0; });
-  const RItem it = items[i];
-  const uint64_t e = g - it.e0;
-  if (e >= it.k) return;
-  const uint64_t ntiles = (it.n + kRedTile - 1) / kRedTile;
-  const uint64_t voff = 16 + pad16(4 * it.k);
-  const uint8_t* sc = src.p[c] + it.slot_off + (uint64_t)c * it.pb;
-  const uint32_t x = reinterpret_cast<const uint32_t*>(sc + 16)[e];
-  const uint32_t t = x / kRedTile;
-  float v[P];
+// Sparse average by output tiles (R16: out = fl(tree_sum(D_0..D_{P-1}) / P), +0.0 where a
+// cluster did not select the index).  Persistent WARPS own contiguous ranges of 512-element
+// output sub-tiles (4 per kRedTile tile).  Per sub-tile, the sub-tile's entries of every
+// cluster are a contiguous run of its ascending index list: a running cursor per cluster (one
+// binary search per warp per bucket, then it only advances).  Each lane loads U entries per
+// cluster per round — index and value together (the value's position is the entry's), all P
+// clusters in flight at once — and drops the in-range ones into the warp's zero-filled
+// shared-memory tile [P][512]; then every output element is written once (float4 when
+// aligned, 512 B per warp store).  No memset pass, no per-entry search, no CTA barrier.
+constexpr int kDenThreads = 256, kDenSub = 512;
+
+template <int P, int U, bool VEC>
+__global__ void __launch_bounds__(kDenThreads) k_topk_densify(const RItem* __restrict__ items, int nitems,
+                                                              uint64_t tiles, Dests src, float* __restrict__ obase,
+                                                              int vt) {
+  extern __shared__ __align__(16) float s_v[];   // per warp: [P][kDenSub]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* sw = s_v + (size_t)warp * P * kDenSub;
+  const uint64_t nsub = tiles * (kRedTile / kDenSub);
+  const uint64_t nw = (uint64_t)gridDim.x * (kDenThreads / 32), gw = (uint64_t)blockIdx.x * (kDenThreads / 32) + warp;
+  const uint64_t per = (nsub + nw - 1) / nw;
+  const uint64_t sa = gw * per, sb = min(nsub, sa + per);
+  int i = -1;
+  RItem it{};
+  uint64_t it_end = 0;   // first sub-tile after the current item
+  uint32_t cur[P];
+  const uint8_t* sl[P];
+  float scale[P];
+  for (uint64_t q = sa; q < sb; ++q) {
+    const uint64_t t = q / (kRedTile / kDenSub);
+    if (i < 0 || q >= it_end) {
+      i = find_by(items, nitems, t, [](const RItem& r) { return r.t0; });
+      it = items[i];
+      it_end = (it.t0 + (it.n + kRedTile - 1) / kRedTile) * (kRedTile / kDenSub);
+      const uint32_t x0 = (uint32_t)((q - it.t0 * (kRedTile / kDenSub)) * kDenSub);
 #pragma unroll
-  for (int c2 = 0; c2 < P; ++c2) {
-    const uint8_t* s2 = src.p[c2] + it.slot_off + (uint64_t)c2 * it.pb;
-    const float scale = *reinterpret_cast<const float*>(s2 + 8);
-    if (c2 == c) {
-      v[c2] = topk_decode(s2 + voff, e, vt, scale);
-      continue;
+      for (int c = 0; c < P; ++c) {
+        sl[c] = src.p[c] + it.slot_off + (uint64_t)c * it.pb;
+        scale[c] = vt == V_I8 ? *reinterpret_cast<const float*>(sl[c] + 8) : 1.0f;
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(sl[c] + 16);
+        uint32_t lo = 0, hi = (uint32_t)it.k;   // lower_bound(x0), warp-uniform
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (idx[mid] < x0) lo = mid + 1; else hi = mid;
+        }
+        cur[c] = lo;
+      }
     }
-    const uint32_t* st2 = start + it.sbase + (uint64_t)c2 * (ntiles + 1);
-    uint32_t lo = st2[t], hi = st2[t + 1];
-    const uint32_t* idx2 = reinterpret_cast<const uint32_t*>(s2 + 16);
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (idx2[mid] < x) lo = mid + 1; else hi = mid;
+    const uint32_t e0 = (uint32_t)((q - it.t0 * (kRedTile / kDenSub)) * kDenSub);
+    if (e0 >= it.n) continue;   // past the end of the item's last (partial) tile
+    const uint32_t e1 = (uint32_t)min(it.n, (uint64_t)e0 + (uint64_t)kDenSub);
+#pragma unroll
+    for (int v = 0; v < P * kDenSub / 128; ++v)
+      reinterpret_cast<float4*>(sw)[v * 32 + lane] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    __syncwarp();
+    const uint64_t voff = 16 + pad16(4 * it.k);
+    // round 1: U entries per lane of every cluster in flight at once (U sized from the density)
+    uint32_t more_mask = 0;
+    {
+      uint32_t x[P][U];
+      float val[P][U];
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(sl[c] + 16);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = cur[c] + (uint32_t)(u * 32 + lane);
+          x[c][u] = 0xFFFFFFFFu;
+          val[c][u] = 0.0f;
+          if (e < it.k) {
+            x[c][u] = idx[e];
+            val[c][u] = topk_decode(sl[c] + voff, e, vt, scale[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        uint32_t nin = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool in = x[c][u] < e1;   // >= e0 holds: the cursor is the run's start
+          if (in) sw[c * kDenSub + (x[c][u] - e0)] = val[c][u];
+          nin += __popc(__ballot_sync(0xFFFFFFFFu, in));
+        }
+        cur[c] += nin;
+        if (nin == 32u * U) more_mask |= 1u << c;
+      }
     }
-    const bool found = lo < st2[t + 1] && idx2[lo] == x;
-    if (found && c2 < c) return;           // a lower cluster owns x
-    v[c2] = found ? topk_decode(s2 + voff, lo, vt, scale) : 0.0f;
+    // long runs (dense stretches, e.g. a tie run of zeros): 256 entries per round per cluster
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      if (!(more_mask >> c & 1u)) continue;
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(sl[c] + 16);
+      while (true) {
+        uint32_t x[8];
+        float val[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = cur[c] + (uint32_t)(u * 32 + lane);
+          x[u] = 0xFFFFFFFFu;
+          val[u] = 0.0f;
+          if (e < it.k) {
+            x[u] = idx[e];
+            val[u] = topk_decode(sl[c] + voff, e, vt, scale[c]);
+          }
+        }
+        uint32_t nin = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool in = x[u] < e1;
+          if (in) sw[c * kDenSub + (x[u] - e0)] = val[u];
+          nin += __popc(__ballot_sync(0xFFFFFFFFu, in));
+        }
+        cur[c] += nin;
+        if (nin < 256u) break;
+      }
+    }
+    __syncwarp();
+    float* out = obase + it.out_off + e0;
+    if (VEC && e1 - e0 == (uint32_t)kDenSub) {
+#pragma unroll
+      for (int v = 0; v < kDenSub / 128; ++v) {
+        const int j = v * 32 + lane;
+        float a[P], b[P], d[P], e[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const float4 w = reinterpret_cast<const float4*>(sw + c * kDenSub)[j];
+          a[c] = w.x; b[c] = w.y; d[c] = w.z; e[c] = w.w;
+        }
+        st4(out + 4 * j, make_float4(div_p_sparse<P>(tree_sum<0, P>(a)), div_p_sparse<P>(tree_sum<0, P>(b)),
+                                     div_p_sparse<P>(tree_sum<0, P>(d)), div_p_sparse<P>(tree_sum<0, P>(e))));
+      }
+    } else {
+      for (uint32_t j = lane; j < e1 - e0; j += 32) {
+        float v[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) v[c] = sw[c * kDenSub + j];
+        out[j] = div_p_sparse<P>(tree_sum<0, P>(v));
+      }
+    }
+    __syncwarp();   // the tile buffer is zeroed for the next sub-tile
   }
-  obase[it.out_off + x] = div_p_sparse<P>(tree_sum<0, P>(v));
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1138,38 +1231,46 @@ void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int i
   else topk_select_all<false, false>(L, B, item0, nitems, a_chunks, aitems, g, r, slots, flags, value_type, merge_tiles);
 }
 
+template <int P, int U>
+static void densify_pu(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
+                       const Dests& slots, float* out) {
+  const size_t smem = (size_t)(kDenThreads / 32) * P * kDenSub * sizeof(float);
+  const void* f = vec ? (const void*)k_topk_densify<P, U, true> : (const void*)k_topk_densify<P, U, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[vec]) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[vec] = true;
+  }
+  const unsigned grid = persistent_grid(L, tiles * (kRedTile / kDenSub) / (kDenThreads / 32) + 1, f, kDenThreads, smem);
+  if (vec) k_topk_densify<P, U, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
+  else k_topk_densify<P, U, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
+}
+
+// U = entries per lane per round: sized so a typical 512-element sub-tile's run fits one round
 template <int P>
-static void scatter_p(const Launch& L, int vt, const RItem* items, int nitems, uint64_t entries, const Dests& slots,
-                      const uint32_t* start, float* out) {
-  dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
-  k_topk_scatter<P><<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start, out, vt);
+static void densify_p(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
+                      uint64_t entries, const Dests& slots, float* out) {
+  const double per_sub = (double)entries / (double)(tiles * (kRedTile / kDenSub));   // entries per sub-tile
+  if (per_sub * 1.25 <= 32.0 || P > 4) densify_pu<P, 1>(L, vt, vec, items, nitems, tiles, slots, out);
+  else if (per_sub <= 64.0 || P > 2) densify_pu<P, 2>(L, vt, vec, items, nitems, tiles, slots, out);
+  else densify_pu<P, 4>(L, vt, vec, items, nitems, tiles, slots, out);
 }
 
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
                         uint64_t entries, uint64_t tiles, const Dests& slots, uint32_t* start, float* out,
                         float* zero_begin, uint64_t zero_count) {
-  (void)vec; (void)tiles;
-  {
-    Mark mk(L, PH_MEMSET);
-    if (zero_count) cudaMemsetAsync(zero_begin, 0, zero_count * sizeof(float), L.stream);
-  }
-  if (!entries) return;
-  {
-    Mark mk(L, PH_TOPK_OFFSETS);
-    dim3 grid((unsigned)((entries + 255) / 256), (unsigned)P);
-    k_topk_offsets<<<grid, 256, 0, L.stream>>>(items, nitems, entries, slots, start);
-    ++*L.launches;
-  }
+  (void)start; (void)zero_begin; (void)zero_count;
+  if (!tiles) return;
   Mark mk(L, PH_TOPK_REDUCE);
   switch (P) {
-    case 1: scatter_p<1>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 2: scatter_p<2>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 3: scatter_p<3>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 4: scatter_p<4>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 5: scatter_p<5>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 6: scatter_p<6>(L, value_type, items, nitems, entries, slots, start, out); break;
-    case 7: scatter_p<7>(L, value_type, items, nitems, entries, slots, start, out); break;
-    default: scatter_p<8>(L, value_type, items, nitems, entries, slots, start, out); break;
+    case 1: densify_p<1>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 2: densify_p<2>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 3: densify_p<3>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 4: densify_p<4>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 5: densify_p<5>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 6: densify_p<6>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    case 7: densify_p<7>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
+    default: densify_p<8>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
   }
   ++*L.launches;
 }
