@@ -11,6 +11,8 @@ Per cluster c, per bucket of n fp32 elements, step t (SURVEY.md §8(c) plain def
     FP16 : h = RNE16(p), error iff any h is +-inf;  D = float(h)      PAPER.md:125-130 Eq.5
     INT8 : m = max|p|, s = fl(m/127) (s := 1 if m == 0 or s == 0)    PAPER.md:101, :418, SPEC.md:134-142
            q = clamp(rint(fl(p/s)), -127, 127);  D = fl(q*s)
+    FP8  : m = max|p|, s = fl(m/448) (s := 1 if m == 0 or s == 0)    PAPER.md:101 "8-bit floating point" (R27)
+           c = RNE_E4M3_satfinite(fl(p/s));  D = fl(E4M3(c)*s)
     TOPK : k largest |p| by fp32 bit key, ties -> lower index,        PAPER.md:63, :99 (cited only; R11-R14)
            idx ascending; values f32 | RNE16 | int8 with the INT8 rule
     r_new = fl(p - D)                                                  R15 (error feedback)
@@ -31,11 +33,12 @@ __all__ = [
     "pad16", "payload_bytes", "body_ratio", "fp16_encode", "int8_scale", "int8_quantize",
     "int8_dequantize", "topk_select", "topk_stats", "compress", "decode_payload",
     "tree_sum", "average", "CompressResult", "cluster_step", "oracle_step",
-    "hierarchical_step", "svd_ratio", "FP16_OVERFLOW_ABS",
+    "hierarchical_step", "svd_ratio", "FP16_OVERFLOW_ABS", "FP8",
+    "fp8_e4m3_encode", "fp8_e4m3_decode", "fp8_scale", "FP8_E4M3_MAX",
 ]
 
 F32 = np.float32
-IDENTITY, FP16, INT8, TOPK = 0, 1, 2, 3
+IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 VALUE_BYTES = {VAL_F32: 4, VAL_F16: 2, VAL_I8: 1}
 NONFINITE, OVERFLOW = "NONFINITE", "OVERFLOW"
@@ -44,6 +47,10 @@ NONFINITE, OVERFLOW = "NONFINITE", "OVERFLOW"
 # ulp of the top binade, 32/2); [65504, 65520) rounds down to 65504.  Used only in
 # messages and pins — the oracle decides overflow from the conversion result itself.
 FP16_OVERFLOW_ABS = 65520.0
+
+# R27 (NEXT-4): OCP FP8 E4M3 ("E4M3FN"): 1 sign, 4 exponent bits (bias 7), 3 mantissa bits,
+# no infinities, S.1111.111 = NaN, so the largest finite magnitude is 1.75 * 2^8 = 448.
+FP8_E4M3_MAX = 448.0
 
 
 class NebulaError(Exception):
@@ -94,7 +101,7 @@ def payload_bytes(method: int, n: int, k: int = 0, value_type: int = VAL_F32) ->
         return 16 + pad16(4 * n)
     if method == FP16:
         return 16 + pad16(2 * n)
-    if method == INT8:
+    if method in (INT8, FP8):
         return 16 + pad16(n)
     if method == TOPK:
         return 16 + pad16(4 * k) + pad16(VALUE_BYTES[value_type] * k)
@@ -108,7 +115,7 @@ def body_ratio(method: int, n: int, k: int = 0, value_type: int = VAL_F32) -> fl
         b = 4 * n
     elif method == FP16:
         b = 2 * n
-    elif method == INT8:
+    elif method in (INT8, FP8):
         b = n
     else:
         b = (4 + VALUE_BYTES[value_type]) * k
@@ -160,6 +167,62 @@ def int8_dequantize(q: np.ndarray, s: np.float32) -> np.ndarray:
     return q.astype(F32) * F32(s)
 
 
+def fp8_scale(p: np.ndarray) -> np.float32:
+    """R27: per-bucket symmetric scale mapping max|p| onto the largest finite E4M3 magnitude,
+    s = fl(m / 448); s := 1 if m == 0 or if fl(m/448) underflows to 0 (the INT8 rule R4 with
+    448 in place of 127)."""
+    m = np.max(np.abs(p)) if p.size else F32(0.0)
+    m = F32(m)
+    s = F32(m / F32(FP8_E4M3_MAX))
+    if m == F32(0.0) or s == F32(0.0):
+        s = F32(1.0)
+    return s
+
+
+def fp8_e4m3_encode(x: np.ndarray) -> np.ndarray:
+    """R27: binary32 -> E4M3 code bytes, round to nearest, ties to even mantissa, saturating
+    to +-448 (no infinities in E4M3); the sign is kept, also when the value rounds to zero.
+    Written from the format's definition, in float64 (exact for binary32 inputs): the quantum
+    of the binade holding |x| is 2^(max(e, -6) - 3) with e = floor(log2|x|) (-6 = the smallest
+    normal exponent; below it the subnormal quantum 2^-9 applies)."""
+    x = np.asarray(x, dtype=F32).ravel()
+    if x.size and np.any(np.isnan(x)):
+        raise NebulaError(NONFINITE, "NaN has no saturating E4M3 code")
+    a = np.abs(x.astype(np.float64))
+    sign = np.where(np.signbit(x), 0x80, 0).astype(np.int64)
+    e = np.frexp(a)[1].astype(np.int64) - 1                 # a = f * 2^e, 1 <= f < 2 (a > 0)
+    quantum = np.ldexp(1.0, np.maximum(e, -6) - 3)
+    v = np.rint(a / quantum) * quantum                       # RNE on the exact quotient
+    v = np.minimum(v, FP8_E4M3_MAX)                          # satfinite
+    ev = np.frexp(v)[1].astype(np.int64) - 1
+    normal = v >= 2.0 ** -6
+    code_sub = (v / 2.0 ** -9).astype(np.int64)              # 0.mmm * 2^-6, mmm = v / 2^-9
+    code_norm = ((ev + 7) << 3) | ((v / np.ldexp(1.0, ev - 3)).astype(np.int64) - 8)
+    code = np.where(normal, code_norm, code_sub)
+    code = np.where(a == 0.0, 0, code)
+    return (sign | code).astype(np.uint8)
+
+
+def fp8_e4m3_decode(c: np.ndarray) -> np.ndarray:
+    """E4M3 code bytes -> binary32 (exact: every E4M3 value is a binary32 value)."""
+    c = np.asarray(c, dtype=np.uint8).ravel().astype(np.int64)
+    s = np.where(c & 0x80, -1.0, 1.0)
+    ef, mf = (c >> 3) & 0xF, c & 0x7
+    v = np.where(ef == 0, mf * 2.0 ** -9, (8 + mf) * np.ldexp(1.0, ef - 10))
+    v = np.where((ef == 0xF) & (mf == 0x7), np.nan, v)
+    return (s * v).astype(F32)
+
+
+def fp8_quantize(p: np.ndarray, s: np.float32) -> np.ndarray:
+    """R27: c = RNE_E4M3_satfinite(fl(p / s)) — IEEE binary32 division first (as R6)."""
+    return fp8_e4m3_encode((p / F32(s)).astype(F32))
+
+
+def fp8_dequantize(c: np.ndarray, s: np.float32) -> np.ndarray:
+    """R27: D = fl(E4M3(c) * s), one rounding."""
+    return (fp8_e4m3_decode(c) * F32(s)).astype(F32)
+
+
 def _keys(p: np.ndarray) -> np.ndarray:
     """R11: selection key = fp32 bit pattern with the sign cleared (|p| order, -0 == +0)."""
     return p.view(np.uint32) & np.uint32(0x7FFFFFFF)
@@ -207,8 +270,10 @@ class CompressResult:
     stats: dict = field(default_factory=dict)
 
 
-def compress(p: np.ndarray, method: int, codec: Codec) -> tuple[bytes, np.ndarray, dict]:
+def compress(p: np.ndarray, method: int, codec: Codec, scale=None) -> tuple[bytes, np.ndarray, dict]:
     """Encode p with ``method`` -> (payload bytes, D = decode(payload), stats).
+    ``scale`` overrides the INT8 / FP8 scale (NEXT-3: the exact cluster-wide scale of a
+    hierarchical shard, R28); None = the scale of p itself.
     Raises NebulaError(NONFINITE) on NaN/Inf (SPEC.md:32 'all entries finite', :358) and
     NebulaError(OVERFLOW) when an fp16-encoded value overflows."""
     p = np.ascontiguousarray(p, dtype=F32)
@@ -220,10 +285,15 @@ def compress(p: np.ndarray, method: int, codec: Codec) -> tuple[bytes, np.ndarra
         h = fp16_encode(p)
         return _preamble(FP16, n, 1.0, 0) + _pad(h.tobytes()), h.astype(F32), {}
     if method == INT8:
-        s = int8_scale(p)
+        s = int8_scale(p) if scale is None else F32(scale)
         q = int8_quantize(p, s)
         return (_preamble(INT8, n, float(s), 0) + _pad(q.tobytes()),
                 int8_dequantize(q, s), {"scale": float(s)})
+    if method == FP8:
+        s = fp8_scale(p) if scale is None else F32(scale)
+        c = fp8_quantize(p, s)
+        return (_preamble(FP8, n, float(s), 0) + _pad(c.tobytes()),
+                fp8_dequantize(c, s), {"scale": float(s)})
     if method == TOPK:
         k = topk_k(n, codec)
         idx = topk_select(p, k)
@@ -261,6 +331,8 @@ def decode_payload(payload: bytes, n: int) -> np.ndarray:
     if method == INT8:
         q = np.frombuffer(body, dtype=np.int8, count=n)
         return int8_dequantize(q, F32(scale))
+    if method == FP8:
+        return fp8_dequantize(np.frombuffer(body, dtype=np.uint8, count=n), F32(scale))
     if method == TOPK:
         k = count
         idx = np.frombuffer(body, dtype="<u4", count=k).astype(np.int64)
@@ -299,7 +371,7 @@ def average(payloads: list, n: int) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- steps
-def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int) -> CompressResult:
+def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int, scale=None) -> CompressResult:
     """One cluster's compress with error feedback (R15):
     lossy: p = fl(g + r); payload = C(p); r_new = fl(p - D(C(p))).
     IDENTITY (t < start_step): payload = g, residual untouched."""
@@ -314,41 +386,57 @@ def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int) -
         p = (g + np.asarray(r, dtype=F32)).astype(F32)
     else:
         p = g
-    payload, D, st = compress(p, method, codec)
+    payload, D, st = compress(p, method, codec, scale)
     r_new = (p - D).astype(F32) if codec.error_feedback else (None if r is None else r.copy())
     return CompressResult(payload, D, r_new, method, st)
 
 
-def oracle_step(gs: list, rs: list, codec: Codec, step: int):
+def oracle_step(gs: list, rs: list, codec: Codec, step: int, scales=None):
     """Whole step for P clusters: compress each cluster, exchange the
     payload bodies (slot c = cluster c), and have every cluster decompress-average all
-    P slots.  Returns (out, [r_new_c], [payload_c], [stats_c])."""
-    res = [cluster_step(g, r, codec, step) for g, r in zip(gs, rs)]
+    P slots.  scales[c] overrides cluster c's INT8/FP8 scale (R28).
+    Returns (out, [r_new_c], [payload_c], [stats_c])."""
+    if scales is None:
+        scales = [None] * len(gs)
+    res = [cluster_step(g, r, codec, step, s) for g, r, s in zip(gs, rs, scales)]
     n = np.asarray(gs[0]).size
     out = average([x.payload for x in res], n)
     return out, [x.r_new for x in res], [x.payload for x in res], [x.stats for x in res]
 
 
-def hierarchical_step(gs: list, rs: list, codec: Codec, step: int):
+def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: bool = False):
     """P clusters x G GPUs (R20, PAPER.md:95 / :288 intra-cluster parallelism + compressed
     inter-cluster hop).  gs[c][l] is GPU l of cluster c's full bucket (n % G == 0);
     rs[c][l] its residual shard.  The cluster gradient is the fp32 mean of its G GPUs
     (sum in GPU order, then / G; tests feed dyadic inputs so any order is exact);
     GPU l codes shard l; peers with the same l exchange; shards are all-gathered.
+    exact_scale (NEXT-3, R28): the INT8 / FP8 scale of every shard is the scale of the whole
+    cluster bucket p_c = concat_l(p_{c,l}) (max over all G shards) instead of the shard's own.
     Returns (out, rs_new[c][l], payloads[c][l])."""
     P, G = len(gs), len(gs[0])
     n = np.asarray(gs[0][0]).size
     assert n % G == 0
     m = n // G
     outs, rs_new, pls = [], [[None] * G for _ in range(P)], [[None] * G for _ in range(P)]
+    shards = [[None] * G for _ in range(P)]
     for l in range(G):
-        shards = []
         for c in range(P):
             acc = np.asarray(gs[c][0][l * m:(l + 1) * m], dtype=F32)
             for j in range(1, G):
                 acc = (acc + np.asarray(gs[c][j][l * m:(l + 1) * m], dtype=F32)).astype(F32)
-            shards.append((acc / F32(G)).astype(F32))
-        out_l, r_l, p_l, _ = oracle_step(shards, [rs[c][l] for c in range(P)], codec, step)
+            shards[c][l] = (acc / F32(G)).astype(F32)
+    scales = [None] * P
+    method = select_method(codec, step)
+    if exact_scale and method in (INT8, FP8):
+        for c in range(P):
+            ps = [shards[c][l] if not codec.error_feedback else
+                  (shards[c][l] + (np.zeros(m, F32) if rs[c][l] is None else np.asarray(rs[c][l], F32))).astype(F32)
+                  for l in range(G)]
+            p_c = np.concatenate(ps)
+            scales[c] = int8_scale(p_c) if method == INT8 else fp8_scale(p_c)
+    for l in range(G):
+        out_l, r_l, p_l, _ = oracle_step([shards[c][l] for c in range(P)], [rs[c][l] for c in range(P)], codec, step,
+                                         scales)
         outs.append(out_l)
         for c in range(P):
             rs_new[c][l] = r_l[c]

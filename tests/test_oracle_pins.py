@@ -402,3 +402,125 @@ def test_hierarchical_G1_equals_flat():
     hier, rh, ph = O.hierarchical_step([[g] for g in gs], [[None] for _ in gs], codec, 0)
     assert np.array_equal(flat, hier)
     assert all(pf[c] == ph[c][0] for c in range(4))
+
+
+# ----------------------------------------------------------------- FP8 E4M3 (NEXT-4, R27)
+def test_fp8_textbook_encodings():
+    g = gold("fp8_e4m3.json")
+    for case in g["cases"]:
+        x = np.array([float(case["x"])], F32)
+        code = int(O.fp8_e4m3_encode(x)[0])
+        assert code == int(case["code"], 16), case
+    # every finite code decodes to the value its bit fields define; the 126 positive finite
+    # codes are strictly increasing (a monotone, gap-free table)
+    vals = O.fp8_e4m3_decode(np.arange(0, 127, dtype=np.uint8)).astype(np.float64)
+    assert vals[0] == 0.0 and vals[-1] == 448.0 and np.all(np.diff(vals) > 0)
+    assert np.isnan(O.fp8_e4m3_decode(np.array([0x7F, 0xFF], np.uint8))).all()
+
+
+def test_fp8_matches_library_conversion():
+    """Against an independent implementation: PyTorch's float8_e4m3fn cast (RNE, no
+    saturation — so inputs stay inside the finite range, |x| < 464)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal(400000) * np.exp(rng.uniform(-14, 7, 400000))).astype(F32)
+    x = x[np.abs(x) < 464]
+    ours = O.fp8_e4m3_encode(x)
+    lib = torch.from_numpy(x).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert np.array_equal(ours, lib)
+    # round trip: decode(encode(v)) == v for every representable v
+    vals = O.fp8_e4m3_decode(np.arange(0, 256, dtype=np.uint8))
+    fin = ~np.isnan(vals)
+    assert np.array_equal(O.fp8_e4m3_decode(O.fp8_e4m3_encode(vals[fin])), vals[fin])
+
+
+@pytest.mark.parametrize("kind", ["normal", "model-like", "uniform", "ties", "mixed-scale", "subnormal"])
+def test_fp8_exact_rational_properties(kind):
+    """R27 in the rationals: s = m/448 correctly rounded; c = nearest E4M3 value of the
+    rounded quotient t = fl(p/s) (distance to every other finite E4M3 value no smaller,
+    ties to an even mantissa); D = c*s correctly rounded."""
+    g = synthetic(3000, 12, kind)
+    payload, D, st = O.compress(g, O.FP8, O.Codec(method=O.FP8))
+    s = F32(st["scale"])
+    m = Fraction(float(np.max(np.abs(g))))
+    if m != 0 and float(s) != 1.0:
+        exact, sf = m / 448, Fraction(float(s))
+        for nb in (np.nextafter(s, F32(np.inf)), np.nextafter(s, F32(0))):
+            assert abs(sf - exact) <= abs(Fraction(float(nb)) - exact)
+    table = [Fraction(float(v)) for v in O.fp8_e4m3_decode(np.arange(0, 127, dtype=np.uint8))]
+    codes = np.frombuffer(payload, dtype=np.uint8, offset=16, count=g.size)
+    sF = Fraction(float(s))
+    for i in range(0, g.size, 11):
+        t = Fraction(float(F32(g[i]) / s))
+        c = int(codes[i])
+        mag = c & 0x7F
+        assert (c >> 7) == int(np.signbit(g[i]))
+        dist = abs(abs(t) - table[mag])
+        best = min(abs(abs(t) - v) for v in table)
+        assert dist == best
+        if sum(1 for v in table if abs(abs(t) - v) == best) > 1:
+            assert mag % 2 == 0                                      # ties -> even mantissa
+        d = Fraction(float(D[i]))
+        prod = (-1 if c >> 7 else 1) * table[mag] * sF
+        assert abs(d - prod) <= max(abs(prod) * Fraction(1, 2 ** 24), Fraction(1, 2 ** 150))  # binary32 subnormal ulp/2
+
+
+def test_fp8_ratio_and_error_bound():
+    """PAPER.md:101 '8-bit floating point ... reduces 75% communication traffic' (body n bytes
+    -> 0.25) and the E4M3 relative error 2^-4 of the normal range (2^-10 * s absolute below)."""
+    t5 = gold("table5_ratios.json")
+    for n in (1, 17, 4096):
+        assert 1.0 - O.body_ratio(O.FP8, n) == t5["int8_traffic_reduction"]
+        assert O.payload_bytes(O.FP8, n) == 16 + math.ceil(n / 16) * 16
+    g = synthetic(20000, 13, "model-like")
+    _, D, st = O.compress(g, O.FP8, O.Codec(method=O.FP8))
+    s = float(st["scale"])
+    err = np.abs(g.astype(np.float64) - D.astype(np.float64))
+    bound = np.maximum(np.abs(g.astype(np.float64)) * 2.0 ** -4, s * 2.0 ** -10) * (1 + 2.0 ** -10)
+    assert np.all(err <= bound)
+
+
+@pytest.mark.parametrize("kind", ["normal", "model-like", "zipf-rows", "ties", "subnormal", "signed-zero", "zeros"])
+def test_fp8_residual_identity_exact(kind):
+    g = synthetic(5000, 23, kind)
+    r0 = synthetic(5000, 24, "normal", sigma=1e-3) if kind != "zeros" else np.zeros(5000, F32)
+    res = O.cluster_step(g, r0, O.Codec(method=O.FP8), step=1)
+    p = (g + r0).astype(F32)
+    assert np.array_equal((res.D + res.r_new).astype(F32), p)
+    for i in np.random.default_rng(1).integers(0, 5000, 300):
+        assert Fraction(float(res.r_new[i])) == Fraction(float(p[i])) - Fraction(float(res.D[i]))
+
+
+def test_fp8_zero_bucket_and_degenerate_scale():
+    _, D, st = O.compress(np.zeros(33, F32), O.FP8, O.Codec(method=O.FP8))
+    assert st["scale"] == 1.0 and np.all(D == 0)
+    g = synthetic(64, 5, "tiny-max")
+    _, D, st = O.compress(g, O.FP8, O.Codec(method=O.FP8))
+    assert st["scale"] == 1.0
+
+
+# ----------------------------------------------------------------- exact cluster scale (NEXT-3, R28)
+@pytest.mark.parametrize("method", [O.INT8, O.FP8])
+def test_hierarchical_exact_scale(method):
+    """With exact_scale every shard of a cluster carries the scale of the WHOLE cluster bucket:
+    equal to the flat (G = 1) compress of the concatenated cluster gradient, shard by shard.
+    Dyadic inputs make the intra-cluster mean exact in any order."""
+    P, G, n = 2, 4, 4096
+    rng = np.random.default_rng(9)
+    gs = [[(rng.integers(-1000, 1000, n) * (4.0 ** rng.integers(-3, 3, n))).astype(F32) * F32(2.0 ** -12)
+           for _ in range(G)] for _ in range(P)]
+    codec = O.Codec(method=method)
+    out, rs, pls = O.hierarchical_step(gs, [[None] * G for _ in range(P)], codec, 0, exact_scale=True)
+    means = [np.sum(np.array(gs[c], np.float64), axis=0) / G for c in range(P)]
+    flat_out, flat_r, flat_pl, _ = O.oracle_step([x.astype(F32) for x in means], [None] * P, codec, 0)
+    assert np.array_equal(out, flat_out)
+    m = n // G
+    for c in range(P):
+        sc = {struct.unpack_from("<f", pls[c][l], 8)[0] for l in range(G)}
+        assert len(sc) == 1 and sc.pop() == struct.unpack_from("<f", flat_pl[c], 8)[0]
+        assert np.array_equal(np.concatenate(rs[c]), flat_r[c])
+        for l in range(G):
+            assert pls[c][l][16:16 + m] == flat_pl[c][16 + l * m:16 + (l + 1) * m]
+    # without exact_scale the shards' scales differ (the per-shard reading R20)
+    _, _, pls2 = O.hierarchical_step(gs, [[None] * G for _ in range(P)], codec, 0)
+    assert len({struct.unpack_from("<f", pls2[0][l], 8)[0] for l in range(G)}) > 1
