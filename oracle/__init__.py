@@ -21,3 +21,4 @@ subsets of tiny vectors, and textbook special cases of the average.  Nothing her
 """
 from .codec import *  # noqa: F401,F403
 from .codec import __all__  # noqa: F401
+from .svd import *  # noqa: F401,F403  (FP16(SVD(rho)) low-rank compressor, NEXT-1)

@@ -105,7 +105,7 @@ def _first_diff(a, b):
 
 
 # ------------------------------------------------------------------ dense codecs
-@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.IDENTITY])
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.IDENTITY, O.FP8])
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 @pytest.mark.parametrize("sizes", [[1], [7], [4096], [4099, 12288, 77777]])
 def test_dense_parity(nb, method, P, sizes):
@@ -171,7 +171,7 @@ def test_fp16_kernels(nb, fp16_kernel, sizes):
     run_loopback(nb, O.FP16, sizes, 3, steps=1, ef=False, fp16_kernel=fp16_kernel)
 
 
-@pytest.mark.parametrize("method", [O.INT8, O.FP16])
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.FP8])
 @pytest.mark.parametrize("kind", ["ties", "subnormal", "mixed-scale", "signed-zero", "zeros", "tiny-max", "zipf-rows"])
 def test_dense_edge_values(nb, method, kind):
     if method == O.FP16 and kind == "mixed-scale":
@@ -179,12 +179,12 @@ def test_dense_edge_values(nb, method, kind):
     run_loopback(nb, method, [5003, 40000], 2, kind=kind)
 
 
-@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.TOPK])
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.TOPK, O.FP8])
 def test_no_error_feedback(nb, method):
     run_loopback(nb, method, [30001], 2, ef=False, rho=0.05)
 
 
-@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.TOPK])
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.TOPK, O.FP8])
 @pytest.mark.parametrize("per_bucket,misalign", [(True, False), (False, True), (True, True)])
 def test_call_shapes_and_alignment(nb, method, per_bucket, misalign):
     run_loopback(nb, method, [4099, 1, 0, 65536, 9], 3, per_bucket=per_bucket, misalign=misalign, rho=0.1)
@@ -238,7 +238,7 @@ def test_topk_fallback_path_is_exercised(nb):
 
 
 # ------------------------------------------------------------------ device errors
-@pytest.mark.parametrize("method", [O.IDENTITY, O.FP16, O.INT8, O.TOPK])
+@pytest.mark.parametrize("method", [O.IDENTITY, O.FP16, O.INT8, O.TOPK, O.FP8])
 @pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
 def test_nonfinite_is_reported(nb, method, bad):
     import torch
@@ -330,7 +330,7 @@ def test_step_host_matches_device_path(nb):
 
 # ------------------------------------------------------------------ pipeline hop (NEXT-2)
 @pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.INT8, 0), (O.IDENTITY, 0), (O.TOPK, O.VAL_F32),
-                                       (O.TOPK, O.VAL_I8)])
+                                       (O.TOPK, O.VAL_I8), (O.FP8, 0)])
 def test_decompress_single_slot(nb, method, vt):
     """Scenario-II hop semantics: each side decodes the OTHER side's
     payload exactly, no averaging, no error feedback; Table 5's ratios hold for the bytes."""
@@ -354,8 +354,8 @@ def test_decompress_single_slot(nb, method, vt):
             res = O.cluster_step(xs[slot][off:off + n], None, codec, 0)
             assert ctx.payload_copy(b, slot) == res.payload
             assert np.array_equal(bits(got[off:off + n]), bits(O.decode_payload(res.payload, n)))
-            if method in (O.FP16, O.INT8):
-                assert (len(res.payload) - 16) / (4 * n) == pytest.approx({O.FP16: 0.50, O.INT8: 0.25}[method],
+            if method in (O.FP16, O.INT8, O.FP8):
+                assert (len(res.payload) - 16) / (4 * n) == pytest.approx({O.FP16: 0.50, O.INT8: 0.25, O.FP8: 0.25}[method],
                                                                         abs=16 / (4 * n))
             off += n
     ctx.decompress_reduce(nb.ALL_BUCKETS, torch.empty(total, device="cuda"))
