@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METHODS = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3}
+METHODS = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3, "fp8": 4}
 VALUES = {"f32": 0, "f16": 1, "i8": 2}
 VB = {0: 4, 1: 2, 2: 1}
 METRIC = "GB/s fp32 gradient synced per GPU (1/2/4/8 B200); % HBM roofline"
@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--gpus-per-cluster", type=int, default=1,
                     help="G > 1: hierarchical topology (P = N / G clusters; BASELINE config 3 is 2 x 4)")
     ap.add_argument("--no-ef", action="store_true")
+    ap.add_argument("--exact-scale", action="store_true",
+                    help="G > 1: cluster-wide INT8/FP8 scale (NEBULA_OPT_EXACT_SCALE, NEXT-3)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
     ap.add_argument("--fp16-kernel", default="tma", choices=["tma", "plain"])
     ap.add_argument("--no-step-fusion", action="store_true",
@@ -103,6 +105,8 @@ def kernel_bytes(phase, method, vt, P, ef, n_elems, k_total):
         return (4 + e) * n_elems
     if phase == "int8_ef_quant_pack":
         return (4 + e + e + 1) * n_elems
+    if phase == "fp8_ef_quant_pack":
+        return (4 + e + e + 1) * n_elems
     if phase == "fp16_ef_pack":
         return (4 + e + e + 2) * n_elems
     if phase == "identity_pack":
@@ -119,7 +123,7 @@ def kernel_bytes(phase, method, vt, P, ef, n_elems, k_total):
 def reduce_bytes(method, vt, P, n_out, k_per_cluster):
     if method == 3:
         return P * k_per_cluster * (4 + VB[vt]) + 4 * n_out
-    b = {0: 4, 1: 2, 2: 1}[method]
+    b = {0: 4, 1: 2, 2: 1, 4: 1}[method]
     return P * b * n_out + 4 * n_out
 
 
@@ -257,7 +261,10 @@ def run_reference(args):
 
 
 def workload_config(args, n, P, G=1):
-    mname = {0: "identity", 1: "fp16+ef", 2: "int8+ef", 3: f"topk{args.density:g}-{args.values}+ef"}[METHODS[args.method]]
+    mname = {0: "identity", 1: "fp16+ef", 2: "int8+ef", 3: f"topk{args.density:g}-{args.values}+ef",
+             4: "fp8e4m3+ef"}[METHODS[args.method]]
+    if args.exact_scale and G > 1:
+        mname += "+exact-cluster-scale"
     if args.no_ef:
         mname = mname.replace("+ef", "")
     return {"workload": f"{args.workload}-" + (f"loopback-P{P}" if args.gpus == 1 else f"P{P}xG{G}"),
@@ -325,6 +332,8 @@ def main():
         ctx.set_int8_kernel(args.int8_kernel)
     if method == 1:
         ctx.set_fp16_kernel(args.fp16_kernel)
+    if args.exact_scale and G > 1:
+        ctx.set_exact_scale(True)
     if args.no_step_fusion:
         ctx.set_step_fusion(False)
     if args.step_config is not None:

@@ -23,7 +23,7 @@
  *
  * Payload body (R18): 16-byte preamble {u32 method, u32 count (n or k), f32 scale (1.0 if
  * unused), u32 aux (TOPK value type, else 0)}, then sections zero-padded to 16 bytes:
- * IDENTITY f32[n] | FP16 binary16[n] | INT8 int8[n] | TOPK u32 idx[k] (ascending) then
+ * IDENTITY f32[n] | FP16 binary16[n] | INT8 int8[n] | FP8 E4M3 u8[n] | TOPK u32 idx[k] (ascending) then
  * val[k] (f32 | binary16 | int8).  All little-endian.  Identical on every transport.
  *
  * Conventions for every entry point:
@@ -73,7 +73,10 @@ typedef enum {
   NEBULA_ERR_UNSUPPORTED = 8  /* e.g. NCCL transport in a build/box without peers */
 } nebula_status;
 
-typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3 } nebula_method;
+/* NEBULA_FP8 (NEXT-4; R27, "8-bit floating point to represent each gradient"):
+ * OCP E4M3, one per-bucket scale s = fl(max|p| / 448) (s := 1 if max == 0 or underflow),
+ * code = RNE-to-E4M3(fl(p / s)) saturating at +-448, D = fl(E4M3(code) * s).  Body: u8[n]. */
+typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4 } nebula_method;
 typedef enum { NEBULA_VAL_F32 = 0, NEBULA_VAL_F16 = 1, NEBULA_VAL_I8 = 2 } nebula_value_type;
 typedef enum { NEBULA_TRANSPORT_NCCL = 0, NEBULA_TRANSPORT_LOOPBACK = 1 } nebula_transport;
 
@@ -223,6 +226,14 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   into one kernel where eligible (see nebula_step), 1 never (three stage launches),
  *   2..12 fused with warp split 0..10 of the kernel's tuning sweep. */
 #define NEBULA_OPT_STEP_FUSION 4
+/*   NEBULA_OPT_EXACT_SCALE (NEXT-3, R28; hierarchical G > 1 only): 0 (default) every GPU's
+ *   shard has its own INT8 / FP8 scale (R20); 1 the scale of the WHOLE cluster bucket: the
+ *   max-abs pass runs on the shard, a 4-byte-per-bucket ncclAllReduce(max) over the
+ *   intra-cluster communicator combines the G shards' maxima, then every shard quantises with
+ *   that scale (two streaming passes instead of the single-pass INT8 kernel).  Payloads and
+ *   residuals then equal the G = 1 compress of the cluster's mean gradient, shard by shard.
+ *   Only between steps. */
+#define NEBULA_OPT_EXACT_SCALE 5
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

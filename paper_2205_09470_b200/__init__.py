@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "IDENTITY", "FP16", "INT8", "TOPK", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
+    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
     "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
     "status_string", "abi_version", "HEADER",
 ]
@@ -23,7 +23,7 @@ __all__ = [
 HERE = os.path.dirname(os.path.abspath(__file__))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
 
-IDENTITY, FP16, INT8, TOPK = 0, 1, 2, 3
+IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK = 0, 1
 ALL_BUCKETS = -1
@@ -31,6 +31,7 @@ OPT_INT8_KERNEL = 1
 OPT_EXCHANGE = 2
 OPT_FP16_KERNEL = 3
 OPT_STEP_FUSION = 4
+OPT_EXACT_SCALE = 5
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -290,6 +291,12 @@ class SyncContext:
         """True (default): step() runs INT8 compress + exchange + reduce as one kernel where
         eligible; False: three stage launches (NEBULA_OPT_STEP_FUSION)."""
         self.set_option(OPT_STEP_FUSION, 0 if on else 1)
+
+    def set_exact_scale(self, on: bool):
+        """Hierarchical (G > 1) INT8/FP8: True = the scale of the whole cluster bucket (one
+        4-byte-per-bucket intra-cluster all-reduce of the maxima, NEBULA_OPT_EXACT_SCALE);
+        False (default) = per-shard scales."""
+        self.set_option(OPT_EXACT_SCALE, int(bool(on)))
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""

@@ -12,7 +12,8 @@ namespace nb {
 enum Phase : int {
   PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
-  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_COUNT
+  PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_FP8_QUANT,
+  PH_NCCL_SCALE, PH_COUNT
 };
 
 struct Launch {
@@ -57,6 +58,9 @@ void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int ni
 // INT8 pass 2: scale from scratch, quantize + pack, r <- p - q*s.
 void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
+// FP8 E4M3 pass 2 (NEXT-4): scale fl(m/448) from scratch, quantise + pack, r <- p - D.
+void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
 // INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
 // p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
 // when a cooperative launch is not possible; the caller then uses the two-pass kernels.

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const Item* __restrict__ it
 }
 
 // ----------------------------------------------------------------------------- INT8 pass 2
-template <bool EF, bool VEC>
+template <bool EF, bool VEC, bool FP8 = false>
 __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict__ items, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
                                                          Dests dst,
@@ -236,12 +236,12 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       if (j == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
       continue;
     }
-    const float s = int8_scale_from_bits(mbits);
-    const float sinv = int8_inv(s);
+    const float s = FP8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
+    const float sinv = FP8 ? 0.0f : int8_inv(s);
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
     const uint64_t bo = it.slot_off + 16;
-    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, s, 0u);
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, FP8 ? M_FP8 : M_INT8, (uint32_t)it.n, s, 0u);
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
@@ -257,12 +257,19 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       uint32_t wv = 0u;
       if (q < n4) {
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
-        int q0 = int8_qi(p.x, s, sinv), q1 = int8_qi(p.y, s, sinv), q2 = int8_qi(p.z, s, sinv), q3 = int8_qi(p.w, s, sinv);
-        wv = pack_i8x4(q0, q1, q2, q3);
+        float d0, d1, d2, d3;
+        if constexpr (FP8) {
+          wv = fp8x2_of(p.x, p.y, s) | (fp8x2_of(p.z, p.w, s) << 16);
+          d0 = __fmul_rn(fp8_val(wv), s); d1 = __fmul_rn(fp8_val(wv >> 8), s);
+          d2 = __fmul_rn(fp8_val(wv >> 16), s); d3 = __fmul_rn(fp8_val(wv >> 24), s);
+        } else {
+          int q0 = int8_qi(p.x, s, sinv), q1 = int8_qi(p.y, s, sinv), q2 = int8_qi(p.z, s, sinv), q3 = int8_qi(p.w, s, sinv);
+          wv = pack_i8x4(q0, q1, q2, q3);
+          d0 = __fmul_rn((float)q0, s); d1 = __fmul_rn((float)q1, s); d2 = __fmul_rn((float)q2, s); d3 = __fmul_rn((float)q3, s);
+        }
         *reinterpret_cast<uint32_t*>(dst.p[0] + bo + 4 * q) = wv;
         if constexpr (EF)
-          st4(r + 4 * q, make_float4(__fsub_rn(p.x, __fmul_rn((float)q0, s)), __fsub_rn(p.y, __fmul_rn((float)q1, s)),
-                                     __fsub_rn(p.z, __fmul_rn((float)q2, s)), __fsub_rn(p.w, __fmul_rn((float)q3, s))));
+          st4(r + 4 * q, make_float4(__fsub_rn(p.x, d0), __fsub_rn(p.y, d1), __fsub_rn(p.z, d2), __fsub_rn(p.w, d3)));
       }
       push_u32(dst, bo + 4 * q, wv, q < n4);   // q % 4 == lane % 4: groups are 16-B aligned
     }
@@ -270,9 +277,18 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       if (threadIdx.x < (it.n & 3)) {
         const uint64_t e = n4 * 4 + threadIdx.x;
         float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
-        int qe = int8_qi(p, s, sinv);
-        put(dst, bo + e, (uint8_t)(qe & 0xFF));
-        if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+        uint32_t ce;
+        float de;
+        if constexpr (FP8) {
+          ce = fp8x2_of(p, 0.0f, s) & 0xFF;
+          de = __fmul_rn(fp8_val(ce), s);
+        } else {
+          const int qe = int8_qi(p, s, sinv);
+          ce = (uint32_t)qe & 0xFF;
+          de = __fmul_rn((float)qe, s);
+        }
+        put(dst, bo + e, (uint8_t)ce);
+        if constexpr (EF) r[e] = __fsub_rn(p, de);
       }
       zero_padding(dst, bo, it.n);
     }
@@ -286,6 +302,7 @@ __device__ __forceinline__ float decode_one(const uint8_t* slot, uint64_t e, flo
   const uint8_t* body = slot + 16;
   if constexpr (METHOD == M_IDENTITY) return reinterpret_cast<const float*>(body)[e];
   else if constexpr (METHOD == M_FP16) return __half2float(reinterpret_cast<const __half*>(body)[e]);
+  else if constexpr (METHOD == M_FP8) return __fmul_rn(fp8_val(body[e]), s);
   else return __fmul_rn((float)(int8_t)body[e], s);
 }
 
@@ -299,6 +316,8 @@ __device__ __forceinline__ float decode_at(const uint4& w, int e, float s) {
     return __uint_as_float(x);
   } else if constexpr (METHOD == M_FP16) {
     return __half2float(__ushort_as_half((unsigned short)((e & 1) ? (x >> 16) : (x & 0xFFFF))));
+  } else if constexpr (METHOD == M_FP8) {
+    return __fmul_rn(fp8_val(x >> (8 * (e & 3))), s);
   } else {
     return __fmul_rn((float)(int8_t)((x >> (8 * (e & 3))) & 0xFF), s);
   }
@@ -340,7 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       cur = i;
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        sc[k] = (METHOD == M_INT8) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
+        sc[k] = (METHOD == M_INT8 || METHOD == M_FP8) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
     }
     const uint64_t j = c - it.chunk0, nfull = it.n / E;   // groups entirely inside the bucket
     float* out = obase + it.out_off;
@@ -642,6 +661,17 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
   ++*L.launches;
 }
 
+void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags) {
+  if (!chunks) return;
+  Mark mk(L, PH_FP8_QUANT);
+  if (ef && vec) k_int8_quant<true, true, true><<<GRID((k_int8_quant<true, true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (ef) k_int8_quant<true, false, true><<<GRID((k_int8_quant<true, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (vec) k_int8_quant<false, true, true><<<GRID((k_int8_quant<false, true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else k_int8_quant<false, false, true><<<GRID((k_int8_quant<false, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  ++*L.launches;
+}
+
 template <int METHOD, int P>
 static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const Dests& slots,
                      float* out) {
@@ -668,6 +698,7 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
   Mark mk(L, PH_REDUCE_DENSE);
   if (method == M_IDENTITY) reduce_m<M_IDENTITY>(L, P, vec, items, nitems, chunks, slots, out);
   else if (method == M_FP16) reduce_m<M_FP16>(L, P, vec, items, nitems, chunks, slots, out);
+  else if (method == M_FP8) reduce_m<M_FP8>(L, P, vec, items, nitems, chunks, slots, out);
   else reduce_m<M_INT8>(L, P, vec, items, nitems, chunks, slots, out);
   ++*L.launches;
 }

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,7 +21,7 @@ constexpr int kChunkQuads = kThreads * kQuadsPerThread;
 constexpr uint64_t kChunkElems = (uint64_t)kChunkQuads * 4;   // 4096 elements per chunk
 
 enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u, kFlagPeerTimeout = 4u };
-enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3 };
+enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3, M_FP8 = 4 };
 enum : int { V_F32 = 0, V_F16 = 1, V_I8 = 2 };
 
 // One (cluster, bucket) unit of codec work.  Offsets are relative to per-call base
@@ -146,6 +147,25 @@ __device__ __forceinline__ float int8_inv(float s) {
 }
 __device__ __forceinline__ int int8_qi(float p, float s, float inv) {
   return inv != 0.0f ? int8_q_fast(p, s, inv) : int8_q(p, s);
+}
+
+// FP8 E4M3 (NEXT-4, R27; "8-bit floating point"): s = fl(m / 448)
+// with the R4 degenerate rules; code = RNE to E4M3 of fl(p / s), saturating to +-448
+// (cvt.rn.satfinite.e4m3x2.f32); D = fl(E4M3(code) * s).
+__device__ __forceinline__ float fp8_scale_from_bits(uint32_t mbits) {
+  float m = __uint_as_float(mbits);
+  float s = __fdiv_rn(m, 448.0f);
+  if (m == 0.0f || s == 0.0f) s = 1.0f;
+  return s;
+}
+// two quotients -> two E4M3 bytes (a in the low byte)
+__device__ __forceinline__ uint32_t fp8x2_of(float pa, float pb, float s) {
+  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(__fdiv_rn(pa, s), __fdiv_rn(pb, s)), __NV_SATFINITE, __NV_E4M3);
+}
+// E4M3 byte -> binary32 (exact: E4M3 values are binary16 values)
+__device__ __forceinline__ float fp8_val(uint32_t byte) {
+  __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(byte & 0xFF), __NV_E4M3);
+  return __half2float(__half(h));
 }
 
 __device__ __forceinline__ uint32_t pack_i8x4(int a, int b, int c, int d) {

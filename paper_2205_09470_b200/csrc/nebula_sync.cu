@@ -113,6 +113,7 @@ struct nebula_ctx {
   int int8_kernel = 0;          // NEBULA_OPT_INT8_KERNEL
   int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
   int step_fusion = 0;          // NEBULA_OPT_STEP_FUSION: 0 fuse INT8 steps where eligible, 1 never
+  int exact_scale = 0;          // NEBULA_OPT_EXACT_SCALE: 1 = cluster-wide INT8/FP8 scale when G > 1 (R28)
   bool onchip_ok = false;
   int onchip_grid = 0;
   size_t onchip_smem = 0;
@@ -188,7 +189,8 @@ static uint64_t payload_bytes_for(int method, uint64_t n, uint64_t k, int vt) {
   switch (method) {
     case M_IDENTITY: return 16 + pad16(4 * n);
     case M_FP16: return 16 + pad16(2 * n);
-    case M_INT8: return 16 + pad16(n);
+    case M_INT8:
+    case M_FP8: return 16 + pad16(n);
     default: return 16 + pad16(4 * k) + pad16(value_bytes(vt) * k);
   }
 }
@@ -215,7 +217,7 @@ static nebula_status validate(const nebula_topology* t, const nebula_codec* c, c
       return fail(nullptr, NEBULA_ERR_INVALID_ARG, "local_rank out of range");
   }
   if (t->device < 0) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "device must be >= 0");
-  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_TOPK)
+  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_FP8)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown method");
   if (c->error_feedback != 0 && c->error_feedback != 1)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "error_feedback must be 0 or 1");
@@ -612,6 +614,18 @@ nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream) {
   return NEBULA_OK;
 }
 
+// NEXT-3 (R28): the max-abs words of this GPU's shards (scratch[b], Ploc == 1 when G > 1;
+// |p| bits order like the floats, NaN/Inf bits above every finite one) -> the max over the G
+// shards of the cluster, so every shard quantises with the scale of the whole cluster bucket.
+// One 4-byte-per-bucket all-reduce on the intra-cluster communicator.
+static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int32_t bucket) {
+  Mark mk(L, PH_NCCL_SCALE);
+  uint32_t* w = ctx->d_scratch + (bucket == NEBULA_ALL_BUCKETS ? 0 : bucket);
+  const size_t cnt = bucket == NEBULA_ALL_BUCKETS ? ctx->b.size() : 1;
+  CKN(ncclAllReduce(w, w, cnt, ncclUint32, ncclMax, ctx->intra, ctx->stream));
+  return NEBULA_OK;
+}
+
 // ============================================================================ stages
 nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
@@ -668,7 +682,8 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       }
       }
       bool onchip = false;
-      if (ctx->onchip_ok) {
+      const bool xscale = ctx->exact_scale && ctx->G > 1;
+      if (ctx->onchip_ok && !xscale) {
         if (ctx->int8_kernel >= 2) onchip = true;
         else if (ctx->int8_kernel == 0) onchip = elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20);
       }
@@ -678,9 +693,25 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
                            ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : (vec ? 10 : 2) /* auto: warp-specialised TMA */);
       } else {
         launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
+        if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
         launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
                           ctx->d_flags);
       }
+      break;
+    }
+    case M_FP8: {   // NEXT-4 (R27): max-abs pass, [cluster-wide max (R28)], quantise pass
+      {
+        Mark mk(L, PH_MEMSET);
+        if (bucket == NEBULA_ALL_BUCKETS) {
+          CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
+        } else {
+          for (int c = 0; c < ctx->Ploc; ++c)
+            CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
+        }
+      }
+      launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
+      if (ctx->exact_scale && ctx->G > 1) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
+      launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
       break;
     }
     case M_TOPK: {
@@ -1026,6 +1057,13 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->fp16_kernel = (int)value;
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_EXACT_SCALE) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exact-scale option must be 0 or 1");
+    for (const auto& bk : ctx->b)
+      if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the scale mode only between steps");
+    ctx->exact_scale = (int)value;
+    return NEBULA_OK;
+  }
   if (option == NEBULA_OPT_EXCHANGE) {
     if (value < 0 || value > 3) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exchange option must be in [0, 3]");
     if (ctx->loopback) return NEBULA_OK;   // nothing moves
@@ -1079,7 +1117,7 @@ const char* nebula_phase_name(uint32_t phase) {
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
       "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
-      "p2p_exchange_flags", "int8_fused_step"};
+      "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

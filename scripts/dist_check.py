@@ -44,15 +44,21 @@ def main():
     P, cl, lr = nb.topology_for_rank(rank, world, G)
     sizes = [4096 * G, 12288 * G, 300004 * G, 8 * G]
     total = sum(sizes)
-    cases = [(O.INT8, 0, "two-pass"), (O.INT8, 0, "onchip"), (O.INT8, 0, "fused-ws"), (O.FP16, 0, None), (O.IDENTITY, 0, None),
-             (O.TOPK, O.VAL_F32, None), (O.TOPK, O.VAL_I8, None), (O.TOPK, O.VAL_F16, None)]
+    # (method, top-k values, INT8 kernel, exact cluster-wide scale (NEXT-3, only meaningful for G > 1))
+    cases = [(O.INT8, 0, "two-pass", False), (O.INT8, 0, "onchip", False), (O.INT8, 0, "fused-ws", False),
+             (O.FP16, 0, None, False), (O.IDENTITY, 0, None, False), (O.FP8, 0, None, False),
+             (O.TOPK, O.VAL_F32, None, False), (O.TOPK, O.VAL_I8, None, False), (O.TOPK, O.VAL_F16, None, False)]
+    if G > 1:
+        cases += [(O.INT8, 0, None, True), (O.FP8, 0, None, True)]
     modes_seen = set()
-    for method, vt, kern in cases:
+    for method, vt, kern, exact in cases:
         for per_bucket, xch in ((False, "pull"), (True, "pull"), (False, "push"), (True, "push"), (False, "nccl")):
             ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
                                                 topk_values=vt, topk_density=0.05)
             if kern:
                 ctx.set_int8_kernel(kern)
+            if exact:
+                ctx.set_exact_scale(True)
             if P > 1:
                 try:
                     ctx.set_exchange(xch)
@@ -97,7 +103,7 @@ def main():
                     else:
                         exp, r_new, pls = O.hierarchical_step([[grad(c, l, b) for l in range(G)] for c in range(P)],
                                                               [[rs[c][l][b] for l in range(G)] for c in range(P)],
-                                                              codec, t)
+                                                              codec, t, exact_scale=exact)
                         myr, mypl = r_new[cl][lr], pls[cl][lr]
                         for c in range(P):
                             for l in range(G):
