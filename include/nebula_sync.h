@@ -253,6 +253,44 @@ nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on);
 nebula_status nebula_timing_read(nebula_ctx* ctx, nebula_phase_time* out, int32_t cap, int32_t* n_out);
 const char* nebula_phase_name(uint32_t phase);
 
+/* ---------------------------------------------------------------------------------------
+ * FP16(SVD(rho)) low-rank compressor of ONE fp32 matrix (PAPER.md:105-130
+ * Eq. 1-5; readings R29-R31).  The paper applies it to the Scenario-II forward activations
+ * (Table 5 "FP16(SVD(r))"): A (m x n) -> U_r, S_r, V_r (top r singular
+ * triples, Eq. 2), each encoded as binary16 (Eq. 5); the receiver rebuilds A' = U_r S_r V_r^T
+ * (Eq. 3).  Value bytes = 2 (m r + r + r n) = Eq. 4 x 4 m n / 2.
+ *
+ * Payload (R31): 16-byte preamble {u32 5, u32 m, u32 n, u32 r}, then binary16 sections
+ * zero-padded to 16 bytes: U_r [m][r] row-major, S_r [r] (descending), V_r [n][r] row-major.
+ * Sign convention (R30): the largest-magnitude entry of every U_r column is positive.
+ * Computation: G = B^T B (B = A if m >= n else A^T) in fp64 on the GPU, a dense symmetric
+ * eigensolver (cuSOLVER syevd) for the top r eigenpairs, U/V = B W_r / sigma, binary16 pack —
+ * all on the handle's stream, no host synchronisation (nebula_svd_check synchronises).
+ * Errors: host-validated arguments return immediately; a non-finite entry of A, a binary16
+ * overflow of a singular value (>= 65520) or an eigensolver failure are reported by
+ * nebula_svd_check (the payload is then unspecified). */
+typedef struct nebula_svd nebula_svd; /* opaque, library-owned workspace for one (m, n, r) */
+
+/* m, n >= 1, min(m, n) <= 16384, 1 <= r <= min(m, n).  Allocates the workspace (fp64 Gram
+ * min(m,n)^2, fp32 max(m,n) x r, solver buffers) on `device`; stream = cudaStream_t. */
+nebula_status nebula_svd_init(nebula_svd** out, int64_t m, int64_t n, int32_t r, int32_t device, void* stream);
+nebula_status nebula_svd_set_stream(nebula_svd* h, void* stream);
+/* Payload size in bytes (preamble + padded sections). */
+nebula_status nebula_svd_payload_bytes(const nebula_svd* h, uint64_t* bytes);
+/* dev_A: fp32 m x n row-major (caller-owned, unmodified); dev_payload: nebula_svd_payload_bytes
+ * bytes of device memory (caller-owned), written completely. */
+nebula_status nebula_svd_compress(nebula_svd* h, const float* dev_A, void* dev_payload);
+/* dev_payload as written by nebula_svd_compress (or by any encoder of the R31 layout with the
+ * handle's m, n, r); dev_out: fp32 m x n row-major, A'[i][j] = sum_q fl(U[i][q] S[q]) V[j][q]
+ * accumulated in fp32 with fused multiply-adds. */
+nebula_status nebula_svd_decompress(nebula_svd* h, const void* dev_payload, float* dev_out);
+/* Synchronises the stream; returns (and clears) NEBULA_ERR_NONFINITE / NEBULA_ERR_OVERFLOW or
+ * NEBULA_ERR_CUDA for an eigensolver failure, else NEBULA_OK. */
+nebula_status nebula_svd_check(nebula_svd* h);
+uint64_t nebula_svd_kernel_launches(const nebula_svd* h);
+nebula_status nebula_svd_destroy(nebula_svd* h);
+const char* nebula_svd_last_error(const nebula_svd* h);
+
 /* Frees everything the context owns (synchronises first).  NULL is a no-op. */
 nebula_status nebula_sync_destroy(nebula_ctx* ctx);
 

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 __all__ = [
     "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
     "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
-    "status_string", "abi_version", "HEADER",
+    "status_string", "abi_version", "HEADER", "SvdCodec", "SVD_FP16",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -26,6 +26,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK = 0, 1
+SVD_FP16 = 5   # payload method id of the FP16(SVD(rho)) compressor (R31)
 ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
 OPT_EXCHANGE = 2
@@ -121,6 +122,15 @@ def load() -> ctypes.CDLL:
         "nebula_timing_read": (I32, [P, ctypes.POINTER(_PhaseTime), I32, ctypes.POINTER(I32)]),
         "nebula_phase_name": (ctypes.c_char_p, [ctypes.c_uint32]),
         "nebula_sync_destroy": (I32, [P]),
+        "nebula_svd_init": (I32, [ctypes.POINTER(P), ctypes.c_int64, ctypes.c_int64, I32, I32, VP]),
+        "nebula_svd_set_stream": (I32, [P, VP]),
+        "nebula_svd_payload_bytes": (I32, [P, ctypes.POINTER(U64)]),
+        "nebula_svd_compress": (I32, [P, VP, VP]),
+        "nebula_svd_decompress": (I32, [P, VP, VP]),
+        "nebula_svd_check": (I32, [P]),
+        "nebula_svd_kernel_launches": (U64, [P]),
+        "nebula_svd_destroy": (I32, [P]),
+        "nebula_svd_last_error": (ctypes.c_char_p, [P]),
         "nebula_last_error": (ctypes.c_char_p, [P]),
     }
     for name, (res, args) in sig.items():
@@ -355,3 +365,59 @@ def init_process_group_context(bucket_numel, *, gpus_per_cluster=1, device=None,
         device = torch.cuda.current_device()
     return SyncContext(bucket_numel, num_clusters=P, cluster_id=c, gpus_per_cluster=gpus_per_cluster,
                        local_rank=l, transport=NCCL, device=device, unique_id=uid, **codec)
+
+
+class SvdCodec:
+    """One ``nebula_svd`` handle: the FP16(SVD(rho)) compressor of an m x n fp32 matrix
+    (NEXT-1; Eq. 1-5).  ``r`` = kept singular triples (or pass ``rho`` for R29's
+    r = clamp(floor(rho min(m, n) + 0.5), 1, min(m, n)))."""
+
+    def __init__(self, m: int, n: int, r: int | None = None, *, rho: float | None = None, device=0, stream=None):
+        import math
+        L = load()
+        self._L = L
+        if r is None:
+            k = min(m, n)
+            r = max(1, min(k, math.floor(float(rho) * k + 0.5)))
+        self.m, self.n, self.r, self.device = int(m), int(n), int(r), device
+        h = ctypes.c_void_p()
+        s = L.nebula_svd_init(ctypes.byref(h), self.m, self.n, self.r, device, _stream_handle(stream, device))
+        if s:
+            raise NebulaError(s, L.nebula_svd_last_error(None).decode())
+        self._h = h
+
+    def _ck(self, s):
+        if s:
+            raise NebulaError(s, self._L.nebula_svd_last_error(self._h).decode())
+
+    def payload_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        self._ck(self._L.nebula_svd_payload_bytes(self._h, ctypes.byref(b)))
+        return b.value
+
+    def compress(self, A, payload):
+        """A: fp32 [m, n] CUDA tensor (row-major); payload: uint8 CUDA tensor of payload_bytes()."""
+        self._ck(self._L.nebula_svd_compress(self._h, _ptr(A), _ptr(payload)))
+
+    def decompress(self, payload, out):
+        self._ck(self._L.nebula_svd_decompress(self._h, _ptr(payload), _ptr(out)))
+
+    def set_stream(self, stream):
+        self._ck(self._L.nebula_svd_set_stream(self._h, _stream_handle(stream, self.device)))
+
+    def check(self):
+        self._ck(self._L.nebula_svd_check(self._h))
+
+    def kernel_launches(self) -> int:
+        return self._L.nebula_svd_kernel_launches(self._h)
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            self._L.nebula_svd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass

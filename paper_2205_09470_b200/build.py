@@ -37,6 +37,19 @@ def _nccl_dirs():
     raise RuntimeError("nccl.h / libnccl.so not found")
 
 
+def _cusolver_dirs():
+    """torch's bundled cuSOLVER (the same libcublas.so.12 torch loads resolves its symbols)."""
+    try:
+        import nvidia.cusolver
+        base = list(nvidia.cusolver.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "cusolverDn.h")) and glob.glob(os.path.join(lib, "libcusolver.so*")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/local/cuda/include", "/usr/local/cuda/lib64"
+
+
 def _nvcc():
     for p in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if p and os.path.exists(p):
@@ -61,11 +74,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     inc, lib = _nccl_dirs()
+    sinc, slib = _cusolver_dirs()
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     cmd = [_nvcc(), ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{INCLUDE}", f"-I{inc}", f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
+           f"-I{sinc}", f"-L{slib}", "-l:libcusolver.so.11", f"-Xlinker=-rpath,{slib}",
            "-o", LIB + ".tmp"] + cus
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -61,6 +61,10 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
 // FP8 E4M3 pass 2 (NEXT-4): scale fl(m/448) from scratch, quantise + pack, r <- p - D.
 void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
+// FP8 single HBM pass: the warp-specialised TMA kernel with the E4M3 quantiser (16-B aligned
+// calls; cooperative, one CTA per SM; done_words >= nitems).
+void launch_fp8_onchip(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                       const Dests& slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words);
 // INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
 // p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
 // when a cooperative launch is not possible; the caller then uses the two-pass kernels.

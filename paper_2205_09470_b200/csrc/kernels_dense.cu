@@ -1510,11 +1510,14 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
 }
 
 // CM: reduce role — 0 none (compress only), 1 TMA variant (LOOPBACK), 2 register loads (P2P pull)
-template <bool EF, int AW, int BW, int CW, int CM>
+// F8: the same single-pass schedule for the FP8 E4M3 codec (NEXT-4, R27) — only the B
+// warps' scale / quantise / dequantise differ; compress-only (no fused reduce role).
+template <bool EF, int AW, int BW, int CW, int CM, bool F8 = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
   static_assert(1 + AW + BW + CW == kWsThreads / 32, "warp roles must fill the CTA");
+  static_assert(!F8 || CW == 0, "FP8 runs the compress-only kernel");
   constexpr int kA = AW * 32, kB = BW * 32, kC = CW * 32;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   WsStageA* ringA = reinterpret_cast<WsStageA*>(ws_smem);
@@ -1677,10 +1680,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           s_scale[0] = 0.0f;
           if (blockIdx.x == 0) atomicOr(flags, kFlagNonfinite);
         } else {
-          const float sc = int8_scale_from_bits(mbits);
+          const float sc = F8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
           s_scale[0] = sc;
-          s_scale[1] = int8_inv(sc);
-          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, M_INT8, (uint32_t)it.n, sc, 0u);
+          s_scale[1] = F8 ? 0.0f : int8_inv(sc);
+          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 ? M_FP8 : M_INT8, (uint32_t)it.n, sc, 0u);
         }
       }
       named_sync(2, kB);
@@ -1702,14 +1705,22 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           uint32_t w = 0u;
           if (valid) {
             const float4 p = S.p[j];
-            const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
-                      a3 = int8_qi(p.w, s, sinv);
-            w = pack_i8x4(a0, a1, a2, a3);
+            float d0, d1, d2, d3;
+            if constexpr (F8) {
+              w = fp8x2_of(p.x, p.y, s) | (fp8x2_of(p.z, p.w, s) << 16);
+              d0 = __fmul_rn(fp8_val(w), s); d1 = __fmul_rn(fp8_val(w >> 8), s);
+              d2 = __fmul_rn(fp8_val(w >> 16), s); d3 = __fmul_rn(fp8_val(w >> 24), s);
+            } else {
+              const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
+                        a3 = int8_qi(p.w, s, sinv);
+              w = pack_i8x4(a0, a1, a2, a3);
+              d0 = __fmul_rn((float)a0, s); d1 = __fmul_rn((float)a1, s);
+              d2 = __fmul_rn((float)a2, s); d3 = __fmul_rn((float)a3, s);
+            }
             st_u32_hint(body + q0 + j, w, CW > 0 ? pol_keep : pol_stream);   // fused: C re-reads it from L2
             if constexpr (EF)
               st4_hint(r + 4 * (q0 + j),
-                       make_float4(__fsub_rn(p.x, __fmul_rn((float)a0, s)), __fsub_rn(p.y, __fmul_rn((float)a1, s)),
-                                   __fsub_rn(p.z, __fmul_rn((float)a2, s)), __fsub_rn(p.w, __fmul_rn((float)a3, s))),
+                       make_float4(__fsub_rn(p.x, d0), __fsub_rn(p.y, d1), __fsub_rn(p.z, d2), __fsub_rn(p.w, d3)),
                        pol_stream);
           }
           push_u32(dst, bo + 4 * (q0 + j), w, valid);
@@ -1722,9 +1733,18 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         if (bt < (int)(it.n & 3)) {
           const uint64_t e = (it.n >> 2) * 4 + bt;
           const float p = EF ? r[e] : g[e];
-          const int qe = int8_qi(p, s, sinv);
-          put(dst, bo + e, (uint8_t)(qe & 0xFF));
-          if constexpr (EF) r[e] = __fsub_rn(p, __fmul_rn((float)qe, s));
+          uint32_t ce;
+          float de;
+          if constexpr (F8) {
+            ce = fp8x2_of(p, 0.0f, s) & 0xFF;
+            de = __fmul_rn(fp8_val(ce), s);
+          } else {
+            const int qe = int8_qi(p, s, sinv);
+            ce = (uint32_t)qe & 0xFF;
+            de = __fmul_rn((float)qe, s);
+          }
+          put(dst, bo + e, (uint8_t)ce);
+          if constexpr (EF) r[e] = __fsub_rn(p, de);
         }
         zero_padding_t(dst, bo, it.n, bt);
       }
@@ -1948,6 +1968,30 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
   cudaGetLastError();
   *smem = bytes;
   return true;
+}
+
+void launch_fp8_onchip(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                       const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words) {
+  Dests slots = slots_in;
+  Mark mk(L, PH_FP8_QUANT);
+  cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+  unsigned* done = done_words;
+  StepArgs sa{};
+  void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
+                  (void*)&flags, (void*)&done, (void*)&sa};
+  const void* f = ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, true> : (const void*)k_int8_ws<false, 8, 23, 0, 0, true>;
+  const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchCooperativeKernel(f, dim3(sms), dim3(kWsThreads), args, smem, L.stream);
+  ++*L.launches;
 }
 
 void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems, const float* g, float* r,

@@ -568,7 +568,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       s = topk_setup(ctx);
       if (s != NEBULA_OK) return bail(s);
     }
-    if (codec->method == NEBULA_INT8) {
+    if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
       if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (2 * ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
         ctx->err = "barrier allocation failed";
@@ -709,8 +709,17 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
             CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
         }
       }
+      const bool xscale = ctx->exact_scale && ctx->G > 1;
+      // single pass (warp-specialised TMA kernel) under the INT8 kernel's rule: buckets averaging
+      // >= 1M elements, 16-B aligned, not overridden to two-pass, no cluster-wide scale
+      if (ctx->onchip_ok && vec && !xscale &&
+          (ctx->int8_kernel >= 2 ||
+           (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)))) {
+        launch_fp8_onchip(L, ef, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar);
+        break;
+      }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-      if (ctx->exact_scale && ctx->G > 1) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
+      if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
       launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
       break;
     }
@@ -1042,7 +1051,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
     if (value < 0 || value > 12) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 12]");
-    if (value >= 2 && ctx->codec.method == NEBULA_INT8 && !ctx->onchip_ok)
+    if (value >= 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8) && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;
     return NEBULA_OK;

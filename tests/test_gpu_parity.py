@@ -164,6 +164,14 @@ def test_topk_i8_near_half_integer_quotients(nb):
     run_loopback(nb, O.TOPK, [50001], 2, kind="half-ties", vt=O.VAL_I8, rho=0.3, steps=1, ef=False)
 
 
+@pytest.mark.parametrize("kern", ["two-pass", "fused-ws"])
+@pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
+@pytest.mark.parametrize("ef", [True, False])
+def test_fp8_kernels(nb, kern, sizes, ef):
+    """FP8 E4M3 (NEXT-4): the two-pass kernels and the single-pass warp-specialised kernel."""
+    assert run_loopback(nb, O.FP8, sizes, 2, int8_kernel=kern, ef=ef, steps=2) > 0
+
+
 @pytest.mark.parametrize("fp16_kernel", ["tma", "plain"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20]])
 def test_fp16_kernels(nb, fp16_kernel, sizes):

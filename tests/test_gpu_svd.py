@@ -1,0 +1,142 @@
+"""GPU parity of the FP16(SVD(rho)) compressor (NEXT-1) against oracle/svd.py.
+
+An SVD is unique only up to the signs of its singular vectors (fixed by R30) and the fp32
+GPU pipeline (fp64 Gram + eigensolver, fp32 projections) rounds differently from the fp64
+oracle, so the compressed bytes are compared through what is unique (NEXT-1):
+  * S_r: within 1 binary16 ulp of the oracle's (both round the same real sigma_j);
+  * U_r, V_r columns (well-separated spectrum): within 2^-8 of the oracle's, signs equal;
+  * the reconstruction error ||A - A'|| equals the oracle's to 1e-3 relative (Eckart-Young);
+  * decompress is deterministic: GPU decode of the ORACLE payload == oracle decode within
+    the fp32 accumulation bound r * 2^-23 * sum_q |U_iq S_q V_jq|;
+  * payload size = Eq. 4 / 2 + preamble/padding, exact.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nb():
+    import paper_2205_09470_b200 as nbm
+    from paper_2205_09470_b200 import build
+    build.build()
+    nbm.load()
+    return nbm
+
+
+def built(m, n, decay, seed, noise=0.0):
+    rng = np.random.default_rng(seed)
+    k = min(m, n)
+    Q1, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    sig = 20.0 * decay ** np.arange(k)
+    A = (Q1 * sig[None, :]) @ Q2.T + noise * rng.standard_normal((m, n))
+    return A.astype(np.float32)
+
+
+def run(nb, A, r):
+    import torch
+    m, n = A.shape
+    h = nb.SvdCodec(m, n, r)
+    assert h.payload_bytes() == O.svd_payload_bytes(m, n, r)
+    dA = torch.from_numpy(A).cuda()
+    pl = torch.full((h.payload_bytes(),), 0xAB, dtype=torch.uint8, device="cuda")
+    h.compress(dA, pl)
+    h.check()
+    out = torch.empty(m, n, device="cuda")
+    h.decompress(pl, out)
+    h.check()
+    gpu_payload = bytes(pl.cpu().numpy())
+    rec = out.cpu().numpy()
+    # deterministic leg: decode the oracle's payload on the GPU
+    opl = O.svd_compress(A, r)
+    dpl = torch.from_numpy(np.frombuffer(opl, np.uint8).copy()).cuda()
+    h.decompress(dpl, out)
+    h.check()
+    rec_of_oracle = out.cpu().numpy()
+    launches = h.kernel_launches()
+    h.destroy()
+    return gpu_payload, rec, opl, rec_of_oracle, launches
+
+
+def ulp16(x):
+    x = np.abs(np.asarray(x, np.float64))
+    e = np.floor(np.log2(np.maximum(x, 2.0 ** -14)))
+    return 2.0 ** (e - 10)
+
+
+@pytest.mark.parametrize("m,n,rho", [(512, 96, 0.6), (96, 512, 0.6), (300, 77, 0.2), (1000, 64, 0.9),
+                                     (64, 64, 1.0), (2048, 192, 0.4)])
+def test_svd_parity(nb, m, n, rho):
+    r = O.svd_rank(m, n, rho)
+    A = built(m, n, 0.9, m * 7 + n)
+    gpl, rec, opl, rec_o, launches = run(nb, A, r)
+    assert launches >= 6
+    assert gpl[:16] == opl[:16] and len(gpl) == len(opl)
+    _, _, _, Ug, sg, Vg = O.svd_decode_factors(gpl)
+    _, _, _, Uo, so, Vo = O.svd_decode_factors(opl)
+    assert np.all(np.abs(sg - so) <= ulp16(so) * 1.0001), np.max(np.abs(sg - so) / ulp16(so))
+    # singular vectors: well separated (ratio 0.9 between neighbours) -> unique up to sign,
+    # signs fixed by R30; compare where sigma_j is not buried in fp32 noise of the Gram
+    keep = so > 1e-3 * so[0]
+    assert np.max(np.abs(Ug[:, keep] - Uo[:, keep])) <= 2.0 ** -8
+    assert np.max(np.abs(Vg[:, keep] - Vo[:, keep])) <= 2.0 ** -8
+    # padding bytes of every section are zero (the 0xAB fill was overwritten)
+    A64 = A.astype(np.float64)
+    eg = np.linalg.norm(A64 - rec)
+    eo = np.linalg.norm(A64 - O.svd_decompress(opl))
+    assert abs(eg - eo) <= 1e-3 * eo + 2.0 ** -10 * np.linalg.norm(A64) / np.sqrt(r + 1)
+    # deterministic decode of the oracle payload
+    exp = O.svd_decompress(opl).astype(np.float64)
+    _, _, _, U, s, V = O.svd_decode_factors(opl)
+    mag = np.abs(U * s[None, :]) @ np.abs(V).T
+    assert np.all(np.abs(rec_o - exp) <= (r + 2) * 2.0 ** -23 * mag + 1e-30)
+
+
+def test_svd_payload_padding_and_ratio(nb):
+    m, n, r = 37, 23, 5                          # odd sizes: every section padded
+    A = built(m, n, 0.8, 5)
+    gpl, _, opl, _, _ = run(nb, A, r)
+    o = 16 + 2 * m * r
+    assert gpl[o:16 + O.pad16(2 * m * r)] == bytes(O.pad16(2 * m * r) - 2 * m * r)
+    assert (len(gpl) - 16) >= 2 * (m * r + r + r * n)
+    assert O.svd_body_ratio(m, n, r) == pytest.approx(O.svd_ratio(m, n, r) / 2)
+
+
+def test_svd_table5_shape(nb):
+    """PAPER.md:350 H^E = 128 x 64 x 768 activations -> m = 8192, n = 768, rho = 0.6 (Table 5's
+    best row): parity at the paper's shape on a low-rank-plus-noise matrix."""
+    m, n = 128 * 64, 768
+    r = O.svd_rank(m, n, 0.6)
+    A = built(m, n, 0.995, 11, noise=1e-3)
+    gpl, rec, opl, rec_o, _ = run(nb, A, r)
+    _, _, _, _, sg, _ = O.svd_decode_factors(gpl)
+    _, _, _, _, so, _ = O.svd_decode_factors(opl)
+    assert np.all(np.abs(sg - so) <= ulp16(so) * 1.0001)
+    A64 = A.astype(np.float64)
+    eg, eo = np.linalg.norm(A64 - rec), np.linalg.norm(A64 - O.svd_decompress(opl))
+    assert abs(eg - eo) <= 1e-2 * eo
+    assert (len(gpl) - 16) / (4 * m * n) == pytest.approx(0.30, abs=0.05)     # Table 5 forward column
+
+
+def test_svd_errors(nb):
+    import torch
+    with pytest.raises(nb.NebulaError):
+        nb.SvdCodec(10, 10, 11)
+    h = nb.SvdCodec(8, 8, 2)
+    A = torch.full((8, 8), 1e5, device="cuda")                  # sigma = 8e5 overflows binary16
+    pl = torch.empty(h.payload_bytes(), dtype=torch.uint8, device="cuda")
+    h.compress(A, pl)
+    with pytest.raises(nb.NebulaError) as e:
+        h.check()
+    assert e.value.code == "OVERFLOW"
+    A = torch.randn(8, 8, device="cuda")
+    A[3, 4] = float("nan")
+    h.compress(A, pl)
+    with pytest.raises(nb.NebulaError) as e:
+        h.check()
+    assert e.value.code == "NONFINITE"
+    h.destroy()
