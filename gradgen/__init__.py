@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -212,6 +212,25 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
         return rng.uniform(-1.0, 1.0, size=n).astype(np.float32)
     if kind == "tiny-max":
         return (rng.uniform(-1.0, 1.0, size=n) * 1e-44).astype(np.float32)
+    if kind == "fp8-ties":
+        # max |g| = 1 and every other value within a few ulps of (midpoint between two
+        # neighbouring E4M3 magnitudes) / 448: with a max-abs/448 scale the quotients sit on or
+        # next to E4M3 rounding boundaries (adversarial for any shortcut around the IEEE division)
+        grid = [mm * 2.0 ** -9 for mm in range(8)] + \
+               [(8 + mm) * 2.0 ** (ee - 10) for ee in range(1, 16) for mm in range(8)]
+        grid = np.array(grid[:-1] + [480.0])            # 448 is the last finite; 480 marks the 464 boundary
+        mids = (grid[:-1] + grid[1:]) / 2.0
+        g = (mids[rng.integers(0, mids.size, size=n)] / 448.0).astype(np.float32)
+        g *= np.where(rng.random(n) < 0.5, -1.0, 1.0).astype(np.float32)
+        steps = rng.integers(-3, 4, size=n)
+        for d in (-3, -2, -1, 1, 2, 3):
+            sel = steps == d
+            toward = np.float32(np.inf) if d > 0 else np.float32(-np.inf)
+            for _ in range(abs(d)):
+                g[sel] = np.nextafter(g[sel], toward)
+        g = np.clip(g, -1.0, 1.0).astype(np.float32)
+        g[0] = np.float32(1.0)
+        return g
     if kind == "half-ties":
         # max |g| = 1 and every other value within a few ulps of (k + 1/2)/127: with a
         # max-abs/127 scale the quotients sit on or next to half-integers (adversarial for any

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       continue;
     }
     const float s = FP8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
-    const float sinv = FP8 ? 0.0f : int8_inv(s);
+    const float sinv = int8_inv(s);   // fl(1/s) if normal, else 0 (both fast paths then divide)
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
     const uint64_t bo = it.slot_off + 16;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
         float d0, d1, d2, d3;
         if constexpr (FP8) {
-          wv = fp8x2_of(p.x, p.y, s) | (fp8x2_of(p.z, p.w, s) << 16);
+          wv = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
           d0 = __fmul_rn(fp8_val(wv), s); d1 = __fmul_rn(fp8_val(wv >> 8), s);
           d2 = __fmul_rn(fp8_val(wv >> 16), s); d3 = __fmul_rn(fp8_val(wv >> 24), s);
         } else {
@@ -1682,7 +1682,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         } else {
           const float sc = F8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
           s_scale[0] = sc;
-          s_scale[1] = F8 ? 0.0f : int8_inv(sc);
+          s_scale[1] = int8_inv(sc);
           if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 ? M_FP8 : M_INT8, (uint32_t)it.n, sc, 0u);
         }
       }
@@ -1707,7 +1707,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const float4 p = S.p[j];
             float d0, d1, d2, d3;
             if constexpr (F8) {
-              w = fp8x2_of(p.x, p.y, s) | (fp8x2_of(p.z, p.w, s) << 16);
+              w = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
               d0 = __fmul_rn(fp8_val(w), s); d1 = __fmul_rn(fp8_val(w >> 8), s);
               d2 = __fmul_rn(fp8_val(w >> 16), s); d3 = __fmul_rn(fp8_val(w >> 24), s);
             } else {

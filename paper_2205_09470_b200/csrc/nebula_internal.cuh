@@ -162,6 +162,25 @@ __device__ __forceinline__ float fp8_scale_from_bits(uint32_t mbits) {
 __device__ __forceinline__ uint32_t fp8x2_of(float pa, float pb, float s) {
   return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(__fdiv_rn(pa, s), __fdiv_rn(pb, s)), __NV_SATFINITE, __NV_E4M3);
 }
+// Same bytes, cheaper (the INT8 argument of int8_q_fast, for the E4M3 grid): x = fl(p * fl(1/s))
+// is within 3 * 2^-24 |x| of y = fl(p / s).  In the binade of |x| (exponent e >= -6, the
+// subnormal quantum below) E4M3 rounds t = |x| 2^(3-e) (exact scaling, t < 16) to an integer,
+// so x and y round alike unless frac(t) is within 3 * 2^-24 * 16 < 4e-6 of one half (binade
+// edges are representable, saturation at 464 = t 14.5 is such a midpoint).  Otherwise — or
+// when inv = fl(1/s) is not a usable normal number (inv == 0) — the IEEE division decides.
+__device__ __forceinline__ float fp8_quotient(float p, float s, float inv) {
+  if (inv == 0.0f) return __fdiv_rn(p, s);
+  const float x = __fmul_rn(p, inv);
+  const uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
+  const int e = max((int)(b >> 23) - 127, -6);
+  if (e > 20) return x;                                   // saturates to +-448 either way
+  const float t = __fmul_rn(__uint_as_float(b), __uint_as_float((uint32_t)(130 - e) << 23));
+  return fabsf(t - floorf(t) - 0.5f) > 4e-6f ? x : __fdiv_rn(p, s);
+}
+__device__ __forceinline__ uint32_t fp8x2_fast(float pa, float pb, float s, float inv) {
+  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(fp8_quotient(pa, s, inv), fp8_quotient(pb, s, inv)),
+                                            __NV_SATFINITE, __NV_E4M3);
+}
 // E4M3 byte -> binary32 (exact: E4M3 values are binary16 values)
 __device__ __forceinline__ float fp8_val(uint32_t byte) {
   __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(byte & 0xFF), __NV_E4M3);

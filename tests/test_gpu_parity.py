@@ -172,6 +172,14 @@ def test_fp8_kernels(nb, kern, sizes, ef):
     assert run_loopback(nb, O.FP8, sizes, 2, int8_kernel=kern, ef=ef, steps=2) > 0
 
 
+@pytest.mark.parametrize("kern", ["two-pass", "fused-ws"])
+def test_fp8_near_rounding_boundaries(nb, kern):
+    """Quotients on / next to E4M3 midpoints: the reciprocal fast path must hand every one of
+    them to the IEEE division (bit-exact payload and residual)."""
+    run_loopback(nb, O.FP8, [50001, 4096], 2, kind="fp8-ties", steps=1, ef=False, int8_kernel=kern)
+    run_loopback(nb, O.FP8, [1 << 20, 7], 2, kind="fp8-ties", steps=2, int8_kernel=kern)
+
+
 @pytest.mark.parametrize("fp16_kernel", ["tma", "plain"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20]])
 def test_fp16_kernels(nb, fp16_kernel, sizes):

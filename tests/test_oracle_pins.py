@@ -428,6 +428,11 @@ def test_fp8_matches_library_conversion():
     ours = O.fp8_e4m3_encode(x)
     lib = torch.from_numpy(x).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
     assert np.array_equal(ours, lib)
+    # quotients on / next to every E4M3 rounding boundary (gradgen "fp8-ties")
+    g = synthetic(50000, 8, "fp8-ties")
+    xq = (g / O.fp8_scale(g)).astype(F32)
+    xq = xq[np.abs(xq) < 464]
+    assert np.array_equal(O.fp8_e4m3_encode(xq), torch.from_numpy(xq).to(torch.float8_e4m3fn).view(torch.uint8).numpy())
     # round trip: decode(encode(v)) == v for every representable v
     vals = O.fp8_e4m3_decode(np.arange(0, 256, dtype=np.uint8))
     fin = ~np.isnan(vals)
