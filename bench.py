@@ -473,7 +473,7 @@ def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):
     """Minimum HBM bytes of one step on one GPU."""
     e = 4 if ef else 0
     clusters_here = P if world == 1 else 1
-    if method == 2:
+    if method in (2, 4):
         comp = (4 + e + e + 1) * n
     elif method == 1:
         comp = (4 + e + e + 2) * n
@@ -481,7 +481,7 @@ def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):
         comp = 8 * n
     else:
         comp = (4 + e + e) * n + k_per_cluster * (4 + VB[vt]) + (4 * k_per_cluster if ef else 0)
-    exch = 0 if world == 1 else 2 * (P - 1) * (n * {0: 4, 1: 2, 2: 1}.get(method, 0) + (k_per_cluster * (4 + VB[vt]) if method == 3 else 0))
+    exch = 0 if world == 1 else 2 * (P - 1) * (n * {0: 4, 1: 2, 2: 1, 4: 1}.get(method, 0) + (k_per_cluster * (4 + VB[vt]) if method == 3 else 0))
     red = reduce_bytes(method, vt, P, n, k_per_cluster)
     return clusters_here * comp + exch + red
 
