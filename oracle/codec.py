@@ -13,6 +13,8 @@ Per cluster c, per bucket of n fp32 elements, step t (SURVEY.md §8(c) plain def
            q = clamp(rint(fl(p/s)), -127, 127);  D = fl(q*s)
     FP8  : m = max|p|, s = fl(m/448) (s := 1 if m == 0 or s == 0)    PAPER.md:101 "8-bit floating point" (R27)
            c = RNE_E4M3_satfinite(fl(p/s));  D = fl(E4M3(c)*s)
+    QSGD : INT8's s; x = fl(p/s); q = floor(x) + [u < x - floor(x)]  PAPER.md:63 (QSGD cited; R32)
+           u = counter-based SplitMix64 uniform of (seed, step, cluster, bucket, shard, e)
     TOPK : k largest |p| by fp32 bit key, ties -> lower index,        PAPER.md:63, :99 (cited only; R11-R14)
            idx ascending; values f32 | RNE16 | int8 with the INT8 rule
     r_new = fl(p - D)                                                  R15 (error feedback)
@@ -35,10 +37,12 @@ __all__ = [
     "tree_sum", "average", "CompressResult", "cluster_step", "oracle_step",
     "hierarchical_step", "svd_ratio", "FP16_OVERFLOW_ABS", "FP8",
     "fp8_e4m3_encode", "fp8_e4m3_decode", "fp8_scale", "FP8_E4M3_MAX",
+    "QSGD", "splitmix64", "qsgd_uniforms", "qsgd_quantize",
 ]
 
 F32 = np.float32
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
+QSGD = 6                     # INT8 levels with stochastic rounding (R32); 5 = the SVD payload id
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 VALUE_BYTES = {VAL_F32: 4, VAL_F16: 2, VAL_I8: 1}
 NONFINITE, OVERFLOW = "NONFINITE", "OVERFLOW"
@@ -72,6 +76,7 @@ class Codec:
     topk_density: float = 0.01
     error_feedback: bool = True
     start_step: int = 0
+    sr_seed: int = 0           # QSGD (R32): seed of the counter-based uniforms
 
 
 def select_method(codec: Codec, step: int) -> int:
@@ -101,7 +106,7 @@ def payload_bytes(method: int, n: int, k: int = 0, value_type: int = VAL_F32) ->
         return 16 + pad16(4 * n)
     if method == FP16:
         return 16 + pad16(2 * n)
-    if method in (INT8, FP8):
+    if method in (INT8, FP8, QSGD):
         return 16 + pad16(n)
     if method == TOPK:
         return 16 + pad16(4 * k) + pad16(VALUE_BYTES[value_type] * k)
@@ -115,7 +120,7 @@ def body_ratio(method: int, n: int, k: int = 0, value_type: int = VAL_F32) -> fl
         b = 4 * n
     elif method == FP16:
         b = 2 * n
-    elif method in (INT8, FP8):
+    elif method in (INT8, FP8, QSGD):
         b = n
     else:
         b = (4 + VALUE_BYTES[value_type]) * k
@@ -223,6 +228,49 @@ def fp8_dequantize(c: np.ndarray, s: np.float32) -> np.ndarray:
     return (fp8_e4m3_decode(c) * F32(s)).astype(F32)
 
 
+# ------------------------------------------------------------------ QSGD (NEXT-4, R32)
+_M64 = (1 << 64) - 1
+_GAMMA = 0x9E3779B97F4A7C15
+
+
+def splitmix64(z):
+    """SplitMix64 output function of state z (Steele, Lea & Flood 2014): one step of the
+    generator whose state is z - gamma, i.e. mix(z + gamma).  Works on Python ints and on
+    numpy uint64 arrays (wrapping arithmetic)."""
+    if isinstance(z, np.ndarray):
+        z = z.astype(np.uint64) + np.uint64(_GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+    z = (int(z) + _GAMMA) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def qsgd_uniforms(n: int, seed: int, step: int, cluster: int, bucket: int, shard: int = 0) -> np.ndarray:
+    """R32 counter-based uniforms in [0, 1) on the 2^-24 grid, one per element e:
+    base = sm(seed ^ sm(step ^ sm(((cluster * 65536 + shard) << 32) | bucket))),
+    u_e = (sm(base + e * gamma) >> 40) * 2^-24   (sm = splitmix64; e * gamma wraps mod 2^64)."""
+    k = (((cluster * 65536 + shard) << 32) | bucket) & _M64
+    base = splitmix64(seed ^ splitmix64(step ^ splitmix64(k)))
+    with np.errstate(over="ignore"):
+        z = np.uint64(base) + np.arange(n, dtype=np.uint64) * np.uint64(_GAMMA)
+        h = splitmix64(z)
+    return ((h >> np.uint64(40)).astype(np.float64) * 2.0 ** -24).astype(F32)
+
+
+def qsgd_quantize(p: np.ndarray, s: np.float32, u: np.ndarray) -> np.ndarray:
+    """R32 (QSGD, PAPER.md:63 cites it; l-inf normalisation with 127 levels): x = fl(p / s),
+    f = floor(x), phi = x - f (exact), q = f + [u < phi], clamped to [-127, 127].
+    E[q * s] = p up to the 2^-24 grid of u (unbiased stochastic rounding)."""
+    x = (p / F32(s)).astype(F32)
+    f = np.floor(x).astype(F32)
+    phi = (x - f).astype(F32)
+    q = f + (u < phi).astype(F32)
+    return np.clip(q, -127, 127).astype(np.int8)
+
+
 def _keys(p: np.ndarray) -> np.ndarray:
     """R11: selection key = fp32 bit pattern with the sign cleared (|p| order, -0 == +0)."""
     return p.view(np.uint32) & np.uint32(0x7FFFFFFF)
@@ -270,7 +318,7 @@ class CompressResult:
     stats: dict = field(default_factory=dict)
 
 
-def compress(p: np.ndarray, method: int, codec: Codec, scale=None) -> tuple[bytes, np.ndarray, dict]:
+def compress(p: np.ndarray, method: int, codec: Codec, scale=None, uniforms=None) -> tuple[bytes, np.ndarray, dict]:
     """Encode p with ``method`` -> (payload bytes, D = decode(payload), stats).
     ``scale`` overrides the INT8 / FP8 scale (NEXT-3: the exact cluster-wide scale of a
     hierarchical shard, R28); None = the scale of p itself.
@@ -288,6 +336,13 @@ def compress(p: np.ndarray, method: int, codec: Codec, scale=None) -> tuple[byte
         s = int8_scale(p) if scale is None else F32(scale)
         q = int8_quantize(p, s)
         return (_preamble(INT8, n, float(s), 0) + _pad(q.tobytes()),
+                int8_dequantize(q, s), {"scale": float(s)})
+    if method == QSGD:
+        s = int8_scale(p) if scale is None else F32(scale)
+        if uniforms is None:
+            raise ValueError("QSGD needs the step's uniforms (qsgd_uniforms)")
+        q = qsgd_quantize(p, s, uniforms)
+        return (_preamble(QSGD, n, float(s), 0) + _pad(q.tobytes()),
                 int8_dequantize(q, s), {"scale": float(s)})
     if method == FP8:
         s = fp8_scale(p) if scale is None else F32(scale)
@@ -333,6 +388,8 @@ def decode_payload(payload: bytes, n: int) -> np.ndarray:
         return int8_dequantize(q, F32(scale))
     if method == FP8:
         return fp8_dequantize(np.frombuffer(body, dtype=np.uint8, count=n), F32(scale))
+    if method == QSGD:
+        return int8_dequantize(np.frombuffer(body, dtype=np.int8, count=n), F32(scale))
     if method == TOPK:
         k = count
         idx = np.frombuffer(body, dtype="<u4", count=k).astype(np.int64)
@@ -371,7 +428,8 @@ def average(payloads: list, n: int) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- steps
-def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int, scale=None) -> CompressResult:
+def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int, scale=None,
+                 ids: tuple = (0, 0, 0)) -> CompressResult:
     """One cluster's compress with error feedback (R15):
     lossy: p = fl(g + r); payload = C(p); r_new = fl(p - D(C(p))).
     IDENTITY (t < start_step): payload = g, residual untouched."""
@@ -386,25 +444,27 @@ def cluster_step(g: np.ndarray, r: np.ndarray | None, codec: Codec, step: int, s
         p = (g + np.asarray(r, dtype=F32)).astype(F32)
     else:
         p = g
-    payload, D, st = compress(p, method, codec, scale)
+    u = qsgd_uniforms(p.size, codec.sr_seed, step, ids[0], ids[1], ids[2]) if method == QSGD else None
+    payload, D, st = compress(p, method, codec, scale, u)
     r_new = (p - D).astype(F32) if codec.error_feedback else (None if r is None else r.copy())
     return CompressResult(payload, D, r_new, method, st)
 
 
-def oracle_step(gs: list, rs: list, codec: Codec, step: int, scales=None):
+def oracle_step(gs: list, rs: list, codec: Codec, step: int, scales=None, bucket: int = 0, shard: int = 0):
     """Whole step for P clusters: compress each cluster, exchange the
     payload bodies (slot c = cluster c), and have every cluster decompress-average all
     P slots.  scales[c] overrides cluster c's INT8/FP8 scale (R28).
     Returns (out, [r_new_c], [payload_c], [stats_c])."""
     if scales is None:
         scales = [None] * len(gs)
-    res = [cluster_step(g, r, codec, step, s) for g, r, s in zip(gs, rs, scales)]
+    res = [cluster_step(g, r, codec, step, s, (c, bucket, shard))
+           for c, (g, r, s) in enumerate(zip(gs, rs, scales))]
     n = np.asarray(gs[0]).size
     out = average([x.payload for x in res], n)
     return out, [x.r_new for x in res], [x.payload for x in res], [x.stats for x in res]
 
 
-def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: bool = False):
+def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: bool = False, bucket: int = 0):
     """P clusters x G GPUs (R20, PAPER.md:95 / :288 intra-cluster parallelism + compressed
     inter-cluster hop).  gs[c][l] is GPU l of cluster c's full bucket (n % G == 0);
     rs[c][l] its residual shard.  The cluster gradient is the fp32 mean of its G GPUs
@@ -427,16 +487,16 @@ def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: 
             shards[c][l] = (acc / F32(G)).astype(F32)
     scales = [None] * P
     method = select_method(codec, step)
-    if exact_scale and method in (INT8, FP8):
+    if exact_scale and method in (INT8, FP8, QSGD):
         for c in range(P):
             ps = [shards[c][l] if not codec.error_feedback else
                   (shards[c][l] + (np.zeros(m, F32) if rs[c][l] is None else np.asarray(rs[c][l], F32))).astype(F32)
                   for l in range(G)]
             p_c = np.concatenate(ps)
-            scales[c] = int8_scale(p_c) if method == INT8 else fp8_scale(p_c)
+            scales[c] = fp8_scale(p_c) if method == FP8 else int8_scale(p_c)
     for l in range(G):
         out_l, r_l, p_l, _ = oracle_step([shards[c][l] for c in range(P)], [rs[c][l] for c in range(P)], codec, step,
-                                         scales)
+                                         scales, bucket, l)
         outs.append(out_l)
         for c in range(P):
             rs_new[c][l] = r_l[c]

@@ -529,3 +529,55 @@ def test_hierarchical_exact_scale(method):
     # without exact_scale the shards' scales differ (the per-shard reading R20)
     _, _, pls2 = O.hierarchical_step(gs, [[None] * G for _ in range(P)], codec, 0)
     assert len({struct.unpack_from("<f", pls2[0][l], 8)[0] for l in range(G)}) > 1
+
+
+# ----------------------------------------------------------------- QSGD stochastic rounding (NEXT-4, R32)
+def test_splitmix64_reference_output():
+    g = gold("splitmix64.json")
+    assert O.splitmix64(0) == int(g["seed0_first_output"], 16)
+    # the vectorised (numpy uint64) and scalar forms agree
+    zs = np.array([0, 1, 2 ** 63, 2 ** 64 - 1, 12345678901234567], dtype=np.uint64)
+    assert [int(v) for v in O.splitmix64(zs)] == [O.splitmix64(int(z)) for z in zs]
+
+
+def test_qsgd_uniforms_are_uniform_and_distinct():
+    u = O.qsgd_uniforms(200000, 7, 3, 1, 2).astype(np.float64)
+    assert u.min() >= 0 and u.max() < 1 and np.all(u * 2 ** 24 == np.floor(u * 2 ** 24))
+    hist, _ = np.histogram(u, bins=64, range=(0, 1))
+    chi2 = float(np.sum((hist - u.size / 64) ** 2 / (u.size / 64)))
+    assert chi2 < 120                                    # 63 dof: p ~ 1e-5
+    for other in [(8, 3, 1, 2), (7, 4, 1, 2), (7, 3, 0, 2), (7, 3, 1, 3)]:
+        assert not np.array_equal(u[:64], O.qsgd_uniforms(64, *other).astype(np.float64))
+
+
+def test_qsgd_rounds_to_neighbours_and_is_unbiased():
+    """q in {floor(x), floor(x) + 1}; integer quotients are kept; the mean of the decoded value
+    over many seeds converges to p (E[D] = p up to the 2^-24 grid of u)."""
+    g = synthetic(4000, 31, "normal")
+    s = O.int8_scale(g)
+    x = (g / s).astype(F32)
+    acc = np.zeros(g.size, np.float64)
+    T = 400
+    for seed in range(T):
+        pl, D, _ = O.compress(g, O.QSGD, O.Codec(method=O.QSGD), uniforms=O.qsgd_uniforms(g.size, seed, 0, 0, 0))
+        q = np.frombuffer(pl, np.int8, count=g.size, offset=16).astype(np.float64)
+        assert np.all((q == np.floor(x)) | (q == np.floor(x) + 1))
+        acc += D
+    mean = acc / T
+    # Var[D] <= s^2 / 4 per seed -> standard error s / (2 sqrt(T)); 6 sigma over 4000 elements
+    assert np.all(np.abs(mean - g) <= 6 * float(s) / (2 * math.sqrt(T)))
+    assert abs(float(np.mean(mean - g))) <= 6 * float(s) / (2 * math.sqrt(T * g.size))
+    xi = np.array([0.0, 1.0, -3.0, 127.0], F32) * s
+    pl, D, _ = O.compress(xi.astype(F32), O.QSGD, O.Codec(method=O.QSGD), uniforms=O.qsgd_uniforms(4, 1, 0, 0, 0))
+    assert np.array_equal(np.frombuffer(pl, np.int8, count=4, offset=16), [0, 1, -3, 127])
+
+
+def test_qsgd_payload_layout_and_ratio():
+    g = synthetic(1001, 5, "model-like")
+    pl, D, st = O.compress(g, O.QSGD, O.Codec(method=O.QSGD), uniforms=O.qsgd_uniforms(1001, 0, 0, 0, 0))
+    assert len(pl) == O.payload_bytes(O.QSGD, 1001) == 16 + O.pad16(1001)
+    assert struct.unpack_from("<IIfI", pl, 0) == (O.QSGD, 1001, st["scale"], 0)
+    assert np.array_equal(O.decode_payload(pl, 1001), D)
+    assert O.body_ratio(O.QSGD, 1001) == 0.25
+    # one quantum: |p - D| < s
+    assert np.all(np.abs(g.astype(np.float64) - D) < float(st["scale"]) * (1 + 2.0 ** -20))
