@@ -23,7 +23,7 @@
  *
  * Payload body (R18): 16-byte preamble {u32 method, u32 count (n or k), f32 scale (1.0 if
  * unused), u32 aux (TOPK value type, else 0)}, then sections zero-padded to 16 bytes:
- * IDENTITY f32[n] | FP16 binary16[n] | INT8 int8[n] | FP8 E4M3 u8[n] | TOPK u32 idx[k] (ascending) then
+ * IDENTITY f32[n] | FP16 binary16[n] | INT8 / QSGD int8[n] | FP8 E4M3 u8[n] | TOPK u32 idx[k] (ascending) then
  * val[k] (f32 | binary16 | int8).  All little-endian.  Identical on every transport.
  *
  * Conventions for every entry point:
@@ -76,7 +76,15 @@ typedef enum {
 /* NEBULA_FP8 (NEXT-4; R27, "8-bit floating point to represent each gradient"):
  * OCP E4M3, one per-bucket scale s = fl(max|p| / 448) (s := 1 if max == 0 or underflow),
  * code = RNE-to-E4M3(fl(p / s)) saturating at +-448, D = fl(E4M3(code) * s).  Body: u8[n]. */
-typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4 } nebula_method;
+/* NEBULA_QSGD (NEXT-4; R32, QSGD is cited at PAPER.md:63, :99): INT8's scale and payload
+ * (method id 6), with stochastic instead of nearest rounding: x = fl(p / s),
+ * q = floor(x) + [u < x - floor(x)] clamped to [-127, 127], u the counter-based SplitMix64
+ * uniform (2^-24 grid) of (seed = NEBULA_OPT_SR_SEED, step, cluster, bucket, shard, element):
+ * base = sm(seed ^ sm(step ^ sm(((cluster * 65536 + shard) << 32) | bucket))),
+ * u_e = (sm(base + e * 0x9E3779B97F4A7C15) >> 40) * 2^-24.  E[D] = p (unbiased).
+ * (5 is the FP16(SVD) payload id, not a bucket method.) */
+typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4,
+               NEBULA_QSGD = 6 } nebula_method;
 typedef enum { NEBULA_VAL_F32 = 0, NEBULA_VAL_F16 = 1, NEBULA_VAL_I8 = 2 } nebula_value_type;
 typedef enum { NEBULA_TRANSPORT_NCCL = 0, NEBULA_TRANSPORT_LOOPBACK = 1 } nebula_transport;
 
@@ -234,6 +242,8 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   residuals then equal the G = 1 compress of the cluster's mean gradient, shard by shard.
  *   Only between steps. */
 #define NEBULA_OPT_EXACT_SCALE 5
+/*   NEBULA_OPT_SR_SEED: the 64-bit seed of NEBULA_QSGD's uniforms (default 0); any time. */
+#define NEBULA_OPT_SR_SEED 6
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
+    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "QSGD", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
     "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
     "status_string", "abi_version", "HEADER", "SvdCodec", "SVD_FP16",
 ]
@@ -24,6 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
 
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
+QSGD = 6
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK = 0, 1
 SVD_FP16 = 5   # payload method id of the FP16(SVD(rho)) compressor (R31)
@@ -33,6 +34,7 @@ OPT_EXCHANGE = 2
 OPT_FP16_KERNEL = 3
 OPT_STEP_FUSION = 4
 OPT_EXACT_SCALE = 5
+OPT_SR_SEED = 6
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -307,6 +309,10 @@ class SyncContext:
         4-byte-per-bucket intra-cluster all-reduce of the maxima, NEBULA_OPT_EXACT_SCALE);
         False (default) = per-shard scales."""
         self.set_option(OPT_EXACT_SCALE, int(bool(on)))
+
+    def set_sr_seed(self, seed: int):
+        """Seed of the QSGD stochastic-rounding uniforms (NEBULA_OPT_SR_SEED)."""
+        self.set_option(OPT_SR_SEED, int(seed) - (1 << 64) if int(seed) >= (1 << 63) else int(seed))
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""

@@ -13,7 +13,7 @@ enum Phase : int {
   PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
   PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_FP8_QUANT,
-  PH_NCCL_SCALE, PH_COUNT
+  PH_NCCL_SCALE, PH_QSGD_QUANT, PH_COUNT
 };
 
 struct Launch {
@@ -61,6 +61,10 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
 // FP8 E4M3 pass 2 (NEXT-4): scale fl(m/448) from scratch, quantise + pack, r <- p - D.
 void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
+// QSGD pass 2 (NEXT-4, R32): INT8 scale, stochastic rounding with counter-based uniforms.
+void launch_qsgd_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags,
+                       const SrArgs& sr);
 // FP8 single HBM pass: the warp-specialised TMA kernel with the E4M3 quantiser (16-B aligned
 // calls; cooperative, one CTA per SM; done_words >= nitems).
 void launch_fp8_onchip(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,

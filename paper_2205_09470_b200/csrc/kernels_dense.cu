@@ -220,11 +220,12 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const Item* __restrict__ it
 }
 
 // ----------------------------------------------------------------------------- INT8 pass 2
-template <bool EF, bool VEC, bool FP8 = false>
+template <bool EF, bool VEC, bool FP8 = false, bool SR = false>
 __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict__ items, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
                                                          Dests dst,
-                                                         const uint32_t* __restrict__ scratch, uint32_t* flags) {
+                                                         const uint32_t* __restrict__ scratch, uint32_t* flags,
+                                                         SrArgs sr = SrArgs{}) {
   int hint = 0;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     const int i = find_item(items, nitems, c, hint);
@@ -241,7 +242,10 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
     const uint64_t bo = it.slot_off + 16;
-    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, FP8 ? M_FP8 : M_INT8, (uint32_t)it.n, s, 0u);
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, FP8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, s, 0u);
+    uint64_t srb = 0;
+    if constexpr (SR)
+      srb = qsgd_base(sr.seed, sr.step, qsgd_key(sr.cluster0 + it.sidx / sr.num_buckets, sr.shard, it.sidx % sr.num_buckets));
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
@@ -262,6 +266,12 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
           wv = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
           d0 = __fmul_rn(fp8_val(wv), s); d1 = __fmul_rn(fp8_val(wv >> 8), s);
           d2 = __fmul_rn(fp8_val(wv >> 16), s); d3 = __fmul_rn(fp8_val(wv >> 24), s);
+        } else if constexpr (SR) {
+          const uint64_t e0 = 4 * q;
+          int q0 = qsgd_q(p.x, s, qsgd_u(srb, e0)), q1 = qsgd_q(p.y, s, qsgd_u(srb, e0 + 1)),
+              q2 = qsgd_q(p.z, s, qsgd_u(srb, e0 + 2)), q3 = qsgd_q(p.w, s, qsgd_u(srb, e0 + 3));
+          wv = pack_i8x4(q0, q1, q2, q3);
+          d0 = __fmul_rn((float)q0, s); d1 = __fmul_rn((float)q1, s); d2 = __fmul_rn((float)q2, s); d3 = __fmul_rn((float)q3, s);
         } else {
           int q0 = int8_qi(p.x, s, sinv), q1 = int8_qi(p.y, s, sinv), q2 = int8_qi(p.z, s, sinv), q3 = int8_qi(p.w, s, sinv);
           wv = pack_i8x4(q0, q1, q2, q3);
@@ -282,6 +292,10 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
         if constexpr (FP8) {
           ce = fp8x2_of(p, 0.0f, s) & 0xFF;
           de = __fmul_rn(fp8_val(ce), s);
+        } else if constexpr (SR) {
+          const int qe = qsgd_q(p, s, qsgd_u(srb, e));
+          ce = (uint32_t)qe & 0xFF;
+          de = __fmul_rn((float)qe, s);
         } else {
           const int qe = int8_qi(p, s, sinv);
           ce = (uint32_t)qe & 0xFF;
@@ -672,6 +686,18 @@ void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int
   ++*L.launches;
 }
 
+void launch_qsgd_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                       const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags,
+                       const SrArgs& sr) {
+  if (!chunks) return;
+  Mark mk(L, PH_QSGD_QUANT);
+  if (ef && vec) k_int8_quant<true, true, false, true><<<GRID((k_int8_quant<true, true, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags, sr);
+  else if (ef) k_int8_quant<true, false, false, true><<<GRID((k_int8_quant<true, false, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags, sr);
+  else if (vec) k_int8_quant<false, true, false, true><<<GRID((k_int8_quant<false, true, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags, sr);
+  else k_int8_quant<false, false, false, true><<<GRID((k_int8_quant<false, false, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags, sr);
+  ++*L.launches;
+}
+
 template <int METHOD, int P>
 static void reduce_p(const Launch& L, bool vec, const RItem* items, int nitems, uint64_t chunks, const Dests& slots,
                      float* out) {
@@ -699,7 +725,7 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
   if (method == M_IDENTITY) reduce_m<M_IDENTITY>(L, P, vec, items, nitems, chunks, slots, out);
   else if (method == M_FP16) reduce_m<M_FP16>(L, P, vec, items, nitems, chunks, slots, out);
   else if (method == M_FP8) reduce_m<M_FP8>(L, P, vec, items, nitems, chunks, slots, out);
-  else reduce_m<M_INT8>(L, P, vec, items, nitems, chunks, slots, out);
+  else reduce_m<M_INT8>(L, P, vec, items, nitems, chunks, slots, out);   // INT8 and QSGD: same decode
   ++*L.launches;
 }
 

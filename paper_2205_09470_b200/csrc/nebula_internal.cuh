@@ -21,7 +21,7 @@ constexpr int kChunkQuads = kThreads * kQuadsPerThread;
 constexpr uint64_t kChunkElems = (uint64_t)kChunkQuads * 4;   // 4096 elements per chunk
 
 enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u, kFlagPeerTimeout = 4u };
-enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3, M_FP8 = 4 };
+enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3, M_FP8 = 4, M_QSGD = 6 };
 enum : int { V_F32 = 0, V_F16 = 1, V_I8 = 2 };
 
 // One (cluster, bucket) unit of codec work.  Offsets are relative to per-call base
@@ -186,6 +186,39 @@ __device__ __forceinline__ float fp8_val(uint32_t byte) {
   __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(byte & 0xFF), __NV_E4M3);
   return __half2float(__half(h));
 }
+
+// QSGD (NEXT-4, R32): counter-based uniforms.  splitmix64(z) = mix(z + gamma) (Steele, Lea &
+// Flood 2014); per (seed, step, cluster, bucket, shard) a base state, per element e the output
+// splitmix64(base + e * gamma) >> 40, scaled by 2^-24 (exact in binary32).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t qsgd_key(uint32_t cluster, uint32_t shard, uint32_t bucket) {
+  return ((((uint64_t)cluster * 65536u + shard) << 32) | bucket);
+}
+__device__ __forceinline__ uint64_t qsgd_base(uint64_t seed, uint64_t step, uint64_t key) {
+  return splitmix64(seed ^ splitmix64(step ^ splitmix64(key)));
+}
+__device__ __forceinline__ float qsgd_u(uint64_t base, uint64_t e) {
+  return (float)(uint32_t)(splitmix64(base + e * 0x9E3779B97F4A7C15ull) >> 40) * 5.9604644775390625e-8f;  // 2^-24
+}
+// q = floor(x) + [u < x - floor(x)], x = fl(p / s) (IEEE division), clamped to [-127, 127]
+__device__ __forceinline__ int qsgd_q(float p, float s, float u) {
+  const float x = __fdiv_rn(p, s);
+  const float f = floorf(x);
+  const float q = __fadd_rn(f, u < __fsub_rn(x, f) ? 1.0f : 0.0f);
+  return max(-127, min(127, (int)q));
+}
+// What the QSGD quantiser needs besides p and s: the generator state of this call.
+struct SrArgs {
+  uint64_t seed, step;
+  uint32_t cluster0;   // cluster id of item sidx / num_buckets == 0 (LOOPBACK 0, else this rank's)
+  uint32_t shard;      // local rank in the cluster (G > 1), else 0
+  uint32_t num_buckets;
+};
 
 __device__ __forceinline__ uint32_t pack_i8x4(int a, int b, int c, int d) {
   return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |

@@ -63,7 +63,7 @@ struct DevGuard {
 struct nebula_ctx {
   nebula_topology topo{};
   nebula_codec codec{};
-  int P = 1, G = 1, Ploc = 1, me = 0, device = 0, num_sms = 148;
+  int P = 1, G = 1, Ploc = 1, me = 0, local_rank = 0, device = 0, num_sms = 148;
   bool loopback = false;
   std::vector<BucketInfo> b;
   uint64_t total_n = 0, total_cn = 0, total_slots = 0;
@@ -113,6 +113,7 @@ struct nebula_ctx {
   int int8_kernel = 0;          // NEBULA_OPT_INT8_KERNEL
   int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
   int step_fusion = 0;          // NEBULA_OPT_STEP_FUSION: 0 fuse INT8 steps where eligible, 1 never
+  uint64_t sr_seed = 0;         // NEBULA_OPT_SR_SEED (QSGD uniforms, R32)
   int exact_scale = 0;          // NEBULA_OPT_EXACT_SCALE: 1 = cluster-wide INT8/FP8 scale when G > 1 (R28)
   bool onchip_ok = false;
   int onchip_grid = 0;
@@ -190,6 +191,7 @@ static uint64_t payload_bytes_for(int method, uint64_t n, uint64_t k, int vt) {
     case M_IDENTITY: return 16 + pad16(4 * n);
     case M_FP16: return 16 + pad16(2 * n);
     case M_INT8:
+    case M_QSGD:
     case M_FP8: return 16 + pad16(n);
     default: return 16 + pad16(4 * k) + pad16(value_bytes(vt) * k);
   }
@@ -217,7 +219,7 @@ static nebula_status validate(const nebula_topology* t, const nebula_codec* c, c
       return fail(nullptr, NEBULA_ERR_INVALID_ARG, "local_rank out of range");
   }
   if (t->device < 0) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "device must be >= 0");
-  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_FP8)
+  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_QSGD || c->method == 5)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown method");
   if (c->error_feedback != 0 && c->error_feedback != 1)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "error_feedback must be 0 or 1");
@@ -505,6 +507,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
   ctx->loopback = topo->transport == NEBULA_TRANSPORT_LOOPBACK;
   ctx->Ploc = ctx->loopback ? ctx->P : 1;
   ctx->me = ctx->loopback ? 0 : topo->cluster_id;
+  ctx->local_rank = ctx->loopback ? 0 : topo->local_rank;
   ctx->device = topo->device;
   ctx->stream = (cudaStream_t)stream;
 
@@ -697,6 +700,22 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
         launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
                           ctx->d_flags);
       }
+      break;
+    }
+    case M_QSGD: {   // NEXT-4 (R32): max-abs pass, [cluster-wide max (R28)], stochastic-rounding pass
+      {
+        Mark mk(L, PH_MEMSET);
+        if (bucket == NEBULA_ALL_BUCKETS) {
+          CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
+        } else {
+          for (int c = 0; c < ctx->Ploc; ++c)
+            CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
+        }
+      }
+      launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
+      if (ctx->exact_scale && ctx->G > 1) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
+      const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
+      launch_qsgd_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, sr);
       break;
     }
     case M_FP8: {   // NEXT-4 (R27): max-abs pass, [cluster-wide max (R28)], quantise pass
@@ -1066,6 +1085,10 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->fp16_kernel = (int)value;
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_SR_SEED) {
+    ctx->sr_seed = (uint64_t)value;
+    return NEBULA_OK;
+  }
   if (option == NEBULA_OPT_EXACT_SCALE) {
     if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exact-scale option must be 0 or 1");
     for (const auto& bk : ctx->b)
@@ -1126,7 +1149,7 @@ const char* nebula_phase_name(uint32_t phase) {
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
       "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
-      "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale"};
+      "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale", "qsgd_ef_quant_pack"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

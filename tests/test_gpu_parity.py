@@ -31,7 +31,7 @@ def bits(a):
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
                  start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
-                 fp16_kernel=None):
+                 fp16_kernel=None, sr_seed=0):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
@@ -42,8 +42,10 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
             ctx.set_step_fusion(False)
     if fp16_kernel:
         ctx.set_fp16_kernel(fp16_kernel)
+    if sr_seed:
+        ctx.set_sr_seed(sr_seed)
     codec = O.Codec(method=method, topk_values=vt, topk_k=k, topk_density=rho, error_feedback=ef,
-                    start_step=start_step)
+                    start_step=start_step, sr_seed=sr_seed)
     total = sum(sizes)
     rs = [[np.zeros(n, F32) for n in sizes] for _ in range(P)]
     for t in range(steps):
@@ -72,7 +74,7 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
         off = 0
         for b, n in enumerate(sizes):
             exp_out, r_new, payloads, stats = O.oracle_step([gs[c][b] for c in range(P)],
-                                                            [rs[c][b] for c in range(P)], codec, t)
+                                                            [rs[c][b] for c in range(P)], codec, t, bucket=b)
             for c in range(P):
                 got = ctx.payload_copy(b, c)
                 assert got == payloads[c], f"payload mismatch bucket {b} cluster {c} step {t}: " \
@@ -172,6 +174,20 @@ def test_fp8_kernels(nb, kern, sizes, ef):
     assert run_loopback(nb, O.FP8, sizes, 2, int8_kernel=kern, ef=ef, steps=2) > 0
 
 
+@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20]])
+@pytest.mark.parametrize("seed", [0, 2 ** 64 - 5])
+def test_qsgd_parity(nb, P, sizes, seed):
+    """QSGD stochastic rounding (NEXT-4, R32): payload bytes (every rounding decision), residuals
+    and averages bit-exact vs the oracle's independent SplitMix64 stream."""
+    assert run_loopback(nb, O.QSGD, sizes, P, steps=2, sr_seed=seed) > 0
+
+
+@pytest.mark.parametrize("kind", ["ties", "half-ties", "zeros", "tiny-max", "subnormal"])
+def test_qsgd_edge_values(nb, kind):
+    run_loopback(nb, O.QSGD, [5000, 17], 2, kind=kind, steps=2, sr_seed=11)
+
+
 @pytest.mark.parametrize("kern", ["two-pass", "fused-ws"])
 def test_fp8_near_rounding_boundaries(nb, kern):
     """Quotients on / next to E4M3 midpoints: the reciprocal fast path must hand every one of
@@ -254,7 +270,7 @@ def test_topk_fallback_path_is_exercised(nb):
 
 
 # ------------------------------------------------------------------ device errors
-@pytest.mark.parametrize("method", [O.IDENTITY, O.FP16, O.INT8, O.TOPK, O.FP8])
+@pytest.mark.parametrize("method", [O.IDENTITY, O.FP16, O.INT8, O.TOPK, O.FP8, O.QSGD])
 @pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
 def test_nonfinite_is_reported(nb, method, bad):
     import torch
