@@ -131,6 +131,7 @@ def load() -> ctypes.CDLL:
         "nebula_svd_decompress": (I32, [P, VP, VP]),
         "nebula_svd_check": (I32, [P]),
         "nebula_svd_kernel_launches": (U64, [P]),
+        "nebula_svd_set_eigensolver": (I32, [P, I32]),
         "nebula_svd_destroy": (I32, [P]),
         "nebula_svd_last_error": (ctypes.c_char_p, [P]),
         "nebula_last_error": (ctypes.c_char_p, [P]),
@@ -416,6 +417,10 @@ class SvdCodec:
 
     def kernel_launches(self) -> int:
         return self._L.nebula_svd_kernel_launches(self._h)
+
+    def set_eigensolver(self, which: str):
+        """'syevd' (default, divide and conquer) | 'syevj' (Jacobi)."""
+        self._ck(self._L.nebula_svd_set_eigensolver(self._h, {"syevd": 0, "syevj": 1}[which]))
 
     def destroy(self):
         if getattr(self, "_h", None):

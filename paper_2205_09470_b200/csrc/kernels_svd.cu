@@ -311,6 +311,8 @@ struct nebula_svd {
   int ntiles = 0, splits = 1;
   int64_t rows_per_split = 0;
   int lwork = 0;
+  int eig = 0;                   // 0: cusolverDnDsyevd (divide & conquer), 1: cusolverDnDsyevj (Jacobi)
+  syevjInfo_t jinfo = nullptr;
   uint64_t launches = 0;
   std::string err;
 };
@@ -386,6 +388,14 @@ nebula_status nebula_svd_init(nebula_svd** out, int64_t m, int64_t n, int32_t r,
   if (cusolverDnDsyevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)k, h->G, (int)k,
                                   h->lambda, &h->lwork) != CUSOLVER_STATUS_SUCCESS)
     return bail(NEBULA_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  int lwj = 0;
+  if (cusolverDnCreateSyevjInfo(&h->jinfo) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnXsyevjSetTolerance(h->jinfo, 1e-14) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnXsyevjSetMaxSweeps(h->jinfo, 30) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDsyevj_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)k, h->G, (int)k,
+                                  h->lambda, &lwj, h->jinfo) != CUSOLVER_STATUS_SUCCESS)
+    return bail(NEBULA_ERR_CUDA, "cusolverDn syevj setup failed");
+  if (lwj > h->lwork) h->lwork = lwj;
   if (cudaMalloc(&h->work, sizeof(double) * (h->lwork > 0 ? h->lwork : 1)) != cudaSuccess)
     return bail(NEBULA_ERR_OOM, "eigensolver workspace allocation failed");
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(NEBULA_ERR_CUDA, "device sync after SVD init failed");
@@ -412,8 +422,12 @@ nebula_status nebula_svd_compress(nebula_svd* h, const float* dev_A, void* dev_p
   k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
   ++h->launches;
   SVD_CK(h, cudaGetLastError());
-  if (cusolverDnDsyevd(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, s.k, h->G, s.k, h->lambda, h->work,
-                       h->lwork, h->info) != CUSOLVER_STATUS_SUCCESS) {
+  const cusolverStatus_t es =
+      h->eig == 1 ? cusolverDnDsyevj(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, s.k, h->G, s.k, h->lambda,
+                                     h->work, h->lwork, h->info, h->jinfo)
+                  : cusolverDnDsyevd(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, s.k, h->G, s.k, h->lambda,
+                                     h->work, h->lwork, h->info);
+  if (es != CUSOLVER_STATUS_SUCCESS) {
     cudaSetDevice(prev);
     return svd_fail(h, NEBULA_ERR_CUDA, "cusolverDnDsyevd failed to launch");
   }
@@ -470,12 +484,20 @@ nebula_status nebula_svd_set_stream(nebula_svd* h, void* stream) {
 
 uint64_t nebula_svd_kernel_launches(const nebula_svd* h) { return h ? h->launches : 0; }
 
+nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which) {
+  if (!h) return NEBULA_ERR_INVALID_ARG;
+  if (which != 0 && which != 1) return svd_fail(h, NEBULA_ERR_INVALID_ARG, "eigensolver must be 0 (syevd) or 1 (syevj)");
+  h->eig = which;
+  return NEBULA_OK;
+}
+
 nebula_status nebula_svd_destroy(nebula_svd* h) {
   if (!h) return NEBULA_OK;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->jinfo) cusolverDnDestroySyevjInfo(h->jinfo);
   if (h->solver) cusolverDnDestroy(h->solver);
   cudaFree(h->G); cudaFree(h->lambda); cudaFree(h->work); cudaFree(h->sigma); cudaFree(h->Wr); cudaFree(h->Y);
   cudaFree(h->sign); cudaFree(h->info); cudaFree(h->flags); cudaFree(h->tiles);

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--rhos", default="0.9,0.8,0.7,0.6,0.5,0.4,0.3,0.2")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--eig", default="syevd", choices=["syevd", "syevj"])
     args = ap.parse_args()
     import torch
     import paper_2205_09470_b200 as nb
@@ -39,6 +40,7 @@ def main():
     out = torch.empty(m, n, device="cuda")
     for rho in [float(x) for x in args.rhos.split(",")]:
         h = nb.SvdCodec(m, n, rho=rho)
+        h.set_eigensolver(args.eig)
         r = h.r
         pl = torch.empty(h.payload_bytes(), dtype=torch.uint8, device="cuda")
         st = torch.cuda.current_stream()
@@ -59,7 +61,7 @@ def main():
         c, d = float(np.median(tc)), float(np.median(td))
         flops_c = L * k * k + 2.0 * L * k * r
         flops_d = 2.0 * m * n * r
-        print(json.dumps({"workload": f"svd-fp16 m={m} n={n}", "rho": rho, "r": r,
+        print(json.dumps({"workload": f"svd-fp16 m={m} n={n}", "eigensolver": args.eig, "rho": rho, "r": r,
                           "payload_ratio": round((h.payload_bytes() - 16) / (4.0 * m * n), 4),
                           "compress_ms": round(c, 4), "decompress_ms": round(d, 4),
                           "compress_gbs_fp32": round(4.0 * m * n / c / 1e6, 2),
