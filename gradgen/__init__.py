@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties", "int-ties")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -222,6 +222,20 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
         mids = (grid[:-1] + grid[1:]) / 2.0
         g = (mids[rng.integers(0, mids.size, size=n)] / 448.0).astype(np.float32)
         g *= np.where(rng.random(n) < 0.5, -1.0, 1.0).astype(np.float32)
+        steps = rng.integers(-3, 4, size=n)
+        for d in (-3, -2, -1, 1, 2, 3):
+            sel = steps == d
+            toward = np.float32(np.inf) if d > 0 else np.float32(-np.inf)
+            for _ in range(abs(d)):
+                g[sel] = np.nextafter(g[sel], toward)
+        g = np.clip(g, -1.0, 1.0).astype(np.float32)
+        g[0] = np.float32(1.0)
+        return g
+    if kind == "int-ties":
+        # max |g| = 1 and every other value within a few ulps of k/127: quotients on or next to
+        # integers (where a floor / fractional-part shortcut is most fragile)
+        k = rng.integers(-127, 128, size=n).astype(np.float64)
+        g = (k / 127.0).astype(np.float32)
         steps = rng.integers(-3, 4, size=n)
         for d in (-3, -2, -1, 1, 2, 3):
             sel = steps == d

@@ -1149,6 +1149,108 @@ __global__ void __launch_bounds__(kDenThreads) k_topk_densify(const RItem* __res
   }
 }
 
+// Sparse variant (a sub-tile holds well under 32 entries per cluster, e.g. rho = 1 %): every
+// lane keeps ONE entry of each cluster resident in registers — a 32-entry window per cluster,
+// reloaded only when a sub-tile consumes all of it — so consecutive sub-tiles of a warp need no
+// global load at all on their critical path (the window covers ~6 sub-tiles at 1 % density):
+// zero the shared tile, drop the window's in-range entries in, store.  Same results as
+// k_topk_densify (same tree order, +0.0 fill).
+template <int P, bool VEC>
+__global__ void __launch_bounds__(kDenThreads) k_topk_densify_w(const RItem* __restrict__ items, int nitems,
+                                                                uint64_t tiles, Dests src, float* __restrict__ obase,
+                                                                int vt) {
+  extern __shared__ __align__(16) float s_v[];   // per warp: [P][kDenSub]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* sw = s_v + (size_t)warp * P * kDenSub;
+  const uint64_t nsub = tiles * (kRedTile / kDenSub);
+  const uint64_t nw = (uint64_t)gridDim.x * (kDenThreads / 32), gw = (uint64_t)blockIdx.x * (kDenThreads / 32) + warp;
+  const uint64_t per = (nsub + nw - 1) / nw;
+  const uint64_t sa = gw * per, sb = min(nsub, sa + per);
+  int i = -1;
+  RItem it{};
+  uint64_t it_end = 0;
+  uint32_t wb[P];        // window base entry of each cluster
+  uint32_t xw[P];        // this lane's entry (wb + lane): index, 0xFFFFFFFF past the end
+  float vw[P];
+  const uint8_t* sl[P];
+  float scale[P];
+  uint64_t voff = 0;
+  auto load_window = [&](int c) {
+    const uint32_t e = wb[c] + (uint32_t)lane;
+    xw[c] = 0xFFFFFFFFu;
+    vw[c] = 0.0f;
+    if (e < it.k) {
+      xw[c] = reinterpret_cast<const uint32_t*>(sl[c] + 16)[e];
+      vw[c] = topk_decode(sl[c] + voff, e, vt, scale[c]);
+    }
+  };
+  for (uint64_t q = sa; q < sb; ++q) {
+    const uint64_t t = q / (kRedTile / kDenSub);
+    if (i < 0 || q >= it_end) {
+      i = find_by(items, nitems, t, [](const RItem& r) { return r.t0; });
+      it = items[i];
+      it_end = (it.t0 + (it.n + kRedTile - 1) / kRedTile) * (kRedTile / kDenSub);
+      voff = 16 + pad16(4 * it.k);
+      const uint32_t x0 = (uint32_t)((q - it.t0 * (kRedTile / kDenSub)) * kDenSub);
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        sl[c] = src.p[c] + it.slot_off + (uint64_t)c * it.pb;
+        scale[c] = vt == V_I8 ? *reinterpret_cast<const float*>(sl[c] + 8) : 1.0f;
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(sl[c] + 16);
+        uint32_t lo = 0, hi = (uint32_t)it.k;   // lower_bound(x0), warp-uniform
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (idx[mid] < x0) lo = mid + 1; else hi = mid;
+        }
+        wb[c] = lo;
+        load_window(c);
+      }
+    }
+    const uint32_t e0 = (uint32_t)((q - it.t0 * (kRedTile / kDenSub)) * kDenSub);
+    if (e0 >= it.n) continue;
+    const uint32_t e1 = (uint32_t)min(it.n, (uint64_t)e0 + (uint64_t)kDenSub);
+#pragma unroll
+    for (int v = 0; v < P * kDenSub / 128; ++v)
+      reinterpret_cast<float4*>(sw)[v * 32 + lane] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      while (true) {
+        const bool in = xw[c] >= e0 && xw[c] < e1;
+        if (in) sw[c * kDenSub + (xw[c] - e0)] = vw[c];
+        // window exhausted inside this sub-tile (every lane's entry is < e1): slide by 32
+        if (__ballot_sync(0xFFFFFFFFu, xw[c] < e1) != 0xFFFFFFFFu) break;
+        wb[c] += 32;
+        load_window(c);
+      }
+    }
+    __syncwarp();
+    float* out = obase + it.out_off + e0;
+    if (VEC && e1 - e0 == (uint32_t)kDenSub) {
+#pragma unroll
+      for (int v = 0; v < kDenSub / 128; ++v) {
+        const int j = v * 32 + lane;
+        float a[P], b[P], d[P], e[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const float4 w = reinterpret_cast<const float4*>(sw + c * kDenSub)[j];
+          a[c] = w.x; b[c] = w.y; d[c] = w.z; e[c] = w.w;
+        }
+        st4(out + 4 * j, make_float4(div_p_sparse<P>(tree_sum<0, P>(a)), div_p_sparse<P>(tree_sum<0, P>(b)),
+                                     div_p_sparse<P>(tree_sum<0, P>(d)), div_p_sparse<P>(tree_sum<0, P>(e))));
+      }
+    } else {
+      for (uint32_t j = lane; j < e1 - e0; j += 32) {
+        float v[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) v[c] = sw[c * kDenSub + j];
+        out[j] = div_p_sparse<P>(tree_sum<0, P>(v));
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <bool EF, bool VEC>
@@ -1246,12 +1348,28 @@ static void densify_pu(const Launch& L, int vt, bool vec, const RItem* items, in
   else k_topk_densify<P, U, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
 }
 
+template <int P>
+static void densify_w(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
+                      const Dests& slots, float* out) {
+  const size_t smem = (size_t)(kDenThreads / 32) * P * kDenSub * sizeof(float);
+  const void* f = vec ? (const void*)k_topk_densify_w<P, true> : (const void*)k_topk_densify_w<P, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[vec]) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[vec] = true;
+  }
+  const unsigned grid = persistent_grid(L, tiles * (kRedTile / kDenSub) / (kDenThreads / 32) + 1, f, kDenThreads, smem);
+  if (vec) k_topk_densify_w<P, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
+  else k_topk_densify_w<P, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
+}
+
 // U = entries per lane per round: sized so a typical 512-element sub-tile's run fits one round
 template <int P>
 static void densify_p(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
                       uint64_t entries, const Dests& slots, float* out) {
   const double per_sub = (double)entries / (double)(tiles * (kRedTile / kDenSub));   // entries per sub-tile
-  if (per_sub * 1.25 <= 32.0 || P > 4) densify_pu<P, 1>(L, vt, vec, items, nitems, tiles, slots, out);
+  if (per_sub * 4.0 <= 32.0) densify_w<P>(L, vt, vec, items, nitems, tiles, slots, out);
+  else if (per_sub * 1.25 <= 32.0 || P > 4) densify_pu<P, 1>(L, vt, vec, items, nitems, tiles, slots, out);
   else if (per_sub <= 64.0 || P > 2) densify_pu<P, 2>(L, vt, vec, items, nitems, tiles, slots, out);
   else densify_pu<P, 4>(L, vt, vec, items, nitems, tiles, slots, out);
 }

@@ -183,7 +183,7 @@ def test_qsgd_parity(nb, P, sizes, seed):
     assert run_loopback(nb, O.QSGD, sizes, P, steps=2, sr_seed=seed) > 0
 
 
-@pytest.mark.parametrize("kind", ["ties", "half-ties", "zeros", "tiny-max", "subnormal"])
+@pytest.mark.parametrize("kind", ["ties", "half-ties", "int-ties", "zeros", "tiny-max", "subnormal"])
 def test_qsgd_edge_values(nb, kind):
     run_loopback(nb, O.QSGD, [5000, 17], 2, kind=kind, steps=2, sr_seed=11)
 
