@@ -212,21 +212,6 @@ __device__ __forceinline__ int qsgd_q(float p, float s, float u) {
   const float q = __fadd_rn(f, u < __fsub_rn(x, f) ? 1.0f : 0.0f);
   return max(-127, min(127, (int)q));
 }
-// Same result without the division where it cannot matter: x' = fl(p * fl(1/s)) is within
-// 3 * 2^-24 |x| < 2.3e-5 of x (|x| <= 128), so if frac(x') is farther than 4e-5 from 0 and 1
-// the floors agree, and if u is farther than 4e-5 from frac(x') the comparison agrees; beyond
-// |x'| >= 127 + 4e-5 both clamp to +-127.  Otherwise (or inv == 0) the IEEE division decides.
-__device__ __forceinline__ int qsgd_q_fast(float p, float s, float inv, float u) {
-  if (inv != 0.0f) {
-    const float x = __fmul_rn(p, inv);
-    if (fabsf(x) >= 127.0f + 4e-5f) return x > 0.0f ? 127 : -127;
-    const float f = floorf(x);
-    const float phi = __fsub_rn(x, f);
-    if (phi > 4e-5f && phi < 1.0f - 4e-5f && fabsf(u - phi) > 4e-5f)
-      return max(-127, min(127, (int)f + (u < phi ? 1 : 0)));
-  }
-  return qsgd_q(p, s, u);
-}
 // What the QSGD quantiser needs besides p and s: the generator state of this call.
 struct SrArgs {
   uint64_t seed, step;

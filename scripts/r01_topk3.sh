@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "topk or qsgd or decompress_single" > gpurun_out/topk_tests.log 2>&1
+timeout 300 python bench.py --method topk --no-cpu --no-e2e --steps 50 > gpurun_out/bench_topk.log 2>&1
+timeout 300 python bench.py --method qsgd --no-cpu --no-e2e --steps 50 > gpurun_out/bench_qsgd.log 2>&1
