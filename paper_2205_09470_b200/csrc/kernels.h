@@ -92,7 +92,7 @@ struct Peers {
 void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
                       const Dests& dst, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
-                      uint64_t seq, int config);
+                      uint64_t seq, int config, bool f8 = false);
 
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.

@@ -1288,7 +1288,14 @@ struct WsCMeta {
   float sc[8];
 };
 
-template <int P>
+// One payload byte -> its decoded value (INT8 / QSGD: q * s; FP8: E4M3(c) * s).
+template <bool F8>
+__device__ __forceinline__ float dec_byte(uint32_t byte, float s) {
+  if constexpr (F8) return __fmul_rn(fp8_val(byte), s);
+  else return __fmul_rn((float)(int8_t)(byte & 0xFF), s);
+}
+
+template <int P, bool F8 = false>
 __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct, int nC, unsigned char* ringC,
                                               uint64_t* fullC, uint64_t* emptyC, WsCMeta* meta) {
   constexpr uint32_t TB = (kWsCStage / P) & ~15u;   // bytes per cluster per stage
@@ -1342,8 +1349,8 @@ __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct,
           float v[P];
 #pragma unroll
           for (int k = 0; k < P; ++k) {
-            const int8_t qv = *reinterpret_cast<volatile const int8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
-            v[k] = __fmul_rn((float)qv, sc[k]);
+            const uint8_t qv = *reinterpret_cast<volatile const uint8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
+            v[k] = dec_byte<F8>(qv, sc[k]);
           }
           out[e] = div_p<P>(tree_sum<0, P>(v));
         }
@@ -1375,7 +1382,7 @@ __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct,
       for (int k = 0; k < P; ++k) {
         const uint32_t w = pay[k * (TB / 4) + j];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) t[e][k] = __fmul_rn((float)(int8_t)((w >> (8 * e)) & 0xFF), sc[k]);
+        for (int e = 0; e < 4; ++e) t[e][k] = dec_byte<F8>(w >> (8 * e), sc[k]);
       }
       st4_hint(out + 4 * j,
                make_float4(div_p<P>(tree_sum<0, P>(t[0])), div_p<P>(tree_sum<0, P>(t[1])),
@@ -1391,7 +1398,7 @@ __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct,
 // Reduce role, register-load variant (P2P pull): buckets in order; this CTA's share of bucket b is the same quad slice its B
 // warps quantised, in 16-element groups (one 16-B load per cluster), staged through a per-warp
 // shared-memory transpose so each store instruction writes 512 contiguous bytes.
-template <int P>
+template <int P, bool F8 = false>
 __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
                                                volatile uint32_t* s_abort, float* s_out, uint32_t* flags) {
   constexpr int E = 16, SROW = E + 1, U = P <= 2 ? 2 : 1;
@@ -1442,7 +1449,7 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
     auto slot = [&](int k, uint64_t gi) { return a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + 16 * gi; };
     auto dec = [&](const uint4& x4, int e, float s) {
       const uint32_t x = (e >> 2) == 0 ? x4.x : (e >> 2) == 1 ? x4.y : (e >> 2) == 2 ? x4.z : x4.w;
-      return __fmul_rn((float)(int8_t)((x >> (8 * (e & 3))) & 0xFF), s);
+      return dec_byte<F8>(x >> (8 * (e & 3)), s);
     };
     for (uint64_t gb = g0 + (uint64_t)cw * 32 * U; gb < g1; gb += (uint64_t)ncw * 32 * U) {
       if constexpr (P <= 4) {
@@ -1526,8 +1533,8 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
         float v[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          const int8_t q = *reinterpret_cast<volatile const int8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
-          v[k] = __fmul_rn((float)q, sc[k]);
+          const uint8_t q = *reinterpret_cast<volatile const uint8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
+          v[k] = dec_byte<F8>(q, sc[k]);
         }
         out[e] = div_p<P>(tree_sum<0, P>(v));
       }
@@ -1536,14 +1543,13 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
 }
 
 // CM: reduce role — 0 none (compress only), 1 TMA variant (LOOPBACK), 2 register loads (P2P pull)
-// F8: the same single-pass schedule for the FP8 E4M3 codec (NEXT-4, R27) — only the B
-// warps' scale / quantise / dequantise differ; compress-only (no fused reduce role).
+// F8: the same schedules for the FP8 E4M3 codec (NEXT-4, R27) — only the B warps' scale /
+// quantise / dequantise and the C warps' byte decode differ.
 template <bool EF, int AW, int BW, int CW, int CM, bool F8 = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
   static_assert(1 + AW + BW + CW == kWsThreads / 32, "warp roles must fill the CTA");
-  static_assert(!F8 || CW == 0, "FP8 runs the compress-only kernel");
   constexpr int kA = AW * 32, kB = BW * 32, kC = CW * 32;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   WsStageA* ringA = reinterpret_cast<WsStageA*>(ws_smem);
@@ -1802,7 +1808,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if constexpr (CM == 1) {
       static_assert(CW >= 2, "the TMA reduce role needs a producer warp and consumer warps");
       unsigned char* ringC = ws_smem + sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
-#define NB_C(PP) ws_reduce_tma<PP>(sa, nb, ct, kC, ringC, fullC, emptyC, s_cmeta)
+#define NB_C(PP) ws_reduce_tma<PP, F8>(sa, nb, ct, kC, ringC, fullC, emptyC, s_cmeta)
       switch (sa.src.n) {
         case 1: NB_C(1); break;
         case 2: NB_C(2); break;
@@ -1816,7 +1822,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #undef NB_C
     } else {
       __shared__ float s_out[CW * 32 * 17];
-#define NB_C(PP) ws_reduce_ld<PP>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags)
+#define NB_C(PP) ws_reduce_ld<PP, F8>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags)
       switch (sa.src.n) {
         case 1: NB_C(1); break;
         case 2: NB_C(2); break;
@@ -2126,7 +2132,8 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
 // warp-specialised kernel with reduce warps).  bar_words: 2 * nitems words (done, bdone).
 // Warp splits (A, B, C) of the fused step; config 0 is the default, the rest a tuning sweep.
 template <bool EF>
-static const void* step_kernel(int config) {
+static const void* step_kernel(int config, bool f8) {
+  if (f8) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, true>;
   switch (config) {
     // LOOPBACK (TMA reduce role)
     case 1: return (const void*)k_int8_ws<EF, 5, 20, 6, 1>;
@@ -2147,7 +2154,7 @@ static const void* step_kernel(int config) {
 void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
                       const Dests& dst_in, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
-                      uint64_t seq, int config) {
+                      uint64_t seq, int config, bool f8) {
   Mark mk(L, PH_INT8_STEP);
   cudaMemsetAsync(bar_words, 0, sizeof(unsigned) * 2 * (size_t)nitems, L.stream);
   Dests dst = dst_in;
@@ -2164,14 +2171,15 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
   sa.PL = PL;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&scratch,
                   (void*)&flags, (void*)&done, (void*)&sa};
-  const void* f = ef ? step_kernel<true>(config) : step_kernel<false>(config);
+  if (f8 && config != 4) config = 0;   // FP8: the two default splits only
+  const void* f = ef ? step_kernel<true>(config, f8) : step_kernel<false>(config, f8);
   // the TMA reduce role (LOOPBACK configs) adds its ring; the register-load role uses static smem
   const bool tma_c = config <= 3 || config > 10;
   const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB + (tma_c ? (size_t)kWsNC * kWsCStage : 0);
-  static bool attr[2][11] = {};
-  if (!attr[ef][config < 0 || config > 10 ? 0 : config]) {
+  static bool attr[2][2][11] = {};
+  if (!attr[f8][ef][config < 0 || config > 10 ? 0 : config]) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[ef][config < 0 || config > 10 ? 0 : config] = true;
+    attr[f8][ef][config < 0 || config > 10 ? 0 : config] = true;
   }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);

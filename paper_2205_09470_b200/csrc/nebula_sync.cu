@@ -887,7 +887,9 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 // call is one the warp-specialised kernel serves and the exchange is LOOPBACK or P2P.
 static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
                          uint64_t step) {
-  if (ctx->step_fusion == 1 || method_at(ctx, step) != M_INT8 || ctx->G != 1 || !ctx->onchip_ok) return false;
+  const int m = method_at(ctx, step);
+  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8) || ctx->G != 1 || !ctx->onchip_ok) return false;
+  if (m == M_FP8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8-only
   // LOOPBACK, or P2P pull (the reduce warps load the peers' payloads); with P2P push the
   // compress kernel's NVLink stores are cheaper outside the fused kernel (fewer quantise warps)
   if (!(ctx->loopback || ctx->P == 1 || ctx->xmode == 3)) return false;
@@ -903,7 +905,7 @@ static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, 
 }
 
 static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* dev_grad,
-                                     float* dev_out) {
+                                     float* dev_out, int method) {
   const bool ef = ctx->codec.error_feedback != 0;
   const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
   const Table& T = ctx->ctab[lay][t];
@@ -928,11 +930,11 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, ctx->b[lo]),
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
                    sources_of(ctx, ctx->b[lo]), dev_out, pe, ctx->d_arrive, ctx->b[lo].seq,
-                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0));
+                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0), method == M_FP8);
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
     ctx->b[i].state = ST_IDLE;
-    ctx->b[i].method = M_INT8;
+    ctx->b[i].method = method;
   }
   return NEBULA_OK;
 }
@@ -943,7 +945,7 @@ nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad
     if (range_of(ctx, bucket, &lo, &hi) && hi > lo && dev_grad && dev_out &&
         step_fusable(ctx, lo, hi, bucket, dev_grad, dev_out, step)) {
       DevGuard dg(ctx->device);
-      return int8_step_fused(ctx, lo, hi, bucket, dev_grad, dev_out);
+      return int8_step_fused(ctx, lo, hi, bucket, dev_grad, dev_out, method_at(ctx, step));
     }
   }
   nebula_status s = nebula_compress(ctx, bucket, dev_grad, step);

@@ -188,6 +188,13 @@ def test_qsgd_edge_values(nb, kind):
     run_loopback(nb, O.QSGD, [5000, 17], 2, kind=kind, steps=2, sr_seed=11)
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_fp8_fused_step(nb, P, per_bucket):
+    """FP8 through the fused compress + exchange + average kernel (buckets >= 1M elements)."""
+    run_loopback(nb, O.FP8, [1 << 20, 3 << 19, (1 << 20) + 5], P, steps=2, per_bucket=per_bucket)
+
+
 @pytest.mark.parametrize("kern", ["two-pass", "fused-ws"])
 def test_fp8_near_rounding_boundaries(nb, kern):
     """Quotients on / next to E4M3 midpoints: the reciprocal fast path must hand every one of
