@@ -418,9 +418,11 @@ class SvdCodec:
     def kernel_launches(self) -> int:
         return self._L.nebula_svd_kernel_launches(self._h)
 
-    def set_eigensolver(self, which: str):
-        """'syevd' (default, divide and conquer) | 'syevj' (Jacobi)."""
-        self._ck(self._L.nebula_svd_set_eigensolver(self._h, {"syevd": 0, "syevj": 1}[which]))
+    def set_eigensolver(self, which: str, gram: str = "dmma"):
+        """which: 'syevd' (default, divide and conquer) | 'syevj' (Jacobi); gram: 'dmma' (FP64
+        tensor cores, default) | 'simt'."""
+        self._ck(self._L.nebula_svd_set_eigensolver(self._h, {"syevd": 0, "syevj": 1}[which] +
+                                                    2 * {"dmma": 0, "simt": 1}[gram]))
 
     def destroy(self):
         if getattr(self, "_h", None):

@@ -109,6 +109,74 @@ __global__ void __launch_bounds__(NT) k_gram(const float* __restrict__ A, Shape 
     }
 }
 
+// Same contraction on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64 — tcgen05 has no fp64
+// kind): a CTA of 4 warps owns the 64 x 64 tile, each warp a 32 x 32 quarter = 4 x 4 MMA tiles
+// of 8 x 8, 32 fp64 accumulators per thread.  Fragments (PTX m8n8k4 .f64): A row-major 8 x 4:
+// a0 = A[g][t]; B col-major 4 x 8: b0 = B[t][g]; C 8 x 8: c{0,1} = C[g][2t + {0,1}], with
+// g = lane / 4, t = lane % 4.  Here A[m][kk] = B(i0 + kk, a0 + m) and B[kk][n] = B(i0 + kk, b0 + n),
+// both read from the fp64 shared slices of k_gram.  Products of fp32 values are exact in fp64
+// and the accumulation is fp64, as in the SIMT kernel (the summation order differs).
+constexpr int GT = 128;   // threads of k_gram_dmma
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(GT) k_gram_dmma(const float* __restrict__ A, Shape s, const int2* __restrict__ tiles,
+                                                 int64_t rows_per_split, double* __restrict__ G, uint32_t* flags) {
+  __shared__ double sa[GK][T + 1], sb[GK][T + 1];
+  const int2 tp = tiles[blockIdx.x];
+  const int a0 = tp.x * T, b0 = tp.y * T;
+  const int64_t i_begin = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t i_end = min(s.L, i_begin + rows_per_split);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;   // warp quarter of the 64 x 64 tile
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][4][2] = {};
+  bool bad = false;
+  for (int64_t i0 = i_begin; i0 < i_end; i0 += GK) {
+#pragma unroll
+    for (int u = 0; u < GK * T / GT; ++u) {
+      const int idx = threadIdx.x + u * GT;
+      const int ii = s.tall ? idx / T : idx % GK;
+      const int aa = s.tall ? idx % T : idx / GK;
+      const int64_t i = i0 + ii;
+      float va = 0.f, vb = 0.f;
+      if (i < i_end) {
+        if (a0 + aa < s.k) va = bval(A, s, i, a0 + aa);
+        if (b0 + aa < s.k) vb = bval(A, s, i, b0 + aa);
+      }
+      bad |= !isfinite(va) || !isfinite(vb);
+      sa[ii][aa] = (double)va;
+      sb[ii][aa] = (double)vb;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int kk = 0; kk < GK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = sa[kk + t][wm + 8 * x + g];
+        fb[x] = sb[kk + t][wn + 8 * x + g];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y], fa[x], fb[y]);
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, F_NONFINITE);
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int a = a0 + wm + 8 * x + g, b = b0 + wn + 8 * y + 2 * t + v;
+        if (a < s.k && b < s.k && a <= b) atomicAdd(&G[(int64_t)a * s.k + b], acc[x][y][v]);
+      }
+}
+
 // ---------------------------------------------------------------- K_prep: top-r eigenpairs
 // cuSOLVER returns ascending lambda and, column-major, eigenvector j in column j: in our
 // row-major view Z[j * k + a] = z_j[a].  sigma_j = sqrt(max(lambda_{k-1-j}, 0)) (fp64);
@@ -312,6 +380,7 @@ struct nebula_svd {
   int64_t rows_per_split = 0;
   int lwork = 0;
   int eig = 0;                   // 0: cusolverDnDsyevd (divide & conquer), 1: cusolverDnDsyevj (Jacobi)
+  int gram_simt = 0;             // 0: FP64 tensor-core Gram (DMMA), 1: SIMT fp64 FMA Gram
   syevjInfo_t jinfo = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -419,7 +488,10 @@ nebula_status nebula_svd_compress(nebula_svd* h, const float* dev_A, void* dev_p
   cudaSetDevice(h->device);
   const Shape s = h->s;
   SVD_CK(h, cudaMemsetAsync(h->G, 0, sizeof(double) * s.k * s.k, h->stream));
-  k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
+  if (h->gram_simt)
+    k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
+  else
+    k_gram_dmma<<<dim3(h->ntiles, h->splits), GT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
   ++h->launches;
   SVD_CK(h, cudaGetLastError());
   const cusolverStatus_t es =
@@ -486,8 +558,9 @@ uint64_t nebula_svd_kernel_launches(const nebula_svd* h) { return h ? h->launche
 
 nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which) {
   if (!h) return NEBULA_ERR_INVALID_ARG;
-  if (which != 0 && which != 1) return svd_fail(h, NEBULA_ERR_INVALID_ARG, "eigensolver must be 0 (syevd) or 1 (syevj)");
-  h->eig = which;
+  if (which < 0 || which > 3) return svd_fail(h, NEBULA_ERR_INVALID_ARG, "eigensolver option must be in [0, 3]");
+  h->eig = which & 1;
+  h->gram_simt = (which >> 1) & 1;
   return NEBULA_OK;
 }
 

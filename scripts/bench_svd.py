@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--eig", default="syevd", choices=["syevd", "syevj"])
+    ap.add_argument("--gram", default="dmma", choices=["dmma", "simt"])
     args = ap.parse_args()
     import torch
     import paper_2205_09470_b200 as nb
@@ -40,7 +41,7 @@ def main():
     out = torch.empty(m, n, device="cuda")
     for rho in [float(x) for x in args.rhos.split(",")]:
         h = nb.SvdCodec(m, n, rho=rho)
-        h.set_eigensolver(args.eig)
+        h.set_eigensolver(args.eig, args.gram)
         r = h.r
         pl = torch.empty(h.payload_bytes(), dtype=torch.uint8, device="cuda")
         st = torch.cuda.current_stream()
@@ -61,7 +62,7 @@ def main():
         c, d = float(np.median(tc)), float(np.median(td))
         flops_c = L * k * k + 2.0 * L * k * r
         flops_d = 2.0 * m * n * r
-        print(json.dumps({"workload": f"svd-fp16 m={m} n={n}", "eigensolver": args.eig, "rho": rho, "r": r,
+        print(json.dumps({"workload": f"svd-fp16 m={m} n={n}", "eigensolver": args.eig, "gram": args.gram, "rho": rho, "r": r,
                           "payload_ratio": round((h.payload_bytes() - 16) / (4.0 * m * n), 4),
                           "compress_ms": round(c, 4), "decompress_ms": round(d, 4),
                           "compress_gbs_fp32": round(4.0 * m * n / c / 1e6, 2),

@@ -37,11 +37,11 @@ def built(m, n, decay, seed, noise=0.0):
     return A.astype(np.float32)
 
 
-def run(nb, A, r, eig="syevd"):
+def run(nb, A, r, eig="syevd", gram="dmma"):
     import torch
     m, n = A.shape
     h = nb.SvdCodec(m, n, r)
-    h.set_eigensolver(eig)
+    h.set_eigensolver(eig, gram)
     assert h.payload_bytes() == O.svd_payload_bytes(m, n, r)
     dA = torch.from_numpy(A).cuda()
     pl = torch.full((h.payload_bytes(),), 0xAB, dtype=torch.uint8, device="cuda")
@@ -71,11 +71,11 @@ def ulp16(x):
 
 @pytest.mark.parametrize("m,n,rho", [(512, 96, 0.6), (96, 512, 0.6), (300, 77, 0.2), (1000, 64, 0.9),
                                      (64, 64, 1.0), (2048, 192, 0.4)])
-@pytest.mark.parametrize("eig", ["syevd", "syevj"])
-def test_svd_parity(nb, m, n, rho, eig):
+@pytest.mark.parametrize("eig,gram", [("syevd", "dmma"), ("syevj", "dmma"), ("syevd", "simt")])
+def test_svd_parity(nb, m, n, rho, eig, gram):
     r = O.svd_rank(m, n, rho)
     A = built(m, n, 0.9, m * 7 + n)
-    gpl, rec, opl, rec_o, launches = run(nb, A, r, eig)
+    gpl, rec, opl, rec_o, launches = run(nb, A, r, eig, gram)
     assert launches >= 6
     assert gpl[:16] == opl[:16] and len(gpl) == len(opl)
     _, _, _, Ug, sg, Vg = O.svd_decode_factors(gpl)
