@@ -244,6 +244,10 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 #define NEBULA_OPT_EXACT_SCALE 5
 /*   NEBULA_OPT_SR_SEED: the 64-bit seed of NEBULA_QSGD's uniforms (default 0); any time. */
 #define NEBULA_OPT_SR_SEED 6
+/*   NEBULA_OPT_TOPK_REDUCE: sparse decompress-average kernel, 0 (default) tile-interleaved
+ *   (per-tile run starts found in parallel, CTAs walk 2048-element tiles grid-stride), 1 warps
+ *   own contiguous ranges of 512-element sub-tiles.  Same results. */
+#define NEBULA_OPT_TOPK_REDUCE 7
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

@@ -35,6 +35,7 @@ OPT_FP16_KERNEL = 3
 OPT_STEP_FUSION = 4
 OPT_EXACT_SCALE = 5
 OPT_SR_SEED = 6
+OPT_TOPK_REDUCE = 7
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 

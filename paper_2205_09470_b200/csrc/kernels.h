@@ -165,8 +165,10 @@ void topk_prepare_bracket(uint32_t keys);
 // Sparse decompress + tree-average (tile merge over the ascending index lists).
 // entries = sum over buckets of (k + 1); tiles = sum of ceil(n / 2048).
 // zero_begin/zero_count: the output range of the call (filled with +0.0 first).
+// start_count = P * sum over the call's buckets of (tiles + 1); variant 0 = tile-interleaved
+// (start offsets kernel + CTA tiles), 1 = per-warp contiguous sub-tile ranges.
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
                         uint64_t entries, uint64_t tiles, const Dests& slots, uint32_t* start, float* out,
-                        float* zero_begin, uint64_t zero_count);
+                        float* zero_begin, uint64_t zero_count, uint64_t start_count, int variant);
 
 }  // namespace nb

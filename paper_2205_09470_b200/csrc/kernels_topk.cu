@@ -1251,6 +1251,95 @@ __global__ void __launch_bounds__(kDenThreads) k_topk_densify_w(const RItem* __r
   }
 }
 
+// Tile-interleaved variant (default).  The contiguous per-warp ranges above leave every warp
+// writing its own far-apart region of the output (~4700 concurrent write streams); here CTAs
+// walk the 2048-element tiles grid-stride, so the active writes form one contiguous window, as
+// in a fill.  A first kernel finds, massively in parallel, where every tile's run starts in
+// every cluster's ascending index list (start[sbase + c (tiles + 1) + t], the last = k); the
+// CTA then zero-fills a shared [P][2048] tile, scatters the run, tree-sums and stores float4.
+__global__ void k_topk_starts(const RItem* __restrict__ items, int nitems, int P, Dests src, uint64_t total,
+                              uint32_t* __restrict__ start) {
+  const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  const uint64_t s = items[0].sbase + x;
+  const int i = find_by(items, nitems, s, [](const RItem& r) { return r.sbase; });
+  const RItem it = items[i];
+  const uint64_t nt = (it.n + kRedTile - 1) / kRedTile;
+  const uint64_t local = s - it.sbase;
+  const int c = (int)(local / (nt + 1));
+  const uint64_t tt = local % (nt + 1);
+  if (c >= P) return;
+  uint32_t v = (uint32_t)it.k;
+  if (tt < nt) {
+    const uint32_t* idx = reinterpret_cast<const uint32_t*>(src.p[c] + it.slot_off + (uint64_t)c * it.pb + 16);
+    const uint32_t x0 = (uint32_t)(tt * kRedTile);
+    uint32_t lo = 0, hi = (uint32_t)it.k;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (idx[mid] < x0) lo = mid + 1; else hi = mid;
+    }
+    v = lo;
+  }
+  start[s] = v;
+}
+
+template <int P, bool VEC>
+__global__ void __launch_bounds__(kDenThreads) k_topk_densify_t(const RItem* __restrict__ items, int nitems,
+                                                                uint64_t tiles, Dests src,
+                                                                const uint32_t* __restrict__ start,
+                                                                float* __restrict__ obase, int vt) {
+  extern __shared__ __align__(16) float s_t[];   // [P][kRedTile]
+  int hint = 0;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int i = hint;
+    while (i + 1 < nitems && items[i + 1].t0 <= t) ++i;
+    hint = i;
+    const RItem it = items[i];
+    const uint64_t tt = t - it.t0, nt = (it.n + kRedTile - 1) / kRedTile;
+    const uint32_t e0 = (uint32_t)(tt * kRedTile);
+    const uint32_t e1 = (uint32_t)min(it.n, (uint64_t)e0 + kRedTile);
+#pragma unroll
+    for (int v = 0; v < P * kRedTile / 4 / kDenThreads; ++v)
+      reinterpret_cast<float4*>(s_t)[v * kDenThreads + threadIdx.x] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    __syncthreads();
+    const uint64_t voff = 16 + pad16(4 * it.k);
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      const uint8_t* sl = src.p[c] + it.slot_off + (uint64_t)c * it.pb;
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(sl + 16);
+      const float scale = vt == V_I8 ? *reinterpret_cast<const float*>(sl + 8) : 1.0f;
+      const uint64_t sb = it.sbase + (uint64_t)c * (nt + 1) + tt;
+      const uint32_t a = start[sb], b = start[sb + 1];
+      for (uint32_t e = a + threadIdx.x; e < b; e += kDenThreads)
+        s_t[c * kRedTile + (idx[e] - e0)] = topk_decode(sl + voff, e, vt, scale);
+    }
+    __syncthreads();
+    float* out = obase + it.out_off + e0;
+    if (VEC && e1 - e0 == (uint32_t)kRedTile) {
+#pragma unroll
+      for (int v = 0; v < kRedTile / 4 / kDenThreads; ++v) {
+        const int j = v * kDenThreads + threadIdx.x;
+        float a[P], b[P], d[P], e[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const float4 w = reinterpret_cast<const float4*>(s_t + c * kRedTile)[j];
+          a[c] = w.x; b[c] = w.y; d[c] = w.z; e[c] = w.w;
+        }
+        st4(out + 4 * j, make_float4(div_p_sparse<P>(tree_sum<0, P>(a)), div_p_sparse<P>(tree_sum<0, P>(b)),
+                                     div_p_sparse<P>(tree_sum<0, P>(d)), div_p_sparse<P>(tree_sum<0, P>(e))));
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < e1 - e0; j += kDenThreads) {
+        float v[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) v[c] = s_t[c * kRedTile + j];
+        out[j] = div_p_sparse<P>(tree_sum<0, P>(v));
+      }
+    }
+    __syncthreads();   // the tile buffer is re-zeroed for the next tile
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <bool EF, bool VEC>
@@ -1349,6 +1438,21 @@ static void densify_pu(const Launch& L, int vt, bool vec, const RItem* items, in
 }
 
 template <int P>
+static void densify_t(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
+                      const Dests& slots, const uint32_t* start, float* out) {
+  const size_t smem = (size_t)P * kRedTile * sizeof(float);
+  const void* f = vec ? (const void*)k_topk_densify_t<P, true> : (const void*)k_topk_densify_t<P, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[vec]) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[vec] = true;
+  }
+  const unsigned grid = persistent_grid(L, tiles, f, kDenThreads, smem);
+  if (vec) k_topk_densify_t<P, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, start, out, vt);
+  else k_topk_densify_t<P, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, start, out, vt);
+}
+
+template <int P>
 static void densify_w(const Launch& L, int vt, bool vec, const RItem* items, int nitems, uint64_t tiles,
                       const Dests& slots, float* out) {
   const size_t smem = (size_t)(kDenThreads / 32) * P * kDenSub * sizeof(float);
@@ -1376,10 +1480,25 @@ static void densify_p(const Launch& L, int vt, bool vec, const RItem* items, int
 
 void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const RItem* items, int nitems,
                         uint64_t entries, uint64_t tiles, const Dests& slots, uint32_t* start, float* out,
-                        float* zero_begin, uint64_t zero_count) {
-  (void)start; (void)zero_begin; (void)zero_count;
+                        float* zero_begin, uint64_t zero_count, uint64_t start_count, int variant) {
+  (void)zero_begin; (void)zero_count;
   if (!tiles) return;
   Mark mk(L, PH_TOPK_REDUCE);
+  if (variant == 0) {   // tile-interleaved (default)
+    k_topk_starts<<<(unsigned)((start_count + 255) / 256), 256, 0, L.stream>>>(items, nitems, P, slots, start_count, start);
+    switch (P) {
+      case 1: densify_t<1>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 2: densify_t<2>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 3: densify_t<3>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 4: densify_t<4>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 5: densify_t<5>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 6: densify_t<6>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      case 7: densify_t<7>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+      default: densify_t<8>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;
+    }
+    *L.launches += 2;
+    return;
+  }
   switch (P) {
     case 1: densify_p<1>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;
     case 2: densify_p<2>(L, value_type, vec, items, nitems, tiles, entries, slots, out); break;

@@ -114,6 +114,7 @@ struct nebula_ctx {
   int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
   int step_fusion = 0;          // NEBULA_OPT_STEP_FUSION: 0 fuse INT8 steps where eligible, 1 never
   uint64_t sr_seed = 0;         // NEBULA_OPT_SR_SEED (QSGD uniforms, R32)
+  int topk_reduce = 0;          // NEBULA_OPT_TOPK_REDUCE: 0 tile-interleaved, 1 per-warp ranges
   int exact_scale = 0;          // NEBULA_OPT_EXACT_SCALE: 1 = cluster-wide INT8/FP8 scale when G > 1 (R28)
   bool onchip_ok = false;
   int onchip_grid = 0;
@@ -818,8 +819,10 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
       zb = obase;
       zc = elems_of(ctx, lo, hi);
     }
+    uint64_t sc = 0;
+    for (int i = lo; i < hi; ++i) sc += (uint64_t)ctx->P * ((ctx->b[i].cn + 2047) / 2048 + 1);
     launch_reduce_topk(L, ctx->codec.topk_values, ctx->P, vec, items, T.count, T.entries, T.tiles, sources_of(ctx, ctx->b[lo]),
-                       ctx->tk.start, obase, zb, zc);
+                       ctx->tk.start, obase, zb, zc, sc, ctx->topk_reduce);
   }
   else
     launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, sources_of(ctx, ctx->b[lo]), obase);
@@ -870,7 +873,7 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
     if (method == M_TOPK) {
       float* zb = ctx->G > 1 ? obase + bk.coff : obase;
       launch_reduce_topk(L, ctx->codec.topk_values, 1, vec, items, T.count, T.entries, T.tiles, src, ctx->tk.start,
-                         obase, zb, bk.cn);
+                         obase, zb, bk.cn, (bk.cn + 2047) / 2048 + 1, ctx->topk_reduce);
     } else {
       launch_reduce_dense(L, method, 1, vec, items, T.count, T.chunks, src, obase);
     }
@@ -1085,6 +1088,11 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
   if (option == NEBULA_OPT_FP16_KERNEL) {
     if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "FP16 kernel option must be 0 or 1");
     ctx->fp16_kernel = (int)value;
+    return NEBULA_OK;
+  }
+  if (option == NEBULA_OPT_TOPK_REDUCE) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "top-k reduce option must be 0 or 1");
+    ctx->topk_reduce = (int)value;
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_SR_SEED) {

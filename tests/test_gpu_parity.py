@@ -31,7 +31,7 @@ def bits(a):
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
                  start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
-                 fp16_kernel=None, sr_seed=0):
+                 fp16_kernel=None, sr_seed=0, topk_reduce=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
@@ -44,6 +44,8 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
         ctx.set_fp16_kernel(fp16_kernel)
     if sr_seed:
         ctx.set_sr_seed(sr_seed)
+    if topk_reduce is not None:
+        ctx.set_option(nb.OPT_TOPK_REDUCE, topk_reduce)
     codec = O.Codec(method=method, topk_values=vt, topk_k=k, topk_density=rho, error_feedback=ef,
                     start_step=start_step, sr_seed=sr_seed)
     total = sum(sizes)
@@ -247,6 +249,15 @@ def test_config1_shape(nb):
 @pytest.mark.parametrize("P", [2, 4])
 def test_topk_parity(nb, vt, rho, P):
     run_loopback(nb, O.TOPK, [200003, 4096, 3], P, vt=vt, rho=rho)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("rho,P", [(0.01, 2), (0.3, 3), (0.001, 8)])
+@pytest.mark.parametrize("per_bucket,misalign", [(False, False), (True, True)])
+def test_topk_reduce_variants(nb, variant, rho, P, per_bucket, misalign):
+    """Both sparse decompress-average kernels (tile-interleaved default, per-warp ranges)."""
+    run_loopback(nb, O.TOPK, [300001, 2048, 4097, 1], P, rho=rho, steps=2, per_bucket=per_bucket,
+                 misalign=misalign, topk_reduce=variant)
 
 
 @pytest.mark.parametrize("kind", ["ties", "zipf-rows", "zeros", "signed-zero", "strided-zeros", "subnormal",
