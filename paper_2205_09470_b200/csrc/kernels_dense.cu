@@ -453,8 +453,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
 // 25 MiB buckets) next to the streamed traffic; if it did not, the cost degrades to the
 // two-pass traffic, never to a wrong result.  Without EF, B re-reads g.
 constexpr int kFusedThreads = 512;
-constexpr int kFusedUnroll = 2;
-constexpr int kFusedLag = 2;
+constexpr int kFusedUnroll = 2;   // (lag 2 is the default LAG template argument of the variants below)
 
 __device__ __forceinline__ void arrive(unsigned* done) {
   __syncthreads();
@@ -1946,14 +1945,12 @@ __global__ void __launch_bounds__(kF16Threads, 1)
 bool launch_fp16_tma(const Launch& L, bool ef, const Item* items, int nitems, uint64_t chunks, const float* g,
                      float* r, const Dests& slots, uint32_t* flags) {
   const size_t smem = sizeof(F16Stage) * kF16NS;
-  const void* f = ef ? (const void*)k_fp16_tma<true> : (const void*)k_fp16_tma<false>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fp16_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_fp16_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  (void)f;
   Mark mk(L, PH_FP16);
   const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)L.num_sms);
   if (ef) k_fp16_tma<true><<<grid, kF16Threads, smem, L.stream>>>(items, nitems, chunks, g, r, slots, flags);

@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(kDenThreads) k_topk_densify_w(const RItem* __r
   int i = -1;
   RItem it{};
   uint64_t it_end = 0;
-  uint32_t wb[P];        // window base entry of each cluster
+  uint32_t wb[P] = {};   // window base entry of each cluster
   uint32_t xw[P];        // this lane's entry (wb + lane): index, 0xFFFFFFFF past the end
   float vw[P];
   const uint8_t* sl[P];
