@@ -244,9 +244,10 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 #define NEBULA_OPT_EXACT_SCALE 5
 /*   NEBULA_OPT_SR_SEED: the 64-bit seed of NEBULA_QSGD's uniforms (default 0); any time. */
 #define NEBULA_OPT_SR_SEED 6
-/*   NEBULA_OPT_TOPK_REDUCE: sparse decompress-average kernel, 0 (default) tile-interleaved
- *   (per-tile run starts found in parallel, CTAs walk 2048-element tiles grid-stride), 1 warps
- *   own contiguous ranges of 512-element sub-tiles.  Same results. */
+/*   NEBULA_OPT_TOPK_REDUCE: sparse decompress-average kernel, 0 tile-interleaved (per-tile run
+ *   starts found in parallel, CTAs walk 2048-element tiles grid-stride), 1 (default) warps own
+ *   contiguous ranges of 512-element sub-tiles (measured 0.30 vs 0.345 ms at BASELINE config 2).
+ *   Same results. */
 #define NEBULA_OPT_TOPK_REDUCE 7
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
@@ -303,8 +304,8 @@ nebula_status nebula_svd_decompress(nebula_svd* h, const void* dev_payload, floa
 nebula_status nebula_svd_check(nebula_svd* h);
 uint64_t nebula_svd_kernel_launches(const nebula_svd* h);
 /* Bit 0: eigensolver of the Gram matrix, 0 (default) cuSOLVER syevd (divide and conquer), 1
- * cuSOLVER syevj (Jacobi, tolerance 1e-14, <= 30 sweeps).  Bit 1: Gram kernel, 0 (default) FP64
- * tensor cores (mma.sync m8n8k4 f64), 1 SIMT fp64 FMA.  All give the same factors to binary16. */
+ * cuSOLVER syevj (Jacobi, tolerance 1e-14, <= 30 sweeps).  Bit 1: Gram kernel, 0 (default) SIMT
+ * fp64 FMA, 1 FP64 tensor cores (mma.sync m8n8k4 f64).  All give the same factors to binary16. */
 nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which);
 nebula_status nebula_svd_destroy(nebula_svd* h);
 const char* nebula_svd_last_error(const nebula_svd* h);

@@ -1251,7 +1251,9 @@ __global__ void __launch_bounds__(kDenThreads) k_topk_densify_w(const RItem* __r
   }
 }
 
-// Tile-interleaved variant (default).  The contiguous per-warp ranges above leave every warp
+// Tile-interleaved variant (NEBULA_OPT_TOPK_REDUCE = 0; measured slower: 0.345 vs 0.30 ms at
+// BASELINE config 2, the extra start-offset kernel and three CTA barriers per tile cost more
+// than the write locality gains).  The contiguous per-warp ranges above leave every warp
 // writing its own far-apart region of the output (~4700 concurrent write streams); here CTAs
 // walk the 2048-element tiles grid-stride, so the active writes form one contiguous window, as
 // in a fill.  A first kernel finds, massively in parallel, where every tile's run starts in
@@ -1484,7 +1486,7 @@ void launch_reduce_topk(const Launch& L, int value_type, int P, bool vec, const 
   (void)zero_begin; (void)zero_count;
   if (!tiles) return;
   Mark mk(L, PH_TOPK_REDUCE);
-  if (variant == 0) {   // tile-interleaved (default)
+  if (variant == 0) {   // tile-interleaved
     k_topk_starts<<<(unsigned)((start_count + 255) / 256), 256, 0, L.stream>>>(items, nitems, P, slots, start_count, start);
     switch (P) {
       case 1: densify_t<1>(L, value_type, vec, items, nitems, tiles, slots, start, out); break;

@@ -114,7 +114,7 @@ struct nebula_ctx {
   int fp16_kernel = 0;          // NEBULA_OPT_FP16_KERNEL: 0 TMA ring, 1 plain streaming
   int step_fusion = 0;          // NEBULA_OPT_STEP_FUSION: 0 fuse INT8 steps where eligible, 1 never
   uint64_t sr_seed = 0;         // NEBULA_OPT_SR_SEED (QSGD uniforms, R32)
-  int topk_reduce = 0;          // NEBULA_OPT_TOPK_REDUCE: 0 tile-interleaved, 1 per-warp ranges
+  int topk_reduce = 1;          // NEBULA_OPT_TOPK_REDUCE: 0 tile-interleaved, 1 per-warp ranges (default)
   int exact_scale = 0;          // NEBULA_OPT_EXACT_SCALE: 1 = cluster-wide INT8/FP8 scale when G > 1 (R28)
   bool onchip_ok = false;
   int onchip_grid = 0;
