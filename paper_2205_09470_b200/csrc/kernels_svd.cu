@@ -54,26 +54,57 @@ __device__ __forceinline__ float bval(const float* A, const Shape& s, int64_t i,
   return s.tall ? A[i * s.n + a] : A[a * s.n + i];
 }
 
-// ---------------------------------------------------------------- K_gram: G += B^T B (upper tiles)
-// grid: (tile pairs ta <= tb, splits over L).  Each CTA loads GK rows of B for both column
-// tiles into shared memory as fp64 (fp32 * fp32 is exact in fp64) and accumulates 4 x 4 fp64
-// per thread; the split partial sums meet in G with fp64 atomics (G zeroed first).
-__global__ void __launch_bounds__(NT) k_gram(const float* __restrict__ A, Shape s, const int2* __restrict__ tiles,
-                                            int64_t rows_per_split, double* __restrict__ G, uint32_t* flags) {
-  __shared__ double sa[GK][T + 1], sb[GK][T + 1];
-  const int2 tp = tiles[blockIdx.x];
-  const int a0 = tp.x * T, b0 = tp.y * T;
-  const int64_t i_begin = (int64_t)blockIdx.y * rows_per_split;
-  const int64_t i_end = min(s.L, i_begin + rows_per_split);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4] = {};
+// Stage rows [i0, i0 + GK) of B's column tiles a0.. and b0.. (64 columns each) into shared
+// memory as fp64.  VEC (A 16-B aligned, n % 4 == 0): one float4 per thread-iteration along the
+// contiguous direction of A (columns of B when tall, rows of B when wide); partial float4s at
+// the matrix edges fall back to scalar loads.  Returns whether a non-finite value was seen.
+template <int NTH>
+__device__ __forceinline__ bool stage_tiles(const float* __restrict__ A, const Shape& s, int a0, int b0, int64_t i0,
+                                            int64_t i_end, double (*sa)[T + 1], double (*sb)[T + 1], bool vec) {
   bool bad = false;
-  for (int64_t i0 = i_begin; i0 < i_end; i0 += GK) {
-    // tile loads: tall -> consecutive threads walk the contiguous column index a;
-    //             wide -> consecutive threads walk the contiguous row index i
+  if (vec) {
 #pragma unroll
-    for (int t = 0; t < GK * T / NT; ++t) {
-      const int idx = threadIdx.x + t * NT;
+    for (int u = 0; u < GK * T / 4 / NTH; ++u) {
+      const int f = threadIdx.x + u * NTH;
+      // tall: 16 float4 per B row (64 columns); wide: 8 float4 per A row (32 B rows)
+      const int ii = s.tall ? f / (T / 4) : (f % (GK / 4)) * 4;
+      const int aa = s.tall ? (f % (T / 4)) * 4 : f / (GK / 4);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int c0 = side ? b0 : a0;
+        double (*dst)[T + 1] = side ? sb : sa;
+        float v[4];
+        if (s.tall) {
+          const int64_t i = i0 + ii;
+          if (i < i_end && c0 + aa + 3 < s.k) {
+            const float4 w = *reinterpret_cast<const float4*>(A + i * s.n + c0 + aa);
+            v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = (i < i_end && c0 + aa + e < s.k) ? A[i * s.n + c0 + aa + e] : 0.0f;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[ii][aa + e] = (double)v[e];
+        } else {
+          const int64_t i = i0 + ii, a = c0 + aa;
+          if (a < s.k && i + 3 < i_end) {
+            const float4 w = *reinterpret_cast<const float4*>(A + (int64_t)a * s.n + i);
+            v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = (a < s.k && i + e < i_end) ? A[(int64_t)a * s.n + i + e] : 0.0f;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[ii + e][aa] = (double)v[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bad |= !isfinite(v[e]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < GK * T / NTH; ++t) {
+      const int idx = threadIdx.x + t * NTH;
       const int ii = s.tall ? idx / T : idx % GK;
       const int aa = s.tall ? idx % T : idx / GK;
       const int64_t i = i0 + ii;
@@ -86,6 +117,26 @@ __global__ void __launch_bounds__(NT) k_gram(const float* __restrict__ A, Shape 
       sa[ii][aa] = (double)va;
       sb[ii][aa] = (double)vb;
     }
+  }
+  return bad;
+}
+
+// ---------------------------------------------------------------- K_gram: G += B^T B (upper tiles)
+// grid: (tile pairs ta <= tb, splits over L).  Each CTA loads GK rows of B for both column
+// tiles into shared memory as fp64 (fp32 * fp32 is exact in fp64) and accumulates 4 x 4 fp64
+// per thread; the split partial sums meet in G with fp64 atomics (G zeroed first).
+__global__ void __launch_bounds__(NT) k_gram(const float* __restrict__ A, Shape s, const int2* __restrict__ tiles,
+                                            int64_t rows_per_split, double* __restrict__ G, uint32_t* flags, bool vec) {
+  __shared__ double sa[GK][T + 1], sb[GK][T + 1];
+  const int2 tp = tiles[blockIdx.x];
+  const int a0 = tp.x * T, b0 = tp.y * T;
+  const int64_t i_begin = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t i_end = min(s.L, i_begin + rows_per_split);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  bool bad = false;
+  for (int64_t i0 = i_begin; i0 < i_end; i0 += GK) {
+    bad |= stage_tiles<NT>(A, s, a0, b0, i0, i_end, sa, sb, vec);
     __syncthreads();
 #pragma unroll 4
     for (int ii = 0; ii < GK; ++ii) {
@@ -123,7 +174,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
 }
 __global__ void __launch_bounds__(GT) k_gram_dmma(const float* __restrict__ A, Shape s, const int2* __restrict__ tiles,
-                                                 int64_t rows_per_split, double* __restrict__ G, uint32_t* flags) {
+                                                 int64_t rows_per_split, double* __restrict__ G, uint32_t* flags, bool vec) {
   __shared__ double sa[GK][T + 1], sb[GK][T + 1];
   const int2 tp = tiles[blockIdx.x];
   const int a0 = tp.x * T, b0 = tp.y * T;
@@ -135,21 +186,7 @@ __global__ void __launch_bounds__(GT) k_gram_dmma(const float* __restrict__ A, S
   double acc[4][4][2] = {};
   bool bad = false;
   for (int64_t i0 = i_begin; i0 < i_end; i0 += GK) {
-#pragma unroll
-    for (int u = 0; u < GK * T / GT; ++u) {
-      const int idx = threadIdx.x + u * GT;
-      const int ii = s.tall ? idx / T : idx % GK;
-      const int aa = s.tall ? idx % T : idx / GK;
-      const int64_t i = i0 + ii;
-      float va = 0.f, vb = 0.f;
-      if (i < i_end) {
-        if (a0 + aa < s.k) va = bval(A, s, i, a0 + aa);
-        if (b0 + aa < s.k) vb = bval(A, s, i, b0 + aa);
-      }
-      bad |= !isfinite(va) || !isfinite(vb);
-      sa[ii][aa] = (double)va;
-      sb[ii][aa] = (double)vb;
-    }
+    bad |= stage_tiles<GT>(A, s, a0, b0, i0, i_end, sa, sb, vec);
     __syncthreads();
 #pragma unroll 2
     for (int kk = 0; kk < GK; kk += 4) {
@@ -489,10 +526,11 @@ nebula_status nebula_svd_compress(nebula_svd* h, const float* dev_A, void* dev_p
   cudaSetDevice(h->device);
   const Shape s = h->s;
   SVD_CK(h, cudaMemsetAsync(h->G, 0, sizeof(double) * s.k * s.k, h->stream));
+  const bool vec = (s.n % 4 == 0) && ((uintptr_t)dev_A % 16 == 0);
   if (h->gram_dmma)
-    k_gram_dmma<<<dim3(h->ntiles, h->splits), GT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
+    k_gram_dmma<<<dim3(h->ntiles, h->splits), GT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags, vec);
   else
-    k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags);
+    k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags, vec);
   ++h->launches;
   SVD_CK(h, cudaGetLastError());
   const cusolverStatus_t es =
