@@ -304,8 +304,8 @@ nebula_status nebula_svd_decompress(nebula_svd* h, const void* dev_payload, floa
 nebula_status nebula_svd_check(nebula_svd* h);
 uint64_t nebula_svd_kernel_launches(const nebula_svd* h);
 /* Bit 0: eigensolver of the Gram matrix, 0 (default) cuSOLVER syevd (divide and conquer), 1
- * cuSOLVER syevj (Jacobi, tolerance 1e-14, <= 30 sweeps).  Bit 1: Gram kernel, 0 (default) SIMT
- * fp64 FMA, 1 FP64 tensor cores (mma.sync m8n8k4 f64).  All give the same factors to binary16. */
+ * cuSOLVER syevj (Jacobi, tolerance 1e-14, <= 30 sweeps).  Bit 1: Gram kernel, 0 (default) FP64
+ * tensor cores (mma.sync m8n8k4 f64), 1 SIMT fp64 FMA.  All give the same factors to binary16. */
 nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which);
 nebula_status nebula_svd_destroy(nebula_svd* h);
 const char* nebula_svd_last_error(const nebula_svd* h);

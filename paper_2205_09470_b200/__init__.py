@@ -419,11 +419,11 @@ class SvdCodec:
     def kernel_launches(self) -> int:
         return self._L.nebula_svd_kernel_launches(self._h)
 
-    def set_eigensolver(self, which: str, gram: str = "simt"):
-        """which: 'syevd' (default, divide and conquer) | 'syevj' (Jacobi); gram: 'simt' (fp64
-        FMA, default) | 'dmma' (FP64 tensor cores)."""
+    def set_eigensolver(self, which: str, gram: str = "dmma"):
+        """which: 'syevd' (default, divide and conquer) | 'syevj' (Jacobi); gram: 'dmma' (FP64
+        tensor cores, default) | 'simt' (fp64 FMA)."""
         self._ck(self._L.nebula_svd_set_eigensolver(self._h, {"syevd": 0, "syevj": 1}[which] +
-                                                    2 * {"simt": 0, "dmma": 1}[gram]))
+                                                    2 * {"dmma": 0, "simt": 1}[gram]))
 
     def destroy(self):
         if getattr(self, "_h", None):

@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(NT) k_gram(const float* __restrict__ A, Shape 
 }
 
 // Same contraction on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64 — tcgen05 has no fp64
-// kind; option, measured 0.84 ms vs 0.76 ms for the SIMT kernel at 8192 x 768: both are bound
-// by the per-element load/convert loop that stages B into shared memory, not by the FMAs): a CTA of 4 warps owns the 64 x 64 tile, each warp a 32 x 32 quarter = 4 x 4 MMA tiles
+// kind; the default: with float4 staging of B the SIMT kernel takes 0.65 ms at 8192 x 768 and
+// this one ~0.2 ms less, per the compress times in DESIGN.md §10): a CTA of 4 warps owns the 64 x 64 tile, each warp a 32 x 32 quarter = 4 x 4 MMA tiles
 // of 8 x 8, 32 fp64 accumulators per thread.  Fragments (PTX m8n8k4 .f64): A row-major 8 x 4:
 // a0 = A[g][t]; B col-major 4 x 8: b0 = B[t][g]; C 8 x 8: c{0,1} = C[g][2t + {0,1}], with
 // g = lane / 4, t = lane % 4.  Here A[m][kk] = B(i0 + kk, a0 + m) and B[kk][n] = B(i0 + kk, b0 + n),
@@ -418,7 +418,7 @@ struct nebula_svd {
   int64_t rows_per_split = 0;
   int lwork = 0;
   int eig = 0;                   // 0: cusolverDnDsyevd (divide & conquer), 1: cusolverDnDsyevj (Jacobi)
-  int gram_dmma = 0;             // 0: SIMT fp64 FMA Gram (0.76 ms at 8192 x 768), 1: FP64 tensor cores (DMMA, 0.84 ms)
+  int gram_simt = 0;             // 0: FP64 tensor cores (DMMA, default), 1: SIMT fp64 FMA
   syevjInfo_t jinfo = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -527,7 +527,7 @@ nebula_status nebula_svd_compress(nebula_svd* h, const float* dev_A, void* dev_p
   const Shape s = h->s;
   SVD_CK(h, cudaMemsetAsync(h->G, 0, sizeof(double) * s.k * s.k, h->stream));
   const bool vec = (s.n % 4 == 0) && ((uintptr_t)dev_A % 16 == 0);
-  if (h->gram_dmma)
+  if (!h->gram_simt)
     k_gram_dmma<<<dim3(h->ntiles, h->splits), GT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags, vec);
   else
     k_gram<<<dim3(h->ntiles, h->splits), NT, 0, h->stream>>>(dev_A, s, h->tiles, h->rows_per_split, h->G, h->flags, vec);
@@ -599,7 +599,7 @@ nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which) {
   if (!h) return NEBULA_ERR_INVALID_ARG;
   if (which < 0 || which > 3) return svd_fail(h, NEBULA_ERR_INVALID_ARG, "eigensolver option must be in [0, 3]");
   h->eig = which & 1;
-  h->gram_dmma = (which >> 1) & 1;
+  h->gram_simt = (which >> 1) & 1;
   return NEBULA_OK;
 }
 

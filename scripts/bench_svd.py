@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--eig", default="syevd", choices=["syevd", "syevj"])
-    ap.add_argument("--gram", default="simt", choices=["simt", "dmma"])
+    ap.add_argument("--gram", default="dmma", choices=["dmma", "simt"])
     args = ap.parse_args()
     import torch
     import paper_2205_09470_b200 as nb
