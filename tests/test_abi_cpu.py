@@ -97,3 +97,25 @@ def test_topology_for_rank():
     assert topology_for_rank(3, 4, 1) == (4, 3, 0)
     with pytest.raises(ValueError):
         topology_for_rank(0, 6, 4)
+
+
+@pytest.mark.parametrize("kwargs,needle", [
+    (dict(method=5), "method"),                 # 5 is the SVD payload id, not a bucket codec
+    (dict(method=7), "method"),
+])
+def test_validation_rejects_unknown_codec_ids(lib, kwargs, needle):
+    with pytest.raises(nb.NebulaError) as e:
+        nb.SyncContext([1024], **kwargs)
+    assert e.value.code == "INVALID_ARG" and needle in str(e.value)
+
+
+@pytest.mark.parametrize("m,n,r,needle", [
+    (0, 5, 1, "m and n"), (5, 0, 1, "m and n"), (8, 4, 0, "r must"), (8, 4, 5, "r must"),
+    (20000, 20000, 4, "min(m, n)"),
+])
+def test_svd_validation_rejects_before_cuda(lib, m, n, r, needle):
+    """nebula_svd_init (NEXT-1) validates the shape and rank before touching the device."""
+    with pytest.raises(nb.NebulaError) as e:
+        nb.SvdCodec(m, n, r)
+    assert e.value.code == "INVALID_ARG" and needle in str(e.value)
+
