@@ -81,7 +81,8 @@ typedef enum {
  * q = floor(x) + [u < x - floor(x)] clamped to [-127, 127], u the counter-based SplitMix64
  * uniform (2^-24 grid) of (seed = NEBULA_OPT_SR_SEED, step, cluster, bucket, shard, element):
  * base = sm(seed ^ sm(step ^ sm(((cluster * 65536 + shard) << 32) | bucket))),
- * u_e = (sm(base + e * 0x9E3779B97F4A7C15) >> 40) * 2^-24.  E[D] = p (unbiased).
+ * h_j = sm(base + j * 0x9E3779B97F4A7C15), u_{2j} = (h_j >> 40) * 2^-24,
+ * u_{2j+1} = ((h_j >> 16) & 0xFFFFFF) * 2^-24.  E[D] = p (unbiased).
  * (5 is the FP16(SVD) payload id, not a bucket method.) */
 typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4,
                NEBULA_QSGD = 6 } nebula_method;

@@ -249,15 +249,18 @@ def splitmix64(z):
 
 
 def qsgd_uniforms(n: int, seed: int, step: int, cluster: int, bucket: int, shard: int = 0) -> np.ndarray:
-    """R32 counter-based uniforms in [0, 1) on the 2^-24 grid, one per element e:
+    """R32 counter-based uniforms in [0, 1) on the 2^-24 grid, two per 64-bit output:
     base = sm(seed ^ sm(step ^ sm(((cluster * 65536 + shard) << 32) | bucket))),
-    u_e = (sm(base + e * gamma) >> 40) * 2^-24   (sm = splitmix64; e * gamma wraps mod 2^64)."""
+    h_j = sm(base + j * gamma)  (sm = splitmix64; j * gamma wraps mod 2^64),
+    u_{2j} = (h_j >> 40) * 2^-24,  u_{2j+1} = ((h_j >> 16) & (2^24 - 1)) * 2^-24."""
     k = (((cluster * 65536 + shard) << 32) | bucket) & _M64
     base = splitmix64(seed ^ splitmix64(step ^ splitmix64(k)))
+    e = np.arange(n, dtype=np.uint64)
     with np.errstate(over="ignore"):
-        z = np.uint64(base) + np.arange(n, dtype=np.uint64) * np.uint64(_GAMMA)
+        z = np.uint64(base) + (e >> np.uint64(1)) * np.uint64(_GAMMA)
         h = splitmix64(z)
-    return ((h >> np.uint64(40)).astype(np.float64) * 2.0 ** -24).astype(F32)
+    bits = np.where((e & np.uint64(1)) == 0, h >> np.uint64(40), (h >> np.uint64(16)) & np.uint64(0xFFFFFF))
+    return (bits.astype(np.float64) * 2.0 ** -24).astype(F32)
 
 
 def qsgd_quantize(p: np.ndarray, s: np.float32, u: np.ndarray) -> np.ndarray:

@@ -267,9 +267,9 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
           d0 = __fmul_rn(fp8_val(wv), s); d1 = __fmul_rn(fp8_val(wv >> 8), s);
           d2 = __fmul_rn(fp8_val(wv >> 16), s); d3 = __fmul_rn(fp8_val(wv >> 24), s);
         } else if constexpr (SR) {
-          const uint64_t e0 = 4 * q;
-          int q0 = qsgd_q(p.x, s, qsgd_u(srb, e0)), q1 = qsgd_q(p.y, s, qsgd_u(srb, e0 + 1)),
-              q2 = qsgd_q(p.z, s, qsgd_u(srb, e0 + 2)), q3 = qsgd_q(p.w, s, qsgd_u(srb, e0 + 3));
+          const uint64_t h0 = qsgd_h(srb, 2 * q), h1 = qsgd_h(srb, 2 * q + 1);   // elements 4q .. 4q+3
+          int q0 = qsgd_q(p.x, s, qsgd_hi(h0)), q1 = qsgd_q(p.y, s, qsgd_lo(h0)),
+              q2 = qsgd_q(p.z, s, qsgd_hi(h1)), q3 = qsgd_q(p.w, s, qsgd_lo(h1));
           wv = pack_i8x4(q0, q1, q2, q3);
           d0 = __fmul_rn((float)q0, s); d1 = __fmul_rn((float)q1, s); d2 = __fmul_rn((float)q2, s); d3 = __fmul_rn((float)q3, s);
         } else {

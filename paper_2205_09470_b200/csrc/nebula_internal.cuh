@@ -188,8 +188,9 @@ __device__ __forceinline__ float fp8_val(uint32_t byte) {
 }
 
 // QSGD (NEXT-4, R32): counter-based uniforms.  splitmix64(z) = mix(z + gamma) (Steele, Lea &
-// Flood 2014); per (seed, step, cluster, bucket, shard) a base state, per element e the output
-// splitmix64(base + e * gamma) >> 40, scaled by 2^-24 (exact in binary32).
+// Flood 2014); per (seed, step, cluster, bucket, shard) a base state; output j =
+// splitmix64(base + j * gamma) feeds elements 2j (bits 63..40) and 2j + 1 (bits 39..16), each
+// scaled by 2^-24 (exact in binary32).
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -202,8 +203,16 @@ __host__ __device__ inline uint64_t qsgd_key(uint32_t cluster, uint32_t shard, u
 __device__ __forceinline__ uint64_t qsgd_base(uint64_t seed, uint64_t step, uint64_t key) {
   return splitmix64(seed ^ splitmix64(step ^ splitmix64(key)));
 }
-__device__ __forceinline__ float qsgd_u(uint64_t base, uint64_t e) {
-  return (float)(uint32_t)(splitmix64(base + e * 0x9E3779B97F4A7C15ull) >> 40) * 5.9604644775390625e-8f;  // 2^-24
+__device__ __forceinline__ uint64_t qsgd_h(uint64_t base, uint64_t j) {
+  return splitmix64(base + j * 0x9E3779B97F4A7C15ull);
+}
+__device__ __forceinline__ float qsgd_hi(uint64_t h) { return (float)(uint32_t)(h >> 40) * 5.9604644775390625e-8f; }
+__device__ __forceinline__ float qsgd_lo(uint64_t h) {
+  return (float)(uint32_t)((h >> 16) & 0xFFFFFFu) * 5.9604644775390625e-8f;
+}
+__device__ __forceinline__ float qsgd_u(uint64_t base, uint64_t e) {   // one element (tails)
+  const uint64_t h = qsgd_h(base, e >> 1);
+  return (e & 1) ? qsgd_lo(h) : qsgd_hi(h);
 }
 // q = floor(x) + [u < x - floor(x)], x = fl(p / s) (IEEE division), clamped to [-127, 127]
 __device__ __forceinline__ int qsgd_q(float p, float s, float u) {

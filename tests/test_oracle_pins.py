@@ -548,6 +548,15 @@ def test_qsgd_uniforms_are_uniform_and_distinct():
     assert chi2 < 120                                    # 63 dof: p ~ 1e-5
     for other in [(8, 3, 1, 2), (7, 4, 1, 2), (7, 3, 0, 2), (7, 3, 1, 3)]:
         assert not np.array_equal(u[:64], O.qsgd_uniforms(64, *other).astype(np.float64))
+    # the two halves of one 64-bit output (even / odd elements) are uncorrelated
+    ev, od = u[0::2] - 0.5, u[1::2] - 0.5
+    assert abs(float(np.mean(ev * od))) < 6 * (1 / 12) / math.sqrt(ev.size)
+    # the even-element stream is the SplitMix64 stream itself (top 24 bits of each output)
+    k = ((1 * 65536 + 0) << 32) | 2
+    base = O.splitmix64(7 ^ O.splitmix64(3 ^ O.splitmix64(k)))
+    for j in range(4):
+        h = O.splitmix64((base + j * 0x9E3779B97F4A7C15) % 2 ** 64)
+        assert u[2 * j] == (h >> 40) * 2.0 ** -24 and u[2 * j + 1] == ((h >> 16) & 0xFFFFFF) * 2.0 ** -24
 
 
 def test_qsgd_rounds_to_neighbours_and_is_unbiased():
