@@ -65,10 +65,11 @@ void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int
 void launch_qsgd_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags,
                        const SrArgs& sr);
-// FP8 single HBM pass: the warp-specialised TMA kernel with the E4M3 quantiser (16-B aligned
-// calls; cooperative, one CTA per SM; done_words >= nitems).
-void launch_fp8_onchip(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
-                       const Dests& slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words);
+// FP8 (kind 1) / QSGD (kind 2) single HBM pass: the warp-specialised TMA kernel with that
+// quantiser (16-B aligned calls; cooperative, one CTA per SM; done_words >= nitems).
+void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, int nitems, const float* g, float* r,
+                        const Dests& slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words,
+                        const SrArgs& sr);
 // INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
 // p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
 // when a cooperative launch is not possible; the caller then uses the two-pass kernels.
@@ -92,7 +93,7 @@ struct Peers {
 void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
                       const Dests& dst, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
-                      uint64_t seq, int config, bool f8 = false);
+                      uint64_t seq, int config, int kind, const SrArgs& sr);   // kind 0 INT8, 1 FP8, 2 QSGD
 
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.

@@ -1269,6 +1269,7 @@ struct StepArgs {
   unsigned long long seq;
   int b0;                            // global index of the call's first bucket (flag index)
   int PL;                            // compress items per bucket (clusters computed on this GPU)
+  SrArgs sr;                         // QSGD generator state (SR kernels only)
 };
 
 // Reduce role, TMA variant (LOOPBACK: every payload is local): warp 0 of the group is the
@@ -1544,7 +1545,7 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
 // CM: reduce role — 0 none (compress only), 1 TMA variant (LOOPBACK), 2 register loads (P2P pull)
 // F8: the same schedules for the FP8 E4M3 codec (NEXT-4, R27) — only the B warps' scale /
 // quantise / dequantise and the C warps' byte decode differ.
-template <bool EF, int AW, int BW, int CW, int CM, bool F8 = false>
+template <bool EF, int AW, int BW, int CW, int CM, bool F8 = false, bool SR = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
@@ -1714,11 +1715,15 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           const float sc = F8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
           s_scale[0] = sc;
           s_scale[1] = int8_inv(sc);
-          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 ? M_FP8 : M_INT8, (uint32_t)it.n, sc, 0u);
+          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, sc, 0u);
         }
       }
       named_sync(2, kB);
       const float s = s_scale[0], sinv = s_scale[1];
+      uint64_t srb = 0;
+      if constexpr (SR)
+        srb = qsgd_base(sa.sr.seed, sa.sr.step,
+                        qsgd_key(sa.sr.cluster0 + it.sidx / sa.sr.num_buckets, sa.sr.shard, it.sidx % sa.sr.num_buckets));
       const bool ok = s != 0.0f;   // scale is never 0 (R4) except for the non-finite marker
       const float* g = gbase + it.g_off;
       float* r = rbase + it.r_off;
@@ -1741,6 +1746,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
               w = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
               d0 = __fmul_rn(fp8_val(w), s); d1 = __fmul_rn(fp8_val(w >> 8), s);
               d2 = __fmul_rn(fp8_val(w >> 16), s); d3 = __fmul_rn(fp8_val(w >> 24), s);
+            } else if constexpr (SR) {
+              const uint64_t h0 = qsgd_h(srb, 2 * (q0 + j)), h1 = qsgd_h(srb, 2 * (q0 + j) + 1);
+              const int a0 = qsgd_q(p.x, s, qsgd_hi(h0)), a1 = qsgd_q(p.y, s, qsgd_lo(h0)),
+                        a2 = qsgd_q(p.z, s, qsgd_hi(h1)), a3 = qsgd_q(p.w, s, qsgd_lo(h1));
+              w = pack_i8x4(a0, a1, a2, a3);
+              d0 = __fmul_rn((float)a0, s); d1 = __fmul_rn((float)a1, s);
+              d2 = __fmul_rn((float)a2, s); d3 = __fmul_rn((float)a3, s);
             } else {
               const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
                         a3 = int8_qi(p.w, s, sinv);
@@ -1769,6 +1781,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           if constexpr (F8) {
             ce = fp8x2_of(p, 0.0f, s) & 0xFF;
             de = __fmul_rn(fp8_val(ce), s);
+          } else if constexpr (SR) {
+            const int qe = qsgd_q(p, s, qsgd_u(srb, e));
+            ce = (uint32_t)qe & 0xFF;
+            de = __fmul_rn((float)qe, s);
           } else {
             const int qe = int8_qi(p, s, sinv);
             ce = (uint32_t)qe & 0xFF;
@@ -1999,21 +2015,28 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
   return true;
 }
 
-void launch_fp8_onchip(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
-                       const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words) {
+void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, int nitems, const float* g, float* r,
+                        const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words,
+                        const SrArgs& srargs) {
   Dests slots = slots_in;
-  Mark mk(L, PH_FP8_QUANT);
+  Mark mk(L, kind == 2 ? PH_QSGD_QUANT : PH_FP8_QUANT);
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;
   StepArgs sa{};
+  sa.sr = srargs;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&slots, (void*)&scratch,
                   (void*)&flags, (void*)&done, (void*)&sa};
-  const void* f = ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, true> : (const void*)k_int8_ws<false, 8, 23, 0, 0, true>;
+  const void* f = kind == 2 ? (ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, false, true>
+                                  : (const void*)k_int8_ws<false, 8, 23, 0, 0, false, true>)
+                            : (ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, true>
+                                  : (const void*)k_int8_ws<false, 8, 23, 0, 0, true>);
   const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_int8_ws<true, 8, 23, 0, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_int8_ws<false, 8, 23, 0, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   int sms = 0, dev = 0;
@@ -2129,8 +2152,10 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
 // warp-specialised kernel with reduce warps).  bar_words: 2 * nitems words (done, bdone).
 // Warp splits (A, B, C) of the fused step; config 0 is the default, the rest a tuning sweep.
 template <bool EF>
-static const void* step_kernel(int config, bool f8) {
-  if (f8) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, true>;
+static const void* step_kernel(int config, int kind) {
+  if (kind == 1) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, true>;
+  if (kind == 2)
+    return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, false, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, false, true>;
   switch (config) {
     // LOOPBACK (TMA reduce role)
     case 1: return (const void*)k_int8_ws<EF, 5, 20, 6, 1>;
@@ -2151,7 +2176,7 @@ static const void* step_kernel(int config, bool f8) {
 void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
                       const Dests& dst_in, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
-                      uint64_t seq, int config, bool f8) {
+                      uint64_t seq, int config, int kind, const SrArgs& srargs) {
   Mark mk(L, PH_INT8_STEP);
   cudaMemsetAsync(bar_words, 0, sizeof(unsigned) * 2 * (size_t)nitems, L.stream);
   Dests dst = dst_in;
@@ -2166,17 +2191,18 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
   sa.seq = (unsigned long long)seq;
   sa.b0 = b0;
   sa.PL = PL;
+  sa.sr = srargs;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&scratch,
                   (void*)&flags, (void*)&done, (void*)&sa};
-  if (f8 && config != 4) config = 0;   // FP8: the two default splits only
-  const void* f = ef ? step_kernel<true>(config, f8) : step_kernel<false>(config, f8);
+  if (kind != 0 && config != 4) config = 0;   // FP8 / QSGD: the two default splits only
+  const void* f = ef ? step_kernel<true>(config, kind) : step_kernel<false>(config, kind);
   // the TMA reduce role (LOOPBACK configs) adds its ring; the register-load role uses static smem
   const bool tma_c = config <= 3 || config > 10;
   const size_t smem = sizeof(WsStageA) * kWsNA + sizeof(WsStageB) * kWsNB + (tma_c ? (size_t)kWsNC * kWsCStage : 0);
-  static bool attr[2][2][11] = {};
-  if (!attr[f8][ef][config < 0 || config > 10 ? 0 : config]) {
+  static bool attr[3][2][11] = {};
+  if (!attr[kind][ef][config < 0 || config > 10 ? 0 : config]) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[f8][ef][config < 0 || config > 10 ? 0 : config] = true;
+    attr[kind][ef][config < 0 || config > 10 ? 0 : config] = true;
   }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);

@@ -572,7 +572,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       s = topk_setup(ctx);
       if (s != NEBULA_OK) return bail(s);
     }
-    if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8) {
+    if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8 || codec->method == NEBULA_QSGD) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
       if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (2 * ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
         ctx->err = "barrier allocation failed";
@@ -713,9 +713,15 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
             CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
         }
       }
+      const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
+      if (ctx->onchip_ok && vec && !(ctx->exact_scale && ctx->G > 1) &&
+          (ctx->int8_kernel >= 2 ||
+           (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)))) {
+        launch_ws_compress(L, ef, 2, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar, sr);
+        break;
+      }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
       if (ctx->exact_scale && ctx->G > 1) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
-      const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
       launch_qsgd_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, sr);
       break;
     }
@@ -735,7 +741,8 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       if (ctx->onchip_ok && vec && !xscale &&
           (ctx->int8_kernel >= 2 ||
            (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)))) {
-        launch_fp8_onchip(L, ef, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar);
+        launch_ws_compress(L, ef, 1, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar,
+                           SrArgs{});
         break;
       }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
@@ -891,8 +898,8 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
                          uint64_t step) {
   const int m = method_at(ctx, step);
-  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8) || ctx->G != 1 || !ctx->onchip_ok) return false;
-  if (m == M_FP8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8-only
+  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD) || ctx->G != 1 || !ctx->onchip_ok) return false;
+  if (m != M_INT8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8-only
   // LOOPBACK, or P2P pull (the reduce warps load the peers' payloads); with P2P push the
   // compress kernel's NVLink stores are cheaper outside the fused kernel (fewer quantise warps)
   if (!(ctx->loopback || ctx->P == 1 || ctx->xmode == 3)) return false;
@@ -908,7 +915,7 @@ static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, 
 }
 
 static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* dev_grad,
-                                     float* dev_out, int method) {
+                                     float* dev_out, int method, uint64_t step) {
   const bool ef = ctx->codec.error_feedback != 0;
   const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
   const Table& T = ctx->ctab[lay][t];
@@ -933,7 +940,9 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, ctx->b[lo]),
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
                    sources_of(ctx, ctx->b[lo]), dev_out, pe, ctx->d_arrive, ctx->b[lo].seq,
-                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0), method == M_FP8);
+                   ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0),
+                   method == M_FP8 ? 1 : (method == M_QSGD ? 2 : 0),
+                   SrArgs{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()});
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
     ctx->b[i].state = ST_IDLE;
@@ -948,7 +957,7 @@ nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad
     if (range_of(ctx, bucket, &lo, &hi) && hi > lo && dev_grad && dev_out &&
         step_fusable(ctx, lo, hi, bucket, dev_grad, dev_out, step)) {
       DevGuard dg(ctx->device);
-      return int8_step_fused(ctx, lo, hi, bucket, dev_grad, dev_out, method_at(ctx, step));
+      return int8_step_fused(ctx, lo, hi, bucket, dev_grad, dev_out, method_at(ctx, step), step);
     }
   }
   nebula_status s = nebula_compress(ctx, bucket, dev_grad, step);
@@ -1075,7 +1084,8 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
     if (value < 0 || value > 12) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 12]");
-    if (value >= 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8) && !ctx->onchip_ok)
+    if (value >= 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8 ||
+                       ctx->codec.method == NEBULA_QSGD) && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;
     return NEBULA_OK;

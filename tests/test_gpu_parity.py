@@ -185,6 +185,15 @@ def test_qsgd_parity(nb, P, sizes, seed):
     assert run_loopback(nb, O.QSGD, sizes, P, steps=2, sr_seed=seed) > 0
 
 
+@pytest.mark.parametrize("kern", ["two-pass", "fused-ws", "fused-ws-staged"])
+@pytest.mark.parametrize("sizes", [[5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_qsgd_kernels(nb, kern, sizes, P):
+    """QSGD through the two-pass kernels, the single-pass warp-specialised compress kernel and
+    the fused compress + exchange + average step (same SplitMix64 stream in every schedule)."""
+    assert run_loopback(nb, O.QSGD, sizes, P, steps=2, sr_seed=3, int8_kernel=kern) > 0
+
+
 @pytest.mark.parametrize("kind", ["ties", "half-ties", "int-ties", "zeros", "tiny-max", "subnormal"])
 def test_qsgd_edge_values(nb, kind):
     run_loopback(nb, O.QSGD, [5000, 17], 2, kind=kind, steps=2, sr_seed=11)
