@@ -47,7 +47,8 @@ def main():
     # (method, top-k values, INT8 kernel, exact cluster-wide scale (NEXT-3, only meaningful for G > 1))
     cases = [(O.INT8, 0, "two-pass", False), (O.INT8, 0, "onchip", False), (O.INT8, 0, "fused-ws", False),
              (O.FP16, 0, None, False), (O.IDENTITY, 0, None, False), (O.FP8, 0, None, False), (O.QSGD, 0, None, False),
-             (O.TOPK, O.VAL_F32, None, False), (O.TOPK, O.VAL_I8, None, False), (O.TOPK, O.VAL_F16, None, False)]
+             (O.TOPK, O.VAL_F32, None, False), (O.TOPK, O.VAL_I8, None, False), (O.TOPK, O.VAL_F16, None, False),
+             (O.FP8, 0, "fused-ws", False), (O.QSGD, 0, "fused-ws", False)]   # fused step over P2P (G = 1)
     if G > 1:
         cases += [(O.INT8, 0, None, True), (O.FP8, 0, None, True)]
     modes_seen = set()
