@@ -2154,8 +2154,11 @@ void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, i
 template <bool EF>
 static const void* step_kernel(int config, int kind) {
   if (kind == 1) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, true>;
-  if (kind == 2)
-    return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, false, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, false, true>;
+  if (kind == 2) {   // QSGD: the quantise warps are instruction-bound, config 1 gives them more warps
+    if (config == 4) return (const void*)k_int8_ws<EF, 4, 16, 11, 2, false, true>;
+    if (config == 1) return (const void*)k_int8_ws<EF, 5, 22, 4, 1, false, true>;
+    return (const void*)k_int8_ws<EF, 8, 19, 4, 1, false, true>;
+  }
   switch (config) {
     // LOOPBACK (TMA reduce role)
     case 1: return (const void*)k_int8_ws<EF, 5, 20, 6, 1>;
@@ -2194,7 +2197,7 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
   sa.sr = srargs;
   void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&scratch,
                   (void*)&flags, (void*)&done, (void*)&sa};
-  if (kind != 0 && config != 4) config = 0;   // FP8 / QSGD: the two default splits only
+  if (kind != 0 && config != 4 && !(kind == 2 && config == 1)) config = 0;   // FP8 / QSGD: few splits
   const void* f = ef ? step_kernel<true>(config, kind) : step_kernel<false>(config, kind);
   // the TMA reduce role (LOOPBACK configs) adds its ring; the register-load role uses static smem
   const bool tma_c = config <= 3 || config > 10;

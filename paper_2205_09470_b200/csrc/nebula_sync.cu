@@ -899,7 +899,7 @@ static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, 
                          uint64_t step) {
   const int m = method_at(ctx, step);
   if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD) || ctx->G != 1 || !ctx->onchip_ok) return false;
-  if (m != M_INT8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8-only
+  if (m == M_FP8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8 / QSGD only
   // LOOPBACK, or P2P pull (the reduce warps load the peers' payloads); with P2P push the
   // compress kernel's NVLink stores are cheaper outside the fused kernel (fewer quantise warps)
   if (!(ctx->loopback || ctx->P == 1 || ctx->xmode == 3)) return false;
