@@ -475,10 +475,8 @@ def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):
     """Minimum HBM bytes of one step on one GPU."""
     e = 4 if ef else 0
     clusters_here = P if world == 1 else 1
-    if method in (2, 4):
+    if method in (2, 4, 6):   # single pass (warp-specialised kernel / fused step) for INT8, FP8, QSGD
         comp = (4 + e + e + 1) * n
-    elif method == 6:   # two passes: max-abs, then stochastic rounding
-        comp = (4 + e) * n + (4 + e + e + 1) * n
     elif method == 1:
         comp = (4 + e + e + 2) * n
     elif method == 0:
