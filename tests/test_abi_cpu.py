@@ -119,3 +119,19 @@ def test_svd_validation_rejects_before_cuda(lib, m, n, r, needle):
         nb.SvdCodec(m, n, r)
     assert e.value.code == "INVALID_ARG" and needle in str(e.value)
 
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/nebula_sync.h is a C ABI: it compiles as C99 (no torch / C++ types) and as C++."""
+    import shutil
+    import subprocess
+    src = tmp_path / "t.c"
+    src.write_text('#include "nebula_sync.h"\nint main(void) { nebula_codec c; nebula_topology t; (void)c; (void)t;\n'
+                   '  return nebula_abi_version() == 0; }\n')
+    inc = str(nb.HEADER).rsplit("/", 1)[0]
+    for cc, std in (("gcc", "-std=c99"), ("g++", "-std=c++11")):
+        if not shutil.which(cc):
+            pytest.skip(f"{cc} not available")
+        r = subprocess.run([cc, std, "-Wall", "-Wextra", "-Werror", "-fsyntax-only", f"-I{inc}", "-x",
+                            "c" if cc == "gcc" else "c++", str(src)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
