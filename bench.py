@@ -59,11 +59,7 @@ def parse():
     ap.add_argument("--no-step-fusion", action="store_true",
                     help="run compress / exchange / reduce as separate launches (NEBULA_OPT_STEP_FUSION=1)")
     ap.add_argument("--step-config", type=int, default=None, help="fused-step warp split 0..10 (tuning)")
-    ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "onchip", "fused-recompute",
-                                                              "fused-park-lag1", "fused-recompute-lag1",
-                                                              "fused-split", "fused-smem", "fused-256x2",
-                                                              "fused-256x4", "fused-1024x2", "fused-tma",
-                                                              "fused-ws"])
+    ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "single-pass", "fused-ws"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -16,10 +16,12 @@
  *                                                                    PAPER.md:95 data parallelism across clusters
  *     out    = fl(tree_sum_c D(payload_c) / P)                       R16 (fixed pairwise tree over cluster ids)
  *
- *   With G > 1 (hierarchical): the cluster gradient is the fp32 mean of its G GPUs
- *   (intra-cluster ReduceScatter), GPU l codes shard l (n/G elements) with its own residual,
- *   exchanges it with the P-1 peers of the same local rank, and the averaged shards are
- *   all-gathered inside the cluster (R20).
+ *   With G > 1 (hierarchical): the cluster gradient is the fp32 mean of its G GPUs, summed in
+ *   local-rank order then divided by G (R20: an intra-cluster reduce-scatter over NVLink peer
+ *   memory; NCCL ReduceScatter(avg), whose order is NCCL's, only when the peers cannot be
+ *   mapped), GPU l codes shard l (n/G elements) with its own residual, exchanges it with the
+ *   P-1 peers of the same local rank, and the averaged shards are all-gathered inside the
+ *   cluster (R20).
  *
  * Payload body (R18): 16-byte preamble {u32 method, u32 count (n or k), f32 scale (1.0 if
  * unused), u32 aux (TOPK value type, else 0)}, then sections zero-padded to 16 bytes:
@@ -87,7 +89,18 @@ typedef enum {
 typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4,
                NEBULA_QSGD = 6 } nebula_method;
 typedef enum { NEBULA_VAL_F32 = 0, NEBULA_VAL_F16 = 1, NEBULA_VAL_I8 = 2 } nebula_value_type;
-typedef enum { NEBULA_TRANSPORT_NCCL = 0, NEBULA_TRANSPORT_LOOPBACK = 1 } nebula_transport;
+/* Transports.  NCCL: one process per GPU (torchrun); peers' buffers are mapped with CUDA IPC
+ * when every rank can reach every peer (NVLink), else NCCL collectives move the bytes.
+ * LOOPBACK: one context simulates all P clusters (G = 1) on its device.  SELF: one context per
+ * (cluster, GPU) inside ONE process, all created with the same 128-byte group id in
+ * nccl_unique_id (any bytes; the group is these contexts) — the contexts reach each other's
+ * buffers directly (same device, or peer-accessible devices), so the P2P exchange, the flag
+ * protocol and the intra-cluster hop run exactly as across processes.  SELF rules: the first
+ * stage call needs every member to exist (else NEBULA_ERR_STATE); members run on their own
+ * streams and the caller enqueues each stage for every member before waiting on any (a
+ * member's exchange waits for its peers' compress); nebula_step runs the staged kernels;
+ * destroy every member only after synchronising all of them. */
+typedef enum { NEBULA_TRANSPORT_NCCL = 0, NEBULA_TRANSPORT_LOOPBACK = 1, NEBULA_TRANSPORT_SELF = 2 } nebula_transport;
 
 /* Codec (SPEC.md:111-122 CodecMethod / CodecSchedule, extended with TOPK and error feedback). */
 typedef struct {
@@ -104,11 +117,13 @@ typedef struct {
 typedef struct {
   int32_t num_clusters;     /* P, 1..NEBULA_MAX_CLUSTERS */
   int32_t cluster_id;       /* 0..P-1 (ignored for LOOPBACK: this device hosts all P) */
-  int32_t gpus_per_cluster; /* G >= 1; G > 1 => hierarchical (NCCL only; every numel % G == 0) */
+  int32_t gpus_per_cluster; /* G >= 1; G > 1 => hierarchical (NCCL or SELF; every numel % G == 0;
+                               the P2P intra-cluster hop needs G <= 8) */
   int32_t local_rank;       /* 0..G-1 */
   int32_t transport;        /* nebula_transport */
   int32_t device;           /* CUDA device ordinal the context lives on */
-  const void* nccl_unique_id; /* NEBULA_UNIQUE_ID_BYTES, identical on all P*G ranks; NULL for LOOPBACK */
+  const void* nccl_unique_id; /* NEBULA_UNIQUE_ID_BYTES, identical on all P*G ranks (SELF: the group
+                                 id); NULL for LOOPBACK */
 } nebula_topology;
 
 /* Integer order statistics of one top-k selection (R25 "ranks"). */
@@ -143,7 +158,10 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
 
 nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream);
 
-/* Stage 1 — EF-accumulate + compress + pack (+ the G>1 intra-cluster ReduceScatter).
+/* Stage 1 — EF-accumulate + compress + pack (+ the G>1 intra-cluster reduce-scatter).
+ * NEBULA_ERR_STATE if a bucket of the call is not idle (compress twice without the other
+ * stages would apply the residual twice) or, for ALL, the buckets are at different step
+ * counts (a mix of per-bucket and ALL calls); nothing is enqueued then.
  * dev_grad: fp32 gradient of the bucket (or of all buckets, back to back, for
  * NEBULA_ALL_BUCKETS).  LOOPBACK: P stacked copies, cluster-major: [P][bucket elems]
  * (for ALL: [P][sum of all bucket elems]).  16-byte alignment enables the vector path;
@@ -155,7 +173,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
 nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket);
 
 /* Stage 3 — decode all P payload slots, tree-sum, divide by P, write dev_out (fp32, the
- * bucket's elements; ALL: back to back) (+ the G>1 intra-cluster AllGather).  dev_out may
+ * bucket's elements; ALL: back to back) (+ the G>1 intra-cluster all-gather).  dev_out may
  * alias dev_grad (non-LOOPBACK) . */
 nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out);
 
@@ -165,12 +183,13 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
  * activation compression ... INT8 quantization was used for back propagation gradient
  * compression", across the Scenario-II boundary PAPER.md:259) — compress with error_feedback
  * 0, exchange, then decompress the peer's slot.  Allowed after exchange (any slot) or after
- * compress (own slot; every slot for LOOPBACK).  Does not change the bucket's state. */
+ * compress (own slot; every slot for LOOPBACK).  Does not change the bucket's state.  With
+ * G > 1 the shards are gathered with NCCL (NEBULA_ERR_UNSUPPORTED on SELF). */
 nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, float* dev_out);
 
 /* All three stages.  Same results, bit for bit, as compress + exchange + decompress_reduce.
- * For INT8 with 16-B aligned pointers, buckets averaging >= 1M elements, G = 1 and a LOOPBACK
- * or P2P pull exchange, the three stages run as ONE cooperative kernel
+ * For INT8 / FP8 / QSGD with 16-B aligned pointers, buckets averaging >= 1M elements, G = 1 and
+ * a LOOPBACK or (NCCL-transport) P2P pull exchange, the three stages run as ONE cooperative kernel
  * (NEBULA_OPT_STEP_FUSION): reduce warps average bucket b — pulling the peers' payloads over
  * NVLink once their system-scope arrival flags say they are complete — while the compress
  * warps of the same kernel stream bucket b+1.  A peer that never arrives sets the peer-timeout
@@ -209,14 +228,12 @@ nebula_status nebula_topk_stats(nebula_ctx* ctx, int32_t bucket, int32_t cluster
 uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 
 /* Tuning knobs (results are bit-identical whichever kernel runs).
- *   NEBULA_OPT_INT8_KERNEL: 0 auto (default), 1 two-pass streaming (max-abs pass + quantise
- *   pass, 21 B/elem of HBM traffic), 2..5 fused single pass (cooperative persistent grid, a
- *   split arrive/wait barrier per bucket; 13 B/elem algorithmic): 2 p parked in r/L2 with the
- *   quantise phase lagging two buckets, 3 the same recomputing p from L2-retained g and r,
- *   4 parked with lag 1, 5 recompute with lag 1, 6 split schedule, 7 lag 2 with alternating
- *   shared-memory parking, 8..10 CTA-shape sweep of 4, 11 TMA ring (cp.async.bulk), 12 warp-
- *   specialised TMA (producer warp + max/park warps + quantise warps, two TMA rings).
- *   Auto = 12 when buckets average >= 1M elements and pointers are 16-B aligned, else 1. */
+ *   NEBULA_OPT_INT8_KERNEL (INT8, FP8 and QSGD): 0 auto (default), 1 two-pass streaming
+ *   (max-abs pass + quantise pass, 21 B/elem of HBM traffic), 2 single pass: the
+ *   warp-specialised TMA kernel (cooperative grid of one CTA per SM: a producer warp feeding
+ *   two cp.async.bulk rings, max/park warps, quantise warps; 13 B/elem algorithmic; needs
+ *   16-B aligned pointers, else two-pass).  Auto = 2 when buckets average >= 1M elements
+ *   and pointers are 16-B aligned, else 1. */
 #define NEBULA_OPT_INT8_KERNEL 1
 /*   NEBULA_OPT_EXCHANGE (NCCL transport): 0 auto (default), 1 ncclAllGather of the payloads
  *   after the compress, 2 P2P push: the compress kernels store every payload word into the
@@ -231,9 +248,10 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 /*   NEBULA_OPT_FP16_KERNEL: 0 (default) TMA-ring streaming kernel for 16-B aligned calls,
  *   1 plain 128-bit-load streaming kernel. */
 #define NEBULA_OPT_FP16_KERNEL 3
-/*   NEBULA_OPT_STEP_FUSION: 0 (default) nebula_step fuses INT8 compress + exchange + reduce
- *   into one kernel where eligible (see nebula_step), 1 never (three stage launches),
- *   2..12 fused with warp split 0..10 of the kernel's tuning sweep. */
+/*   NEBULA_OPT_STEP_FUSION: 0 (default) nebula_step fuses INT8 / FP8 / QSGD compress + exchange
+ *   + reduce into one kernel where eligible (see nebula_step), 1 never (three stage launches),
+ *   2..12 fused with warp split 0..10 of the kernel's tuning sweep (6 = split 4, the P2P-pull
+ *   reducer with register loads; FP8 / QSGD take splits 0 and 4). */
 #define NEBULA_OPT_STEP_FUSION 4
 /*   NEBULA_OPT_EXACT_SCALE (NEXT-3, R28; hierarchical G > 1 only): 0 (default) every GPU's
  *   shard has its own INT8 / FP8 scale (R20); 1 the scale of the WHOLE cluster bucket: the
@@ -250,10 +268,17 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   contiguous ranges of 512-element sub-tiles (measured 0.30 vs 0.345 ms at BASELINE config 2).
  *   Same results. */
 #define NEBULA_OPT_TOPK_REDUCE 7
+/*   NEBULA_OPT_INTRA (G > 1): 0 (default) the intra-cluster reduce-scatter / all-gather over
+ *   NVLink peer memory with a fixed summation order when every GPU of the cluster is mapped,
+ *   1 NCCL ReduceScatter(avg) / AllGather (NCCL transport only).  Only between steps. */
+#define NEBULA_OPT_INTRA 8
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */
 int32_t nebula_exchange_mode(const nebula_ctx* ctx);
+/* Intra-cluster hop in use: 0 none (G = 1), 1 NCCL ReduceScatter(avg) / AllGather, 2 P2P
+ * fixed-order reduce-scatter / all-gather over NVLink peer memory; -1 for NULL. */
+int32_t nebula_intra_mode(const nebula_ctx* ctx);
 
 /* Per-kernel device timers.  When enabled, every kernel / collective the context enqueues is
  * bracketed by a CUDA event pair recorded on the context's stream (the stream the kernel
@@ -290,6 +315,11 @@ typedef struct nebula_svd nebula_svd; /* opaque, library-owned workspace for one
 /* m, n >= 1, min(m, n) <= 16384, 1 <= r <= min(m, n).  Allocates the workspace (fp64 Gram
  * min(m,n)^2, fp32 max(m,n) x r, solver buffers) on `device`; stream = cudaStream_t. */
 nebula_status nebula_svd_init(nebula_svd** out, int64_t m, int64_t n, int32_t r, int32_t device, void* stream);
+/* R29: the kept rank for a ratio rho in (0, 1]: r = clamp(floor(rho * min(m, n) + 1/2), 1,
+ * min(m, n)) ("r is the used ratio of the total singular values");
+ * 0 for invalid arguments.  nebula_svd_init_density = nebula_svd_init with that r. */
+int32_t nebula_svd_rank(int64_t m, int64_t n, double rho);
+nebula_status nebula_svd_init_density(nebula_svd** out, int64_t m, int64_t n, double rho, int32_t device, void* stream);
 nebula_status nebula_svd_set_stream(nebula_svd* h, void* stream);
 /* Payload size in bytes (preamble + padded sections). */
 nebula_status nebula_svd_payload_bytes(const nebula_svd* h, uint64_t* bytes);
@@ -311,7 +341,10 @@ nebula_status nebula_svd_set_eigensolver(nebula_svd* h, int32_t which);
 nebula_status nebula_svd_destroy(nebula_svd* h);
 const char* nebula_svd_last_error(const nebula_svd* h);
 
-/* Frees everything the context owns (synchronises first).  NULL is a no-op. */
+/* Frees everything the context owns (synchronises first).  NULL is a no-op.  COLLECTIVE for
+ * the NCCL transport when peers are mapped (P2P exchange or intra-cluster hop): every rank must
+ * call it, since peers may still read this rank's buffers over NVLink until all ranks arrive
+ * (a 4-byte all-reduce quiesces them before the mappings are closed and the memory freed). */
 nebula_status nebula_sync_destroy(nebula_ctx* ctx);
 
 /* Last error message of ctx (or of the last failed nebula_sync_init when ctx is NULL). */

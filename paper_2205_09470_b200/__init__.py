@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "QSGD", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK",
+    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "QSGD", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK", "SELF",
     "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
     "status_string", "abi_version", "HEADER", "SvdCodec", "SVD_FP16",
 ]
@@ -26,7 +26,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 QSGD = 6
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
-NCCL, LOOPBACK = 0, 1
+NCCL, LOOPBACK, SELF = 0, 1, 2
 SVD_FP16 = 5   # payload method id of the FP16(SVD(rho)) compressor (R31)
 ALL_BUCKETS = -1
 OPT_INT8_KERNEL = 1
@@ -36,6 +36,7 @@ OPT_STEP_FUSION = 4
 OPT_EXACT_SCALE = 5
 OPT_SR_SEED = 6
 OPT_TOPK_REDUCE = 7
+OPT_INTRA = 8
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -122,10 +123,13 @@ def load() -> ctypes.CDLL:
         "nebula_timing_enable": (I32, [P, I32]),
         "nebula_set_option": (I32, [P, I32, ctypes.c_int64]),
         "nebula_exchange_mode": (I32, [P]),
+        "nebula_intra_mode": (I32, [P]),
         "nebula_timing_read": (I32, [P, ctypes.POINTER(_PhaseTime), I32, ctypes.POINTER(I32)]),
         "nebula_phase_name": (ctypes.c_char_p, [ctypes.c_uint32]),
         "nebula_sync_destroy": (I32, [P]),
         "nebula_svd_init": (I32, [ctypes.POINTER(P), ctypes.c_int64, ctypes.c_int64, I32, I32, VP]),
+        "nebula_svd_init_density": (I32, [ctypes.POINTER(P), ctypes.c_int64, ctypes.c_int64, ctypes.c_double, I32, VP]),
+        "nebula_svd_rank": (I32, [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
         "nebula_svd_set_stream": (I32, [P, VP]),
         "nebula_svd_payload_bytes": (I32, [P, ctypes.POINTER(U64)]),
         "nebula_svd_compress": (I32, [P, VP, VP]),
@@ -166,11 +170,29 @@ def get_unique_id() -> bytes:
 
 
 def _ptr(x) -> int:
-    """Device/host pointer of a torch tensor, or an int address."""
+    """Device/host pointer of a torch tensor, or an int address (passed through unchecked)."""
     if x is None:
         return 0
     if isinstance(x, int):
         return x
+    return x.data_ptr()
+
+
+def _dev_f32(x, device: int, min_numel: int, what: str) -> int:
+    """Pointer of a caller buffer after the checks the C ABI cannot make: fp32, contiguous, on
+    the context's device, at least `min_numel` elements (the library reads / writes exactly
+    that many; a smaller buffer would be an out-of-bounds device access).  Ints pass through."""
+    if x is None or isinstance(x, int):
+        return _ptr(x)
+    import torch
+    if x.dtype != torch.float32:
+        raise ValueError(f"{what}: expected torch.float32, got {x.dtype}")
+    if not x.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+    if x.device.type != "cuda" or x.device.index != device:
+        raise ValueError(f"{what}: must live on cuda:{device}, got {x.device}")
+    if x.numel() < min_numel:
+        raise ValueError(f"{what}: {x.numel()} elements, the call needs {min_numel}")
     return x.data_ptr()
 
 
@@ -224,21 +246,31 @@ class SyncContext:
         self._ck(self._L.nebula_set_stream(self._h, _stream_handle(stream, self.device)))
 
     # ------------------------------------------------------------------ stages
+    def _elems(self, bucket) -> int:
+        return sum(self.bucket_numel) if bucket == ALL_BUCKETS else self.bucket_numel[bucket]
+
+    def _grad(self, bucket, grad) -> int:
+        stacked = self.num_clusters if self.transport == LOOPBACK else 1   # LOOPBACK: [P][elems]
+        return _dev_f32(grad, self.device, stacked * self._elems(bucket), "grad")
+
+    def _out(self, bucket, out) -> int:
+        return _dev_f32(out, self.device, self._elems(bucket), "out")
+
     def compress(self, bucket, grad, step):
-        self._ck(self._L.nebula_compress(self._h, bucket, _ptr(grad), step))
+        self._ck(self._L.nebula_compress(self._h, bucket, self._grad(bucket, grad), step))
 
     def exchange(self, bucket):
         self._ck(self._L.nebula_exchange(self._h, bucket))
 
     def decompress_reduce(self, bucket, out):
-        self._ck(self._L.nebula_decompress_reduce(self._h, bucket, _ptr(out)))
+        self._ck(self._L.nebula_decompress_reduce(self._h, bucket, self._out(bucket, out)))
 
     def decompress(self, bucket, slot, out):
         """Decode one cluster's payload (no averaging): the pipeline-hop use (NEXT-2)."""
-        self._ck(self._L.nebula_decompress(self._h, bucket, slot, _ptr(out)))
+        self._ck(self._L.nebula_decompress(self._h, bucket, slot, self._out(bucket, out)))
 
     def step(self, bucket, grad, out, step):
-        self._ck(self._L.nebula_step(self._h, bucket, _ptr(grad), _ptr(out), step))
+        self._ck(self._L.nebula_step(self._h, bucket, self._grad(bucket, grad), self._out(bucket, out), step))
 
     def step_host(self, host_grad, host_out, step):
         """host_grad / host_out: CPU tensors (pinned for full bandwidth) or numpy arrays."""
@@ -291,11 +323,10 @@ class SyncContext:
         self._ck(self._L.nebula_set_option(self._h, option, value))
 
     def set_int8_kernel(self, which: str):
-        """'auto' | 'two-pass' | 'onchip' (NEBULA_OPT_INT8_KERNEL)."""
-        self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "onchip": 2, "fused-recompute": 3,
-                                          "fused-park-lag1": 4, "fused-recompute-lag1": 5,
-                                          "fused-split": 6, "fused-smem": 7, "fused-256x2": 8, "fused-256x4": 9,
-                                          "fused-1024x2": 10, "fused-tma": 11, "fused-ws": 12}[which])
+        """'auto' | 'two-pass' | 'single-pass' (= 'onchip' = 'fused-ws': the warp-specialised
+        TMA kernel) (NEBULA_OPT_INT8_KERNEL; INT8, FP8 and QSGD)."""
+        self.set_option(OPT_INT8_KERNEL, {"auto": 0, "two-pass": 1, "single-pass": 2, "onchip": 2,
+                                          "fused-ws": 2}[which])
 
     def set_fp16_kernel(self, which: str):
         """'tma' (default) | 'plain' (NEBULA_OPT_FP16_KERNEL)."""
@@ -316,12 +347,20 @@ class SyncContext:
         """Seed of the QSGD stochastic-rounding uniforms (NEBULA_OPT_SR_SEED)."""
         self.set_option(OPT_SR_SEED, int(seed) - (1 << 64) if int(seed) >= (1 << 63) else int(seed))
 
+    def set_intra(self, which: str):
+        """G > 1: 'p2p' (default: fixed-order reduce-scatter / all-gather over NVLink peer
+        memory) | 'nccl' (NEBULA_OPT_INTRA)."""
+        self.set_option(OPT_INTRA, {"p2p": 0, "auto": 0, "nccl": 1}[which])
+
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""
         self.set_option(OPT_EXCHANGE, {"auto": 0, "nccl": 1, "push": 2, "pull": 3, "p2p": 3}[which])
 
     def exchange_mode(self) -> str:
         return EXCHANGE_MODES[self._L.nebula_exchange_mode(self._h)]
+
+    def intra_mode(self) -> str:
+        return {0: "none", 1: "nccl", 2: "p2p"}[self._L.nebula_intra_mode(self._h)]
 
     def timing_enable(self, on: bool = True):
         self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))
@@ -354,6 +393,30 @@ def broadcast_unique_id(src: int = 0, group=None) -> bytes:
     return uid[0]
 
 
+def self_group_id() -> bytes:
+    """A fresh 128-byte group id for SELF-transport contexts (any bytes shared by the group)."""
+    return os.urandom(UNIQUE_ID_BYTES)
+
+
+def self_group(bucket_numel, *, num_clusters, gpus_per_cluster=1, device=0, streams=None, **codec):
+    """All P x G contexts of one SELF-transport group on `device` (one process; every P2P path
+    of the NCCL transport runs on one GPU).  Returns [[ctx of (cluster c, local rank l)]];
+    streams[c][l] (torch streams) default to fresh ones — members need their own streams."""
+    import torch
+    gid = self_group_id()
+    P, G = num_clusters, gpus_per_cluster
+    out = []
+    for c in range(P):
+        row = []
+        for l in range(G):
+            st = streams[c][l] if streams is not None else torch.cuda.Stream(device=device)
+            row.append(SyncContext(bucket_numel, num_clusters=P, cluster_id=c, gpus_per_cluster=G, local_rank=l,
+                                   transport=SELF, device=device, unique_id=gid, stream=st, **codec))
+            row[-1].stream = st
+        out.append(row)
+    return out
+
+
 def topology_for_rank(rank: int, world: int, gpus_per_cluster: int = 1):
     """(num_clusters, cluster_id, local_rank) of a rank: cluster r // G, local rank r % G
     (G = 1 -> topology A, G > 1 -> topology B)."""
@@ -381,17 +444,19 @@ class SvdCodec:
     r = clamp(floor(rho min(m, n) + 0.5), 1, min(m, n)))."""
 
     def __init__(self, m: int, n: int, r: int | None = None, *, rho: float | None = None, device=0, stream=None):
-        import math
         L = load()
         self._L = L
-        if r is None:
-            k = min(m, n)
-            r = max(1, min(k, math.floor(float(rho) * k + 0.5)))
-        self.m, self.n, self.r, self.device = int(m), int(n), int(r), device
+        self.m, self.n, self.device = int(m), int(n), device
         h = ctypes.c_void_p()
-        s = L.nebula_svd_init(ctypes.byref(h), self.m, self.n, self.r, device, _stream_handle(stream, device))
+        if r is None:   # R29 is computed by the library (nebula_svd_init_density)
+            s = L.nebula_svd_init_density(ctypes.byref(h), self.m, self.n, float(rho), device,
+                                          _stream_handle(stream, device))
+            r = L.nebula_svd_rank(self.m, self.n, float(rho))
+        else:
+            s = L.nebula_svd_init(ctypes.byref(h), self.m, self.n, int(r), device, _stream_handle(stream, device))
         if s:
             raise NebulaError(s, L.nebula_svd_last_error(None).decode())
+        self.r = int(r)
         self._h = h
 
     def _ck(self, s):

@@ -70,24 +70,45 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources() + [__file__])
 
 
+def _compile_one(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return r.returncode, r.stdout + r.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (one nvcc per file), then link the shared
+    library.  Same flags for every translation unit."""
     if not force and up_to_date():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     inc, lib = _nccl_dirs()
     sinc, slib = _cusolver_dirs()
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    cmd = [_nvcc(), ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
-           "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-           "-Xptxas", "-v" if verbose else "-O3",
-           f"-I{INCLUDE}", f"-I{inc}", f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
-           f"-I{sinc}", f"-L{slib}", "-l:libcusolver.so.11", f"-Xlinker=-rpath,{slib}",
-           "-o", LIB + ".tmp"] + cus
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libnebula_sync.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    common = [_nvcc(), ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
+              "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
+              "-Xptxas", "-v" if verbose else "-O3", f"-I{INCLUDE}", f"-I{inc}", f"-I{sinc}"]
+    objs, cmds = [], []
+    for cu in cus:
+        o = os.path.join(objdir, os.path.basename(cu)[:-3] + ".o")
+        objs.append(o)
+        cmds.append(common + ["-c", cu, "-o", o])
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(_compile_one, cmds))
+    for (rc, out), cu in zip(results, cus):
+        if rc != 0:
+            sys.stderr.write(out)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(cu)}")
+        if verbose:
+            sys.stderr.write(out)
+    link = [_nvcc(), ARCH, "-shared", "-Xcompiler", "-fPIC", f"-L{lib}", "-l:libnccl.so.2",
+            f"-Xlinker=-rpath,{lib}", f"-L{slib}", "-l:libcusolver.so.11", f"-Xlinker=-rpath,{slib}",
+            "-o", LIB + ".tmp"] + objs
+    rc, out = _compile_one(link)
+    if rc != 0:
+        sys.stderr.write(out)
+        raise RuntimeError("nvcc failed linking libnebula_sync.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

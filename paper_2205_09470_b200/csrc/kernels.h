@@ -13,7 +13,8 @@ enum Phase : int {
   PH_IDENTITY = 0, PH_FP16, PH_ABSMAX, PH_INT8_QUANT, PH_TOPK_A, PH_TOPK_BRACKET, PH_TOPK_CLASSIFY,
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
   PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_FP8_QUANT,
-  PH_NCCL_SCALE, PH_QSGD_QUANT, PH_COUNT
+  PH_NCCL_SCALE, PH_QSGD_QUANT, PH_RS_PUSH, PH_RS_REDUCE, PH_AG_PULL, PH_SCALE_MAIL,
+  PH_P2P_FLAGS_RS, PH_P2P_FLAGS_AG, PH_COUNT
 };
 
 struct Launch {
@@ -28,6 +29,9 @@ struct Launch {
 // kernel's occupancy), never more than the work — a grid larger than one wave leaves a
 // partial second wave (the tail effect ncu showed on the reducer).
 int occupancy_per_sm(const void* kernel, int threads, size_t smem);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the CURRENT device, once per
+// (device, kernel, bytes) — the attribute is per device context (thread-safe cache).
+void ensure_smem_attr(const void* kernel, size_t bytes);
 inline unsigned persistent_grid(const Launch& L, uint64_t chunks, const void* kernel, int threads, size_t smem = 0) {
   uint64_t g = (uint64_t)L.num_sms * (uint64_t)occupancy_per_sm(kernel, threads, smem);
   if (chunks < g) g = chunks;
@@ -65,19 +69,15 @@ void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int
 void launch_qsgd_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags,
                        const SrArgs& sr);
-// FP8 (kind 1) / QSGD (kind 2) single HBM pass: the warp-specialised TMA kernel with that
-// quantiser (16-B aligned calls; cooperative, one CTA per SM; done_words >= nitems).
+// INT8 (kind 0) / FP8 (kind 1) / QSGD (kind 2) single HBM pass: the warp-specialised TMA
+// kernel with that quantiser (16-B aligned calls; cooperative, one CTA per SM; done_words >=
+// nitems words, zeroed by the launcher).
 void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, int nitems, const float* g, float* r,
                         const Dests& slots, uint32_t* scratch, uint32_t* flags, uint32_t* done_words,
                         const SrArgs& sr);
-// INT8 single HBM pass (cooperative persistent grid, split arrive/wait barrier per bucket,
-// p parked in r / L2 between the max-abs and the quantisation).  capacity() returns false
-// when a cooperative launch is not possible; the caller then uses the two-pass kernels.
-// done_words: >= nitems words (zeroed by the launcher).
+// capacity(): false when the device cannot host the single-pass kernels' cooperative grid
+// (one 1024-thread CTA per SM with the TMA rings); the caller then uses the two-pass kernels.
 bool int8_onchip_capacity(int device, uint64_t* max_elems, int* grid, size_t* smem);
-void launch_int8_onchip(const Launch& L, bool ef, bool vec, const Item* items, int nitems,
-                        const float* g, float* r, const Dests& slots, uint32_t* scratch, uint32_t* flags,
-                        uint32_t* done_words, int grid, size_t smem, int variant);
 // Dense decompress + tree-average over P slots.
 void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RItem* items, int nitems,
                          uint64_t chunks, const Dests& slots, float* out);
@@ -98,7 +98,29 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.
 void launch_exchange_flags(const Launch& L, const Peers& pe, unsigned long long* local_arrive, int lo, int hi,
-                           uint64_t seq, uint32_t* flags);
+                           uint64_t seq, uint32_t* flags, int phase = PH_P2P_FLAGS);
+
+// ---- intra-cluster hop over NVLink peer memory, G > 1 (kernels_intra.cu) ----
+struct IItem {          // one bucket of an intra-cluster call
+  uint64_t off;         // element offset of the bucket in the caller's buffers (gradient / output)
+  uint64_t coff;        // element offset of the shard in library coded buffers (multiple of 4)
+  uint64_t cn;          // shard elements (bucket numel / G)
+  uint64_t chunk0;      // first 4096-element chunk of this item in the launch
+};
+struct PeerF { float* p[8]; int n, me; };   // a float buffer of every GPU of the cluster (own at [me])
+struct PeerU { uint32_t* p[8]; };
+// RS step 1: slice j of this GPU's gradient -> peer j's receive buffer, slot me (NVLink stores).
+void launch_rs_push(const Launch& L, bool vec, const IItem* items, int nitems, uint64_t chunks, const float* g,
+                    const PeerF& recv, uint64_t stride);
+// RS step 2 (after the flags): shard = fl(sum in local-rank order) / G.
+void launch_rs_reduce(const Launch& L, bool vec, const IItem* items, int nitems, uint64_t chunks, const float* g,
+                      const float* recv, uint64_t stride, int G, int me, float* shard);
+// AG (after the flags): out[slice j] = GPU j's averaged shard (NVLink loads).
+void launch_ag_pull(const Launch& L, bool vec, const IItem* items, int nitems, uint64_t chunks, const PeerF& shards,
+                    float* out);
+// NEXT-3 exact cluster scale: scratch[b] <- max over the G GPUs' scratch[b] (mailbox + flags).
+void launch_scale_mail(const Launch& L, const Peers& pe, const PeerU& mails, uint32_t* scratch, uint32_t* my_mail,
+                       unsigned long long* local_arrive, int lo, int hi, uint64_t seq, uint32_t* flags);
 
 // ---- top-k (kernels_topk.cu) ----
 struct TopkItem {       // per (cluster, bucket) top-k state, device resident

@@ -28,6 +28,7 @@
 #include <cusolverDn.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -439,6 +440,25 @@ static nebula_status svd_fail(nebula_svd* h, nebula_status st, const std::string
   } while (0)
 
 extern "C" {
+
+// R29: r = clamp(floor(rho * min(m, n) + 1/2), 1, min(m, n)) — "r is the used ratio of the total
+// singular values", rounded as R12.
+int32_t nebula_svd_rank(int64_t m, int64_t n, double rho) {
+  if (m < 1 || n < 1 || !(rho > 0.0 && rho <= 1.0)) return 0;
+  const int64_t k = m < n ? m : n;
+  double r = std::floor(rho * (double)k + 0.5);
+  if (r < 1) r = 1;
+  if (r > (double)k) r = (double)k;
+  return (int32_t)r;
+}
+
+nebula_status nebula_svd_init_density(nebula_svd** out, int64_t m, int64_t n, double rho, int32_t device, void* stream) {
+  if (!out) return svd_fail(nullptr, NEBULA_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  const int32_t r = nebula_svd_rank(m, n, rho);
+  if (r < 1) return svd_fail(nullptr, NEBULA_ERR_INVALID_ARG, "m, n must be >= 1 and rho in (0, 1]");
+  return nebula_svd_init(out, m, n, r, device, stream);
+}
 
 nebula_status nebula_svd_init(nebula_svd** out, int64_t m, int64_t n, int32_t r, int32_t device, void* stream) {
   if (!out) return svd_fail(nullptr, NEBULA_ERR_INVALID_ARG, "null out");

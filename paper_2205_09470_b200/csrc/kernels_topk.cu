@@ -1429,11 +1429,7 @@ static void densify_pu(const Launch& L, int vt, bool vec, const RItem* items, in
                        const Dests& slots, float* out) {
   const size_t smem = (size_t)(kDenThreads / 32) * P * kDenSub * sizeof(float);
   const void* f = vec ? (const void*)k_topk_densify<P, U, true> : (const void*)k_topk_densify<P, U, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[vec]) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[vec] = true;
-  }
+  ensure_smem_attr(f, smem);
   const unsigned grid = persistent_grid(L, tiles * (kRedTile / kDenSub) / (kDenThreads / 32) + 1, f, kDenThreads, smem);
   if (vec) k_topk_densify<P, U, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
   else k_topk_densify<P, U, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
@@ -1444,11 +1440,7 @@ static void densify_t(const Launch& L, int vt, bool vec, const RItem* items, int
                       const Dests& slots, const uint32_t* start, float* out) {
   const size_t smem = (size_t)P * kRedTile * sizeof(float);
   const void* f = vec ? (const void*)k_topk_densify_t<P, true> : (const void*)k_topk_densify_t<P, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[vec]) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[vec] = true;
-  }
+  ensure_smem_attr(f, smem);
   const unsigned grid = persistent_grid(L, tiles, f, kDenThreads, smem);
   if (vec) k_topk_densify_t<P, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, start, out, vt);
   else k_topk_densify_t<P, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, start, out, vt);
@@ -1459,11 +1451,7 @@ static void densify_w(const Launch& L, int vt, bool vec, const RItem* items, int
                       const Dests& slots, float* out) {
   const size_t smem = (size_t)(kDenThreads / 32) * P * kDenSub * sizeof(float);
   const void* f = vec ? (const void*)k_topk_densify_w<P, true> : (const void*)k_topk_densify_w<P, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[vec]) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[vec] = true;
-  }
+  ensure_smem_attr(f, smem);
   const unsigned grid = persistent_grid(L, tiles * (kRedTile / kDenSub) / (kDenThreads / 32) + 1, f, kDenThreads, smem);
   if (vec) k_topk_densify_w<P, true><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);
   else k_topk_densify_w<P, false><<<grid, kDenThreads, smem, L.stream>>>(items, nitems, tiles, slots, out, vt);

@@ -246,6 +246,21 @@ __device__ __forceinline__ float tree_sum(const float* v) {
   }
 }
 
+// System-scope flag protocol of the P2P exchanges (peers' words reached over NVLink).
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns_u64() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void write_preamble(uint8_t* slot, uint32_t method, uint32_t count, float scale,
                                                uint32_t aux) {
   uint4 pre = make_uint4(method, count, __float_as_uint(scale), aux);

@@ -2,17 +2,26 @@
 // plan, the three stages, NCCL transport over NVLink, LOOPBACK transport.
 //
 // Stage map:
-//   compress           a0 method gate -> [G>1: ncclReduceScatter(avg), PAPER.md:95]
-//                      -> a2..a6 EF + codec kernels (kernels_dense.cu / kernels_topk.cu)
-//   exchange           a7 in-place ncclAllGather of fixed-size payloads over the inter-cluster
-//                      communicator (slot c = cluster c); LOOPBACK: no-op
-//   decompress_reduce  a8 tree-average of the P slots -> [G>1: ncclAllGather of the shards]
+//   compress           a0 method gate -> [G>1: intra-cluster mean of the G GPUs'
+//                      buckets: fixed-order P2P reduce-scatter (kernels_intra.cu),
+//                      or ncclReduceScatter(avg) when the peers cannot be mapped]
+//                      -> a2..a6 EF + codec kernels (kernels_dense.cu / kernels_ws.cu / kernels_topk.cu)
+//   exchange           a7 payloads between clusters (slot c = cluster c): P2P
+//                      push / pull over NVLink with arrival flags, or an in-place ncclAllGather;
+//                      LOOPBACK: nothing moves
+//   decompress_reduce  a8 tree-average of the P slots -> [G>1: P2P all-gather of the shards]
+//
+// Transports: NCCL (one process per GPU; CUDA IPC maps the peers' buffers), LOOPBACK (all P
+// clusters simulated in one context), SELF (one context per (cluster, GPU) in ONE process —
+// the contexts reach each other's buffers directly, so every P2P code path runs on one GPU).
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -45,6 +54,12 @@ struct Table {         // one launch's work list, resident in d_items / d_ritems
   uint64_t chunks = 0;
   uint64_t entries = 0, tiles = 0;  // TOPK reduce: sum(k + 1), sum(ceil(n / 2048))
   bool aligned = true; // every g_off (or out_off) is a multiple of 4 elements
+};
+
+struct ITable {        // one intra-cluster call's bucket list, resident in d_iitems
+  int first = 0, count = 0;
+  uint64_t chunks = 0;
+  bool aligned = true;  // every off and cn a multiple of 4 elements
 };
 
 struct DevGuard {
@@ -83,6 +98,29 @@ struct nebula_ctx {
   std::vector<Table> rtab[2];
   float* d_shard_in = nullptr;   // G > 1
   float* d_shard_out = nullptr;
+
+  // ---- intra-cluster hop over NVLink peer memory (G > 1; kernels_intra.cu)
+  bool intra_p2p = false;        // every GPU of the cluster mapped (NCCL: IPC, SELF: same process)
+  int intra_opt = 0;             // NEBULA_OPT_INTRA: 0 auto (P2P when mapped), 1 NCCL RS/AG
+  float* d_recv = nullptr;       // [G][total_cn]: slot j = GPU j's slice of this GPU's shard
+  unsigned long long* d_arr_rs = nullptr;   // [B][G] arrival words: RS slices, AG shards, scale mail
+  unsigned long long* d_arr_ag = nullptr;
+  unsigned long long* d_arr_sc = nullptr;
+  uint32_t* d_mail = nullptr;    // [B][G] max-abs words of the G shards (exact cluster scale)
+  IItem* d_iitems = nullptr;
+  std::vector<ITable> itab;      // [0] = ALL, [1+b] = bucket b
+  float* ip_recv[8] = {};        // the cluster's GPUs' buffers, indexed by local rank
+  float* ip_out[8] = {};
+  unsigned long long* ip_arr_rs[8] = {};
+  unsigned long long* ip_arr_ag[8] = {};
+  unsigned long long* ip_arr_sc[8] = {};
+  uint32_t* ip_mail[8] = {};
+  std::vector<void*> ipc_opened; // CUDA IPC mappings to close at destroy
+
+  // ---- SELF transport: the group (unique id) this context belongs to
+  bool self = false;
+  bool peers_resolved = false;
+  std::string group;
   float* d_hgrad = nullptr;      // nebula_step_host staging (bucket-major)
   float* d_hout = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;   // nebula_step_host copy streams
@@ -116,6 +154,7 @@ struct nebula_ctx {
   uint64_t sr_seed = 0;         // NEBULA_OPT_SR_SEED (QSGD uniforms, R32)
   int topk_reduce = 1;          // NEBULA_OPT_TOPK_REDUCE: 0 tile-interleaved, 1 per-warp ranges (default)
   int exact_scale = 0;          // NEBULA_OPT_EXACT_SCALE: 1 = cluster-wide INT8/FP8 scale when G > 1 (R28)
+  bool ready = false;           // init completed (destroy may then run the collective quiesce)
   bool onchip_ok = false;
   int onchip_grid = 0;
   size_t onchip_smem = 0;
@@ -206,14 +245,17 @@ static nebula_status validate(const nebula_topology* t, const nebula_codec* c, c
   if (nb_ < 1) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "num_buckets must be >= 1");
   if (t->num_clusters < 1 || t->num_clusters > NEBULA_MAX_CLUSTERS)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "num_clusters must be in [1, 8]");
-  if (t->transport != NEBULA_TRANSPORT_NCCL && t->transport != NEBULA_TRANSPORT_LOOPBACK)
+  if (t->transport != NEBULA_TRANSPORT_NCCL && t->transport != NEBULA_TRANSPORT_LOOPBACK &&
+      t->transport != NEBULA_TRANSPORT_SELF)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown transport");
   if (t->gpus_per_cluster < 1 || t->gpus_per_cluster > 64)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "gpus_per_cluster must be >= 1");
   if (t->transport == NEBULA_TRANSPORT_LOOPBACK && t->gpus_per_cluster != 1)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "LOOPBACK simulates P clusters x 1 GPU (gpus_per_cluster must be 1)");
-  if (t->transport == NEBULA_TRANSPORT_NCCL) {
-    if (!t->nccl_unique_id) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "NCCL transport needs nccl_unique_id");
+  if (t->transport == NEBULA_TRANSPORT_SELF && t->gpus_per_cluster > 8)
+    return fail(nullptr, NEBULA_ERR_INVALID_ARG, "SELF transport: gpus_per_cluster must be <= 8");
+  if (t->transport != NEBULA_TRANSPORT_LOOPBACK) {
+    if (!t->nccl_unique_id) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "NCCL / SELF transport needs nccl_unique_id (the group id)");
     if (t->cluster_id < 0 || t->cluster_id >= t->num_clusters)
       return fail(nullptr, NEBULA_ERR_INVALID_ARG, "cluster_id out of range");
     if (t->local_rank < 0 || t->local_rank >= t->gpus_per_cluster)
@@ -326,10 +368,42 @@ static nebula_status build_tables(nebula_ctx* ctx, int lay) {
 
 nebula_status topk_setup(nebula_ctx* ctx);  // below
 
+// ---- SELF transport registry: the contexts of one group (same unique id) in this process.
+struct SelfGroup {
+  std::map<int, nebula_ctx*> members;   // global rank (cluster * G + local rank) -> context
+};
+static std::mutex g_self_mu;
+static std::map<std::string, SelfGroup> g_self;
+
+static void self_unregister(nebula_ctx* ctx) {
+  if (!ctx->self) return;
+  std::lock_guard<std::mutex> lk(g_self_mu);
+  auto it = g_self.find(ctx->group);
+  if (it == g_self.end()) return;
+  const int rank = ctx->topo.cluster_id * ctx->G + ctx->topo.local_rank;
+  auto m = it->second.members.find(rank);
+  if (m != it->second.members.end() && m->second == ctx) it->second.members.erase(m);
+  if (it->second.members.empty()) g_self.erase(it);
+}
+
 static void release(nebula_ctx* ctx) {
   if (!ctx) return;
   DevGuard g(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  // Collective quiesce (NCCL transport with peer mappings): a peer may still be reading our
+  // exported buffers over NVLink (P2P pull reducer, all-gather pull), so nobody unmaps or frees
+  // before every rank reached destroy.  nebula_sync_destroy is collective in that case.
+  if (ctx->ready && ctx->world && (ctx->p2p_ok || ctx->intra_p2p)) {
+    int32_t* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int32_t)) == cudaSuccess) {
+      cudaMemset(d, 0, sizeof(int32_t));
+      ncclAllReduce(d, d, 1, ncclInt32, ncclSum, ctx->world, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(d);
+    }
+  }
+  self_unregister(ctx);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(ctx->d_resid);
   cudaFree(ctx->d_slots);
   cudaFree(ctx->d_flags);
@@ -340,6 +414,12 @@ static void release(nebula_ctx* ctx) {
   }
   cudaFree(ctx->d_shard_in);
   cudaFree(ctx->d_shard_out);
+  cudaFree(ctx->d_recv);
+  cudaFree(ctx->d_arr_rs);
+  cudaFree(ctx->d_arr_ag);
+  cudaFree(ctx->d_arr_sc);
+  cudaFree(ctx->d_mail);
+  cudaFree(ctx->d_iitems);
   cudaFree(ctx->d_hgrad);
   cudaFree(ctx->d_hout);
   for (cudaEvent_t e : ctx->ev_in) cudaEventDestroy(e);
@@ -349,11 +429,6 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_topk_mem);
   cudaFree(ctx->d_bar);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
-  for (int c = 0; c < NEBULA_MAX_CLUSTERS; ++c) {
-    if (c == ctx->me) continue;
-    if (ctx->peer_slots[c]) cudaIpcCloseMemHandle(ctx->peer_slots[c]);
-    if (ctx->peer_arrive[c]) cudaIpcCloseMemHandle(ctx->peer_arrive[c]);
-  }
   cudaFree(ctx->d_arrive);
   if (ctx->intra) ncclCommDestroy(ctx->intra);
   if (ctx->inter && ctx->inter != ctx->world) ncclCommDestroy(ctx->inter);
@@ -361,91 +436,162 @@ static void release(nebula_ctx* ctx) {
   delete ctx;
 }
 
-// P2P push setup (collective over the inter-cluster communicator): every cluster shares its
-// device ordinal, a host id and CUDA IPC handles of its slot buffer and arrival flags through
-// ncclAllGather; the push is enabled only if EVERY rank can map every peer (same host,
-// cudaDeviceCanAccessPeer), so all ranks agree on the transport.
+// ---- NCCL transport: peer mappings (collective over all P*G ranks).  Every rank exports CUDA
+// IPC handles of its slot buffer and arrival words (inter-cluster exchange) and of its receive
+// buffer, averaged shard, intra arrival words and scale mailbox (intra-cluster hop); the
+// handles travel through one ncclAllGather.  Each rank OPENS its peers' handles first, then all
+// ranks agree (ncclMin) on whether every rank mapped every peer; if not, everybody closes its
+// mappings and keeps the NCCL collectives, so all ranks always use the same transport.
 struct P2PInfo {
-  cudaIpcMemHandle_t slots, arrive;
-  int32_t device, ok;
-  uint64_t host;
+  cudaIpcMemHandle_t h[8];   // slots, arrive, recv, shard_out, arr_rs, arr_ag, arr_sc, mail
+  int32_t device, ok, pad0, pad1;
 };
 
-static uint64_t host_id() {
-  char name[256] = {0};
-  FILE* f = fopen("/proc/sys/kernel/hostname", "r");
-  if (f) {
-    if (!fgets(name, sizeof(name), f)) name[0] = 0;
-    fclose(f);
+static void* ipc_open(nebula_ctx* ctx, const cudaIpcMemHandle_t& h, bool* ok) {
+  void* p = nullptr;
+  if (!*ok) return nullptr;
+  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    *ok = false;
+    return nullptr;
   }
-  uint64_t h = 1469598103934665603ull;
-  for (const char* p = name; *p; ++p) h = (h ^ (uint64_t)(unsigned char)*p) * 1099511628211ull;
-  return h;
+  ctx->ipc_opened.push_back(p);
+  return p;
 }
 
 static nebula_status p2p_setup(nebula_ctx* ctx) {
-  const int P = ctx->P, B = (int)ctx->b.size();
-  CKC(cudaMalloc(&ctx->d_arrive, sizeof(unsigned long long) * (size_t)B * P));
-  CKC(cudaMemset(ctx->d_arrive, 0, sizeof(unsigned long long) * (size_t)B * P));
+  const int P = ctx->P, G = ctx->G, N = P * G;
+  const int cl = ctx->topo.cluster_id, lr = ctx->local_rank, me = cl * G + lr;
   P2PInfo mine{};
   mine.device = ctx->device;
-  mine.host = host_id();
-  mine.ok = cudaIpcGetMemHandle(&mine.slots, ctx->d_slots) == cudaSuccess &&
-            cudaIpcGetMemHandle(&mine.arrive, ctx->d_arrive) == cudaSuccess;
+  void* bufs[8] = {ctx->d_slots, ctx->d_arrive, ctx->d_recv, ctx->d_shard_out, ctx->d_arr_rs, ctx->d_arr_ag,
+                   ctx->d_arr_sc, ctx->d_mail};
+  mine.ok = 1;
+  for (int k = 0; k < 8; ++k)
+    if (bufs[k] && cudaIpcGetMemHandle(&mine.h[k], bufs[k]) != cudaSuccess) mine.ok = 0;
   cudaGetLastError();
   P2PInfo* d_info = nullptr;
-  CKC(cudaMalloc(&d_info, sizeof(P2PInfo) * P));
-  CKC(cudaMemcpy(d_info + ctx->me, &mine, sizeof(P2PInfo), cudaMemcpyHostToDevice));
-  CKN(ncclAllGather(d_info + ctx->me, d_info, sizeof(P2PInfo), ncclUint8, ctx->inter, ctx->stream));
+  CKC(cudaMalloc(&d_info, sizeof(P2PInfo) * N));
+  CKC(cudaMemcpy(d_info + me, &mine, sizeof(P2PInfo), cudaMemcpyHostToDevice));
+  CKN(ncclAllGather(d_info + me, d_info, sizeof(P2PInfo), ncclUint8, ctx->world, ctx->stream));
   CKC(cudaStreamSynchronize(ctx->stream));
-  std::vector<P2PInfo> all(P);
-  CKC(cudaMemcpy(all.data(), d_info, sizeof(P2PInfo) * P, cudaMemcpyDeviceToHost));
-  int ok = 1;
-  for (int c = 0; c < P; ++c) {
-    if (c == ctx->me) continue;
-    int can = 0;
-    if (!all[c].ok || all[c].host != mine.host || all[c].device == ctx->device ||
-        cudaDeviceCanAccessPeer(&can, ctx->device, all[c].device) != cudaSuccess || !can)
-      ok = 0;
-  }
-  cudaGetLastError();
-  // agree: P2P only if every rank can reach every peer
-  int32_t* d_ok = reinterpret_cast<int32_t*>(d_info);
-  CKC(cudaMemcpy(d_ok, &ok, sizeof(int32_t), cudaMemcpyHostToDevice));
-  CKN(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, ctx->inter, ctx->stream));
-  CKC(cudaStreamSynchronize(ctx->stream));
-  CKC(cudaMemcpy(&ok, d_ok, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<P2PInfo> all(N);
+  CKC(cudaMemcpy(all.data(), d_info, sizeof(P2PInfo) * N, cudaMemcpyDeviceToHost));
   cudaFree(d_info);
-  if (!ok) return NEBULA_OK;   // NCCL all-gather transport
-  for (int c = 0; c < P; ++c) {
-    if (c == ctx->me) {
+  // inter-cluster peers: same local rank in every other cluster
+  bool inter_ok = P > 1;
+  const size_t inter_mark = ctx->ipc_opened.size();
+  for (int c = 0; c < P && inter_ok; ++c) {
+    const P2PInfo& q = all[c * G + lr];
+    if (c == cl) {
       ctx->peer_slots[c] = ctx->d_slots;
       ctx->peer_arrive[c] = ctx->d_arrive;
       continue;
     }
-    void* ps = nullptr;
-    void* pa = nullptr;
-    CKC(cudaIpcOpenMemHandle(&ps, all[c].slots, cudaIpcMemLazyEnablePeerAccess));
-    CKC(cudaIpcOpenMemHandle(&pa, all[c].arrive, cudaIpcMemLazyEnablePeerAccess));
-    ctx->peer_slots[c] = static_cast<uint8_t*>(ps);
-    ctx->peer_arrive[c] = static_cast<unsigned long long*>(pa);
+    inter_ok = q.ok && mine.ok && q.device != ctx->device;
+    ctx->peer_slots[c] = static_cast<uint8_t*>(ipc_open(ctx, q.h[0], &inter_ok));
+    ctx->peer_arrive[c] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[1], &inter_ok));
   }
-  ctx->p2p_ok = true;
+  const size_t intra_mark = ctx->ipc_opened.size();
+  bool intra_ok = G > 1 && G <= 8;
+  for (int j = 0; j < G && intra_ok; ++j) {
+    const P2PInfo& q = all[cl * G + j];
+    if (j == lr) {
+      ctx->ip_recv[j] = ctx->d_recv;
+      ctx->ip_out[j] = ctx->d_shard_out;
+      ctx->ip_arr_rs[j] = ctx->d_arr_rs;
+      ctx->ip_arr_ag[j] = ctx->d_arr_ag;
+      ctx->ip_arr_sc[j] = ctx->d_arr_sc;
+      ctx->ip_mail[j] = ctx->d_mail;
+      continue;
+    }
+    intra_ok = q.ok && mine.ok && q.device != ctx->device;
+    ctx->ip_recv[j] = static_cast<float*>(ipc_open(ctx, q.h[2], &intra_ok));
+    ctx->ip_out[j] = static_cast<float*>(ipc_open(ctx, q.h[3], &intra_ok));
+    ctx->ip_arr_rs[j] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[4], &intra_ok));
+    ctx->ip_arr_ag[j] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[5], &intra_ok));
+    ctx->ip_arr_sc[j] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[6], &intra_ok));
+    ctx->ip_mail[j] = static_cast<uint32_t*>(ipc_open(ctx, q.h[7], &intra_ok));
+  }
+  // agree (every rank mapped every peer), else everybody unmaps and keeps NCCL
+  int32_t ok2[2] = {inter_ok ? 1 : 0, intra_ok ? 1 : 0};
+  int32_t* d_ok = nullptr;
+  CKC(cudaMalloc(&d_ok, sizeof(ok2)));
+  CKC(cudaMemcpy(d_ok, ok2, sizeof(ok2), cudaMemcpyHostToDevice));
+  CKN(ncclAllReduce(d_ok, d_ok, 2, ncclInt32, ncclMin, ctx->world, ctx->stream));
+  CKC(cudaStreamSynchronize(ctx->stream));
+  CKC(cudaMemcpy(ok2, d_ok, sizeof(ok2), cudaMemcpyDeviceToHost));
+  cudaFree(d_ok);
+  auto close_from = [&](size_t a, size_t b) {
+    for (size_t k = a; k < b; ++k) cudaIpcCloseMemHandle(ctx->ipc_opened[k]);
+    for (size_t k = a; k < b; ++k) ctx->ipc_opened[k] = nullptr;
+  };
+  if (!ok2[1]) close_from(intra_mark, ctx->ipc_opened.size());
+  if (!ok2[0]) close_from(inter_mark, intra_mark);
+  ctx->ipc_opened.erase(std::remove(ctx->ipc_opened.begin(), ctx->ipc_opened.end(), nullptr), ctx->ipc_opened.end());
+  ctx->p2p_ok = ok2[0] != 0;
+  ctx->intra_p2p = ok2[1] != 0;
+  if (!ctx->p2p_ok)
+    for (int c = 0; c < NEBULA_MAX_CLUSTERS; ++c) ctx->peer_slots[c] = nullptr, ctx->peer_arrive[c] = nullptr;
   return NEBULA_OK;
 }
 
-// Slot buffer of a bucket's current exchange (the P2P modes double-buffer by seq parity).
-static uint8_t* slots_of(const nebula_ctx* ctx, const BucketInfo& bk) {
-  return ctx->d_slots + (ctx->xmode >= 2 ? (bk.seq & 1) * ctx->slot_span : 0);
+// ---- SELF transport: resolve the group's buffers (all P*G contexts must exist by the first
+// stage call; their devices must be peer-accessible, the same device always is).
+static nebula_status self_resolve(nebula_ctx* ctx) {
+  if (!ctx->self || ctx->peers_resolved) return NEBULA_OK;
+  std::lock_guard<std::mutex> lk(g_self_mu);
+  auto it = g_self.find(ctx->group);
+  const int P = ctx->P, G = ctx->G, cl = ctx->topo.cluster_id, lr = ctx->local_rank;
+  if (it == g_self.end() || (int)it->second.members.size() != P * G)
+    return fail(ctx, NEBULA_ERR_STATE, "SELF transport: not every (cluster, GPU) context of the group exists yet");
+  auto& m = it->second.members;
+  auto reach = [&](const nebula_ctx* q) -> bool {
+    if (q->device == ctx->device) return true;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, ctx->device, q->device) != cudaSuccess || !can) return false;
+    cudaError_t e = cudaDeviceEnablePeerAccess(q->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return false;
+    cudaGetLastError();
+    return true;
+  };
+  for (int c = 0; c < P; ++c) {
+    const nebula_ctx* q = m[c * G + lr];
+    if (q->P != P || q->G != G || q->codec.method != ctx->codec.method || q->b.size() != ctx->b.size() || !reach(q))
+      return fail(ctx, NEBULA_ERR_INVALID_ARG, "SELF transport: group members disagree (topology / codec / buckets) or cannot reach each other");
+    ctx->peer_slots[c] = q->d_slots;
+    ctx->peer_arrive[c] = q->d_arrive;
+  }
+  for (int j = 0; j < G; ++j) {
+    const nebula_ctx* q = m[cl * G + j];
+    if (q->P != P || q->G != G || q->b.size() != ctx->b.size() || !reach(q))
+      return fail(ctx, NEBULA_ERR_INVALID_ARG, "SELF transport: group members disagree or cannot reach each other");
+    ctx->ip_recv[j] = q->d_recv;
+    ctx->ip_out[j] = q->d_shard_out;
+    ctx->ip_arr_rs[j] = q->d_arr_rs;
+    ctx->ip_arr_ag[j] = q->d_arr_ag;
+    ctx->ip_arr_sc[j] = q->d_arr_sc;
+    ctx->ip_mail[j] = q->d_mail;
+  }
+  ctx->p2p_ok = P > 1;
+  ctx->intra_p2p = G > 1;
+  ctx->peers_resolved = true;
+  return NEBULA_OK;
 }
 
-// Payload destinations of a compress: own slot buffer, plus every peer's for the P2P push.
-static Dests dests_of(const nebula_ctx* ctx, const BucketInfo& bk) {
+// Slot buffer of a bucket's exchange `seq` (the P2P modes double-buffer by seq parity).
+static uint8_t* slots_at(const nebula_ctx* ctx, uint64_t seq) {
+  return ctx->d_slots + (ctx->xmode >= 2 ? (seq & 1) * ctx->slot_span : 0);
+}
+static uint8_t* slots_of(const nebula_ctx* ctx, const BucketInfo& bk) { return slots_at(ctx, bk.seq); }
+
+// Payload destinations of a compress `seq`: own slot buffer, plus every peer's for the P2P push.
+static Dests dests_of(const nebula_ctx* ctx, uint64_t seq) {
   Dests d{};
-  d.p[0] = slots_of(ctx, bk);
+  d.p[0] = slots_at(ctx, seq);
   d.n = 1;
   if (ctx->xmode == 2) {
-    const uint64_t half = (bk.seq & 1) * ctx->slot_span;
+    const uint64_t half = (seq & 1) * ctx->slot_span;
     for (int c = 0; c < ctx->P; ++c)
       if (c != ctx->me) d.p[d.n++] = ctx->peer_slots[c] + half;
   }
@@ -453,13 +599,56 @@ static Dests dests_of(const nebula_ctx* ctx, const BucketInfo& bk) {
 }
 
 // Where the reducer finds cluster c's payload: the local slot buffer, or (P2P pull) cluster
-// c's own buffer through its IPC mapping.
+// c's own buffer (IPC-mapped, or the group member's for SELF).
 static Dests sources_of(const nebula_ctx* ctx, const BucketInfo& bk) {
   Dests d{};
   d.n = ctx->P;
   for (int c = 0; c < ctx->P; ++c)
     d.p[c] = ctx->xmode == 3 ? ctx->peer_slots[c] + (bk.seq & 1) * ctx->slot_span : slots_of(ctx, bk);
   return d;
+}
+
+static Peers inter_peers(const nebula_ctx* ctx) {
+  Peers pe{};
+  for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
+  pe.n = ctx->P;
+  pe.me = ctx->me;
+  return pe;
+}
+static Peers intra_peers(const nebula_ctx* ctx, unsigned long long* const* arr) {
+  Peers pe{};
+  for (int j = 0; j < ctx->G; ++j) pe.arrive[j] = arr[j];
+  pe.n = ctx->G;
+  pe.me = ctx->local_rank;
+  return pe;
+}
+static bool intra_p2p_on(const nebula_ctx* ctx) { return ctx->G > 1 && ctx->intra_p2p && ctx->intra_opt == 0; }
+
+// Intra-cluster tables: per call type one IItem per bucket (ALL: caller offsets bk.off).
+static nebula_status build_itables(nebula_ctx* ctx) {
+  const int B = (int)ctx->b.size();
+  std::vector<IItem> items;
+  for (int t = 0; t <= B; ++t) {
+    ITable T;
+    T.first = (int)items.size();
+    const int blo = t == 0 ? 0 : t - 1, bhi = t == 0 ? B : t;
+    for (int bi = blo; bi < bhi; ++bi) {
+      const BucketInfo& bk = ctx->b[bi];
+      IItem it{};
+      it.off = t == 0 ? bk.off : 0;
+      it.coff = bk.coff;
+      it.cn = bk.cn;
+      it.chunk0 = T.chunks;
+      T.chunks += (bk.cn + 4095) / 4096;
+      T.aligned &= (it.off % 4 == 0) && (bk.cn % 4 == 0);
+      items.push_back(it);
+    }
+    T.count = (int)items.size() - T.first;
+    ctx->itab.push_back(T);
+  }
+  CKC(cudaMalloc(&ctx->d_iitems, std::max<size_t>(1, items.size()) * sizeof(IItem)));
+  CKC(cudaMemcpy(ctx->d_iitems, items.data(), items.size() * sizeof(IItem), cudaMemcpyHostToDevice));
+  return NEBULA_OK;
 }
 
 extern "C" {
@@ -506,6 +695,8 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
   ctx->P = topo->num_clusters;
   ctx->G = topo->gpus_per_cluster;
   ctx->loopback = topo->transport == NEBULA_TRANSPORT_LOOPBACK;
+  ctx->self = topo->transport == NEBULA_TRANSPORT_SELF;
+  if (ctx->self) ctx->group.assign(static_cast<const char*>(topo->nccl_unique_id), NEBULA_UNIQUE_ID_BYTES);
   ctx->Ploc = ctx->loopback ? ctx->P : 1;
   ctx->me = ctx->loopback ? 0 : topo->cluster_id;
   ctx->local_rank = ctx->loopback ? 0 : topo->local_rank;
@@ -564,6 +755,27 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     if (ctx->G > 1) {
       if (cudaMalloc(&ctx->d_shard_in, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess ||
           cudaMalloc(&ctx->d_shard_out, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess) { ctx->err = "shard allocation failed"; return bail(NEBULA_ERR_OOM); }
+      if (ctx->G <= 8) {   // intra-cluster P2P hop buffers (used when every peer can be mapped)
+        const size_t aw = sizeof(unsigned long long) * (size_t)num_buckets * ctx->G;
+        if (cudaMalloc(&ctx->d_recv, std::max<uint64_t>(16, (uint64_t)ctx->G * ctx->total_cn * 4)) != cudaSuccess ||
+            cudaMalloc(&ctx->d_arr_rs, aw) != cudaSuccess || cudaMalloc(&ctx->d_arr_ag, aw) != cudaSuccess ||
+            cudaMalloc(&ctx->d_arr_sc, aw) != cudaSuccess ||
+            cudaMalloc(&ctx->d_mail, sizeof(uint32_t) * (size_t)num_buckets * ctx->G) != cudaSuccess) {
+          ctx->err = "intra-cluster buffer allocation failed";
+          return bail(NEBULA_ERR_OOM);
+        }
+        if (cudaMemset(ctx->d_arr_rs, 0, aw) != cudaSuccess || cudaMemset(ctx->d_arr_ag, 0, aw) != cudaSuccess ||
+            cudaMemset(ctx->d_arr_sc, 0, aw) != cudaSuccess) { ctx->err = "memset failed"; return bail(NEBULA_ERR_CUDA); }
+        nebula_status si = build_itables(ctx);
+        if (si != NEBULA_OK) return bail(si);
+      }
+    }
+    if (!ctx->loopback && ctx->P > 1) {   // inter-cluster arrival words [B][P] (P2P exchange)
+      const size_t aw = sizeof(unsigned long long) * (size_t)num_buckets * ctx->P;
+      if (cudaMalloc(&ctx->d_arrive, aw) != cudaSuccess || cudaMemset(ctx->d_arrive, 0, aw) != cudaSuccess) {
+        ctx->err = "arrival-word allocation failed";
+        return bail(NEBULA_ERR_OOM);
+      }
     }
     nebula_status s = NEBULA_OK;
     for (int l = 0; l < ctx->nlayouts && s == NEBULA_OK; ++l) s = build_tables(ctx, l);
@@ -582,7 +794,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     }
 
     // ---- communicators (collective over all P*G ranks)
-    if (!ctx->loopback) {
+    if (!ctx->loopback && !ctx->self) {
       ncclUniqueId id;
       std::memcpy(&id, topo->nccl_unique_id, sizeof(id));
       const int nranks = ctx->P * ctx->G, rank = topo->cluster_id * ctx->G + topo->local_rank;
@@ -598,16 +810,31 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     }
     if (!ctx->loopback) {
       ctx->xmode = 1;
-      if (ctx->P > 1) {
+      if (ctx->self) {
+        // peers are the other contexts of the group in this process (resolved at the first
+        // stage call, once every member exists); the exchange is always P2P
+        std::lock_guard<std::mutex> lk(g_self_mu);
+        SelfGroup& grp = g_self[ctx->group];
+        const int rank = topo->cluster_id * ctx->G + topo->local_rank;
+        if (grp.members.count(rank)) {
+          ctx->err = "SELF transport: this (cluster, local rank) already has a context in the group";
+          ctx->self = false;   // not registered: release must not unregister the other context
+          return bail(NEBULA_ERR_INVALID_ARG);
+        }
+        grp.members[rank] = ctx;
+        ctx->p2p_ok = ctx->P > 1;
+        ctx->intra_p2p = ctx->G > 1;
+      } else if (ctx->P > 1 || ctx->G > 1) {
         nebula_status ps = p2p_setup(ctx);
         if (ps != NEBULA_OK) return bail(ps);
-        // auto: P = 2 -> push (one peer: the NVLink egress hides inside the compress kernel);
-        // P > 2 -> pull (NVLink loads outrun SM-issued stores once every GPU feeds P - 1 peers)
-        if (ctx->p2p_ok) ctx->xmode = ctx->P == 2 ? 2 : 3;
       }
+      // auto: P = 2 -> push (one peer: the NVLink egress hides inside the compress kernel);
+      // P > 2 -> pull (NVLink loads outrun SM-issued stores once every GPU feeds P - 1 peers)
+      if (ctx->p2p_ok && ctx->P > 1) ctx->xmode = ctx->P == 2 ? 2 : 3;
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
   }
+  ctx->ready = true;
   *out = ctx;
   return NEBULA_OK;
 }
@@ -621,13 +848,108 @@ nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream) {
 // NEXT-3 (R28): the max-abs words of this GPU's shards (scratch[b], Ploc == 1 when G > 1;
 // |p| bits order like the floats, NaN/Inf bits above every finite one) -> the max over the G
 // shards of the cluster, so every shard quantises with the scale of the whole cluster bucket.
-// One 4-byte-per-bucket all-reduce on the intra-cluster communicator.
-static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int32_t bucket) {
+// P2P: a mailbox + flag kernel over the cluster's GPUs; else one 4-byte-per-bucket
+// ncclAllReduce(max) on the intra-cluster communicator.
+static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi, uint64_t seq) {
+  if (intra_p2p_on(ctx)) {
+    PeerU mails{};
+    for (int j = 0; j < ctx->G; ++j) mails.p[j] = ctx->ip_mail[j];
+    launch_scale_mail(L, intra_peers(ctx, ctx->ip_arr_sc), mails, ctx->d_scratch, ctx->d_mail, ctx->d_arr_sc, lo, hi,
+                      seq, ctx->d_flags);
+    CKC(cudaGetLastError());
+    return NEBULA_OK;
+  }
   Mark mk(L, PH_NCCL_SCALE);
   uint32_t* w = ctx->d_scratch + (bucket == NEBULA_ALL_BUCKETS ? 0 : bucket);
   const size_t cnt = bucket == NEBULA_ALL_BUCKETS ? ctx->b.size() : 1;
   CKN(ncclAllReduce(w, w, cnt, ncclUint32, ncclMax, ctx->intra, ctx->stream));
   return NEBULA_OK;
+}
+
+// G > 1: this GPU's shard of the cluster mean (R20).  P2P: push the peers' slices, flag
+// handshake, fixed-order sum / G (bit-identical to the oracle for any input); else NCCL
+// ReduceScatter(avg) (order and pre-scaling are NCCL's).
+static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi,
+                                          const float* g, uint64_t seq) {
+  if (intra_p2p_on(ctx)) {
+    const ITable& T = ctx->itab[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+    const IItem* it = ctx->d_iitems + T.first;
+    const bool vec = T.aligned && (uintptr_t)g % 16 == 0;
+    PeerF recv{};
+    for (int j = 0; j < ctx->G; ++j) recv.p[j] = ctx->ip_recv[j];
+    recv.n = ctx->G;
+    recv.me = ctx->local_rank;
+    launch_rs_push(L, vec, it, T.count, T.chunks, g, recv, ctx->total_cn);
+    launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_rs), ctx->d_arr_rs, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_RS);
+    launch_rs_reduce(L, vec, it, T.count, T.chunks, g, ctx->d_recv, ctx->total_cn, ctx->G, ctx->local_rank,
+                     ctx->d_shard_in);
+    CKC(cudaGetLastError());
+    return NEBULA_OK;
+  }
+  if (!ctx->intra) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "no intra-cluster transport (peers not mapped, no NCCL)");
+  Mark mk(L, PH_NCCL_RS);
+  CKN(ncclGroupStart());
+  for (int i = lo; i < hi; ++i) {
+    const BucketInfo& bk = ctx->b[i];
+    if (!bk.cn) continue;
+    const float* src = g + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+    CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.coff, bk.cn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
+  }
+  CKN(ncclGroupEnd());
+  return NEBULA_OK;
+}
+
+// G > 1: every GPU of the cluster gathers the P2P-averaged shards into dev_out.  P2P: flag
+// handshake, then NVLink loads of the peers' shards; else NCCL AllGather.
+static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi, float* dev_out,
+                                      uint64_t seq) {
+  if (intra_p2p_on(ctx)) {
+    const ITable& T = ctx->itab[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+    launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_ag), ctx->d_arr_ag, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_AG);
+    PeerF outs{};
+    for (int j = 0; j < ctx->G; ++j) outs.p[j] = ctx->ip_out[j];
+    outs.n = ctx->G;
+    outs.me = ctx->local_rank;
+    launch_ag_pull(L, T.aligned && (uintptr_t)dev_out % 16 == 0, ctx->d_iitems + T.first, T.count, T.chunks, outs, dev_out);
+    CKC(cudaGetLastError());
+    return NEBULA_OK;
+  }
+  if (!ctx->intra) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "no intra-cluster transport (peers not mapped, no NCCL)");
+  Mark mk(L, PH_NCCL_AG);
+  CKN(ncclGroupStart());
+  for (int i = lo; i < hi; ++i) {
+    const BucketInfo& bk = ctx->b[i];
+    if (!bk.cn) continue;
+    float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+    CKN(ncclAllGather(ctx->d_shard_out + bk.coff, dst, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
+  }
+  CKN(ncclGroupEnd());
+  return NEBULA_OK;
+}
+
+static nebula_status zero_scratch(nebula_ctx* ctx, const Launch& L, int32_t bucket) {
+  Mark mk(L, PH_MEMSET);
+  if (bucket == NEBULA_ALL_BUCKETS) {
+    CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
+  } else {
+    for (int c = 0; c < ctx->Ploc; ++c)
+      CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
+  }
+  return NEBULA_OK;
+}
+
+// Call preconditions shared by compress and the fused step: every bucket of the call is idle
+// (a second compress would apply the residual twice) and, for ALL calls, at the same
+// step count, so one sequence number names the exchange of every bucket of the call.
+static nebula_status stage_start(nebula_ctx* ctx, int lo, int hi) {
+  for (int i = lo; i < hi; ++i)
+    if (ctx->b[i].state != ST_IDLE)
+      return fail(ctx, NEBULA_ERR_STATE, "compress: bucket " + std::to_string(i) +
+                                             " is mid-step (compress -> exchange -> decompress_reduce)");
+  for (int i = lo + 1; i < hi; ++i)
+    if (ctx->b[i].seq != ctx->b[lo].seq)
+      return fail(ctx, NEBULA_ERR_STATE, "ALL-bucket call over buckets at different step counts");
+  return self_resolve(ctx);
 }
 
 // ============================================================================ stages
@@ -636,33 +958,26 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
   if (!dev_grad && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
+  nebula_status st0 = stage_start(ctx, lo, hi);
+  if (st0 != NEBULA_OK) return st0;
   DevGuard dg(ctx->device);
   const int method = method_at(ctx, step);
   const bool ef = ctx->codec.error_feedback != 0;
   const int lay = layout_of(ctx, method);
   const Table& T = ctx->ctab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
   const Launch L = launch_of(ctx);
-  for (int i = lo + 1; i < hi; ++i)
-    if ((ctx->b[i].seq & 1) != (ctx->b[lo].seq & 1))
-      return fail(ctx, NEBULA_ERR_STATE, "ALL-bucket call over buckets at different exchange parities");
-  for (int i = lo; i < hi; ++i) ctx->b[i].seq += 1;
-  const Dests dst = dests_of(ctx, ctx->b[lo]);
+  const uint64_t seq = ctx->b[lo].seq + 1;   // this exchange; committed once everything is enqueued
+  const Dests dst = dests_of(ctx, seq);
 
   const float* gbase = dev_grad;
   if (ctx->G > 1) {  // intra-cluster mean of the G GPUs' buckets -> this GPU's shard (R20)
-    Mark mk(L, PH_NCCL_RS);
-    CKN(ncclGroupStart());
-    for (int i = lo; i < hi; ++i) {
-      const BucketInfo& bk = ctx->b[i];
-      if (!bk.cn) continue;
-      const float* src = dev_grad + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
-      CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.coff, bk.cn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
-    }
-    CKN(ncclGroupEnd());
+    nebula_status s = intra_reduce_scatter(ctx, L, bucket, lo, hi, dev_grad, seq);
+    if (s != NEBULA_OK) return s;
     gbase = ctx->d_shard_in;
   }
   const bool vec = T.aligned && ((uintptr_t)gbase % 16 == 0);
   const Item* items = ctx->d_items[lay] + T.first;
+  const bool xscale = ctx->exact_scale && ctx->G > 1;
 
   switch (method) {
     case M_IDENTITY:
@@ -674,80 +989,29 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       else
         launch_fp16(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_flags);
       break;
-    case M_INT8: {
-      // zero the max-abs words of the items in this call (sidx = c * B + b)
-      {
-        Mark mk(L, PH_MEMSET);
-      if (bucket == NEBULA_ALL_BUCKETS) {
-        CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
-      } else {
-        for (int c = 0; c < ctx->Ploc; ++c)
-          CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
-      }
-      }
-      bool onchip = false;
-      const bool xscale = ctx->exact_scale && ctx->G > 1;
-      if (ctx->onchip_ok && !xscale) {
-        if (ctx->int8_kernel >= 2) onchip = true;
-        else if (ctx->int8_kernel == 0) onchip = elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20);
-      }
-      if (onchip) {
-        launch_int8_onchip(L, ef, vec, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
-                           ctx->d_bar, ctx->onchip_grid, ctx->onchip_smem,
-                           ctx->int8_kernel >= 2 ? ctx->int8_kernel - 2 : (vec ? 10 : 2) /* auto: warp-specialised TMA */);
-      } else {
-        launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-        if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
-        launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch,
-                          ctx->d_flags);
-      }
-      break;
-    }
-    case M_QSGD: {   // NEXT-4 (R32): max-abs pass, [cluster-wide max (R28)], stochastic-rounding pass
-      {
-        Mark mk(L, PH_MEMSET);
-        if (bucket == NEBULA_ALL_BUCKETS) {
-          CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
-        } else {
-          for (int c = 0; c < ctx->Ploc; ++c)
-            CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
-        }
-      }
+    case M_INT8:
+    case M_FP8:
+    case M_QSGD: {
+      // one per-bucket scale: max-abs words zeroed, then either the single-pass warp-specialised
+      // kernel (16-B aligned, buckets averaging >= 1M elements, no cluster-wide scale) or the
+      // max-abs pass, [the cluster-wide max (R28)], and the quantise pass
+      { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
+      const int kind = method == M_FP8 ? 1 : (method == M_QSGD ? 2 : 0);
       const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
-      if (ctx->onchip_ok && vec && !(ctx->exact_scale && ctx->G > 1) &&
-          (ctx->int8_kernel >= 2 ||
-           (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)))) {
-        launch_ws_compress(L, ef, 2, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar, sr);
+      // (SELF: auto never picks the cooperative kernel — group members' grids share one GPU)
+      const bool single = ctx->onchip_ok && vec && !xscale &&
+                          (ctx->int8_kernel == 2 ||
+                           (ctx->int8_kernel == 0 && !ctx->self &&
+                            elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)));
+      if (single) {
+        launch_ws_compress(L, ef, kind, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar, sr);
         break;
       }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-      if (ctx->exact_scale && ctx->G > 1) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
-      launch_qsgd_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, sr);
-      break;
-    }
-    case M_FP8: {   // NEXT-4 (R27): max-abs pass, [cluster-wide max (R28)], quantise pass
-      {
-        Mark mk(L, PH_MEMSET);
-        if (bucket == NEBULA_ALL_BUCKETS) {
-          CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
-        } else {
-          for (int c = 0; c < ctx->Ploc; ++c)
-            CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
-        }
-      }
-      const bool xscale = ctx->exact_scale && ctx->G > 1;
-      // single pass (warp-specialised TMA kernel) under the INT8 kernel's rule: buckets averaging
-      // >= 1M elements, 16-B aligned, not overridden to two-pass, no cluster-wide scale
-      if (ctx->onchip_ok && vec && !xscale &&
-          (ctx->int8_kernel >= 2 ||
-           (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)))) {
-        launch_ws_compress(L, ef, 1, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar,
-                           SrArgs{});
-        break;
-      }
-      launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-      if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket); if (xs != NEBULA_OK) return xs; }
-      launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
+      if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket, lo, hi, seq); if (xs != NEBULA_OK) return xs; }
+      if (kind == 1) launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
+      else if (kind == 2) launch_qsgd_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, sr);
+      else launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
       break;
     }
     case M_TOPK: {
@@ -759,6 +1023,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   }
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
+    ctx->b[i].seq = seq;
     ctx->b[i].state = ST_COMPRESSED;
     ctx->b[i].method = method;
   }
@@ -774,11 +1039,7 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
   DevGuard dg(ctx->device);
   if (ctx->xmode >= 2) {   // push: payloads already in our slots; pull: peers' own slots ready
     const Launch L = launch_of(ctx);
-    Peers pe{};
-    for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
-    pe.n = ctx->P;
-    pe.me = ctx->me;
-    launch_exchange_flags(L, pe, ctx->d_arrive, lo, hi, ctx->b[lo].seq, ctx->d_flags);
+    launch_exchange_flags(L, inter_peers(ctx), ctx->d_arrive, lo, hi, ctx->b[lo].seq, ctx->d_flags);
     CKC(cudaGetLastError());
   } else if (!ctx->loopback && ctx->P > 1) {
     const Launch L = launch_of(ctx);
@@ -835,15 +1096,8 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
     launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, sources_of(ctx, ctx->b[lo]), obase);
   CKC(cudaGetLastError());
   if (ctx->G > 1) {
-    Mark mk(L, PH_NCCL_AG);
-    CKN(ncclGroupStart());
-    for (int i = lo; i < hi; ++i) {
-      const BucketInfo& bk = ctx->b[i];
-      if (!bk.cn) continue;
-      float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
-      CKN(ncclAllGather(ctx->d_shard_out + bk.coff, dst, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
-    }
-    CKN(ncclGroupEnd());
+    nebula_status s = intra_all_gather(ctx, L, bucket, lo, hi, dev_out, ctx->b[lo].seq);
+    if (s != NEBULA_OK) return s;
   }
   for (int i = lo; i < hi; ++i) ctx->b[i].state = ST_IDLE;
   return NEBULA_OK;
@@ -864,6 +1118,8 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
     if (!(st == ST_EXCHANGED || (st == ST_COMPRESSED && own)))
       return fail(ctx, NEBULA_ERR_STATE, "decompress needs the slot's payload (compress / exchange first)");
   }
+  if (ctx->G > 1 && !ctx->intra)   // the shards are gathered with NCCL (no P2P sequence for this call)
+    return fail(ctx, NEBULA_ERR_UNSUPPORTED, "single-slot decompress with G > 1 needs the NCCL transport");
   DevGuard dg(ctx->device);
   const Launch L = launch_of(ctx);
   for (int i = lo; i < hi; ++i) {
@@ -899,18 +1155,18 @@ static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, 
                          uint64_t step) {
   const int m = method_at(ctx, step);
   if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD) || ctx->G != 1 || !ctx->onchip_ok) return false;
-  if (m == M_FP8 && ctx->step_fusion >= 2) return false;   // the tuning sweep is INT8 / QSGD only
+  // SELF: the peers' cooperative kernels share this GPU — two grid-wide kernels waiting on each
+  // other's flags could never be co-resident, so SELF always runs the staged stages
+  if (ctx->self) return false;
   // LOOPBACK, or P2P pull (the reduce warps load the peers' payloads); with P2P push the
   // compress kernel's NVLink stores are cheaper outside the fused kernel (fewer quantise warps)
   if (!(ctx->loopback || ctx->P == 1 || ctx->xmode == 3)) return false;
-  if (!(ctx->int8_kernel == 0 || ctx->int8_kernel == 12)) return false;
+  if (!(ctx->int8_kernel == 0 || ctx->int8_kernel == 2)) return false;
   if (ctx->int8_kernel == 0 && elems_of(ctx, lo, hi) < (uint64_t)(hi - lo) * (1ull << 20)) return false;
   const int lay = layout_of(ctx, M_INT8), t = bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket;
   const Table& T = ctx->ctab[lay][t];
   const Table& R = ctx->rtab[lay][t];
   if (!T.aligned || !R.aligned || (uintptr_t)g % 16 || (uintptr_t)out % 16) return false;
-  for (int i = lo + 1; i < hi; ++i)
-    if ((ctx->b[i].seq & 1) != (ctx->b[lo].seq & 1)) return false;   // the staged path reports it
   return true;
 }
 
@@ -921,30 +1177,23 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   const Table& T = ctx->ctab[lay][t];
   const Table& R = ctx->rtab[lay][t];
   const Launch L = launch_of(ctx);
-  for (int i = lo; i < hi; ++i) ctx->b[i].seq += 1;
-  {
-    Mark mk(L, PH_MEMSET);
-    if (bucket == NEBULA_ALL_BUCKETS) {
-      CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
-    } else {
-      for (int c = 0; c < ctx->Ploc; ++c)
-        CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
-    }
-  }
+  nebula_status st0 = stage_start(ctx, lo, hi);
+  if (st0 != NEBULA_OK) return st0;
+  const uint64_t seq = ctx->b[lo].seq + 1;
+  { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
   Peers pe{};
-  if (!ctx->loopback && ctx->P > 1) {
-    for (int c = 0; c < ctx->P; ++c) pe.arrive[c] = ctx->peer_arrive[c];
-    pe.n = ctx->P;
-    pe.me = ctx->me;
-  }
-  launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, ctx->b[lo]),
+  if (!ctx->loopback && ctx->P > 1) pe = inter_peers(ctx);
+  BucketInfo probe = ctx->b[lo];
+  probe.seq = seq;
+  launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, seq),
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
-                   sources_of(ctx, ctx->b[lo]), dev_out, pe, ctx->d_arrive, ctx->b[lo].seq,
+                   sources_of(ctx, probe), dev_out, pe, ctx->d_arrive, seq,
                    ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0),
                    method == M_FP8 ? 1 : (method == M_QSGD ? 2 : 0),
                    SrArgs{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()});
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
+    ctx->b[i].seq = seq;
     ctx->b[i].state = ST_IDLE;
     ctx->b[i].method = method;
   }
@@ -1083,8 +1332,8 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx) { return ctx ? ctx->launc
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if (option == NEBULA_OPT_INT8_KERNEL) {
-    if (value < 0 || value > 12) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 12]");
-    if (value >= 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8 ||
+    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 2]");
+    if (value == 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8 ||
                        ctx->codec.method == NEBULA_QSGD) && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;
@@ -1126,10 +1375,25 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? (ctx->P == 2 ? 2 : 3) : (int)value);
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_INTRA) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "intra option must be 0 or 1");
+    if (value == 1 && ctx->G > 1 && !ctx->intra)
+      return fail(ctx, NEBULA_ERR_UNSUPPORTED, "no intra-cluster NCCL communicator (SELF transport)");
+    for (const auto& bk : ctx->b)
+      if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the intra-cluster hop only between steps");
+    ctx->intra_opt = (int)value;
+    return NEBULA_OK;
+  }
   return fail(ctx, NEBULA_ERR_INVALID_ARG, "unknown option");
 }
 
 int32_t nebula_exchange_mode(const nebula_ctx* ctx) { return ctx ? ctx->xmode : -1; }
+
+int32_t nebula_intra_mode(const nebula_ctx* ctx) {
+  if (!ctx) return -1;
+  if (ctx->G == 1) return 0;
+  return intra_p2p_on(ctx) ? 2 : 1;
+}
 
 nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
@@ -1169,7 +1433,8 @@ const char* nebula_phase_name(uint32_t phase) {
       "topk_bracket", "topk_classify", "topk_resolve", "topk_fallback", "topk_merge_pack",
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
       "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
-      "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale", "qsgd_ef_quant_pack"};
+      "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale", "qsgd_ef_quant_pack",
+      "intra_rs_push", "intra_rs_reduce", "intra_ag_pull", "intra_scale_mail", "p2p_flags_intra_rs", "p2p_flags_intra_ag"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

@@ -4,7 +4,9 @@
 Every rank is one GPU of cluster rank // G.  Each step every rank regenerates ALL ranks'
 seeded gradients on the host (gradgen), runs the C-ABI step on its own, and checks:
   * its output is bit-identical to the oracle (flat P x 1: oracle_step; G > 1:
-    hierarchical_step on dyadic inputs whose fp32 cluster mean is exact in any order),
+    hierarchical_step — on model-like (non-dyadic) inputs when the intra-cluster hop is the
+    fixed-order P2P reduce-scatter, on dyadic inputs (mean exact in any order) for the NCCL
+    ReduceScatter(avg) fallback, whose summation order is NCCL's),
   * its own payload slot and residual are bit-identical to the oracle's,
   * all ranks' outputs are bit-identical (all-gathered and compared on every rank).
 Prints "DIST OK ..." on rank 0 and exits 0, else raises.
@@ -44,16 +46,20 @@ def main():
     P, cl, lr = nb.topology_for_rank(rank, world, G)
     sizes = [4096 * G, 12288 * G, 300004 * G, 8 * G]
     total = sum(sizes)
-    # (method, top-k values, INT8 kernel, exact cluster-wide scale (NEXT-3, only meaningful for G > 1))
-    cases = [(O.INT8, 0, "two-pass", False), (O.INT8, 0, "onchip", False), (O.INT8, 0, "fused-ws", False),
-             (O.FP16, 0, None, False), (O.IDENTITY, 0, None, False), (O.FP8, 0, None, False), (O.QSGD, 0, None, False),
-             (O.TOPK, O.VAL_F32, None, False), (O.TOPK, O.VAL_I8, None, False), (O.TOPK, O.VAL_F16, None, False),
-             (O.FP8, 0, "fused-ws", False), (O.QSGD, 0, "fused-ws", False)]   # fused step over P2P (G = 1)
+    # (method, top-k values, INT8 kernel, exact cluster-wide scale (NEXT-3, only meaningful for G > 1),
+    #  intra-cluster hop for G > 1: "p2p" (auto) or "nccl")
+    cases = [(O.INT8, 0, "two-pass", False, "p2p"), (O.INT8, 0, "fused-ws", False, "p2p"),
+             (O.FP16, 0, None, False, "p2p"), (O.IDENTITY, 0, None, False, "p2p"), (O.FP8, 0, None, False, "p2p"),
+             (O.QSGD, 0, None, False, "p2p"), (O.TOPK, O.VAL_F32, None, False, "p2p"),
+             (O.TOPK, O.VAL_I8, None, False, "p2p"), (O.TOPK, O.VAL_F16, None, False, "p2p"),
+             (O.FP8, 0, "fused-ws", False, "p2p"), (O.QSGD, 0, "fused-ws", False, "p2p")]   # fused step over P2P (G = 1)
     if G > 1:
-        cases += [(O.INT8, 0, None, True), (O.FP8, 0, None, True)]
+        cases += [(O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"),
+                  (O.TOPK, O.VAL_F32, None, False, "nccl"), (O.INT8, 0, None, True, "nccl")]
+    intra_seen = set()
     modes_seen = set()
     modes = ((False, "pull"), (True, "pull"), (False, "push"), (True, "push"), (False, "nccl"))
-    for ci, (method, vt, kern, exact) in enumerate(cases):
+    for ci, (method, vt, kern, exact, intra) in enumerate(cases):
         # INT8 (the default codec) runs every (call shape, exchange) mode; the other cases rotate
         # through two modes each, so every mode is still met by several codecs at a fraction of
         # the oracle time (each rank recomputes every cluster's oracle step)
@@ -65,6 +71,10 @@ def main():
                 ctx.set_int8_kernel(kern)
             if exact:
                 ctx.set_exact_scale(True)
+            if G > 1:
+                ctx.set_intra(intra)
+            exact_order = ctx.intra_mode() != "nccl"   # fixed-order P2P mean: any input is exact
+            intra_seen.add(ctx.intra_mode())
             if P > 1:
                 try:
                     ctx.set_exchange(xch)
@@ -78,7 +88,7 @@ def main():
             for t in range(args.steps):
                 # gradient of (cluster c, gpu l, bucket b)
                 def grad(c, l, b):
-                    if G > 1:
+                    if G > 1 and not exact_order:
                         return dyadic(sizes[b], seed_for(c, l, t, salt=b))
                     return synthetic(sizes[b], seed_for(c, l, t, salt=b), "model-like")
                 mine = np.concatenate([grad(cl, lr, b) for b in range(len(sizes))])
@@ -126,11 +136,12 @@ def main():
                         for c in range(P):
                             assert ctx.payload_copy(b, c) == payloads[c], f"slot {c} mismatch b{b}"
                     off += n
+            dist.barrier()          # nebula_sync_destroy is collective with peer mappings
             ctx.destroy()
     dist.barrier()
     if rank == 0:
         print(f"DIST OK world={world} P={P} G={G} cases={len(cases)} steps={args.steps} "
-              f"exchange={sorted(modes_seen)}", flush=True)
+              f"exchange={sorted(modes_seen)} intra={sorted(intra_seen)}", flush=True)
     dist.destroy_process_group()
 
 

@@ -54,6 +54,9 @@ def test_abi_version_and_status_strings(lib):
     (dict(transport=nb.NCCL, unique_id=b"\0" * 128, cluster_id=2), "cluster_id"),
     (dict(transport=nb.NCCL, unique_id=b"\0" * 128, gpus_per_cluster=2, local_rank=2), "local_rank"),
     (dict(device=-1), "device"),
+    (dict(transport=nb.SELF), "nccl_unique_id"),
+    (dict(transport=nb.SELF, unique_id=b"\1" * 128, gpus_per_cluster=9, local_rank=0), "gpus_per_cluster"),
+    (dict(transport=nb.SELF, unique_id=b"\1" * 128, cluster_id=3), "cluster_id"),
 ])
 def test_validation_rejects_before_cuda(lib, kwargs, needle):
     with pytest.raises(nb.NebulaError) as e:

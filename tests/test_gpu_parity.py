@@ -31,7 +31,7 @@ def bits(a):
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
                  start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
-                 fp16_kernel=None, sr_seed=0, topk_reduce=None):
+                 fp16_kernel=None, sr_seed=0, topk_reduce=None, step_config=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
@@ -42,6 +42,8 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
             ctx.set_step_fusion(False)
     if fp16_kernel:
         ctx.set_fp16_kernel(fp16_kernel)
+    if step_config is not None:                      # fused-step warp split (NEBULA_OPT_STEP_FUSION)
+        ctx.set_option(nb.OPT_STEP_FUSION, 2 + step_config)
     if sr_seed:
         ctx.set_sr_seed(sr_seed)
     if topk_reduce is not None:
@@ -116,9 +118,7 @@ def test_dense_parity(nb, method, P, sizes):
     assert run_loopback(nb, method, sizes, P) > 0
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-recompute", "fused-park-lag1",
-                                         "fused-recompute-lag1", "fused-split", "fused-smem", "fused-tma",
-                                         "fused-ws", "fused-ws-staged"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "auto", "fused-ws", "fused-ws-staged"])
 @pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [9_000_003]])
 @pytest.mark.parametrize("ef", [True, False])
 def test_int8_kernels(nb, int8_kernel, sizes, ef):
@@ -127,8 +127,7 @@ def test_int8_kernels(nb, int8_kernel, sizes, ef):
     run_loopback(nb, O.INT8, sizes, 2, steps=2, ef=ef, int8_kernel=int8_kernel)
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-park-lag1", "fused-smem", "fused-tma", "fused-ws",
-                                         "fused-ws-staged"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-ws", "fused-ws-staged"])
 def test_int8_near_half_integer_quotients(nb, int8_kernel):
     # exercises the exact fallback of the reciprocal-multiply fast path (int8_q_fast)
     run_loopback(nb, O.INT8, [50001, 4096], 2, kind="half-ties", steps=1, ef=False, int8_kernel=int8_kernel)
@@ -142,6 +141,18 @@ def test_int8_fused_step(nb, P, per_bucket):
     # schedules of the reduce warps), whole-group / ragged / tiny buckets, ALL and per bucket
     run_loopback(nb, O.INT8, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003], P, steps=3, per_bucket=per_bucket,
                  int8_kernel="fused-ws")
+
+
+@pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD])
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_pull_reducer_in_fused_step(nb, method, P, per_bucket):
+    """The P2P-pull reduce role of the fused step (ws_reduce_ld: 16-B register loads of every
+    cluster's payload, both tree-sum schedules: P <= 4 and the two-subtree P > 4 branch) runs
+    here on one GPU: LOOPBACK with warp split 4 (the pull default), the peers' slots being the
+    local slot buffer.  Bit-exact vs the oracle, ragged / tiny / multi-group buckets."""
+    run_loopback(nb, method, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003], P, steps=3, per_bucket=per_bucket,
+                 int8_kernel="fused-ws", step_config=4, sr_seed=7 if method == O.QSGD else 0)
 
 
 def test_int8_fused_step_is_one_launch(nb):
@@ -313,8 +324,7 @@ def test_nonfinite_is_reported(nb, method, bad):
     ctx.destroy()
 
 
-@pytest.mark.parametrize("int8_kernel", ["two-pass", "onchip", "fused-split", "fused-smem", "fused-tma",
-                                         "fused-ws"])
+@pytest.mark.parametrize("int8_kernel", ["two-pass", "fused-ws"])
 def test_int8_nonfinite_writes_nothing(nb, int8_kernel):
     import torch
     ctx = nb.SyncContext([1000], nb.INT8, num_clusters=1, transport=nb.LOOPBACK)
