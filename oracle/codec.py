@@ -13,6 +13,8 @@ Per cluster c, per bucket of n fp32 elements, step t (SURVEY.md §8(c) plain def
            q = clamp(rint(fl(p/s)), -127, 127);  D = fl(q*s)
     FP8  : m = max|p|, s = fl(m/448) (s := 1 if m == 0 or s == 0)    PAPER.md:101 "8-bit floating point" (R27)
            c = RNE_E4M3_satfinite(fl(p/s));  D = fl(E4M3(c)*s)
+    E5M2 : the same with OFP8 E5M2 (max 57344): s = fl(m/57344)      PAPER.md:101 (R33)
+           c = RNE_E5M2_satfinite(fl(p/s));  D = fl(E5M2(c)*s)
     QSGD : INT8's s; x = fl(p/s); q = floor(x) + [u < x - floor(x)]  PAPER.md:63 (QSGD cited; R32)
            u = counter-based SplitMix64 uniform of (seed, step, cluster, bucket, shard, e)
     TOPK : k largest |p| by fp32 bit key, ties -> lower index,        PAPER.md:63, :99 (cited only; R11-R14)
@@ -38,11 +40,13 @@ __all__ = [
     "hierarchical_step", "svd_ratio", "FP16_OVERFLOW_ABS", "FP8",
     "fp8_e4m3_encode", "fp8_e4m3_decode", "fp8_scale", "FP8_E4M3_MAX",
     "QSGD", "splitmix64", "qsgd_uniforms", "qsgd_quantize",
+    "FP8_E5M2", "FP8_E5M2_MAX", "fp8_e5m2_encode", "fp8_e5m2_decode",
 ]
 
 F32 = np.float32
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 QSGD = 6                     # INT8 levels with stochastic rounding (R32); 5 = the SVD payload id
+FP8_E5M2 = 7                 # OFP8 E5M2 reading of "8-bit floating point" (R33)
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 VALUE_BYTES = {VAL_F32: 4, VAL_F16: 2, VAL_I8: 1}
 NONFINITE, OVERFLOW = "NONFINITE", "OVERFLOW"
@@ -55,6 +59,10 @@ FP16_OVERFLOW_ABS = 65520.0
 # R27 (NEXT-4): OCP FP8 E4M3 ("E4M3FN"): 1 sign, 4 exponent bits (bias 7), 3 mantissa bits,
 # no infinities, S.1111.111 = NaN, so the largest finite magnitude is 1.75 * 2^8 = 448.
 FP8_E4M3_MAX = 448.0
+
+# R33 (NEXT-4): OCP FP8 E5M2: 1 sign, 5 exponent bits (bias 15), 2 mantissa bits, IEEE-style
+# infinities (S.11111.00) and NaNs, so the largest finite magnitude is 1.75 * 2^15 = 57344.
+FP8_E5M2_MAX = 57344.0
 
 
 class NebulaError(Exception):
@@ -106,7 +114,7 @@ def payload_bytes(method: int, n: int, k: int = 0, value_type: int = VAL_F32) ->
         return 16 + pad16(4 * n)
     if method == FP16:
         return 16 + pad16(2 * n)
-    if method in (INT8, FP8, QSGD):
+    if method in (INT8, FP8, QSGD, FP8_E5M2):
         return 16 + pad16(n)
     if method == TOPK:
         return 16 + pad16(4 * k) + pad16(VALUE_BYTES[value_type] * k)
@@ -120,7 +128,7 @@ def body_ratio(method: int, n: int, k: int = 0, value_type: int = VAL_F32) -> fl
         b = 4 * n
     elif method == FP16:
         b = 2 * n
-    elif method in (INT8, FP8, QSGD):
+    elif method in (INT8, FP8, QSGD, FP8_E5M2):
         b = n
     else:
         b = (4 + VALUE_BYTES[value_type]) * k
@@ -172,13 +180,13 @@ def int8_dequantize(q: np.ndarray, s: np.float32) -> np.ndarray:
     return q.astype(F32) * F32(s)
 
 
-def fp8_scale(p: np.ndarray) -> np.float32:
-    """R27: per-bucket symmetric scale mapping max|p| onto the largest finite E4M3 magnitude,
-    s = fl(m / 448); s := 1 if m == 0 or if fl(m/448) underflows to 0 (the INT8 rule R4 with
-    448 in place of 127)."""
+def fp8_scale(p: np.ndarray, fmax: float = FP8_E4M3_MAX) -> np.float32:
+    """R27 / R33: per-bucket symmetric scale mapping max|p| onto the largest finite FP8
+    magnitude (448 for E4M3, 57344 for E5M2), s = fl(m / fmax); s := 1 if m == 0 or if
+    fl(m / fmax) underflows to 0 (the INT8 rule R4 with fmax in place of 127)."""
     m = np.max(np.abs(p)) if p.size else F32(0.0)
     m = F32(m)
-    s = F32(m / F32(FP8_E4M3_MAX))
+    s = F32(m / F32(fmax))
     if m == F32(0.0) or s == F32(0.0):
         s = F32(1.0)
     return s
@@ -215,6 +223,41 @@ def fp8_e4m3_decode(c: np.ndarray) -> np.ndarray:
     ef, mf = (c >> 3) & 0xF, c & 0x7
     v = np.where(ef == 0, mf * 2.0 ** -9, (8 + mf) * np.ldexp(1.0, ef - 10))
     v = np.where((ef == 0xF) & (mf == 0x7), np.nan, v)
+    return (s * v).astype(F32)
+
+
+def fp8_e5m2_encode(x: np.ndarray) -> np.ndarray:
+    """R33: binary32 -> E5M2 code bytes, round to nearest, ties to even mantissa, saturating to
+    +-57344 (the satfinite conversion: magnitudes that would round to infinity give the largest
+    finite code); the sign is kept, also when the value rounds to zero.  From the format's
+    definition, in float64 (exact for binary32 inputs): the quantum of the binade holding |x| is
+    2^(max(e, -14) - 2) (-14 = the smallest normal exponent; subnormal quantum 2^-16)."""
+    x = np.asarray(x, dtype=F32).ravel()
+    if x.size and np.any(np.isnan(x)):
+        raise NebulaError(NONFINITE, "NaN has no saturating E5M2 code")
+    a = np.abs(x.astype(np.float64))
+    sign = np.where(np.signbit(x), 0x80, 0).astype(np.int64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        e = np.frexp(np.minimum(a, 2.0 ** 20))[1].astype(np.int64) - 1
+        quantum = np.ldexp(1.0, np.maximum(e, -14) - 2)
+        v = np.rint(np.minimum(a, 2.0 ** 20) / quantum) * quantum     # RNE on the exact quotient
+    v = np.minimum(v, FP8_E5M2_MAX)                                   # satfinite
+    ev = np.frexp(v)[1].astype(np.int64) - 1
+    normal = v >= 2.0 ** -14
+    code_sub = (v / 2.0 ** -16).astype(np.int64)                      # 0.mm * 2^-14
+    code_norm = ((ev + 15) << 2) | ((v / np.ldexp(1.0, ev - 2)).astype(np.int64) - 4)
+    code = np.where(normal, code_norm, code_sub)
+    code = np.where(a == 0.0, 0, code)
+    return (sign | code).astype(np.uint8)
+
+
+def fp8_e5m2_decode(c: np.ndarray) -> np.ndarray:
+    """E5M2 code bytes -> binary32 (exact); exponent field 31 holds +-inf (mantissa 0) / NaN."""
+    c = np.asarray(c, dtype=np.uint8).ravel().astype(np.int64)
+    s = np.where(c & 0x80, -1.0, 1.0)
+    ef, mf = (c >> 2) & 0x1F, c & 0x3
+    v = np.where(ef == 0, mf * 2.0 ** -16, (4 + mf) * np.ldexp(1.0, ef - 17))
+    v = np.where(ef == 0x1F, np.where(mf == 0, np.inf, np.nan), v)
     return (s * v).astype(F32)
 
 
@@ -352,6 +395,12 @@ def compress(p: np.ndarray, method: int, codec: Codec, scale=None, uniforms=None
         c = fp8_quantize(p, s)
         return (_preamble(FP8, n, float(s), 0) + _pad(c.tobytes()),
                 fp8_dequantize(c, s), {"scale": float(s)})
+    if method == FP8_E5M2:
+        # R33: s = fl(m / 57344); c = RNE_E5M2_satfinite(fl(p / s)); D = fl(E5M2(c) * s)
+        s = fp8_scale(p, FP8_E5M2_MAX) if scale is None else F32(scale)
+        c = fp8_e5m2_encode((p / F32(s)).astype(F32))
+        return (_preamble(FP8_E5M2, n, float(s), 0) + _pad(c.tobytes()),
+                (fp8_e5m2_decode(c) * F32(s)).astype(F32), {"scale": float(s)})
     if method == TOPK:
         k = topk_k(n, codec)
         idx = topk_select(p, k)
@@ -391,6 +440,8 @@ def decode_payload(payload: bytes, n: int) -> np.ndarray:
         return int8_dequantize(q, F32(scale))
     if method == FP8:
         return fp8_dequantize(np.frombuffer(body, dtype=np.uint8, count=n), F32(scale))
+    if method == FP8_E5M2:
+        return (fp8_e5m2_decode(np.frombuffer(body, dtype=np.uint8, count=n)) * F32(scale)).astype(F32)
     if method == QSGD:
         return int8_dequantize(np.frombuffer(body, dtype=np.int8, count=n), F32(scale))
     if method == TOPK:
@@ -490,13 +541,14 @@ def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: 
             shards[c][l] = (acc / F32(G)).astype(F32)
     scales = [None] * P
     method = select_method(codec, step)
-    if exact_scale and method in (INT8, FP8, QSGD):
+    if exact_scale and method in (INT8, FP8, QSGD, FP8_E5M2):
         for c in range(P):
             ps = [shards[c][l] if not codec.error_feedback else
                   (shards[c][l] + (np.zeros(m, F32) if rs[c][l] is None else np.asarray(rs[c][l], F32))).astype(F32)
                   for l in range(G)]
             p_c = np.concatenate(ps)
-            scales[c] = fp8_scale(p_c) if method == FP8 else int8_scale(p_c)
+            scales[c] = (fp8_scale(p_c) if method == FP8 else
+                         fp8_scale(p_c, FP8_E5M2_MAX) if method == FP8_E5M2 else int8_scale(p_c))
     for l in range(G):
         out_l, r_l, p_l, _ = oracle_step([shards[c][l] for c in range(P)], [rs[c][l] for c in range(P)], codec, step,
                                          scales, bucket, l)

@@ -590,3 +590,88 @@ def test_qsgd_payload_layout_and_ratio():
     assert O.body_ratio(O.QSGD, 1001) == 0.25
     # one quantum: |p - D| < s
     assert np.all(np.abs(g.astype(np.float64) - D) < float(st["scale"]) * (1 + 2.0 ** -20))
+
+
+# ----------------------------------------------------------------- FP8 E5M2 (NEXT-4, R33)
+def test_e5m2_textbook_encodings():
+    g = gold("fp8_e5m2.json")
+    for case in g["cases"]:
+        x = np.array([float(case["x"])], F32)
+        code = int(O.fp8_e5m2_encode(x)[0])
+        assert code == int(case["code"], 16), case
+    # the 123 positive finite codes decode to strictly increasing values ending at 57344;
+    # exponent field 31 holds infinity (mantissa 0) and NaNs
+    vals = O.fp8_e5m2_decode(np.arange(0, 124, dtype=np.uint8)).astype(np.float64)
+    assert vals[0] == 0.0 and vals[-1] == 57344.0 and np.all(np.diff(vals) > 0)
+    assert np.isinf(O.fp8_e5m2_decode(np.array([0x7C, 0xFC], np.uint8))).all()
+    assert np.isnan(O.fp8_e5m2_decode(np.array([0x7D, 0x7E, 0x7F, 0xFF], np.uint8))).all()
+
+
+def test_e5m2_matches_library_conversion():
+    """Against an independent implementation: PyTorch's float8_e5m2 cast (RNE; it overflows to
+    infinity instead of saturating, so inputs stay below the 61440 rounding boundary)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(6)
+    x = (rng.standard_normal(400000) * np.exp(rng.uniform(-20, 11, 400000))).astype(F32)
+    x = x[np.abs(x) < 61440]
+    assert np.array_equal(O.fp8_e5m2_encode(x), torch.from_numpy(x).to(torch.float8_e5m2).view(torch.uint8).numpy())
+    # every midpoint between neighbouring E5M2 magnitudes, and its binary32 neighbours
+    vals = O.fp8_e5m2_decode(np.arange(0, 124, dtype=np.uint8)).astype(np.float64)
+    mids = ((vals[:-1] + vals[1:]) / 2).astype(F32)
+    for m in (mids, np.nextafter(mids, F32(np.inf)), np.nextafter(mids, F32(0))):
+        xm = np.concatenate([m, -m]).astype(F32)
+        assert np.array_equal(O.fp8_e5m2_encode(xm), torch.from_numpy(xm).to(torch.float8_e5m2).view(torch.uint8).numpy())
+    fin = np.arange(0, 256, dtype=np.uint8)
+    v = O.fp8_e5m2_decode(fin)
+    ok = np.isfinite(v)
+    assert np.array_equal(O.fp8_e5m2_decode(O.fp8_e5m2_encode(v[ok])), v[ok])
+
+
+@pytest.mark.parametrize("kind", ["normal", "model-like", "uniform", "ties", "mixed-scale", "subnormal"])
+def test_e5m2_exact_rational_properties(kind):
+    """R33 in the rationals: s = m/57344 correctly rounded; c = nearest E5M2 value of t = fl(p/s)
+    (ties to an even mantissa); D = c*s correctly rounded."""
+    g = synthetic(3000, 14, kind)
+    payload, D, st = O.compress(g, O.FP8_E5M2, O.Codec(method=O.FP8_E5M2))
+    s = F32(st["scale"])
+    m = Fraction(float(np.max(np.abs(g))))
+    if m != 0 and float(s) != 1.0:
+        exact, sf = m / 57344, Fraction(float(s))
+        for nb in (np.nextafter(s, F32(np.inf)), np.nextafter(s, F32(0))):
+            assert abs(sf - exact) <= abs(Fraction(float(nb)) - exact)
+    table = [Fraction(float(v)) for v in O.fp8_e5m2_decode(np.arange(0, 124, dtype=np.uint8))]
+    codes = np.frombuffer(payload, dtype=np.uint8, offset=16, count=g.size)
+    sF = Fraction(float(s))
+    for i in range(0, g.size, 11):
+        t = Fraction(float(F32(g[i]) / s))
+        c = int(codes[i])
+        mag = c & 0x7F
+        assert (c >> 7) == int(np.signbit(g[i]))
+        best = min(abs(abs(t) - v) for v in table)
+        assert abs(abs(t) - table[mag]) == best
+        if sum(1 for v in table if abs(abs(t) - v) == best) > 1:
+            assert mag % 2 == 0
+        d = Fraction(float(D[i]))
+        prod = (-1 if c >> 7 else 1) * table[mag] * sF
+        assert abs(d - prod) <= max(abs(prod) * Fraction(1, 2 ** 24), Fraction(1, 2 ** 150))
+
+
+def test_e5m2_ratio_error_bound_and_residual_identity():
+    """PAPER.md:101 (body n bytes -> ratio 0.25, a 75 % reduction); E5M2's relative error 2^-3
+    in the normal range (2^-17 * s absolute below); p == D + r_new bit for bit."""
+    t5 = gold("table5_ratios.json")
+    for n in (1, 17, 4096):
+        assert 1.0 - O.body_ratio(O.FP8_E5M2, n) == t5["int8_traffic_reduction"]
+        assert O.payload_bytes(O.FP8_E5M2, n) == 16 + math.ceil(n / 16) * 16
+    g = synthetic(20000, 15, "model-like")
+    _, D, st = O.compress(g, O.FP8_E5M2, O.Codec(method=O.FP8_E5M2))
+    s = float(st["scale"])
+    err = np.abs(g.astype(np.float64) - D.astype(np.float64))
+    assert np.all(err <= np.maximum(np.abs(g.astype(np.float64)) * 2.0 ** -3, s * 2.0 ** -17) * (1 + 2.0 ** -10))
+    for kind in ("normal", "zipf-rows", "subnormal", "signed-zero", "zeros"):
+        g = synthetic(5000, 25, kind)
+        r0 = synthetic(5000, 26, "normal", sigma=1e-3) if kind != "zeros" else np.zeros(5000, F32)
+        res = O.cluster_step(g, r0, O.Codec(method=O.FP8_E5M2), step=1)
+        assert np.array_equal((res.D + res.r_new).astype(F32), (g + r0).astype(F32))
+    _, D, st = O.compress(np.zeros(33, F32), O.FP8_E5M2, O.Codec(method=O.FP8_E5M2))
+    assert st["scale"] == 1.0 and np.all(D == 0)
