@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METHODS = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3, "fp8": 4, "qsgd": 6}
+METHODS = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3, "fp8": 4, "qsgd": 6, "fp8e5m2": 7}
 VALUES = {"f32": 0, "f16": 1, "i8": 2}
 VB = {0: 4, 1: 2, 2: 1}
 METRIC = "GB/s fp32 gradient synced per GPU (1/2/4/8 B200); % HBM roofline"
@@ -121,7 +121,7 @@ def kernel_bytes(phase, method, vt, P, ef, n_elems, k_total):
 def reduce_bytes(method, vt, P, n_out, k_per_cluster):
     if method == 3:
         return P * k_per_cluster * (4 + VB[vt]) + 4 * n_out
-    b = {0: 4, 1: 2, 2: 1, 4: 1, 6: 1}[method]
+    b = {0: 4, 1: 2, 2: 1, 4: 1, 6: 1, 7: 1}[method]
     return P * b * n_out + 4 * n_out
 
 
@@ -260,7 +260,7 @@ def run_reference(args):
 
 def workload_config(args, n, P, G=1):
     mname = {0: "identity", 1: "fp16+ef", 2: "int8+ef", 3: f"topk{args.density:g}-{args.values}+ef",
-             4: "fp8e4m3+ef", 6: "qsgd-int8-sr+ef"}[METHODS[args.method]]
+             4: "fp8e4m3+ef", 6: "qsgd-int8-sr+ef", 7: "fp8e5m2+ef"}[METHODS[args.method]]
     if args.exact_scale and G > 1:
         mname += "+exact-cluster-scale"
     if args.no_ef:
@@ -471,7 +471,7 @@ def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):
     """Minimum HBM bytes of one step on one GPU."""
     e = 4 if ef else 0
     clusters_here = P if world == 1 else 1
-    if method in (2, 4, 6):   # single pass (warp-specialised kernel / fused step) for INT8, FP8, QSGD
+    if method in (2, 4, 6, 7):   # single pass (warp-specialised kernel / fused step) for INT8, FP8, QSGD
         comp = (4 + e + e + 1) * n
     elif method == 1:
         comp = (4 + e + e + 2) * n
@@ -479,7 +479,7 @@ def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):
         comp = 8 * n
     else:
         comp = (4 + e + e) * n + k_per_cluster * (4 + VB[vt]) + (4 * k_per_cluster if ef else 0)
-    exch = 0 if world == 1 else 2 * (P - 1) * (n * {0: 4, 1: 2, 2: 1, 4: 1, 6: 1}.get(method, 0) + (k_per_cluster * (4 + VB[vt]) if method == 3 else 0))
+    exch = 0 if world == 1 else 2 * (P - 1) * (n * {0: 4, 1: 2, 2: 1, 4: 1, 6: 1, 7: 1}.get(method, 0) + (k_per_cluster * (4 + VB[vt]) if method == 3 else 0))
     red = reduce_bytes(method, vt, P, n, k_per_cluster)
     return clusters_here * comp + exch + red
 

@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties", "int-ties")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties", "e5m2-ties", "int-ties")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -221,6 +221,24 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
         grid = np.array(grid[:-1] + [480.0])            # 448 is the last finite; 480 marks the 464 boundary
         mids = (grid[:-1] + grid[1:]) / 2.0
         g = (mids[rng.integers(0, mids.size, size=n)] / 448.0).astype(np.float32)
+        g *= np.where(rng.random(n) < 0.5, -1.0, 1.0).astype(np.float32)
+        steps = rng.integers(-3, 4, size=n)
+        for d in (-3, -2, -1, 1, 2, 3):
+            sel = steps == d
+            toward = np.float32(np.inf) if d > 0 else np.float32(-np.inf)
+            for _ in range(abs(d)):
+                g[sel] = np.nextafter(g[sel], toward)
+        g = np.clip(g, -1.0, 1.0).astype(np.float32)
+        g[0] = np.float32(1.0)
+        return g
+    if kind == "e5m2-ties":
+        # max |g| = 1 and every other value within a few ulps of (midpoint between two
+        # neighbouring E5M2 magnitudes) / 57344 (the E5M2 analogue of "fp8-ties")
+        grid = [mm * 2.0 ** -16 for mm in range(4)] + \
+               [(4 + mm) * 2.0 ** (ee - 17) for ee in range(1, 31) for mm in range(4)]
+        grid = np.array(grid + [65536.0])              # 57344 is the last finite; 65536 marks 61440
+        mids = (grid[:-1] + grid[1:]) / 2.0
+        g = (mids[rng.integers(0, mids.size, size=n)] / 57344.0).astype(np.float32)
         g *= np.where(rng.random(n) < 0.5, -1.0, 1.0).astype(np.float32)
         steps = rng.integers(-3, 4, size=n)
         for d in (-3, -2, -1, 1, 2, 3):

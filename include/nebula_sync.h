@@ -25,7 +25,7 @@
  *
  * Payload body (R18): 16-byte preamble {u32 method, u32 count (n or k), f32 scale (1.0 if
  * unused), u32 aux (TOPK value type, else 0)}, then sections zero-padded to 16 bytes:
- * IDENTITY f32[n] | FP16 binary16[n] | INT8 / QSGD int8[n] | FP8 E4M3 u8[n] | TOPK u32 idx[k] (ascending) then
+ * IDENTITY f32[n] | FP16 binary16[n] | INT8 / QSGD int8[n] | FP8 E4M3 / E5M2 u8[n] | TOPK u32 idx[k] (ascending) then
  * val[k] (f32 | binary16 | int8).  All little-endian.  Identical on every transport.
  *
  * Conventions for every entry point:
@@ -86,8 +86,11 @@ typedef enum {
  * h_j = sm(base + j * 0x9E3779B97F4A7C15), u_{2j} = (h_j >> 40) * 2^-24,
  * u_{2j+1} = ((h_j >> 16) & 0xFFFFFF) * 2^-24.  E[D] = p (unbiased).
  * (5 is the FP16(SVD) payload id, not a bucket method.) */
+/* NEBULA_FP8_E5M2 (NEXT-4; R33): OCP E5M2, s = fl(max|p| / 57344) (R4 rules),
+ * code = RNE-to-E5M2(fl(p / s)) saturating at +-57344 (never an infinity code),
+ * D = fl(E5M2(code) * s).  Body: u8[n]. */
 typedef enum { NEBULA_IDENTITY = 0, NEBULA_FP16 = 1, NEBULA_INT8 = 2, NEBULA_TOPK = 3, NEBULA_FP8 = 4,
-               NEBULA_QSGD = 6 } nebula_method;
+               NEBULA_QSGD = 6, NEBULA_FP8_E5M2 = 7 } nebula_method;
 typedef enum { NEBULA_VAL_F32 = 0, NEBULA_VAL_F16 = 1, NEBULA_VAL_I8 = 2 } nebula_value_type;
 /* Transports.  NCCL: one process per GPU (torchrun); peers' buffers are mapped with CUDA IPC
  * when every rank can reach every peer (NVLink), else NCCL collectives move the bytes.
@@ -228,7 +231,7 @@ nebula_status nebula_topk_stats(nebula_ctx* ctx, int32_t bucket, int32_t cluster
 uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 
 /* Tuning knobs (results are bit-identical whichever kernel runs).
- *   NEBULA_OPT_INT8_KERNEL (INT8, FP8 and QSGD): 0 auto (default), 1 two-pass streaming
+ *   NEBULA_OPT_INT8_KERNEL (INT8, FP8 E4M3 / E5M2 and QSGD): 0 auto (default), 1 two-pass streaming
  *   (max-abs pass + quantise pass, 21 B/elem of HBM traffic), 2 single pass: the
  *   warp-specialised TMA kernel (cooperative grid of one CTA per SM: a producer warp feeding
  *   two cp.async.bulk rings, max/park warps, quantise warps; 13 B/elem algorithmic; needs

@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "QSGD", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK", "SELF",
+    "IDENTITY", "FP16", "INT8", "TOPK", "FP8", "QSGD", "FP8_E5M2", "VAL_F32", "VAL_F16", "VAL_I8", "NCCL", "LOOPBACK", "SELF",
     "ALL_BUCKETS", "NebulaError", "load", "lib_path", "get_unique_id", "SyncContext", "TopkInfo",
     "status_string", "abi_version", "HEADER", "SvdCodec", "SVD_FP16",
 ]
@@ -25,6 +25,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "nebula_sync.h")
 
 IDENTITY, FP16, INT8, TOPK, FP8 = 0, 1, 2, 3, 4
 QSGD = 6
+FP8_E5M2 = 7
 VAL_F32, VAL_F16, VAL_I8 = 0, 1, 2
 NCCL, LOOPBACK, SELF = 0, 1, 2
 SVD_FP16 = 5   # payload method id of the FP16(SVD(rho)) compressor (R31)

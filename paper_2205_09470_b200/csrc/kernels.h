@@ -46,6 +46,16 @@ struct Mark {
   ~Mark() { if (L.mark) L.mark(L.mctx, ph, 1); }
 };
 
+// Load every kernel of the library into the current device's context (called by
+// nebula_sync_init).  CUDA's lazy loading would otherwise load a kernel at its first launch,
+// which may wait for the kernels already running — and the P2P flag kernels spin until a peer
+// (another stream or process) runs: a launch-time load behind such a spin can deadlock.
+void preload_kernels();
+void preload_dense();
+void preload_ws();
+void preload_intra();
+void preload_topk();
+
 // ---- dense codecs (kernels_dense.cu) ----
 // IDENTITY: payload <- g (+ non-finite check).  Residual untouched (R15).
 void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks,
@@ -62,14 +72,15 @@ void launch_absmax(const Launch& L, bool ef, bool vec, const Item* items, int ni
 // INT8 pass 2: scale from scratch, quantize + pack, r <- p - q*s.
 void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
-// FP8 E4M3 pass 2 (NEXT-4): scale fl(m/448) from scratch, quantise + pack, r <- p - D.
+// FP8 pass 2 (NEXT-4): fmt 1 = E4M3 (scale fl(m/448)), 2 = E5M2 (fl(m/57344)); quantise + pack,
+// r <- p - D.
 void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
-                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags);
+                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags, int fmt);
 // QSGD pass 2 (NEXT-4, R32): INT8 scale, stochastic rounding with counter-based uniforms.
 void launch_qsgd_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags,
                        const SrArgs& sr);
-// INT8 (kind 0) / FP8 (kind 1) / QSGD (kind 2) single HBM pass: the warp-specialised TMA
+// INT8 (kind 0) / FP8 E4M3 (kind 1) / QSGD (kind 2) / FP8 E5M2 (kind 3) single HBM pass: the warp-specialised TMA
 // kernel with that quantiser (16-B aligned calls; cooperative, one CTA per SM; done_words >=
 // nitems words, zeroed by the launcher).
 void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, int nitems, const float* g, float* r,
@@ -93,7 +104,7 @@ struct Peers {
 void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
                       const Dests& dst, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
-                      uint64_t seq, int config, int kind, const SrArgs& sr);   // kind 0 INT8, 1 FP8, 2 QSGD
+                      uint64_t seq, int config, int kind, const SrArgs& sr);   // kind 0 INT8, 1 E4M3, 2 QSGD, 3 E5M2
 
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.

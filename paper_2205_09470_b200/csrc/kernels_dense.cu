@@ -19,6 +19,7 @@
 #include <map>
 #include <set>
 #include <tuple>
+#include <utility>
 
 #include "kernels.h"
 #include "dense_common.cuh"
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_absmax(const Item* __restrict__ it
 }
 
 // ----------------------------------------------------------------------------- INT8 pass 2
-template <bool EF, bool VEC, bool FP8 = false, bool SR = false>
+template <bool EF, bool VEC, int FP8 = 0, bool SR = false>
 __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict__ items, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,
                                                          Dests dst,
@@ -224,12 +225,12 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
       if (j == 0 && threadIdx.x == 0) atomicOr(flags, kFlagNonfinite);
       continue;
     }
-    const float s = FP8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
+    const float s = FP8 ? fp8_scale_from_bits<FP8>(mbits) : int8_scale_from_bits(mbits);
     const float sinv = int8_inv(s);   // fl(1/s) if normal, else 0 (both fast paths then divide)
     const float* g = gbase + it.g_off;
     float* r = rbase + it.r_off;
     const uint64_t bo = it.slot_off + 16;
-    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, FP8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, s, 0u);
+    if (j == 0 && threadIdx.x == 0) put_preamble(dst, it.slot_off, FP8 == 2 ? M_FP8_E5M2 : FP8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, s, 0u);
     uint64_t srb = 0;
     if constexpr (SR)
       srb = qsgd_base(sr.seed, sr.step, qsgd_key(sr.cluster0 + it.sidx / sr.num_buckets, sr.shard, it.sidx % sr.num_buckets));
@@ -250,9 +251,9 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
         float4 p = EF ? add4(gv[u], rv[u]) : gv[u];
         float d0, d1, d2, d3;
         if constexpr (FP8) {
-          wv = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
-          d0 = __fmul_rn(fp8_val(wv), s); d1 = __fmul_rn(fp8_val(wv >> 8), s);
-          d2 = __fmul_rn(fp8_val(wv >> 16), s); d3 = __fmul_rn(fp8_val(wv >> 24), s);
+          wv = fp8x2_fast<FP8>(p.x, p.y, s, sinv) | (fp8x2_fast<FP8>(p.z, p.w, s, sinv) << 16);
+          d0 = __fmul_rn(fp8_val<FP8>(wv), s); d1 = __fmul_rn(fp8_val<FP8>(wv >> 8), s);
+          d2 = __fmul_rn(fp8_val<FP8>(wv >> 16), s); d3 = __fmul_rn(fp8_val<FP8>(wv >> 24), s);
         } else if constexpr (SR) {
           const uint64_t h0 = qsgd_h(srb, 2 * q), h1 = qsgd_h(srb, 2 * q + 1);   // elements 4q .. 4q+3
           int q0 = qsgd_q(p.x, s, qsgd_hi(h0)), q1 = qsgd_q(p.y, s, qsgd_lo(h0)),
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
         uint32_t ce;
         float de;
         if constexpr (FP8) {
-          ce = fp8x2_of(p, 0.0f, s) & 0xFF;
-          de = __fmul_rn(fp8_val(ce), s);
+          ce = fp8x2_of<FP8>(p, 0.0f, s) & 0xFF;
+          de = __fmul_rn(fp8_val<FP8>(ce), s);
         } else if constexpr (SR) {
           const int qe = qsgd_q(p, s, qsgd_u(srb, e));
           ce = (uint32_t)qe & 0xFF;
@@ -303,7 +304,8 @@ __device__ __forceinline__ float decode_one(const uint8_t* slot, uint64_t e, flo
   const uint8_t* body = slot + 16;
   if constexpr (METHOD == M_IDENTITY) return reinterpret_cast<const float*>(body)[e];
   else if constexpr (METHOD == M_FP16) return __half2float(reinterpret_cast<const __half*>(body)[e]);
-  else if constexpr (METHOD == M_FP8) return __fmul_rn(fp8_val(body[e]), s);
+  else if constexpr (METHOD == M_FP8) return __fmul_rn(fp8_val<1>(body[e]), s);
+  else if constexpr (METHOD == M_FP8_E5M2) return __fmul_rn(fp8_val<2>(body[e]), s);
   else return __fmul_rn((float)(int8_t)body[e], s);
 }
 
@@ -318,7 +320,9 @@ __device__ __forceinline__ float decode_at(const uint4& w, int e, float s) {
   } else if constexpr (METHOD == M_FP16) {
     return __half2float(__ushort_as_half((unsigned short)((e & 1) ? (x >> 16) : (x & 0xFFFF))));
   } else if constexpr (METHOD == M_FP8) {
-    return __fmul_rn(fp8_val(x >> (8 * (e & 3))), s);
+    return __fmul_rn(fp8_val<1>(x >> (8 * (e & 3))), s);
+  } else if constexpr (METHOD == M_FP8_E5M2) {
+    return __fmul_rn(fp8_val<2>(x >> (8 * (e & 3))), s);
   } else {
     return __fmul_rn((float)(int8_t)((x >> (8 * (e & 3))) & 0xFF), s);
   }
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_dense(const RItem* __restri
       cur = i;
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        sc[k] = (METHOD == M_INT8 || METHOD == M_FP8) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
+        sc[k] = (METHOD == M_INT8 || METHOD == M_FP8 || METHOD == M_FP8_E5M2) ? *reinterpret_cast<const float*>(src.p[k] + it.slot_off + k * it.pb + 8) : 1.0f;
     }
     const uint64_t j = c - it.chunk0, nfull = it.n / E;   // groups entirely inside the bucket
     float* out = obase + it.out_off;
@@ -460,6 +464,48 @@ void ensure_smem_attr(const void* kernel, size_t bytes) {
     done.insert({dev, kernel, bytes});
 }
 
+static void touch(const void* f) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, f);
+}
+template <int M, int... Ps>
+static void touch_reduce(std::integer_sequence<int, Ps...>) {
+  (touch((const void*)k_reduce_dense<M, Ps + 1, true>), ...);
+  (touch((const void*)k_reduce_dense<M, Ps + 1, false>), ...);
+}
+void preload_dense() {
+  touch((const void*)k_identity<true>); touch((const void*)k_identity<false>);
+  touch((const void*)k_fp16<true, true>); touch((const void*)k_fp16<true, false>);
+  touch((const void*)k_fp16<false, true>); touch((const void*)k_fp16<false, false>);
+  touch((const void*)k_absmax<true, true>); touch((const void*)k_absmax<true, false>);
+  touch((const void*)k_absmax<false, true>); touch((const void*)k_absmax<false, false>);
+#define NB_Q(F, SR)                                                                                   \
+  touch((const void*)k_int8_quant<true, true, F, SR>); touch((const void*)k_int8_quant<true, false, F, SR>); \
+  touch((const void*)k_int8_quant<false, true, F, SR>); touch((const void*)k_int8_quant<false, false, F, SR>)
+  NB_Q(0, false); NB_Q(1, false); NB_Q(2, false); NB_Q(0, true);
+#undef NB_Q
+  touch_reduce<M_IDENTITY>(std::make_integer_sequence<int, 8>{});
+  touch_reduce<M_FP16>(std::make_integer_sequence<int, 8>{});
+  touch_reduce<M_INT8>(std::make_integer_sequence<int, 8>{});
+  touch_reduce<M_FP8>(std::make_integer_sequence<int, 8>{});
+  touch_reduce<M_FP8_E5M2>(std::make_integer_sequence<int, 8>{});
+}
+
+void preload_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return;
+  preload_dense();
+  preload_ws();
+  preload_intra();
+  preload_topk();
+  cudaGetLastError();
+  done.insert(dev);
+}
+
 #define GRID(kernel) persistent_grid(L, chunks, (const void*)(kernel), kThreads)
 
 void launch_identity(const Launch& L, bool vec, const Item* items, int nitems, uint64_t chunks, const float* g,
@@ -504,14 +550,21 @@ void launch_int8_quant(const Launch& L, bool ef, bool vec, const Item* items, in
   ++*L.launches;
 }
 
+template <int F>
+static void fp8_quant_f(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
+                        const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags) {
+  if (ef && vec) k_int8_quant<true, true, F><<<GRID((k_int8_quant<true, true, F>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (ef) k_int8_quant<true, false, F><<<GRID((k_int8_quant<true, false, F>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else if (vec) k_int8_quant<false, true, F><<<GRID((k_int8_quant<false, true, F>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  else k_int8_quant<false, false, F><<<GRID((k_int8_quant<false, false, F>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+}
+
 void launch_fp8_quant(const Launch& L, bool ef, bool vec, const Item* items, int nitems, uint64_t chunks,
-                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags) {
+                      const float* g, float* r, const Dests& slots, const uint32_t* scratch, uint32_t* flags, int fmt) {
   if (!chunks) return;
   Mark mk(L, PH_FP8_QUANT);
-  if (ef && vec) k_int8_quant<true, true, true><<<GRID((k_int8_quant<true, true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else if (ef) k_int8_quant<true, false, true><<<GRID((k_int8_quant<true, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else if (vec) k_int8_quant<false, true, true><<<GRID((k_int8_quant<false, true, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
-  else k_int8_quant<false, false, true><<<GRID((k_int8_quant<false, false, true>)), kThreads, 0, L.stream>>>(items, nitems, chunks, g, r, slots, scratch, flags);
+  if (fmt == 2) fp8_quant_f<2>(L, ef, vec, items, nitems, chunks, g, r, slots, scratch, flags);
+  else fp8_quant_f<1>(L, ef, vec, items, nitems, chunks, g, r, slots, scratch, flags);
   ++*L.launches;
 }
 
@@ -554,6 +607,7 @@ void launch_reduce_dense(const Launch& L, int method, int P, bool vec, const RIt
   if (method == M_IDENTITY) reduce_m<M_IDENTITY>(L, P, vec, items, nitems, chunks, slots, out);
   else if (method == M_FP16) reduce_m<M_FP16>(L, P, vec, items, nitems, chunks, slots, out);
   else if (method == M_FP8) reduce_m<M_FP8>(L, P, vec, items, nitems, chunks, slots, out);
+  else if (method == M_FP8_E5M2) reduce_m<M_FP8_E5M2>(L, P, vec, items, nitems, chunks, slots, out);
   else reduce_m<M_INT8>(L, P, vec, items, nitems, chunks, slots, out);   // INT8 and QSGD: same decode
   ++*L.launches;
 }

@@ -168,6 +168,17 @@ __global__ void k_scale_mail(Peers pe, PeerU mails, uint32_t* scratch, uint32_t*
   }
 }
 
+void preload_intra() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)k_rs_push<true>);
+  cudaFuncGetAttributes(&a, (const void*)k_rs_push<false>);
+  cudaFuncGetAttributes(&a, (const void*)k_rs_reduce<true>);
+  cudaFuncGetAttributes(&a, (const void*)k_rs_reduce<false>);
+  cudaFuncGetAttributes(&a, (const void*)k_ag_pull<true>);
+  cudaFuncGetAttributes(&a, (const void*)k_ag_pull<false>);
+  cudaFuncGetAttributes(&a, (const void*)k_scale_mail);
+}
+
 static unsigned grid_of(const Launch& L, uint64_t chunks, const void* f) {
   return persistent_grid(L, chunks, f, kIThreads);
 }

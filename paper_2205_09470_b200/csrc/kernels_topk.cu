@@ -1410,6 +1410,39 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   *L.launches += 18;
 }
 
+static void touch_t(const void* f) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, f);
+}
+template <int P>
+static void touch_densify() {
+  touch_t((const void*)k_topk_densify<P, 1, true>); touch_t((const void*)k_topk_densify<P, 1, false>);
+  touch_t((const void*)k_topk_densify<P, 2, true>); touch_t((const void*)k_topk_densify<P, 2, false>);
+  touch_t((const void*)k_topk_densify<P, 4, true>); touch_t((const void*)k_topk_densify<P, 4, false>);
+  touch_t((const void*)k_topk_densify_w<P, true>); touch_t((const void*)k_topk_densify_w<P, false>);
+  touch_t((const void*)k_topk_densify_t<P, true>); touch_t((const void*)k_topk_densify_t<P, false>);
+}
+void preload_topk() {
+  touch_t((const void*)k_topk_bracket);
+  touch_t((const void*)k_topk_sample<true>); touch_t((const void*)k_topk_sample<false>);
+  for (const void* f : {(const void*)k_topk_pass<true, true, true>, (const void*)k_topk_pass<true, true, false>,
+                        (const void*)k_topk_pass<true, false, true>, (const void*)k_topk_pass<true, false, false>,
+                        (const void*)k_topk_pass<false, true, true>, (const void*)k_topk_pass<false, true, false>,
+                        (const void*)k_topk_pass<false, false, true>, (const void*)k_topk_pass<false, false, false>})
+    touch_t(f);
+  touch_t((const void*)k_topk_stage<true, true>); touch_t((const void*)k_topk_stage<true, false>);
+  touch_t((const void*)k_topk_stage<false, true>); touch_t((const void*)k_topk_stage<false, false>);
+  touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan);
+  touch_t((const void*)k_topk_write<true>); touch_t((const void*)k_topk_write<false>);
+  touch_t((const void*)k_topk_resolve);
+  touch_t((const void*)k_topk_hist<true>); touch_t((const void*)k_topk_hist<false>);
+  touch_t((const void*)k_topk_hist_select); touch_t((const void*)k_topk_splits);
+  touch_t((const void*)k_topk_merge<true>); touch_t((const void*)k_topk_merge<false>);
+  touch_t((const void*)k_topk_starts);
+  touch_densify<1>(); touch_densify<2>(); touch_densify<3>(); touch_densify<4>();
+  touch_densify<5>(); touch_densify<6>(); touch_densify<7>(); touch_densify<8>();
+}
+
 void topk_prepare_bracket(uint32_t keys) {
   cudaFuncSetAttribute(k_topk_bracket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(keys * 4));
 }

@@ -93,13 +93,13 @@ struct WsCMeta {
 };
 
 // One payload byte -> its decoded value (INT8 / QSGD: q * s; FP8: E4M3(c) * s).
-template <bool F8>
+template <int F8>
 __device__ __forceinline__ float dec_byte(uint32_t byte, float s) {
-  if constexpr (F8) return __fmul_rn(fp8_val(byte), s);
+  if constexpr (F8) return __fmul_rn(fp8_val<F8>(byte), s);
   else return __fmul_rn((float)(int8_t)(byte & 0xFF), s);
 }
 
-template <int P, bool F8 = false>
+template <int P, int F8 = 0>
 __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct, int nC, unsigned char* ringC,
                                               uint64_t* fullC, uint64_t* emptyC, WsCMeta* meta) {
   constexpr uint32_t TB = (kWsCStage / P) & ~15u;   // bytes per cluster per stage
@@ -202,7 +202,7 @@ __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct,
 // Reduce role, register-load variant (P2P pull): buckets in order; this CTA's share of bucket b is the same quad slice its B
 // warps quantised, in 16-element groups (one 16-B load per cluster), staged through a per-warp
 // shared-memory transpose so each store instruction writes 512 contiguous bytes.
-template <int P, bool F8 = false>
+template <int P, int F8 = 0>
 __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
                                                volatile uint32_t* s_abort, float* s_out, uint32_t* flags) {
   constexpr int E = 16, SROW = E + 1, U = P <= 2 ? 2 : 1;
@@ -349,7 +349,7 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
 // CM: reduce role — 0 none (compress only), 1 TMA variant (LOOPBACK), 2 register loads (P2P pull)
 // F8: the same schedules for the FP8 E4M3 codec (NEXT-4, R27) — only the B warps' scale /
 // quantise / dequantise and the C warps' byte decode differ.
-template <bool EF, int AW, int BW, int CW, int CM, bool F8 = false, bool SR = false>
+template <bool EF, int AW, int BW, int CW, int CM, int F8 = 0, bool SR = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_int8_ws(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
               Dests dst, uint32_t* scratch, uint32_t* flags, unsigned* done, StepArgs sa) {
@@ -516,10 +516,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           s_scale[0] = 0.0f;
           if (blockIdx.x == 0) atomicOr(flags, kFlagNonfinite);
         } else {
-          const float sc = F8 ? fp8_scale_from_bits(mbits) : int8_scale_from_bits(mbits);
+          const float sc = F8 ? fp8_scale_from_bits<F8>(mbits) : int8_scale_from_bits(mbits);
           s_scale[0] = sc;
           s_scale[1] = int8_inv(sc);
-          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, sc, 0u);
+          if (blockIdx.x == 0) put_preamble(dst, it.slot_off, F8 == 2 ? M_FP8_E5M2 : F8 ? M_FP8 : (SR ? M_QSGD : M_INT8), (uint32_t)it.n, sc, 0u);
         }
       }
       named_sync(2, kB);
@@ -547,9 +547,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const float4 p = S.p[j];
             float d0, d1, d2, d3;
             if constexpr (F8) {
-              w = fp8x2_fast(p.x, p.y, s, sinv) | (fp8x2_fast(p.z, p.w, s, sinv) << 16);
-              d0 = __fmul_rn(fp8_val(w), s); d1 = __fmul_rn(fp8_val(w >> 8), s);
-              d2 = __fmul_rn(fp8_val(w >> 16), s); d3 = __fmul_rn(fp8_val(w >> 24), s);
+              w = fp8x2_fast<F8>(p.x, p.y, s, sinv) | (fp8x2_fast<F8>(p.z, p.w, s, sinv) << 16);
+              d0 = __fmul_rn(fp8_val<F8>(w), s); d1 = __fmul_rn(fp8_val<F8>(w >> 8), s);
+              d2 = __fmul_rn(fp8_val<F8>(w >> 16), s); d3 = __fmul_rn(fp8_val<F8>(w >> 24), s);
             } else if constexpr (SR) {
               const uint64_t h0 = qsgd_h(srb, 2 * (q0 + j)), h1 = qsgd_h(srb, 2 * (q0 + j) + 1);
               const int a0 = qsgd_q(p.x, s, qsgd_hi(h0)), a1 = qsgd_q(p.y, s, qsgd_lo(h0)),
@@ -583,8 +583,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           uint32_t ce;
           float de;
           if constexpr (F8) {
-            ce = fp8x2_of(p, 0.0f, s) & 0xFF;
-            de = __fmul_rn(fp8_val(ce), s);
+            ce = fp8x2_of<F8>(p, 0.0f, s) & 0xFF;
+            de = __fmul_rn(fp8_val<F8>(ce), s);
           } else if constexpr (SR) {
             const int qe = qsgd_q(p, s, qsgd_u(srb, e));
             ce = (uint32_t)qe & 0xFF;
@@ -791,18 +791,39 @@ bool int8_onchip_capacity(int device, uint64_t* max_items, int* grid, size_t* sm
 
 // kind: 0 INT8, 1 FP8 E4M3, 2 QSGD (compress only: no reduce warps)
 static const void* ws_compress_kernel(bool ef, int kind) {
-  if (kind == 2) return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, false, true>
-                           : (const void*)k_int8_ws<false, 8, 23, 0, 0, false, true>;
-  if (kind == 1) return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, true>
-                           : (const void*)k_int8_ws<false, 8, 23, 0, 0, true>;
+  if (kind == 3) return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, 2> : (const void*)k_int8_ws<false, 8, 23, 0, 0, 2>;
+  if (kind == 2) return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, 0, true>
+                           : (const void*)k_int8_ws<false, 8, 23, 0, 0, 0, true>;
+  if (kind == 1) return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0, 1>
+                           : (const void*)k_int8_ws<false, 8, 23, 0, 0, 1>;
   return ef ? (const void*)k_int8_ws<true, 8, 23, 0, 0> : (const void*)k_int8_ws<false, 8, 23, 0, 0>;
+}
+
+template <bool EF>
+static const void* step_kernel(int config, int kind);
+__global__ void k_exchange_flags(Peers pe, unsigned long long* local, int lo, int hi, unsigned long long seq,
+                                 uint32_t* flags);
+
+void preload_ws() {
+  cudaFuncAttributes a;
+  for (int kind = 0; kind < 4; ++kind)
+    for (int ef = 0; ef < 2; ++ef) {
+      cudaFuncGetAttributes(&a, ws_compress_kernel(ef != 0, kind));
+      for (int config = 0; config <= 10; ++config) {
+        cudaFuncGetAttributes(&a, step_kernel<true>(config, kind));
+        cudaFuncGetAttributes(&a, step_kernel<false>(config, kind));
+      }
+    }
+  cudaFuncGetAttributes(&a, (const void*)k_fp16_tma<true>);
+  cudaFuncGetAttributes(&a, (const void*)k_fp16_tma<false>);
+  cudaFuncGetAttributes(&a, (const void*)k_exchange_flags);
 }
 
 void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, int nitems, const float* g, float* r,
                         const Dests& slots_in, uint32_t* scratch, uint32_t* flags, uint32_t* done_words,
                         const SrArgs& srargs) {
   Dests slots = slots_in;
-  Mark mk(L, kind == 2 ? PH_QSGD_QUANT : (kind == 1 ? PH_FP8_QUANT : PH_INT8_ONCHIP));
+  Mark mk(L, kind == 2 ? PH_QSGD_QUANT : (kind == 1 || kind == 3 ? PH_FP8_QUANT : PH_INT8_ONCHIP));
   cudaMemsetAsync(done_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
   unsigned* done = done_words;
   StepArgs sa{};
@@ -822,11 +843,12 @@ void launch_ws_compress(const Launch& L, bool ef, int kind, const Item* items, i
 // Warp splits (A, B, C) of the fused step; config 0 is the default, the rest a tuning sweep.
 template <bool EF>
 static const void* step_kernel(int config, int kind) {
-  if (kind == 1) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, true> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, true>;
+  if (kind == 1) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, 1> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, 1>;
+  if (kind == 3) return config == 4 ? (const void*)k_int8_ws<EF, 4, 16, 11, 2, 2> : (const void*)k_int8_ws<EF, 8, 19, 4, 1, 2>;
   if (kind == 2) {   // QSGD: the quantise warps are instruction-bound, config 1 gives them more warps
-    if (config == 4) return (const void*)k_int8_ws<EF, 4, 16, 11, 2, false, true>;
-    if (config == 1) return (const void*)k_int8_ws<EF, 5, 22, 4, 1, false, true>;
-    return (const void*)k_int8_ws<EF, 8, 19, 4, 1, false, true>;
+    if (config == 4) return (const void*)k_int8_ws<EF, 4, 16, 11, 2, 0, true>;
+    if (config == 1) return (const void*)k_int8_ws<EF, 5, 22, 4, 1, 0, true>;
+    return (const void*)k_int8_ws<EF, 8, 19, 4, 1, 0, true>;
   }
   switch (config) {
     // LOOPBACK (TMA reduce role)

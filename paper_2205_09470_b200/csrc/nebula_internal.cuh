@@ -21,7 +21,7 @@ constexpr int kChunkQuads = kThreads * kQuadsPerThread;
 constexpr uint64_t kChunkElems = (uint64_t)kChunkQuads * 4;   // 4096 elements per chunk
 
 enum : uint32_t { kFlagNonfinite = 1u, kFlagOverflow = 2u, kFlagPeerTimeout = 4u };
-enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3, M_FP8 = 4, M_QSGD = 6 };
+enum : int { M_IDENTITY = 0, M_FP16 = 1, M_INT8 = 2, M_TOPK = 3, M_FP8 = 4, M_QSGD = 6, M_FP8_E5M2 = 7 };
 enum : int { V_F32 = 0, V_F16 = 1, V_I8 = 2 };
 
 // One (cluster, bucket) unit of codec work.  Offsets are relative to per-call base
@@ -149,41 +149,53 @@ __device__ __forceinline__ int int8_qi(float p, float s, float inv) {
   return inv != 0.0f ? int8_q_fast(p, s, inv) : int8_q(p, s);
 }
 
-// FP8 E4M3 (NEXT-4, R27; "8-bit floating point"): s = fl(m / 448)
-// with the R4 degenerate rules; code = RNE to E4M3 of fl(p / s), saturating to +-448
-// (cvt.rn.satfinite.e4m3x2.f32); D = fl(E4M3(code) * s).
+// FP8 (NEXT-4; "8-bit floating point"), format F: 1 = OCP E4M3 (R27: max 448, 3
+// mantissa bits, smallest normal exponent -6), 2 = OCP E5M2 (R33: max 57344, 2 mantissa bits,
+// smallest normal exponent -14).  s = fl(m / max) with the R4 degenerate rules; code = RNE of
+// fl(p / s) to the format, saturating to +-max (cvt.rn.satfinite.{e4m3,e5m2}x2.f32);
+// D = fl(FP8(code) * s).
+template <int F>
+__device__ __forceinline__ constexpr float fp8_max() { return F == 2 ? 57344.0f : 448.0f; }
+template <int F>
+__device__ __forceinline__ __nv_fp8_interpretation_t fp8_kind() { return F == 2 ? __NV_E5M2 : __NV_E4M3; }
+template <int F = 1>
 __device__ __forceinline__ float fp8_scale_from_bits(uint32_t mbits) {
   float m = __uint_as_float(mbits);
-  float s = __fdiv_rn(m, 448.0f);
+  float s = __fdiv_rn(m, fp8_max<F>());
   if (m == 0.0f || s == 0.0f) s = 1.0f;
   return s;
 }
-// two quotients -> two E4M3 bytes (a in the low byte)
+// two quotients -> two FP8 bytes (a in the low byte)
+template <int F = 1>
 __device__ __forceinline__ uint32_t fp8x2_of(float pa, float pb, float s) {
-  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(__fdiv_rn(pa, s), __fdiv_rn(pb, s)), __NV_SATFINITE, __NV_E4M3);
+  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(__fdiv_rn(pa, s), __fdiv_rn(pb, s)), __NV_SATFINITE, fp8_kind<F>());
 }
-// Same bytes, cheaper (the INT8 argument of int8_q_fast, for the E4M3 grid): x = fl(p * fl(1/s))
-// is within 3 * 2^-24 |x| of y = fl(p / s).  In the binade of |x| (exponent e >= -6, the
-// subnormal quantum below) E4M3 rounds t = |x| 2^(3-e) (exact scaling, t < 16) to an integer,
-// so x and y round alike unless frac(t) is within 3 * 2^-24 * 16 < 4e-6 of one half (binade
-// edges are representable, saturation at 464 = t 14.5 is such a midpoint).  Otherwise — or
+// Same bytes, cheaper (the INT8 argument of int8_q_fast, for the FP8 grid): x = fl(p * fl(1/s))
+// is within 3 * 2^-24 |x| of y = fl(p / s).  In the binade of |x| (exponent e >= emin, the
+// subnormal quantum below) the format rounds t = |x| 2^(MB-e) (exact scaling, t < 2^(MB+1)) to
+// an integer, so x and y round alike unless frac(t) is within 3 * 2^-24 * 16 < 4e-6 of one half
+// (binade edges are representable; the saturation boundary is such a midpoint).  Otherwise — or
 // when inv = fl(1/s) is not a usable normal number (inv == 0) — the IEEE division decides.
+template <int F = 1>
 __device__ __forceinline__ float fp8_quotient(float p, float s, float inv) {
+  constexpr int MB = F == 2 ? 2 : 3, EMIN = F == 2 ? -14 : -6, ESAT = F == 2 ? 17 : 20;
   if (inv == 0.0f) return __fdiv_rn(p, s);
   const float x = __fmul_rn(p, inv);
   const uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
-  const int e = max((int)(b >> 23) - 127, -6);
-  if (e > 20) return x;                                   // saturates to +-448 either way
-  const float t = __fmul_rn(__uint_as_float(b), __uint_as_float((uint32_t)(130 - e) << 23));
+  const int e = max((int)(b >> 23) - 127, EMIN);
+  if (e > ESAT) return x;                                 // saturates to +-max either way
+  const float t = __fmul_rn(__uint_as_float(b), __uint_as_float((uint32_t)(127 + MB - e) << 23));
   return fabsf(t - floorf(t) - 0.5f) > 4e-6f ? x : __fdiv_rn(p, s);
 }
+template <int F = 1>
 __device__ __forceinline__ uint32_t fp8x2_fast(float pa, float pb, float s, float inv) {
-  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(fp8_quotient(pa, s, inv), fp8_quotient(pb, s, inv)),
-                                            __NV_SATFINITE, __NV_E4M3);
+  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(fp8_quotient<F>(pa, s, inv), fp8_quotient<F>(pb, s, inv)),
+                                            __NV_SATFINITE, fp8_kind<F>());
 }
-// E4M3 byte -> binary32 (exact: E4M3 values are binary16 values)
+// FP8 byte -> binary32 (exact: E4M3 and E5M2 values are binary16 values)
+template <int F = 1>
 __device__ __forceinline__ float fp8_val(uint32_t byte) {
-  __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(byte & 0xFF), __NV_E4M3);
+  __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(byte & 0xFF), fp8_kind<F>());
   return __half2float(__half(h));
 }
 

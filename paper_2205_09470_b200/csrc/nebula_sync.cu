@@ -232,7 +232,8 @@ static uint64_t payload_bytes_for(int method, uint64_t n, uint64_t k, int vt) {
     case M_FP16: return 16 + pad16(2 * n);
     case M_INT8:
     case M_QSGD:
-    case M_FP8: return 16 + pad16(n);
+    case M_FP8:
+    case M_FP8_E5M2: return 16 + pad16(n);
     default: return 16 + pad16(4 * k) + pad16(value_bytes(vt) * k);
   }
 }
@@ -262,7 +263,7 @@ static nebula_status validate(const nebula_topology* t, const nebula_codec* c, c
       return fail(nullptr, NEBULA_ERR_INVALID_ARG, "local_rank out of range");
   }
   if (t->device < 0) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "device must be >= 0");
-  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_QSGD || c->method == 5)
+  if (c->method < NEBULA_IDENTITY || c->method > NEBULA_FP8_E5M2 || c->method == 5)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown method");
   if (c->error_feedback != 0 && c->error_feedback != 1)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "error_feedback must be 0 or 1");
@@ -718,6 +719,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       return bail(NEBULA_ERR_CUDA);
     }
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    preload_kernels();   // no lazy kernel load may ever wait behind a spinning flag kernel
 
     // ---- memory plan
     ctx->b.resize(num_buckets);
@@ -784,7 +786,8 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       s = topk_setup(ctx);
       if (s != NEBULA_OK) return bail(s);
     }
-    if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8 || codec->method == NEBULA_QSGD) {
+    if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8 || codec->method == NEBULA_QSGD ||
+        codec->method == NEBULA_FP8_E5M2) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
       if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (2 * ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
         ctx->err = "barrier allocation failed";
@@ -991,12 +994,13 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       break;
     case M_INT8:
     case M_FP8:
+    case M_FP8_E5M2:
     case M_QSGD: {
       // one per-bucket scale: max-abs words zeroed, then either the single-pass warp-specialised
       // kernel (16-B aligned, buckets averaging >= 1M elements, no cluster-wide scale) or the
       // max-abs pass, [the cluster-wide max (R28)], and the quantise pass
       { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
-      const int kind = method == M_FP8 ? 1 : (method == M_QSGD ? 2 : 0);
+      const int kind = method == M_FP8 ? 1 : (method == M_QSGD ? 2 : (method == M_FP8_E5M2 ? 3 : 0));
       const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
       // (SELF: auto never picks the cooperative kernel — group members' grids share one GPU)
       const bool single = ctx->onchip_ok && vec && !xscale &&
@@ -1009,7 +1013,9 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
       if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket, lo, hi, seq); if (xs != NEBULA_OK) return xs; }
-      if (kind == 1) launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
+      if (kind == 1 || kind == 3)
+        launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
+                         kind == 3 ? 2 : 1);
       else if (kind == 2) launch_qsgd_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, sr);
       else launch_int8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags);
       break;
@@ -1154,7 +1160,9 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
                          uint64_t step) {
   const int m = method_at(ctx, step);
-  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD) || ctx->G != 1 || !ctx->onchip_ok) return false;
+  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD && m != M_FP8_E5M2) || ctx->G != 1 ||
+      !ctx->onchip_ok)
+    return false;
   // SELF: the peers' cooperative kernels share this GPU — two grid-wide kernels waiting on each
   // other's flags could never be co-resident, so SELF always runs the staged stages
   if (ctx->self) return false;
@@ -1189,7 +1197,7 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
                    sources_of(ctx, probe), dev_out, pe, ctx->d_arrive, seq,
                    ctx->step_fusion >= 2 ? ctx->step_fusion - 2 : (ctx->xmode == 3 ? 4 : 0),
-                   method == M_FP8 ? 1 : (method == M_QSGD ? 2 : 0),
+                   method == M_FP8 ? 1 : (method == M_QSGD ? 2 : (method == M_FP8_E5M2 ? 3 : 0)),
                    SrArgs{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()});
   CKC(cudaGetLastError());
   for (int i = lo; i < hi; ++i) {
@@ -1334,6 +1342,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
   if (option == NEBULA_OPT_INT8_KERNEL) {
     if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "INT8 kernel option must be in [0, 2]");
     if (value == 2 && (ctx->codec.method == NEBULA_INT8 || ctx->codec.method == NEBULA_FP8 ||
+                       ctx->codec.method == NEBULA_FP8_E5M2 ||
                        ctx->codec.method == NEBULA_QSGD) && !ctx->onchip_ok)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "cooperative on-chip INT8 kernel not available on this device");
     ctx->int8_kernel = (int)value;

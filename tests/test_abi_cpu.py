@@ -104,7 +104,7 @@ def test_topology_for_rank():
 
 @pytest.mark.parametrize("kwargs,needle", [
     (dict(method=5), "method"),                 # 5 is the SVD payload id, not a bucket codec
-    (dict(method=7), "method"),
+    (dict(method=8), "method"),
 ])
 def test_validation_rejects_unknown_codec_ids(lib, kwargs, needle):
     with pytest.raises(nb.NebulaError) as e:

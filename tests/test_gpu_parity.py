@@ -111,7 +111,7 @@ def _first_diff(a, b):
 
 
 # ------------------------------------------------------------------ dense codecs
-@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.IDENTITY, O.FP8])
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.IDENTITY, O.FP8, O.FP8_E5M2])
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 @pytest.mark.parametrize("sizes", [[1], [7], [4096], [4099, 12288, 77777]])
 def test_dense_parity(nb, method, P, sizes):
@@ -143,7 +143,7 @@ def test_int8_fused_step(nb, P, per_bucket):
                  int8_kernel="fused-ws")
 
 
-@pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD])
+@pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD, O.FP8_E5M2])
 @pytest.mark.parametrize("P", [2, 3, 5, 8])
 @pytest.mark.parametrize("per_bucket", [False, True])
 def test_pull_reducer_in_fused_step(nb, method, P, per_bucket):
@@ -173,6 +173,23 @@ def test_int8_fused_step_is_one_launch(nb):
     ctx.check()
     assert ctx.kernel_launches() - n0 == 2
     ctx.destroy()
+
+
+@pytest.mark.parametrize("kern", ["two-pass", "fused-ws", "fused-ws-staged"])
+@pytest.mark.parametrize("sizes", [[1], [5, 4096, 4099], [300001, 7, 1 << 20], [3_000_003]])
+@pytest.mark.parametrize("ef", [True, False])
+def test_e5m2_kernels(nb, kern, sizes, ef):
+    """FP8 E5M2 (NEXT-4, R33): two-pass, single-pass and fused-step schedules, bit-exact."""
+    assert run_loopback(nb, O.FP8_E5M2, sizes, 2, int8_kernel=kern, ef=ef, steps=2) > 0
+
+
+@pytest.mark.parametrize("kern", ["two-pass", "fused-ws"])
+@pytest.mark.parametrize("kind", ["e5m2-ties", "subnormal", "mixed-scale", "tiny-max", "zeros"])
+def test_e5m2_near_rounding_boundaries(nb, kern, kind):
+    # quotients on / next to E5M2 rounding midpoints: the reciprocal fast path must defer to the
+    # IEEE division there
+    run_loopback(nb, O.FP8_E5M2, [50001, 4096], 2, kind=kind, steps=1, ef=False, int8_kernel=kern)
+    run_loopback(nb, O.FP8_E5M2, [1 << 20, 7], 2, kind=kind, steps=2, int8_kernel=kern)
 
 
 def test_topk_i8_near_half_integer_quotients(nb):
