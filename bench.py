@@ -10,8 +10,11 @@ exchange, decompress+average, residual update) over every bucket of one syntheti
   N > 1 : (torchrun) one cluster per GPU, P = N, NCCL over NVLink, same gradient shape per
           GPU (weak scaling: every GPU syncs its full replica gradient).
 
-value = fp32 gradient bytes synced by all clusters / device time of K steps (max over
-ranks).  e2e = the same through nebula_step_host (pinned host buffers, H2D + D2H inside the
+value = fp32 gradient GB/s synced PER GPU (the BASELINE metric's unit): the fp32 bytes of the
+gradient(s) one GPU synchronises / device time of K steps (max over ranks) — at N = 1 the GPU
+hosts both simulated clusters (2 n elements), at N > 1 its own replica (n elements);
+value_aggregate = the same summed over the N GPUs.  At N > 1 the roofline is the larger of the
+HBM time and the NVLink time, the latter against an in-run 1 GiB all-gather bus bandwidth.  e2e = the same through nebula_step_host (pinned host buffers, H2D + D2H inside the
 timed region).  cpu_baseline = the CPU oracle on a bounded sample (rank 0, N = 1 only).
 `--impl reference` runs the oracle as the reference arm.
 """
@@ -233,7 +236,8 @@ def run_reference(args):
     from gradgen import fixed_buckets, model_numel
     n = model_numel(args.workload)
     per = fixed_buckets(n, int(args.bucket_mib * 2 ** 20))[0]
-    P = args.clusters if args.gpus == 1 else args.gpus
+    G = args.gpus_per_cluster if args.gpus > 1 else 1
+    P = args.clusters if args.gpus == 1 else args.gpus // G
     budget = max(1.0, 120.0 / max(1, args.steps + args.warmup))
     from gradgen import model_gradient
     gs = [model_gradient(args.workload, cluster=c) for c in range(P)]
@@ -244,11 +248,11 @@ def run_reference(args):
         e, tt, _ = oracle_sample(method, vt, args.density, ef, P, per, budget, gs)
         elems += e
         t += tt
-    value = P * elems * 4 / t / 1e9
+    value = (P if args.gpus == 1 else 1) * elems * 4 / t / 1e9   # per GPU, as the repo arm
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": workload_config(args, n, P),
+            "data": "synthetic", "config": workload_config(args, n, P, G),
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"per step: P={P} clusters x 25 MiB buckets of the {args.workload} gradient "
                                        f"until ~{budget:.1f}s; single-threaded NumPy on '{cpu_desc()}' "
@@ -291,9 +295,11 @@ def main():
     if rank == 0:
         build.build()
     torch.cuda.set_device(local)
+    busbw = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
+        busbw = nvlink_busbw(world)
     if rank != 0:
         build.build()   # up to date after rank 0's build + barrier: loads only
     method, vt, ef = METHODS[args.method], VALUES[args.values], not args.no_ef
@@ -376,8 +382,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_step = t_max / args.steps
-    synced_bytes = P * n * 4 if world == 1 else world * n * 4
-    value = synced_bytes / (ms_step * 1e-3) / 1e9
+    gpu_bytes = P * n * 4 if world == 1 else n * 4      # fp32 bytes this GPU synchronises per step
+    synced_bytes = gpu_bytes * world                     # all GPUs
+    value = gpu_bytes / (ms_step * 1e-3) / 1e9
+    value_aggregate = synced_bytes / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel
     peak, peak_src = load_peaks()
@@ -410,6 +418,18 @@ def main():
                     "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": int(byt), "ms_per_launch": round(tot / cnt, 4)}
     step_bytes = step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world)
+    if world > 1 and (busbw or 0) > 0:
+        # NVLink bound: bytes INTO this GPU per step (P - 1 peers' payloads of its shard, plus
+        # the G > 1 intra-cluster fp32 hop: (G - 1) / G of the bucket in each of RS and AG)
+        pb = payload_elems_bytes(method, vt, n // G, k_per_cluster)
+        nv = (P - 1) * pb + (2 * (G - 1) * (n // G) * 4 if G > 1 else 0)
+        t_hbm, t_nv = step_bytes / peak, nv / busbw
+        if t_nv > t_hbm:
+            roof = {"kernel": "whole step (exchange)", "bound": "nvlink",
+                    "achieved": round(nv / (ms_step * 1e-3) / 1e9, 1), "peak": round(busbw, 1), "unit": "GB/s",
+                    "frac": round(nv / (ms_step * 1e-3) / 1e9 / busbw, 4), "traffic": None,
+                    "peak_source": "in-run ncclAllGather bus bandwidth, 1 GiB, min over ranks",
+                    "nvlink_bytes_in_per_step": int(nv), "hbm_kernel_roofline": roof}
     step_roof = {"algorithmic_bytes_per_step": int(step_bytes),
                  "achieved_gbs": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
                  "frac_of_hbm_peak": round(step_bytes / (ms_step * 1e-3) / 1e9 / peak, 4)}
@@ -457,7 +477,9 @@ def main():
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload_config(args, n, P, G), exchange=ctx.exchange_mode()), "roofline": roof, "step_roofline": step_roof,
+                "value_aggregate": round(value_aggregate, 2), "exchange": ctx.exchange_mode(),
+                "intra": ctx.intra_mode(), "nvlink_busbw_gbs": round(busbw, 1) if busbw else None,
+                "config": workload_config(args, n, P, G), "roofline": roof, "step_roofline": step_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "kernels": kern,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
@@ -465,6 +487,36 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def payload_elems_bytes(method, vt, n, k):
+    """Payload bytes of one cluster's bucket(s) of n coded elements (k = top-k entries)."""
+    if method == 3:
+        return k * (4 + VB[vt])
+    return n * {0: 4, 1: 2, 2: 1, 4: 1, 6: 1, 7: 1}[method]
+
+
+def nvlink_busbw(world):
+    """In-run NVLink roofline: ncclAllGather bus bandwidth over 1 GiB (min over ranks)."""
+    import torch
+    import torch.distributed as dist
+    x = torch.empty((1 << 30) // world // 4, device="cuda")
+    y = torch.empty(x.numel() * world, device="cuda")
+    for _ in range(3):
+        dist.all_gather_into_tensor(y, x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        dist.all_gather_into_tensor(y, x)
+    e1.record()
+    torch.cuda.synchronize()
+    bw = (world - 1) / world * y.numel() * 4 / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e9
+    t = torch.tensor([bw], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    del x, y
+    torch.cuda.empty_cache()
+    return float(t.item())
 
 
 def step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world):

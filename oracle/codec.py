@@ -518,7 +518,8 @@ def oracle_step(gs: list, rs: list, codec: Codec, step: int, scales=None, bucket
     return out, [x.r_new for x in res], [x.payload for x in res], [x.stats for x in res]
 
 
-def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: bool = False, bucket: int = 0):
+def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: bool = False, bucket: int = 0,
+                      exact_topk: bool = False):
     """P clusters x G GPUs (R20, PAPER.md:95 / :288 intra-cluster parallelism + compressed
     inter-cluster hop).  gs[c][l] is GPU l of cluster c's full bucket (n % G == 0);
     rs[c][l] its residual shard.  The cluster gradient is the fp32 mean of its G GPUs
@@ -526,6 +527,10 @@ def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: 
     GPU l codes shard l; peers with the same l exchange; shards are all-gathered.
     exact_scale (NEXT-3, R28): the INT8 / FP8 scale of every shard is the scale of the whole
     cluster bucket p_c = concat_l(p_{c,l}) (max over all G shards) instead of the shard's own.
+    exact_topk (NEXT-3, R34; TOPK only): the selection is the top-k of the WHOLE cluster bucket,
+    k = k(rho, n) over p_c = concat_l(mean shards) + r_c, instead of k(rho, n/G) per shard: every
+    GPU of cluster c holds the cluster's full residual rs[c][l] (identical for all l, n elements)
+    and the cluster's one payload; the average is over the P clusters' full-bucket payloads.
     Returns (out, rs_new[c][l], payloads[c][l])."""
     P, G = len(gs), len(gs[0])
     n = np.asarray(gs[0][0]).size
@@ -539,8 +544,14 @@ def hierarchical_step(gs: list, rs: list, codec: Codec, step: int, exact_scale: 
             for j in range(1, G):
                 acc = (acc + np.asarray(gs[c][j][l * m:(l + 1) * m], dtype=F32)).astype(F32)
             shards[c][l] = (acc / F32(G)).astype(F32)
-    scales = [None] * P
     method = select_method(codec, step)
+    if exact_topk and codec.method == TOPK:
+        # R34: one selection over the whole cluster bucket (the G shards' means, in order)
+        full = [np.concatenate([shards[c][l] for l in range(G)]).astype(F32) for c in range(P)]
+        out, r_full, pl_full, _ = oracle_step(full, [rs[c][0] for c in range(P)], codec, step, None, bucket, 0)
+        return (out, [[r_full[c] for _ in range(G)] for c in range(P)],
+                [[pl_full[c] for _ in range(G)] for c in range(P)])
+    scales = [None] * P
     if exact_scale and method in (INT8, FP8, QSGD, FP8_E5M2):
         for c in range(P):
             ps = [shards[c][l] if not codec.error_feedback else

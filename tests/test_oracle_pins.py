@@ -675,3 +675,48 @@ def test_e5m2_ratio_error_bound_and_residual_identity():
         assert np.array_equal((res.D + res.r_new).astype(F32), (g + r0).astype(F32))
     _, D, st = O.compress(np.zeros(33, F32), O.FP8_E5M2, O.Codec(method=O.FP8_E5M2))
     assert st["scale"] == 1.0 and np.all(D == 0)
+
+
+# ----------------------------------------------------------------- exact cluster-wide top-k (NEXT-3, R34)
+def _brute_topk(p, k):
+    """Brute force (independent of topk_select's lexsort): repeatedly take the largest |p| key,
+    lowest index first among equal keys, k times."""
+    keys = (p.view(np.uint32) & 0x7FFFFFFF).astype(np.int64)
+    taken = np.zeros(p.size, bool)
+    sel = []
+    for _ in range(k):
+        best = -1
+        for i in range(p.size):
+            if not taken[i] and (best < 0 or keys[i] > keys[best]):
+                best = i
+        taken[best] = True
+        sel.append(best)
+    return sorted(sel)
+
+
+@pytest.mark.parametrize("vt", [O.VAL_F32, O.VAL_I8])
+def test_hierarchical_exact_topk_is_global_selection(vt):
+    """R34: the selection is the top-k of the concatenated cluster bucket (brute force over the
+    concatenation), not k/G per shard; one shard holding every large value makes the two
+    readings differ."""
+    P, G, m = 2, 4, 24
+    rng = np.random.default_rng(17)
+    gs = [[(rng.integers(-50, 50, G * m) * 2.0 ** -6).astype(F32) for _ in range(G)] for _ in range(P)]
+    for c in range(P):      # shard 1 of every GPU's bucket carries the large values
+        for l in range(G):
+            gs[c][l][m:2 * m] *= F32(64.0)
+    codec = O.Codec(method=O.TOPK, topk_values=vt, topk_density=0.125)
+    out, rs, pls = O.hierarchical_step(gs, [[None] * G for _ in range(P)], codec, 0, exact_topk=True)
+    k = O.topk_k(G * m, codec)
+    assert k == 12
+    for c in range(P):
+        p_c = (np.sum(np.array(gs[c], np.float64), axis=0) / G).astype(F32)   # dyadic: exact mean
+        idx = np.frombuffer(pls[c][0], dtype="<u4", count=k, offset=16)
+        assert list(idx) == _brute_topk(p_c, k)
+        assert all(pls[c][l] == pls[c][0] for l in range(G))
+        assert np.all(idx >= m) and np.all(idx < 2 * m)          # all from shard 1
+        D = O.decode_payload(pls[c][0], G * m)
+        assert np.array_equal((D + rs[c][0]).astype(F32), p_c)  # residual identity on the full bucket
+    # per-shard reading (R20) selects k/G = 3 per shard instead
+    _, _, pls2 = O.hierarchical_step(gs, [[None] * G for _ in range(P)], codec, 0)
+    assert struct.unpack_from("<I", pls2[0][0], 4)[0] == O.topk_k(m, codec) == 3
