@@ -112,9 +112,18 @@ typedef struct {
   uint64_t topk_k;         /* >0: exact k per coded bucket (capped at n); 0: derive from density */
   double topk_density;     /* rho in (0,1]; k = clamp(floor(rho*n + 0.5), 1, n)  (R12) */
   int32_t error_feedback;  /* 1: p = g + r and r <- p - D(C(p)) (R15); 0: p = g, no residual */
-  int32_t reserved0;
+  int32_t flags;           /* NEBULA_CODEC_* bits (0 = defaults) */
   uint64_t start_step;     /* IDENTITY while step < start_step */
 } nebula_codec;
+
+/* NEBULA_CODEC_EXACT_TOPK (NEXT-3, R34; TOPK with G > 1): the selection is the top-k of the
+ * WHOLE cluster bucket (k from the bucket's numel) instead of k/G per GPU shard (R20).  Every
+ * GPU of the cluster all-gathers the fixed-order cluster mean, codes the whole bucket with the
+ * cluster's full residual (replicated on the G GPUs, bit-identical), exchanges the full payload
+ * with its inter-cluster peers and averages the whole bucket (no intra all-gather afterwards).
+ * Cost: G x the per-GPU codec work and inter-cluster bytes of the per-shard reading.  Ignored
+ * when G == 1 (the same thing).  Residual length (nebula_residual_ptr): numel. */
+#define NEBULA_CODEC_EXACT_TOPK 1
 
 /* Topology: P clusters x G GPUs.  Global rank = cluster_id * G + local_rank. */
 typedef struct {
@@ -221,7 +230,8 @@ nebula_status nebula_payload_copy(nebula_ctx* ctx, int32_t bucket, int32_t slot,
 /* Device pointer to the residual of (bucket, cluster) — the caller saves / restores it with
  * its optimizer state (checkpointing) or zeroes it after a device error.  cluster is the
  * simulated cluster for LOOPBACK and must be the context's own cluster otherwise.  Length:
- * the coded elements of the bucket (numel, or numel/G when hierarchical). */
+ * the coded elements of the bucket (numel, or numel/G when hierarchical without
+ * NEBULA_CODEC_EXACT_TOPK). */
 nebula_status nebula_residual_ptr(nebula_ctx* ctx, int32_t bucket, int32_t cluster, float** dev_residual);
 
 /* Synchronises and returns the order statistics of the last TOPK compress of (bucket, cluster). */

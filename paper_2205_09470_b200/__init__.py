@@ -38,6 +38,7 @@ OPT_EXACT_SCALE = 5
 OPT_SR_SEED = 6
 OPT_TOPK_REDUCE = 7
 OPT_INTRA = 8
+CODEC_EXACT_TOPK = 1   # NEBULA_CODEC_EXACT_TOPK (NEXT-3, R34)
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128
 
@@ -55,7 +56,7 @@ class NebulaError(RuntimeError):
 class _Codec(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("topk_values", ctypes.c_int32), ("topk_k", ctypes.c_uint64),
                 ("topk_density", ctypes.c_double), ("error_feedback", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("start_step", ctypes.c_uint64)]
+                ("flags", ctypes.c_int32), ("start_step", ctypes.c_uint64)]
 
 
 class _Topology(ctypes.Structure):
@@ -212,7 +213,7 @@ class SyncContext:
     """One ``nebula_ctx``.  Arguments mirror ``nebula_topology`` / ``nebula_codec``."""
 
     def __init__(self, bucket_numel, method=INT8, *, topk_values=VAL_F32, topk_k=0, topk_density=0.01,
-                 error_feedback=True, start_step=0, num_clusters=2, cluster_id=0, gpus_per_cluster=1,
+                 error_feedback=True, start_step=0, exact_topk=False, num_clusters=2, cluster_id=0, gpus_per_cluster=1,
                  local_rank=0, transport=LOOPBACK, device=0, unique_id: bytes | None = None, stream=None):
         L = load()
         self._L = L
@@ -220,8 +221,9 @@ class SyncContext:
         self.num_clusters, self.cluster_id = num_clusters, cluster_id
         self.gpus_per_cluster, self.local_rank = gpus_per_cluster, local_rank
         self.transport, self.device = transport, device
-        self.codec = _Codec(method, topk_values, int(topk_k), float(topk_density), int(bool(error_feedback)), 0,
-                            int(start_step))
+        self.exact_topk = bool(exact_topk)
+        self.codec = _Codec(method, topk_values, int(topk_k), float(topk_density), int(bool(error_feedback)),
+                            CODEC_EXACT_TOPK if exact_topk else 0, int(start_step))
         self._uid = ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES) if unique_id is not None else None
         topo = _Topology(num_clusters, cluster_id, gpus_per_cluster, local_rank, transport, device,
                          ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None)
@@ -305,7 +307,8 @@ class SyncContext:
     def residual(self, bucket, cluster):
         """A torch view (no copy) of the library-owned residual (checkpoint / restore it)."""
         import torch
-        n = self.bucket_numel[bucket] // self.gpus_per_cluster
+        exact = self.exact_topk and self.codec.method == TOPK
+        n = self.bucket_numel[bucket] // (1 if exact else self.gpus_per_cluster)
         ptr = self.residual_ptr(bucket, cluster)
 
         class _CAI:

@@ -41,6 +41,8 @@ struct BucketInfo {
   uint64_t cn = 0;     // coded elements (n / G)
   uint64_t off = 0;    // element offset in the caller's flat ALL buffers
   uint64_t coff = 0;   // element offset in library coded buffers (multiple of 4)
+  uint64_t sn = 0;     // intra-cluster shard elements (n / G)
+  uint64_t soff = 0;   // element offset in the shard buffers (multiple of 4)
   uint64_t k = 0;      // TOPK entries
   uint64_t pb[2] = {0, 0};  // payload bytes per slot, per layout (0: codec method, 1: IDENTITY phase)
   uint64_t so[2] = {0, 0};  // byte offset of this bucket's [P][pb] slot block, per layout
@@ -81,7 +83,8 @@ struct nebula_ctx {
   int P = 1, G = 1, Ploc = 1, me = 0, local_rank = 0, device = 0, num_sms = 148;
   bool loopback = false;
   std::vector<BucketInfo> b;
-  uint64_t total_n = 0, total_cn = 0, total_slots = 0;
+  uint64_t total_n = 0, total_cn = 0, total_sn = 0, total_slots = 0;
+  bool xtopk = false;            // NEXT-3 (R34): G > 1 top-k over the whole cluster bucket
   cudaStream_t stream = nullptr;
 
   float* d_resid = nullptr;      // [Ploc][total_cn]
@@ -102,7 +105,9 @@ struct nebula_ctx {
   // ---- intra-cluster hop over NVLink peer memory (G > 1; kernels_intra.cu)
   bool intra_p2p = false;        // every GPU of the cluster mapped (NCCL: IPC, SELF: same process)
   int intra_opt = 0;             // NEBULA_OPT_INTRA: 0 auto (P2P when mapped), 1 NCCL RS/AG
-  float* d_recv = nullptr;       // [G][total_cn]: slot j = GPU j's slice of this GPU's shard
+  float* d_recv = nullptr;       // [G][total_sn]: slot j = GPU j's slice of this GPU's shard
+  float* d_full = nullptr;       // xtopk: the whole cluster-mean bucket(s) [total_n]
+  float* ip_in[8] = {};          // the cluster's GPUs' mean shards (xtopk all-gather)
   unsigned long long* d_arr_rs = nullptr;   // [B][G] arrival words: RS slices, AG shards, scale mail
   unsigned long long* d_arr_ag = nullptr;
   unsigned long long* d_arr_sc = nullptr;
@@ -267,6 +272,7 @@ static nebula_status validate(const nebula_topology* t, const nebula_codec* c, c
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown method");
   if (c->error_feedback != 0 && c->error_feedback != 1)
     return fail(nullptr, NEBULA_ERR_INVALID_ARG, "error_feedback must be 0 or 1");
+  if (c->flags & ~NEBULA_CODEC_EXACT_TOPK) return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown codec flags");
   if (c->method == NEBULA_TOPK) {
     if (c->topk_values < NEBULA_VAL_F32 || c->topk_values > NEBULA_VAL_I8)
       return fail(nullptr, NEBULA_ERR_INVALID_ARG, "unknown topk value type");
@@ -326,7 +332,7 @@ static nebula_status build_tables(nebula_ctx* ctx, int lay) {
       const BucketInfo& bk = ctx->b[bi];
       for (int c = 0; c < ctx->Ploc; ++c) {  // bucket-major, cluster-minor
         Item it{};
-        if (ctx->G > 1) it.g_off = bk.coff;
+        if (ctx->G > 1 && !ctx->xtopk) it.g_off = bk.soff;
         else if (ctx->loopback) it.g_off = (t == 0) ? (uint64_t)c * ctx->total_n + bk.off : (uint64_t)c * bk.n;
         else it.g_off = (t == 0) ? bk.off : 0;
         it.r_off = (uint64_t)c * rtotal + bk.coff;
@@ -342,7 +348,7 @@ static nebula_status build_tables(nebula_ctx* ctx, int lay) {
       RItem ri{};
       ri.slot_off = bk.so[lay];
       ri.pb = bk.pb[lay];
-      ri.out_off = ctx->G > 1 ? bk.coff : (t == 0 ? bk.off : 0);
+      ri.out_off = (ctx->G > 1 && !ctx->xtopk) ? bk.soff : (t == 0 ? bk.off : 0);
       ri.n = bk.cn;
       ri.k = bk.k;
       ri.chunk0 = rt.chunks;
@@ -416,6 +422,7 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_shard_in);
   cudaFree(ctx->d_shard_out);
   cudaFree(ctx->d_recv);
+  cudaFree(ctx->d_full);
   cudaFree(ctx->d_arr_rs);
   cudaFree(ctx->d_arr_ag);
   cudaFree(ctx->d_arr_sc);
@@ -444,7 +451,7 @@ static void release(nebula_ctx* ctx) {
 // ranks agree (ncclMin) on whether every rank mapped every peer; if not, everybody closes its
 // mappings and keeps the NCCL collectives, so all ranks always use the same transport.
 struct P2PInfo {
-  cudaIpcMemHandle_t h[8];   // slots, arrive, recv, shard_out, arr_rs, arr_ag, arr_sc, mail
+  cudaIpcMemHandle_t h[9];   // slots, arrive, recv, shard_out, arr_rs, arr_ag, arr_sc, mail, shard_in
   int32_t device, ok, pad0, pad1;
 };
 
@@ -465,10 +472,10 @@ static nebula_status p2p_setup(nebula_ctx* ctx) {
   const int cl = ctx->topo.cluster_id, lr = ctx->local_rank, me = cl * G + lr;
   P2PInfo mine{};
   mine.device = ctx->device;
-  void* bufs[8] = {ctx->d_slots, ctx->d_arrive, ctx->d_recv, ctx->d_shard_out, ctx->d_arr_rs, ctx->d_arr_ag,
-                   ctx->d_arr_sc, ctx->d_mail};
+  void* bufs[9] = {ctx->d_slots, ctx->d_arrive, ctx->d_recv, ctx->d_shard_out, ctx->d_arr_rs, ctx->d_arr_ag,
+                   ctx->d_arr_sc, ctx->d_mail, ctx->d_shard_in};
   mine.ok = 1;
-  for (int k = 0; k < 8; ++k)
+  for (int k = 0; k < 9; ++k)
     if (bufs[k] && cudaIpcGetMemHandle(&mine.h[k], bufs[k]) != cudaSuccess) mine.ok = 0;
   cudaGetLastError();
   P2PInfo* d_info = nullptr;
@@ -504,6 +511,7 @@ static nebula_status p2p_setup(nebula_ctx* ctx) {
       ctx->ip_arr_ag[j] = ctx->d_arr_ag;
       ctx->ip_arr_sc[j] = ctx->d_arr_sc;
       ctx->ip_mail[j] = ctx->d_mail;
+      ctx->ip_in[j] = ctx->d_shard_in;
       continue;
     }
     intra_ok = q.ok && mine.ok && q.device != ctx->device;
@@ -513,6 +521,7 @@ static nebula_status p2p_setup(nebula_ctx* ctx) {
     ctx->ip_arr_ag[j] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[5], &intra_ok));
     ctx->ip_arr_sc[j] = static_cast<unsigned long long*>(ipc_open(ctx, q.h[6], &intra_ok));
     ctx->ip_mail[j] = static_cast<uint32_t*>(ipc_open(ctx, q.h[7], &intra_ok));
+    ctx->ip_in[j] = static_cast<float*>(ipc_open(ctx, q.h[8], &intra_ok));
   }
   // agree (every rank mapped every peer), else everybody unmaps and keeps NCCL
   int32_t ok2[2] = {inter_ok ? 1 : 0, intra_ok ? 1 : 0};
@@ -573,6 +582,7 @@ static nebula_status self_resolve(nebula_ctx* ctx) {
     ctx->ip_arr_ag[j] = q->d_arr_ag;
     ctx->ip_arr_sc[j] = q->d_arr_sc;
     ctx->ip_mail[j] = q->d_mail;
+    ctx->ip_in[j] = q->d_shard_in;
   }
   ctx->p2p_ok = P > 1;
   ctx->intra_p2p = G > 1;
@@ -637,11 +647,11 @@ static nebula_status build_itables(nebula_ctx* ctx) {
       const BucketInfo& bk = ctx->b[bi];
       IItem it{};
       it.off = t == 0 ? bk.off : 0;
-      it.coff = bk.coff;
-      it.cn = bk.cn;
+      it.coff = bk.soff;
+      it.cn = bk.sn;
       it.chunk0 = T.chunks;
-      T.chunks += (bk.cn + 4095) / 4096;
-      T.aligned &= (it.off % 4 == 0) && (bk.cn % 4 == 0);
+      T.chunks += (bk.sn + 4095) / 4096;
+      T.aligned &= (it.off % 4 == 0) && (bk.sn % 4 == 0);
       items.push_back(it);
     }
     T.count = (int)items.size() - T.first;
@@ -723,13 +733,17 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
 
     // ---- memory plan
     ctx->b.resize(num_buckets);
-    uint64_t off = 0, coff = 0, so = 0, so1 = 0;
+    ctx->xtopk = ctx->G > 1 && codec->method == NEBULA_TOPK && (codec->flags & NEBULA_CODEC_EXACT_TOPK);
+    uint64_t off = 0, coff = 0, soff = 0, so = 0, so1 = 0;
     for (int i = 0; i < num_buckets; ++i) {
       BucketInfo& bk = ctx->b[i];
       bk.n = bucket_numel[i];
-      bk.cn = bk.n / ctx->G;
+      bk.sn = bk.n / ctx->G;
+      bk.cn = ctx->xtopk ? bk.n : bk.sn;   // coded elements: the shard, or (R34) the whole bucket
       bk.off = off;
       bk.coff = coff;
+      bk.soff = soff;
+      soff += (bk.sn + 3) / 4 * 4;
       bk.k = codec->method == NEBULA_TOPK ? topk_k_of(bk.cn, *codec) : 0;
       bk.pb[0] = payload_bytes_for(codec->method, bk.cn, bk.k, codec->topk_values);
       bk.pb[1] = payload_bytes_for(M_IDENTITY, bk.cn, 0, 0);
@@ -743,6 +757,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     ctx->nlayouts = (codec->start_step > 0 && codec->method != NEBULA_IDENTITY) ? 2 : 1;
     ctx->total_n = off;
     ctx->total_cn = coff;
+    ctx->total_sn = soff;
     ctx->total_slots = ctx->nlayouts == 2 ? std::max(so, so1) : so;
 
     size_t rbytes = std::max<uint64_t>(16, (uint64_t)ctx->Ploc * ctx->total_cn * sizeof(float));
@@ -755,11 +770,15 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     if (cudaMemset(ctx->d_resid, 0, rbytes) != cudaSuccess || cudaMemset(ctx->d_slots, 0, halves * ctx->slot_span) != cudaSuccess ||
         cudaMemset(ctx->d_flags, 0, 16) != cudaSuccess) { ctx->err = "memset failed"; return bail(NEBULA_ERR_CUDA); }
     if (ctx->G > 1) {
-      if (cudaMalloc(&ctx->d_shard_in, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess ||
-          cudaMalloc(&ctx->d_shard_out, std::max<uint64_t>(16, ctx->total_cn * 4)) != cudaSuccess) { ctx->err = "shard allocation failed"; return bail(NEBULA_ERR_OOM); }
+      if (cudaMalloc(&ctx->d_shard_in, std::max<uint64_t>(16, ctx->total_sn * 4)) != cudaSuccess ||
+          cudaMalloc(&ctx->d_shard_out, std::max<uint64_t>(16, ctx->total_sn * 4)) != cudaSuccess ||
+          (ctx->xtopk && cudaMalloc(&ctx->d_full, std::max<uint64_t>(16, ctx->total_n * 4)) != cudaSuccess)) {
+        ctx->err = "shard allocation failed";
+        return bail(NEBULA_ERR_OOM);
+      }
       if (ctx->G <= 8) {   // intra-cluster P2P hop buffers (used when every peer can be mapped)
         const size_t aw = sizeof(unsigned long long) * (size_t)num_buckets * ctx->G;
-        if (cudaMalloc(&ctx->d_recv, std::max<uint64_t>(16, (uint64_t)ctx->G * ctx->total_cn * 4)) != cudaSuccess ||
+        if (cudaMalloc(&ctx->d_recv, std::max<uint64_t>(16, (uint64_t)ctx->G * ctx->total_sn * 4)) != cudaSuccess ||
             cudaMalloc(&ctx->d_arr_rs, aw) != cudaSuccess || cudaMalloc(&ctx->d_arr_ag, aw) != cudaSuccess ||
             cudaMalloc(&ctx->d_arr_sc, aw) != cudaSuccess ||
             cudaMalloc(&ctx->d_mail, sizeof(uint32_t) * (size_t)num_buckets * ctx->G) != cudaSuccess) {
@@ -882,9 +901,9 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
     for (int j = 0; j < ctx->G; ++j) recv.p[j] = ctx->ip_recv[j];
     recv.n = ctx->G;
     recv.me = ctx->local_rank;
-    launch_rs_push(L, vec, it, T.count, T.chunks, g, recv, ctx->total_cn);
+    launch_rs_push(L, vec, it, T.count, T.chunks, g, recv, ctx->total_sn);
     launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_rs), ctx->d_arr_rs, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_RS);
-    launch_rs_reduce(L, vec, it, T.count, T.chunks, g, ctx->d_recv, ctx->total_cn, ctx->G, ctx->local_rank,
+    launch_rs_reduce(L, vec, it, T.count, T.chunks, g, ctx->d_recv, ctx->total_sn, ctx->G, ctx->local_rank,
                      ctx->d_shard_in);
     CKC(cudaGetLastError());
     return NEBULA_OK;
@@ -894,9 +913,9 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
   CKN(ncclGroupStart());
   for (int i = lo; i < hi; ++i) {
     const BucketInfo& bk = ctx->b[i];
-    if (!bk.cn) continue;
+    if (!bk.sn) continue;
     const float* src = g + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
-    CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.coff, bk.cn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
+    CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.soff, bk.sn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
   }
   CKN(ncclGroupEnd());
   return NEBULA_OK;
@@ -905,12 +924,15 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
 // G > 1: every GPU of the cluster gathers the P2P-averaged shards into dev_out.  P2P: flag
 // handshake, then NVLink loads of the peers' shards; else NCCL AllGather.
 static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi, float* dev_out,
-                                      uint64_t seq) {
+                                      uint64_t seq, bool from_in = false) {
+  // from_in (xtopk): gather the G mean shards (d_shard_in) instead of the averaged ones
+  float* const* srcs = from_in ? ctx->ip_in : ctx->ip_out;
+  float* own = from_in ? ctx->d_shard_in : ctx->d_shard_out;
   if (intra_p2p_on(ctx)) {
     const ITable& T = ctx->itab[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
     launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_ag), ctx->d_arr_ag, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_AG);
     PeerF outs{};
-    for (int j = 0; j < ctx->G; ++j) outs.p[j] = ctx->ip_out[j];
+    for (int j = 0; j < ctx->G; ++j) outs.p[j] = srcs[j];
     outs.n = ctx->G;
     outs.me = ctx->local_rank;
     launch_ag_pull(L, T.aligned && (uintptr_t)dev_out % 16 == 0, ctx->d_iitems + T.first, T.count, T.chunks, outs, dev_out);
@@ -922,9 +944,9 @@ static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int32_t 
   CKN(ncclGroupStart());
   for (int i = lo; i < hi; ++i) {
     const BucketInfo& bk = ctx->b[i];
-    if (!bk.cn) continue;
+    if (!bk.sn) continue;
     float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
-    CKN(ncclAllGather(ctx->d_shard_out + bk.coff, dst, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
+    CKN(ncclAllGather(own + bk.soff, dst, bk.sn, ncclFloat32, ctx->intra, ctx->stream));
   }
   CKN(ncclGroupEnd());
   return NEBULA_OK;
@@ -977,6 +999,11 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
     nebula_status s = intra_reduce_scatter(ctx, L, bucket, lo, hi, dev_grad, seq);
     if (s != NEBULA_OK) return s;
     gbase = ctx->d_shard_in;
+    if (ctx->xtopk) {   // R34: every GPU of the cluster codes the whole cluster-mean bucket
+      s = intra_all_gather(ctx, L, bucket, lo, hi, ctx->d_full, seq, true);
+      if (s != NEBULA_OK) return s;
+      gbase = ctx->d_full;
+    }
   }
   const bool vec = T.aligned && ((uintptr_t)gbase % 16 == 0);
   const Item* items = ctx->d_items[lay] + T.first;
@@ -1077,7 +1104,8 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
   DevGuard dg(ctx->device);
   const int lay = layout_of(ctx, method);
   const Table& T = ctx->rtab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
-  float* obase = ctx->G > 1 ? ctx->d_shard_out : dev_out;
+  const bool sharded = ctx->G > 1 && !ctx->xtopk;   // reduce this GPU's shard, then all-gather
+  float* obase = sharded ? ctx->d_shard_out : dev_out;
   const bool vec = T.aligned && ((uintptr_t)obase % 16 == 0);
   const Launch L = launch_of(ctx);
   const RItem* items = ctx->d_ritems[lay] + T.first;
@@ -1086,9 +1114,9 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
     // output range of this call: buckets [lo, hi) are contiguous in the out buffer
     float* zb;
     uint64_t zc;
-    if (ctx->G > 1) {
-      zb = obase + ctx->b[lo].coff;
-      zc = (hi == (int)ctx->b.size() ? ctx->total_cn : ctx->b[hi].coff) - ctx->b[lo].coff;
+    if (sharded) {
+      zb = obase + ctx->b[lo].soff;
+      zc = (hi == (int)ctx->b.size() ? ctx->total_sn : ctx->b[hi].soff) - ctx->b[lo].soff;
     } else {
       zb = obase;
       zc = elems_of(ctx, lo, hi);
@@ -1101,7 +1129,7 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
   else
     launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, sources_of(ctx, ctx->b[lo]), obase);
   CKC(cudaGetLastError());
-  if (ctx->G > 1) {
+  if (sharded) {
     nebula_status s = intra_all_gather(ctx, L, bucket, lo, hi, dev_out, ctx->b[lo].seq);
     if (s != NEBULA_OK) return s;
   }
@@ -1124,7 +1152,8 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
     if (!(st == ST_EXCHANGED || (st == ST_COMPRESSED && own)))
       return fail(ctx, NEBULA_ERR_STATE, "decompress needs the slot's payload (compress / exchange first)");
   }
-  if (ctx->G > 1 && !ctx->intra)   // the shards are gathered with NCCL (no P2P sequence for this call)
+  const bool sharded = ctx->G > 1 && !ctx->xtopk;
+  if (sharded && !ctx->intra)   // the shards are gathered with NCCL (no P2P sequence for this call)
     return fail(ctx, NEBULA_ERR_UNSUPPORTED, "single-slot decompress with G > 1 needs the NCCL transport");
   DevGuard dg(ctx->device);
   const Launch L = launch_of(ctx);
@@ -1134,22 +1163,22 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
     const Table& T = ctx->rtab[lay][1 + i];
     const RItem* items = ctx->d_ritems[lay] + T.first;
     float* out_b = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
-    float* obase = ctx->G > 1 ? ctx->d_shard_out : out_b;
+    float* obase = sharded ? ctx->d_shard_out : out_b;
     const bool vec = T.aligned && ((uintptr_t)obase % 16 == 0);
     Dests src{};
     src.n = 1;
     src.p[0] = sources_of(ctx, bk).p[slot] + (uint64_t)slot * bk.pb[lay];   // slot c read as "cluster 0"
     if (method == M_TOPK) {
-      float* zb = ctx->G > 1 ? obase + bk.coff : obase;
+      float* zb = sharded ? obase + bk.soff : obase;
       launch_reduce_topk(L, ctx->codec.topk_values, 1, vec, items, T.count, T.entries, T.tiles, src, ctx->tk.start,
                          obase, zb, bk.cn, (bk.cn + 2047) / 2048 + 1, ctx->topk_reduce);
     } else {
       launch_reduce_dense(L, method, 1, vec, items, T.count, T.chunks, src, obase);
     }
     CKC(cudaGetLastError());
-    if (ctx->G > 1 && bk.cn) {
+    if (sharded && bk.sn) {
       Mark mk(L, PH_NCCL_AG);
-      CKN(ncclAllGather(ctx->d_shard_out + bk.coff, out_b, bk.cn, ncclFloat32, ctx->intra, ctx->stream));
+      CKN(ncclAllGather(ctx->d_shard_out + bk.soff, out_b, bk.sn, ncclFloat32, ctx->intra, ctx->stream));
     }
   }
   return NEBULA_OK;
@@ -1378,6 +1407,8 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     if (value < 0 || value > 3) return fail(ctx, NEBULA_ERR_INVALID_ARG, "exchange option must be in [0, 3]");
     if (ctx->loopback) return NEBULA_OK;   // nothing moves
     if (value >= 2 && !ctx->p2p_ok) return fail(ctx, NEBULA_ERR_UNSUPPORTED, "P2P not available (peers not mappable)");
+    if (value == 1 && ctx->self && ctx->P > 1)
+      return fail(ctx, NEBULA_ERR_UNSUPPORTED, "SELF transport has no NCCL communicator");
     for (const auto& bk : ctx->b)
       if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
     ctx->xopt = (int)value;

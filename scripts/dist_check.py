@@ -54,7 +54,8 @@ def main():
              (O.TOPK, O.VAL_I8, None, False, "p2p"), (O.TOPK, O.VAL_F16, None, False, "p2p"),
              (O.FP8, 0, "fused-ws", False, "p2p"), (O.QSGD, 0, "fused-ws", False, "p2p")]   # fused step over P2P (G = 1)
     if G > 1:
-        cases += [(O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"),
+        cases += [(O.TOPK, O.VAL_F32, None, "exact-topk", "p2p"), (O.TOPK, O.VAL_I8, None, "exact-topk", "nccl"),
+                  (O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"),
                   (O.TOPK, O.VAL_F32, None, False, "nccl"), (O.INT8, 0, None, True, "nccl")]
     intra_seen = set()
     modes_seen = set()
@@ -65,8 +66,10 @@ def main():
         # the oracle time (each rank recomputes every cluster's oracle step)
         sel_modes = modes if ci == 0 else (modes[ci % len(modes)], modes[(ci + 2) % len(modes)])
         for per_bucket, xch in sel_modes:
+            xtopk = exact == "exact-topk"
             ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
-                                                topk_values=vt, topk_density=0.05)
+                                                topk_values=vt, topk_density=0.05, exact_topk=xtopk)
+            exact = exact is True
             if kern:
                 ctx.set_int8_kernel(kern)
             if exact:
@@ -83,7 +86,7 @@ def main():
                     ctx.set_exchange("nccl")
             modes_seen.add(ctx.exchange_mode())
             codec = O.Codec(method=method, topk_values=vt, topk_density=0.05)
-            m = [s // G for s in sizes]
+            m = [s if xtopk else s // G for s in sizes]
             rs = [[[np.zeros(mb, np.float32) for mb in m] for _ in range(G)] for _ in range(P)]
             for t in range(args.steps):
                 # gradient of (cluster c, gpu l, bucket b)
@@ -119,7 +122,8 @@ def main():
                     else:
                         exp, r_new, pls = O.hierarchical_step([[grad(c, l, b) for l in range(G)] for c in range(P)],
                                                               [[rs[c][l][b] for l in range(G)] for c in range(P)],
-                                                              codec, t, exact_scale=exact, bucket=b)
+                                                              codec, t, exact_scale=exact, bucket=b,
+                                                              exact_topk=xtopk)
                         myr, mypl = r_new[cl][lr], pls[cl][lr]
                         for c in range(P):
                             for l in range(G):

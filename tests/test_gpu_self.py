@@ -37,13 +37,13 @@ def _sync(grid):
 
 
 def run_self(nb, method, P, G, sizes, *, steps=2, vt=0, rho=0.05, exchange="auto", per_bucket=False,
-             exact=False, int8_kernel="two-pass", kind="model-like", sr_seed=0, ef=True):
+             exact=False, int8_kernel="two-pass", kind="model-like", sr_seed=0, ef=True, exact_topk=False):
     import torch
     grid = nb.self_group(sizes, num_clusters=P, gpus_per_cluster=G, device=0, method=method, topk_values=vt,
-                         topk_density=rho, error_feedback=ef)
+                         topk_density=rho, error_feedback=ef, exact_topk=exact_topk)
     for row in grid:
         for ctx in row:
-            if method in (O.INT8, O.FP8, O.QSGD):
+            if method in (O.INT8, O.FP8, O.QSGD, O.FP8_E5M2):
                 ctx.set_int8_kernel(int8_kernel)
             if P > 1:
                 ctx.set_exchange(exchange)
@@ -53,7 +53,7 @@ def run_self(nb, method, P, G, sizes, *, steps=2, vt=0, rho=0.05, exchange="auto
                 ctx.set_sr_seed(sr_seed)
     codec = O.Codec(method=method, topk_values=vt, topk_density=rho, sr_seed=sr_seed, error_feedback=ef)
     total = sum(sizes)
-    m = [s // G for s in sizes]
+    m = [s if exact_topk else s // G for s in sizes]   # coded elements per GPU (R34: the whole bucket)
     rs = [[[np.zeros(mb, F32) for mb in m] for _ in range(G)] for _ in range(P)]
     modes = {grid[0][0].exchange_mode()}
     for t in range(steps):
@@ -97,7 +97,7 @@ def run_self(nb, method, P, G, sizes, *, steps=2, vt=0, rho=0.05, exchange="auto
             else:
                 exp, r_new, pls = O.hierarchical_step([[grad(c, l, b) for l in range(G)] for c in range(P)],
                                                       [[rs[c][l][b] for l in range(G)] for c in range(P)], codec, t,
-                                                      exact_scale=exact, bucket=b)
+                                                      exact_scale=exact, bucket=b, exact_topk=exact_topk)
             assert np.array_equal(ref[off:off + n].view(np.uint32), exp.view(np.uint32)), \
                 f"out mismatch bucket {b} step {t}: {np.flatnonzero(ref[off:off + n].view(np.uint32) != exp.view(np.uint32))[:8]}"
             for c in range(P):
@@ -134,7 +134,7 @@ def test_self_p2p_exchange_int8(nb, P, exchange, per_bucket):
     assert modes == {"p2p-" + exchange}
 
 
-@pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.IDENTITY, 0), (O.FP8, 0), (O.QSGD, 0),
+@pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.IDENTITY, 0), (O.FP8, 0), (O.QSGD, 0), (O.FP8_E5M2, 0),
                                        (O.TOPK, O.VAL_F32), (O.TOPK, O.VAL_F16), (O.TOPK, O.VAL_I8)])
 @pytest.mark.parametrize("exchange", ["push", "pull"])
 def test_self_p2p_exchange_codecs(nb, method, vt, exchange):
@@ -156,12 +156,23 @@ def test_self_hierarchical_codecs(nb, method, vt):
              sr_seed=9 if method == O.QSGD else 0)
 
 
-@pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD])
+@pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD, O.FP8_E5M2])
 @pytest.mark.parametrize("P,G", [(2, 2), (1, 4)])
 def test_self_exact_cluster_scale(nb, method, P, G):
     """NEXT-3 (R28): every shard quantises with the scale of the whole cluster bucket; the G
     shards' max words meet in the P2P mailbox kernel."""
     run_self(nb, method, P, G, [s * G for s in [4096, 300004, 8]], exact=True, sr_seed=3 if method == O.QSGD else 0)
+
+
+@pytest.mark.parametrize("vt", [O.VAL_F32, O.VAL_F16, O.VAL_I8])
+@pytest.mark.parametrize("P,G", [(2, 2), (1, 4), (2, 4)])
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_self_exact_cluster_topk(nb, vt, P, G, per_bucket):
+    """NEXT-3 (R34): with NEBULA_CODEC_EXACT_TOPK every GPU selects the top-k of the WHOLE
+    cluster bucket (fixed-order P2P mean, all-gathered), so payloads, the cluster's full
+    residual and the average equal the oracle's global selection bit for bit."""
+    run_self(nb, O.TOPK, P, G, [s * G for s in [4096, 300004, 8, 12288]], vt=vt, rho=0.02, per_bucket=per_bucket,
+             exact_topk=True, steps=3)
 
 
 def test_self_state_rules(nb):
