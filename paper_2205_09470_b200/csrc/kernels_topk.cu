@@ -36,7 +36,8 @@
 namespace nb {
 
 constexpr int kSelThreads = 1024;  // single-CTA radix select
-constexpr int kMergeTile = 1024;   // outputs per merge CTA
+constexpr int kMergeThreads = 256, kMergeVT = 8;
+constexpr int kMergeTile = kMergeThreads * kMergeVT;   // 2048 outputs per merge CTA
 constexpr int kRedTile = 2048;     // elements per sparse-reduce CTA
 
 // tile words: (winners << 32) | candidates — per-tile counts, then exclusive prefixes
@@ -346,11 +347,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
     float* r = rbase + it.r_off;
     uint32_t kb[kQuadsPerThread][4];
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
-    // winners' residual written here (ADVICE/VERDICT r1: the merge's scattered residual writes
-    // at the k selected positions were a full residual RMW at 10 %): a winner (key > t_hi) is
-    // selected for sure, so for f32 / f16 values r = p - D(v) is known now (D needs no bucket
-    // scale); int8 values need the bucket max, so their residual stays with the merge
-    const int vtv = (int)titems[i].value_type;
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
       const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
@@ -367,9 +363,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
       uint32_t wn = 0, cn = 0;
       if (q < n4) {
         float4 p = gv[u];
-        if constexpr (EF)
+        if constexpr (EF) {
           p = make_float4(__fadd_rn(p.x, rv[u].x), __fadd_rn(p.y, rv[u].y), __fadd_rn(p.z, rv[u].z),
                           __fadd_rn(p.w, rv[u].w));
+          st4(r + 4 * q, p);
+        }
         kb[u][0] = __float_as_uint(p.x); kb[u][1] = __float_as_uint(p.y);
         kb[u][2] = __float_as_uint(p.z); kb[u][3] = __float_as_uint(p.w);
 #pragma unroll
@@ -390,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
     if (has_tail) {
       const uint64_t e = n4 * 4 + threadIdx.x;
       const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      if constexpr (EF) r[e] = p;
       tkb = __float_as_uint(p);
       const uint32_t key = tkb & 0x7FFFFFFFu;
       m = max(m, key);
@@ -433,36 +432,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restri
     if (fits) pos += staged;
     if (threadIdx.x == 0) {
       counts[ti.status_off + j] = pack_wc(tileW, tileC);
-      soff[ti.status_off + j] = base | (fits ? 0ull : (1ull << 63));   // bit 63: entries not staged
+      soff[ti.status_off + j] = base;
       if (!fits) atomicOr(&st[i].stage_ovf, 1u);   // this bucket goes to the exact fallback
-    }
-    if constexpr (EF) {
-      // r <- p, or the final residual of a staged winner (restored to p by k_topk_restore if
-      // this bucket later falls back to the exact radix path)
-      const bool wres = fits && vtv != V_I8;
-#pragma unroll
-      for (int u = 0; u < kQuadsPerThread; ++u) {
-        const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
-        if (q < n4) {
-          float o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float pe = __uint_as_float(kb[u][e]);
-            o[e] = pe;
-            if (wres && (kb[u][e] & 0x7FFFFFFFu) > t_hi) {
-              const float de = vtv == V_F32 ? pe : __half2float(__float2half_rn(pe));
-              o[e] = __fsub_rn(pe, de);
-            }
-          }
-          st4(r + 4 * q, make_float4(o[0], o[1], o[2], o[3]));
-        }
-      }
-      if (has_tail) {
-        const float pe = __uint_as_float(tkb);
-        float o = pe;
-        if (wres && (tkb & 0x7FFFFFFFu) > t_hi) o = __fsub_rn(pe, vtv == V_F32 ? pe : __half2float(__float2half_rn(pe)));
-        r[n4 * 4 + threadIdx.x] = o;
-      }
     }
     if (staged && fits) {
       uint2* S = stage;
@@ -525,7 +496,7 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
   if (!(W + C)) return;
   const unsigned long long pf = pref[ti.status_off + j];
   const uint64_t pw = pf >> 32, pc = pf & 0xFFFFFFFFull;
-  const uint2* src = stage + (soff[ti.status_off + j] & ~(1ull << 63));
+  const uint2* src = stage + soff[ti.status_off + j];
   uint2* dw = wl + ti.list_off;
   uint2* dc = cl + ti.list_off;
   for (uint32_t x = lane; x < W; x += 32)
@@ -533,39 +504,6 @@ __global__ void __launch_bounds__(256) k_topk_move(const Item* __restrict__ aite
   if (!tie_mode)
     for (uint32_t x = lane; x < C; x += 32)
       if (pc + x < ti.ccap) dc[pc + x] = src[W + x];
-}
-
-// ---------------------------------------------------------------- R: undo winners' residuals
-// Buckets that fall back to the exact radix path (bracket failed / staging overflowed) re-read
-// p from r, but the stage pass already stored the final residual at its staged winners: put p
-// back (the staged entries hold p's bits).  One warp per chunk; a no-op unless any_failed.
-__global__ void __launch_bounds__(256) k_topk_restore(const Item* __restrict__ aitems,
-                                                      const TopkItem* __restrict__ titems,
-                                                      const TopkState* __restrict__ st, int nitems, uint64_t chunks,
-                                                      const unsigned long long* __restrict__ counts,
-                                                      const unsigned long long* __restrict__ soff,
-                                                      const uint2* __restrict__ stage, float* __restrict__ rbase,
-                                                      const uint32_t* any_failed) {
-  if (*((volatile const uint32_t*)any_failed) == 0) return;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < chunks;
-       c += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-    int lo = 0, hi = nitems - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (aitems[mid].chunk0 <= c) lo = mid; else hi = mid - 1;
-    }
-    const TopkItem& ti = titems[lo];
-    const TopkState& S = st[lo];
-    if (S.mode != 1 || S.failed == 2 || ti.value_type == V_I8) continue;
-    const uint64_t j = c - aitems[lo].chunk0;
-    const unsigned long long so = soff[ti.status_off + j];
-    if (so >> 63) continue;                        // nothing was staged (nor overwritten) here
-    const uint32_t W = (uint32_t)(counts[ti.status_off + j] >> 32);
-    const uint2* src = stage + so;
-    float* r = rbase + aitems[lo].r_off;
-    for (uint32_t x = lane; x < W; x += 32) r[src[x].x] = __uint_as_float(src[x].y);
-  }
 }
 
 // ---------------------------------------------------------------- X: scan tile counts
@@ -952,13 +890,19 @@ __global__ void k_topk_splits(const TopkItem* __restrict__ titems, const TopkSta
   splits[x] = merge_split(wl + ti.list_off, W, cl + ti.list_off, Ns, d);
 }
 
+// Merge of one 2048-output tile (ModernGPU-style): the tile's ranges of the two ascending lists
+// are staged in shared memory; each of the 256 threads finds its 8-output diagonal on the merge
+// path (one binary search per thread, not per output) and merges its 8 outputs serially into a
+// shared output buffer; the tile is then written with coalesced stores — index section,
+// value section (f32 / RNE binary16 / int8 with the bucket scale), and the residual
+// r = p - D(v) at the selected positions (ascending addresses within the tile).
 template <bool EF>
-__global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __restrict__ titems,
+__global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __restrict__ titems,
                                                            const TopkState* __restrict__ st, int nitems, uint64_t tbase,
                                                            const uint2* __restrict__ wl, const uint2* __restrict__ cl,
                                                            Dests dst, float* __restrict__ rbase, uint32_t* flags,
                                                            const uint64_t* __restrict__ splits) {
-  __shared__ uint2 sw[kMergeTile], ss[kMergeTile];
+  __shared__ uint2 sab[kMergeTile], so[kMergeTile];   // sab: the A range, then the B range (na + nb = nout)
   __shared__ uint64_t s_split[2];
   const uint64_t t = tbase + blockIdx.x;
   int i = 0;
@@ -973,50 +917,60 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
   const TopkItem ti = titems[i];
   const TopkState& S = st[i];
   if (S.failed == 2) return;
-  const uint64_t so = ti.slot_off;
+  const uint64_t so_off = ti.slot_off;
   if (ti.k == 0) {
     if (threadIdx.x == 0) {
-      put_preamble(dst, so, M_TOPK, 0u, 1.0f, ti.value_type);
+      put_preamble(dst, so_off, M_TOPK, 0u, 1.0f, ti.value_type);
       if (dst.n > 1) __threadfence_system();
     }
     return;
   }
-  const uint64_t k = ti.k, W = S.wcount, Ns = k - W;
+  const uint64_t k = ti.k;
   const uint64_t d0 = (t - ti.mt0) * kMergeTile, d1 = d0 + kMergeTile < k ? d0 + kMergeTile : k;
   const uint2* A = wl + ti.list_off;
   const uint2* B = cl + ti.list_off;
   if (threadIdx.x < 2) s_split[threadIdx.x] = splits[2 * blockIdx.x + threadIdx.x];
   __syncthreads();
-  (void)W; (void)Ns;
   const uint64_t a0 = s_split[0], a1 = s_split[1], b0 = d0 - a0, b1 = d1 - a1;
-  const uint32_t na = (uint32_t)(a1 - a0), nbb = (uint32_t)(b1 - b0);
-  if (threadIdx.x < na) sw[threadIdx.x] = A[a0 + threadIdx.x];
-  if (threadIdx.x < nbb) ss[threadIdx.x] = B[b0 + threadIdx.x];
+  const uint32_t na = (uint32_t)(a1 - a0), nbb = (uint32_t)(b1 - b0), nout = (uint32_t)(d1 - d0);
+  uint2* sa = sab;
+  uint2* sb = sab + na;
+  for (uint32_t x = threadIdx.x; x < na; x += kMergeThreads) sa[x] = A[a0 + x];
+  for (uint32_t x = threadIdx.x; x < nbb; x += kMergeThreads) sb[x] = B[b0 + x];
+  __syncthreads();
+  {
+    const uint32_t diag = threadIdx.x * kMergeVT;
+    if (diag < nout) {
+      // number of A entries among the first `diag` outputs of this tile (indices are distinct)
+      uint32_t lo = diag > nbb ? diag - nbb : 0, hi = diag < na ? diag : na;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sa[mid].x < sb[diag - 1 - mid].x) lo = mid + 1;
+        else hi = mid;
+      }
+      uint32_t ia = lo, ib = diag - lo;
+#pragma unroll
+      for (int v = 0; v < kMergeVT; ++v) {
+        if (diag + v < nout) {
+          const bool takeA = ib >= nbb || (ia < na && sa[ia].x < sb[ib].x);
+          so[diag + v] = takeA ? sa[ia] : sb[ib];
+          ia += takeA;
+          ib += !takeA;
+        }
+      }
+    }
+  }
   __syncthreads();
   const int vt = (int)ti.value_type;
   const float s = S.scale;
   const float sinv = int8_inv(s);
-  if (d0 == 0 && threadIdx.x == 0) put_preamble(dst, so, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
-  const uint64_t io = so + 16, vo = so + 16 + pad16(4 * k);   // idx / value section offsets
+  if (d0 == 0 && threadIdx.x == 0) put_preamble(dst, so_off, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
+  const uint64_t io = so_off + 16, vo = so_off + 16 + pad16(4 * k);   // idx / value section offsets
   float* r = rbase + ti.r_off;
   bool ovf = false;
-  const uint32_t x = threadIdx.x;
-  if (x < na + nbb) {
-    uint2 e;
-    uint32_t pos;
-    if (x < na) {  // lower_bound of sw[x].x in ss
-      e = sw[x];
-      uint32_t lo = 0, hi = nbb;
-      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (ss[mid].x < e.x) lo = mid + 1; else hi = mid; }
-      pos = x + lo;
-    } else {
-      const uint32_t y = x - na;
-      e = ss[y];
-      uint32_t lo = 0, hi = na;
-      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (sw[mid].x < e.x) lo = mid + 1; else hi = mid; }
-      pos = y + lo;
-    }
-    const uint64_t o = d0 + pos;
+  for (uint32_t x = threadIdx.x; x < nout; x += kMergeThreads) {
+    const uint2 e = so[x];
+    const uint64_t o = d0 + x;
     const float pv = __uint_as_float(e.y);
     put(dst, io + 4 * o, e.x);
     float dv;
@@ -1026,7 +980,7 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
     } else if (vt == V_F16) {
       __half h = __float2half_rn(pv);
       const uint16_t hb = __half_as_ushort(h);
-      ovf = (hb & 0x7FFFu) == 0x7C00u;
+      ovf |= (hb & 0x7FFFu) == 0x7C00u;
       put(dst, vo + 2 * o, hb);
       dv = __half2float(h);
     } else {
@@ -1034,10 +988,7 @@ __global__ void __launch_bounds__(kMergeTile) k_topk_merge(const TopkItem* __res
       put(dst, vo + o, (uint8_t)(q & 0xFF));
       dv = __fmul_rn((float)q, s);
     }
-    // winners of a bracket-path bucket already hold their residual (stage pass), except for
-    // int8 values whose decode needs the bucket scale
-    if constexpr (EF)
-      if (!(x < na && S.mode == 0 && vt != V_I8)) r[e.x] = __fsub_rn(pv, dv);
+    if constexpr (EF) r[e.x] = __fsub_rn(pv, dv);
   }
   // zero the padding of the two sections (the tile that ends the item)
   if (d1 == k) {
@@ -1461,8 +1412,6 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
     Mark mk(L, PH_TOPK_FALLBACK);
-    if (EF)
-      k_topk_restore<<<gsm, 256, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, B.status, B.soff, B.stage, r, anyf);
     for (int d = 0; d < 3; ++d) {
       k_topk_hist<VEC><<<gh, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g,
                                                       B.hist + (size_t)item0 * 2048, d, anyf);
@@ -1478,9 +1427,9 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   const uint64_t tbase = B.host_mt0[item0];
   k_topk_splits<<<(unsigned)((2 * merge_tiles + 255) / 256), 256, 0, L.stream>>>(ti, st, nitems, tbase, merge_tiles,
                                                                                 B.wlist, B.clist, B.splits);
-  k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeTile, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots,
+  k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeThreads, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots,
                                                                       r, flags, B.splits);
-  *L.launches += EF ? 19 : 18;
+  *L.launches += 18;
 }
 
 static void touch_t(const void* f) {
@@ -1505,7 +1454,7 @@ void preload_topk() {
     touch_t(f);
   touch_t((const void*)k_topk_stage<true, true>); touch_t((const void*)k_topk_stage<true, false>);
   touch_t((const void*)k_topk_stage<false, true>); touch_t((const void*)k_topk_stage<false, false>);
-  touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan); touch_t((const void*)k_topk_restore);
+  touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan);
   touch_t((const void*)k_topk_write<true>); touch_t((const void*)k_topk_write<false>);
   touch_t((const void*)k_topk_resolve);
   touch_t((const void*)k_topk_hist<true>); touch_t((const void*)k_topk_hist<false>);
