@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const uint64_t q = sa_.q0 + (uint64_t)ka * kWsTQ;
             const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sa_.q1 - q);
             mbar_expect_tx(&fullA[st], nq * (EF ? 32u : 16u));
-            bulk_g2s(ringA[st].g, gbase + it.g_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
+            // without EF the quantise warps re-read g (ring B): keep it in L2 (clean lines, no
+            // write-back) so that re-read is an L2 hit — 5 B/elem of DRAM instead of 9
+            bulk_g2s(ringA[st].g, gbase + it.g_off + 4 * q, nq * 16u, &fullA[st], EF ? pol_stream : pol_keep);
             if (EF) bulk_g2s(ringA[st].r, rbase + it.r_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
             ++fa;
             ++ka;
