@@ -14,7 +14,7 @@ enum Phase : int {
   PH_TOPK_RESOLVE, PH_TOPK_FALLBACK, PH_TOPK_MERGE, PH_REDUCE_DENSE, PH_TOPK_OFFSETS, PH_TOPK_REDUCE,
   PH_NCCL_EXCHANGE, PH_NCCL_RS, PH_NCCL_AG, PH_MEMSET, PH_INT8_ONCHIP, PH_P2P_FLAGS, PH_INT8_STEP, PH_FP8_QUANT,
   PH_NCCL_SCALE, PH_QSGD_QUANT, PH_RS_PUSH, PH_RS_REDUCE, PH_AG_PULL, PH_SCALE_MAIL,
-  PH_P2P_FLAGS_RS, PH_P2P_FLAGS_AG, PH_COUNT
+  PH_P2P_FLAGS_RS, PH_P2P_FLAGS_AG, PH_FP16_STEP, PH_COUNT
 };
 
 struct Launch {
@@ -105,6 +105,13 @@ void launch_int8_step(const Launch& L, bool ef, const Item* items, int nitems, c
                       const Dests& dst, uint32_t* scratch, uint32_t* flags, uint32_t* bar_words, const RItem* ritems,
                       int b0, int PL, const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive,
                       uint64_t seq, int config, int kind, const SrArgs& sr);   // kind 0 INT8, 1 E4M3, 2 QSGD, 3 E5M2
+
+// Fused FP16 step (compress + LOOPBACK / P2P-pull exchange + average in one cooperative kernel);
+// config 0 LOOPBACK warp split, 1 P2P pull.  bar_words: nitems words.
+void launch_fp16_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                      const Dests& dst, uint32_t* flags, uint32_t* bar_words, const RItem* ritems, int b0, int PL,
+                      const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive, uint64_t seq,
+                      int config);
 
 // For buckets [lo, hi): tell every peer that this cluster's payloads of exchange `seq` are in
 // its slots (system-scope release), then wait until every peer said the same to us.

@@ -205,7 +205,9 @@ __device__ __forceinline__ void ws_reduce_tma(const StepArgs& a, int nb, int ct,
 template <int P, int F8 = 0>
 __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, int nC, float* s_sc,
                                                volatile uint32_t* s_abort, float* s_out, uint32_t* flags) {
-  constexpr int E = 16, SROW = E + 1, U = P <= 2 ? 2 : 1;
+  // F8: 0 INT8 / QSGD bytes, 1 E4M3, 2 E5M2, 3 FP16 (2-byte codes, no scale).  E elements per
+  // 16-byte group; a CTA's quad slice is 4-quad aligned, so groups never straddle two CTAs.
+  constexpr int E = F8 == 3 ? 8 : 16, QPG = E / 4, SROW = E + 1, U = P <= 2 ? 2 : 1;
   const unsigned G = gridDim.x;
   const int lane = ct & 31, cw = ct >> 5, ncw = nC / 32;
   float* sw = s_out + cw * 32 * SROW;
@@ -239,7 +241,7 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
       }
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        scb[k] = *reinterpret_cast<volatile const float*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 8);
+        scb[k] = F8 == 3 ? 1.0f : *reinterpret_cast<volatile const float*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 8);
     }
     named_sync(3, nC);
     if (*s_abort) return;
@@ -248,12 +250,27 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
     for (int k = 0; k < P; ++k) sc[k] = scb[k];
     const uint64_t n4 = it.n >> 2;
     const Slice sl = slice_of(n4, G);
-    const uint64_t g0 = sl.q0 >> 2, g1 = sl.q1 >> 2;   // whole 16-element groups of this slice
+    const uint64_t g0 = sl.q0 / QPG, g1 = sl.q1 / QPG;   // whole E-element groups of this slice
     float* out = a.obase + it.out_off;
     auto slot = [&](int k, uint64_t gi) { return a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + 16 * gi; };
     auto dec = [&](const uint4& x4, int e, float s) {
-      const uint32_t x = (e >> 2) == 0 ? x4.x : (e >> 2) == 1 ? x4.y : (e >> 2) == 2 ? x4.z : x4.w;
-      return dec_byte<F8>(x >> (8 * (e & 3)), s);
+      if constexpr (F8 == 3) {
+        const uint32_t x = (e >> 1) == 0 ? x4.x : (e >> 1) == 1 ? x4.y : (e >> 1) == 2 ? x4.z : x4.w;
+        return __half2float(__ushort_as_half((unsigned short)((e & 1) ? (x >> 16) : (x & 0xFFFFu))));
+      } else {
+        const uint32_t x = (e >> 2) == 0 ? x4.x : (e >> 2) == 1 ? x4.y : (e >> 2) == 2 ? x4.z : x4.w;
+        return dec_byte<F8>(x >> (8 * (e & 3)), s);
+      }
+    };
+    auto store_groups = [&](uint64_t gw0, uint64_t gend) {   // the warp's 32 groups from the transpose buffer
+#pragma unroll
+      for (int v = 0; v < E / 4; ++v) {
+        const int qq = v * 32 + lane, src_lane = qq / QPG, src_e = (qq % QPG) * 4;
+        if (gw0 + src_lane < gend) {
+          const float* r = sw + src_lane * SROW + src_e;
+          st4_hint(out + 4 * (gw0 * QPG + qq), make_float4(r[0], r[1], r[2], r[3]), pol);
+        }
+      }
     };
     for (uint64_t gb = g0 + (uint64_t)cw * 32 * U; gb < g1; gb += (uint64_t)ncw * 32 * U) {
       if constexpr (P <= 4) {
@@ -277,15 +294,7 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
             sw[lane * SROW + e] = div_p<P>(tree_sum<0, P>(t));
           }
           __syncwarp();
-          const uint64_t gw0 = gb + u * 32;
-#pragma unroll
-          for (int v = 0; v < E / 4; ++v) {
-            const int qq = v * 32 + lane, src_lane = qq >> 2, src_e = (qq & 3) * 4;
-            if (gw0 + src_lane < g1) {
-              const float* r = sw + src_lane * SROW + src_e;
-              st4_hint(out + 4 * (gw0 * 4 + qq), make_float4(r[0], r[1], r[2], r[3]), pol);
-            }
-          }
+          store_groups(gb + u * 32, g1);
           __syncwarp();
         }
       } else {
@@ -319,26 +328,25 @@ __device__ __forceinline__ void ws_reduce_ld(const StepArgs& a, int nb, int ct, 
           }
         }
         __syncwarp();
-#pragma unroll
-        for (int v = 0; v < E / 4; ++v) {
-          const int qq = v * 32 + lane, src_lane = qq >> 2, src_e = (qq & 3) * 4;
-          if (gb + src_lane < g1) {
-            const float* r = sw + src_lane * SROW + src_e;
-            st4_hint(out + 4 * (gb * 4 + qq), make_float4(r[0], r[1], r[2], r[3]), pol);
-          }
-        }
+        store_groups(gb, g1);
         __syncwarp();
       }
     }
-    // the < 16 elements after the last whole group of the bucket
-    if (blockIdx.x == G - 1 && ct < 16) {
-      const uint64_t e = 16 * (n4 >> 2) + ct;
+    // the < E elements after the last whole group of the bucket
+    if (blockIdx.x == G - 1 && ct < E) {
+      const uint64_t e = (uint64_t)E * (n4 / QPG) + ct;
       if (e < it.n) {
         float v[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          const uint8_t q = *reinterpret_cast<volatile const uint8_t*>(a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16 + e);
-          v[k] = dec_byte<F8>(q, sc[k]);
+          const uint8_t* body = a.src.p[k] + it.slot_off + (uint64_t)k * it.pb + 16;
+          if constexpr (F8 == 3) {
+            const unsigned short hb = *reinterpret_cast<volatile const unsigned short*>(body + 2 * e);
+            v[k] = __half2float(__ushort_as_half(hb));
+          } else {
+            const uint8_t q = *reinterpret_cast<volatile const uint8_t*>(body + e);
+            v[k] = dec_byte<F8>(q, sc[k]);
+          }
         }
         out[e] = div_p<P>(tree_sum<0, P>(v));
       }
@@ -660,6 +668,177 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 }
 
 
+// ----------------------------------------------------------------------------- FP16 step
+// FP16 compress + exchange + average in ONE cooperative kernel (LOOPBACK or P2P pull; the
+// FP16 analogue of the fused INT8 step).  FP16 needs no bucket-wide scale, so the compress side
+// streams without a grid barrier:
+//   warp 0           producer: TMA ring of the g and r tiles of the CTA's slice of item t
+//   warps 1..AW      p = g + r, h = RNE16(p) -> payload (8 B per quad), r <- p - h; when the CTA's
+//                    slice of item t is done: fence, ARRIVE on bdone[t]; the last CTA to arrive
+//                    publishes bucket t to the peers (system-scope release of the arrival word)
+//   CW warps         reduce role (ws_reduce_ld<P, 3>): per bucket wait for bdone and, P2P, for
+//                    every peer's arrival word, load the P payloads (peers' over NVLink, 16-B
+//                    loads), tree-sum, divide, store — overlapping the NVLink-bound pull of bucket
+//                    b with the HBM-bound compress of bucket b + 1.
+template <bool EF, int AW, int CW>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_fp16_step(const Item* __restrict__ items, int nitems, const float* __restrict__ gbase, float* __restrict__ rbase,
+                Dests dst, uint32_t* flags, StepArgs sa) {
+  static_assert(1 + AW + CW == kWsThreads / 32, "warp roles must fill the CTA");
+  constexpr int kA = AW * 32, kC = CW * 32;
+  extern __shared__ __align__(128) unsigned char f16s_smem[];
+  WsStageA* ringA = reinterpret_cast<WsStageA*>(f16s_smem);
+  __shared__ __align__(8) uint64_t fullA[kWsNA], emptyA[kWsNA];
+  __shared__ float s_sc[16];
+  __shared__ volatile uint32_t s_abort;
+  __shared__ float s_out[CW * 32 * 9];
+  const unsigned G = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], AW); }
+    s_abort = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+  auto tiles_of = [&](int t, Slice& sl) {
+    sl = slice_of(items[t].n >> 2, G);
+    return (int)((sl.q1 - sl.q0 + kWsTQ - 1) / kWsTQ);
+  };
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane != 0) return;
+    uint32_t fa = 0;
+    for (int t = 0; t < nitems; ++t) {
+      Slice sl;
+      const int nt = tiles_of(t, sl);
+      const Item it = items[t];
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t st = fa % kWsNA, use = fa / kWsNA;
+        if (use) mbar_wait(&emptyA[st], (use - 1) & 1u);
+        const uint64_t q = sl.q0 + (uint64_t)k * kWsTQ;
+        const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q);
+        mbar_expect_tx(&fullA[st], nq * (EF ? 32u : 16u));
+        bulk_g2s(ringA[st].g, gbase + it.g_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
+        if (EF) bulk_g2s(ringA[st].r, rbase + it.r_off + 4 * q, nq * 16u, &fullA[st], pol_stream);
+        ++fa;
+      }
+    }
+    return;
+  }
+  if (warp <= AW) {
+    // ------------------------------------------------------------------ compress warps
+    const int at = threadIdx.x - 32;
+    bool bad = false, ovf = false;
+    uint32_t fa = 0;
+    for (int t = 0; t < nitems; ++t) {
+      Slice sl;
+      const int nt = tiles_of(t, sl);
+      const Item it = items[t];
+      const float* g = gbase + it.g_off;
+      float* r = rbase + it.r_off;
+      const uint64_t bo = it.slot_off + 16;
+      if (blockIdx.x == 0 && at == 0) put_preamble(dst, it.slot_off, M_FP16, (uint32_t)it.n, 1.0f, 0u);
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t st = fa % kWsNA, use = fa / kWsNA;
+        mbar_wait(&fullA[st], use & 1u);
+        const uint64_t q0 = sl.q0 + (uint64_t)k * kWsTQ;
+        const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sl.q1 - q0);
+        const WsStageA& S = ringA[st];
+        for (uint32_t j = at; j < nq; j += kA) {
+          const float4 p = EF ? add4(S.g[j], S.r[j]) : S.g[j];
+          uint16_t h0, h1, h2, h3;
+          float4 d;
+          d.x = fp16_one(p.x, h0, bad, ovf);
+          d.y = fp16_one(p.y, h1, bad, ovf);
+          d.z = fp16_one(p.z, h2, bad, ovf);
+          d.w = fp16_one(p.w, h3, bad, ovf);
+          // the reduce role re-reads this payload from L2 (local) or a peer pulls it (NVLink)
+          const uint2 packed = make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16));
+          asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(dst.p[0] + bo + 8 * (q0 + j)),
+                       "r"(packed.x), "r"(packed.y), "l"(pol_keep) : "memory");
+          if constexpr (EF)
+            st4_hint(r + 4 * (q0 + j),
+                     make_float4(__fsub_rn(p.x, d.x), __fsub_rn(p.y, d.y), __fsub_rn(p.z, d.z), __fsub_rn(p.w, d.w)),
+                     pol_stream);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[st]);
+        ++fa;
+      }
+      if (blockIdx.x == G - 1) {   // tail elements (n % 4) and the 16-byte padding
+        if (at < (int)(it.n & 3)) {
+          const uint64_t e = (it.n >> 2) * 4 + at;
+          const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+          uint16_t hb;
+          const float d = fp16_one(p, hb, bad, ovf);
+          put(dst, bo + 2 * e, hb);
+          if constexpr (EF) r[e] = __fsub_rn(p, d);
+        }
+        zero_padding_t(dst, bo, 2 * it.n, at);
+      }
+      named_sync(1, kA);
+      if (at == 0) {
+        __threadfence_system();   // payload (incl. the peers' view of it) before the counter / flag
+        const unsigned old = atomicAdd(&sa.bdone[t], 1u);
+        if (old == G - 1 && sa.pe.n > 1) {
+          __threadfence_system();
+          for (int c = 0; c < sa.pe.n; ++c)
+            if (c != sa.pe.me) st_release_sys_u64(sa.pe.arrive[c] + (size_t)(sa.b0 + t) * sa.pe.n + sa.pe.me, sa.seq);
+        }
+      }
+    }
+    raise_flags(flags, bad, ovf);
+    return;
+  }
+  // -------------------------------------------------------------------- reduce warps
+  const int ct = threadIdx.x - 32 * (1 + AW);
+  const int nb = nitems / sa.PL;
+#define NB_C(PP) ws_reduce_ld<PP, 3>(sa, nb, ct, kC, s_sc, &s_abort, s_out, flags)
+  switch (sa.src.n) {
+    case 1: NB_C(1); break;
+    case 2: NB_C(2); break;
+    case 3: NB_C(3); break;
+    case 4: NB_C(4); break;
+    case 5: NB_C(5); break;
+    case 6: NB_C(6); break;
+    case 7: NB_C(7); break;
+    default: NB_C(8); break;
+  }
+#undef NB_C
+}
+
+// FP16 fused step launcher; config 0 = LOOPBACK split, 1 = P2P-pull split.
+static const void* fp16_step_kernel(bool ef, int config) {
+  if (config == 1) return ef ? (const void*)k_fp16_step<true, 19, 12> : (const void*)k_fp16_step<false, 19, 12>;
+  return ef ? (const void*)k_fp16_step<true, 23, 8> : (const void*)k_fp16_step<false, 23, 8>;
+}
+
+void launch_fp16_step(const Launch& L, bool ef, const Item* items, int nitems, const float* g, float* r,
+                      const Dests& dst_in, uint32_t* flags, uint32_t* bar_words, const RItem* ritems, int b0, int PL,
+                      const Dests& src, float* obase, const Peers& pe, unsigned long long* local_arrive, uint64_t seq,
+                      int config) {
+  Mark mk(L, PH_FP16_STEP);
+  cudaMemsetAsync(bar_words, 0, sizeof(unsigned) * (size_t)nitems, L.stream);
+  Dests dst = dst_in;
+  StepArgs sa{};
+  sa.ritems = ritems;
+  sa.src = src;
+  sa.obase = obase;
+  sa.bdone = bar_words;
+  sa.pe = pe;
+  sa.local_arrive = local_arrive;
+  sa.seq = (unsigned long long)seq;
+  sa.b0 = b0;
+  sa.PL = PL;
+  void* args[] = {(void*)&items, (void*)&nitems, (void*)&g, (void*)&r, (void*)&dst, (void*)&flags, (void*)&sa};
+  const void* f = fp16_step_kernel(ef, config);
+  const size_t smem = sizeof(WsStageA) * kWsNA;
+  ensure_smem_attr(f, smem);
+  cudaLaunchCooperativeKernel(f, dim3(L.num_sms), dim3(kWsThreads), args, smem, L.stream);
+  ++*L.launches;
+}
+
 // ----------------------------------------------------------------------------- FP16 TMA
 // FP16 + EF streaming with a TMA ring (default for 16-B aligned calls): one CTA per SM walks
 // the same grid-stride chunk sequence as k_fp16; warp 0 bulk-loads the g and r tiles of each
@@ -803,6 +982,7 @@ static const void* ws_compress_kernel(bool ef, int kind) {
 
 template <bool EF>
 static const void* step_kernel(int config, int kind);
+static const void* fp16_step_kernel(bool ef, int config);
 __global__ void k_exchange_flags(Peers pe, unsigned long long* local, int lo, int hi, unsigned long long seq,
                                  uint32_t* flags);
 
@@ -816,6 +996,10 @@ void preload_ws() {
         cudaFuncGetAttributes(&a, step_kernel<false>(config, kind));
       }
     }
+  for (int c = 0; c < 2; ++c) {
+    cudaFuncGetAttributes(&a, fp16_step_kernel(true, c));
+    cudaFuncGetAttributes(&a, fp16_step_kernel(false, c));
+  }
   cudaFuncGetAttributes(&a, (const void*)k_fp16_tma<true>);
   cudaFuncGetAttributes(&a, (const void*)k_fp16_tma<false>);
   cudaFuncGetAttributes(&a, (const void*)k_exchange_flags);

@@ -806,7 +806,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       if (s != NEBULA_OK) return bail(s);
     }
     if (codec->method == NEBULA_INT8 || codec->method == NEBULA_FP8 || codec->method == NEBULA_QSGD ||
-        codec->method == NEBULA_FP8_E5M2) {
+        codec->method == NEBULA_FP8_E5M2 || codec->method == NEBULA_FP16) {
       ctx->onchip_ok = int8_onchip_capacity(ctx->device, &ctx->onchip_elems, &ctx->onchip_grid, &ctx->onchip_smem);
       if (ctx->onchip_ok && cudaMalloc(&ctx->d_bar, sizeof(uint32_t) * (2 * ctx->Ploc * num_buckets + 1)) != cudaSuccess) {
         ctx->err = "barrier allocation failed";
@@ -1189,9 +1189,10 @@ nebula_status nebula_decompress(nebula_ctx* ctx, int32_t bucket, int32_t slot, f
 static bool step_fusable(const nebula_ctx* ctx, int lo, int hi, int32_t bucket, const float* g, const float* out,
                          uint64_t step) {
   const int m = method_at(ctx, step);
-  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD && m != M_FP8_E5M2) || ctx->G != 1 ||
-      !ctx->onchip_ok)
+  if (ctx->step_fusion == 1 || (m != M_INT8 && m != M_FP8 && m != M_QSGD && m != M_FP8_E5M2 && m != M_FP16) ||
+      ctx->G != 1 || !ctx->onchip_ok)
     return false;
+  if (m == M_FP16 && ctx->fp16_kernel != 0) return false;   // the plain FP16 kernel option stays staged
   // SELF: the peers' cooperative kernels share this GPU — two grid-wide kernels waiting on each
   // other's flags could never be co-resident, so SELF always runs the staged stages
   if (ctx->self) return false;
@@ -1222,6 +1223,11 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   if (!ctx->loopback && ctx->P > 1) pe = inter_peers(ctx);
   BucketInfo probe = ctx->b[lo];
   probe.seq = seq;
+  if (method == M_FP16) {
+    launch_fp16_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, seq),
+                     ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc, sources_of(ctx, probe),
+                     dev_out, pe, ctx->d_arrive, seq, ctx->xmode == 3 ? 1 : 0);
+  } else
   launch_int8_step(L, ef, ctx->d_items[lay] + T.first, T.count, dev_grad, ctx->d_resid, dests_of(ctx, seq),
                    ctx->d_scratch, ctx->d_flags, ctx->d_bar, ctx->d_ritems[lay] + R.first, lo, ctx->Ploc,
                    sources_of(ctx, probe), dev_out, pe, ctx->d_arrive, seq,
@@ -1474,7 +1480,8 @@ const char* nebula_phase_name(uint32_t phase) {
       "dense_decompress_reduce", "topk_offsets", "sparse_decompress_reduce", "nccl_allgather_payload",
       "nccl_reducescatter_intra", "nccl_allgather_intra", "memset", "int8_fused_ef_quant_pack",
       "p2p_exchange_flags", "int8_fused_step", "fp8_ef_quant_pack", "nccl_allreduce_cluster_scale", "qsgd_ef_quant_pack",
-      "intra_rs_push", "intra_rs_reduce", "intra_ag_pull", "intra_scale_mail", "p2p_flags_intra_rs", "p2p_flags_intra_ag"};
+      "intra_rs_push", "intra_rs_reduce", "intra_ag_pull", "intra_scale_mail", "p2p_flags_intra_rs", "p2p_flags_intra_ag",
+      "fp16_fused_step"};
   return phase < PH_COUNT ? names[phase] : "unknown";
 }
 

@@ -155,6 +155,36 @@ def test_pull_reducer_in_fused_step(nb, method, P, per_bucket):
                  int8_kernel="fused-ws", step_config=4, sr_seed=7 if method == O.QSGD else 0)
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("per_bucket", [False, True])
+def test_fp16_fused_step(nb, P, per_bucket):
+    """FP16 through its fused compress + exchange + average kernel (k_fp16_step: no grid barrier,
+    per-bucket arrival counters, the register-load reduce role on 2-byte codes), incl. ragged,
+    tiny and odd-quad buckets; and the overflow / non-finite flags from inside it."""
+    run_loopback(nb, O.FP16, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003, (1 << 20) + 4], P, steps=3,
+                 per_bucket=per_bucket, int8_kernel="fused-ws")   # (forces fusion on small buckets)
+
+
+def test_fp16_fused_step_is_one_launch(nb):
+    import torch
+    sizes = [1 << 20, (1 << 20) + 8]
+    ctx = nb.SyncContext(sizes, nb.FP16, num_clusters=2, transport=nb.LOOPBACK)
+    g = torch.randn(2 * sum(sizes), device="cuda")
+    out = torch.empty(sum(sizes), device="cuda")
+    ctx.step(nb.ALL_BUCKETS, g, out, 0)
+    ctx.check()
+    n0 = ctx.kernel_launches()
+    ctx.step(nb.ALL_BUCKETS, g, out, 1)
+    ctx.check()
+    assert ctx.kernel_launches() - n0 == 1
+    g[12345] = 70000.0
+    ctx.step(nb.ALL_BUCKETS, g, out, 2)
+    with pytest.raises(nb.NebulaError) as e:
+        ctx.check()
+    assert e.value.code == "OVERFLOW"
+    ctx.destroy()
+
+
 def test_int8_fused_step_is_one_launch(nb):
     import torch
     sizes = [1 << 20, 1 << 20]
