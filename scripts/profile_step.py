@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--method", default="int8", choices=["identity", "fp16", "int8", "topk"])
+    ap.add_argument("--method", default="int8", choices=["identity", "fp16", "int8", "topk", "fp8", "qsgd", "fp8e5m2"])
+    ap.add_argument("--no-ef", action="store_true")
     ap.add_argument("--int8-kernel", default="auto")
     ap.add_argument("--values", default="f32", choices=["f32", "f16", "i8"])
     ap.add_argument("--density", type=float, default=0.01)
@@ -29,9 +30,10 @@ def main():
     for c in range(P):
         g[c * n:(c + 1) * n].copy_(torch.from_numpy(host[c]))
     out = torch.empty(n, device="cuda")
-    m = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3}[args.method]
+    m = {"identity": 0, "fp16": 1, "int8": 2, "topk": 3, "fp8": 4, "qsgd": 6, "fp8e5m2": 7}[args.method]
     ctx = nb.SyncContext(fixed_buckets(n, 25 << 20), m, topk_values={"f32": 0, "f16": 1, "i8": 2}[args.values],
-                         topk_density=args.density, num_clusters=P, transport=nb.LOOPBACK)
+                         topk_density=args.density, num_clusters=P, transport=nb.LOOPBACK,
+                         error_feedback=not args.no_ef)
     if m == 2:
         ctx.set_int8_kernel(args.int8_kernel)
     for s in range(args.steps):

@@ -10,7 +10,7 @@ for f in kernels_ws.o; do
 done
 echo
 echo "# excerpt: k_int8_ws<EF=1, AW=8, BW=19, CW=4, CM=1> (the default INT8 fused step, LOOPBACK)"
-cuobjdump -sass -fun '_ZN2nb9k_int8_wsILb1ELi8ELi19ELi4ELi1ELi0ELb0EEEvPKNS_4ItemEiPKfPfNS_5DestsEPjS8_S8_NS_8StepArgsE' $O/kernels_ws.o | grep -E "UBLKCP|SYNCS" | head -20
+cuobjdump -sass -fun '_ZN2nb9k_int8_wsILb1ELi8ELi19ELi4ELi1ELi0ELb0EEEvPKNS_4ItemEiPKfPfNS_5DestsEPjS8_S8_NS_8StepArgsE' $O/kernels_ws.o | grep -E "UBLKCP|TRYWAIT|ARRIVE" | head -16
 echo
 echo "# excerpt: k_fp16_tma<EF=1> (the default FP16 compressor)"
-cuobjdump -sass -fun '_ZN2nb10k_fp16_tmaILb1EEEvPKNS_4ItemEimPKfPfNS_5DestsEPj' $O/kernels_ws.o | grep -E "UBLKCP|SYNCS" | head -12
+cuobjdump -sass -fun '_ZN2nb10k_fp16_tmaILb1EEEvPKNS_4ItemEimPKfPfNS_5DestsEPj' $O/kernels_ws.o | grep -E "UBLKCP|TRYWAIT|ARRIVE" | head -10
