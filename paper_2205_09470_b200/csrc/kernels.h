@@ -167,13 +167,13 @@ struct TopkState {      // per item, device resident, rewritten every step
   uint32_t hist_prefix; // fallback radix state
   uint64_t count_above, need;
   uint64_t rank_left;   // fallback radix: rank still to find inside the prefix
-  uint32_t tile_ctr;    // (unused)
+  uint32_t wide;        // resolve on the multi-CTA path (candidate list too long for one CTA)
   uint32_t path;
   float scale;
   uint32_t maxbits;
-  unsigned long long stage_top;   // (unused)
+  unsigned long long wide_above;  // multi-CTA resolve: candidates above the running prefix
   uint32_t stage_ovf;             // pass A ran out of staging space for this bucket -> fallback
-  uint32_t pad2;
+  uint32_t wchunk0;               // multi-CTA resolve: first work unit of this item (prefix over items)
 };
 struct TopkBuffers {
   TopkItem* items;      // [nitems] (bucket-major, cluster-minor: same order as the Item tables)
@@ -181,6 +181,7 @@ struct TopkBuffers {
   uint32_t* sample;
   uint2* wlist;         // (idx, p bits)
   uint2* clist;
+  uint2* clist2;        // compacted candidates of the multi-CTA resolve (merge input for wide items)
   unsigned long long* status;  // per-chunk (winners << 32 | candidates) counts
   unsigned long long* pref;    // per-chunk exclusive prefixes of the counts
   unsigned long long* soff;    // per-chunk offset of its staged entries

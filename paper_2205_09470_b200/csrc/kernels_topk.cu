@@ -39,6 +39,7 @@ constexpr int kSelThreads = 1024;  // single-CTA radix select
 constexpr int kMergeThreads = 256, kMergeVT = 8;
 constexpr int kMergeTile = kMergeThreads * kMergeVT;   // 2048 outputs per merge CTA
 constexpr int kRedTile = 2048;     // elements per sparse-reduce CTA
+constexpr uint32_t kWideMin = 131072;  // candidate lists longer than this resolve on many CTAs (one CTA: ~0.1 ms per 75K)
 
 // tile words: (winners << 32) | candidates — per-tile counts, then exclusive prefixes
 __device__ __forceinline__ unsigned long long pack_wc(uint64_t w, uint64_t c) { return (w << 32) | c; }
@@ -710,6 +711,21 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   uint2* cand = cl + ti.list_off;
   const uint32_t m = (uint32_t)(C < ti.ccap ? C : ti.ccap);
   uint32_t T, above_c = 0;
+  if (!retry && S.t_lo != S.t_hi && m > kWideMin) {
+    // long candidate list (a huge bucket, or a large k): the multi-CTA radix select and
+    // compaction below (k_topk_wide_*) — one CTA would walk millions of entries
+    if (threadIdx.x == 0) {
+      const uint32_t hi31 = S.t_hi > 0x7FFFFFFFu ? 0x7FFFFFFFu : S.t_hi;
+      const uint32_t x = S.t_lo ^ hi31;
+      const int known = x ? (__clz(x) - 1) : 31;
+      const int lo_bit = 31 - known;
+      S.wide = 1u | ((uint32_t)lo_bit << 8);            // bits [lo_bit, 31) shared by every candidate
+      S.hist_prefix = known > 0 ? (S.t_lo >> lo_bit) : 0u;
+      S.rank_left = need;
+      S.wide_above = 0;
+    }
+    return;
+  }
   if (S.t_lo == S.t_hi) {
     // exact tie set: every candidate == T and the list holds the first need ties in index
     // order (k_topk_write), already the compacted selection
@@ -768,6 +784,220 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
     S.threshold = T;
     S.count_above = W + above_c;
     S.need = needT;
+  }
+}
+
+// ---------------------------------------------------------------- D': multi-CTA resolve
+// For candidate lists longer than kWideMin: the radix select of the need-th largest candidate
+// key runs as (histogram over all CTAs -> one CTA picks the bin) x up to 3 digits, then a
+// stable three-kernel compaction (per-chunk (gt, tie) counts -> per-item scan -> positioned
+// writes into clist2).  Same selection as the one-CTA resolve: keys > T, then the first need_T
+// keys == T in index order.  S.wide = 1 | lo_bit << 8 (bits still to resolve); the running
+// prefix / rank / count-above live in hist_prefix, rank_left, wide_above.
+constexpr uint32_t kWideChunk = 4096;
+
+__device__ __forceinline__ bool wide_active(const TopkState& S) { return (S.wide & 1u) && S.failed == 0; }
+
+__device__ __forceinline__ uint32_t wide_m(const TopkItem& ti, const TopkState& S) {
+  return (uint32_t)(S.ccount < ti.ccap ? S.ccount : ti.ccap);
+}
+
+// 1 CTA: work units (kWideChunk candidates) of every wide item, flattened: S.wchunk0 = exclusive
+// prefix of the items' unit counts, *total = their sum (every unit is one CTA-iteration below,
+// so the work spreads over all CTAs however the candidates split between items)
+__global__ void __launch_bounds__(kSelThreads) k_topk_wide_plan(const TopkItem* __restrict__ titems,
+                                                                TopkState* __restrict__ st, int nitems,
+                                                                uint32_t* total) {
+  __shared__ unsigned long long scan[32];
+  unsigned long long carry = 0;
+  for (int i0 = 0; i0 < nitems; i0 += kSelThreads) {
+    const int i = i0 + threadIdx.x;
+    unsigned long long v = 0;
+    if (i < nitems && wide_active(st[i])) v = (wide_m(titems[i], st[i]) + kWideChunk - 1) / kWideChunk;
+    unsigned long long tot;
+    const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
+    if (i < nitems) st[i].wchunk0 = (uint32_t)(carry + incl - v);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = (uint32_t)carry;
+}
+
+// the item owning work unit u: the last item whose first unit is <= u (items without units
+// share their successor's prefix, so the last such item is the one with units)
+__device__ __forceinline__ int wide_item_of(const TopkState* st, int nitems, uint32_t u) {
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (st[mid].wchunk0 <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_topk_wide_hist(const TopkItem* __restrict__ titems,
+                                                        const TopkState* __restrict__ st, int nitems,
+                                                        const uint2* __restrict__ cl, uint32_t* __restrict__ ghist,
+                                                        const uint32_t* total) {
+  __shared__ uint32_t hist[2048];
+  const uint32_t nu = *total;
+  for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+    const int i = wide_item_of(st, nitems, u);
+    const TopkState& S = st[i];
+    const int lo_bit = (int)(S.wide >> 8);
+    if (lo_bit <= 0) continue;
+    const int bits = lo_bit < 11 ? lo_bit : 11, shift = lo_bit - bits, hs = lo_bit, nb = 1 << bits;
+    const uint32_t prefix = S.hist_prefix;
+    const TopkItem& ti = titems[i];
+    const uint32_t m = wide_m(ti, S), c = u - S.wchunk0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint2* cand = cl + ti.list_off;
+    const uint32_t lim = min(m, (c + 1) * kWideChunk);
+#pragma unroll 4
+    for (uint32_t x = c * kWideChunk + threadIdx.x; x < lim; x += blockDim.x) {
+      const uint32_t key = cand[x].y & 0x7FFFFFFFu;
+      hist_add(hist, hs >= 31 || (key >> hs) == prefix, (key >> shift) & (nb - 1));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (hist[b]) atomicAdd(&ghist[(size_t)i * 2048 + b], hist[b]);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_topk_wide_pick(TopkState* __restrict__ st, uint32_t* ghist) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t misc[4];
+  __shared__ unsigned long long scan[32];
+  TopkState& S = st[blockIdx.x];
+  if (!wide_active(S)) return;
+  const int lo_bit = (int)(S.wide >> 8);
+  if (lo_bit <= 0) return;
+  const int bits = lo_bit < 11 ? lo_bit : 11, shift = lo_bit - bits, nb = 1 << bits;
+  uint32_t* gh = ghist + (size_t)blockIdx.x * 2048;
+  for (int b = threadIdx.x; b < 2048; b += blockDim.x) { hist[b] = b < nb ? gh[b] : 0; gh[b] = 0; }
+  __syncthreads();
+  const uint32_t left = (uint32_t)S.rank_left;
+  find_bin(hist, nb, left, &misc[0], &misc[1], scan);
+  if (threadIdx.x == 0) {
+    S.hist_prefix = (S.hist_prefix << bits) | misc[0];
+    S.wide_above += misc[1];
+    S.rank_left = left - misc[1];
+    S.wide = 1u | ((uint32_t)shift << 8);
+  }
+}
+
+// per work unit (item, chunk of kWideChunk candidates): (#key > T) << 32 | #key == T
+__global__ void __launch_bounds__(256) k_topk_wide_count(const TopkItem* __restrict__ titems,
+                                                         const TopkState* __restrict__ st, int nitems,
+                                                         const uint2* __restrict__ cl,
+                                                         unsigned long long* __restrict__ counts,
+                                                         const uint32_t* total) {
+  __shared__ unsigned long long s_w[8];
+  const uint32_t nu = *total;
+  for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+    const int i = wide_item_of(st, nitems, u);
+    const TopkState& S = st[i];
+    const TopkItem& ti = titems[i];
+    const uint32_t T = S.hist_prefix, m = wide_m(ti, S), c = u - S.wchunk0;
+    const uint2* cand = cl + ti.list_off;
+    unsigned long long v = 0;
+    const uint32_t lim = min(m, (c + 1) * kWideChunk);
+#pragma unroll 4
+    for (uint32_t x = c * kWideChunk + threadIdx.x; x < lim; x += blockDim.x) {
+      const uint32_t key = cand[x].y & 0x7FFFFFFFu;
+      v += ((unsigned long long)(key > T) << 32) | (unsigned long long)(key == T);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < 8; ++w) t += s_w[w];
+      counts[ti.status_off + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// 1 CTA per item: exclusive scan of the chunk counts (in place into pref) and the final stats
+__global__ void __launch_bounds__(kSelThreads) k_topk_wide_scan(const TopkItem* __restrict__ titems,
+                                                                TopkState* __restrict__ st,
+                                                                const unsigned long long* __restrict__ counts,
+                                                                unsigned long long* __restrict__ pref) {
+  __shared__ unsigned long long scan[32];
+  const TopkItem ti = titems[blockIdx.x];
+  TopkState& S = st[blockIdx.x];
+  if (!wide_active(S)) return;
+  const uint32_t nch = (wide_m(ti, S) + kWideChunk - 1) / kWideChunk;
+  unsigned long long carry = 0;
+  for (uint32_t j0 = 0; j0 < nch; j0 += kSelThreads) {
+    const uint32_t j = j0 + threadIdx.x;
+    const unsigned long long v = j < nch ? counts[ti.status_off + j] : 0ull;
+    unsigned long long tot;
+    const unsigned long long incl = block_incl_scan<kSelThreads>(v, scan, &tot);
+    if (j < nch) pref[ti.status_off + j] = carry + incl - v;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t W = S.wcount;
+    S.threshold = S.hist_prefix;
+    S.count_above = W + S.wide_above;
+    S.need = S.rank_left;
+  }
+}
+
+// per work unit: stable positioned write of the selected candidates into clist2
+__global__ void __launch_bounds__(256) k_topk_wide_write(const TopkItem* __restrict__ titems,
+                                                         const TopkState* __restrict__ st, int nitems,
+                                                         const uint2* __restrict__ cl, uint2* __restrict__ cl2,
+                                                         const unsigned long long* __restrict__ pref,
+                                                         const uint32_t* total) {
+  __shared__ unsigned long long scan[32];
+  const uint32_t nu = *total;
+  for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+    const int i = wide_item_of(st, nitems, u);
+    const TopkState& S = st[i];
+    const TopkItem& ti = titems[i];
+    const uint32_t T = S.hist_prefix, needT = (uint32_t)S.rank_left, m = wide_m(ti, S), c = u - S.wchunk0;
+    const uint2* cand = cl + ti.list_off;
+    uint2* outl = cl2 + ti.list_off;
+    const unsigned long long pc = pref[ti.status_off + c];
+    uint32_t gt_seen = (uint32_t)(pc >> 32), tie_seen = (uint32_t)(pc & 0xFFFFFFFFull);
+    const uint32_t lim = min(m, (c + 1) * kWideChunk);
+    // 4 entries per thread per round: the round's (gt, tie) prefix gives every entry's position
+    for (uint32_t x0 = c * kWideChunk; x0 < lim; x0 += 4 * blockDim.x) {
+      uint2 e[4];
+      uint32_t ngt = 0, ntie = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = x0 + 4 * threadIdx.x + q;
+        e[q] = x < lim ? cand[x] : make_uint2(0u, 0u);
+        const uint32_t key = e[q].y & 0x7FFFFFFFu;
+        ngt += (x < lim) && key > T;
+        ntie += (x < lim) && key == T;
+      }
+      const unsigned long long v = ((unsigned long long)ngt << 32) | ntie;
+      unsigned long long tot;
+      const unsigned long long excl = block_incl_scan<256>(v, scan, &tot) - v;
+      uint32_t gb = gt_seen + (uint32_t)(excl >> 32), tb = tie_seen + (uint32_t)(excl & 0xFFFFFFFFu);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = x0 + 4 * threadIdx.x + q;
+        if (x >= lim) break;
+        const uint32_t key = e[q].y & 0x7FFFFFFFu;
+        if (key > T) {
+          outl[gb + min(tb, needT)] = e[q];
+          ++gb;
+        } else if (key == T) {
+          if (tb < needT) outl[gb + tb] = e[q];
+          ++tb;
+        }
+      }
+      gt_seen += (uint32_t)(tot >> 32);
+      tie_seen += (uint32_t)(tot & 0xFFFFFFFFull);
+      __syncthreads();
+    }
   }
 }
 
@@ -872,7 +1102,8 @@ __device__ __forceinline__ uint64_t merge_split(const uint2* A, uint64_t na, con
 // latency-bound binary searches in flight at once instead of one per merge CTA).
 __global__ void k_topk_splits(const TopkItem* __restrict__ titems, const TopkState* __restrict__ st, int nitems,
                               uint64_t tbase, uint64_t ntiles, const uint2* __restrict__ wl,
-                              const uint2* __restrict__ cl, uint64_t* __restrict__ splits) {
+                              const uint2* __restrict__ cl, const uint2* __restrict__ cl2,
+                              uint64_t* __restrict__ splits) {
   const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 2 * ntiles) return;
   const uint64_t t = tbase + x / 2;
@@ -887,7 +1118,7 @@ __global__ void k_topk_splits(const TopkItem* __restrict__ titems, const TopkSta
   const uint64_t k = ti.k, W = S.wcount, Ns = k - W;
   const uint64_t d0 = (t - ti.mt0) * kMergeTile;
   const uint64_t d = (x & 1) ? (d0 + kMergeTile < k ? d0 + kMergeTile : k) : d0;
-  splits[x] = merge_split(wl + ti.list_off, W, cl + ti.list_off, Ns, d);
+  splits[x] = merge_split(wl + ti.list_off, W, (wide_active(S) ? cl2 : cl) + ti.list_off, Ns, d);
 }
 
 // Merge of one 2048-output tile (ModernGPU-style): the tile's ranges of the two ascending lists
@@ -900,6 +1131,7 @@ template <bool EF>
 __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __restrict__ titems,
                                                            const TopkState* __restrict__ st, int nitems, uint64_t tbase,
                                                            const uint2* __restrict__ wl, const uint2* __restrict__ cl,
+                                                           const uint2* __restrict__ cl2,
                                                            Dests dst, float* __restrict__ rbase, uint32_t* flags,
                                                            const uint64_t* __restrict__ splits) {
   __shared__ uint2 sab[kMergeTile], so[kMergeTile];   // sab: the A range, then the B range (na + nb = nout)
@@ -928,7 +1160,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __
   const uint64_t k = ti.k;
   const uint64_t d0 = (t - ti.mt0) * kMergeTile, d1 = d0 + kMergeTile < k ? d0 + kMergeTile : k;
   const uint2* A = wl + ti.list_off;
-  const uint2* B = cl + ti.list_off;
+  const uint2* B = (wide_active(S) ? cl2 : cl) + ti.list_off;
   if (threadIdx.x < 2) s_split[threadIdx.x] = splits[2 * blockIdx.x + threadIdx.x];
   __syncthreads();
   const uint64_t a0 = s_split[0], a1 = s_split[1], b0 = d0 - a0, b1 = d1 - a1;
@@ -1408,6 +1640,17 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     Mark mk(L, PH_TOPK_RESOLVE);
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
+    // long candidate lists: multi-CTA radix select + compaction (no-ops for the others)
+    const unsigned gwide = (unsigned)L.num_sms * 8;
+    uint32_t* wtotal = B.ctrs + 3;
+    k_topk_wide_plan<<<1, kSelThreads, 0, L.stream>>>(ti, st, nitems, wtotal);
+    for (int d = 0; d < 3; ++d) {
+      k_topk_wide_hist<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.hist + (size_t)item0 * 2048, wtotal);
+      k_topk_wide_pick<<<nitems, kSelThreads, 0, L.stream>>>(st, B.hist + (size_t)item0 * 2048);
+    }
+    k_topk_wide_count<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.status, wtotal);
+    k_topk_wide_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref);
+    k_topk_wide_write<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.clist2, B.pref, wtotal);
   }
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
@@ -1426,10 +1669,10 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   Mark mk(L, PH_TOPK_MERGE);
   const uint64_t tbase = B.host_mt0[item0];
   k_topk_splits<<<(unsigned)((2 * merge_tiles + 255) / 256), 256, 0, L.stream>>>(ti, st, nitems, tbase, merge_tiles,
-                                                                                B.wlist, B.clist, B.splits);
-  k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeThreads, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, slots,
+                                                                                B.wlist, B.clist, B.clist2, B.splits);
+  k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeThreads, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, B.clist2, slots,
                                                                       r, flags, B.splits);
-  *L.launches += 18;
+  *L.launches += 28;
 }
 
 static void touch_t(const void* f) {
@@ -1455,6 +1698,9 @@ void preload_topk() {
   touch_t((const void*)k_topk_stage<true, true>); touch_t((const void*)k_topk_stage<true, false>);
   touch_t((const void*)k_topk_stage<false, true>); touch_t((const void*)k_topk_stage<false, false>);
   touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan);
+  touch_t((const void*)k_topk_wide_hist); touch_t((const void*)k_topk_wide_pick); touch_t((const void*)k_topk_wide_plan);
+  touch_t((const void*)k_topk_wide_count); touch_t((const void*)k_topk_wide_scan);
+  touch_t((const void*)k_topk_wide_write);
   touch_t((const void*)k_topk_write<true>); touch_t((const void*)k_topk_write<false>);
   touch_t((const void*)k_topk_resolve);
   touch_t((const void*)k_topk_hist<true>); touch_t((const void*)k_topk_hist<false>);

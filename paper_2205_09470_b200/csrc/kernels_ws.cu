@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last(), pol_unch = l2_evict_unchanged();
+  const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   auto tiles_of = [&](int t, Slice& sl) {
     sl = slice_of(items[t].n >> 2, G);
     return (int)((sl.q1 - sl.q0 + kWsTQ - 1) / kWsTQ);
@@ -440,11 +440,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const uint64_t q = sb.q0 + (uint64_t)kb * kWsTQ;
             const uint32_t nq = (uint32_t)min((uint64_t)kWsTQ, sb.q1 - q);
             mbar_expect_tx(&fullB[st], nq * 16u);
-            // EF: the parked p lines are dirty and are overwritten by the residual within
-            // microseconds — reading them with evict_first got ~14 % of them written back to DRAM
-            // in between (ncu r01: 4.21 GB written vs 3.89 algorithmic); keep their priority
-            bulk_g2s(ringB[st].p, (EF ? rbase + it.r_off : gbase + it.g_off) + 4 * q, nq * 16u, &fullB[st],
-                     EF ? pol_unch : pol_stream);
+            bulk_g2s(ringB[st].p, (EF ? rbase + it.r_off : gbase + it.g_off) + 4 * q, nq * 16u, &fullB[st], pol_stream);
             ++fb;
             ++kb;
             progress = true;

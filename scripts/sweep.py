@@ -130,6 +130,8 @@ def main():
             for s in range(3):
                 ctx.step(nb.ALL_BUCKETS, g, out, s)
             ctx.check()
+            ctx.timing_enable(True)
+            ctx.timing_read()
             times = []
             for s in range(args.steps):
                 flush.fill_(float(s))
@@ -143,6 +145,8 @@ def main():
                 b.synchronize()
                 times.append(a.elapsed_time(b))
             ctx.check()
+            phases = ctx.timing_read()
+            ctx.timing_enable(False)
             ms = float(np.median(times))
             if world > 1:
                 tt = torch.tensor([ms], device="cuda")
@@ -158,7 +162,8 @@ def main():
                    "us_per_step": round(ms * 1e3, 2),
                    "gbs_fp32_synced_per_gpu": round(P_here * n * 4 / (ms * 1e-3) / 1e9, 2),
                    "hbm_algorithmic_bytes": byt, "hbm_frac": round(byt / (ms * 1e-3) / 1e9 / peak, 4),
-                   "payload_bytes": payload(method, vt, n, k)}
+                   "payload_bytes": payload(method, vt, n, k),
+                   "phase_ms_per_step": {kk: round(v[1] / args.steps, 4) for kk, v in phases.items()}}
             if world > 1:
                 nv = (P - 1) * payload(method, vt, n, k)      # bytes into this GPU per step
                 rec["nvlink_bytes_in"] = nv
