@@ -406,6 +406,8 @@ def main():
         elif dom == "int8_fused_step":   # compress of the local clusters + the average (one kernel)
             byt = kernel_bytes("int8_fused_ef_quant_pack", method, vt, P, ef, n_local, 0) + \
                 reduce_bytes(method, vt, P, n // G, 0)
+        elif dom == "fp16_fused_step":
+            byt = kernel_bytes("fp16_ef_pack", method, vt, P, ef, n_local, 0) + reduce_bytes(method, vt, P, n // G, 0)
         else:
             byt = kernel_bytes(dom, method, vt, P, ef, n_local, k_per_cluster * (P if world == 1 else 1))
         if byt:

@@ -35,8 +35,11 @@
  *     nebula_check, nebula_payload_copy, nebula_topk_stats and nebula_step_host, which
  *     synchronise that stream.  One host thread per context.
  *   - Host-validated errors return immediately with nothing enqueued.  Device-detected
- *     errors (non-finite p, fp16 overflow) set a sticky device flag returned by
- *     nebula_check (which clears it).  After a device error the affected buckets' residuals
+ *     errors (non-finite p, fp16 overflow, a P2P peer timeout) set a sticky device flag returned
+ *     by nebula_check (which clears it) and, without any synchronisation, by the next
+ *     compress / step call once the step that raised it has completed: every step and
+ *     decompress_reduce ends with an asynchronous 4-byte copy of the flag word into pinned
+ *     host memory, which the next stage call reads before enqueuing anything.  After a device error the affected buckets' residuals
  *     and dev_out are unspecified (the caller skips the step and zeroes or restores the
  *     residual via nebula_residual_ptr); INT8 writes no payload for such a bucket.
  *   - No C++ exception crosses the ABI.  nebula_last_error() describes the last failure.

@@ -90,6 +90,9 @@ struct nebula_ctx {
   float* d_resid = nullptr;      // [Ploc][total_cn]
   uint8_t* d_slots = nullptr;    // [sum_b P * pb_b]
   uint32_t* d_flags = nullptr;   // sticky device error bits
+  uint32_t* h_flags = nullptr;   // pinned host mirror of d_flags, refreshed by an async 4-byte copy
+                                 // after every step / reduce: later calls see a device error
+                                 // without synchronising (ABI "host-mapped word")
   uint32_t* d_scratch = nullptr; // [Ploc * B] per-item max-abs bits
   // Two slot layouts: [0] for the codec's method, [1] for the IDENTITY phase before
   // start_step (only built when start_step > 0 and the method is lossy).  Slots are sized
@@ -217,6 +220,19 @@ static nebula_status fail(nebula_ctx* ctx, nebula_status s, const std::string& m
   if (ctx) ctx->err = msg;
   else g_init_error = msg;
   return s;
+}
+
+// Device errors seen by the host mirror (no synchronisation): the sticky bits the kernels raised
+// up to the last completed mirror copy.  Returned by every stage call until nebula_check.
+static nebula_status pending_device_error(nebula_ctx* ctx) {
+  const uint32_t f = ctx->h_flags ? *reinterpret_cast<volatile uint32_t*>(ctx->h_flags) : 0u;
+  if (f & kFlagPeerTimeout) return fail(ctx, NEBULA_ERR_NCCL, "P2P exchange: a peer's payload did not arrive (timeout); call nebula_check");
+  if (f & kFlagNonfinite) return fail(ctx, NEBULA_ERR_NONFINITE, "non-finite element in g + r (a previous step); call nebula_check");
+  if (f & kFlagOverflow) return fail(ctx, NEBULA_ERR_OVERFLOW, "fp16 overflow (a previous step); call nebula_check");
+  return NEBULA_OK;
+}
+static void mirror_flags(nebula_ctx* ctx) {
+  cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream);
 }
 
 static uint64_t topk_k_of(uint64_t n, const nebula_codec& c) {
@@ -414,6 +430,7 @@ static void release(nebula_ctx* ctx) {
   cudaFree(ctx->d_resid);
   cudaFree(ctx->d_slots);
   cudaFree(ctx->d_flags);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   cudaFree(ctx->d_scratch);
   for (int l = 0; l < 2; ++l) {
     cudaFree(ctx->d_items[l]);
@@ -588,6 +605,16 @@ static nebula_status self_resolve(nebula_ctx* ctx) {
   ctx->intra_p2p = G > 1;
   ctx->peers_resolved = true;
   return NEBULA_OK;
+}
+
+// Auto exchange mode: P = 2 -> push (one peer: the compress kernel's NVLink stores hide inside
+// it); P > 2 -> pull for the dense codecs (NVLink loads outrun SM-issued stores once every GPU
+// feeds P - 1 peers, and the fused step overlaps them with the compress) but push for TOPK (its
+// payload is small and the sparse reducer's scattered window loads would each pay the NVLink
+// latency: 0.90 ms at P = 4 pulling, r02).
+static int auto_xmode(const nebula_ctx* ctx) {
+  if (ctx->P == 2 || ctx->codec.method == NEBULA_TOPK) return 2;
+  return 3;
 }
 
 // Slot buffer of a bucket's exchange `seq` (the P2P modes double-buffer by seq parity).
@@ -766,6 +793,8 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
     const int halves = (!ctx->loopback && ctx->P > 1) ? 2 : 1;   // double buffer for the P2P push
     if (cudaMalloc(&ctx->d_slots, halves * ctx->slot_span) != cudaSuccess) { ctx->err = "payload allocation failed"; return bail(NEBULA_ERR_OOM); }
     if (cudaMalloc(&ctx->d_flags, 16) != cudaSuccess) { ctx->err = "flag allocation failed"; return bail(NEBULA_ERR_OOM); }
+    if (cudaHostAlloc(&ctx->h_flags, 16, cudaHostAllocDefault) != cudaSuccess) { ctx->err = "host flag allocation failed"; return bail(NEBULA_ERR_OOM); }
+    std::memset(ctx->h_flags, 0, 16);
     if (cudaMalloc(&ctx->d_scratch, sizeof(uint32_t) * ctx->Ploc * num_buckets) != cudaSuccess) { ctx->err = "scratch allocation failed"; return bail(NEBULA_ERR_OOM); }
     if (cudaMemset(ctx->d_resid, 0, rbytes) != cudaSuccess || cudaMemset(ctx->d_slots, 0, halves * ctx->slot_span) != cudaSuccess ||
         cudaMemset(ctx->d_flags, 0, 16) != cudaSuccess) { ctx->err = "memset failed"; return bail(NEBULA_ERR_CUDA); }
@@ -852,7 +881,7 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
       }
       // auto: P = 2 -> push (one peer: the NVLink egress hides inside the compress kernel);
       // P > 2 -> pull (NVLink loads outrun SM-issued stores once every GPU feeds P - 1 peers)
-      if (ctx->p2p_ok && ctx->P > 1) ctx->xmode = ctx->P == 2 ? 2 : 3;
+      if (ctx->p2p_ok && ctx->P > 1) ctx->xmode = auto_xmode(ctx);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
   }
@@ -984,6 +1013,8 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
   if (!dev_grad && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
   nebula_status st0 = stage_start(ctx, lo, hi);
+  if (st0 != NEBULA_OK) return st0;
+  st0 = pending_device_error(ctx);
   if (st0 != NEBULA_OK) return st0;
   DevGuard dg(ctx->device);
   const int method = method_at(ctx, step);
@@ -1133,6 +1164,7 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
     nebula_status s = intra_all_gather(ctx, L, bucket, lo, hi, dev_out, ctx->b[lo].seq);
     if (s != NEBULA_OK) return s;
   }
+  mirror_flags(ctx);
   for (int i = lo; i < hi; ++i) ctx->b[i].state = ST_IDLE;
   return NEBULA_OK;
 }
@@ -1217,6 +1249,8 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   const Launch L = launch_of(ctx);
   nebula_status st0 = stage_start(ctx, lo, hi);
   if (st0 != NEBULA_OK) return st0;
+  st0 = pending_device_error(ctx);
+  if (st0 != NEBULA_OK) return st0;
   const uint64_t seq = ctx->b[lo].seq + 1;
   { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
   Peers pe{};
@@ -1235,6 +1269,7 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
                    method == M_FP8 ? 1 : (method == M_QSGD ? 2 : (method == M_FP8_E5M2 ? 3 : 0)),
                    SrArgs{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()});
   CKC(cudaGetLastError());
+  mirror_flags(ctx);
   for (int i = lo; i < hi; ++i) {
     ctx->b[i].seq = seq;
     ctx->b[i].state = ST_IDLE;
@@ -1320,6 +1355,7 @@ nebula_status nebula_check(nebula_ctx* ctx) {
   uint32_t f = 0;
   CKC(cudaMemcpy(&f, ctx->d_flags, 4, cudaMemcpyDeviceToHost));
   CKC(cudaMemset(ctx->d_flags, 0, 4));
+  *reinterpret_cast<volatile uint32_t*>(ctx->h_flags) = 0u;
   if (!ctx->loopback && ctx->world) {
     ncclResult_t async_err = ncclSuccess;
     ncclCommGetAsyncError(ctx->world, &async_err);
@@ -1418,7 +1454,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     for (const auto& bk : ctx->b)
       if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
     ctx->xopt = (int)value;
-    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? (ctx->P == 2 ? 2 : 3) : (int)value);
+    ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? auto_xmode(ctx) : (int)value);
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_INTRA) {

@@ -62,7 +62,10 @@ def main():
                     rs[c][b] = r_new[c] if r_new[c] is not None else rs[c][b]
                 off += n
         dec = torch.empty(sizes[0], device="cuda")
+        ctx.compress(nb.ALL_BUCKETS, dev, steps)   # the staged calls and the single-slot decode
+        ctx.exchange(nb.ALL_BUCKETS)
         ctx.decompress(0, 0, dec)
+        ctx.decompress_reduce(nb.ALL_BUCKETS, out)
         ctx.check()
         ctx.destroy()
 

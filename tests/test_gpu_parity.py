@@ -222,6 +222,14 @@ def test_e5m2_near_rounding_boundaries(nb, kern, kind):
     run_loopback(nb, O.FP8_E5M2, [1 << 20, 7], 2, kind=kind, steps=2, int8_kernel=kern)
 
 
+@pytest.mark.parametrize("vt,rho", [(O.VAL_F32, 0.2), (O.VAL_I8, 0.3), (O.VAL_F16, 0.25)])
+def test_topk_wide_resolve(nb, vt, rho):
+    """Candidate lists above kWideMin (131072) resolve on many CTAs (k_topk_wide_*: radix-select
+    histograms over all CTAs, stable compaction into the second list): bit-exact k, T,
+    count_above, need, payloads and residuals, next to a bucket that takes the one-CTA path."""
+    run_loopback(nb, O.TOPK, [4_000_003, 9000, 1 << 20], 2, vt=vt, rho=rho, steps=2, kind="normal")
+
+
 def test_topk_i8_near_half_integer_quotients(nb):
     run_loopback(nb, O.TOPK, [50001], 2, kind="half-ties", vt=O.VAL_I8, rho=0.3, steps=1, ef=False)
 
@@ -368,6 +376,34 @@ def test_nonfinite_is_reported(nb, method, bad):
         ctx.check()
     assert e.value.code == "NONFINITE"
     ctx.check()   # sticky flag was cleared by the check
+    ctx.destroy()
+
+
+@pytest.mark.parametrize("method", [O.INT8, O.FP16, O.TOPK])
+def test_device_error_seen_by_next_call(nb, method):
+    """ABI: a device-detected error is returned by the next stage call (through the pinned host
+    mirror of the flag word, refreshed asynchronously after every step) without nebula_check;
+    nothing is enqueued by that call; nebula_check then clears it."""
+    import torch
+    ctx = nb.SyncContext([1 << 20, 4100], method, num_clusters=2, transport=nb.LOOPBACK, topk_density=0.1)
+    n = (1 << 20) + 4100
+    g = torch.randn(2 * n, device="cuda")
+    g[12345] = float("inf")
+    out = torch.empty(n, device="cuda")
+    ctx.step(nb.ALL_BUCKETS, g, out, 0)
+    torch.cuda.synchronize()                       # the step (and its mirror copy) completed
+    l0 = ctx.kernel_launches()
+    with pytest.raises(nb.NebulaError) as e:
+        ctx.step(nb.ALL_BUCKETS, g, out, 1)
+    assert e.value.code == "NONFINITE" and ctx.kernel_launches() == l0
+    with pytest.raises(nb.NebulaError) as e:
+        ctx.check()
+    assert e.value.code == "NONFINITE"
+    g[12345] = 0.0
+    for r in range(2):
+        ctx.residual(0, r).zero_()                 # the caller resets the residual after the error
+    ctx.step(nb.ALL_BUCKETS, g, out, 1)
+    ctx.check()
     ctx.destroy()
 
 
