@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--exact-scale", action="store_true",
                     help="G > 1: cluster-wide INT8/FP8 scale (NEBULA_OPT_EXACT_SCALE, NEXT-3)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
+    ap.add_argument("--intra", default="auto", choices=["auto", "p2p", "p2p-ce", "nccl"],
+                    help="G > 1: intra-cluster hop (NEBULA_OPT_INTRA)")
     ap.add_argument("--fp16-kernel", default="tma", choices=["tma", "plain"])
     ap.add_argument("--no-step-fusion", action="store_true",
                     help="run compress / exchange / reduce as separate launches (NEBULA_OPT_STEP_FUSION=1)")
@@ -344,6 +346,8 @@ def main():
         ctx.set_option(nb.OPT_STEP_FUSION, 2 + args.step_config)
     if world > 1 and args.exchange != "auto":
         ctx.set_exchange(args.exchange)
+    if G > 1 and args.intra != "auto":
+        ctx.set_intra(args.intra)
     torch.cuda.synchronize()
 
     def barrier():

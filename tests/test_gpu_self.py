@@ -37,7 +37,8 @@ def _sync(grid):
 
 
 def run_self(nb, method, P, G, sizes, *, steps=2, vt=0, rho=0.05, exchange="auto", per_bucket=False,
-             exact=False, int8_kernel="two-pass", kind="model-like", sr_seed=0, ef=True, exact_topk=False):
+             exact=False, int8_kernel="two-pass", kind="model-like", sr_seed=0, ef=True, exact_topk=False,
+             intra=None):
     import torch
     grid = nb.self_group(sizes, num_clusters=P, gpus_per_cluster=G, device=0, method=method, topk_values=vt,
                          topk_density=rho, error_feedback=ef, exact_topk=exact_topk)
@@ -51,6 +52,8 @@ def run_self(nb, method, P, G, sizes, *, steps=2, vt=0, rho=0.05, exchange="auto
                 ctx.set_exact_scale(True)
             if sr_seed:
                 ctx.set_sr_seed(sr_seed)
+            if intra:
+                ctx.set_intra(intra)
     codec = O.Codec(method=method, topk_values=vt, topk_density=rho, sr_seed=sr_seed, error_feedback=ef)
     total = sum(sizes)
     m = [s if exact_topk else s // G for s in sizes]   # coded elements per GPU (R34: the whole bucket)
@@ -147,6 +150,13 @@ def test_self_hierarchical_exact_any_input(nb, P, G, per_bucket):
     """G > 1: the cluster mean is the fixed-order P2P reduce-scatter (push + flags + sum in
     local-rank order / G), so it is bit-identical to the oracle on non-dyadic inputs."""
     run_self(nb, O.INT8, P, G, [s * G for s in [4096, 12288, 300004, 8]], per_bucket=per_bucket)
+
+
+@pytest.mark.parametrize("P,G", [(1, 2), (2, 2), (1, 4)])
+def test_self_hierarchical_copy_engines(nb, P, G):
+    """NEBULA_OPT_INTRA = 2: the intra-cluster transfers on copy engines, same bits."""
+    run_self(nb, O.INT8, P, G, [s * G for s in [4096, 300004, 8]], intra="p2p-ce", per_bucket=True)
+    run_self(nb, O.TOPK, P, G, [s * G for s in [4096, 300004, 8]], intra="p2p-ce", exact_topk=True)
 
 
 @pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.TOPK, O.VAL_F32), (O.TOPK, O.VAL_I8), (O.FP8, 0),
