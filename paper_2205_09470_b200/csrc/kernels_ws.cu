@@ -458,10 +458,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     uint32_t fa = 0;
     for (int t = 0; t < nitems; ++t) {
       if (t >= 2)
-        // B(t-2) finished: bounded L2 footprint.  A long sleep: A is two items ahead, and every
-        // wake-up is issue slots taken from the quantise warps (ncu r02: this loop was 13 % of
-        // the INT8 step's and 17 % of the QSGD step's instructions at a 64 ns sleep)
-        while (s_bdone < (uint32_t)(t - 1)) __nanosleep(2000);
+        // B(t-2) finished: bounded L2 footprint.  (ncu r02: this spin is 13 % of the INT8
+        // step's instructions, but a 2 us sleep made the step 4 % slower — A's late wake-up
+        // costs more than the issue slots it takes; QSGD did not change either way)
+        while (s_bdone < (uint32_t)(t - 1)) __nanosleep(64);
       Slice sl;
       const int nt = tiles_of(t, sl);
       const Item it = items[t];

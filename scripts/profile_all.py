@@ -21,8 +21,10 @@ def main():
     from gradgen import fixed_buckets, model_gradient
 
     P = 2
-    host = [model_gradient("ernie-m-base", cluster=c) for c in range(P)]
-    n = host[0].size
+    # the bench's per-launch shape on a shorter gradient: 8 buckets of 25 MiB per cluster (ncu
+    # replays each kernel ~40 times, saving and restoring its working set every time)
+    n = 8 * ((25 << 20) // 4)
+    host = [model_gradient("ernie-m-base", cluster=c)[:n].copy() for c in range(P)]
     g = torch.empty(P * n, device="cuda")
     for c in range(P):
         g[c * n:(c + 1) * n].copy_(torch.from_numpy(host[c]))
