@@ -135,6 +135,10 @@ struct nebula_ctx {
   std::vector<cudaEvent_t> ev_in, ev_done;
 
   TopkBuffers tk{};
+  uint2* tk_stage2 = nullptr;          // staging of the second half of a pipelined top-k step
+  int topk_pipe = 1;                   // NEBULA_OPT_TOPK_PIPELINE
+  cudaStream_t side = nullptr;         // second stream of the pipelined top-k step
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* d_topk_mem = nullptr;
   std::vector<uint64_t> tk_mtiles;   // merge tiles per call type ([0] ALL, [1+b])
   std::vector<uint64_t> tk_host_mt0; // per item
@@ -316,6 +320,19 @@ static Launch launch_of(nebula_ctx* ctx) {
   return Launch{ctx->stream, ctx->num_sms, &ctx->launches, ctx->timing ? timing_mark : nullptr, ctx};
 }
 
+// Call ids ("t"): 0 = ALL buckets, 1 + b = bucket b alone, B + 1 / B + 2 = the first / second
+// half of the buckets (internal: the pipelined top-k step).  ALL and the halves address the
+// caller's flat buffers at the buckets' offsets ("flat"); a single-bucket call at offset 0.
+static int tab_of(int32_t bucket) { return bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket; }
+static bool flat_of(const nebula_ctx* ctx, int t) { return t == 0 || t > (int)ctx->b.size(); }
+static void call_range(const nebula_ctx* ctx, int t, int* lo, int* hi) {
+  const int B = (int)ctx->b.size(), mid = B / 2;
+  if (t == 0) { *lo = 0; *hi = B; }
+  else if (t <= B) { *lo = t - 1; *hi = t; }
+  else if (t == B + 1) { *lo = 0; *hi = mid; }
+  else { *lo = mid; *hi = B; }
+}
+
 // Bucket range of a call: ALL -> [0, B), b -> [b, b+1).
 static bool range_of(nebula_ctx* ctx, int32_t bucket, int* lo, int* hi) {
   const int B = (int)ctx->b.size();
@@ -339,18 +356,20 @@ static nebula_status build_tables(nebula_ctx* ctx, int lay) {
   const uint64_t rtotal = ctx->total_cn;
   std::vector<uint64_t> sbase(B + 1, 0);  // absolute start-offset bases (TOPK reduce)
   for (int bi = 0; bi < B; ++bi) sbase[bi + 1] = sbase[bi] + (uint64_t)ctx->P * ((ctx->b[bi].cn + 2047) / 2048 + 1);
-  for (int t = 0; t <= B; ++t) {  // t == 0: ALL; t == 1 + b: bucket b alone
+  for (int t = 0; t <= B + 2; ++t) {  // every call id (tab_of / call_range)
     Table ct, rt;
     ct.first = (int)items.size();
     rt.first = (int)ritems.size();
-    const int blo = t == 0 ? 0 : t - 1, bhi = t == 0 ? B : t;
+    int blo, bhi;
+    call_range(ctx, t, &blo, &bhi);
+    const bool flat = flat_of(ctx, t);
     for (int bi = blo; bi < bhi; ++bi) {
       const BucketInfo& bk = ctx->b[bi];
       for (int c = 0; c < ctx->Ploc; ++c) {  // bucket-major, cluster-minor
         Item it{};
         if (ctx->G > 1 && !ctx->xtopk) it.g_off = bk.soff;
-        else if (ctx->loopback) it.g_off = (t == 0) ? (uint64_t)c * ctx->total_n + bk.off : (uint64_t)c * bk.n;
-        else it.g_off = (t == 0) ? bk.off : 0;
+        else if (ctx->loopback) it.g_off = flat ? (uint64_t)c * ctx->total_n + bk.off : (uint64_t)c * bk.n;
+        else it.g_off = flat ? bk.off : 0;
         it.r_off = (uint64_t)c * rtotal + bk.coff;
         const int cl = ctx->loopback ? c : ctx->me;
         it.slot_off = bk.so[lay] + (uint64_t)cl * bk.pb[lay];
@@ -364,7 +383,7 @@ static nebula_status build_tables(nebula_ctx* ctx, int lay) {
       RItem ri{};
       ri.slot_off = bk.so[lay];
       ri.pb = bk.pb[lay];
-      ri.out_off = (ctx->G > 1 && !ctx->xtopk) ? bk.soff : (t == 0 ? bk.off : 0);
+      ri.out_off = (ctx->G > 1 && !ctx->xtopk) ? bk.soff : (flat ? bk.off : 0);
       ri.n = bk.cn;
       ri.k = bk.k;
       ri.chunk0 = rt.chunks;
@@ -450,6 +469,9 @@ static void release(nebula_ctx* ctx) {
   for (cudaEvent_t e : ctx->ev_in) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_done) cudaEventDestroy(e);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   cudaFree(ctx->d_topk_mem);
   cudaFree(ctx->d_bar);
@@ -666,14 +688,15 @@ static bool intra_p2p_on(const nebula_ctx* ctx) { return ctx->G > 1 && ctx->intr
 static nebula_status build_itables(nebula_ctx* ctx) {
   const int B = (int)ctx->b.size();
   std::vector<IItem> items;
-  for (int t = 0; t <= B; ++t) {
+  for (int t = 0; t <= B + 2; ++t) {
     ITable T;
     T.first = (int)items.size();
-    const int blo = t == 0 ? 0 : t - 1, bhi = t == 0 ? B : t;
+    int blo, bhi;
+    call_range(ctx, t, &blo, &bhi);
     for (int bi = blo; bi < bhi; ++bi) {
       const BucketInfo& bk = ctx->b[bi];
       IItem it{};
-      it.off = t == 0 ? bk.off : 0;
+      it.off = flat_of(ctx, t) ? bk.off : 0;
       it.coff = bk.soff;
       it.cn = bk.sn;
       it.chunk0 = T.chunks;
@@ -901,7 +924,7 @@ nebula_status nebula_set_stream(nebula_ctx* ctx, void* stream) {
 // shards of the cluster, so every shard quantises with the scale of the whole cluster bucket.
 // P2P: a mailbox + flag kernel over the cluster's GPUs; else one 4-byte-per-bucket
 // ncclAllReduce(max) on the intra-cluster communicator.
-static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi, uint64_t seq) {
+static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int lo, int hi, uint64_t seq) {
   if (intra_p2p_on(ctx)) {
     PeerU mails{};
     for (int j = 0; j < ctx->G; ++j) mails.p[j] = ctx->ip_mail[j];
@@ -911,19 +934,18 @@ static nebula_status cluster_scale(nebula_ctx* ctx, const Launch& L, int32_t buc
     return NEBULA_OK;
   }
   Mark mk(L, PH_NCCL_SCALE);
-  uint32_t* w = ctx->d_scratch + (bucket == NEBULA_ALL_BUCKETS ? 0 : bucket);
-  const size_t cnt = bucket == NEBULA_ALL_BUCKETS ? ctx->b.size() : 1;
-  CKN(ncclAllReduce(w, w, cnt, ncclUint32, ncclMax, ctx->intra, ctx->stream));
+  uint32_t* w = ctx->d_scratch + lo;   // Ploc == 1 when G > 1: word b is bucket b
+  CKN(ncclAllReduce(w, w, (size_t)(hi - lo), ncclUint32, ncclMax, ctx->intra, ctx->stream));
   return NEBULA_OK;
 }
 
 // G > 1: this GPU's shard of the cluster mean (R20).  P2P: push the peers' slices, flag
 // handshake, fixed-order sum / G (bit-identical to the oracle for any input); else NCCL
 // ReduceScatter(avg) (order and pre-scaling are NCCL's).
-static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi,
+static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int t, int lo, int hi,
                                           const float* g, uint64_t seq) {
   if (intra_p2p_on(ctx)) {
-    const ITable& T = ctx->itab[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+    const ITable& T = ctx->itab[t];
     const IItem* it = ctx->d_iitems + T.first;
     const bool vec = T.aligned && (uintptr_t)g % 16 == 0;
     if (ctx->intra_opt == 2) {   // copy engines: one DMA per (bucket, peer) over NVLink
@@ -931,7 +953,7 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
       for (int i = lo; i < hi; ++i) {
         const BucketInfo& bk = ctx->b[i];
         if (!bk.sn) continue;
-        const float* src = g + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+        const float* src = g + (flat_of(ctx, t) ? bk.off : 0);
         for (int j = 0; j < ctx->G; ++j)
           if (j != ctx->local_rank)
             CKC(cudaMemcpyAsync(ctx->ip_recv[j] + (uint64_t)ctx->local_rank * ctx->total_sn + bk.soff,
@@ -956,7 +978,7 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
   for (int i = lo; i < hi; ++i) {
     const BucketInfo& bk = ctx->b[i];
     if (!bk.sn) continue;
-    const float* src = g + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+    const float* src = g + (flat_of(ctx, t) ? bk.off : 0);
     CKN(ncclReduceScatter(src, ctx->d_shard_in + bk.soff, bk.sn, ncclFloat32, ncclAvg, ctx->intra, ctx->stream));
   }
   CKN(ncclGroupEnd());
@@ -965,20 +987,20 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int3
 
 // G > 1: every GPU of the cluster gathers the P2P-averaged shards into dev_out.  P2P: flag
 // handshake, then NVLink loads of the peers' shards; else NCCL AllGather.
-static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int32_t bucket, int lo, int hi, float* dev_out,
+static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int t, int lo, int hi, float* dev_out,
                                       uint64_t seq, bool from_in = false) {
   // from_in (xtopk): gather the G mean shards (d_shard_in) instead of the averaged ones
   float* const* srcs = from_in ? ctx->ip_in : ctx->ip_out;
   float* own = from_in ? ctx->d_shard_in : ctx->d_shard_out;
   if (intra_p2p_on(ctx)) {
-    const ITable& T = ctx->itab[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+    const ITable& T = ctx->itab[t];
     launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_ag), ctx->d_arr_ag, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_AG);
     if (ctx->intra_opt == 2) {   // copy engines: one DMA per (bucket, GPU of the cluster)
       Mark mk(L, PH_AG_PULL);
       for (int i = lo; i < hi; ++i) {
         const BucketInfo& bk = ctx->b[i];
         if (!bk.sn) continue;
-        float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+        float* dst = dev_out + (flat_of(ctx, t) ? bk.off : 0);
         for (int j = 0; j < ctx->G; ++j)
           CKC(cudaMemcpyAsync(dst + (uint64_t)j * bk.sn, srcs[j] + bk.soff, bk.sn * 4, cudaMemcpyDeviceToDevice,
                               ctx->stream));
@@ -999,21 +1021,18 @@ static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int32_t 
   for (int i = lo; i < hi; ++i) {
     const BucketInfo& bk = ctx->b[i];
     if (!bk.sn) continue;
-    float* dst = dev_out + (bucket == NEBULA_ALL_BUCKETS ? bk.off : 0);
+    float* dst = dev_out + (flat_of(ctx, t) ? bk.off : 0);
     CKN(ncclAllGather(own + bk.soff, dst, bk.sn, ncclFloat32, ctx->intra, ctx->stream));
   }
   CKN(ncclGroupEnd());
   return NEBULA_OK;
 }
 
-static nebula_status zero_scratch(nebula_ctx* ctx, const Launch& L, int32_t bucket) {
+static nebula_status zero_scratch(nebula_ctx* ctx, const Launch& L, int lo, int hi) {
   Mark mk(L, PH_MEMSET);
-  if (bucket == NEBULA_ALL_BUCKETS) {
-    CKC(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(uint32_t) * ctx->Ploc * ctx->b.size(), ctx->stream));
-  } else {
-    for (int c = 0; c < ctx->Ploc; ++c)
-      CKC(cudaMemsetAsync(ctx->d_scratch + c * ctx->b.size() + bucket, 0, sizeof(uint32_t), ctx->stream));
-  }
+  for (int c = 0; c < ctx->Ploc; ++c)
+    CKC(cudaMemsetAsync(ctx->d_scratch + (size_t)c * ctx->b.size() + lo, 0, sizeof(uint32_t) * (size_t)(hi - lo),
+                        ctx->stream));
   return NEBULA_OK;
 }
 
@@ -1032,10 +1051,9 @@ static nebula_status stage_start(nebula_ctx* ctx, int lo, int hi) {
 }
 
 // ============================================================================ stages
-nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step) {
-  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+static nebula_status compress_t(nebula_ctx* ctx, int t, const float* dev_grad, uint64_t step) {
   int lo, hi;
-  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  call_range(ctx, t, &lo, &hi);
   if (!dev_grad && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_grad");
   nebula_status st0 = stage_start(ctx, lo, hi);
   if (st0 != NEBULA_OK) return st0;
@@ -1045,18 +1063,18 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   const int method = method_at(ctx, step);
   const bool ef = ctx->codec.error_feedback != 0;
   const int lay = layout_of(ctx, method);
-  const Table& T = ctx->ctab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+  const Table& T = ctx->ctab[lay][t];
   const Launch L = launch_of(ctx);
   const uint64_t seq = ctx->b[lo].seq + 1;   // this exchange; committed once everything is enqueued
   const Dests dst = dests_of(ctx, seq);
 
   const float* gbase = dev_grad;
   if (ctx->G > 1) {  // intra-cluster mean of the G GPUs' buckets -> this GPU's shard (R20)
-    nebula_status s = intra_reduce_scatter(ctx, L, bucket, lo, hi, dev_grad, seq);
+    nebula_status s = intra_reduce_scatter(ctx, L, t, lo, hi, dev_grad, seq);
     if (s != NEBULA_OK) return s;
     gbase = ctx->d_shard_in;
     if (ctx->xtopk) {   // R34: every GPU of the cluster codes the whole cluster-mean bucket
-      s = intra_all_gather(ctx, L, bucket, lo, hi, ctx->d_full, seq, true);
+      s = intra_all_gather(ctx, L, t, lo, hi, ctx->d_full, seq, true);
       if (s != NEBULA_OK) return s;
       gbase = ctx->d_full;
     }
@@ -1082,7 +1100,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       // one per-bucket scale: max-abs words zeroed, then either the single-pass warp-specialised
       // kernel (16-B aligned, buckets averaging >= 1M elements, no cluster-wide scale) or the
       // max-abs pass, [the cluster-wide max (R28)], and the quantise pass
-      { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
+      { nebula_status zs = zero_scratch(ctx, L, lo, hi); if (zs != NEBULA_OK) return zs; }
       const int kind = method == M_FP8 ? 1 : (method == M_QSGD ? 2 : (method == M_FP8_E5M2 ? 3 : 0));
       const SrArgs sr{ctx->sr_seed, step, (uint32_t)ctx->me, (uint32_t)ctx->local_rank, (uint32_t)ctx->b.size()};
       // (SELF: auto never picks the cooperative kernel — group members' grids share one GPU)
@@ -1095,7 +1113,7 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
         break;
       }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
-      if (xscale) { nebula_status xs = cluster_scale(ctx, L, bucket, lo, hi, seq); if (xs != NEBULA_OK) return xs; }
+      if (xscale) { nebula_status xs = cluster_scale(ctx, L, lo, hi, seq); if (xs != NEBULA_OK) return xs; }
       if (kind == 1 || kind == 3)
         launch_fp8_quant(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
                          kind == 3 ? 2 : 1);
@@ -1104,9 +1122,14 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
       break;
     }
     case M_TOPK: {
-      const int item0 = bucket == NEBULA_ALL_BUCKETS ? 0 : bucket * ctx->Ploc;
-      launch_topk(L, ef, vec, ctx->tk, item0, T.count, T.chunks, items, gbase, ctx->d_resid, dst,
-                  ctx->d_flags, ctx->codec.topk_values, ctx->tk_mtiles[bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket]);
+      const int item0 = lo * ctx->Ploc;
+      TopkBuffers tkb = ctx->tk;
+      if (t == (int)ctx->b.size() + 2) {   // second half of a pipelined step: own counters / staging
+        tkb.ctrs = ctx->tk.ctrs + 4;
+        tkb.stage = ctx->tk_stage2;
+      }
+      launch_topk(L, ef, vec, tkb, item0, T.count, T.chunks, items, gbase, ctx->d_resid, dst,
+                  ctx->d_flags, ctx->codec.topk_values, ctx->tk_mtiles[t]);
       break;
     }
   }
@@ -1119,10 +1142,16 @@ nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_
   return NEBULA_OK;
 }
 
-nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
+nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  return compress_t(ctx, tab_of(bucket), dev_grad, step);
+}
+
+static nebula_status exchange_t(nebula_ctx* ctx, int t) {
+  int lo, hi;
+  call_range(ctx, t, &lo, &hi);
   for (int i = lo; i < hi; ++i)
     if (ctx->b[i].state != ST_COMPRESSED) return fail(ctx, NEBULA_ERR_STATE, "exchange before compress");
   DevGuard dg(ctx->device);
@@ -1147,10 +1176,16 @@ nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
   return NEBULA_OK;
 }
 
-nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out) {
+nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  return exchange_t(ctx, tab_of(bucket));
+}
+
+static nebula_status reduce_t(nebula_ctx* ctx, int t, float* dev_out) {
+  int lo, hi;
+  call_range(ctx, t, &lo, &hi);
   if (!dev_out && elems_of(ctx, lo, hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null dev_out");
   for (int i = lo; i < hi; ++i)
     if (ctx->b[i].state != ST_EXCHANGED) return fail(ctx, NEBULA_ERR_STATE, "decompress_reduce before exchange");
@@ -1159,7 +1194,7 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
     if (ctx->b[i].method != method) return fail(ctx, NEBULA_ERR_STATE, "buckets compressed with different methods");
   DevGuard dg(ctx->device);
   const int lay = layout_of(ctx, method);
-  const Table& T = ctx->rtab[lay][bucket == NEBULA_ALL_BUCKETS ? 0 : 1 + bucket];
+  const Table& T = ctx->rtab[lay][t];
   const bool sharded = ctx->G > 1 && !ctx->xtopk;   // reduce this GPU's shard, then all-gather
   float* obase = sharded ? ctx->d_shard_out : dev_out;
   const bool vec = T.aligned && ((uintptr_t)obase % 16 == 0);
@@ -1186,12 +1221,19 @@ nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* d
     launch_reduce_dense(L, method, ctx->P, vec, items, T.count, T.chunks, sources_of(ctx, ctx->b[lo]), obase);
   CKC(cudaGetLastError());
   if (sharded) {
-    nebula_status s = intra_all_gather(ctx, L, bucket, lo, hi, dev_out, ctx->b[lo].seq);
+    nebula_status s = intra_all_gather(ctx, L, t, lo, hi, dev_out, ctx->b[lo].seq);
     if (s != NEBULA_OK) return s;
   }
   mirror_flags(ctx);
   for (int i = lo; i < hi; ++i) ctx->b[i].state = ST_IDLE;
   return NEBULA_OK;
+}
+
+nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out) {
+  if (!ctx) return NEBULA_ERR_INVALID_ARG;
+  int lo, hi;
+  if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
+  return reduce_t(ctx, tab_of(bucket), dev_out);
 }
 
 // Decode ONE cluster's payload (no averaging) — the pipeline-hop use of the codecs (SURVEY.md
@@ -1277,7 +1319,7 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   st0 = pending_device_error(ctx);
   if (st0 != NEBULA_OK) return st0;
   const uint64_t seq = ctx->b[lo].seq + 1;
-  { nebula_status zs = zero_scratch(ctx, L, bucket); if (zs != NEBULA_OK) return zs; }
+  { nebula_status zs = zero_scratch(ctx, L, lo, hi); if (zs != NEBULA_OK) return zs; }
   Peers pe{};
   if (!ctx->loopback && ctx->P > 1) pe = inter_peers(ctx);
   BucketInfo probe = ctx->b[lo];
@@ -1303,7 +1345,47 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   return NEBULA_OK;
 }
 
+// Pipelined top-k step: the buckets split into two halves, each a full compress -> exchange ->
+// reduce on its own stream, so the latency-bound selection kernels of one half (bracket,
+// scan, resolve, merge, one CTA per bucket or small grids) overlap the HBM-bound stage pass of
+// the other.  Same kernels, same per-bucket state, same bits.  LOOPBACK and P2P exchanges only
+// (two NCCL collectives on one communicator from two streams could interleave differently on
+// different ranks); SELF runs the staged calls as its rules say.
+static bool topk_pipelinable(const nebula_ctx* ctx, int32_t bucket, uint64_t step) {
+  return ctx->topk_pipe && bucket == NEBULA_ALL_BUCKETS && method_at(ctx, step) == M_TOPK && ctx->b.size() >= 2 &&
+         ctx->G == 1 && !ctx->self && ctx->xmode != 1 && ctx->topk_reduce == 1;
+}
+
+static nebula_status topk_step_pipelined(nebula_ctx* ctx, const float* dev_grad, float* dev_out, uint64_t step) {
+  DevGuard dg(ctx->device);
+  if (!ctx->side) {
+    CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  const int B = (int)ctx->b.size();
+  for (int i = 1; i < B; ++i)   // validate before anything is enqueued (as the ALL call would)
+    if (ctx->b[i].state != ST_IDLE || ctx->b[i].seq != ctx->b[0].seq || ctx->b[0].state != ST_IDLE)
+      return fail(ctx, NEBULA_ERR_STATE, "ALL-bucket step over buckets that are mid-step or at different step counts");
+  CKC(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  CKC(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  nebula_status s = compress_t(ctx, B + 1, dev_grad, step);
+  if (s == NEBULA_OK) s = exchange_t(ctx, B + 1);
+  if (s == NEBULA_OK) s = reduce_t(ctx, B + 1, dev_out);
+  if (s != NEBULA_OK) return s;
+  cudaStream_t main = ctx->stream;
+  ctx->stream = ctx->side;
+  s = compress_t(ctx, B + 2, dev_grad, step);
+  if (s == NEBULA_OK) s = exchange_t(ctx, B + 2);
+  if (s == NEBULA_OK) s = reduce_t(ctx, B + 2, dev_out);
+  ctx->stream = main;
+  CKC(cudaEventRecord(ctx->ev_join, ctx->side));
+  CKC(cudaStreamWaitEvent(main, ctx->ev_join, 0));
+  return s;
+}
+
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
+  if (ctx && topk_pipelinable(ctx, bucket, step) && dev_grad && dev_out) return topk_step_pipelined(ctx, dev_grad, dev_out, step);
   if (ctx) {
     int lo, hi;
     if (range_of(ctx, bucket, &lo, &hi) && hi > lo && dev_grad && dev_out &&
@@ -1480,6 +1562,11 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
       if (bk.state != ST_IDLE) return fail(ctx, NEBULA_ERR_STATE, "change the exchange only between steps");
     ctx->xopt = (int)value;
     ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? auto_xmode(ctx) : (int)value);
+    return NEBULA_OK;
+  }
+  if (option == NEBULA_OPT_TOPK_PIPELINE) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "top-k pipeline option must be 0 or 1");
+    ctx->topk_pipe = (int)value;
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_INTRA) {

@@ -31,7 +31,7 @@ def bits(a):
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
                  start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
-                 fp16_kernel=None, sr_seed=0, topk_reduce=None, step_config=None):
+                 fp16_kernel=None, sr_seed=0, topk_reduce=None, step_config=None, topk_pipeline=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
@@ -42,6 +42,8 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
             ctx.set_step_fusion(False)
     if fp16_kernel:
         ctx.set_fp16_kernel(fp16_kernel)
+    if topk_pipeline is not None:                    # NEBULA_OPT_TOPK_PIPELINE
+        ctx.set_option(nb.OPT_TOPK_PIPELINE, int(topk_pipeline))
     if step_config is not None:                      # fused-step warp split (NEBULA_OPT_STEP_FUSION)
         ctx.set_option(nb.OPT_STEP_FUSION, 2 + step_config)
     if sr_seed:
@@ -324,6 +326,15 @@ def test_config1_shape(nb):
 @pytest.mark.parametrize("P", [2, 4])
 def test_topk_parity(nb, vt, rho, P):
     run_loopback(nb, O.TOPK, [200003, 4096, 3], P, vt=vt, rho=rho)
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+@pytest.mark.parametrize("sizes", [[200003, 4096], [1, 70001, 3, 4096 * 9, 2], [300000] * 5])
+def test_topk_two_stream_pipeline(nb, pipeline, sizes):
+    """The ALL-bucket top-k step on two streams (first / second half of the buckets, own
+    counters and staging) and on one: both bit-exact vs the oracle, incl. odd bucket counts."""
+    run_loopback(nb, O.TOPK, sizes, 2, rho=0.02, steps=3, topk_pipeline=pipeline)
+    run_loopback(nb, O.TOPK, sizes, 3, vt=O.VAL_I8, rho=0.2, steps=2, topk_pipeline=pipeline)
 
 
 @pytest.mark.parametrize("variant", [0, 1])
