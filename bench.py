@@ -415,6 +415,9 @@ def main():
         else:
             byt = kernel_bytes(dom, method, vt, P, ef, n_local, k_per_cluster * (P if world == 1 else 1))
         if byt:
+            # byt covers every element the phase processes in a step; with several launches per
+            # step (e.g. the two halves of the pipelined top-k step) each launch moves its share
+            byt = byt / max(1.0, cnt / args.steps)
             per_launch_s = tot / cnt * 1e-3
             ach = byt / per_launch_s / 1e9
             wc = workload_config(args, n, P, G)
