@@ -1109,7 +1109,9 @@ static nebula_status compress_t(nebula_ctx* ctx, int t, const float* dev_grad, u
                            (ctx->int8_kernel == 0 && !ctx->self &&
                             elems_of(ctx, lo, hi) / ctx->G >= (uint64_t)(hi - lo) * (1ull << 20)));
       if (single) {
-        launch_ws_compress(L, ef, kind, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags, ctx->d_bar, sr);
+        // done words of the call's own items: the two halves of a pipelined step run concurrently
+        launch_ws_compress(L, ef, kind, items, T.count, gbase, ctx->d_resid, dst, ctx->d_scratch, ctx->d_flags,
+                           ctx->d_bar + (size_t)lo * ctx->Ploc, sr);
         break;
       }
       launch_absmax(L, ef, vec, items, T.count, T.chunks, gbase, ctx->d_resid, ctx->d_scratch);
@@ -1345,18 +1347,24 @@ static nebula_status int8_step_fused(nebula_ctx* ctx, int lo, int hi, int32_t bu
   return NEBULA_OK;
 }
 
-// Pipelined top-k step: the buckets split into two halves, each a full compress -> exchange ->
-// reduce on its own stream, so the latency-bound selection kernels of one half (bracket,
-// scan, resolve, merge, one CTA per bucket or small grids) overlap the HBM-bound stage pass of
-// the other.  Same kernels, same per-bucket state, same bits.  LOOPBACK and P2P exchanges only
-// (two NCCL collectives on one communicator from two streams could interleave differently on
-// different ranks); SELF runs the staged calls as its rules say.
-static bool topk_pipelinable(const nebula_ctx* ctx, int32_t bucket, uint64_t step) {
-  return ctx->topk_pipe && bucket == NEBULA_ALL_BUCKETS && method_at(ctx, step) == M_TOPK && ctx->b.size() >= 2 &&
-         ctx->G == 1 && !ctx->self && ctx->xmode != 1 && ctx->topk_reduce == 1;
+// Pipelined step: the buckets split into two halves, each a full compress -> exchange ->
+// reduce on its own stream.  TOPK: the latency-bound selection kernels of one half (bracket,
+// scan, resolve, merge: one CTA per bucket or small grids) overlap the HBM-bound stage pass of
+// the other.  G > 1 (every codec): one half's NVLink-bound intra-cluster reduce-scatter /
+// all-gather overlaps the other half's HBM-bound codec.  Same kernels, same per-bucket state,
+// same bits.  P2P / LOOPBACK transports only (two NCCL collectives on one communicator from two
+// streams could interleave differently on different ranks); SELF runs the staged calls as its
+// rules say.
+static bool step_pipelinable(const nebula_ctx* ctx, int32_t bucket, uint64_t step) {
+  if (!ctx->topk_pipe || bucket != NEBULA_ALL_BUCKETS || ctx->b.size() < 2 || ctx->self) return false;
+  if (ctx->P > 1 && ctx->xmode == 1) return false;
+  const int m = method_at(ctx, step);
+  if (m == M_TOPK && ctx->topk_reduce != 1) return false;
+  if (ctx->G > 1) return intra_p2p_on(ctx);
+  return m == M_TOPK;
 }
 
-static nebula_status topk_step_pipelined(nebula_ctx* ctx, const float* dev_grad, float* dev_out, uint64_t step) {
+static nebula_status step_pipelined(nebula_ctx* ctx, const float* dev_grad, float* dev_out, uint64_t step) {
   DevGuard dg(ctx->device);
   if (!ctx->side) {
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
@@ -1385,7 +1393,7 @@ static nebula_status topk_step_pipelined(nebula_ctx* ctx, const float* dev_grad,
 }
 
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
-  if (ctx && topk_pipelinable(ctx, bucket, step) && dev_grad && dev_out) return topk_step_pipelined(ctx, dev_grad, dev_out, step);
+  if (ctx && step_pipelinable(ctx, bucket, step) && dev_grad && dev_out) return step_pipelined(ctx, dev_grad, dev_out, step);
   if (ctx) {
     int lo, hi;
     if (range_of(ctx, bucket, &lo, &hi) && hi > lo && dev_grad && dev_out &&
@@ -1564,8 +1572,8 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? auto_xmode(ctx) : (int)value);
     return NEBULA_OK;
   }
-  if (option == NEBULA_OPT_TOPK_PIPELINE) {
-    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "top-k pipeline option must be 0 or 1");
+  if (option == NEBULA_OPT_PIPELINE) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "pipeline option must be 0 or 1");
     ctx->topk_pipe = (int)value;
     return NEBULA_OK;
   }
