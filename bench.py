@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--exact-scale", action="store_true",
                     help="G > 1: cluster-wide INT8/FP8 scale (NEBULA_OPT_EXACT_SCALE, NEXT-3)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "push", "pull"])
-    ap.add_argument("--intra", default="auto", choices=["auto", "p2p", "p2p-ce", "nccl"],
+    ap.add_argument("--intra", default="auto", choices=["auto", "p2p", "nccl"],
                     help="G > 1: intra-cluster hop (NEBULA_OPT_INTRA)")
     ap.add_argument("--fp16-kernel", default="tma", choices=["tma", "plain"])
     ap.add_argument("--no-step-fusion", action="store_true",

@@ -287,8 +287,7 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 /*   NEBULA_OPT_INTRA (G > 1): 0 (default) the intra-cluster reduce-scatter / all-gather over
  *   NVLink peer memory with a fixed summation order when every GPU of the cluster is mapped
  *   (SM-issued NVLink stores / loads), 1 NCCL ReduceScatter(avg) / AllGather (NCCL transport
- *   only), 2 the same as 0 with the NVLink transfers on the copy engines (one DMA per bucket
- *   and peer; same bits).  Only between steps. */
+ *   only).  Only between steps. */
 #define NEBULA_OPT_INTRA 8
 /*   NEBULA_OPT_PIPELINE: 1 (default) an ALL-bucket nebula_step over >= 2 buckets runs its two
  *   halves of buckets on two streams when that helps — TOPK (G = 1, LOOPBACK or P2P exchange):
@@ -302,8 +301,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */
 int32_t nebula_exchange_mode(const nebula_ctx* ctx);
 /* Intra-cluster hop in use: 0 none (G = 1), 1 NCCL ReduceScatter(avg) / AllGather, 2 P2P
- * fixed-order reduce-scatter / all-gather over NVLink peer memory, 3 the same on copy engines;
- * -1 for NULL. */
+ * fixed-order reduce-scatter / all-gather over NVLink peer memory; -1 for NULL. */
 int32_t nebula_intra_mode(const nebula_ctx* ctx);
 
 /* Per-kernel device timers.  When enabled, every kernel / collective the context enqueues is

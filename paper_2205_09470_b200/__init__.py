@@ -354,8 +354,8 @@ class SyncContext:
 
     def set_intra(self, which: str):
         """G > 1: 'p2p' (default: fixed-order reduce-scatter / all-gather over NVLink peer
-        memory) | 'p2p-ce' (the same transfers on copy engines) | 'nccl' (NEBULA_OPT_INTRA)."""
-        self.set_option(OPT_INTRA, {"p2p": 0, "auto": 0, "nccl": 1, "p2p-ce": 2}[which])
+        memory) | 'nccl' (NEBULA_OPT_INTRA)."""
+        self.set_option(OPT_INTRA, {"p2p": 0, "auto": 0, "nccl": 1}[which])
 
     def set_exchange(self, which: str):
         """'auto' | 'nccl' | 'push' | 'pull' (NEBULA_OPT_EXCHANGE; between steps only)."""
@@ -365,7 +365,7 @@ class SyncContext:
         return EXCHANGE_MODES[self._L.nebula_exchange_mode(self._h)]
 
     def intra_mode(self) -> str:
-        return {0: "none", 1: "nccl", 2: "p2p", 3: "p2p-ce"}[self._L.nebula_intra_mode(self._h)]
+        return {0: "none", 1: "nccl", 2: "p2p"}[self._L.nebula_intra_mode(self._h)]
 
     def timing_enable(self, on: bool = True):
         self._ck(self._L.nebula_timing_enable(self._h, int(bool(on))))

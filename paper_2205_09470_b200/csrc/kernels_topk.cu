@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__
 
 // ---------------------------------------------------------------- A: EF pass + classify + stage
 template <bool EF, bool VEC>
-__global__ void __launch_bounds__(kThreads, 4) k_topk_stage(const Item* __restrict__ aitems,
+__global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restrict__ aitems,
                                                          const TopkItem* __restrict__ titems,
                                                          TopkState* __restrict__ st, int nitems, uint64_t chunks,
                                                          const float* __restrict__ gbase, float* __restrict__ rbase,

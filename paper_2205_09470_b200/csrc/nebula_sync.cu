@@ -948,18 +948,7 @@ static nebula_status intra_reduce_scatter(nebula_ctx* ctx, const Launch& L, int 
     const ITable& T = ctx->itab[t];
     const IItem* it = ctx->d_iitems + T.first;
     const bool vec = T.aligned && (uintptr_t)g % 16 == 0;
-    if (ctx->intra_opt == 2) {   // copy engines: one DMA per (bucket, peer) over NVLink
-      Mark mk(L, PH_RS_PUSH);
-      for (int i = lo; i < hi; ++i) {
-        const BucketInfo& bk = ctx->b[i];
-        if (!bk.sn) continue;
-        const float* src = g + (flat_of(ctx, t) ? bk.off : 0);
-        for (int j = 0; j < ctx->G; ++j)
-          if (j != ctx->local_rank)
-            CKC(cudaMemcpyAsync(ctx->ip_recv[j] + (uint64_t)ctx->local_rank * ctx->total_sn + bk.soff,
-                                src + (uint64_t)j * bk.sn, bk.sn * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-      }
-    } else {
+    {
       PeerF recv{};
       for (int j = 0; j < ctx->G; ++j) recv.p[j] = ctx->ip_recv[j];
       recv.n = ctx->G;
@@ -995,18 +984,6 @@ static nebula_status intra_all_gather(nebula_ctx* ctx, const Launch& L, int t, i
   if (intra_p2p_on(ctx)) {
     const ITable& T = ctx->itab[t];
     launch_exchange_flags(L, intra_peers(ctx, ctx->ip_arr_ag), ctx->d_arr_ag, lo, hi, seq, ctx->d_flags, PH_P2P_FLAGS_AG);
-    if (ctx->intra_opt == 2) {   // copy engines: one DMA per (bucket, GPU of the cluster)
-      Mark mk(L, PH_AG_PULL);
-      for (int i = lo; i < hi; ++i) {
-        const BucketInfo& bk = ctx->b[i];
-        if (!bk.sn) continue;
-        float* dst = dev_out + (flat_of(ctx, t) ? bk.off : 0);
-        for (int j = 0; j < ctx->G; ++j)
-          CKC(cudaMemcpyAsync(dst + (uint64_t)j * bk.sn, srcs[j] + bk.soff, bk.sn * 4, cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-      }
-      return NEBULA_OK;
-    }
     PeerF outs{};
     for (int j = 0; j < ctx->G; ++j) outs.p[j] = srcs[j];
     outs.n = ctx->G;
@@ -1578,7 +1555,7 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     return NEBULA_OK;
   }
   if (option == NEBULA_OPT_INTRA) {
-    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "intra option must be 0, 1 or 2");
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "intra option must be 0 or 1");
     if (value == 1 && ctx->G > 1 && !ctx->intra)
       return fail(ctx, NEBULA_ERR_UNSUPPORTED, "no intra-cluster NCCL communicator (SELF transport)");
     for (const auto& bk : ctx->b)
@@ -1594,7 +1571,7 @@ int32_t nebula_exchange_mode(const nebula_ctx* ctx) { return ctx ? ctx->xmode : 
 int32_t nebula_intra_mode(const nebula_ctx* ctx) {
   if (!ctx) return -1;
   if (ctx->G == 1) return 0;
-  return intra_p2p_on(ctx) ? (ctx->intra_opt == 2 ? 3 : 2) : 1;
+  return intra_p2p_on(ctx) ? 2 : 1;
 }
 
 nebula_status nebula_timing_enable(nebula_ctx* ctx, int32_t on) {

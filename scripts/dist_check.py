@@ -55,7 +55,7 @@ def main():
              (O.FP8, 0, "fused-ws", False, "p2p"), (O.QSGD, 0, "fused-ws", False, "p2p")]   # fused step over P2P (G = 1)
     if G > 1:
         cases += [(O.TOPK, O.VAL_F32, None, "exact-topk", "p2p"), (O.TOPK, O.VAL_I8, None, "exact-topk", "nccl"),
-                  (O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"), (O.INT8, 0, None, False, "p2p-ce"),
+                  (O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"),
                   (O.TOPK, O.VAL_F32, None, False, "nccl"), (O.INT8, 0, None, True, "nccl")]
     intra_seen = set()
     modes_seen = set()

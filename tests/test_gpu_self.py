@@ -152,13 +152,6 @@ def test_self_hierarchical_exact_any_input(nb, P, G, per_bucket):
     run_self(nb, O.INT8, P, G, [s * G for s in [4096, 12288, 300004, 8]], per_bucket=per_bucket)
 
 
-@pytest.mark.parametrize("P,G", [(1, 2), (2, 2), (1, 4)])
-def test_self_hierarchical_copy_engines(nb, P, G):
-    """NEBULA_OPT_INTRA = 2: the intra-cluster transfers on copy engines, same bits."""
-    run_self(nb, O.INT8, P, G, [s * G for s in [4096, 300004, 8]], intra="p2p-ce", per_bucket=True)
-    run_self(nb, O.TOPK, P, G, [s * G for s in [4096, 300004, 8]], intra="p2p-ce", exact_topk=True)
-
-
 @pytest.mark.parametrize("method,vt", [(O.FP16, 0), (O.TOPK, O.VAL_F32), (O.TOPK, O.VAL_I8), (O.FP8, 0),
                                        (O.QSGD, 0), (O.IDENTITY, 0)])
 def test_self_hierarchical_codecs(nb, method, vt):
