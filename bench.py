@@ -65,6 +65,10 @@ def parse():
                     help="run compress / exchange / reduce as separate launches (NEBULA_OPT_STEP_FUSION=1)")
     ap.add_argument("--step-config", type=int, default=None, help="fused-step warp split 0..10 (tuning)")
     ap.add_argument("--int8-kernel", default="auto", choices=["auto", "two-pass", "single-pass", "fused-ws"])
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="one stream per step (no two-half pipelining of ALL-bucket steps)")
+    ap.add_argument("--topk-stage", default="tma", choices=["tma", "plain"],
+                    help="top-k stage pass: TMA ring (default) or plain vector loads")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -275,7 +279,9 @@ def workload_config(args, n, P, G=1):
             "elements_per_cluster": n, "clusters": P, "gpus_per_cluster": G, "method": mname,
             "bucketing": f"fixed {args.bucket_mib:g} MiB slices of the flat gradient",
             "transport": "loopback" if args.gpus == 1 else "nvlink",
-            "l2": "inputs (>= 1.1 GB per cluster) exceed the 126 MB L2; no flush needed"}
+            "l2": (f"per-GPU working set (gradient + residual + output, {3 * 4 * n / 1e6:.0f} MB) exceeds "
+                   "the 126 MB L2; no flush needed"),
+            "pipeline": "off" if args.no_pipeline else "auto"}
 
 
 # ----------------------------------------------------------------------------- main arm
@@ -344,6 +350,10 @@ def main():
         ctx.set_step_fusion(False)
     if args.step_config is not None:
         ctx.set_option(nb.OPT_STEP_FUSION, 2 + args.step_config)
+    if args.no_pipeline:
+        ctx.set_option(nb.OPT_PIPELINE, 0)
+    if method == 3 and args.topk_stage == "plain":
+        ctx.set_option(nb.OPT_TOPK_STAGE, 0)
     if world > 1 and args.exchange != "auto":
         ctx.set_exchange(args.exchange)
     if G > 1 and args.intra != "auto":

@@ -291,11 +291,15 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
 #define NEBULA_OPT_INTRA 8
 /*   NEBULA_OPT_PIPELINE: 1 (default) an ALL-bucket nebula_step over >= 2 buckets runs its two
  *   halves of buckets on two streams when that helps — TOPK (G = 1, LOOPBACK or P2P exchange):
- *   the latency-bound selection kernels of one half overlap the streaming pass of the other;
- *   G > 1 with the P2P intra-cluster hop (every codec): one half's NVLink-bound intra-cluster
- *   traffic overlaps the other half's HBM-bound codec.  Same bits; 0 = one stream.  The
- *   context's stream waits for both halves. */
+ *   the latency-bound selection kernels of one half overlap the streaming pass of the other.
+ *   2 = also G > 1 with the P2P intra-cluster hop (every codec; one half's intra-cluster
+ *   traffic against the other half's codec — measured 1-9 % slower at 2 x 2 / 1 x 4, so not
+ *   the default).  Same bits; 0 = one stream.  The context's stream waits for both halves. */
 #define NEBULA_OPT_PIPELINE 9
+/*   NEBULA_OPT_TOPK_STAGE: top-k streaming pass (p = g + r, classify, stage) for 16-B aligned
+ *   calls, 1 (default) a producer warp feeds the tiles through a TMA shared-memory ring, 0 plain
+ *   vector loads.  Same results; any time between steps. */
+#define NEBULA_OPT_TOPK_STAGE 10
 nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value);
 
 /* Exchange transport in use: 0 LOOPBACK, 1 NCCL all-gather, 2 P2P push, 3 P2P pull; -1 for NULL. */

@@ -39,6 +39,7 @@ OPT_SR_SEED = 6
 OPT_TOPK_REDUCE = 7
 OPT_INTRA = 8
 OPT_PIPELINE = OPT_TOPK_PIPELINE = 9
+OPT_TOPK_STAGE = 10
 CODEC_EXACT_TOPK = 1   # NEBULA_CODEC_EXACT_TOPK (NEXT-3, R34)
 EXCHANGE_MODES = {0: "loopback", 1: "nccl-allgather", 2: "p2p-push", 3: "p2p-pull"}
 UNIQUE_ID_BYTES = 128

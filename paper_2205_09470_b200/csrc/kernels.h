@@ -189,6 +189,7 @@ struct TopkBuffers {
   uint64_t stage_entries;      // staging capacity (split evenly between the pass-A CTAs)
   uint64_t* splits;            // merge-path split points, 2 per merge tile
   uint32_t bracket_smem_keys;  // shared-memory sample capacity of k_topk_bracket
+  bool stage_tma = true;       // NEBULA_OPT_TOPK_STAGE: TMA-ring stage pass for 16-B aligned calls
   uint32_t* hist;       // [nitems][2048] fallback histograms
   uint32_t* ctrs;       // 2 dynamic tile counters
   uint32_t* start;      // sparse-reduce start offsets

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <new>
 
+#include "dense_common.cuh"
 #include "kernels.h"
 
 namespace nb {
@@ -307,24 +308,69 @@ __global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__
 }
 
 // ---------------------------------------------------------------- A: EF pass + classify + stage
-template <bool EF, bool VEC>
-__global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restrict__ aitems,
-                                                         const TopkItem* __restrict__ titems,
-                                                         TopkState* __restrict__ st, int nitems, uint64_t chunks,
-                                                         const float* __restrict__ gbase, float* __restrict__ rbase,
-                                                         unsigned long long* __restrict__ counts,
-                                                         unsigned long long* __restrict__ soff,
-                                                         uint2* __restrict__ stage, uint64_t region) {
+// TMA = false: plain vector loads, kThreads threads, 3 CTAs / SM.  TMA = true (16-B aligned
+// calls): one producer warp bulk-loads each chunk's g and r tiles into a kStageNS-deep
+// shared-memory ring (cp.async.bulk + mbarrier transaction counts, L2 evict_first) while the
+// kThreads consumer threads — the same per-thread code, reading the tiles from shared memory —
+// form p, stage and count; consumers synchronise on named barrier 1 (the producer runs ahead).
+constexpr int kStageNS = 3;
+struct __align__(128) StageTile {
+  float4 g[kChunkQuads];
+  float4 r[kChunkQuads];
+};
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" :: "n"(kThreads) : "memory"); }
+
+template <bool EF, bool VEC, bool TMA>
+__global__ void __launch_bounds__(TMA ? kThreads + 32 : kThreads, TMA ? 2 : 3)
+    k_topk_stage(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems, TopkState* __restrict__ st,
+                 int nitems, uint64_t chunks, const float* __restrict__ gbase, float* __restrict__ rbase,
+                 unsigned long long* __restrict__ counts, unsigned long long* __restrict__ soff,
+                 uint2* __restrict__ stage, uint64_t region) {
   // warp totals, double-buffered by chunk parity: one barrier per chunk
   __shared__ unsigned long long s_wt[2][kThreads / 32], s_ct[2][kThreads / 32];
+  extern __shared__ __align__(128) unsigned char stage_smem[];
+  StageTile* ring = reinterpret_cast<StageTile*>(stage_smem);
+  __shared__ __align__(8) uint64_t full[kStageNS], empty[kStageNS];
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kStageNS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kThreads / 32); }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // ---------------- producer
+      if (threadIdx.x != 0) return;
+      const uint64_t pol = l2_evict_first();
+      int hint = 0;
+      uint32_t f = 0;
+      for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++f) {
+        const int i = find_item(aitems, nitems, c, hint);
+        hint = i;
+        const Item it = aitems[i];
+        const uint64_t j = c - it.chunk0, n4 = it.n >> 2, q0 = j * kChunkQuads;
+        const uint32_t nq = q0 < n4 ? (uint32_t)min((uint64_t)kChunkQuads, n4 - q0) : 0u;
+        const uint32_t sl = f % kStageNS, use = f / kStageNS;
+        if (use) mbar_wait(&empty[sl], (use - 1) & 1u);
+        if (nq) {
+          mbar_expect_tx(&full[sl], nq * (EF ? 32u : 16u));
+          bulk_g2s(ring[sl].g, gbase + it.g_off + 4 * q0, nq * 16u, &full[sl], pol);
+          if (EF) bulk_g2s(ring[sl].r, rbase + it.r_off + 4 * q0, nq * 16u, &full[sl], pol);
+        } else {
+          mbar_arrive(&full[sl]);
+        }
+      }
+      return;
+    }
+  }
+  const int tid = TMA ? (int)threadIdx.x - 32 : (int)threadIdx.x;
   // this CTA's private staging region: entries are appended in chunk order, no atomics
   uint64_t pos = (uint64_t)blockIdx.x * region;
   const uint64_t region_end = pos + region;
   int par = 0;
   int hint = 0, cur = -1;
   uint32_t m = 0, t_lo = 0, t_hi = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t f = 0;
+  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++f) {
     const int i = find_item(aitems, nitems, c, hint);
     hint = i;
     if (i != cur) {
@@ -348,19 +394,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
     float* r = rbase + it.r_off;
     uint32_t kb[kQuadsPerThread][4];
     float4 gv[kQuadsPerThread], rv[kQuadsPerThread];
+    const uint32_t sl = f % kStageNS;
+    if constexpr (TMA) mbar_wait(&full[sl], (f / kStageNS) & 1u);
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
-      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + tid;
       if (q < n4) {
-        if constexpr (VEC) gv[u] = ld4_stream(g + 4 * q);
-        else gv[u] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
-        if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+        if constexpr (TMA) {
+          gv[u] = ring[sl].g[u * kThreads + tid];
+          if constexpr (EF) rv[u] = ring[sl].r[u * kThreads + tid];
+        } else {
+          if constexpr (VEC) gv[u] = ld4_stream(g + 4 * q);
+          else gv[u] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+          if constexpr (EF) rv[u] = ld4_stream(r + 4 * q);
+        }
       }
+    }
+    if constexpr (TMA) {   // the tile is in registers: hand the ring slot back to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
     }
     unsigned long long pw = 0, pc = 0;
 #pragma unroll
     for (int u = 0; u < kQuadsPerThread; ++u) {
-      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+      const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + tid;
       uint32_t wn = 0, cn = 0;
       if (q < n4) {
         float4 p = gv[u];
@@ -385,9 +442,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
       pc |= (unsigned long long)cn << (12 * u);
     }
     uint32_t tkb = 0, tw = 0, tcn = 0;
-    const bool has_tail = (j == n4 / kChunkQuads) && threadIdx.x < (it.n & 3);
+    const bool has_tail = (j == n4 / kChunkQuads) && tid < (it.n & 3);
     if (has_tail) {
-      const uint64_t e = n4 * 4 + threadIdx.x;
+      const uint64_t e = n4 * 4 + tid;
       const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
       if constexpr (EF) r[e] = p;
       tkb = __float_as_uint(p);
@@ -407,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
       if (lane >= o) { iw += a1; ic += a2; }
     }
     if (lane == 31) { s_wt[par][warp] = iw; s_ct[par][warp] = ic; }
-    __syncthreads();
+    if constexpr (TMA) consumers_sync(); else __syncthreads();
     unsigned long long ew = iw - pw, ec = ic - pc, totw = 0, totc = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
@@ -431,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
     const uint64_t base = pos;                      // identical in every thread of the CTA
     const bool fits = pos + staged <= region_end;
     if (fits) pos += staged;
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       counts[ti.status_off + j] = pack_wc(tileW, tileC);
       soff[ti.status_off + j] = base;
       if (!fits) atomicOr(&st[i].stage_ovf, 1u);   // this bucket goes to the exact fallback
@@ -440,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
       uint2* S = stage;
 #pragma unroll
       for (int u = 0; u < kQuadsPerThread; ++u) {
-        const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + threadIdx.x;
+        const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + tid;
         if (q < n4) {
           uint32_t w = baseW[u], cc = baseC[u];
 #pragma unroll
@@ -457,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_topk_stage(const Item* __restri
       }
       if (has_tail) {
         const uint32_t key = tkb & 0x7FFFFFFFu;
-        const uint32_t idx = (uint32_t)(n4 * 4 + threadIdx.x);
+        const uint32_t idx = (uint32_t)(n4 * 4 + tid);
         if (key > t_hi) S[base + baseW[kQuadsPerThread]] = make_uint2(idx, tkb);
         else if (key >= t_lo && !tie_mode) S[base + tileW + baseC[kQuadsPerThread]] = make_uint2(idx, tkb);
       }
@@ -1601,7 +1658,12 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   const TopkItem* ti = B.items + item0;
   TopkState* st = B.state + item0;
   uint32_t* anyf = B.ctrs + 2;
-  const unsigned ga = persistent_grid(L, a_chunks, (const void*)k_topk_stage<EF, VEC>, kThreads);
+  // the TMA stage kernel for 16-B aligned calls (NEBULA_OPT_TOPK_STAGE = 1, the default)
+  const bool tma = VEC && B.stage_tma;
+  const void* kst = tma ? (const void*)k_topk_stage<EF, VEC, true> : (const void*)k_topk_stage<EF, VEC, false>;
+  const size_t st_smem = tma ? sizeof(StageTile) * kStageNS : 0;
+  if (tma) ensure_smem_attr(kst, st_smem);
+  const unsigned ga = persistent_grid(L, a_chunks, kst, tma ? kThreads + 32 : kThreads, st_smem);
   // The fallback kernels run every step but exit at once unless a bracket failed (adversarial
   // inputs): one CTA per SM keeps those no-op launches at ~2 us instead of draining a full
   // occupancy grid each (measured 51 us per step for the eight of them at 8 CTAs / SM).
@@ -1624,8 +1686,13 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   }
   {
     Mark mk(L, PH_TOPK_A);
-    k_topk_stage<EF, VEC><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status, B.soff,
-                                                         B.stage, B.stage_entries / ga);
+    if (tma)
+      k_topk_stage<EF, VEC, true><<<ga, kThreads + 32, st_smem, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r,
+                                                                           B.status, B.soff, B.stage,
+                                                                           B.stage_entries / ga);
+    else
+      k_topk_stage<EF, VEC, false><<<ga, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, g, r, B.status,
+                                                                  B.soff, B.stage, B.stage_entries / ga);
   }
   {
     Mark mk(L, PH_TOPK_CLASSIFY);
@@ -1695,8 +1762,9 @@ void preload_topk() {
                         (const void*)k_topk_pass<false, true, true>, (const void*)k_topk_pass<false, true, false>,
                         (const void*)k_topk_pass<false, false, true>, (const void*)k_topk_pass<false, false, false>})
     touch_t(f);
-  touch_t((const void*)k_topk_stage<true, true>); touch_t((const void*)k_topk_stage<true, false>);
-  touch_t((const void*)k_topk_stage<false, true>); touch_t((const void*)k_topk_stage<false, false>);
+  touch_t((const void*)k_topk_stage<true, true, false>); touch_t((const void*)k_topk_stage<true, false, false>);
+  touch_t((const void*)k_topk_stage<false, true, false>); touch_t((const void*)k_topk_stage<false, false, false>);
+  touch_t((const void*)k_topk_stage<true, true, true>); touch_t((const void*)k_topk_stage<false, true, true>);
   touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan);
   touch_t((const void*)k_topk_wide_hist); touch_t((const void*)k_topk_wide_pick); touch_t((const void*)k_topk_wide_plan);
   touch_t((const void*)k_topk_wide_count); touch_t((const void*)k_topk_wide_scan);

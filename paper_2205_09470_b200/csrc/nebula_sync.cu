@@ -1337,7 +1337,9 @@ static bool step_pipelinable(const nebula_ctx* ctx, int32_t bucket, uint64_t ste
   if (ctx->P > 1 && ctx->xmode == 1) return false;
   const int m = method_at(ctx, step);
   if (m == M_TOPK && ctx->topk_reduce != 1) return false;
-  if (ctx->G > 1) return intra_p2p_on(ctx);
+  // G > 1 only when asked for (value 2): measured at 2 x 2 and 1 x 4 it was 1-9 % slower than
+  // one stream (profiles/r02/g_gt1_pipeline) — the halves' intra-cluster kernels contend
+  if (ctx->G > 1) return ctx->topk_pipe == 2 && intra_p2p_on(ctx);
   return m == M_TOPK;
 }
 
@@ -1549,8 +1551,13 @@ nebula_status nebula_set_option(nebula_ctx* ctx, int32_t option, int64_t value) 
     ctx->xmode = (value == 1 || !ctx->p2p_ok || ctx->P == 1) ? 1 : (value == 0 ? auto_xmode(ctx) : (int)value);
     return NEBULA_OK;
   }
+  if (option == NEBULA_OPT_TOPK_STAGE) {
+    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "top-k stage option must be 0 or 1");
+    ctx->tk.stage_tma = value == 1;
+    return NEBULA_OK;
+  }
   if (option == NEBULA_OPT_PIPELINE) {
-    if (value < 0 || value > 1) return fail(ctx, NEBULA_ERR_INVALID_ARG, "pipeline option must be 0 or 1");
+    if (value < 0 || value > 2) return fail(ctx, NEBULA_ERR_INVALID_ARG, "pipeline option must be in [0, 2]");
     ctx->topk_pipe = (int)value;
     return NEBULA_OK;
   }

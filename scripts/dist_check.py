@@ -56,7 +56,10 @@ def main():
     if G > 1:
         cases += [(O.TOPK, O.VAL_F32, None, "exact-topk", "p2p"), (O.TOPK, O.VAL_I8, None, "exact-topk", "nccl"),
                   (O.INT8, 0, None, True, "p2p"), (O.FP8, 0, None, True, "p2p"), (O.INT8, 0, None, False, "nccl"),
-                  (O.TOPK, O.VAL_F32, None, False, "nccl"), (O.INT8, 0, None, True, "nccl")]
+                  (O.TOPK, O.VAL_F32, None, False, "nccl"), (O.INT8, 0, None, True, "nccl"),
+                  # the two-stream ALL-bucket step over the P2P intra hop (NEBULA_OPT_PIPELINE = 2)
+                  (O.INT8, 0, "pipeline2", False, "p2p"), (O.TOPK, O.VAL_F32, "pipeline2", False, "p2p"),
+                  (O.FP16, 0, "pipeline2", False, "p2p")]
     intra_seen = set()
     modes_seen = set()
     modes = ((False, "pull"), (True, "pull"), (False, "push"), (True, "push"), (False, "nccl"))
@@ -70,7 +73,9 @@ def main():
             ctx = nb.init_process_group_context(sizes, gpus_per_cluster=G, device=local, method=method,
                                                 topk_values=vt, topk_density=0.05, exact_topk=xtopk)
             exact = exact is True
-            if kern:
+            if kern == "pipeline2":
+                ctx.set_option(nb.OPT_PIPELINE, 2)
+            elif kern:
                 ctx.set_int8_kernel(kern)
             if exact:
                 ctx.set_exact_scale(True)

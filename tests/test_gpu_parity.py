@@ -31,7 +31,8 @@ def bits(a):
 
 def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.01, k=0, ef=True,
                  start_step=0, per_bucket=False, misalign=False, mutate=None, int8_kernel=None,
-                 fp16_kernel=None, sr_seed=0, topk_reduce=None, step_config=None, topk_pipeline=None):
+                 fp16_kernel=None, sr_seed=0, topk_reduce=None, step_config=None, topk_pipeline=None,
+                 topk_stage=None):
     import torch
     ctx = nb.SyncContext(sizes, method, topk_values=vt, topk_density=rho, topk_k=k, error_feedback=ef,
                          start_step=start_step, num_clusters=P, transport=nb.LOOPBACK)
@@ -44,6 +45,8 @@ def run_loopback(nb, method, sizes, P, steps=3, kind="model-like", vt=0, rho=0.0
         ctx.set_fp16_kernel(fp16_kernel)
     if topk_pipeline is not None:                    # NEBULA_OPT_TOPK_PIPELINE
         ctx.set_option(nb.OPT_TOPK_PIPELINE, int(topk_pipeline))
+    if topk_stage is not None:                       # NEBULA_OPT_TOPK_STAGE (TMA ring or plain loads)
+        ctx.set_option(nb.OPT_TOPK_STAGE, int(topk_stage))
     if step_config is not None:                      # fused-step warp split (NEBULA_OPT_STEP_FUSION)
         ctx.set_option(nb.OPT_STEP_FUSION, 2 + step_config)
     if sr_seed:
@@ -335,6 +338,18 @@ def test_topk_two_stream_pipeline(nb, pipeline, sizes):
     counters and staging) and on one: both bit-exact vs the oracle, incl. odd bucket counts."""
     run_loopback(nb, O.TOPK, sizes, 2, rho=0.02, steps=3, topk_pipeline=pipeline)
     run_loopback(nb, O.TOPK, sizes, 3, vt=O.VAL_I8, rho=0.2, steps=2, topk_pipeline=pipeline)
+
+
+@pytest.mark.parametrize("stage", [0, 1])
+@pytest.mark.parametrize("ef", [True, False])
+@pytest.mark.parametrize("misalign", [False, True])
+def test_topk_stage_variants(nb, stage, ef, misalign):
+    """The stage pass with plain vector loads (0) and through the TMA ring (1, the default for
+    16-B aligned calls; misaligned calls take the scalar kernel): bit-exact vs the oracle over
+    buckets with ragged tails, a bucket shorter than one chunk and several chunks per CTA."""
+    sizes = [200003, 4096 * 3 + 5, 7, 1 << 20]
+    run_loopback(nb, O.TOPK, sizes, 2, rho=0.01, steps=3, ef=ef, misalign=misalign, topk_stage=stage)
+    run_loopback(nb, O.TOPK, sizes, 3, vt=O.VAL_F16, rho=0.3, steps=2, ef=ef, misalign=misalign, topk_stage=stage)
 
 
 @pytest.mark.parametrize("variant", [0, 1])
