@@ -196,6 +196,7 @@ struct TopkBuffers {
   uint64_t* host_mt0;   // host copy of items[].mt0 and merge tiles per item (for grid sizing)
   uint64_t* host_mtiles;
   uint64_t* host_sample_off;  // [nitems + 1] prefix of sample counts
+  uint64_t* host_ccap;        // [nitems] candidate capacities (no list longer than kWideMin: no wide resolve)
 };
 // Runs the whole selection for items [item0, item0 + nitems) (their TopkItem rows), writes
 // payloads, updates residuals.  aitems = the call's Item table (same order), g = gradient

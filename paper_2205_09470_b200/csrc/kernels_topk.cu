@@ -1707,7 +1707,11 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     Mark mk(L, PH_TOPK_RESOLVE);
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
-    // long candidate lists: multi-CTA radix select + compaction (no-ops for the others)
+    // long candidate lists: multi-CTA radix select + compaction (no-ops for the others; not
+    // launched at all when no item's candidate capacity exceeds kWideMin, e.g. rho = 1 %)
+    bool may_wide = false;
+    for (int x = 0; x < nitems; ++x) may_wide |= B.host_ccap[item0 + x] > kWideMin;
+    if (may_wide) {
     const unsigned gwide = (unsigned)L.num_sms * 8;
     uint32_t* wtotal = B.ctrs + 3;
     k_topk_wide_plan<<<1, kSelThreads, 0, L.stream>>>(ti, st, nitems, wtotal);
@@ -1718,6 +1722,8 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     k_topk_wide_count<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.status, wtotal);
     k_topk_wide_scan<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.status, B.pref);
     k_topk_wide_write<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.clist2, B.pref, wtotal);
+    *L.launches += 10;
+    }
   }
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
@@ -1739,7 +1745,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
                                                                                 B.wlist, B.clist, B.clist2, B.splits);
   k_topk_merge<EF><<<(unsigned)merge_tiles, kMergeThreads, 0, L.stream>>>(ti, st, nitems, tbase, B.wlist, B.clist, B.clist2, slots,
                                                                       r, flags, B.splits);
-  *L.launches += 28;
+  *L.launches += 19;
 }
 
 static void touch_t(const void* f) {

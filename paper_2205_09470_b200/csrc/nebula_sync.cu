@@ -143,6 +143,7 @@ struct nebula_ctx {
   std::vector<uint64_t> tk_mtiles;   // merge tiles per call type ([0] ALL, [1+b])
   std::vector<uint64_t> tk_host_mt0; // per item
   std::vector<uint64_t> tk_sample_off; // [items + 1]
+  std::vector<uint64_t> tk_ccap;       // per item candidate capacity
 
   ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
   uint64_t launches = 0;
@@ -1336,7 +1337,7 @@ static bool step_pipelinable(const nebula_ctx* ctx, int32_t bucket, uint64_t ste
   if (!ctx->topk_pipe || bucket != NEBULA_ALL_BUCKETS || ctx->b.size() < 2 || ctx->self) return false;
   if (ctx->P > 1 && ctx->xmode == 1) return false;
   const int m = method_at(ctx, step);
-  if (m == M_TOPK && ctx->topk_reduce != 1) return false;
+  if (m == M_TOPK && ctx->topk_reduce == 0) return false;   // variant 0's start offsets are shared
   // G > 1 only when asked for (value 2): measured at 2 x 2 and 1 x 4 it was 1-9 % slower than
   // one stream (profiles/r02/g_gt1_pipeline) — the halves' intra-cluster kernels contend
   if (ctx->G > 1) return ctx->topk_pipe == 2 && intra_p2p_on(ctx);

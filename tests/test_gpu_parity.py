@@ -141,23 +141,26 @@ def test_int8_near_half_integer_quotients(nb, int8_kernel):
 
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("per_bucket", [False, True])
-def test_int8_fused_step(nb, P, per_bucket):
+@pytest.mark.parametrize("ef", [True, False])
+def test_int8_fused_step(nb, P, per_bucket, ef):
     # the one-kernel INT8 step (compress + exchange + reduce): every P (both subtree
-    # schedules of the reduce warps), whole-group / ragged / tiny buckets, ALL and per bucket
-    run_loopback(nb, O.INT8, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003], P, steps=3, per_bucket=per_bucket,
-                 int8_kernel="fused-ws")
+    # schedules of the reduce warps), whole-group / ragged / tiny buckets, ALL and per bucket;
+    # without EF the max warps' ring tiles are twice as long (a slice of 2048 quads + 5 below)
+    run_loopback(nb, O.INT8, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003, 148 * 8192 + 20 + 3], P, steps=3,
+                 per_bucket=per_bucket, int8_kernel="fused-ws", ef=ef)
 
 
 @pytest.mark.parametrize("method", [O.INT8, O.FP8, O.QSGD, O.FP8_E5M2])
 @pytest.mark.parametrize("P", [2, 3, 5, 8])
 @pytest.mark.parametrize("per_bucket", [False, True])
-def test_pull_reducer_in_fused_step(nb, method, P, per_bucket):
+@pytest.mark.parametrize("ef", [True, False])
+def test_pull_reducer_in_fused_step(nb, method, P, per_bucket, ef):
     """The P2P-pull reduce role of the fused step (ws_reduce_ld: 16-B register loads of every
     cluster's payload, both tree-sum schedules: P <= 4 and the two-subtree P > 4 branch) runs
     here on one GPU: LOOPBACK with warp split 4 (the pull default), the peers' slots being the
     local slot buffer.  Bit-exact vs the oracle, ragged / tiny / multi-group buckets."""
     run_loopback(nb, method, [4096 * 37 + 5, 16, 3, 1 << 18, 1000003], P, steps=3, per_bucket=per_bucket,
-                 int8_kernel="fused-ws", step_config=4, sr_seed=7 if method == O.QSGD else 0)
+                 int8_kernel="fused-ws", step_config=4, sr_seed=7 if method == O.QSGD else 0, ef=ef)
 
 
 @pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
@@ -356,7 +359,7 @@ def test_topk_stage_variants(nb, stage, ef, misalign):
 @pytest.mark.parametrize("rho,P", [(0.01, 2), (0.3, 3), (0.001, 8)])
 @pytest.mark.parametrize("per_bucket,misalign", [(False, False), (True, True)])
 def test_topk_reduce_variants(nb, variant, rho, P, per_bucket, misalign):
-    """Both sparse decompress-average kernels (tile-interleaved default, per-warp ranges)."""
+    """Both sparse decompress-average kernels (tile-interleaved, per-warp ranges: the default)."""
     run_loopback(nb, O.TOPK, [300001, 2048, 4097, 1], P, rho=rho, steps=2, per_bucket=per_bucket,
                  misalign=misalign, topk_reduce=variant)
 
