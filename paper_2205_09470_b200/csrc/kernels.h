@@ -191,7 +191,7 @@ struct TopkBuffers {
   uint32_t bracket_smem_keys;  // shared-memory sample capacity of k_topk_bracket
   bool stage_tma = true;       // NEBULA_OPT_TOPK_STAGE: TMA-ring stage pass for 16-B aligned calls
   uint32_t* hist;       // [nitems][2048] fallback histograms
-  uint32_t* ctrs;       // 2 dynamic tile counters
+  uint32_t* ctrs;       // [2] any bracket failed, [3] wide-resolve units, [4] any exact-tie bracket
   uint32_t* start;      // sparse-reduce start offsets
   uint64_t* host_mt0;   // host copy of items[].mt0 and merge tiles per item (for grid sizing)
   uint64_t* host_mtiles;

@@ -164,7 +164,7 @@ __device__ uint32_t cta_select(GetKey get, uint32_t m, uint32_t rank, uint32_t* 
 __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st,
                                                               const uint32_t* __restrict__ sample,
-                                                              uint32_t smem_keys) {
+                                                              uint32_t smem_keys, uint32_t* any_tie) {
   extern __shared__ uint32_t s_keys[];   // the item's sample, loaded once for the 6 radix passes
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_bracket(const TopkItem* __
     S.t_hi = t_hi;
     S.mode = 0;
     S.path = 0;
+    if (t_lo == t_hi) atomicOr(any_tie, 1u);   // k_topk_write's tie pass has work
   }
 }
 
@@ -205,7 +206,7 @@ template <bool EF>
 __global__ void k_topk_sample(const Item* __restrict__ aitems, const TopkItem* __restrict__ titems, int nitems,
                               uint64_t sbase, uint64_t total, const float* __restrict__ gbase,
                               const float* __restrict__ rbase, uint32_t* __restrict__ sample, uint32_t* ctrs) {
-  if (blockIdx.x == 0 && threadIdx.x < 4) ctrs[threadIdx.x] = 0;   // [2] = any bracket failed
+  if (blockIdx.x == 0 && threadIdx.x < 8) ctrs[threadIdx.x] = 0;   // [2] any bracket failed, [3] wide units, [4] any exact-tie bracket
   const uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= total) return;
   const uint64_t a = sbase + gi;
@@ -616,7 +617,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
                                                          const uint32_t* any_failed) {
   // retry == 1: fallback buckets (both lists); retry == 2: exact-tie buckets of the first
   // pass (ties only, winners were staged)
-  if (retry == 1 && *((volatile const uint32_t*)any_failed) == 0) return;
+  // any_failed: retry 1 -> "some bracket failed", retry 2 -> "some bracket is an exact tie"
+  if (*((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long s_wt[kThreads / 32], s_ct[kThreads / 32];
   int hint = 0;
   for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
@@ -1682,7 +1684,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     k_topk_sample<EF><<<(unsigned)((scount + 255) / 256 ? (scount + 255) / 256 : 1), 256, 0, L.stream>>>(
         aitems, ti, nitems, sbase, scount, g, r, B.sample, B.ctrs);
     k_topk_bracket<<<nitems, kSelThreads, (size_t)B.bracket_smem_keys * 4, L.stream>>>(ti, st, B.sample,
-                                                                                      B.bracket_smem_keys);
+                                                                                      B.bracket_smem_keys, B.ctrs + 4);
   }
   {
     Mark mk(L, PH_TOPK_A);
@@ -1702,7 +1704,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
                                                                              B.wlist, B.clist);
     // exact-tie buckets: their first need_T ties in index order, at the scanned offsets
     k_topk_write<VEC><<<gw, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g, B.wlist, B.clist,
-                                                     B.pref, 2, anyf);
+                                                     B.pref, 2, B.ctrs + 4);
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);

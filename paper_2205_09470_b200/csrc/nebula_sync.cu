@@ -1105,7 +1105,7 @@ static nebula_status compress_t(nebula_ctx* ctx, int t, const float* dev_grad, u
       const int item0 = lo * ctx->Ploc;
       TopkBuffers tkb = ctx->tk;
       if (t == (int)ctx->b.size() + 2) {   // second half of a pipelined step: own counters / staging
-        tkb.ctrs = ctx->tk.ctrs + 4;
+        tkb.ctrs = ctx->tk.ctrs + 8;
         tkb.stage = ctx->tk_stage2;
       }
       launch_topk(L, ef, vec, tkb, item0, T.count, T.chunks, items, gbase, ctx->d_resid, dst,
