@@ -257,8 +257,8 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   3 P2P pull: compress writes locally, the decompress-reduce kernel loads each peer's slot
  *   directly from the peer over NVLink.  In 2 and 3 the exchange is a per-bucket flag
  *   handshake (release/acquire at system scope) and slots are double-buffered by step parity.
- *   Auto (every rank can map every peer, decided collectively at init): 2 for P = 2, 3 for
- *   P > 2; else 1.
+ *   Auto (every rank can map every peer, decided collectively at init): 2 for TOPK and, at
+ *   P = 2, for IDENTITY / INT8 / FP8; 3 otherwise (P > 2, and FP16 / QSGD at P = 2); else 1.
  *   Only between steps. */
 #define NEBULA_OPT_EXCHANGE 2
 /*   NEBULA_OPT_FP16_KERNEL: 0 (default) TMA-ring streaming kernel for 16-B aligned calls,

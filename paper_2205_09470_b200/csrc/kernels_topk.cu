@@ -744,7 +744,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_write(const Item* __restrict_
 // ---------------------------------------------------------------- D: resolve among candidates
 __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __restrict__ titems,
                                                               TopkState* __restrict__ st, uint2* __restrict__ cl,
-                                                              int retry, uint32_t* any_failed) {
+                                                              int retry, uint32_t* any_failed,
+                                                              uint32_t wide_min = kWideMin) {
   if (retry && *((volatile uint32_t*)any_failed) == 0) return;
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t misc[4];
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_resolve(const TopkItem* __
   uint2* cand = cl + ti.list_off;
   const uint32_t m = (uint32_t)(C < ti.ccap ? C : ti.ccap);
   uint32_t T, above_c = 0;
-  if (!retry && S.t_lo != S.t_hi && m > kWideMin) {
+  if (!retry && S.t_lo != S.t_hi && m > wide_min) {
     // long candidate list (a huge bucket, or a large k): the multi-CTA radix select and
     // compaction below (k_topk_wide_*) — one CTA would walk millions of entries
     if (threadIdx.x == 0) {
@@ -1708,11 +1709,12 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
-    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf);
+    static const uint32_t wide_min = [] { const char* e = getenv("NEBULA_EXPERIMENT_WIDE_MIN"); return e ? (uint32_t)atoi(e) : kWideMin; }();
+    k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf, wide_min);
     // long candidate lists: multi-CTA radix select + compaction (no-ops for the others; not
     // launched at all when no item's candidate capacity exceeds kWideMin, e.g. rho = 1 %)
     bool may_wide = false;
-    for (int x = 0; x < nitems; ++x) may_wide |= B.host_ccap[item0 + x] > kWideMin;
+    for (int x = 0; x < nitems; ++x) may_wide |= B.host_ccap[item0 + x] > wide_min;
     if (may_wide) {
     const unsigned gwide = (unsigned)L.num_sms * 8;
     uint32_t* wtotal = B.ctrs + 3;

@@ -635,8 +635,14 @@ static nebula_status self_resolve(nebula_ctx* ctx) {
 // feeds P - 1 peers, and the fused step overlaps them with the compress) but push for TOPK (its
 // payload is small and the sparse reducer's scattered window loads would each pay the NVLink
 // latency: 0.90 ms at P = 4 pulling, r02).
+// Measured at N = 2 / 4 (profiles/r02/p2_policy, bench_n4f_*): top-k pushes (its payloads are
+// written once, the pull reducer's window loads each paid the NVLink latency); at P = 2 INT8 /
+// FP8 push and pull tie (1.145 / 1.13 ms) and push is kept, while FP16 and QSGD gain from the
+// fused step over pull (FP16 1.61 -> 1.28 ms, QSGD 1.53 -> 1.40 ms); P > 2 pulls.
 static int auto_xmode(const nebula_ctx* ctx) {
-  if (ctx->P == 2 || ctx->codec.method == NEBULA_TOPK) return 2;
+  const int m = ctx->codec.method;
+  if (m == NEBULA_TOPK) return 2;
+  if (ctx->P == 2 && m != NEBULA_FP16 && m != NEBULA_QSGD) return 2;
   return 3;
 }
 
