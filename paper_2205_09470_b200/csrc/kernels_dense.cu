@@ -256,10 +256,10 @@ __global__ void __launch_bounds__(kThreads) k_int8_quant(const Item* __restrict_
           d2 = __fmul_rn(fp8_val<FP8>(wv >> 16), s); d3 = __fmul_rn(fp8_val<FP8>(wv >> 24), s);
         } else if constexpr (SR) {
           const uint64_t h0 = qsgd_h(srb, 2 * q), h1 = qsgd_h(srb, 2 * q + 1);   // elements 4q .. 4q+3
-          int q0 = qsgd_q(p.x, s, qsgd_hi(h0)), q1 = qsgd_q(p.y, s, qsgd_lo(h0)),
-              q2 = qsgd_q(p.z, s, qsgd_hi(h1)), q3 = qsgd_q(p.w, s, qsgd_lo(h1));
-          wv = pack_i8x4(q0, q1, q2, q3);
-          d0 = __fmul_rn((float)q0, s); d1 = __fmul_rn((float)q1, s); d2 = __fmul_rn((float)q2, s); d3 = __fmul_rn((float)q3, s);
+          const float q0 = qsgd_qf(p.x, s, sinv, qsgd_hi_f(h0)), q1 = qsgd_qf(p.y, s, sinv, qsgd_lo_f(h0)),
+                      q2 = qsgd_qf(p.z, s, sinv, qsgd_hi_f(h1)), q3 = qsgd_qf(p.w, s, sinv, qsgd_lo_f(h1));
+          wv = byte_of_intf(q0) | (byte_of_intf(q1) << 8) | (byte_of_intf(q2) << 16) | (byte_of_intf(q3) << 24);
+          d0 = __fmul_rn(q0, s); d1 = __fmul_rn(q1, s); d2 = __fmul_rn(q2, s); d3 = __fmul_rn(q3, s);
         } else {
           int q0 = int8_qi(p.x, s, sinv), q1 = int8_qi(p.y, s, sinv), q2 = int8_qi(p.z, s, sinv), q3 = int8_qi(p.w, s, sinv);
           wv = pack_i8x4(q0, q1, q2, q3);
@@ -454,14 +454,18 @@ int occupancy_per_sm(const void* kernel, int threads, size_t smem) {
 }
 
 void ensure_smem_attr(const void* kernel, size_t bytes) {
+  // the attribute is an upper bound: keep the largest value set per (device, kernel) — setting a
+  // smaller one for a later call would break the earlier size (e.g. the bracket kernel's
+  // sample capacity differs between contexts)
   static std::mutex mu;
-  static std::set<std::tuple<int, const void*, size_t>> done;
+  static std::map<std::pair<int, const void*>, size_t> done;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  if (done.count({dev, kernel, bytes})) return;
+  auto it = done.find({dev, kernel});
+  if (it != done.end() && it->second >= bytes) return;
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess)
-    done.insert({dev, kernel, bytes});
+    done[{dev, kernel}] = bytes;
 }
 
 static void touch(const void* f) {

@@ -1709,7 +1709,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
-    static const uint32_t wide_min = [] { const char* e = getenv("NEBULA_EXPERIMENT_WIDE_MIN"); return e ? (uint32_t)atoi(e) : kWideMin; }();
+    const uint32_t wide_min = kWideMin;   // 32768 / 8192 measured the same at config 2
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf, wide_min);
     // long candidate lists: multi-CTA radix select + compaction (no-ops for the others; not
     // launched at all when no item's candidate capacity exceeds kWideMin, e.g. rho = 1 %)
@@ -1789,9 +1789,7 @@ void preload_topk() {
   touch_densify<5>(); touch_densify<6>(); touch_densify<7>(); touch_densify<8>();
 }
 
-void topk_prepare_bracket(uint32_t keys) {
-  cudaFuncSetAttribute(k_topk_bracket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(keys * 4));
-}
+void topk_prepare_bracket(uint32_t keys) { ensure_smem_attr((const void*)k_topk_bracket, (size_t)keys * 4); }
 
 void launch_topk(const Launch& L, bool ef, bool vec, const TopkBuffers& B, int item0, int nitems, uint64_t a_chunks,
                  const Item* aitems, const float* g, float* r, const Dests& slots, uint32_t* flags, int value_type,

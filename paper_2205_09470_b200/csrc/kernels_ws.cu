@@ -565,11 +565,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
               d2 = __fmul_rn(fp8_val<F8>(w >> 16), s); d3 = __fmul_rn(fp8_val<F8>(w >> 24), s);
             } else if constexpr (SR) {
               const uint64_t h0 = qsgd_h(srb, 2 * (q0 + j)), h1 = qsgd_h(srb, 2 * (q0 + j) + 1);
-              const int a0 = qsgd_q(p.x, s, qsgd_hi(h0)), a1 = qsgd_q(p.y, s, qsgd_lo(h0)),
-                        a2 = qsgd_q(p.z, s, qsgd_hi(h1)), a3 = qsgd_q(p.w, s, qsgd_lo(h1));
-              w = pack_i8x4(a0, a1, a2, a3);
-              d0 = __fmul_rn((float)a0, s); d1 = __fmul_rn((float)a1, s);
-              d2 = __fmul_rn((float)a2, s); d3 = __fmul_rn((float)a3, s);
+              const float a0 = qsgd_qf(p.x, s, sinv, qsgd_hi_f(h0)), a1 = qsgd_qf(p.y, s, sinv, qsgd_lo_f(h0)),
+                          a2 = qsgd_qf(p.z, s, sinv, qsgd_hi_f(h1)), a3 = qsgd_qf(p.w, s, sinv, qsgd_lo_f(h1));
+              w = byte_of_intf(a0) | (byte_of_intf(a1) << 8) | (byte_of_intf(a2) << 16) | (byte_of_intf(a3) << 24);
+              d0 = __fmul_rn(a0, s); d1 = __fmul_rn(a1, s);
+              d2 = __fmul_rn(a2, s); d3 = __fmul_rn(a3, s);
             } else {
               const int a0 = int8_qi(p.x, s, sinv), a1 = int8_qi(p.y, s, sinv), a2 = int8_qi(p.z, s, sinv),
                         a3 = int8_qi(p.w, s, sinv);

@@ -238,6 +238,48 @@ __device__ __forceinline__ int qsgd_q(float p, float s, float u) {
   const float q = __fadd_rn(f, u < __fsub_rn(x, f) ? 1.0f : 0.0f);
   return max(-127, min(127, (int)q));
 }
+
+// ---- the same quantiser without the SFU / conversion unit (the fused QSGD step was bound by
+// its ~5 XU operations per element: reciprocal, floor, float<->int conversions).  Same bits.
+//
+// x = fl(p / s): q1 = q0 + fl(p - q0 s)·inv with q0 = fl(p·inv), inv = fl(1/s), accepted when
+// |p - q1·s| < ulp(q1)/2 · s — then q1 IS the correctly rounded quotient (a quotient of two
+// binary32 numbers never lies on a rounding midpoint; the FMA residuals are exact for a q
+// within one ulp of p/s and no underflow, guarded by |p| >= 2^-90).  q1 a power of two (its
+// rounding interval is asymmetric), a failed check, or inv == 0: the IEEE division.
+__device__ __forceinline__ float div_rn_fma(float p, float s, float inv) {
+  if (p == 0.0f) return p;                       // fl(+-0 / s) = +-0 for s > 0
+  if (inv != 0.0f && fabsf(p) >= 8.077935669463161e-28f) {   // 2^-90
+    const float q0 = __fmul_rn(p, inv);
+    const float q1 = __fmaf_rn(__fmaf_rn(-q0, s, p), inv, q0);
+    const uint32_t b = __float_as_uint(q1), e = b & 0x7F800000u;
+    if (e >= (25u << 23) && e < 0x7F800000u && (b & 0x7FFFFFu) != 0u) {
+      const float r1 = __fmaf_rn(-q1, s, p);
+      if (fabsf(r1) < __fmul_rn(__uint_as_float(e - (24u << 23)), s)) return q1;
+    }
+  }
+  return __fdiv_rn(p, s);
+}
+// m * 2^-24 for a 24-bit m, exactly, with integer / FMA-pipe operations only
+__device__ __forceinline__ float u24_to_unit(uint32_t m) {
+  return __fadd_rn(__fsub_rn(__uint_as_float(0x3F800000u | (m >> 1)), 1.0f), (m & 1u) ? 5.9604644775390625e-8f : 0.0f);
+}
+__device__ __forceinline__ float qsgd_hi_f(uint64_t h) { return u24_to_unit((uint32_t)(h >> 40)); }
+__device__ __forceinline__ float qsgd_lo_f(uint64_t h) { return u24_to_unit((uint32_t)((h >> 16) & 0xFFFFFFu)); }
+// the QSGD code as an integer-valued float in [-127, 127] (|x| <= 128: floor by the 1.5 * 2^23
+// round-to-integer trick, exact for |x| < 2^22)
+__device__ __forceinline__ float qsgd_qf(float p, float s, float inv, float u) {
+  const float x = div_rn_fma(p, s, inv);
+  const float rn = __fsub_rn(__fadd_rn(x, 12582912.0f), 12582912.0f);
+  const float f = rn > x ? __fsub_rn(rn, 1.0f) : rn;
+  const float q = __fadd_rn(f, u < __fsub_rn(x, f) ? 1.0f : 0.0f);
+  return fminf(fmaxf(q, -127.0f), 127.0f);
+}
+// low byte of an integer-valued float in [-128, 127] (two's complement), no conversion unit
+__device__ __forceinline__ uint32_t byte_of_intf(float q) {
+  return (uint32_t)(__float_as_int(__fadd_rn(q, 12582912.0f)) - 0x4B400000) & 0xFFu;
+}
+
 // What the QSGD quantiser needs besides p and s: the generator state of this call.
 struct SrArgs {
   uint64_t seed, step;
