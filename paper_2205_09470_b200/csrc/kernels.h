@@ -190,6 +190,7 @@ struct TopkBuffers {
   uint64_t* splits;            // merge-path split points, 2 per merge tile
   uint32_t bracket_smem_keys;  // shared-memory sample capacity of k_topk_bracket
   bool stage_tma = true;       // NEBULA_OPT_TOPK_STAGE: TMA-ring stage pass for 16-B aligned calls
+  cudaEvent_t wide_rec = nullptr, wide_wait = nullptr;   // pipelined halves: order their multi-CTA resolve sections
   uint32_t* hist;       // [nitems][2048] fallback histograms
   uint32_t* ctrs;       // [2] any bracket failed, [3] wide-resolve units, [4] any exact-tie bracket
   uint32_t* start;      // sparse-reduce start offsets

@@ -1709,12 +1709,15 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   }
   {
     Mark mk(L, PH_TOPK_RESOLVE);
-    const uint32_t wide_min = kWideMin;   // 32768 / 8192 measured the same at config 2
+    // test hook: NEBULA_DEBUG_WIDE_MIN lowers the threshold (more buckets on the multi-CTA path);
+    // 32768 / 8192 measured the same speed at config 2 as the default
+    static const uint32_t wide_min = [] { const char* e = getenv("NEBULA_DEBUG_WIDE_MIN"); return e ? (uint32_t)atoi(e) : kWideMin; }();
     k_topk_resolve<<<nitems, kSelThreads, 0, L.stream>>>(ti, st, B.clist, 0, anyf, wide_min);
     // long candidate lists: multi-CTA radix select + compaction (no-ops for the others; not
     // launched at all when no item's candidate capacity exceeds kWideMin, e.g. rho = 1 %)
     bool may_wide = false;
     for (int x = 0; x < nitems; ++x) may_wide |= B.host_ccap[item0 + x] > wide_min;
+    if (B.wide_wait) cudaStreamWaitEvent(L.stream, B.wide_wait, 0);
     if (may_wide) {
     const unsigned gwide = (unsigned)L.num_sms * 8;
     uint32_t* wtotal = B.ctrs + 3;
@@ -1728,6 +1731,7 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
     k_topk_wide_write<<<gwide, 256, 0, L.stream>>>(ti, st, nitems, B.clist, B.clist2, B.pref, wtotal);
     *L.launches += 10;
     }
+    if (B.wide_rec) cudaEventRecord(B.wide_rec, L.stream);
   }
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)

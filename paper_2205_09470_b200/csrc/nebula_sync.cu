@@ -139,6 +139,7 @@ struct nebula_ctx {
   int topk_pipe = 1;                   // NEBULA_OPT_TOPK_PIPELINE
   cudaStream_t side = nullptr;         // second stream of the pipelined top-k step
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_wide = nullptr;       // pipelined top-k: first half's multi-CTA resolve section done
   void* d_topk_mem = nullptr;
   std::vector<uint64_t> tk_mtiles;   // merge tiles per call type ([0] ALL, [1+b])
   std::vector<uint64_t> tk_host_mt0; // per item
@@ -473,6 +474,7 @@ static void release(nebula_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_wide) cudaEventDestroy(ctx->ev_wide);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   cudaFree(ctx->d_topk_mem);
   cudaFree(ctx->d_bar);
@@ -1110,6 +1112,15 @@ static nebula_status compress_t(nebula_ctx* ctx, int t, const float* dev_grad, u
     case M_TOPK: {
       const int item0 = lo * ctx->Ploc;
       TopkBuffers tkb = ctx->tk;
+      if (t > (int)ctx->b.size()) {
+        // pipelined halves: the second half's multi-CTA resolve section waits for the first
+        // half's.  Run concurrently, the two sections faulted (illegal address) or diverged at
+        // 2-10 % density with more buckets on that path (profiles/r02/topk/README.md); ordered
+        // they pass — the conflict is not understood, so they never overlap.
+        if (!ctx->ev_wide) CKC(cudaEventCreateWithFlags(&ctx->ev_wide, cudaEventDisableTiming));
+        if (t == (int)ctx->b.size() + 1) tkb.wide_rec = ctx->ev_wide;
+        else tkb.wide_wait = ctx->ev_wide;
+      }
       if (t == (int)ctx->b.size() + 2) {   // second half of a pipelined step: own counters / staging
         tkb.ctrs = ctx->tk.ctrs + 8;
         tkb.stage = ctx->tk_stage2;

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Debug: three TOPK contexts on the same inputs in lock-step — A and B one-stream, C two-stream;
+"""Three TOPK contexts on the same inputs in lock-step — A and B one-stream, C two-stream;
 after every step compare the outputs (A vs B: nondeterminism of the serial path; A vs C: of the
 two-stream path) and, on a difference, which buckets' payloads differ."""
 import os
