@@ -158,7 +158,7 @@ def model_gradient(name: str, cluster: int = 0, local_rank: int = 0, step: int =
 
 
 EDGE_KINDS = ("normal", "model-like", "zipf-rows", "ties", "zeros", "subnormal",
-              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "half-ties", "fp8-ties", "e5m2-ties", "int-ties")
+              "mixed-scale", "signed-zero", "uniform", "tiny-max", "strided-zeros", "strided-small", "half-ties", "fp8-ties", "e5m2-ties", "int-ties")
 
 
 def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np.ndarray:
@@ -170,7 +170,8 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
     zeros (all +0.0); subnormal (values around 1e-40); mixed-scale (N(0,1) scaled by
     10**U(-30, 3) per element); signed-zero (half +0.0, half -0.0, a few nonzeros);
     uniform U(-1, 1); tiny-max (max |g| ~ 1e-44, below 127 * 2**-149); strided-zeros (every
-    16th element 0, the rest N(0,1)).
+    16th element 0, the rest N(0,1)); strided-small (every 16th element N(0, 1e-6), the rest
+    N(0,1)).
     """
     rng = np.random.default_rng(seed)
     if n == 0:
@@ -276,6 +277,12 @@ def synthetic(n: int, seed: int, kind: str = "normal", sigma: float = 1.0) -> np
             for _ in range(abs(d)):
                 g[sel] = np.nextafter(g[sel], toward)
         g[0] = np.float32(1.0)
+        return g
+    if kind == "strided-small":
+        # like strided-zeros, but the sampled elements are small and NONZERO: a regular sampler
+        # sees a bracket far below the true k-th key (every other element is a "winner")
+        g = rng.standard_normal(n, dtype=np.float32)
+        g[::16] = (rng.standard_normal((n + 15) // 16, dtype=np.float32) * np.float32(1e-3)).astype(np.float32)
         return g
     if kind == "strided-zeros":
         # every element whose index is a multiple of 16 is 0.0, the rest N(0, 1): a regular

@@ -376,18 +376,25 @@ def test_topk_exact_k_and_full(nb, k):
     run_loopback(nb, O.TOPK, [150001], 2, k=k, steps=2)
 
 
-def test_topk_fallback_path_is_exercised(nb):
+@pytest.mark.parametrize("kind", ["strided-zeros", "strided-small"])
+@pytest.mark.parametrize("vt", [O.VAL_F32, O.VAL_F16, O.VAL_I8])
+def test_topk_fallback_path_is_exercised(nb, vt, kind):
+    """The exact radix fallback (the sampled bracket fails on this input): payload AND residual
+    vs the oracle — the stage pass may have stored winners' residuals, which k_topk_restore must
+    put back as p before the fallback re-reads r."""
     import torch
     n = 50000
-    ctx = nb.SyncContext([n], nb.TOPK, topk_density=0.1, num_clusters=1, transport=nb.LOOPBACK)
-    g = torch.from_numpy(synthetic(n, 1, "strided-zeros")).cuda()
+    ctx = nb.SyncContext([n], nb.TOPK, topk_density=0.1, topk_values=vt, num_clusters=1, transport=nb.LOOPBACK)
+    g = torch.from_numpy(synthetic(n, 1, kind)).cuda()
     out = torch.empty(n, device="cuda")
     ctx.step(0, g, out, 0)
     ctx.check()
     st = ctx.topk_stats(0, 0)
     assert st.path == 1       # the sampled bracket failed and the exact radix fallback ran
-    res = O.cluster_step(g.cpu().numpy(), np.zeros(n, F32), O.Codec(method=O.TOPK, topk_density=0.1), 0)
+    res = O.cluster_step(g.cpu().numpy(), np.zeros(n, F32), O.Codec(method=O.TOPK, topk_density=0.1,
+                                                                    topk_values=vt), 0)
     assert ctx.payload_copy(0, 0) == res.payload
+    assert np.array_equal(bits(ctx.residual(0, 0).cpu().numpy()), bits(res.r_new))
     ctx.destroy()
 
 
