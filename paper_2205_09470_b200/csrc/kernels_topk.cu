@@ -308,21 +308,6 @@ __global__ void __launch_bounds__(kThreads) k_topk_pass(const Item* __restrict__
   }
 }
 
-// Winners' residuals in the stage pass (f32 / f16 values with EF): a winner (key > t_hi) is
-// selected for sure, and its residual p - D(p) needs no bucket statistic (f32: D = p, so +0;
-// f16: D = RNE16(p)), so the stage pass stores it directly instead of parking p — the merge
-// then writes residuals only for the selected candidates (at rho = 10 % the winners' scattered
-// residual writes were a read-modify-write of nearly every residual sector).  Only with t_lo > 0
-// (a stored 0 can then never look like a candidate or a tie to the passes that re-read p from
-// r), only for chunks whose winners were staged (their p can be restored from the staging area
-// if the bucket falls back to the exact path: k_topk_restore).
-__device__ __forceinline__ bool winners_in_stage(int vt, uint32_t t_lo) {
-  return (vt == V_F32 || vt == V_F16) && t_lo > 0u;
-}
-__device__ __forceinline__ float winner_residual(float p, int vt) {
-  return vt == V_F32 ? 0.0f : __fsub_rn(p, __half2float(__float2half_rn(p)));
-}
-
 // ---------------------------------------------------------------- A: EF pass + classify + stage
 // TMA = false: plain vector loads, kThreads threads, 3 CTAs / SM.  TMA = true (16-B aligned
 // calls): one producer warp bulk-loads each chunk's g and r tiles into a kStageNS-deep
@@ -437,9 +422,11 @@ __global__ void __launch_bounds__(TMA ? kThreads + 32 : kThreads, TMA ? 2 : 3)
       uint32_t wn = 0, cn = 0;
       if (q < n4) {
         float4 p = gv[u];
-        if constexpr (EF)   // p -> r is stored after the chunk's staging decision (below)
+        if constexpr (EF) {
           p = make_float4(__fadd_rn(p.x, rv[u].x), __fadd_rn(p.y, rv[u].y), __fadd_rn(p.z, rv[u].z),
                           __fadd_rn(p.w, rv[u].w));
+          st4(r + 4 * q, p);
+        }
         kb[u][0] = __float_as_uint(p.x); kb[u][1] = __float_as_uint(p.y);
         kb[u][2] = __float_as_uint(p.z); kb[u][3] = __float_as_uint(p.w);
 #pragma unroll
@@ -460,6 +447,7 @@ __global__ void __launch_bounds__(TMA ? kThreads + 32 : kThreads, TMA ? 2 : 3)
     if (has_tail) {
       const uint64_t e = n4 * 4 + tid;
       const float p = EF ? __fadd_rn(g[e], r[e]) : g[e];
+      if constexpr (EF) r[e] = p;
       tkb = __float_as_uint(p);
       const uint32_t key = tkb & 0x7FFFFFFFu;
       m = max(m, key);
@@ -503,29 +491,8 @@ __global__ void __launch_bounds__(TMA ? kThreads + 32 : kThreads, TMA ? 2 : 3)
     if (fits) pos += staged;
     if (tid == 0) {
       counts[ti.status_off + j] = pack_wc(tileW, tileC);
-      soff[ti.status_off + j] = fits ? base : ~0ull;   // ~0: nothing staged (k_topk_restore skips it)
+      soff[ti.status_off + j] = base;
       if (!fits) atomicOr(&st[i].stage_ovf, 1u);   // this bucket goes to the exact fallback
-    }
-    if constexpr (EF) {   // p -> r; a staged winner's final residual instead (winners_in_stage)
-      const int vt = (int)ti.value_type;
-      const bool wis = fits && winners_in_stage(vt, t_lo);
-#pragma unroll
-      for (int u = 0; u < kQuadsPerThread; ++u) {
-        const uint64_t q = j * kChunkQuads + (uint64_t)u * kThreads + tid;
-        if (q < n4) {
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float pe = __uint_as_float(kb[u][e]);
-            v[e] = (wis && (kb[u][e] & 0x7FFFFFFFu) > t_hi) ? winner_residual(pe, vt) : pe;
-          }
-          st4(r + 4 * q, make_float4(v[0], v[1], v[2], v[3]));
-        }
-      }
-      if (has_tail) {
-        const float pe = __uint_as_float(tkb);
-        r[n4 * 4 + tid] = (wis && (tkb & 0x7FFFFFFFu) > t_hi) ? winner_residual(pe, vt) : pe;
-      }
     }
     if (staged && fits) {
       uint2* S = stage;
@@ -606,7 +573,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __res
                                                            const unsigned long long* __restrict__ tiles,
                                                            unsigned long long* __restrict__ pref, int retry,
                                                            uint32_t* flags, int value_type,
-                                                           uint32_t* any_failed) {
+                                                           const uint32_t* any_failed) {
   if (retry && *((volatile const uint32_t*)any_failed) == 0) return;
   __shared__ unsigned long long scan[32];
   const TopkItem ti = titems[blockIdx.x];
@@ -616,8 +583,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __res
   } else {
     const uint32_t mb = S.maxbits;
     if (nonfinite_bits(mb)) {
-      // any_failed also wakes k_topk_restore (the stage pass may have stored winners' residuals)
-      if (threadIdx.x == 0) { S.failed = 2; atomicOr(flags, kFlagNonfinite); atomicOr(any_failed, 1u); }
+      if (threadIdx.x == 0) { S.failed = 2; atomicOr(flags, kFlagNonfinite); }
       return;
     }
     if (threadIdx.x == 0) S.scale = value_type == V_I8 ? int8_scale_from_bits(mb) : 1.0f;
@@ -636,37 +602,6 @@ __global__ void __launch_bounds__(kSelThreads) k_topk_scan(const TopkItem* __res
   if (threadIdx.x == 0) {
     S.wcount = carry >> 32;
     S.ccount = carry & 0xFFFFFFFFull;
-  }
-}
-
-// ---------------------------------------------------------------- R: restore parked p
-// A bucket that leaves the normal path (bracket failed, staging overflow, non-finite) needs p
-// in r at every position: put back the p of the winners whose residual the stage pass stored
-// (winners_in_stage), from the staging area (each staged chunk's first W entries).
-__global__ void __launch_bounds__(kThreads) k_topk_restore(const Item* __restrict__ aitems,
-                                                           const TopkItem* __restrict__ titems,
-                                                           const TopkState* __restrict__ st, int nitems,
-                                                           uint64_t chunks, const unsigned long long* __restrict__ counts,
-                                                           const unsigned long long* __restrict__ soff,
-                                                           const uint2* __restrict__ stage, float* __restrict__ rbase,
-                                                           const uint32_t* any_failed) {
-  if (*((volatile const uint32_t*)any_failed) == 0) return;
-  int hint = 0;
-  for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
-    const int i = find_item(aitems, nitems, c, hint);
-    hint = i;
-    const TopkState& S = st[i];
-    const TopkItem& ti = titems[i];
-    if (S.failed == 0 || !winners_in_stage((int)ti.value_type, S.t_lo)) continue;
-    const uint64_t j = c - aitems[i].chunk0;
-    const unsigned long long so = soff[ti.status_off + j];
-    if (so == ~0ull) continue;
-    const uint32_t W = (uint32_t)(counts[ti.status_off + j] >> 32);
-    float* r = rbase + ti.r_off;
-    for (uint32_t x = threadIdx.x; x < W; x += blockDim.x) {
-      const uint2 e = stage[so + x];
-      r[e.x] = __uint_as_float(e.y);
-    }
   }
 }
 
@@ -1260,7 +1195,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __
                                                            Dests dst, float* __restrict__ rbase, uint32_t* flags,
                                                            const uint64_t* __restrict__ splits) {
   __shared__ uint2 sab[kMergeTile], so[kMergeTile];   // sab: the A range, then the B range (na + nb = nout)
-  __shared__ uint8_t s_from_a[kMergeTile];             // output came from the winner list
   __shared__ uint64_t s_split[2];
   const uint64_t t = tbase + blockIdx.x;
   int i = 0;
@@ -1312,7 +1246,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __
         if (diag + v < nout) {
           const bool takeA = ib >= nbb || (ia < na && sa[ia].x < sb[ib].x);
           so[diag + v] = takeA ? sa[ia] : sb[ib];
-          s_from_a[diag + v] = takeA;
           ia += takeA;
           ib += !takeA;
         }
@@ -1326,8 +1259,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __
   if (d0 == 0 && threadIdx.x == 0) put_preamble(dst, so_off, M_TOPK, (uint32_t)k, s, (uint32_t)vt);
   const uint64_t io = so_off + 16, vo = so_off + 16 + pad16(4 * k);   // idx / value section offsets
   float* r = rbase + ti.r_off;
-  // the normal path's winners already hold their residual (stored by the stage pass)
-  const bool skip_a = S.failed == 0 && winners_in_stage(vt, S.t_lo);
   bool ovf = false;
   for (uint32_t x = threadIdx.x; x < nout; x += kMergeThreads) {
     const uint2 e = so[x];
@@ -1349,8 +1280,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_topk_merge(const TopkItem* __
       put(dst, vo + o, (uint8_t)(q & 0xFF));
       dv = __fmul_rn((float)q, s);
     }
-    if constexpr (EF)
-      if (!(skip_a && s_from_a[x])) r[e.x] = __fsub_rn(pv, dv);
+    if constexpr (EF) r[e.x] = __fsub_rn(pv, dv);
   }
   // zero the padding of the two sections (the tile that ends the item)
   if (d1 == k) {
@@ -1806,11 +1736,6 @@ static void topk_select_all(const Launch& L, const TopkBuffers& B, int item0, in
   {
     // fallback for items whose bracket failed (every kernel exits at once otherwise)
     Mark mk(L, PH_TOPK_FALLBACK);
-    if (EF) {
-      k_topk_restore<<<gsm, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, B.status, B.soff, B.stage, r,
-                                                     anyf);
-      ++*L.launches;
-    }
     for (int d = 0; d < 3; ++d) {
       k_topk_hist<VEC><<<gh, kThreads, 0, L.stream>>>(aitems, ti, st, nitems, a_chunks, r, EF, g,
                                                       B.hist + (size_t)item0 * 2048, d, anyf);
@@ -1857,7 +1782,7 @@ void preload_topk() {
   touch_t((const void*)k_topk_move); touch_t((const void*)k_topk_scan);
   touch_t((const void*)k_topk_wide_hist); touch_t((const void*)k_topk_wide_pick); touch_t((const void*)k_topk_wide_plan);
   touch_t((const void*)k_topk_wide_count); touch_t((const void*)k_topk_wide_scan);
-  touch_t((const void*)k_topk_wide_write); touch_t((const void*)k_topk_restore);
+  touch_t((const void*)k_topk_wide_write);
   touch_t((const void*)k_topk_write<true>); touch_t((const void*)k_topk_write<false>);
   touch_t((const void*)k_topk_resolve);
   touch_t((const void*)k_topk_hist<true>); touch_t((const void*)k_topk_hist<false>);
