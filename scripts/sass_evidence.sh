@@ -14,3 +14,7 @@ cuobjdump -sass -fun '_ZN2nb9k_int8_wsILb1ELi8ELi19ELi4ELi1ELi0ELb0EEEvPKNS_4Ite
 echo
 echo "# excerpt: k_fp16_tma<EF=1> (the default FP16 compressor)"
 cuobjdump -sass -fun '_ZN2nb10k_fp16_tmaILb1EEEvPKNS_4ItemEimPKfPfNS_5DestsEPj' $O/kernels_ws.o | grep -E "UBLKCP|TRYWAIT|ARRIVE" | head -10
+echo
+echo "# k_topk_stage<EF=1, VEC=1, TMA=1> (the default top-k stage pass, round 2): counts, then excerpt"
+cuobjdump -sass $O/kernels_topk.o | awk '/Function : /{fn=$3} /UBLKCP|SYNCS/{split($0,a,";"); n=split(a[1],w," "); op=""; for(i=1;i<=n;i++) if (w[i] ~ /^(UBLKCP|SYNCS)/) op=w[i]; c[fn" "op]++} END{for(k in c) print c[k], k}' | sort -k2 | grep -E "k_topk_stageILb1ELb1ELb1E"
+cuobjdump -sass -fun '_ZN2nb12k_topk_stageILb1ELb1ELb1EEEvPKNS_4ItemEPKNS_8TopkItemEPNS_9TopkStateEimPKfPfPySC_P5uint2m' $O/kernels_topk.o | grep -E "UBLKCP|TRYWAIT|ARRIVE" | head -8
