@@ -436,6 +436,11 @@ def main():
                     "traffic": load_traffic(wc["workload"], wc["method"], args.bucket_mib, dom),
                     "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": int(byt), "ms_per_launch": round(tot / cnt, 4)}
+            if method == 3 and cnt > args.steps:
+                roof["note"] = ("two-stream top-k step: the two halves' launches of this kernel run "
+                                "concurrently and share HBM, so each launch's duration includes the "
+                                "other's traffic; serialized (--no-pipeline, or ncu) the kernel runs "
+                                "at ~0.86-0.90 of the peak; step_roofline is the whole-step figure")
     step_bytes = step_algorithmic_bytes(method, vt, P, ef, n, k_per_cluster, world)
     if world > 1 and (busbw or 0) > 0:
         # NVLink bound: bytes INTO this GPU per step (P - 1 peers' payloads of its shard, plus
