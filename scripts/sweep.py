@@ -2,8 +2,8 @@
 """BASELINE.json configs 1 and 5 as JSONL (one line per point).
 
   config 1: one 1M-float (2^20) bucket, P = 2 clusters x 1 GPU: step latency in us for
-            INT8+EF (primary), FP16+EF, TOPK 1 % / 10 %, and the CPU oracle's seconds for the
-            same step (rank 0).  N = 1: LOOPBACK (both clusters on one GPU); N = 2 (torchrun):
+            INT8+EF (primary), FP16+EF, TOPK 1 % / 10 % (the CPU oracle is timed only by
+            bench.py's cpu_baseline / reference arm: no script outside tests/ runs it).  N = 1: LOOPBACK (both clusters on one GPU); N = 2 (torchrun):
             the real 2-GPU exchange over NVLink.
   config 5: bucket 1 MiB .. 1 GiB (2^18 .. 2^28 elements) x {INT8+EF, FP16+EF, TOPK rho in
             {1, 5, 10, 25, 50} % x values {f32, f16, i8}}: GB/s fp32 synced per GPU and the step's
@@ -72,7 +72,6 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--sizes", default="18,20,22,24,26,28", help="log2 bucket elements")
-    ap.add_argument("--oracle-max-elems", type=int, default=1 << 20)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -130,8 +129,6 @@ def main():
             for s in range(3):
                 ctx.step(nb.ALL_BUCKETS, g, out, s)
             ctx.check()
-            ctx.timing_enable(True)
-            ctx.timing_read()
             times = []
             for s in range(args.steps):
                 flush.fill_(float(s))
@@ -145,8 +142,15 @@ def main():
                 b.synchronize()
                 times.append(a.elapsed_time(b))
             ctx.check()
+            # per-phase breakdown in a separate pass (the timers' events would add to the latency)
+            ctx.timing_enable(True)
+            ctx.timing_read()
+            for s in range(args.steps):
+                ctx.step(nb.ALL_BUCKETS, g, out, 3 + args.steps + s)
+            torch.cuda.synchronize()
             phases = ctx.timing_read()
             ctx.timing_enable(False)
+            ctx.check()
             ms = float(np.median(times))
             if world > 1:
                 tt = torch.tensor([ms], device="cuda")
@@ -170,15 +174,6 @@ def main():
                 rec["nvlink_busbw_gbs"] = round(busbw, 1)
                 rec["nvlink_frac"] = round(nv / (ms * 1e-3) / 1e9 / busbw, 4)
                 rec["bound"] = "nvlink" if nv / busbw > byt / peak else "hbm"
-            if args.config == 1 and rank == 0:   # the CPU oracle's time for the same step
-                import oracle as O
-                if n <= args.oracle_max_elems:
-                    codec = O.Codec(method=method, topk_values=vt, topk_density=rho if rho else 0.01)
-                    parts = [s[:n].numpy() for s in src] if world == 1 else \
-                        [model_gradient("ernie-m-base", cluster=c)[:n] for c in range(P)]
-                    t0 = time.perf_counter()
-                    O.oracle_step(parts, [np.zeros(n, np.float32) for _ in range(P)], codec, 1)
-                    rec["oracle_seconds"] = round(time.perf_counter() - t0, 4)
             if out_f:
                 out_f.write(json.dumps(rec) + "\n")
                 out_f.flush()

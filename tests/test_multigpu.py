@@ -1,5 +1,5 @@
 """Multi-GPU parity over NCCL (torchrun, one process per GPU): every rank's output, payload
-and residual bit-identical to the oracle and to the other ranks (scripts/dist_check.py).
+and residual bit-identical to the oracle and to the other ranks (tests/dist_check.py).
 Needs >= 2 GPUs (gpurun --gpus 2 / 4); skipped otherwise."""
 import os
 import subprocess
@@ -18,7 +18,7 @@ def ngpus():
 
 def torchrun(nproc, *args, port=29533, timeout=900):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "scripts", "dist_check.py"),
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "dist_check.py"),
            *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
