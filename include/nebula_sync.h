@@ -258,8 +258,7 @@ uint64_t nebula_kernel_launches(const nebula_ctx* ctx);
  *   directly from the peer over NVLink.  In 2 and 3 the exchange is a per-bucket flag
  *   handshake (release/acquire at system scope) and slots are double-buffered by step parity.
  *   Auto (every rank can map every peer, decided collectively at init): 2 for TOPK and, at
- *   P = 2, for IDENTITY / INT8 / FP8 (and FP16 / QSGD when the mean bucket is < 8 MiB); 3
- *   otherwise (P > 2, and FP16 / QSGD at P = 2 on buckets >= 8 MiB); else 1.
+ *   P = 2, for IDENTITY / INT8 / FP8; 3 otherwise (P > 2, and FP16 / QSGD at P = 2); else 1.
  *   Only between steps. */
 #define NEBULA_OPT_EXCHANGE 2
 /*   NEBULA_OPT_FP16_KERNEL: 0 (default) TMA-ring streaming kernel for 16-B aligned calls,

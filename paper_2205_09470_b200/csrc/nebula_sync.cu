@@ -644,13 +644,8 @@ static nebula_status self_resolve(nebula_ctx* ctx) {
 static int auto_xmode(const nebula_ctx* ctx) {
   const int m = ctx->codec.method;
   if (m == NEBULA_TOPK) return 2;
-  if (ctx->P == 2) {
-    // the fused pull pays off on large buckets (BASELINE config 2's 25 MiB); a 4 MiB bucket
-    // (config 1) steps faster staged + push (FP16 39 vs 44 us)
-    const uint64_t nb = ctx->b.empty() ? 1 : ctx->b.size();
-    const bool big = ctx->total_n * 4 / nb >= (8ull << 20);
-    return (big && (m == NEBULA_FP16 || m == NEBULA_QSGD)) ? 3 : 2;
-  }
+  // (a 4 MiB bucket too: FP16 pull 43.7 us vs push 46.0 us, profiles/r02/config1_n2_*.jsonl)
+  if (ctx->P == 2 && m != NEBULA_FP16 && m != NEBULA_QSGD) return 2;
   return 3;
 }
 
@@ -918,8 +913,8 @@ nebula_status nebula_sync_init(nebula_ctx** out, const nebula_topology* topo, co
         if (ps != NEBULA_OK) return bail(ps);
       }
       // auto (auto_xmode): push for top-k and at P = 2 (one peer: the NVLink egress hides inside
-      // the compress kernel) except FP16 / QSGD on large buckets; otherwise pull (NVLink loads
-      // outrun SM-issued stores once every GPU feeds P - 1 peers)
+      // the compress kernel) except FP16 / QSGD; otherwise pull (NVLink loads outrun SM-issued
+      // stores once every GPU feeds P - 1 peers)
       if (ctx->p2p_ok && ctx->P > 1) ctx->xmode = auto_xmode(ctx);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { ctx->err = "device sync after init failed"; return bail(NEBULA_ERR_CUDA); }
