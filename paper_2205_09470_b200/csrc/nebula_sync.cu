@@ -15,6 +15,7 @@
 // clusters simulated in one context), SELF (one context per (cluster, GPU) in ONE process —
 // the contexts reach each other's buffers directly, so every P2P code path runs on one GPU).
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -26,6 +27,15 @@
 #include <vector>
 
 #include "../../include/nebula_sync.h"
+
+// NVTX ranges around the public stage calls (nsys / ncu --nvtx show them as "nebula_*"; header-
+// only NVTX 3: without a tool attached each push / pop is one predictable branch)
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 #include "kernels.h"
 
 using namespace nb;
@@ -1142,6 +1152,7 @@ static nebula_status compress_t(nebula_ctx* ctx, int t, const float* dev_grad, u
 }
 
 nebula_status nebula_compress(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, uint64_t step) {
+  NvtxRange nvtx_range("nebula_compress");
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
@@ -1176,6 +1187,7 @@ static nebula_status exchange_t(nebula_ctx* ctx, int t) {
 }
 
 nebula_status nebula_exchange(nebula_ctx* ctx, int32_t bucket) {
+  NvtxRange nvtx_range("nebula_exchange");
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
@@ -1229,6 +1241,7 @@ static nebula_status reduce_t(nebula_ctx* ctx, int t, float* dev_out) {
 }
 
 nebula_status nebula_decompress_reduce(nebula_ctx* ctx, int32_t bucket, float* dev_out) {
+  NvtxRange nvtx_range("nebula_decompress_reduce");
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   int lo, hi;
   if (!range_of(ctx, bucket, &lo, &hi)) return fail(ctx, NEBULA_ERR_INVALID_ARG, "bucket index out of range");
@@ -1392,6 +1405,7 @@ static nebula_status step_pipelined(nebula_ctx* ctx, const float* dev_grad, floa
 }
 
 nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad, float* dev_out, uint64_t step) {
+  NvtxRange nvtx_range("nebula_step");
   if (ctx && step_pipelinable(ctx, bucket, step) && dev_grad && dev_out) return step_pipelined(ctx, dev_grad, dev_out, step);
   if (ctx) {
     int lo, hi;
@@ -1413,6 +1427,7 @@ nebula_status nebula_step(nebula_ctx* ctx, int32_t bucket, const float* dev_grad
 // event;  d2h stream: wait, copy bucket b's average out.  Device staging is bucket-major
 // ([P][n_b] per bucket for LOOPBACK, as a per-bucket call expects).
 nebula_status nebula_step_host(nebula_ctx* ctx, const float* host_grad, float* host_out, uint64_t step) {
+  NvtxRange nvtx_range("nebula_step_host");
   if (!ctx) return NEBULA_ERR_INVALID_ARG;
   if ((!host_grad || !host_out) && ctx->total_n) return fail(ctx, NEBULA_ERR_INVALID_ARG, "null host buffer");
   DevGuard dg(ctx->device);
